@@ -1,0 +1,659 @@
+/*
+ * dkv_oracle.c — serial CPU oracle for DiffKV's on-GPU KV memory manager (arXiv 2412.03131).
+ *
+ * TEST INFRASTRUCTURE ONLY (see dkv_oracle.h).  Built with -O2 -ffp-contract=off, no fast-math:
+ * every float expression below is one IEEE binary32 operation rounded to nearest-even, in the order
+ * written.  Shares no code with the CUDA path.
+ *
+ * Structure follows the paper:
+ *   §2.2   asymmetric per-vector quantization            -> orc_quantize / orc_dequantize
+ *   §4   prompt-phase classification                   -> orc_classify_prefill
+ *   Alg.1  generation-phase policy                       -> orc_classify_decode
+ *   §5.2   unified pages, circular free list, bidir table-> orc_geometry, orc_compact_alloc
+ *   §5.3   compaction workflow (prompt / generation)     -> orc_compact_alloc, orc_quant_write_*,
+ *                                                                       orc_prefill_conservative (Fig. 5)
+ */
+#include "dkv_oracle.h"
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------------------------------
+ * IEEE binary16 conversion, round-to-nearest-even (Q16: "FP16 RNE").  value = m * 2^E exactly;
+ * pick the binary16 quantum 2^k for its magnitude, round m*2^(E-k) to an integer with RNE.
+ * ----------------------------------------------------------------------------------------------*/
+uint16_t orc_f16_from_f32(float x) {
+  uint32_t b;
+  memcpy(&b, &x, 4);
+  uint16_t sign = (uint16_t)((b >> 16) & 0x8000u);
+  uint32_t exp = (b >> 23) & 0xFFu, man = b & 0x7FFFFFu;
+  if (exp == 0xFFu) return (uint16_t)(sign | (man ? 0x7E00u : 0x7C00u));
+  if (exp == 0 && man == 0) return sign;
+  int64_t m = exp ? (int64_t)(man | 0x800000u) : (int64_t)man;
+  int32_t E = exp ? (int32_t)exp - 150 : -149;
+  int32_t msb = 63 - __builtin_clzll((unsigned long long)m);
+  int32_t k = msb + E - 10;            /* quantum exponent for an 11-bit significand */
+  if (k < -24) k = -24;                /* binary16 subnormal quantum */
+  int32_t sh = k - E;
+  int64_t q;
+  if (sh <= 0) {
+    q = m << (-sh);
+  } else if (sh >= 40) {
+    q = 0;
+  } else {
+    q = m >> sh;
+    int64_t rem = m & ((((int64_t)1) << sh) - 1), half = ((int64_t)1) << (sh - 1);
+    if (rem > half || (rem == half && (q & 1))) q++;
+  }
+  if (k == -24 && q < 1024) return (uint16_t)(sign | (uint16_t)q);   /* subnormal or zero */
+  if (q == 2048) { q = 1024; k++; }
+  int32_t e16 = k + 25;
+  if (e16 >= 31) return (uint16_t)(sign | 0x7C00u);                 /* overflow -> inf */
+  return (uint16_t)(sign | (uint16_t)(e16 << 10) | (uint16_t)(q - 1024));
+}
+
+float orc_f32_from_f16(uint16_t h) {
+  uint32_t sign = ((uint32_t)h & 0x8000u) << 16, e = (h >> 10) & 0x1Fu, m = h & 0x3FFu, b;
+  if (e == 0) {
+    if (m == 0) { b = sign; }
+    else {                                       /* subnormal: m * 2^-24, normalise */
+      int32_t sh = 0;
+      while (!(m & 0x400u)) { m <<= 1; sh++; }
+      m &= 0x3FFu;
+      b = sign | ((uint32_t)(127 - 15 + 1 - sh) << 23) | (m << 13);
+    }
+  } else if (e == 31) {
+    b = sign | 0x7F800000u | (m << 13);
+  } else {
+    b = sign | ((e - 15 + 127) << 23) | (m << 13);
+  }
+  float f;
+  memcpy(&f, &b, 4);
+  return f;
+}
+
+void orc_f16_from_f32_array(const float* x, uint16_t* out, int64_t n) {
+  for (int64_t i = 0; i < n; i++) out[i] = orc_f16_from_f32(x[i]);
+}
+
+/* Total order on finite floats with -0 < +0 (Q16 "min/max under the total order"). */
+static uint32_t total_key(float f) {
+  uint32_t b;
+  memcpy(&b, &f, 4);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * §2.2: "compute the scale s and zero point z based on X_min and X_max, then apply
+ * quantization element-wise as Q = round((X - z)/s) ... X^ = s*Q + z ... metadata s and z are kept in
+ * higher precision (e.g., FP16)"; applied "to each key and value vector independently".
+ * Arithmetic fixed by reading Q16; packing by Q17.
+ * ----------------------------------------------------------------------------------------------*/
+int32_t orc_quantize(const float* x, int32_t d, int32_t bits, uint8_t* codes, uint16_t* s16, uint16_t* z16) {
+  if (!(bits == 2 || bits == 4 || bits == 8) || d <= 0 || (d * bits) % 8) return ORC_ERR_INVALID;
+  for (int32_t i = 0; i < d; i++)
+    if (!isfinite(x[i])) return ORC_ERR_NONFINITE;
+  float mn = x[0], mx = x[0];
+  for (int32_t i = 1; i < d; i++) {
+    if (total_key(x[i]) < total_key(mn)) mn = x[i];
+    if (total_key(x[i]) > total_key(mx)) mx = x[i];
+  }
+  int32_t Q = (1 << bits) - 1;
+  float s32 = mx - mn;                 /* fsub_rn */
+  s32 = s32 / (float)Q;                /* fdiv_rn */
+  *s16 = orc_f16_from_f32(s32);
+  *z16 = orc_f16_from_f32(mn);
+  float sf = orc_f32_from_f16(*s16), zf = orc_f32_from_f16(*z16);
+  memset(codes, 0, (size_t)(d * bits / 8));
+  for (int32_t i = 0; i < d; i++) {
+    int32_t q = 0;
+    if (sf != 0.0f) {
+      float inv = 1.0f / sf;           /* fdiv_rn: reciprocal form is normative (Q16) */
+      float t = x[i] - zf;             /* fsub_rn */
+      t = t * inv;                     /* fmul_rn */
+      float r = roundf(t);             /* round half away from zero */
+      if (r < 0.0f) r = 0.0f;
+      if (r > (float)Q) r = (float)Q;
+      q = (int32_t)r;
+    }
+    int32_t bit = i * bits;            /* Q17: little-endian in the byte, lowest index in the LSBs */
+    codes[bit >> 3] |= (uint8_t)(q << (bit & 7));
+  }
+  return ORC_OK;
+}
+
+void orc_dequantize(const uint8_t* codes, int32_t d, int32_t bits, uint16_t s16, uint16_t z16, float* out) {
+  float sf = orc_f32_from_f16(s16), zf = orc_f32_from_f16(z16);
+  int32_t Q = (1 << bits) - 1;
+  for (int32_t i = 0; i < d; i++) {
+    int32_t bit = i * bits;
+    int32_t q = (codes[bit >> 3] >> (bit & 7)) & Q;
+    float y = sf * (float)q;           /* exact: s16 has 11 significant bits, q <= 8 bits */
+    out[i] = y + zf;                   /* fadd_rn */
+  }
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * Geometry.  P:466-471: six segments in order (quantized keys, key metadata, quantized values, value
+ * metadata, token scores, positions); tokens per page depend on the precision (Q11: C_h, C_l given).
+ * Every segment starts on a 16-byte boundary; page size = max over classes, rounded to 128 B (Q18).
+ * P:499 table length, corrected by Q12: L = ceil(M / C_h) + (W < C_h ? 1 : 0).
+ * ----------------------------------------------------------------------------------------------*/
+static int32_t align_up(int32_t x, int32_t a) { return (x + a - 1) / a * a; }
+
+static void class_geom(int32_t d, int32_t C, int32_t kb, int32_t vb, orc_class_geom* g) {
+  g->C = C; g->kbits = kb; g->vbits = vb;
+  g->k_row = d * kb / 8;
+  g->v_row = d * vb / 8;
+  g->off_k = 0;
+  g->off_kmeta = align_up(g->off_k + C * g->k_row, 16);
+  g->off_v = align_up(g->off_kmeta + 4 * C, 16);
+  g->off_vmeta = align_up(g->off_v + C * g->v_row, 16);
+  g->off_score = align_up(g->off_vmeta + 4 * C, 16);
+  g->off_pos = align_up(g->off_score + 4 * C, 16);
+  g->end = g->off_pos + 4 * C;
+}
+
+static int bits_ok(int32_t b) { return b == 2 || b == 4 || b == 8; }
+
+int32_t orc_geometry(const orc_config* c, int32_t* U, int32_t* L, int32_t* page_bytes,
+                     orc_class_geom* high, orc_class_geom* low) {
+  if (c->R < 1 || c->Ly < 1 || c->H < 1 || c->d < 8 || c->d % 8 || c->M < 1 || c->W < 0 ||
+      c->Ch < 1 || c->Cl < c->Ch || c->P < 1 || !bits_ok(c->kbh) || !bits_ok(c->vbh) ||
+      !bits_ok(c->kbl) || !bits_ok(c->vbl) || !isfinite(c->alpha_h) || !isfinite(c->alpha_l) ||
+      c->alpha_h < 0 || c->alpha_l < 0 || (c->prompt_denominator != 0 && c->prompt_denominator != 1))
+    return ORC_ERR_INVALID;
+  orc_class_geom gh, gl;
+  class_geom(c->d, c->Ch, c->kbh, c->vbh, &gh);
+  class_geom(c->d, c->Cl, c->kbl, c->vbl, &gl);
+  if (U) *U = c->R * c->Ly * c->H;
+  if (L) *L = (c->M + c->Ch - 1) / c->Ch + (c->W < c->Ch ? 1 : 0);
+  if (page_bytes) *page_bytes = align_up(gh.end > gl.end ? gh.end : gl.end, 128);
+  if (high) *high = gh;
+  if (low) *low = gl;
+  return ORC_OK;
+}
+
+/* "with a batch size of 128 on Llama3-8B, which has 32 layers and 8 KV heads per layer, the total
+   size of all bidirectional page tables is only 32 MB" — one 4-byte page ID per slot (Q19). */
+int64_t orc_table_bytes(int64_t batch, int64_t layers, int64_t kv_heads, int64_t L) {
+  return batch * layers * kv_heads * L * 4;
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * Pool state (c.1).  ring = iota, start = 0, free = P; tables = -1; counts = 0.
+ * ----------------------------------------------------------------------------------------------*/
+orc_pool* orc_pool_new(const orc_config* c) {
+  orc_pool* p = (orc_pool*)calloc(1, sizeof(orc_pool));
+  if (!p) return NULL;
+  p->c = *c;
+  if (orc_geometry(c, &p->U, &p->L, &p->page_bytes, &p->g[ORC_CLS_HIGH], &p->g[ORC_CLS_LOW]) != ORC_OK) {
+    free(p);
+    return NULL;
+  }
+  size_t U = (size_t)p->U, L = (size_t)p->L, P = (size_t)c->P, R = (size_t)c->R;
+  p->ring = (int32_t*)malloc(P * 4);
+  p->table = (int32_t*)malloc(U * L * 4);
+  p->n_h = (int32_t*)calloc(U, 4);
+  p->n_l = (int32_t*)calloc(U, 4);
+  p->req_state = (int8_t*)calloc(R, 1);
+  p->seq_len = (int32_t*)calloc(R, 4);
+  p->prompt_len = (int32_t*)calloc(R, 4);
+  p->pages = (uint8_t*)calloc(P, (size_t)p->page_bytes);
+  size_t wn = U * (size_t)c->W * (size_t)c->d;
+  p->win_k = (uint16_t*)calloc(wn ? wn : 1, 2);
+  p->win_v = (uint16_t*)calloc(wn ? wn : 1, 2);
+  p->pf_nh = (int32_t*)calloc(U, 4);
+  p->pf_nl = (int32_t*)calloc(U, 4);
+  p->admit_list = (int32_t*)calloc(R, 4);
+  if (!p->ring || !p->table || !p->n_h || !p->n_l || !p->req_state || !p->seq_len || !p->prompt_len ||
+      !p->pages || !p->win_k || !p->win_v || !p->pf_nh || !p->pf_nl || !p->admit_list) {
+    orc_pool_delete(p);
+    return NULL;
+  }
+  for (size_t i = 0; i < P; i++) p->ring[i] = (int32_t)i;
+  for (size_t i = 0; i < U * L; i++) p->table[i] = -1;
+  p->start = 0;
+  p->free = c->P;
+  p->last_phase = -1;
+  return p;
+}
+
+void orc_pool_delete(orc_pool* p) {
+  if (!p) return;
+  free(p->ring); free(p->table); free(p->n_h); free(p->n_l); free(p->req_state); free(p->seq_len);
+  free(p->prompt_len); free(p->pages); free(p->win_k); free(p->win_v); free(p->pf_nh); free(p->pf_nl);
+  free(p->admit_list);
+  free(p);
+}
+
+static void set_status(orc_pool* p, int32_t st) { if (p->status == ORC_OK) p->status = st; }
+
+int32_t orc_take_status(orc_pool* p) { int32_t s = p->status; p->status = ORC_OK; return s; }
+
+/* Section slot s of class c lives at page table[u][s/C_h] (High, left) or table[u][L-1-s/C_l] (Low,
+   right), index s mod C (c.1). */
+static uint8_t* slot_page(orc_pool* p, int cls, int32_t u, int32_t s, int32_t* idx) {
+  const orc_class_geom* g = &p->g[cls];
+  int32_t k = (cls == ORC_CLS_HIGH) ? s / g->C : p->L - 1 - s / g->C;
+  int32_t pid = p->table[(size_t)u * p->L + k];
+  *idx = s % g->C;
+  return p->pages + (size_t)pid * (size_t)p->page_bytes;
+}
+
+static float slot_sig(orc_pool* p, int cls, int32_t u, int32_t s) {
+  int32_t idx; uint8_t* pg = slot_page(p, cls, u, s, &idx);
+  float f; memcpy(&f, pg + p->g[cls].off_score + 4 * idx, 4); return f;
+}
+
+static int32_t slot_pos(orc_pool* p, int cls, int32_t u, int32_t s) {
+  int32_t idx; uint8_t* pg = slot_page(p, cls, u, s, &idx);
+  int32_t v; memcpy(&v, pg + p->g[cls].off_pos + 4 * idx, 4); return v;
+}
+
+/* Quantize one token's K and V (fp32 inputs) at class `cls` bits and store all six segments. */
+static int32_t write_token(orc_pool* p, int cls, int32_t u, int32_t s, const float* k, const float* v,
+                           float sig, int32_t pos) {
+  const orc_class_geom* g = &p->g[cls];
+  int32_t idx; uint8_t* pg = slot_page(p, cls, u, s, &idx);
+  uint16_t ks, kz, vs, vz;
+  int32_t st = orc_quantize(k, p->c.d, g->kbits, pg + g->off_k + idx * g->k_row, &ks, &kz);
+  if (st != ORC_OK) return st;
+  st = orc_quantize(v, p->c.d, g->vbits, pg + g->off_v + idx * g->v_row, &vs, &vz);
+  if (st != ORC_OK) return st;
+  uint8_t* km = pg + g->off_kmeta + 4 * idx; uint8_t* vm = pg + g->off_vmeta + 4 * idx;
+  memcpy(km, &ks, 2); memcpy(km + 2, &kz, 2);          /* meta = {s16, z16}, s at the lower address */
+  memcpy(vm, &vs, 2); memcpy(vm + 2, &vz, 2);
+  memcpy(pg + g->off_score + 4 * idx, &sig, 4);
+  memcpy(pg + g->off_pos + 4 * idx, &pos, 4);
+  return ORC_OK;
+}
+
+static void read_token(orc_pool* p, int cls, int32_t u, int32_t s, float* k, float* v, float* sig, int32_t* pos) {
+  const orc_class_geom* g = &p->g[cls];
+  int32_t idx; uint8_t* pg = slot_page(p, cls, u, s, &idx);
+  uint16_t ks, kz, vs, vz;
+  memcpy(&ks, pg + g->off_kmeta + 4 * idx, 2); memcpy(&kz, pg + g->off_kmeta + 4 * idx + 2, 2);
+  memcpy(&vs, pg + g->off_vmeta + 4 * idx, 2); memcpy(&vz, pg + g->off_vmeta + 4 * idx + 2, 2);
+  orc_dequantize(pg + g->off_k + idx * g->k_row, p->c.d, g->kbits, ks, kz, k);
+  orc_dequantize(pg + g->off_v + idx * g->v_row, p->c.d, g->vbits, vs, vz, v);
+  memcpy(sig, pg + g->off_score + 4 * idx, 4);
+  memcpy(pos, pg + g->off_pos + 4 * idx, 4);
+}
+
+static int32_t ceil_div(int32_t a, int32_t b) { return (a + b - 1) / b; }
+
+/* ------------------------------------------------------------------------------------------------
+ * Algorithm 1, generation phase, one unit at a time (c.2).
+ *   N  = tokens of the request including the one appended this step (Q3)
+ *   t_c = earliest window token, position N-1-W
+ *   thresholds alpha/N in fp32 round-to-nearest (Q3); half-open classes (Q2)
+ *   victim = lexicographic argmin of (score, position) over the section t_c joins, t_c included (Q6, Q7)
+ *   t_c takes the victim's slot when the victim leaves; a downgraded victim goes to the KV_l tail (Q8)
+ * ----------------------------------------------------------------------------------------------*/
+static void empty_decision(orc_decision* d) {
+  memset(d, 0, sizeof(*d));
+  d->v_slot = d->tc_slot = d->v_dst_slot = -1;
+}
+
+int32_t orc_classify_decode(orc_pool* p, const float* cand_sig, orc_decision* dec) {
+  const orc_config* c = &p->c;
+  for (int32_t r = 0; r < c->R; r++)
+    if (p->req_state[r] == ORC_REQ_ACTIVE && p->seq_len[r] >= c->M) return ORC_ERR_STATE;
+  p->last_phase = ORC_DECODE;
+  int32_t LyH = c->Ly * c->H;
+  for (int32_t u = 0; u < p->U; u++) {
+    orc_decision* D = &dec[u];
+    empty_decision(D);
+    if (p->status != ORC_OK) continue;                       /* sticky error: no-op */
+    int32_t r = u / LyH;
+    if (p->req_state[r] != ORC_REQ_ACTIVE) continue;
+    int32_t N = p->seq_len[r] + 1;
+    int32_t pc = N - 1 - c->W;
+    if (pc < 0) continue;                                     /* no token leaves the window yet */
+    float sc = cand_sig[u];
+    if (!isfinite(sc) || sc < 0.0f) { set_status(p, ORC_ERR_NONFINITE); continue; }
+    if (sc == 0.0f) sc = 0.0f;                                /* canonicalise -0 -> +0 (Q6) */
+    float th = c->alpha_h / (float)N;                         /* alpha_h / N */
+    float tl = c->alpha_l / (float)N;                         /* alpha_l / N */
+    int cls;
+    if (sc >= th) cls = ORC_CLS_HIGH;                         /* line q_high */
+    else if (sc >= tl) cls = ORC_CLS_LOW;                     /* line q_low  */
+    else { D->tc_class = ORC_CLS_PRUNED; continue; }          /* t_c pruned */
+    int32_t n = (cls == ORC_CLS_HIGH) ? p->n_h[u] : p->n_l[u];
+    /* t_v = argmin over the section with t_c added (lines v_high / v_low). */
+    int32_t vslot = -1; float vs = sc; int32_t vp = pc;       /* start from t_c itself */
+    for (int32_t s = 0; s < n; s++) {
+      float sg = slot_sig(p, cls, u, s);
+      int32_t ps = slot_pos(p, cls, u, s);
+      if (sg < vs || (sg == vs && ps < vp)) { vs = sg; vp = ps; vslot = s; }
+    }
+    D->tc_class = (uint8_t)cls;
+    if (cls == ORC_CLS_HIGH) {
+      if (vslot < 0 || vs >= th) {                            /* t_v stays in KV_h */
+        D->v_action = ORC_V_KEEP; D->grow = ORC_GROW_HIGH;
+        D->demand = (p->n_h[u] % c->Ch == 0); D->tc_slot = p->n_h[u];
+      } else if (vs >= tl) {                                  /* line requant_high: downgrade t_v */
+        D->v_action = ORC_V_DOWN; D->grow = ORC_GROW_LOW;
+        D->demand = (p->n_l[u] % c->Cl == 0);
+        D->v_slot = vslot; D->tc_slot = vslot; D->v_dst_slot = p->n_l[u];
+      } else {                                                /* prune t_v */
+        D->v_action = ORC_V_PRUNE; D->grow = ORC_GROW_NONE; D->demand = 0;
+        D->v_slot = vslot; D->tc_slot = vslot;
+      }
+    } else {
+      if (vslot < 0 || vs >= tl) {
+        D->v_action = ORC_V_KEEP; D->grow = ORC_GROW_LOW;
+        D->demand = (p->n_l[u] % c->Cl == 0); D->tc_slot = p->n_l[u];
+      } else {                                                /* line prune_low */
+        D->v_action = ORC_V_PRUNE; D->grow = ORC_GROW_NONE; D->demand = 0;
+        D->v_slot = vslot; D->tc_slot = vslot;
+      }
+    }
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * §4 prompt phase, c.6: token i (1-indexed) of a prompt of length n is High if its
+ * significance >= alpha_h/den, Low if >= alpha_l/den, else pruned (Q2 half-open), den = i (Q4 default)
+ * or n; the newest W tokens stay in the FP16 window (Q10).
+ * ----------------------------------------------------------------------------------------------*/
+static int32_t admit(orc_pool* p, const int32_t* req, const int32_t* len, int32_t n) {
+  const orc_config* c = &p->c;
+  if (n < 0 || n > c->R) return ORC_ERR_INVALID;
+  for (int32_t i = 0; i < n; i++) {
+    if (req[i] < 0 || req[i] >= c->R || len[i] < 0 || len[i] > c->M) return ORC_ERR_INVALID;
+    if (p->req_state[req[i]] != ORC_REQ_IDLE) return ORC_ERR_STATE;
+    for (int32_t j = 0; j < i; j++) if (req[j] == req[i]) return ORC_ERR_INVALID;
+  }
+  for (int32_t i = 0; i < n; i++) {
+    p->req_state[req[i]] = ORC_REQ_ADMITTING;
+    p->prompt_len[req[i]] = len[i];
+    p->admit_list[i] = req[i];
+  }
+  p->n_admit = n;
+  return ORC_OK;
+}
+
+static int prompt_class(const orc_config* c, float s, int32_t t, int32_t n) {
+  float den = (c->prompt_denominator == 0) ? (float)(t + 1) : (float)n;
+  float th = c->alpha_h / den, tl = c->alpha_l / den;
+  if (s >= th) return ORC_CLS_HIGH;
+  if (s >= tl) return ORC_CLS_LOW;
+  return ORC_CLS_PRUNED;
+}
+
+int32_t orc_classify_prefill(orc_pool* p, const int32_t* req, const int32_t* len, int32_t n,
+                             const float* sig, int64_t sig_stride, uint8_t* token_class) {
+  const orc_config* c = &p->c;
+  for (int32_t i = 0; i < n; i++) if (len[i] > sig_stride) return ORC_ERR_INVALID;
+  int32_t st = admit(p, req, len, n);
+  if (st != ORC_OK) return st;
+  p->last_phase = ORC_PREFILL;
+  int32_t LyH = c->Ly * c->H;
+  for (int32_t i = 0; i < n; i++) {
+    int32_t r = req[i], T = len[i];
+    for (int32_t j = 0; j < LyH; j++) {
+      int32_t u = r * LyH + j;
+      const float* row = sig + ((int64_t)i * LyH + j) * sig_stride;
+      uint8_t* crow = token_class ? token_class + ((int64_t)i * LyH + j) * sig_stride : NULL;
+      int32_t nh = 0, nl = 0;
+      for (int32_t t = 0; t < T; t++) {
+        int cls = ORC_CLS_NONE;                               /* window token */
+        if (t < T - c->W && p->status == ORC_OK) {
+          float s = row[t];
+          if (!isfinite(s) || s < 0.0f) { set_status(p, ORC_ERR_NONFINITE); s = 0.0f; }
+          cls = prompt_class(c, s, t, T);
+          if (cls == ORC_CLS_HIGH) nh++;
+          if (cls == ORC_CLS_LOW) nl++;
+        }
+        if (crow) crow[t] = (uint8_t)cls;
+      }
+      p->pf_nh[u] = nh;
+      p->pf_nl[u] = nl;
+    }
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * Coordination (c.3).  P:485-488: "after each head determines the number of pages to be allocated or
+ * freed, a parallel prefix sum ... computes a unique offset for each head relative to the start or end
+ * pointer ... For memory allocation, each head concurrently retrieves its new page IDs from its
+ * designated region ... with the start pointer incremented by the cumulative number of pages ...
+ * for memory recycling, each head writes freed page IDs to its designated region, with the end pointer
+ * incremented by the total number of pages released."  Serial here: the running offset IS the prefix
+ * sum.  Order: recycle first (Q14), canonical order u = (r*Ly + l)*H + h (Q13), all-or-nothing (Q15).
+ * ----------------------------------------------------------------------------------------------*/
+int32_t orc_compact_alloc(orc_pool* p, const orc_decision* dec) {
+  const orc_config* c = &p->c;
+  int32_t LyH = c->Ly * c->H, L = p->L, P = c->P;
+  if (p->last_phase == ORC_DECODE && !dec) return ORC_ERR_INVALID;
+  if (p->last_phase < 0) return ORC_ERR_STATE;
+  /* 1. recycle finished requests into the ring at end = start + free */
+  int64_t freed = 0;
+  for (int32_t r = 0; r < c->R; r++) {
+    if (p->req_state[r] != ORC_REQ_PENDING_FREE) continue;
+    for (int32_t j = 0; j < LyH; j++) {
+      int32_t u = r * LyH + j;
+      for (int32_t k = 0; k < L; k++) {
+        int32_t* slot = &p->table[(size_t)u * L + k];
+        if (*slot != -1) {
+          p->ring[(p->start + p->free) % P] = *slot;
+          p->free += 1; freed += 1;
+          *slot = -1;
+        }
+      }
+      p->n_h[u] = 0; p->n_l[u] = 0;
+    }
+    p->req_state[r] = ORC_REQ_IDLE;
+    p->seq_len[r] = 0;
+    p->prompt_len[r] = 0;
+  }
+  p->last_freed = freed;
+  if (p->status != ORC_OK) { p->last_demand = 0; return ORC_OK; }   /* allocation is a no-op */
+  /* 2. per-head demand and the all-or-nothing check */
+  int64_t D = 0;
+  for (int32_t u = 0; u < p->U; u++) {
+    int32_t r = u / LyH;
+    if (p->last_phase == ORC_DECODE) {
+      if (p->req_state[r] == ORC_REQ_ACTIVE) D += dec[u].demand;
+    } else if (p->req_state[r] == ORC_REQ_ADMITTING) {
+      D += ceil_div(p->pf_nh[u], c->Ch) + ceil_div(p->pf_nl[u], c->Cl);
+    }
+  }
+  p->last_demand = D;
+  if (D > p->free) { set_status(p, ORC_ERR_OOM); p->oom_count++; return ORC_OK; }
+  /* 3. grant in canonical order; high IDs left-to-right, low IDs right-to-left */
+  int64_t off = 0;
+  for (int32_t u = 0; u < p->U; u++) {
+    int32_t r = u / LyH;
+    int32_t* row = &p->table[(size_t)u * L];
+    if (p->last_phase == ORC_DECODE) {
+      if (p->req_state[r] != ORC_REQ_ACTIVE || !dec[u].demand) continue;
+      int32_t ph = ceil_div(p->n_h[u], c->Ch), pl = ceil_div(p->n_l[u], c->Cl);
+      if (ph + pl + 1 > L) { set_status(p, ORC_ERR_OVERFLOW); continue; }
+      int32_t k = (dec[u].grow == ORC_GROW_HIGH) ? p->n_h[u] / c->Ch : L - 1 - p->n_l[u] / c->Cl;
+      row[k] = p->ring[(p->start + off) % P];
+      off += 1;
+    } else {
+      if (p->req_state[r] != ORC_REQ_ADMITTING) continue;
+      int32_t ph = ceil_div(p->pf_nh[u], c->Ch), pl = ceil_div(p->pf_nl[u], c->Cl);
+      if (ph + pl > L) { set_status(p, ORC_ERR_OVERFLOW); off += ph + pl; continue; }
+      for (int32_t k = 0; k < ph; k++) { row[k] = p->ring[(p->start + off) % P]; off += 1; }
+      for (int32_t k = 0; k < pl; k++) { row[L - 1 - k] = p->ring[(p->start + off) % P]; off += 1; }
+    }
+  }
+  p->start = (p->start + D) % P;
+  p->free -= D;
+  /* 4. counts (a5) and the request length */
+  for (int32_t u = 0; u < p->U; u++) {
+    int32_t r = u / LyH;
+    if (p->last_phase == ORC_DECODE) {
+      if (p->req_state[r] != ORC_REQ_ACTIVE) continue;
+      if (dec[u].grow == ORC_GROW_HIGH) p->n_h[u] += 1;
+      if (dec[u].grow == ORC_GROW_LOW) p->n_l[u] += 1;       /* DOWN: n_h unchanged, n_l + 1 */
+    } else if (p->req_state[r] == ORC_REQ_ADMITTING) {
+      p->n_h[u] = p->pf_nh[u];
+      p->n_l[u] = p->pf_nl[u];
+    }
+  }
+  for (int32_t r = 0; r < c->R; r++) {
+    if (p->last_phase == ORC_DECODE && p->req_state[r] == ORC_REQ_ACTIVE) p->seq_len[r] += 1;
+    if (p->last_phase == ORC_PREFILL && p->req_state[r] == ORC_REQ_ADMITTING) p->seq_len[r] = p->prompt_len[r];
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * KV compressor, generation step (c.4): downgrade t_v (Q9: re-quantize the stored P_h
+ * values), quantize t_c out of the FP16 window into its slot, push the new token into the window.
+ * ----------------------------------------------------------------------------------------------*/
+int32_t orc_quant_write_decode(orc_pool* p, const orc_decision* dec, const uint16_t* k_new,
+                               const uint16_t* v_new, const float* cand_sig) {
+  if (p->status != ORC_OK) return ORC_OK;
+  const orc_config* c = &p->c;
+  int32_t LyH = c->Ly * c->H, d = c->d, W = c->W;
+  float* kx = (float*)malloc((size_t)d * 4); float* vx = (float*)malloc((size_t)d * 4);
+  for (int32_t u = 0; u < p->U; u++) {
+    int32_t r = u / LyH;
+    if (p->req_state[r] != ORC_REQ_ACTIVE) continue;
+    const orc_decision* D = &dec[u];
+    int32_t N = p->seq_len[r];                      /* already includes the new token */
+    int32_t pc = N - 1 - W;
+    if (D->v_action == ORC_V_DOWN) {
+      float sg; int32_t ps;
+      read_token(p, ORC_CLS_HIGH, u, D->v_slot, kx, vx, &sg, &ps);
+      int32_t st = write_token(p, ORC_CLS_LOW, u, D->v_dst_slot, kx, vx, sg, ps);
+      if (st != ORC_OK) { set_status(p, st); continue; }
+    }
+    const uint16_t* kn = k_new + (size_t)u * d; const uint16_t* vn = v_new + (size_t)u * d;
+    uint16_t* wk = W ? p->win_k + ((size_t)u * W + (size_t)((N - 1) % W)) * d : NULL;
+    uint16_t* wv = W ? p->win_v + ((size_t)u * W + (size_t)((N - 1) % W)) * d : NULL;
+    if (D->tc_class == ORC_CLS_HIGH || D->tc_class == ORC_CLS_LOW) {
+      /* t_c sits in window slot p_c mod W == (N-1) mod W; read it before the push overwrites it */
+      const uint16_t* sk = W ? wk : kn; const uint16_t* sv = W ? wv : vn;
+      for (int32_t i = 0; i < d; i++) { kx[i] = orc_f32_from_f16(sk[i]); vx[i] = orc_f32_from_f16(sv[i]); }
+      float sc = cand_sig[u];
+      if (sc == 0.0f) sc = 0.0f;
+      int32_t st = write_token(p, D->tc_class, u, D->tc_slot, kx, vx, sc, pc);
+      if (st != ORC_OK) { set_status(p, st); continue; }
+    }
+    if (W) { memcpy(wk, kn, (size_t)d * 2); memcpy(wv, vn, (size_t)d * 2); }
+  }
+  free(kx); free(vx);
+  return ORC_OK;
+}
+
+/* Prompt phase bulk write (a8): each kept token goes to the next slot of its class in position order;
+   the newest min(W, n) tokens go to the window at slot pos mod W; then ADMITTING -> ACTIVE. */
+int32_t orc_quant_write_prefill(orc_pool* p, const uint16_t* k, const uint16_t* v, int64_t kv_stride,
+                                const float* sig, int64_t sig_stride) {
+  if (p->status != ORC_OK) return ORC_OK;
+  const orc_config* c = &p->c;
+  int32_t LyH = c->Ly * c->H, d = c->d, W = c->W;
+  float* kx = (float*)malloc((size_t)d * 4); float* vx = (float*)malloc((size_t)d * 4);
+  for (int32_t i = 0; i < p->n_admit; i++) {
+    int32_t r = p->admit_list[i], T = p->prompt_len[r];
+    if (p->req_state[r] != ORC_REQ_ADMITTING) continue;
+    for (int32_t j = 0; j < LyH; j++) {
+      int32_t u = r * LyH + j;
+      int32_t h = 0, l = 0;
+      for (int32_t t = 0; t < T; t++) {
+        const uint16_t* kr = k + (((int64_t)i * LyH + j) * kv_stride + t) * d;
+        const uint16_t* vr = v + (((int64_t)i * LyH + j) * kv_stride + t) * d;
+        if (t < T - W) {
+          float s = sig[((int64_t)i * LyH + j) * sig_stride + t];
+          if (s == 0.0f) s = 0.0f;
+          int cls = prompt_class(c, s, t, T);
+          if (cls == ORC_CLS_PRUNED) continue;
+          for (int32_t e = 0; e < d; e++) { kx[e] = orc_f32_from_f16(kr[e]); vx[e] = orc_f32_from_f16(vr[e]); }
+          int32_t slot = (cls == ORC_CLS_HIGH) ? h++ : l++;
+          int32_t st = write_token(p, cls, u, slot, kx, vx, s, t);
+          if (st != ORC_OK) set_status(p, st);
+        } else {
+          memcpy(p->win_k + ((size_t)u * W + (size_t)(t % W)) * d, kr, (size_t)d * 2);
+          memcpy(p->win_v + ((size_t)u * W + (size_t)(t % W)) * d, vr, (size_t)d * 2);
+        }
+      }
+    }
+  }
+  free(kx); free(vx);
+  if (p->status != ORC_OK) return ORC_OK;
+  for (int32_t i = 0; i < p->n_admit; i++)
+    if (p->req_state[p->admit_list[i]] == ORC_REQ_ADMITTING) p->req_state[p->admit_list[i]] = ORC_REQ_ACTIVE;
+  p->n_admit = 0;
+  return ORC_OK;
+}
+
+/* "Once a request is finished, all pages allocated for that request are recycled" — the request
+   becomes PENDING_FREE; its pages return to the ring in the next orc_compact_alloc (a7). */
+int32_t orc_free(orc_pool* p, const int32_t* req, int32_t n) {
+  for (int32_t i = 0; i < n; i++) {
+    if (req[i] < 0 || req[i] >= p->c.R) return ORC_ERR_INVALID;
+    if (p->req_state[req[i]] != ORC_REQ_ACTIVE) return ORC_ERR_STATE;
+    for (int32_t j = 0; j < i; j++) if (req[j] == req[i]) return ORC_ERR_STATE;
+  }
+  for (int32_t i = 0; i < n; i++) p->req_state[req[i]] = ORC_REQ_PENDING_FREE;
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * NEXT-1, the paper's prompt workflow (Fig. 5): "conservatively allocate ... assuming all
+ * tokens are stored at high precision" (ceil((n-W)/C_h) pages per head into slots 0..c-1), then the
+ * planning phase, then keep high pages left-to-right and low pages right-to-left, and "reclaim unused
+ * pages ... via a parallel prefix-sum" appended at the end pointer.  The plan's low pages are the last
+ * pl pages of the conservative block, moved to the right end of the table (a no-op when c == L, as in
+ * Fig. 5); the reclaimed middle is slots [ph, c - pl).  Returns ORC_ERR_OVERFLOW if ph + pl > c.
+ * ----------------------------------------------------------------------------------------------*/
+int32_t orc_prefill_conservative(orc_pool* p, const int32_t* req, const int32_t* len, int32_t n,
+                                 const float* sig, int64_t sig_stride, int32_t* reclaimed_out, int64_t* n_reclaimed) {
+  const orc_config* c = &p->c;
+  int32_t LyH = c->Ly * c->H, L = p->L, P = c->P;
+  int32_t st = orc_classify_prefill(p, req, len, n, sig, sig_stride, NULL);
+  if (st != ORC_OK) return st;
+  /* conservative allocation */
+  int64_t D = 0;
+  for (int32_t i = 0; i < n; i++) {
+    int32_t kept = len[i] - c->W > 0 ? len[i] - c->W : 0;
+    D += (int64_t)LyH * ceil_div(kept, c->Ch);
+  }
+  if (D > p->free) { set_status(p, ORC_ERR_OOM); return ORC_OK; }
+  int64_t off = 0;
+  for (int32_t i = 0; i < n; i++) {
+    int32_t kept = len[i] - c->W > 0 ? len[i] - c->W : 0, cc = ceil_div(kept, c->Ch);
+    if (cc > L) return ORC_ERR_OVERFLOW;
+    for (int32_t j = 0; j < LyH; j++)
+      for (int32_t k = 0; k < cc; k++) { p->table[(size_t)(req[i] * LyH + j) * L + k] = p->ring[(p->start + off) % P]; off++; }
+  }
+  p->start = (p->start + D) % P;
+  p->free -= D;
+  /* planning result -> keep left ph, move last pl to the right end, reclaim the middle */
+  int64_t nr = 0;
+  for (int32_t i = 0; i < n; i++) {
+    int32_t kept = len[i] - c->W > 0 ? len[i] - c->W : 0, cc = ceil_div(kept, c->Ch);
+    for (int32_t j = 0; j < LyH; j++) {
+      int32_t u = req[i] * LyH + j;
+      int32_t* row = &p->table[(size_t)u * L];
+      int32_t ph = ceil_div(p->pf_nh[u], c->Ch), pl = ceil_div(p->pf_nl[u], c->Cl);
+      if (ph + pl > cc) return ORC_ERR_OVERFLOW;
+      int32_t lows[64];
+      if (pl > 64) return ORC_ERR_INVALID;                                  /* oracle-level helper bound */
+      for (int32_t k = 0; k < pl; k++) lows[k] = row[cc - 1 - k];         /* k-th low page */
+      for (int32_t k = ph; k < cc - pl; k++) {
+        p->ring[(p->start + p->free) % P] = row[k];
+        if (reclaimed_out) reclaimed_out[nr] = row[k];
+        p->free += 1; nr++;
+      }
+      for (int32_t k = ph; k < cc; k++) row[k] = -1;
+      for (int32_t k = 0; k < pl; k++) row[L - 1 - k] = lows[k];
+      p->n_h[u] = p->pf_nh[u];
+      p->n_l[u] = p->pf_nl[u];
+    }
+    p->seq_len[req[i]] = len[i];
+  }
+  if (n_reclaimed) *n_reclaimed = nr;
+  p->last_phase = ORC_PREFILL;
+  return ORC_OK;
+}
