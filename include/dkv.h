@@ -1,0 +1,185 @@
+/*
+ * dkv.h — C ABI of the B200-native DiffKV KV memory manager (arXiv 2412.03131).
+ *
+ * The library implements the data-parallel hot path of DiffKV's on-GPU memory manager ("parallel KV
+ * compaction", §5 of the paper) as hand-written sm_100a CUDA kernels:
+ *
+ *   planning      dkv_classify      per-(request, layer, KV-head) significance classification and page
+ *                                   demand — "each attention head independently determines its memory
+ *                                   allocation requirements"; Algorithm 1 in the
+ *                                   generation phase, §4's thresholds in the prompt phase.
+ *   coordination  dkv_compact_alloc recycle finished requests' pages into the circular free list and grant
+ *                                   every head its pages from one exclusive scan — "a parallel prefix sum
+ *                                   operation computes a unique offset for each head relative to the start
+ *                                   or end pointer"; bidirectional table writes.
+ *   compressor    dkv_quant_write   quantize K/V into unified pages at K8V4 / K4V2 (P:173-177, P:347-349,
+ *                                   P:466-471).
+ *   release       dkv_free          "once a request is finished, all pages allocated for that request are
+ *                                   recycled".
+ *
+ * Citation convention: "P:n" = line n of the paper's LaTeX source; "Qn" = reading n of the
+ * ambiguity ledger in DESIGN.md §3.  No torch types cross this boundary: device buffers are plain
+ * pointers, host buffers are plain pointers, streams are CUDA runtime streams (cudaStream_t).
+ *
+ * Ownership.  The caller owns the device arena (>= dkv_arena_bytes(), 256-byte aligned, e.g. a torch
+ * uint8 CUDA tensor), every per-call device buffer and the streams.  The library owns only the host
+ * handle (created by dkv_pool_init, released by dkv_pool_destroy) and a host mirror of request states.
+ * It never allocates device memory after dkv_pool_init and keeps no reference to per-call buffers beyond
+ * stream-ordered execution; the arena must outlive the handle.  One handle = one host thread, calls
+ * ordered on one stream (or event-synchronised).
+ *
+ * Errors.  Host-detectable errors (bad arguments, request state, call order) return a negative status
+ * immediately, enqueue nothing and change nothing.  Device-detected errors (OOM, non-finite input,
+ * table overflow) are recorded in a sticky device status word — first error wins; while it is set
+ * dkv_classify / dkv_quant_write kernels are no-ops and dkv_compact_alloc only recycles.  dkv_pool_query
+ * returns and clears it and re-synchronises the host mirror.  The product path has no CPU fallback:
+ * every call fails with DKV_ERR_CUDA when no CUDA device is usable.
+ *
+ * Determinism.  Every output (decisions, ring, pointers, tables, counts, page bytes, window) is a pure
+ * function of the inputs and the pool state, identical for any launch configuration (tile size).
+ */
+#ifndef DKV_H
+#define DKV_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* dkv_stream_t;       /* a cudaStream_t; NULL = legacy default stream */
+typedef struct dkv_pool* dkv_pool_t;            /* opaque host handle */
+typedef int32_t dkv_status_t;
+
+enum {
+  DKV_OK = 0,
+  DKV_ERR_INVALID_ARG = -1,   /* bad config / pointer / size / request id */
+  DKV_ERR_STATE = -2,         /* request state or call order violated (host-detected) */
+  DKV_ERR_OOM = -3,           /* device: demand > free pages; allocation not applied (Q15) */
+  DKV_ERR_NONFINITE = -4,     /* device: NaN/Inf K/V, or significance NaN/Inf/negative */
+  DKV_ERR_OVERFLOW = -5,      /* device: table slot collision (unreachable by construction, Q12) */
+  DKV_ERR_CUDA = -6           /* CUDA runtime error (no device, launch failure, ...) */
+};
+enum { DKV_PHASE_DECODE = 0, DKV_PHASE_PREFILL = 1 };
+enum { DKV_CLS_NONE = 0, DKV_CLS_HIGH = 1, DKV_CLS_LOW = 2, DKV_CLS_PRUNED = 3 };
+enum { DKV_V_NONE = 0, DKV_V_KEEP = 1, DKV_V_DOWN = 2, DKV_V_PRUNE = 3 };
+enum { DKV_GROW_NONE = 0, DKV_GROW_HIGH = 1, DKV_GROW_LOW = 2 };
+enum { DKV_REQ_IDLE = 0, DKV_REQ_ADMITTING = 1, DKV_REQ_ACTIVE = 2, DKV_REQ_PENDING_FREE = 3 };
+
+/* Pool configuration.  Units u = (r*num_layers + l)*num_kv_heads + h (Q13).
+ * Constraints: head_dim in {64, 128}; bits in {2, 4, 8} with key bits >= 2; page_tokens_* multiples of 4,
+ * page_tokens_low >= page_tokens_high ("low-precision pages always contain more tokens");
+ * 1 <= num_pages < 2^31; window >= 0; alpha finite >= 0; units * table_len < 2^28. */
+typedef struct {
+  int32_t max_requests;        /* R: request slots */
+  int32_t num_layers;          /* Ly */
+  int32_t num_kv_heads;        /* H: KV heads held by THIS pool (one GPU's shard) */
+  int32_t head_dim;            /* d */
+  int32_t max_seq_len;         /* M: tokens per request incl. window */
+  int32_t window;              /* W: recent FP16 window, "typically set to 64" (Q10) */
+  int32_t page_tokens_high;    /* C_h (Q11) */
+  int32_t page_tokens_low;     /* C_l (Q11) */
+  int32_t kbits_high, vbits_high, kbits_low, vbits_low;   /* 8,4 / 4,2 = K8V4 / K4V2 */
+  int32_t num_pages;           /* P */
+  float   alpha_h, alpha_l;    /* thresholds (calibrated values P:702-703) */
+  int32_t prompt_denominator;  /* Q4: 0 = 1-indexed position i; 1 = prompt length n */
+  int32_t tile_units;          /* scan tile (units per CTA): 0 = default 1024; 256, 512 or 1024 */
+  int32_t reserved[2];         /* must be zero */
+} dkv_config_t;
+
+/* 16-byte per-unit decision written by dkv_classify(DECODE); padding-free, compared byte for byte.
+ * tc_class: class of t_c, the token leaving the window, or NONE when the request is not
+ *   ACTIVE or has no token outside the window.  v_action: fate of the victim t_v = lexicographic argmin
+ *   of (score, position) over the section t_c joins (Q6/Q7).  grow: section gaining a token.
+ *   demand: 1 iff the growing section's tail page is full.  Slots are section slot indices
+ *   (-1 if none): v_slot = victim's slot, tc_slot = where t_c is written (t_c takes the victim's slot when
+ *   the victim leaves, Q8), v_dst_slot = KV_l slot of a downgraded victim. */
+typedef struct {
+  uint8_t tc_class, v_action, grow, demand;
+  int32_t v_slot, tc_slot, v_dst_slot;
+} dkv_decision_t;
+
+typedef struct {
+  int64_t free_pages, used_pages, start, last_demand, last_freed;
+  int32_t status, oom_count;
+} dkv_stats_t;
+
+/* Byte offsets of every buffer inside the arena plus the page segment geometry (Q18: segments in
+ * the paper's order — K codes, K meta {s16,z16}, V codes, V meta, fp32 scores, int32 positions — each on
+ * a 16-byte boundary, token-major rows, codes packed LSB-first (Q17)).  Index 1 = high, 2 = low. */
+typedef struct {
+  int64_t arena_bytes;
+  int64_t off_ctrl, off_tile_status, off_ring, off_table, off_n_h, off_n_l, off_req_state, off_seq_len,
+          off_prompt_len, off_admit, off_pf_nh, off_pf_nl, off_pf_seg, off_win_k, off_win_v, off_pages,
+          off_stats;
+  int32_t units, table_len, page_bytes, num_tiles, tile_units, seg_tokens, num_segs;
+  int32_t C[3], k_row[3], v_row[3], off_k[3], off_kmeta[3], off_v[3], off_vmeta[3], off_score[3], off_pos[3];
+} dkv_layout_t;
+
+/* Arena size for `cfg`, or 0 if the configuration is invalid. */
+size_t dkv_arena_bytes(const dkv_config_t* cfg);
+
+/* Fill *out with the arena layout of `cfg` (host only, no CUDA call).  DKV_ERR_INVALID_ARG if invalid. */
+dkv_status_t dkv_pool_layout(const dkv_config_t* cfg, dkv_layout_t* out);
+
+/* Carve `d_arena` (device, >= dkv_arena_bytes, 256-B aligned) and initialise it on `s`: ring = iota,
+ * start = 0, free = P, tables = -1, counts = 0, pages and window zeroed.  *out receives the
+ * handle.  Asynchronous on `s`. */
+dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_bytes, dkv_stream_t s,
+                           dkv_pool_t* out);
+dkv_status_t dkv_pool_destroy(dkv_pool_t p);
+
+/* Planning.
+ * DECODE : every ACTIVE request appends one token this step.  d_sig = device fp32[U]: significance of
+ *          each unit's t_c (values for non-ACTIVE units are ignored).  Writes d_dec[U] (device).
+ *          h_req/h_len/n/sig_stride/d_token_class unused (NULL/0).  DKV_ERR_STATE if an ACTIVE request
+ *          already holds max_seq_len tokens.
+ * PREFILL: admits host arrays h_req[0..n) (IDLE -> ADMITTING) with prompt lengths h_len[0..n) <= M.
+ *          d_sig = device fp32[n][Ly*H][sig_stride] (request-major in h_req order, then l, then h; token
+ *          t at index t; sig_stride >= max prompt length).  Per-unit class counts and per-segment ranks go
+ *          to pool scratch; if d_token_class != NULL it receives u8[n][Ly*H][sig_stride] classes
+ *          (DKV_CLS_*, NONE for window tokens).  d_dec unused. */
+dkv_status_t dkv_classify(dkv_pool_t p, int32_t phase, const int32_t* h_req, const int32_t* h_len, int32_t n,
+                          const float* d_sig, int64_t sig_stride, dkv_decision_t* d_dec, uint8_t* d_token_class,
+                          dkv_stream_t s);
+
+/* Coordination.  Recycles every PENDING_FREE request (its pages go to the ring at end = start + free in
+ * canonical order, Q13; the request becomes IDLE), then grants the demand of the most recent dkv_classify
+ * all-or-nothing (Q15): decode demand from d_dec (device, as written by dkv_classify(DECODE)); prefill
+ * demand ceil(n_h/C_h) + ceil(n_l/C_l) from pool scratch (d_dec may be NULL).  Writes the bidirectional
+ * tables (high left-to-right, low right-to-left) and counts, advances start/free.  On OOM: sticky
+ * DKV_ERR_OOM, allocation state unchanged, recycling applied.  May be re-issued with the same d_dec
+ * after an OOM (only ACTIVE / ADMITTING requests take part). */
+dkv_status_t dkv_compact_alloc(dkv_pool_t p, const dkv_decision_t* d_dec, dkv_stream_t s);
+
+/* KV compressor.
+ * DECODE : d_dec as above; d_k/d_v = device fp16 bits [U][d], the new token of each unit (pushed into the
+ *          window); d_sig = the same cand_sig as dkv_classify; kv_stride/sig_stride unused (0).  For each
+ *          ACTIVE unit: downgrade t_v (re-quantize its stored K8V4 values at K4V2, Q9), quantize t_c out of
+ *          the window into tc_slot, then write the new token into window slot (N-1) mod W.
+ * PREFILL: d_k/d_v = device fp16 bits [n][Ly*H][kv_stride][d], d_sig = [n][Ly*H][sig_stride] as given to
+ *          dkv_classify(PREFILL); writes every kept token into its pages (slot = rank within its class in
+ *          position order) and the newest min(W, n) tokens into the window; ADMITTING -> ACTIVE. */
+dkv_status_t dkv_quant_write(dkv_pool_t p, int32_t phase, const dkv_decision_t* d_dec, const uint16_t* d_k,
+                             const uint16_t* d_v, int64_t kv_stride, const float* d_sig, int64_t sig_stride,
+                             dkv_stream_t s);
+
+/* Release: host array h_req[0..n) of ACTIVE requests -> PENDING_FREE (double free / not active ->
+ * DKV_ERR_STATE).  Allowed between sequences only (after dkv_quant_write, before dkv_classify).  Pages are
+ * recycled by the next dkv_compact_alloc; the slot is IDLE (re-admissible) after that call. */
+dkv_status_t dkv_free(dkv_pool_t p, const int32_t* h_req, int32_t n, dkv_stream_t s);
+
+/* Synchronises `s`; fills *out; returns the sticky device status (DKV_OK if none) and clears it; re-syncs
+ * the host mirror of request states and lengths from the device. */
+dkv_status_t dkv_pool_query(dkv_pool_t p, dkv_stats_t* out, dkv_stream_t s);
+
+/* Device address of the pool's int64[4] admission counters {free_pages, -last_demand, -used_pages,
+ * -status}, rewritten by every dkv_compact_alloc — the payload of the per-step count all-reduce (MIN). */
+int64_t* dkv_pool_stats_device_ptr(dkv_pool_t p);
+
+const char* dkv_status_string(dkv_status_t st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DKV_H */

@@ -1,0 +1,230 @@
+// dkv_internal.cuh — device-side structures and primitives shared by the sm_100a kernels.
+// Product code: never includes or links anything under oracle/.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dkv.h"
+
+namespace dkv {
+
+constexpr int kSegTokens = 256;         // prefill rank checkpoint granularity (tokens per segment)
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// Device control block at arena offset 0 (256 B).
+struct Ctrl {
+  int64_t start;                 // ring index of the first free page (allocation pointer)
+  int64_t free;                  // free pages; end = (start + free) mod P (recycling pointer, Q1)
+  int32_t status;                // sticky device status, first error wins
+  int32_t oom_count;
+  unsigned long long ticket;     // dynamic tile tickets of compact_alloc (monotonic)
+  unsigned long long arrive;     // grid-barrier arrivals of compact_alloc (monotonic)
+  int64_t last_demand, last_freed;
+  int64_t total_dem, total_fr;   // published by the last scan tile before the barrier
+  int64_t pad[6];
+};
+static_assert(sizeof(Ctrl) <= 256, "ctrl block");
+
+struct ClassGeom {
+  int32_t C, kbits, vbits, k_row, v_row, off_k, off_kmeta, off_v, off_vmeta, off_score, off_pos;
+};
+
+// Everything a kernel needs, passed by value.
+struct PoolDev {
+  int32_t R, Ly, H, LyH, U, d, M, W, L, P, page_bytes, Ch, Cl;
+  int32_t prompt_den, num_tiles, tile_units, nseg;
+  float alpha_h, alpha_l;
+  ClassGeom g[3];
+  Ctrl* ctrl;
+  unsigned long long* tile_status;
+  int32_t* ring;
+  int32_t* table;
+  int32_t* n_h;
+  int32_t* n_l;
+  int8_t* req_state;
+  int32_t* seq_len;
+  int32_t* prompt_len;
+  int32_t* admit;
+  int32_t* pf_nh;
+  int32_t* pf_nl;
+  int32_t* pf_seg;      // [U][nseg][2] exclusive (high, low) ranks at each segment start
+  __half* win_k;
+  __half* win_v;
+  uint8_t* pages;
+  int64_t* stats;       // int64[4] admission counters
+};
+
+// ------------------------------------------------------------------------------------- memory ops
+__device__ __forceinline__ int32_t ld_volatile(const int32_t* p) { return *(volatile const int32_t*)p; }
+__device__ __forceinline__ int64_t ld_volatile(const int64_t* p) { return *(volatile const int64_t*)p; }
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_nc_u32(const void* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+// streaming loads of inputs read exactly once
+__device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void set_status(Ctrl* c, int32_t st) { atomicCAS(&c->status, 0, st); }
+
+// ------------------------------------------------------------------------------------- float helpers
+// Total order on finite floats with -0 < +0 (Q16): monotone unsigned key.
+__device__ __forceinline__ uint32_t total_key(float f) {
+  uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key_to_float(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+__device__ __forceinline__ bool finite_f(float x) { return (__float_as_uint(x) & 0x7F800000u) != 0x7F800000u; }
+__device__ __forceinline__ float canon_zero(float x) { return x == 0.0f ? 0.0f : x; }
+
+__device__ __forceinline__ void unpack_h8(const uint4& v, float x[8]) {
+  const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    float2 f = __half22float2(h[i]);
+    x[2 * i] = f.x;
+    x[2 * i + 1] = f.y;
+  }
+}
+
+// Quantize the 8 values each lane of a group of `gl` lanes holds (one d-vector per group) at `bits`
+// (Q16).  Returns the packed codes of this lane's 8 elements (8*bits bits, lowest element in
+// the LSBs, Q17) and the group's fp16 (s, z) as one u32 {s16 | z16 << 16}.  `ok` = all finite.
+template <int GL>
+__device__ __forceinline__ uint64_t quantize8(const float x[8], int bits, uint32_t& meta, bool& ok) {
+  uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+  bool fin = true;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    fin &= finite_f(x[i]);
+    uint32_t k = total_key(x[i]);
+    kmin = min(kmin, k);
+    kmax = max(kmax, k);
+  }
+#pragma unroll
+  for (int o = GL / 2; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(kFull, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
+  }
+  unsigned allfin = __ballot_sync(kFull, fin);
+  const int lane = threadIdx.x & 31;
+  const unsigned gmask = ((GL == 32) ? kFull : ((1u << GL) - 1u)) << (lane & ~(GL - 1) & 31);
+  ok = (allfin & gmask) == gmask;
+  const float mn = key_to_float(kmin), mx = key_to_float(kmax);
+  const int Q = (1 << bits) - 1;
+  float s32 = __fdiv_rn(__fsub_rn(mx, mn), (float)Q);
+  __half s16 = __float2half_rn(s32), z16 = __float2half_rn(mn);
+  const float sf = __half2float(s16), zf = __half2float(z16);
+  meta = (uint32_t)__half_as_ushort(s16) | ((uint32_t)__half_as_ushort(z16) << 16);
+  uint64_t packed = 0;
+  if (sf != 0.0f) {
+    const float inv = __fdiv_rn(1.0f, sf);
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      float t = __fmul_rn(__fsub_rn(x[i], zf), inv);
+      float r = roundf(t);                       // round half away from zero
+      r = fminf(fmaxf(r, 0.0f), (float)Q);
+      packed |= (uint64_t)(uint32_t)r << (i * bits);
+    }
+  }
+  return packed;
+}
+
+// Dequantize this lane's 8 codes (X^ = s*Q + z).
+__device__ __forceinline__ void dequant8(uint64_t packed, int bits, uint32_t meta, float x[8]) {
+  const float sf = __half2float(__ushort_as_half((unsigned short)(meta & 0xFFFFu)));
+  const float zf = __half2float(__ushort_as_half((unsigned short)(meta >> 16)));
+  const uint32_t Q = (1u << bits) - 1u;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    uint32_t q = (uint32_t)(packed >> (i * bits)) & Q;
+    x[i] = __fadd_rn(__fmul_rn(sf, (float)q), zf);
+  }
+}
+
+__device__ __forceinline__ void store_codes(uint8_t* dst, uint64_t packed, int bits) {
+  if (bits == 8) *reinterpret_cast<uint2*>(dst) = make_uint2((uint32_t)packed, (uint32_t)(packed >> 32));
+  else if (bits == 4) *reinterpret_cast<uint32_t*>(dst) = (uint32_t)packed;
+  else *reinterpret_cast<uint16_t*>(dst) = (uint16_t)packed;
+}
+__device__ __forceinline__ uint64_t load_codes(const uint8_t* src, int bits) {
+  if (bits == 8) {
+    uint2 v = *reinterpret_cast<const uint2*>(src);
+    return (uint64_t)v.x | ((uint64_t)v.y << 32);
+  }
+  if (bits == 4) return *reinterpret_cast<const uint32_t*>(src);
+  return *reinterpret_cast<const uint16_t*>(src);
+}
+
+// Geometry of class `cls` selected field by field (a runtime index into the kernel-parameter struct
+// would force a local-memory copy of it).
+__device__ __forceinline__ ClassGeom geom_of(const PoolDev& p, int cls) {
+  const bool h = cls == DKV_CLS_HIGH;
+  ClassGeom g;
+  g.C = h ? p.g[1].C : p.g[2].C;
+  g.kbits = h ? p.g[1].kbits : p.g[2].kbits;
+  g.vbits = h ? p.g[1].vbits : p.g[2].vbits;
+  g.k_row = h ? p.g[1].k_row : p.g[2].k_row;
+  g.v_row = h ? p.g[1].v_row : p.g[2].v_row;
+  g.off_k = h ? p.g[1].off_k : p.g[2].off_k;
+  g.off_kmeta = h ? p.g[1].off_kmeta : p.g[2].off_kmeta;
+  g.off_v = h ? p.g[1].off_v : p.g[2].off_v;
+  g.off_vmeta = h ? p.g[1].off_vmeta : p.g[2].off_vmeta;
+  g.off_score = h ? p.g[1].off_score : p.g[2].off_score;
+  g.off_pos = h ? p.g[1].off_pos : p.g[2].off_pos;
+  return g;
+}
+
+// Section slot s of class cls of unit u -> (page pointer, index in page)  (c.1)
+__device__ __forceinline__ uint8_t* slot_page(const PoolDev& p, int cls, int u, int s, int& idx) {
+  const int C = cls == DKV_CLS_HIGH ? p.g[1].C : p.g[2].C;
+  const int k = (cls == DKV_CLS_HIGH) ? s / C : p.L - 1 - s / C;
+  const int pid = p.table[(size_t)u * p.L + k];
+  idx = s % C;
+  return p.pages + (size_t)pid * (size_t)p.page_bytes;
+}
+
+__device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------------------------- launchers
+// Each returns a cudaError_t from the launch.
+cudaError_t launch_init(const PoolDev& p, cudaStream_t s);
+cudaError_t launch_set_requests(const PoolDev& p, const int32_t* req, const int32_t* len, int n, int mode,
+                                cudaStream_t s);
+cudaError_t launch_clear_status(const PoolDev& p, cudaStream_t s);
+cudaError_t launch_classify_decode(const PoolDev& p, const float* sig, dkv_decision_t* dec, cudaStream_t s);
+cudaError_t launch_classify_prefill(const PoolDev& p, int n, const float* sig, int64_t sig_stride, uint8_t* cls,
+                                    int max_len, cudaStream_t s);
+cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s);
+cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
+                                const float* sig, cudaStream_t s);
+cudaError_t launch_quant_prefill(const PoolDev& p, int n, const uint16_t* k, const uint16_t* v, int64_t kv_stride,
+                                 const float* sig, int64_t sig_stride, int max_len, cudaStream_t s);
+int compact_max_coresident(int tile_units);
+
+}  // namespace dkv

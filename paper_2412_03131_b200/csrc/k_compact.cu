@@ -1,0 +1,288 @@
+// k_compact.cu — coordination: recycle (stream compaction into the circular free list) + allocation
+// (exclusive scan of per-head demand, all-or-nothing grant, bidirectional table write) in ONE kernel.
+//
+// "after each head determines the number of pages to be allocated or freed, a parallel prefix
+// sum operation computes a unique offset for each head relative to the start or end pointer ... each head
+// concurrently retrieves its new page IDs from its designated region in the list, with the start pointer
+// incremented by the cumulative number of pages required ... for memory recycling, each head writes freed
+// page IDs to its designated region, with the end pointer incremented by the total number of pages
+// released."
+//
+// One CTA = one tile of `tile_units` consecutive units (one thread per unit).  Both scans (demand, freed
+// pages) run in a single pass: warp ballot/popc (0/1 decode demand) or shuffle scans, a shared-memory
+// scan of warp totals, then a decoupled look-back across tiles on one 64-bit status word per tile
+// {tag:6 | flag:2 | freed:28 | demand:28} published with st.release.gpu / read with ld.acquire.gpu; tile
+// order comes from a ticket counter and the epoch tag is the ticket quotient, so status words never need
+// resetting.  Recycled IDs are written right after the look-back.  All-or-nothing allocation (Q15) needs
+// the grid-wide demand before any grant, and grants may read ring slots recycled by other tiles in this
+// call (Q14), so the kernel then crosses one software grid barrier (arrival counter; the launch is
+// cooperative, which guarantees co-residency) and grants.
+#include <cooperative_groups.h>
+
+#include "dkv_internal.cuh"
+
+namespace dkv {
+
+constexpr uint64_t kFlagAgg = 1, kFlagPre = 2;
+constexpr uint32_t kValMask = (1u << 28) - 1u;
+
+__device__ __forceinline__ unsigned long long pack_status(uint32_t tag, uint64_t flag, uint32_t fr, uint32_t dem) {
+  return ((unsigned long long)(tag & 63u) << 58) | (flag << 56) | ((unsigned long long)(fr & kValMask) << 28) |
+         (unsigned long long)(dem & kValMask);
+}
+__device__ __forceinline__ uint32_t st_tag(unsigned long long w) { return (uint32_t)(w >> 58); }
+__device__ __forceinline__ uint32_t st_flag(unsigned long long w) { return (uint32_t)(w >> 56) & 3u; }
+__device__ __forceinline__ uint32_t st_fr(unsigned long long w) { return (uint32_t)(w >> 28) & kValMask; }
+__device__ __forceinline__ uint32_t st_dem(unsigned long long w) { return (uint32_t)w & kValMask; }
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += y;
+  }
+  return v;
+}
+
+template <int TU>
+__global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, int phase) {
+  constexpr int NW = TU / 32;
+  __shared__ int s_tile;
+  __shared__ unsigned long long s_epoch;
+  __shared__ int64_t s_start0, s_free0, s_D, s_F;
+  __shared__ int s_status0;
+  __shared__ uint32_t s_wdem[NW], s_wfr[NW];
+  __shared__ uint32_t s_exdem, s_exfr, s_incdem, s_incfr;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  Ctrl* ctrl = p.ctrl;
+  if (tid == 0) {
+    const unsigned long long t = atomicAdd(&ctrl->ticket, 1ull);
+    s_tile = (int)(t % (unsigned long long)p.num_tiles);
+    s_epoch = t / (unsigned long long)p.num_tiles;
+    s_start0 = ld_volatile(&ctrl->start);
+    s_free0 = ld_volatile(&ctrl->free);
+    s_status0 = ld_volatile(&ctrl->status);
+  }
+  __syncthreads();
+  const int tile = s_tile;
+  const unsigned long long epoch = s_epoch;
+  const uint32_t tag = (uint32_t)(epoch & 63ull);
+  const int64_t start0 = s_start0, free0 = s_free0;
+  const int status0 = s_status0;
+  const int P = p.P, L = p.L;
+
+  // ---- per-unit demand and freed pages (planning results)
+  const int u = tile * TU + tid;
+  int st = -1, r = 0, nh = 0, nl = 0, grow = 0;
+  uint32_t dem = 0, fr = 0;
+  if (u < p.U) {
+    r = u / p.LyH;
+    st = p.req_state[r];
+    nh = p.n_h[u];
+    nl = p.n_l[u];
+    if (st == DKV_REQ_PENDING_FREE) fr = ceil_div(nh, p.Ch) + ceil_div(nl, p.Cl);
+    if (status0 == 0) {
+      if (phase == DKV_PHASE_DECODE) {
+        if (st == DKV_REQ_ACTIVE) {
+          const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(dec + u));
+          dem = w >> 24;
+          grow = (w >> 16) & 0xFF;
+        }
+      } else if (st == DKV_REQ_ADMITTING) {
+        dem = ceil_div(p.pf_nh[u], p.Ch) + ceil_div(p.pf_nl[u], p.Cl);
+      }
+    }
+  }
+
+  // ---- tile-local exclusive scans
+  uint32_t inc_dem;
+  if (phase == DKV_PHASE_DECODE) {                               // demand is 0/1: ballot + popc
+    const unsigned m = __ballot_sync(kFull, dem != 0);
+    inc_dem = __popc(m & (0xFFFFFFFFu >> (31 - lane)));
+  } else {
+    inc_dem = warp_incl_scan(dem, lane);
+  }
+  const uint32_t inc_fr = warp_incl_scan(fr, lane);
+  if (lane == 31) { s_wdem[warp] = inc_dem; s_wfr[warp] = inc_fr; }
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t a = lane < NW ? s_wdem[lane] : 0u, b = lane < NW ? s_wfr[lane] : 0u;
+    const uint32_t ia = warp_incl_scan(a, lane), ib = warp_incl_scan(b, lane);
+    if (lane < NW) { s_wdem[lane] = ia - a; s_wfr[lane] = ib - b; }
+    const uint32_t tot_dem = __shfl_sync(kFull, ia, 31), tot_fr = __shfl_sync(kFull, ib, 31);
+    // ---- decoupled look-back across tiles
+    unsigned long long* stat = p.tile_status;
+    uint32_t ex_d = 0, ex_f = 0;
+    if (tile == 0) {
+      if (lane == 0) st_release(&stat[0], pack_status(tag, kFlagPre, tot_fr, tot_dem));
+    } else {
+      if (lane == 0) st_release(&stat[tile], pack_status(tag, kFlagAgg, tot_fr, tot_dem));
+      int look = tile - 1;
+      while (true) {
+        const int idx = look - lane;
+        const unsigned long long w = idx >= 0 ? ld_acquire(&stat[idx]) : pack_status(tag, kFlagPre, 0, 0);
+        const bool valid = st_tag(w) == tag && st_flag(w) != 0;
+        const unsigned vm = __ballot_sync(kFull, valid);
+        const unsigned pm = __ballot_sync(kFull, valid && st_flag(w) == kFlagPre);
+        if (pm) {
+          const int jl = __ffs(pm) - 1;
+          const unsigned need = (jl == 31) ? kFull : ((2u << jl) - 1u);
+          if ((vm & need) != need) continue;                     // a nearer predecessor not published yet
+          ex_d += __reduce_add_sync(kFull, lane <= jl ? st_dem(w) : 0u);
+          ex_f += __reduce_add_sync(kFull, lane <= jl ? st_fr(w) : 0u);
+          break;
+        }
+        if (vm == kFull) {
+          ex_d += __reduce_add_sync(kFull, st_dem(w));
+          ex_f += __reduce_add_sync(kFull, st_fr(w));
+          look -= 32;
+        }
+      }
+      if (lane == 0) st_release(&stat[tile], pack_status(tag, kFlagPre, ex_f + tot_fr, ex_d + tot_dem));
+    }
+    if (lane == 0) { s_exdem = ex_d; s_exfr = ex_f; s_incdem = ex_d + tot_dem; s_incfr = ex_f + tot_fr; }
+  }
+  __syncthreads();
+  const uint32_t off_dem = s_exdem + s_wdem[warp] + inc_dem - (phase == DKV_PHASE_DECODE ? (dem != 0) : dem);
+  const uint32_t off_fr = s_exfr + s_wfr[warp] + inc_fr - fr;
+
+  // ---- recycle: freed IDs -> ring[(end + off + k) mod P], canonical slot order (Q13); warp-cooperative
+  {
+    const int64_t end0 = (start0 + free0) % P;
+    unsigned fm = __ballot_sync(kFull, fr != 0);
+    while (fm) {
+      const int src = __ffs(fm) - 1;
+      fm &= fm - 1;
+      const int uu = __shfl_sync(kFull, u, src);
+      const uint32_t off = __shfl_sync(kFull, off_fr, src);
+      const int nfr = (int)__shfl_sync(kFull, fr, src);
+      const int ph = __shfl_sync(kFull, ceil_div(nh, p.Ch), src);
+      int32_t* row = p.table + (size_t)uu * L;
+      for (int k = lane; k < nfr; k += 32) {
+        const int slot = k < ph ? k : L - nfr + k;               // [0, ph) then [L - pl, L)
+        const int32_t pid = row[slot];
+        p.ring[(end0 + off + k) % P] = pid;
+        row[slot] = -1;
+      }
+    }
+    if (fr != 0) { p.n_h[u] = 0; p.n_l[u] = 0; }
+  }
+  __syncthreads();
+
+  // ---- grid barrier: every tile's recycle writes are visible and the totals are known
+  if (tid == 0) {
+    if (tile == p.num_tiles - 1) { ctrl->total_dem = s_incdem; ctrl->total_fr = s_incfr; }
+    __threadfence();
+    atomicAdd(&ctrl->arrive, 1ull);
+    const unsigned long long target = (epoch + 1ull) * (unsigned long long)p.num_tiles;
+    while (ld_acquire(&ctrl->arrive) < target) __nanosleep(40);
+    s_D = ld_volatile(&ctrl->total_dem);
+    s_F = ld_volatile(&ctrl->total_fr);
+  }
+  __syncthreads();
+  const int64_t D = s_D, F = s_F, free_avail = free0 + F;
+  const bool ok = (status0 == 0) && (D <= free_avail);
+
+  // ---- grant + bidirectional table write + counts
+  if (ok) {
+    if (phase == DKV_PHASE_DECODE) {
+      if (dem) {
+        const int ph = ceil_div(nh, p.Ch), pl = ceil_div(nl, p.Cl);
+        if (ph + pl + 1 > L) {
+          set_status(ctrl, DKV_ERR_OVERFLOW);
+        } else {
+          const int slot = (grow == DKV_GROW_HIGH) ? nh / p.Ch : L - 1 - nl / p.Cl;
+          p.table[(size_t)u * L + slot] = __ldcg(p.ring + (start0 + off_dem) % P);
+        }
+      }
+      if (st == DKV_REQ_ACTIVE) {
+        if (grow == DKV_GROW_HIGH) p.n_h[u] = nh + 1;
+        if (grow == DKV_GROW_LOW) p.n_l[u] = nl + 1;             // DOWN: n_h unchanged, n_l + 1
+      }
+    } else {
+      unsigned gm = __ballot_sync(kFull, dem != 0);
+      while (gm) {
+        const int src = __ffs(gm) - 1;
+        gm &= gm - 1;
+        const int uu = __shfl_sync(kFull, u, src);
+        const uint32_t off = __shfl_sync(kFull, off_dem, src);
+        const int nd = (int)__shfl_sync(kFull, dem, src);
+        const int ph = ceil_div(p.pf_nh[uu], p.Ch);
+        if (nd > L) {
+          if (lane == 0) set_status(ctrl, DKV_ERR_OVERFLOW);
+          continue;
+        }
+        int32_t* row = p.table + (size_t)uu * L;
+        for (int k = lane; k < nd; k += 32) {
+          const int slot = k < ph ? k : L - 1 - (k - ph);       // high left-to-right, low right-to-left
+          row[slot] = __ldcg(p.ring + (start0 + off + k) % P);
+        }
+      }
+      if (st == DKV_REQ_ADMITTING) { p.n_h[u] = p.pf_nh[u]; p.n_l[u] = p.pf_nl[u]; }
+    }
+  }
+  // ---- request-level transitions (all tiles read req_state before the barrier)
+  if (u < p.U && u % p.LyH == 0) {
+    if (st == DKV_REQ_PENDING_FREE) {
+      p.req_state[r] = DKV_REQ_IDLE; p.seq_len[r] = 0; p.prompt_len[r] = 0;
+    } else if (ok && phase == DKV_PHASE_DECODE && st == DKV_REQ_ACTIVE) {
+      p.seq_len[r] += 1;
+    } else if (ok && phase == DKV_PHASE_PREFILL && st == DKV_REQ_ADMITTING) {
+      p.seq_len[r] = p.prompt_len[r];
+    }
+  }
+  // ---- pointers (every tile read them before arriving at the barrier)
+  if (tile == 0 && tid == 0) {
+    if (status0 == 0 && !ok) { set_status(ctrl, DKV_ERR_OOM); ctrl->oom_count += 1; }
+    const int64_t ns = ok ? (start0 + D) % P : start0;
+    const int64_t nf = ok ? free_avail - D : free_avail;
+    ctrl->start = ns;
+    ctrl->free = nf;
+    ctrl->last_demand = status0 == 0 ? D : 0;
+    ctrl->last_freed = F;
+    p.stats[0] = nf;
+    p.stats[1] = -(status0 == 0 ? D : 0);
+    p.stats[2] = -((int64_t)P - nf);
+    p.stats[3] = -(int64_t)ld_volatile(&ctrl->status);
+  }
+}
+
+template <int TU>
+static cudaError_t launch_tu(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.num_tiles);
+  cfg.blockDim = dim3(TU);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, compact_alloc_kernel<TU>, p, dec, phase);
+}
+
+cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s) {
+  switch (p.tile_units) {
+    case 256: return launch_tu<256>(p, dec, phase, s);
+    case 512: return launch_tu<512>(p, dec, phase, s);
+    default: return launch_tu<1024>(p, dec, phase, s);
+  }
+}
+
+int compact_max_coresident(int tile_units) {
+  int dev = 0, sms = 0, per = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  cudaError_t e;
+  switch (tile_units) {
+    case 256: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, compact_alloc_kernel<256>, 256, 0); break;
+    case 512: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, compact_alloc_kernel<512>, 512, 0); break;
+    default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, compact_alloc_kernel<1024>, 1024, 0); break;
+  }
+  if (e != cudaSuccess) return 0;
+  return per * sms;
+}
+
+}  // namespace dkv

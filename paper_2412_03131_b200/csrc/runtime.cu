@@ -1,0 +1,371 @@
+// runtime.cu — host side of the C ABI (include/dkv.h): validation, arena layout, the request-state
+// mirror and call sequencing, kernel launches.  No device memory is allocated after dkv_pool_init; every
+// call is asynchronous on the caller's stream except dkv_pool_query.
+#include <stdlib.h>
+#include <string.h>
+
+#include <vector>
+
+#include "dkv_internal.cuh"
+
+using namespace dkv;
+
+namespace {
+
+constexpr int64_t kAlign = 256;
+int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+bool bits_ok(int32_t b) { return b == 2 || b == 4 || b == 8; }
+
+void class_geom(int d, int C, int kb, int vb, ClassGeom& g) {
+  auto a16 = [](int x) { return (x + 15) / 16 * 16; };
+  g.C = C; g.kbits = kb; g.vbits = vb;
+  g.k_row = d * kb / 8;
+  g.v_row = d * vb / 8;
+  g.off_k = 0;
+  g.off_kmeta = a16(g.off_k + C * g.k_row);
+  g.off_v = a16(g.off_kmeta + 4 * C);
+  g.off_vmeta = a16(g.off_v + C * g.v_row);
+  g.off_score = a16(g.off_vmeta + 4 * C);
+  g.off_pos = a16(g.off_score + 4 * C);
+}
+int class_end(const ClassGeom& g) { return g.off_pos + 4 * g.C; }
+
+struct Geometry {
+  int32_t U, L, page_bytes, num_tiles, tile_units, nseg;
+  ClassGeom g[3];
+};
+
+bool validate(const dkv_config_t* c, Geometry& G) {
+  if (!c) return false;
+  if (c->max_requests < 1 || c->num_layers < 1 || c->num_kv_heads < 1) return false;
+  if (c->head_dim != 64 && c->head_dim != 128) return false;
+  if (c->max_seq_len < 1 || c->window < 0 || c->window > c->max_seq_len) return false;
+  if (c->page_tokens_high < 4 || c->page_tokens_high % 4 || c->page_tokens_low < c->page_tokens_high ||
+      c->page_tokens_low % 4)
+    return false;
+  if (!bits_ok(c->kbits_high) || !bits_ok(c->vbits_high) || !bits_ok(c->kbits_low) || !bits_ok(c->vbits_low))
+    return false;
+  if (c->num_pages < 1) return false;
+  if (!(c->alpha_h >= 0.0f && c->alpha_h <= 3.0e38f) || !(c->alpha_l >= 0.0f && c->alpha_l <= 3.0e38f)) return false;
+  if (c->prompt_denominator != 0 && c->prompt_denominator != 1) return false;
+  if (c->tile_units != 0 && c->tile_units != 256 && c->tile_units != 512 && c->tile_units != 1024) return false;
+  if (c->reserved[0] || c->reserved[1]) return false;
+  const int64_t U = (int64_t)c->max_requests * c->num_layers * c->num_kv_heads;
+  if (U >= (1 << 24)) return false;
+  G.U = (int32_t)U;
+  // P:499 table length, corrected by Q12
+  G.L = (c->max_seq_len + c->page_tokens_high - 1) / c->page_tokens_high + (c->window < c->page_tokens_high ? 1 : 0);
+  if ((int64_t)G.U * G.L >= (1 << 28)) return false;
+  class_geom(c->head_dim, c->page_tokens_high, c->kbits_high, c->vbits_high, G.g[DKV_CLS_HIGH]);
+  class_geom(c->head_dim, c->page_tokens_low, c->kbits_low, c->vbits_low, G.g[DKV_CLS_LOW]);
+  G.g[0] = G.g[DKV_CLS_HIGH];
+  const int e = class_end(G.g[1]) > class_end(G.g[2]) ? class_end(G.g[1]) : class_end(G.g[2]);
+  G.page_bytes = (e + 127) / 128 * 128;
+  G.tile_units = c->tile_units ? c->tile_units : 1024;
+  G.num_tiles = (G.U + G.tile_units - 1) / G.tile_units;
+  G.nseg = (c->max_seq_len + kSegTokens - 1) / kSegTokens;
+  return true;
+}
+
+bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
+  if (!validate(c, G)) return false;
+  memset(&Lo, 0, sizeof(Lo));
+  const int64_t U = G.U, R = c->max_requests, P = c->num_pages;
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) { int64_t at = o; o = align_up(o + bytes, kAlign); return at; };
+  Lo.off_ctrl = take(256);
+  Lo.off_stats = take(32);
+  Lo.off_tile_status = take(8 * (int64_t)G.num_tiles);
+  Lo.off_ring = take(4 * P);
+  Lo.off_table = take(4 * U * G.L);
+  Lo.off_n_h = take(4 * U);
+  Lo.off_n_l = take(4 * U);
+  Lo.off_req_state = take(R);
+  Lo.off_seq_len = take(4 * R);
+  Lo.off_prompt_len = take(4 * R);
+  Lo.off_admit = take(4 * R);
+  Lo.off_pf_nh = take(4 * U);
+  Lo.off_pf_nl = take(4 * U);
+  Lo.off_pf_seg = take(8 * U * G.nseg);
+  const int64_t wbytes = 2 * U * (int64_t)c->window * c->head_dim;
+  Lo.off_win_k = take(wbytes);
+  Lo.off_win_v = take(wbytes);
+  o = align_up(o, 4096);
+  Lo.off_pages = take(P * (int64_t)G.page_bytes);
+  Lo.arena_bytes = o;
+  Lo.units = G.U; Lo.table_len = G.L; Lo.page_bytes = G.page_bytes; Lo.num_tiles = G.num_tiles;
+  Lo.tile_units = G.tile_units; Lo.seg_tokens = kSegTokens; Lo.num_segs = G.nseg;
+  for (int k = 1; k <= 2; k++) {
+    const ClassGeom& g = G.g[k];
+    Lo.C[k] = g.C; Lo.k_row[k] = g.k_row; Lo.v_row[k] = g.v_row; Lo.off_k[k] = g.off_k;
+    Lo.off_kmeta[k] = g.off_kmeta; Lo.off_v[k] = g.off_v; Lo.off_vmeta[k] = g.off_vmeta;
+    Lo.off_score[k] = g.off_score; Lo.off_pos[k] = g.off_pos;
+  }
+  return true;
+}
+
+enum Seq { SEQ_IDLE = 0, SEQ_CLASSIFIED = 1, SEQ_COMPACTED = 2 };
+
+}  // namespace
+
+struct dkv_pool {
+  dkv_config_t cfg;
+  Geometry G;
+  dkv_layout_t lay;
+  PoolDev dev;
+  uint8_t* base;
+  std::vector<int8_t> req_state;     // host mirror
+  std::vector<int32_t> seq_len;      // host mirror
+  std::vector<int32_t> admitted;     // current admission batch
+  std::vector<int32_t> admitted_len;
+  int seq;                           // SEQ_*
+  int phase;                         // phase of the last classify
+  Ctrl* h_ctrl;                      // pinned host staging for query
+  int8_t* h_req;
+  int32_t* h_seq;
+  bool recovering;                   // last query reported an error: frees allowed out of sequence
+};
+
+static dkv_status_t cuda_status(cudaError_t e) { return e == cudaSuccess ? DKV_OK : DKV_ERR_CUDA; }
+
+extern "C" {
+
+const char* dkv_status_string(dkv_status_t st) {
+  switch (st) {
+    case DKV_OK: return "ok";
+    case DKV_ERR_INVALID_ARG: return "invalid argument";
+    case DKV_ERR_STATE: return "request state or call order violated";
+    case DKV_ERR_OOM: return "out of pages (allocation not applied)";
+    case DKV_ERR_NONFINITE: return "non-finite input";
+    case DKV_ERR_OVERFLOW: return "page table overflow";
+    case DKV_ERR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+size_t dkv_arena_bytes(const dkv_config_t* cfg) {
+  Geometry G;
+  dkv_layout_t Lo;
+  if (!make_layout(cfg, G, Lo)) return 0;
+  return (size_t)Lo.arena_bytes;
+}
+
+dkv_status_t dkv_pool_layout(const dkv_config_t* cfg, dkv_layout_t* out) {
+  Geometry G;
+  if (!out || !make_layout(cfg, G, *out)) return DKV_ERR_INVALID_ARG;
+  return DKV_OK;
+}
+
+dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_bytes, dkv_stream_t s,
+                           dkv_pool_t* out) {
+  if (!out) return DKV_ERR_INVALID_ARG;
+  *out = nullptr;
+  Geometry G;
+  dkv_layout_t Lo;
+  if (!make_layout(cfg, G, Lo)) return DKV_ERR_INVALID_ARG;
+  if (!d_arena || ((uintptr_t)d_arena % kAlign) || arena_bytes < (size_t)Lo.arena_bytes) return DKV_ERR_INVALID_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return DKV_ERR_CUDA;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, d_arena) != cudaSuccess || attr.type != cudaMemoryTypeDevice) {
+    cudaGetLastError();
+    return DKV_ERR_INVALID_ARG;
+  }
+  const int cores = compact_max_coresident(G.tile_units);
+  if (cores <= 0) return DKV_ERR_CUDA;
+  if (G.num_tiles > cores) return DKV_ERR_INVALID_ARG;   // the scan's grid barrier needs co-residency
+  dkv_pool* p = new dkv_pool();
+  p->cfg = *cfg;
+  p->G = G;
+  p->lay = Lo;
+  p->base = (uint8_t*)d_arena;
+  p->req_state.assign(cfg->max_requests, DKV_REQ_IDLE);
+  p->seq_len.assign(cfg->max_requests, 0);
+  p->seq = SEQ_IDLE;
+  p->phase = -1;
+  p->recovering = false;
+  if (cudaMallocHost(&p->h_ctrl, sizeof(Ctrl)) != cudaSuccess ||
+      cudaMallocHost(&p->h_req, cfg->max_requests) != cudaSuccess ||
+      cudaMallocHost(&p->h_seq, 4 * (size_t)cfg->max_requests) != cudaSuccess) {
+    delete p;
+    return DKV_ERR_CUDA;
+  }
+  PoolDev& d = p->dev;
+  memset(&d, 0, sizeof(d));
+  d.R = cfg->max_requests; d.Ly = cfg->num_layers; d.H = cfg->num_kv_heads; d.LyH = d.Ly * d.H; d.U = G.U;
+  d.d = cfg->head_dim; d.M = cfg->max_seq_len; d.W = cfg->window; d.L = G.L; d.P = cfg->num_pages;
+  d.page_bytes = G.page_bytes; d.Ch = cfg->page_tokens_high; d.Cl = cfg->page_tokens_low;
+  d.prompt_den = cfg->prompt_denominator; d.num_tiles = G.num_tiles; d.tile_units = G.tile_units; d.nseg = G.nseg;
+  d.alpha_h = cfg->alpha_h; d.alpha_l = cfg->alpha_l;
+  for (int k = 0; k < 3; k++) d.g[k] = G.g[k];
+  uint8_t* b = p->base;
+  d.ctrl = (Ctrl*)(b + Lo.off_ctrl);
+  d.stats = (int64_t*)(b + Lo.off_stats);
+  d.tile_status = (unsigned long long*)(b + Lo.off_tile_status);
+  d.ring = (int32_t*)(b + Lo.off_ring);
+  d.table = (int32_t*)(b + Lo.off_table);
+  d.n_h = (int32_t*)(b + Lo.off_n_h);
+  d.n_l = (int32_t*)(b + Lo.off_n_l);
+  d.req_state = (int8_t*)(b + Lo.off_req_state);
+  d.seq_len = (int32_t*)(b + Lo.off_seq_len);
+  d.prompt_len = (int32_t*)(b + Lo.off_prompt_len);
+  d.admit = (int32_t*)(b + Lo.off_admit);
+  d.pf_nh = (int32_t*)(b + Lo.off_pf_nh);
+  d.pf_nl = (int32_t*)(b + Lo.off_pf_nl);
+  d.pf_seg = (int32_t*)(b + Lo.off_pf_seg);
+  d.win_k = (__half*)(b + Lo.off_win_k);
+  d.win_v = (__half*)(b + Lo.off_win_v);
+  d.pages = b + Lo.off_pages;
+  cudaError_t e = cudaMemsetAsync(b + Lo.off_pages, 0, (size_t)(Lo.arena_bytes - Lo.off_pages), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(b + Lo.off_win_k, 0, (size_t)(Lo.off_pages - Lo.off_win_k), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(b + Lo.off_pf_seg, 0, (size_t)(Lo.off_win_k - Lo.off_pf_seg), s);
+  if (e == cudaSuccess) e = launch_init(d, s);
+  if (e != cudaSuccess) {
+    dkv_pool_destroy(p);
+    return DKV_ERR_CUDA;
+  }
+  *out = p;
+  return DKV_OK;
+}
+
+dkv_status_t dkv_pool_destroy(dkv_pool_t p) {
+  if (!p) return DKV_ERR_INVALID_ARG;
+  if (p->h_ctrl) cudaFreeHost(p->h_ctrl);
+  if (p->h_req) cudaFreeHost(p->h_req);
+  if (p->h_seq) cudaFreeHost(p->h_seq);
+  delete p;
+  return DKV_OK;
+}
+
+dkv_status_t dkv_classify(dkv_pool_t p, int32_t phase, const int32_t* h_req, const int32_t* h_len, int32_t n,
+                          const float* d_sig, int64_t sig_stride, dkv_decision_t* d_dec, uint8_t* d_token_class,
+                          dkv_stream_t s) {
+  if (!p) return DKV_ERR_INVALID_ARG;
+  // a decode step interrupted by a device error may be abandoned (its compact_alloc applied nothing)
+  if (p->seq != SEQ_IDLE && !(p->recovering && p->phase == DKV_PHASE_DECODE)) return DKV_ERR_STATE;
+  const int R = p->cfg.max_requests;
+  if (phase == DKV_PHASE_DECODE) {
+    if (!d_sig || !d_dec) return DKV_ERR_INVALID_ARG;
+    for (int r = 0; r < R; r++)
+      if (p->req_state[r] == DKV_REQ_ACTIVE && p->seq_len[r] >= p->cfg.max_seq_len) return DKV_ERR_STATE;
+    cudaError_t e = launch_classify_decode(p->dev, d_sig, d_dec, (cudaStream_t)s);
+    if (e != cudaSuccess) return DKV_ERR_CUDA;
+  } else if (phase == DKV_PHASE_PREFILL) {
+    if (n < 0 || n > R || (n > 0 && (!h_req || !h_len || !d_sig))) return DKV_ERR_INVALID_ARG;
+    int max_len = 0;
+    std::vector<char> seen(R, 0);
+    for (int i = 0; i < n; i++) {
+      const int r = h_req[i];
+      if (r < 0 || r >= R || h_len[i] < 0 || h_len[i] > p->cfg.max_seq_len || h_len[i] > sig_stride || seen[r])
+        return DKV_ERR_INVALID_ARG;
+      if (p->req_state[r] != DKV_REQ_IDLE) return DKV_ERR_STATE;
+      seen[r] = 1;
+      if (h_len[i] > max_len) max_len = h_len[i];
+    }
+    cudaError_t e = launch_set_requests(p->dev, h_req, h_len, n, 0, (cudaStream_t)s);
+    if (e == cudaSuccess) e = launch_classify_prefill(p->dev, n, d_sig, sig_stride, d_token_class, max_len, (cudaStream_t)s);
+    if (e != cudaSuccess) return DKV_ERR_CUDA;
+    p->admitted.assign(h_req, h_req + n);
+    p->admitted_len.assign(h_len, h_len + n);
+    for (int i = 0; i < n; i++) p->req_state[h_req[i]] = DKV_REQ_ADMITTING;
+  } else {
+    return DKV_ERR_INVALID_ARG;
+  }
+  p->phase = phase;
+  p->seq = SEQ_CLASSIFIED;
+  return DKV_OK;
+}
+
+dkv_status_t dkv_compact_alloc(dkv_pool_t p, const dkv_decision_t* d_dec, dkv_stream_t s) {
+  if (!p) return DKV_ERR_INVALID_ARG;
+  if (p->seq == SEQ_IDLE && !p->recovering) return DKV_ERR_STATE;
+  if (p->phase == DKV_PHASE_DECODE && !d_dec) return DKV_ERR_INVALID_ARG;
+  cudaError_t e = launch_compact_alloc(p->dev, d_dec, p->phase, (cudaStream_t)s);
+  if (e != cudaSuccess) return DKV_ERR_CUDA;
+  const int R = p->cfg.max_requests;
+  for (int r = 0; r < R; r++) {
+    if (p->req_state[r] == DKV_REQ_PENDING_FREE) { p->req_state[r] = DKV_REQ_IDLE; p->seq_len[r] = 0; }
+    else if (p->phase == DKV_PHASE_DECODE && p->req_state[r] == DKV_REQ_ACTIVE) p->seq_len[r] += 1;
+  }
+  if (p->phase == DKV_PHASE_PREFILL)
+    for (size_t i = 0; i < p->admitted.size(); i++) p->seq_len[p->admitted[i]] = p->admitted_len[i];
+  p->seq = SEQ_COMPACTED;
+  return DKV_OK;
+}
+
+dkv_status_t dkv_quant_write(dkv_pool_t p, int32_t phase, const dkv_decision_t* d_dec, const uint16_t* d_k,
+                             const uint16_t* d_v, int64_t kv_stride, const float* d_sig, int64_t sig_stride,
+                             dkv_stream_t s) {
+  if (!p) return DKV_ERR_INVALID_ARG;
+  if (p->seq != SEQ_COMPACTED || phase != p->phase) return DKV_ERR_STATE;
+  cudaError_t e;
+  if (phase == DKV_PHASE_DECODE) {
+    if (!d_dec || !d_k || !d_v || !d_sig) return DKV_ERR_INVALID_ARG;
+    e = launch_quant_decode(p->dev, d_dec, d_k, d_v, d_sig, (cudaStream_t)s);
+  } else {
+    const int n = (int)p->admitted.size();
+    int max_len = 0;
+    for (int i = 0; i < n; i++) max_len = p->admitted_len[i] > max_len ? p->admitted_len[i] : max_len;
+    if (n > 0 && (!d_k || !d_v || !d_sig || kv_stride < max_len || sig_stride < max_len)) return DKV_ERR_INVALID_ARG;
+    e = launch_quant_prefill(p->dev, n, d_k, d_v, kv_stride, d_sig, sig_stride, max_len, (cudaStream_t)s);
+    for (int i = 0; i < n; i++) p->req_state[p->admitted[i]] = DKV_REQ_ACTIVE;
+    p->admitted.clear();
+    p->admitted_len.clear();
+  }
+  if (e != cudaSuccess) return DKV_ERR_CUDA;
+  p->seq = SEQ_IDLE;
+  p->recovering = false;
+  return DKV_OK;
+}
+
+dkv_status_t dkv_free(dkv_pool_t p, const int32_t* h_req, int32_t n, dkv_stream_t s) {
+  if (!p) return DKV_ERR_INVALID_ARG;
+  if (p->seq != SEQ_IDLE && !p->recovering) return DKV_ERR_STATE;
+  const int R = p->cfg.max_requests;
+  if (n < 0 || n > R || (n > 0 && !h_req)) return DKV_ERR_INVALID_ARG;
+  std::vector<char> seen(R, 0);
+  for (int i = 0; i < n; i++) {
+    const int r = h_req[i];
+    if (r < 0 || r >= R) return DKV_ERR_INVALID_ARG;
+    if (p->req_state[r] != DKV_REQ_ACTIVE || seen[r]) return DKV_ERR_STATE;
+    seen[r] = 1;
+  }
+  cudaError_t e = launch_set_requests(p->dev, h_req, nullptr, n, 1, (cudaStream_t)s);
+  if (e != cudaSuccess) return DKV_ERR_CUDA;
+  for (int i = 0; i < n; i++) p->req_state[h_req[i]] = DKV_REQ_PENDING_FREE;
+  return DKV_OK;
+}
+
+dkv_status_t dkv_pool_query(dkv_pool_t p, dkv_stats_t* out, dkv_stream_t s) {
+  if (!p) return DKV_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)s;
+  const int R = p->cfg.max_requests;
+  cudaError_t e = cudaMemcpyAsync(p->h_ctrl, p->dev.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(p->h_req, p->dev.req_state, R, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(p->h_seq, p->dev.seq_len, 4 * (size_t)R, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = launch_clear_status(p->dev, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return DKV_ERR_CUDA;
+  const Ctrl& c = *p->h_ctrl;
+  if (out) {
+    out->free_pages = c.free;
+    out->used_pages = (int64_t)p->cfg.num_pages - c.free;
+    out->start = c.start;
+    out->last_demand = c.last_demand;
+    out->last_freed = c.last_freed;
+    out->status = c.status;
+    out->oom_count = c.oom_count;
+  }
+  for (int r = 0; r < R; r++) { p->req_state[r] = p->h_req[r]; p->seq_len[r] = p->h_seq[r]; }
+  if (c.status != DKV_OK) {
+    p->recovering = true;
+    // an interrupted sequence may be resumed (re-issue dkv_compact_alloc) or abandoned
+    if (p->seq == SEQ_COMPACTED) p->seq = SEQ_CLASSIFIED;
+  }
+  return c.status;
+}
+
+int64_t* dkv_pool_stats_device_ptr(dkv_pool_t p) { return p ? p->dev.stats : nullptr; }
+
+}  // extern "C"

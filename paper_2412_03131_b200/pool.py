@@ -1,0 +1,98 @@
+"""Pool: a torch-owned arena plus the C-ABI handle (plumbing only — every step runs in libdkv.so).
+
+torch supplies the device memory (one uint8 CUDA tensor, the arena) and the stream; the methods call
+the C ABI by name.  ``views()`` exposes the arena's buffers as torch views at the offsets the library
+reports (dkv_pool_layout) for inspection by tests and the admission logic.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import dkv as _d
+
+
+class Pool:
+    def __init__(self, cfg: _d.dkv_config_t, device=None, stream=None):
+        self.cfg = cfg
+        self.layout = _d.dkv_pool_layout(cfg)
+        self.device = torch.device(device if device is not None else "cuda")
+        nbytes = int(self.layout.arena_bytes)
+        self.arena = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.stream = stream
+        self.handle = _d.dkv_pool_init(cfg, self.arena, nbytes, stream)
+        L = self.layout
+        self.U, self.L, self.page_bytes = L.units, L.table_len, L.page_bytes
+        self.LyH = cfg.num_layers * cfg.num_kv_heads
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _d.dkv_pool_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- the ABI, by name
+    def classify_decode(self, sig, dec, stream=None):
+        return _d.dkv_classify(self.handle, _d.DKV_PHASE_DECODE, None, None, 0, sig, 0, dec, None,
+                               stream or self.stream)
+
+    def classify_prefill(self, reqs, lens, sig, token_class=None, stream=None):
+        return _d.dkv_classify(self.handle, _d.DKV_PHASE_PREFILL, reqs, lens, len(reqs), sig, sig.shape[-1], None,
+                               token_class, stream or self.stream)
+
+    def compact_alloc(self, dec=None, stream=None):
+        return _d.dkv_compact_alloc(self.handle, dec, stream or self.stream)
+
+    def quant_write_decode(self, dec, k, v, sig, stream=None):
+        return _d.dkv_quant_write(self.handle, _d.DKV_PHASE_DECODE, dec, k, v, 0, sig, 0, stream or self.stream)
+
+    def quant_write_prefill(self, k, v, sig, stream=None):
+        return _d.dkv_quant_write(self.handle, _d.DKV_PHASE_PREFILL, None, k, v, k.shape[-2], sig, sig.shape[-1],
+                                  stream or self.stream)
+
+    def free(self, reqs, stream=None):
+        return _d.dkv_free(self.handle, reqs, len(reqs), stream or self.stream)
+
+    def query(self, stream=None):
+        return _d.dkv_pool_query(self.handle, stream or self.stream)
+
+    def new_decisions(self):
+        return torch.empty((self.U, 4), dtype=torch.int32, device=self.device)
+
+    # ---- views (plumbing for tests / admission)
+    def _view(self, off, nbytes, dtype, shape):
+        t = self.arena[int(off): int(off) + int(nbytes)]
+        return t.view(dtype).view(shape)
+
+    def views(self):
+        L, c = self.layout, self.cfg
+        U, R, P = self.U, c.max_requests, c.num_pages
+        W, d = c.window, c.head_dim
+        return dict(
+            ctrl=self._view(L.off_ctrl, 32, torch.int64, (4,)),           # start, free, {status, oom}
+            ring=self._view(L.off_ring, 4 * P, torch.int32, (P,)),
+            table=self._view(L.off_table, 4 * U * self.L, torch.int32, (U, self.L)),
+            n_h=self._view(L.off_n_h, 4 * U, torch.int32, (U,)),
+            n_l=self._view(L.off_n_l, 4 * U, torch.int32, (U,)),
+            req_state=self._view(L.off_req_state, R, torch.int8, (R,)),
+            seq_len=self._view(L.off_seq_len, 4 * R, torch.int32, (R,)),
+            win_k=self._view(L.off_win_k, 2 * U * W * d, torch.int16, (U, W, d)),
+            win_v=self._view(L.off_win_v, 2 * U * W * d, torch.int16, (U, W, d)),
+            pages=self._view(L.off_pages, P * self.page_bytes, torch.uint8, (P, self.page_bytes)),
+            stats=self._view(L.off_stats, 32, torch.int64, (4,)),
+        )
+
+    def geom(self):
+        L = self.layout
+        return {c: dict(C=L.C[c], k_row=L.k_row[c], v_row=L.v_row[c], off_k=L.off_k[c], off_kmeta=L.off_kmeta[c],
+                        off_v=L.off_v[c], off_vmeta=L.off_vmeta[c], off_score=L.off_score[c], off_pos=L.off_pos[c])
+                for c in (1, 2)}
+
+
+def decisions_to_numpy(dec: torch.Tensor) -> np.ndarray:
+    return dec.detach().cpu().contiguous().numpy().view(_d.DECISION_DTYPE).reshape(-1)

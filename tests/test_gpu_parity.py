@@ -1,0 +1,94 @@
+"""GPU-vs-oracle parity through the C ABI: bit-exact decisions, ring, pointers, tables, counts, request
+state, window and page bytes after EVERY call, on seeded synthetic lifecycles (prefill, decode with
+significance drift, frees, re-admission)."""
+import numpy as np
+import pytest
+import torch
+
+from tests import harness as H
+
+pytestmark = pytest.mark.gpu
+
+
+def _mk(scn):
+    from tests.gpu_backend import GpuBackend
+    return H.OracleBackend(scn), GpuBackend(scn)
+
+
+def _lifecycle(scn, steps, prompt_lens, frees=(), readmit_len=None, pages_every=1, tol_steps=None):
+    from tests.gpu_backend import compare_state, dec_np
+    o, g = _mk(scn)
+    inp = H.Inputs(scn)
+    life = H.Lifecycle(scn)
+    counter = {"n": 0}
+
+    def check(where, decs=None):
+        counter["n"] += 1
+        if decs is not None:
+            a, b = dec_np(decs[0]), dec_np(decs[1])
+            if not np.array_equal(a.view(np.uint8), b.view(np.uint8)):
+                bad = np.nonzero(a != b)[0]
+                raise AssertionError(f"[{where}] decisions differ at units {bad[:8].tolist()}: oracle {a[bad[0]]} gpu {b[bad[0]]}")
+        with_pages = (counter["n"] % pages_every == 0) or where.endswith("prefill")
+        so, sg = o.snapshot(pages=with_pages), g.snapshot(pages=with_pages)
+        compare_state(so, sg, where=where)
+        assert sg["status"] == 0, f"[{where}] device status {sg['status']}"
+
+    reqs = list(range(len(prompt_lens)))
+    H.admit([o, g], inp, life, reqs, prompt_lens, check=check)
+    pending = {}
+    frees = dict(frees)
+    for step in range(steps):
+        H.decode_step([o, g], inp, life, step, check=check)
+        for r, t in list(pending.items()):
+            if step >= t and o.pool.req_state[r] == 0:
+                H.admit([o, g], inp, life, [r], [readmit_len or prompt_lens[r]], check=check)
+                del pending[r]
+        if step in frees:
+            H.free([o, g], life, frees[step])
+            check(f"free@{step}")
+            for r in frees[step]:
+                pending[r] = step + 1
+    return o, g, life
+
+
+def test_tiny_parity_every_call():
+    # BASELINE configs[0]: 4 requests x 2 layers x 4 KV heads, head_dim 64, 64-token prompts, 16-token pages,
+    # 1024 pages; 64 decode steps, one request freed at step 32 and re-admitted
+    _lifecycle(H.TINY, steps=64, prompt_lens=[64, 64, 64, 64], frees=[(32, [1])], readmit_len=48)
+
+
+@pytest.mark.parametrize("tile_units", [256, 1024])
+def test_multi_tile_ragged_parity(tile_units):
+    # U = 7 * 5 * 40 = 1400 units: 6 tiles of 256 (ragged tail 120) or 2 of 1024; d = 128, K8V4/K4V2,
+    # W = 64, ragged prompt lengths (some <= W), frees of several requests in one step
+    scn = H.TINY.replace(R=7, Ly=5, H=40, d=128, M=1100, W=64, P=40000, seed=11, tile_units=tile_units)
+    lens = [300, 64, 517, 40, 0, 1000, 129]
+    _lifecycle(scn, steps=40, prompt_lens=lens, frees=[(12, [0, 2]), (25, [5])], readmit_len=260, pages_every=7)
+
+
+def test_prompt_denominator_and_qwen_thresholds_parity():
+    # Q4's alternative reading (alpha / n) and the Qwen/QwQ thresholds alpha_h = 3, alpha_l = 0 (Q24)
+    scn = H.TINY.replace(R=3, Ly=3, H=8, d=128, M=512, W=32, P=6000, alpha_h=3.0, alpha_l=0.0,
+                         prompt_denominator=1, seed=5, mix=(0.40, 0.60, 0.0))
+    _lifecycle(scn, steps=30, prompt_lens=[200, 333, 90], frees=[(10, [1])], readmit_len=120)
+
+
+def test_tile_size_determinism():
+    # PIN-14: the decoupled look-back order must not leak into results
+    scn = H.TINY.replace(R=6, Ly=4, H=50, d=64, M=256, W=16, P=30000, seed=3)
+    from tests.gpu_backend import GpuBackend
+    snaps = []
+    for tu in (256, 512, 1024):
+        g = GpuBackend(scn.replace(tile_units=tu))
+        inp = H.Inputs(scn)
+        life = H.Lifecycle(scn)
+        H.admit([g], inp, life, list(range(6)), [200, 17, 256, 100, 5, 150])
+        for step in range(20):
+            H.decode_step([g], inp, life, step)
+            if step == 7:
+                H.free([g], life, [2, 3])
+        snaps.append(g.snapshot())
+    from tests.gpu_backend import compare_state
+    compare_state(snaps[0], snaps[1], where="256 vs 512")
+    compare_state(snaps[0], snaps[2], where="256 vs 1024")
