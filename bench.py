@@ -1,0 +1,553 @@
+#!/usr/bin/env python
+"""bench.py — DiffKV on-GPU KV memory manager on B200 (arXiv 2412.03131), BASELINE.json's metric:
+"µs per decode-step compact+alloc (64 req×32L×8H); quant-write GB/s vs HBM peak, 1/2/4/8 GPU".
+
+Workload (BASELINE configs[1]): Llama-3-8B KV shape — 64 requests x 32 layers x 8 KV heads
+per GPU (16,384 units), head_dim 128, 4096-token prompts, max 8192 tokens, W = 64, K8V4 (16-token pages)
+/ K4V2 (32-token pages), 2^22 pages (15 GB) per GPU, alpha_h = 1, alpha_l = 0.02, seeded synthetic
+significance / K / V (synth/).  At N GPUs the global batch is 64*N requests and the 8 KV heads are
+sharded N-way (one independent pool per GPU): per-GPU work is constant ("weak" scaling).
+
+Phases (each bracketed by barrier + synchronize, every kernel timed with CUDA events on its stream):
+  bulk   : K rounds of dkv_quant_write(PREFILL) of the whole batch (the HBM-bound writer) -> GB/s, roofline
+  decode : W warm-up + K decode steps dkv_classify -> dkv_compact_alloc -> dkv_quant_write; between timed
+           steps (untimed) the significance drift (attention stand-in), next-step inputs and a 256 MiB L2
+           flush; every 10th step frees one request first (its compact_alloc recycles ~37k pages) and
+           re-admits it after.  value = mean µs of dkv_compact_alloc per decode step (max over ranks).
+  e2e    : K decode steps through the same C-ABI with pinned HOST inputs (cand_sig, new K/V) copied in and
+           the decisions copied out inside the timed region.
+At N > 1 each step also all-reduces the pool's int64[4] admission counters (MIN) over NCCL on a side
+stream (one-step lag), the only collective of the path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+CONFIGS = {
+    "llama3_8b": dict(R=64, Ly=32, H=8, d=128, prompt=4096, M=8192, W=64, Ch=16, Cl=32, P=1 << 22,
+                      alpha_h=1.0, alpha_l=0.02, mix=(0.35, 0.45, 0.20), seed=2),
+    "tiny": dict(R=4, Ly=2, H=4, d=64, prompt=64, M=128, W=16, Ch=16, Cl=32, P=1024,
+                 alpha_h=1.0, alpha_l=0.02, mix=(0.35, 0.45, 0.20), seed=1),
+}
+METRIC = "µs per decode-step compact+alloc (64 req×32L×8H); quant-write GB/s vs HBM peak, 1/2/4/8 GPU"
+
+
+# ----------------------------------------------------------------------------------------- distributed
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/dkv_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.path)
+        load = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------------------------------- workload
+class Workload:
+    """Synthetic inputs of one GPU's shard, generated on the device from counters (synth/)."""
+
+    def __init__(self, c, rank, world, device):
+        self.c = c
+        self.world = world
+        assert c["H"] % world == 0
+        self.Hl = c["H"] // world
+        self.R = c["R"] * world                      # weak scaling: global batch grows with N
+        self.shape = synth.Shape(self.R, c["Ly"], self.Hl, H_total=c["H"], h0=rank * self.Hl)
+        self.LyH = c["Ly"] * self.Hl
+        self.U = self.R * self.LyH
+        self.device = device
+        ug = self.shape.global_units(list(range(self.R)), device="cpu")
+        mh, ml = synth.unit_mix(c["seed"], ug, c["mix"], Ly=c["Ly"], Ht=c["H"])
+        self.ug = ug.to(device)
+        self.mix_h, self.mix_l = mh.to(device), ml.to(device)
+
+    def prefill_inputs(self, T):
+        c, dev = self.c, self.device
+        sig = torch.empty((self.R, self.LyH, T), dtype=torch.float32, device=dev)
+        k = torch.empty((self.R, self.LyH, T, c["d"]), dtype=torch.float16, device=dev)
+        v = torch.empty_like(k)
+        step = max(1, (64 if dev.type == "cuda" else 4) // max(1, T // 512))
+        for r in range(self.R):
+            sig[r] = synth.prefill_sig(c["seed"], self.ug[r], T, c["alpha_h"], c["alpha_l"], self.mix_h[r],
+                                       self.mix_l[r])
+            for j0 in range(0, self.LyH, step):
+                g = self.ug[r, j0:j0 + step]
+                k[r, j0:j0 + step] = synth.kv_values(c["seed"], synth.S_KEY, g, 0, T, c["d"])
+                v[r, j0:j0 + step] = synth.kv_values(c["seed"], synth.S_VAL, g, 0, T, c["d"])
+        return sig, k, v
+
+    def decode_inputs(self, seq_len_host, active_host):
+        c = self.c
+        N = torch.as_tensor(np.where(active_host, seq_len_host + 1, 0), dtype=torch.int64, device=self.device)
+        N = N.view(-1, 1).expand(-1, self.LyH).reshape(-1)
+        ug = self.ug.reshape(-1)
+        cand = synth.decode_sig(c["seed"], ug, N, c["W"], c["alpha_h"], c["alpha_l"], self.mix_h.reshape(-1),
+                                self.mix_l.reshape(-1))
+        k, v = synth.new_token_kv(c["seed"], ug, (N - 1).clamp(min=0), c["d"])
+        return cand.contiguous(), k.contiguous(), v.contiguous()
+
+
+def bulk_bytes(pool, geom, W, d, T, units):
+    """Algorithmic bytes of one dkv_quant_write(PREFILL) of `units` prompts of T tokens."""
+    v = pool.views()
+    nh = int(v["n_h"].sum().item())
+    nl = int(v["n_l"].sum().item())
+    kept = units * max(T - W, 0)
+    npr = kept - nh - nl
+    nw = units * min(W, T)
+    rd = 2 * d * 2 + 4
+    hb = rd + geom[1]["k_row"] + geom[1]["v_row"] + 16
+    lb = rd + geom[2]["k_row"] + geom[2]["v_row"] + 16
+    return nh * hb + nl * lb + npr * 4 + nw * 4 * d, dict(high=nh, low=nl, pruned=npr, window=nw)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+# ----------------------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local):
+    from paper_2412_03131_b200 import Pool
+    from paper_2412_03131_b200 import dkv as D
+
+    c = CONFIGS[args.config]
+    dev = torch.device("cuda", local)
+    wl = Workload(c, rank, world, dev)
+    cfg = D.make_config(wl.R, c["Ly"], wl.Hl, c["d"], c["M"], c["W"], c["Ch"], c["Cl"], P=c["P"],
+                        alpha_h=c["alpha_h"], alpha_l=c["alpha_l"])
+    pool = Pool(cfg, device=dev)
+    geom = pool.geom()
+    T = c["prompt"]
+    sig, kk, vv = wl.prefill_inputs(T)
+    k16, v16 = kk.view(torch.int16), vv.view(torch.int16)
+    reqs = list(range(wl.R))
+    lens = [T] * wl.R
+    dec = pool.new_decisions()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    launches = 0
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
+
+    def empty_step():
+        """decode step used only to recycle PENDING_FREE requests (no ACTIVE request, untimed)"""
+        z = torch.zeros(wl.U, dtype=torch.float32, device=dev)
+        zk = torch.zeros((wl.U, c["d"]), dtype=torch.int16, device=dev)
+        pool.classify_decode(z, dec)
+        pool.compact_alloc(dec)
+        pool.quant_write_decode(dec, zk, zk, z)
+
+    # ---------------- bulk phase: K rounds of prefill quant-write of the whole batch
+    sampler = ClockSampler(local)
+    bulk_ms = []
+    nrounds = args.warmup + args.steps
+    sampler.start()
+    t_wall0 = time.time()
+    for i in range(nrounds):
+        if i > 0:
+            pool.free(reqs)
+            empty_step()
+        pool.classify_prefill(reqs, lens, sig)
+        pool.compact_alloc(None)
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = ev(), ev()
+        e0.record()
+        pool.quant_write_prefill(k16, v16, sig)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            bulk_ms.append(e0.elapsed_time(e1))
+            launches += 2                                  # quant_prefill_kernel + finish_prefill_kernel
+    st, stats = pool.query()
+    assert st == 0, f"device status {st} after prefill"
+    bbytes, bmix = bulk_bytes(pool, geom, c["W"], c["d"], T, wl.U)
+    bulk_mean = statistics.mean(bulk_ms)
+    bulk_max = max_over_ranks(bulk_mean, world)
+
+    # ---------------- decode phase
+    seq = np.full(wl.R, T, np.int64)
+    active = np.ones(wl.R, bool)
+    side = torch.cuda.Stream(device=dev) if world > 1 else None
+    stats_view = pool.views()["stats"]
+    red = torch.empty(4, dtype=torch.int64, device=dev)
+    comp_us, cls_us, qw_us, step_us, cls_bytes = [], [], [], [], []
+    freed_steps = 0
+    total_steps = args.warmup + args.steps
+    for s in range(total_steps):
+        timed = s >= args.warmup
+        # untimed: attention stand-in (significance drift), inputs, churn, L2 flush
+        v = pool.views()
+        synth.apply_drift(c["seed"], s, wl.shape, v["pages"], v["table"], v["n_h"], v["n_l"],
+                          {k_: (geom[k_]["C"], geom[k_]["off_score"], geom[k_]["off_pos"]) for k_ in (1, 2)}, pool.L)
+        churn = timed and (s - args.warmup) % 10 == 5
+        if churn:
+            r = (s * 7) % wl.R
+            pool.free([r])
+            active[r] = False
+            freed_steps += 1
+        cand, nk, nv = wl.decode_inputs(seq, active)
+        nh0, nl0 = v["n_h"].clone(), v["n_l"].clone()
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier(world)
+        e = [ev() for _ in range(4)]
+        e[0].record()
+        pool.classify_decode(cand, dec)
+        e[1].record()
+        pool.compact_alloc(dec)
+        e[2].record()
+        if side is not None:                                # count all-reduce, overlapped (one-step lag)
+            import torch.distributed as dist
+            side.wait_event(e[2])
+            with torch.cuda.stream(side):
+                red.copy_(stats_view)
+                dist.all_reduce(red, op=dist.ReduceOp.MIN)
+        pool.quant_write_decode(dec, nk.view(torch.int16), nv.view(torch.int16), cand)
+        e[3].record()
+        torch.cuda.synchronize()
+        seq[active] += 1
+        if churn:                                           # re-admit (untimed prefill of 4096 tokens)
+            pool.classify_prefill([r], [T], sig[r:r + 1])
+            pool.compact_alloc(None)
+            pool.quant_write_prefill(k16[r:r + 1], v16[r:r + 1], sig[r:r + 1])
+            seq[r] = T
+            active[r] = True
+        if timed:
+            cls_us.append(e[0].elapsed_time(e[1]) * 1e3)
+            comp_us.append(e[1].elapsed_time(e[2]) * 1e3)
+            qw_us.append(e[2].elapsed_time(e[3]) * 1e3)
+            step_us.append(e[0].elapsed_time(e[3]) * 1e3)
+            launches += 3                                   # classify, compact_alloc, quant_decode kernels
+            tc = dec.view(torch.uint8).view(-1, 16)[:, 0].cpu().numpy()
+            sec = np.where(tc == 1, nh0.cpu().numpy(), np.where(tc == 2, nl0.cpu().numpy(), 0)).astype(np.int64)
+            C = np.where(tc == 1, geom[1]["C"], geom[2]["C"])
+            cls_bytes.append(int((4 * sec + 4 * ((sec + C - 1) // C)).sum() + 28 * wl.U))
+    st, stats = pool.query()
+    assert st == 0, f"device status {st} after decode"
+    wall = time.time() - t_wall0
+    clocks = sampler.stop()
+
+    # ---------------- e2e: same decode step through the C ABI with host buffers
+    e2e_us = []
+    pin_c = torch.empty((args.steps, wl.U), dtype=torch.float32).pin_memory()
+    pin_k = torch.empty((args.steps, wl.U, c["d"]), dtype=torch.int16).pin_memory()
+    pin_v = torch.empty_like(pin_k).pin_memory()
+    pin_dec = torch.empty((wl.U, 4), dtype=torch.int32).pin_memory()
+    for i in range(args.steps):
+        cand, nk, nv = wl.decode_inputs(seq + i, active)
+        pin_c[i].copy_(cand)
+        pin_k[i].copy_(nk.view(torch.int16))
+        pin_v[i].copy_(nv.view(torch.int16))
+    d_c = torch.empty(wl.U, dtype=torch.float32, device=dev)
+    d_k = torch.empty((wl.U, c["d"]), dtype=torch.int16, device=dev)
+    d_v = torch.empty_like(d_k)
+    for i in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = ev(), ev()
+        e0.record()
+        d_c.copy_(pin_c[i], non_blocking=True)
+        d_k.copy_(pin_k[i], non_blocking=True)
+        d_v.copy_(pin_v[i], non_blocking=True)
+        pool.classify_decode(d_c, dec)
+        pool.compact_alloc(dec)
+        pool.quant_write_decode(dec, d_k, d_v, d_c)
+        pin_dec.copy_(dec, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_us.append(e0.elapsed_time(e1) * 1e3)
+    st, stats = pool.query()
+    assert st == 0, f"device status {st} after e2e"
+
+    # ---------------- aggregate (max over ranks)
+    comp_mean = max_over_ranks(statistics.mean(comp_us), world)
+    step_mean = max_over_ranks(statistics.mean(step_us), world)
+    cls_mean = max_over_ranks(statistics.mean(cls_us), world)
+    qw_mean = max_over_ranks(statistics.mean(qw_us), world)
+    e2e_mean = max_over_ranks(statistics.mean(e2e_us), world)
+    bulk_gbs_rank = bbytes / (bulk_mean * 1e-3) / 1e9
+    agg_bulk_gbs = sum_over_ranks(bbytes, world) / (bulk_max * 1e-3) / 1e9
+    peak, peak_src = load_peaks()
+    traffic = load_traffic()
+    cls_gbs = statistics.mean(cls_bytes) / (statistics.mean(cls_us) * 1e-6) / 1e9
+    out = {
+        "metric": METRIC,
+        "value": round(comp_mean, 3),
+        "unit": "us",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(step_mean / 1e3, 6),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp16 in / u8 codes (fp32 quantizer arithmetic, int32 scans)",
+        "data": "synthetic (seeded counter-based significance / K / V, synth/)",
+        "config": {
+            "workload": f"{args.config}: Llama-3-8B KV shape, {c['R']}x{world} req x {c['Ly']} layers x {c['H']} KV heads "
+                        f"(sharded {world}-way), d {c['d']}, prompt {T}, M {c['M']}, W {c['W']}, K8V4/16-token + "
+                        f"K4V2/32-token pages, {c['P']} pages per GPU, alpha {c['alpha_h']}/{c['alpha_l']}",
+            "units_per_gpu": wl.U,
+            "global_batch": wl.R,
+            "parallelism": f"kv-head shard x{world} (independent pools)",
+            "l2": "flushed between timed steps (256 MiB write); bulk inputs 32 GiB >> L2",
+        },
+        "decode_step_us": {"classify": round(cls_mean, 3), "compact_alloc": round(comp_mean, 3),
+                           "quant_write": round(qw_mean, 3), "step": round(step_mean, 3),
+                           "compact_alloc_p50": round(float(np.percentile(comp_us, 50)), 3),
+                           "compact_alloc_p99": round(float(np.percentile(comp_us, 99)), 3),
+                           "recycle_steps": freed_steps},
+        "quant_write": {"gbs": round(agg_bulk_gbs, 1), "gbs_per_gpu": round(bulk_gbs_rank, 1),
+                        "ms": round(bulk_max, 3), "algorithmic_bytes_per_gpu": bbytes, "token_mix": bmix,
+                        "frac_of_hbm_peak": round(bulk_gbs_rank / peak, 4)},
+        "roofline": {"kernel": "quant_prefill_kernel (dkv_quant_write PREFILL, bulk writer)", "bound": "hbm",
+                     "achieved": round(bulk_gbs_rank, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": round(bulk_gbs_rank / peak, 4),
+                     "traffic": traffic.get("quant_prefill_kernel")},
+        "roofline_decode": {"kernel": "classify_decode_kernel", "bound": "hbm", "achieved": round(cls_gbs, 1),
+                            "peak": peak, "unit": "GB/s", "frac": round(cls_gbs / peak, 4),
+                            "algorithmic_bytes": int(statistics.mean(cls_bytes)),
+                            "traffic": traffic.get("classify_decode_kernel")},
+        "e2e": {"value": round(e2e_mean, 3), "unit": "us per decode step (H2D inputs + classify + compact_alloc + "
+                                                     "quant_write + D2H decisions)",
+                "h2d_bytes_per_step": wl.U * (4 + 2 * 2 * c["d"]), "d2h_bytes_per_step": wl.U * 16},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "wall_s": round(wall, 1),
+    }
+    return out
+
+
+# ----------------------------------------------------------------------------------------- oracle arm
+def run_oracle_sample(args, sample_requests=1, steps=None):
+    """The serial C oracle (oracle/, as it stands) on a bounded sample of the same workload: the first
+    `sample_requests` requests (all their layers and heads), prefill + decode steps; times scaled to the
+    full per-GPU batch by the unit ratio."""
+    import oracle  # test infrastructure: bench's cpu_baseline / --impl reference legs only
+
+    c = CONFIGS[args.config]
+    Rs = sample_requests
+    T = c["prompt"]
+    need = Rs * c["Ly"] * c["H"] * ((T // c["Ch"]) + 4)
+    cfg = oracle.make_config(R=Rs, Ly=c["Ly"], H=c["H"], d=c["d"], M=c["M"], W=c["W"], Ch=c["Ch"], Cl=c["Cl"],
+                             P=int(need * 1.1), alpha_h=c["alpha_h"], alpha_l=c["alpha_l"])
+    pool = oracle.OraclePool(cfg)
+    wl = Workload(dict(c, R=Rs), 0, 1, torch.device("cpu"))
+    sig, kk, vv = wl.prefill_inputs(T)
+    sig_np = sig.numpy()
+    k_np, v_np = kk.view(torch.int16).numpy().view(np.uint16), vv.view(torch.int16).numpy().view(np.uint16)
+    t0 = time.perf_counter()
+    pool.classify_prefill(list(range(Rs)), [T] * Rs, sig_np, want_classes=False)
+    pool.compact_alloc(None)
+    t1 = time.perf_counter()
+    pool.quant_write_prefill(k_np, v_np, sig_np)
+    t2 = time.perf_counter()
+    units = Rs * c["Ly"] * c["H"]
+    # algorithmic bytes of the sample's bulk write (same accounting as the GPU)
+    nh, nl = int(pool.n_h.sum()), int(pool.n_l.sum())
+    kept = units * (T - c["W"])
+    g = pool.geom
+    rd = 2 * c["d"] * 2 + 4
+    bb = nh * (rd + g[1].k_row + g[1].v_row + 16) + nl * (rd + g[2].k_row + g[2].v_row + 16) + \
+        (kept - nh - nl) * 4 + units * c["W"] * 4 * c["d"]
+    seq = np.full(Rs, T, np.int64)
+    act = np.ones(Rs, bool)
+    comp, cls, qw = [], [], []
+    steps = steps or max(3, min(args.steps, 20))
+    for s in range(steps):
+        cand, nk, nv = wl.decode_inputs(seq, act)
+        cand_np = cand.numpy()
+        nk_np, nv_np = nk.view(torch.int16).numpy().view(np.uint16), nv.view(torch.int16).numpy().view(np.uint16)
+        a = time.perf_counter()
+        st, dec = pool.classify_decode(cand_np)
+        b = time.perf_counter()
+        pool.compact_alloc(dec)
+        cc = time.perf_counter()
+        pool.quant_write_decode(dec, nk_np, nv_np, cand_np)
+        dd = time.perf_counter()
+        cls.append(b - a); comp.append(cc - b); qw.append(dd - cc)
+        seq += 1
+    scale = (c["R"] * c["Ly"] * c["H"]) / units
+    return {
+        "compact_us": statistics.mean(comp) * 1e6 * scale,
+        "classify_us": statistics.mean(cls) * 1e6 * scale,
+        "quant_us": statistics.mean(qw) * 1e6 * scale,
+        "bulk_gbs": bb / (t2 - t1) / 1e9,
+        "prefill_classify_s": t1 - t0,
+        "sample": f"{Rs} of {c['R']} requests ({units} of {c['R'] * c['Ly'] * c['H']} units), prompt {T}, "
+                  f"{steps} decode steps; µs scaled by the unit ratio x{scale:g}",
+        "cores": 1,
+    }
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    t0 = time.time()
+    o = run_oracle_sample(args)
+    c = CONFIGS[args.config]
+    return {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(o["compact_us"], 3),
+        "unit": "us",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round((o["compact_us"] + o["classify_us"] + o["quant_us"]) / 1e3, 6),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp16 in / u8 codes (fp32 quantizer arithmetic)",
+        "data": "synthetic (seeded counter-based, synth/)",
+        "config": {"workload": f"{args.config} (oracle sample)", "global_batch": c["R"]},
+        "cpu_baseline": {"value": round(o["compact_us"], 3), "unit": "us", "cores": o["cores"], "kind": "oracle",
+                         "sample": o["sample"], "quant_write_gbs": round(o["bulk_gbs"], 3),
+                         "classify_us": round(o["classify_us"], 1), "quant_write_decode_us": round(o["quant_us"], 1)},
+        "e2e": {"value": round(o["compact_us"], 3), "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": round(time.time() - t0, 1),
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="llama3_8b", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 1
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    rank, world, local = dist_init()
+    out = run_ours(args, rank, world, local)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            o = run_oracle_sample(args)
+            out["cpu_baseline"] = {"value": round(o["compact_us"], 3), "unit": "us", "cores": o["cores"],
+                                   "kind": "oracle", "sample": o["sample"],
+                                   "quant_write_gbs": round(o["bulk_gbs"], 3),
+                                   "classify_us": round(o["classify_us"], 1),
+                                   "quant_write_decode_us": round(o["quant_us"], 1)}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -76,7 +76,7 @@ def test_prompt_denominator_and_qwen_thresholds_parity():
 
 def test_tile_size_determinism():
     # PIN-14: the decoupled look-back order must not leak into results
-    scn = H.TINY.replace(R=6, Ly=4, H=50, d=64, M=256, W=16, P=30000, seed=3)
+    scn = H.TINY.replace(R=6, Ly=4, H=50, d=64, M=300, W=16, P=30000, seed=3)
     from tests.gpu_backend import GpuBackend
     snaps = []
     for tu in (256, 512, 1024):
