@@ -155,6 +155,115 @@ __device__ __forceinline__ uint64_t quantize8(const float x[8], int bits, uint32
   return packed;
 }
 
+// ------------------------------------------------------------------------------------- fast fp16 quantizer
+// Same arithmetic as quantize8 (and the oracle) for FP16 inputs, with far fewer instructions:
+//  * min / max on packed half2 with NaN propagation (min.NaN / max.NaN), reduced across the group as one
+//    half2 {min, -max}; a NaN or Inf input makes min or max non-finite -> ok = false;
+//  * the sign of a zero minimum is fixed up exactly (total order -0 < +0, Q16) in a rare warp-uniform path;
+//  * x - z with one mixed-precision add (add.rn.f32.f16: fp16 operand, fp32 result, one RN rounding —
+//    identical to fsub_rn(float(x), z) since float(x) is exact);
+//  * t >= 0 always (z = min exactly), so round-half-away(t) = floor(t + 1/2), computed exactly as
+//    RD(RD(t + 1/2) + 2^23): the code lands in the low mantissa bits, no float->int conversion;
+//  * t <= Q + 1/8 when s16 is a normal binary16 number, so the clamp is only applied when s16 is subnormal.
+__device__ __forceinline__ float mixed_add_h(uint32_t h16, float c) {
+  float r;
+  asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(r) : "h"((unsigned short)h16), "f"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t pack4_lo_bytes(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+
+// Each lane of a G-lane group holds NW half2 words (elements [2*NW*gl, 2*NW*(gl+1)) of the vector).
+// Writes NW*2*BITS/32 packed code words (lowest element in the LSBs, Q17) and meta = s16 | z16 << 16.
+template <int G, int NW, int BITS>
+__device__ __forceinline__ void quant_h16(const uint32_t (&x)[NW], uint32_t (&cw)[(NW * 2 * BITS) / 32],
+                                          uint32_t& meta, bool& ok) {
+  constexpr int NCW = (NW * 2 * BITS) / 32;
+  constexpr float Qf = (float)((1 << BITS) - 1);
+  __half2 lo = *reinterpret_cast<const __half2*>(&x[0]), hi = lo;
+#pragma unroll
+  for (int i = 1; i < NW; i++) {
+    const __half2 v = *reinterpret_cast<const __half2*>(&x[i]);
+    lo = __hmin2_nan(lo, v);
+    hi = __hmax2_nan(hi, v);
+  }
+  __half2 key = __halves2half2(__hmin_nan(__low2half(lo), __high2half(lo)),
+                               __hneg(__hmax_nan(__low2half(hi), __high2half(hi))));
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    uint32_t k = *reinterpret_cast<uint32_t*>(&key);
+    k = __shfl_xor_sync(kFull, k, o);
+    key = __hmin2_nan(key, *reinterpret_cast<__half2*>(&k));
+  }
+  unsigned short mnb = __half_as_ushort(__low2half(key));
+  const unsigned short mxb = __half_as_ushort(__hneg(__high2half(key)));
+  const bool zmin = (mnb & 0x7FFFu) == 0;
+  if (__any_sync(kFull, zmin)) {                        // rare: which zero is the minimum?
+    bool negz = false;
+#pragma unroll
+    for (int i = 0; i < NW; i++) negz |= ((x[i] & 0xFFFFu) == 0x8000u) | ((x[i] >> 16) == 0x8000u);
+    const unsigned b = __ballot_sync(kFull, negz);
+    const int lane = threadIdx.x & 31;
+    const unsigned gmask = ((G == 32) ? kFull : ((1u << G) - 1u)) << (lane & ~(G - 1) & 31);
+    if (zmin) mnb = (b & gmask) ? 0x8000u : 0x0000u;
+  }
+  ok = ((mnb & 0x7C00u) != 0x7C00u) && ((mxb & 0x7C00u) != 0x7C00u);
+  const float mn = __half2float(__ushort_as_half(mnb)), mx = __half2float(__ushort_as_half(mxb));
+  const float s32 = __fdiv_rn(__fsub_rn(mx, mn), Qf);
+  const __half s16 = __float2half_rn(s32);
+  meta = (uint32_t)__half_as_ushort(s16) | ((uint32_t)mnb << 16);
+  const float sf = __half2float(s16);
+  if (sf == 0.0f) {
+#pragma unroll
+    for (int w = 0; w < NCW; w++) cw[w] = 0u;
+    return;
+  }
+  const float inv = __fdiv_rn(1.0f, sf);
+  const float nz = -mn;                                  // z = min exactly (FP16 input)
+  const float cap = (sf >= 6.103515625e-05f) ? 3.0e38f : Qf;   // clamp only for subnormal s16
+  uint32_t ub[NW * 2];
+#pragma unroll
+  for (int i = 0; i < NW; i++) {
+#pragma unroll
+    for (int hh = 0; hh < 2; hh++) {
+      const float d = mixed_add_h(hh ? (x[i] >> 16) : (x[i] & 0xFFFFu), nz);
+      float t = __fmul_rn(d, inv);
+      t = fminf(t, cap);
+      const float a = __fadd_rd(t, 0.5f);
+      ub[2 * i + hh] = __float_as_uint(__fadd_rd(a, 8388608.0f));
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < NCW; w++) {
+    if constexpr (BITS == 8) {
+      cw[w] = pack4_lo_bytes(ub[4 * w], ub[4 * w + 1], ub[4 * w + 2], ub[4 * w + 3]);
+    } else if constexpr (BITS == 4) {
+      const uint32_t ev = pack4_lo_bytes(ub[8 * w], ub[8 * w + 2], ub[8 * w + 4], ub[8 * w + 6]);
+      const uint32_t od = pack4_lo_bytes(ub[8 * w + 1], ub[8 * w + 3], ub[8 * w + 5], ub[8 * w + 7]);
+      cw[w] = ev | (od << 4);
+    } else {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int m = 0; m < 4; m++)
+        acc |= pack4_lo_bytes(ub[16 * w + m], ub[16 * w + m + 4], ub[16 * w + m + 8], ub[16 * w + m + 12]) << (2 * m);
+      cw[w] = acc;
+    }
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void store_words(uint8_t* dst, const uint32_t (&w)[N]) {
+  if constexpr (N % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) reinterpret_cast<uint4*>(dst)[i / 4] = make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]);
+  } else if constexpr (N == 2) {
+    *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+  } else {
+    *reinterpret_cast<uint32_t*>(dst) = w[0];
+  }
+}
+
 // Dequantize this lane's 8 codes (X^ = s*Q + z).
 __device__ __forceinline__ void dequant8(uint64_t packed, int bits, uint32_t meta, float x[8]) {
   const float sf = __half2float(__ushort_as_half((unsigned short)(meta & 0xFFFFu)));

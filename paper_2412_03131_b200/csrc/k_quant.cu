@@ -116,7 +116,10 @@ cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, con
 }
 
 // ------------------------------------------------------------------------------------------- bulk
-constexpr int kBulkUnroll = 4;
+// One warp per (admitted unit, 256-token segment).  Groups of 4 lanes own one token: lane quarter q of
+// the group holds elements [q*d/4, (q+1)*d/4) of the K row and of the V row (d/4 halves = d/8 bytes*4).
+constexpr int kBulkWarps = 4;
+constexpr int kBulkG = 4;
 
 __device__ __forceinline__ int prompt_class_q(const PoolDev& p, float s, int t, int T) {
   const float den = (p.prompt_den == 0) ? (float)(t + 1) : (float)T;
@@ -124,17 +127,39 @@ __device__ __forceinline__ int prompt_class_q(const PoolDev& p, float s, int t, 
   return s >= th ? DKV_CLS_HIGH : (s >= tl ? DKV_CLS_LOW : DKV_CLS_PRUNED);
 }
 
-template <int G>
-__global__ void __launch_bounds__(kQWarps * 32)
+template <int NW>
+__device__ __forceinline__ void quant_store_vec(const uint32_t (&x)[NW], int bits, uint8_t* dst, uint32_t& meta,
+                                                bool& ok) {
+  // dst = this lane's part of the token's code row
+  if (bits == 8) {
+    uint32_t cw[NW / 2];
+    quant_h16<kBulkG, NW, 8>(x, cw, meta, ok);
+    store_words(dst, cw);
+  } else if (bits == 4) {
+    uint32_t cw[NW / 4];
+    quant_h16<kBulkG, NW, 4>(x, cw, meta, ok);
+    store_words(dst, cw);
+  } else {
+    uint32_t cw[(NW / 8) > 0 ? NW / 8 : 1];
+    if constexpr (NW >= 8) {
+      quant_h16<kBulkG, NW, 2>(x, cw, meta, ok);
+      store_words(dst, cw);
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBulkWarps * 32)
 quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const uint16_t* __restrict__ vin,
                      int64_t kv_stride, const float* __restrict__ sig, int64_t sig_stride, int nseg_max) {
-  constexpr int TPS = 32 / G;                        // tokens per warp step
-  __shared__ uint32_t s_ent[kQWarps][kSegTokens];    // (t - t0) | cls << 9 | slot << 11
-  __shared__ uint32_t s_sig[kQWarps][kSegTokens];
+  constexpr int NW = D / 8;                            // half2 words per lane per vector (d/4 halves)
+  constexpr int TPS = 32 / kBulkG;                     // tokens per warp step
+  __shared__ uint32_t s_ent[kBulkWarps][kSegTokens];   // high list from the front, low list from the back
+  __shared__ uint32_t s_sig[kBulkWarps][kSegTokens];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long item = (long)blockIdx.x * kQWarps + warp;
+  const long item = (long)blockIdx.x * kBulkWarps + warp;
   const int seg = (int)(item % nseg_max);
-  const long wi = item / nseg_max;                   // admitted unit index (i * LyH + j)
+  const long wi = item / nseg_max;                     // admitted unit index (i * LyH + j)
   if (wi >= (long)n * p.LyH) return;
   if (ld_volatile(&p.ctrl->status) != 0) return;
   const int i = (int)(wi / p.LyH), j = (int)(wi % p.LyH);
@@ -146,15 +171,14 @@ quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const u
   const int t1 = min(t0 + kSegTokens, T);
   const int kept = max(T - p.W, 0);
   const int ke = min(t1, kept);
-  const int d = p.d;
   const float* srow = sig + wi * sig_stride;
-  const uint16_t* kbase = kin + wi * kv_stride * d;
-  const uint16_t* vbase = vin + wi * kv_stride * d;
+  const uint16_t* kbase = kin + wi * kv_stride * D;
+  const uint16_t* vbase = vin + wi * kv_stride * D;
 
-  // phase A: classes + ranks (ballot/popc) -> kept-token list
+  // phase A: classes + per-class ranks (warp ballot/popc + running offsets) -> two kept lists
   int hr = p.pf_seg[((size_t)u * p.nseg + seg) * 2];
   int lr = p.pf_seg[((size_t)u * p.nseg + seg) * 2 + 1];
-  int cnt = 0;
+  int nh = 0, nl = 0;
   const unsigned lt = (1u << lane) - 1u;
   for (int c = t0; c < ke; c += 32) {
     const int t = c + lane;
@@ -166,71 +190,96 @@ quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const u
     }
     const unsigned hm = __ballot_sync(kFull, cl == DKV_CLS_HIGH);
     const unsigned lm = __ballot_sync(kFull, cl == DKV_CLS_LOW);
-    const unsigned km = hm | lm;
-    if (cl == DKV_CLS_HIGH || cl == DKV_CLS_LOW) {
-      const int slot = cl == DKV_CLS_HIGH ? hr + __popc(hm & lt) : lr + __popc(lm & lt);
-      const int e = cnt + __popc(km & lt);
-      s_ent[warp][e] = (uint32_t)(t - t0) | ((uint32_t)cl << 9) | ((uint32_t)slot << 11);
+    if (cl == DKV_CLS_HIGH) {
+      const int e = nh + __popc(hm & lt);
+      s_ent[warp][e] = (uint32_t)(t - t0) | ((uint32_t)(hr + __popc(hm & lt)) << 8);
+      s_sig[warp][e] = __float_as_uint(s);
+    } else if (cl == DKV_CLS_LOW) {
+      const int e = kSegTokens - 1 - (nl + __popc(lm & lt));
+      s_ent[warp][e] = (uint32_t)(t - t0) | ((uint32_t)(lr + __popc(lm & lt)) << 8);
       s_sig[warp][e] = __float_as_uint(s);
     }
-    hr += __popc(hm);
-    lr += __popc(lm);
-    cnt += __popc(km);
+    hr += __popc(hm); nh += __popc(hm);
+    lr += __popc(lm); nl += __popc(lm);
   }
   __syncwarp();
 
-  // phase B: stream kept rows, quantize, store
-  const int grp = lane / G, gl = lane % G;
+  // phase B: per class (warp-uniform bit widths), 8 tokens per step, only kept rows are read
+  const int grp = lane / kBulkG, q = lane % kBulkG;
   bool bad = false;
-  for (int e0 = 0; e0 < cnt; e0 += TPS * kBulkUnroll) {
-    uint4 xk[kBulkUnroll], xv[kBulkUnroll];
-    uint32_t ent[kBulkUnroll];
+#pragma unroll 1
+  for (int cls = DKV_CLS_HIGH; cls <= DKV_CLS_LOW; cls++) {
+    const ClassGeom g = geom_of(p, cls);
+    const int cnt = cls == DKV_CLS_HIGH ? nh : nl;
+    const int kbytes = (D / 4) * g.kbits / 8, vbytes = (D / 4) * g.vbits / 8;
+#pragma unroll 1
+    for (int e0 = 0; e0 < cnt; e0 += TPS) {
+      const int e = e0 + grp;
+      const bool valid = e < cnt;
+      const int ix = cls == DKV_CLS_HIGH ? e : kSegTokens - 1 - e;
+      const uint32_t ent = valid ? s_ent[warp][ix] : 0u;
+      const int t = t0 + (int)(ent & 255u);
+      const int slot = (int)(ent >> 8);
+      uint32_t xk[NW], xv[NW];
+      if (valid) {
+        const uint4* ks = reinterpret_cast<const uint4*>(kbase + (size_t)t * D + q * (D / 4));
+        const uint4* vs = reinterpret_cast<const uint4*>(vbase + (size_t)t * D + q * (D / 4));
 #pragma unroll
-    for (int q = 0; q < kBulkUnroll; q++) {
-      const int e = e0 + q * TPS + grp;
-      ent[q] = e < cnt ? s_ent[warp][e] : 0xFFFFFFFFu;
-      xk[q] = make_uint4(0, 0, 0, 0);
-      xv[q] = make_uint4(0, 0, 0, 0);
-      if (e < cnt) {
-        const size_t t = (size_t)(t0 + (ent[q] & 511u));
-        xk[q] = ld_stream_v4(kbase + t * d + gl * 8);
-        xv[q] = ld_stream_v4(vbase + t * d + gl * 8);
+        for (int w = 0; w < NW / 4; w++) {
+          const uint4 a = ld_stream_v4(ks + w);
+          xk[4 * w] = a.x; xk[4 * w + 1] = a.y; xk[4 * w + 2] = a.z; xk[4 * w + 3] = a.w;
+        }
+#pragma unroll
+        for (int w = 0; w < NW / 4; w++) {
+          const uint4 a = ld_stream_v4(vs + w);
+          xv[4 * w] = a.x; xv[4 * w + 1] = a.y; xv[4 * w + 2] = a.z; xv[4 * w + 3] = a.w;
+        }
+      } else {
+#pragma unroll
+        for (int w = 0; w < NW; w++) { xk[w] = 0u; xv[w] = 0u; }
       }
-    }
-#pragma unroll
-    for (int q = 0; q < kBulkUnroll; q++) {
-      if (e0 + q * TPS >= cnt) break;                // warp-uniform
-      const bool valid = ent[q] != 0xFFFFFFFFu;
-      const int cl = valid ? (int)((ent[q] >> 9) & 3u) : DKV_CLS_HIGH;
-      const int slot = (int)(ent[q] >> 11);
-      const ClassGeom g = geom_of(p, cl);
-      float x[8];
+      int idx;
+      uint8_t* pg = valid ? slot_page(p, cls, u, slot, idx) : nullptr;
+      if (!valid) idx = 0;
       uint32_t mk, mv;
       bool fk, fv;
-      unpack_h8(xk[q], x);
-      const uint64_t qk = quantize8<G>(x, g.kbits, mk, fk);
-      unpack_h8(xv[q], x);
-      const uint64_t qv = quantize8<G>(x, g.vbits, mv, fv);
+      uint8_t* kd = pg + g.off_k + idx * g.k_row + q * kbytes;
+      uint8_t* vd = pg + g.off_v + idx * g.v_row + q * vbytes;
+      // quantize (all lanes; invalid groups compute on zeros and store nothing)
+      uint32_t ck[NW / 2], cv[NW / 2];
+      if (g.kbits == 8) quant_h16<kBulkG, NW, 8>(xk, *reinterpret_cast<uint32_t(*)[NW / 2]>(ck), mk, fk);
+      else if (g.kbits == 4) quant_h16<kBulkG, NW, 4>(xk, *reinterpret_cast<uint32_t(*)[NW / 4]>(ck), mk, fk);
+      else quant_h16<kBulkG, NW, 2>(xk, *reinterpret_cast<uint32_t(*)[NW / 8]>(ck), mk, fk);
+      if (g.vbits == 8) quant_h16<kBulkG, NW, 8>(xv, *reinterpret_cast<uint32_t(*)[NW / 2]>(cv), mv, fv);
+      else if (g.vbits == 4) quant_h16<kBulkG, NW, 4>(xv, *reinterpret_cast<uint32_t(*)[NW / 4]>(cv), mv, fv);
+      else quant_h16<kBulkG, NW, 2>(xv, *reinterpret_cast<uint32_t(*)[NW / 8]>(cv), mv, fv);
       if (valid) {
         bad |= !(fk && fv);
-        int idx;
-        uint8_t* pg = slot_page(p, cl, u, slot, idx);
-        store_codes(pg + g.off_k + idx * g.k_row + gl * g.kbits, qk, g.kbits);
-        store_codes(pg + g.off_v + idx * g.v_row + gl * g.vbits, qv, g.vbits);
-        if (gl == 0) *reinterpret_cast<uint32_t*>(pg + g.off_kmeta + 4 * idx) = mk;
-        if (gl == 1) *reinterpret_cast<uint32_t*>(pg + g.off_vmeta + 4 * idx) = mv;
-        if (gl == 2) *reinterpret_cast<uint32_t*>(pg + g.off_score + 4 * idx) = s_sig[warp][e0 + q * TPS + grp];
-        if (gl == 3) *reinterpret_cast<int32_t*>(pg + g.off_pos + 4 * idx) = t0 + (int)(ent[q] & 511u);
+        if (g.kbits == 8) store_words(kd, *reinterpret_cast<uint32_t(*)[NW / 2]>(ck));
+        else if (g.kbits == 4) store_words(kd, *reinterpret_cast<uint32_t(*)[NW / 4]>(ck));
+        else store_words(kd, *reinterpret_cast<uint32_t(*)[NW / 8]>(ck));
+        if (g.vbits == 8) store_words(vd, *reinterpret_cast<uint32_t(*)[NW / 2]>(cv));
+        else if (g.vbits == 4) store_words(vd, *reinterpret_cast<uint32_t(*)[NW / 4]>(cv));
+        else store_words(vd, *reinterpret_cast<uint32_t(*)[NW / 8]>(cv));
+        if (q == 0) *reinterpret_cast<uint32_t*>(pg + g.off_kmeta + 4 * idx) = mk;
+        if (q == 1) *reinterpret_cast<uint32_t*>(pg + g.off_vmeta + 4 * idx) = mv;
+        if (q == 2) *reinterpret_cast<uint32_t*>(pg + g.off_score + 4 * idx) = s_sig[warp][ix];
+        if (q == 3) *reinterpret_cast<int32_t*>(pg + g.off_pos + 4 * idx) = t;
       }
     }
   }
   // phase C: the newest min(W, T) tokens -> FP16 window slot t mod W (Q10)
-  for (int t = max(t0, kept) + grp; t < t1; t += TPS) {
-    const uint4 a = ld_stream_v4(kbase + (size_t)t * d + gl * 8);
-    const uint4 b = ld_stream_v4(vbase + (size_t)t * d + gl * 8);
-    const size_t w = ((size_t)u * p.W + (t % p.W)) * d + gl * 8;
-    *reinterpret_cast<uint4*>(p.win_k + w) = a;
-    *reinterpret_cast<uint4*>(p.win_v + w) = b;
+  {
+    constexpr int LPT = D / 8;                         // lanes per row (16-B chunks)
+    constexpr int RPS = 32 / LPT;                      // rows per step
+    const int rr = lane / LPT, cc = lane % LPT;
+    for (int t = max(t0, kept) + rr; t < t1; t += RPS) {
+      const uint4 a = ld_stream_v4(kbase + (size_t)t * D + cc * 8);
+      const uint4 b = ld_stream_v4(vbase + (size_t)t * D + cc * 8);
+      const size_t w = ((size_t)u * p.W + (t % p.W)) * D + cc * 8;
+      *reinterpret_cast<uint4*>(p.win_k + w) = a;
+      *reinterpret_cast<uint4*>(p.win_v + w) = b;
+    }
   }
   if (__any_sync(kFull, bad) && lane == 0) set_status(p.ctrl, DKV_ERR_NONFINITE);
 }
@@ -249,11 +298,11 @@ cudaError_t launch_quant_prefill(const PoolDev& p, int n, const uint16_t* k, con
   const int nseg_max = (max_len + kSegTokens - 1) / kSegTokens;
   const long items = (long)n * p.LyH * nseg_max;
   if (items > 0) {
-    const long grid = (items + kQWarps - 1) / kQWarps;
+    const long grid = (items + kBulkWarps - 1) / kBulkWarps;
     if (p.d == 128)
-      quant_prefill_kernel<16><<<(unsigned)grid, kQWarps * 32, 0, s>>>(p, n, k, v, kv_stride, sig, sig_stride, nseg_max);
+      quant_prefill_kernel<128><<<(unsigned)grid, kBulkWarps * 32, 0, s>>>(p, n, k, v, kv_stride, sig, sig_stride, nseg_max);
     else
-      quant_prefill_kernel<8><<<(unsigned)grid, kQWarps * 32, 0, s>>>(p, n, k, v, kv_stride, sig, sig_stride, nseg_max);
+      quant_prefill_kernel<64><<<(unsigned)grid, kBulkWarps * 32, 0, s>>>(p, n, k, v, kv_stride, sig, sig_stride, nseg_max);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

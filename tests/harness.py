@@ -225,7 +225,10 @@ def decode_step(backends, inp: Inputs, life: Lifecycle, step: int, check=None, d
     if check: check("quant_write_decode", decs=decs)
     life.seq[active] += 1
     d0 = _np(decs[0])
-    pr = (d0["tc_class"] == 3).astype(np.int64) + (d0["v_action"] == 3).astype(np.int64)
+    if d0.dtype.names is None:                       # CUDA decisions: int32 [U, 4] -> 16-byte records
+        import oracle
+        d0 = np.ascontiguousarray(d0).view(oracle.DECISION_DTYPE).reshape(-1)
+    pr =(d0["tc_class"] == 3).astype(np.int64) + (d0["v_action"] == 3).astype(np.int64)
     life.pruned += pr
     return decs
 
