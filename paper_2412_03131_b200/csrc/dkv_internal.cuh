@@ -22,7 +22,8 @@ struct Ctrl {
   unsigned long long arrive;     // grid-barrier arrivals of compact_alloc (monotonic)
   int64_t last_demand, last_freed;
   int64_t total_dem, total_fr;   // published by the last scan tile before the barrier
-  int64_t pad[6];
+  unsigned long long bar_epoch;  // grid barriers crossed (only calls that take the barrier path)
+  int64_t pad[5];
 };
 static_assert(sizeof(Ctrl) <= 256, "ctrl block");
 
@@ -89,6 +90,48 @@ __device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
 }
 
 __device__ __forceinline__ void set_status(Ctrl* c, int32_t st) { atomicCAS(&c->status, 0, st); }
+
+// ------------------------------------------------------------------------------------- async bulk copies
+// 1-D TMA (cp.async.bulk) global -> shared with mbarrier transaction counting (sm_90+ / sm_100a).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// Ampere-style per-thread 16-byte async copies (LDGSTS), L2-only (.cg).
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool pred) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %2, 0;\n"
+      "@p cp.async.cg.shared.global [%0], [%1], 16;\n"
+      "}\n" ::"r"(smem_u32(dst)), "l"(src), "r"((int)pred) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
 
 // ------------------------------------------------------------------------------------- float helpers
 // Total order on finite floats with -0 < +0 (Q16): monotone unsigned key.
@@ -261,6 +304,389 @@ __device__ __forceinline__ void store_words(uint8_t* dst, const uint32_t (&w)[N]
     *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
   } else {
     *reinterpret_cast<uint32_t*>(dst) = w[0];
+  }
+}
+
+// ---- chunk-interleaved quantizer.  A d-vector is spread over a G-lane group in 8-element (16-B) chunks,
+// lane q holding chunks q, q+G, q+2G, ... so that each warp-wide 16-B load / code store of the group
+// touches contiguous bytes.  Chunk c's codes occupy bytes [c*bits, (c+1)*bits) of the code row.
+__device__ __forceinline__ uint2 pack8_codes(const uint32_t (&ub)[8], int bits) {
+  if (bits == 8)
+    return make_uint2(pack4_lo_bytes(ub[0], ub[1], ub[2], ub[3]), pack4_lo_bytes(ub[4], ub[5], ub[6], ub[7]));
+  if (bits == 4) {
+    const uint32_t ev = pack4_lo_bytes(ub[0], ub[2], ub[4], ub[6]);
+    const uint32_t od = pack4_lo_bytes(ub[1], ub[3], ub[5], ub[7]);
+    return make_uint2(ev | (od << 4), 0u);
+  }
+  uint32_t acc = 0;
+#pragma unroll
+  for (int m = 0; m < 4; m++) acc |= __byte_perm(ub[m], ub[m + 4], 0x0040) << (2 * m);
+  return make_uint2(acc & 0xFFFFu, 0u);
+}
+
+__device__ __forceinline__ void store_chunk_codes(uint8_t* row, int chunk, int bits, uint2 v) {
+  uint8_t* d = row + chunk * bits;
+  if (bits == 8) *reinterpret_cast<uint2*>(d) = v;
+  else if (bits == 4) *reinterpret_cast<uint32_t*>(d) = v.x;
+  else *reinterpret_cast<uint16_t*>(d) = (uint16_t)v.x;
+}
+
+// FP16 input (x[c][w] = half2 word w of this lane's chunk c), runtime bits, group-masked collectives.
+// Arithmetic identical to quant_h16 / the oracle.
+template <int G, int NCH>
+__device__ __forceinline__ void quant_chunks_h16(const uint32_t (&x)[NCH][4], int bits, unsigned gmask,
+                                                 uint2 (&pk)[NCH], uint32_t& meta, bool& ok) {
+  const float Qf = (float)((1 << bits) - 1);
+  __half2 lo = *reinterpret_cast<const __half2*>(&x[0][0]), hi = lo;
+#pragma unroll
+  for (int c = 0; c < NCH; c++)
+#pragma unroll
+    for (int w = 0; w < 4; w++) {
+      if (c == 0 && w == 0) continue;
+      const __half2 v = *reinterpret_cast<const __half2*>(&x[c][w]);
+      lo = __hmin2_nan(lo, v);
+      hi = __hmax2_nan(hi, v);
+    }
+  __half2 key = __halves2half2(__hmin_nan(__low2half(lo), __high2half(lo)),
+                               __hneg(__hmax_nan(__low2half(hi), __high2half(hi))));
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    uint32_t k = *reinterpret_cast<uint32_t*>(&key);
+    k = __shfl_xor_sync(gmask, k, o);
+    key = __hmin2_nan(key, *reinterpret_cast<__half2*>(&k));
+  }
+  unsigned short mnb = __half_as_ushort(__low2half(key));
+  const unsigned short mxb = __half_as_ushort(__hneg(__high2half(key)));
+  if ((mnb & 0x7FFFu) == 0) {                           // group-uniform: which zero is the minimum?
+    bool negz = false;
+#pragma unroll
+    for (int c = 0; c < NCH; c++)
+#pragma unroll
+      for (int w = 0; w < 4; w++) negz |= ((x[c][w] & 0xFFFFu) == 0x8000u) | ((x[c][w] >> 16) == 0x8000u);
+    mnb = (__ballot_sync(gmask, negz) & gmask) ? 0x8000u : 0x0000u;
+  }
+  ok = ((mnb & 0x7C00u) != 0x7C00u) && ((mxb & 0x7C00u) != 0x7C00u);
+  const float mn = __half2float(__ushort_as_half(mnb)), mx = __half2float(__ushort_as_half(mxb));
+  const float s32 = __fdiv_rn(__fsub_rn(mx, mn), Qf);
+  const __half s16 = __float2half_rn(s32);
+  meta = (uint32_t)__half_as_ushort(s16) | ((uint32_t)mnb << 16);
+  const float sf = __half2float(s16);
+  const float inv = __fdiv_rn(1.0f, sf);
+  const float nz = -mn;
+  const float cap = (sf >= 6.103515625e-05f) ? 3.0e38f : Qf;
+  const uint32_t zmask = sf != 0.0f ? 0xFFFFFFFFu : 0u;  // s16 == 0: all codes 0
+#pragma unroll
+  for (int c = 0; c < NCH; c++) {
+    uint32_t ub[8];
+#pragma unroll
+    for (int w = 0; w < 4; w++)
+#pragma unroll
+      for (int hh = 0; hh < 2; hh++) {
+        const float d = mixed_add_h(hh ? (x[c][w] >> 16) : (x[c][w] & 0xFFFFu), nz);
+        float t = __fmul_rn(d, inv);
+        t = fminf(t, cap);
+        const float a = __fadd_rd(t, 0.5f);
+        ub[2 * w + hh] = __float_as_uint(__fadd_rd(a, 8388608.0f)) & zmask;
+      }
+    pk[c] = pack8_codes(ub, bits);
+  }
+}
+
+template <int BITS>
+__device__ __forceinline__ uint2 pack8_codes_ct(const uint32_t (&ub)[8]) {
+  if constexpr (BITS == 8) {
+    return make_uint2(pack4_lo_bytes(ub[0], ub[1], ub[2], ub[3]), pack4_lo_bytes(ub[4], ub[5], ub[6], ub[7]));
+  } else if constexpr (BITS == 4) {
+    const uint32_t ev = pack4_lo_bytes(ub[0], ub[2], ub[4], ub[6]);
+    const uint32_t od = pack4_lo_bytes(ub[1], ub[3], ub[5], ub[7]);
+    return make_uint2(ev | (od << 4), 0u);
+  } else {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int m = 0; m < 4; m++) acc |= __byte_perm(ub[m], ub[m + 4], 0x0040) << (2 * m);
+    return make_uint2(acc & 0xFFFFu, 0u);
+  }
+}
+
+template <int BITS>
+__device__ __forceinline__ void store_chunk_codes_ct(uint8_t* row, int chunk, uint2 v) {
+  uint8_t* d = row + chunk * BITS;
+  if constexpr (BITS == 8) *reinterpret_cast<uint2*>(d) = v;
+  else if constexpr (BITS == 4) *reinterpret_cast<uint32_t*>(d) = v.x;
+  else *reinterpret_cast<uint16_t*>(d) = (uint16_t)v.x;
+}
+
+// Compile-time bit width, called by ALL 32 lanes of the warp (warp-uniform fast path): as
+// quant_chunks_h16, but the clamp (subnormal s16) and the s16 == 0 masking run only when some group of
+// the warp needs them.
+template <int G, int NCH, int BITS>
+__device__ __forceinline__ void quant_chunks_h16_ct(const uint32_t (&x)[NCH][4], unsigned gmask, uint2 (&pk)[NCH],
+                                                    uint32_t& meta, bool& ok) {
+  constexpr float Qf = (float)((1 << BITS) - 1);
+  __half2 lo = *reinterpret_cast<const __half2*>(&x[0][0]), hi = lo;
+#pragma unroll
+  for (int c = 0; c < NCH; c++)
+#pragma unroll
+    for (int w = 0; w < 4; w++) {
+      if (c == 0 && w == 0) continue;
+      const __half2 v = *reinterpret_cast<const __half2*>(&x[c][w]);
+      lo = __hmin2_nan(lo, v);
+      hi = __hmax2_nan(hi, v);
+    }
+  __half2 key = __halves2half2(__hmin_nan(__low2half(lo), __high2half(lo)),
+                               __hneg(__hmax_nan(__low2half(hi), __high2half(hi))));
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    uint32_t k = *reinterpret_cast<uint32_t*>(&key);
+    k = __shfl_xor_sync(kFull, k, o);
+    key = __hmin2_nan(key, *reinterpret_cast<__half2*>(&k));
+  }
+  unsigned short mnb = __half_as_ushort(__low2half(key));
+  const unsigned short mxb = __half_as_ushort(__hneg(__high2half(key)));
+  const bool zmin = (mnb & 0x7FFFu) == 0;
+  if (__any_sync(kFull, zmin)) {                        // rare: which zero is the minimum?
+    bool negz = false;
+#pragma unroll
+    for (int c = 0; c < NCH; c++)
+#pragma unroll
+      for (int w = 0; w < 4; w++) negz |= ((x[c][w] & 0xFFFFu) == 0x8000u) | ((x[c][w] >> 16) == 0x8000u);
+    const unsigned b = __ballot_sync(kFull, negz);
+    if (zmin) mnb = (b & gmask) ? 0x8000u : 0x0000u;
+  }
+  ok = ((mnb & 0x7C00u) != 0x7C00u) && ((mxb & 0x7C00u) != 0x7C00u);
+  const float mn = __half2float(__ushort_as_half(mnb)), mx = __half2float(__ushort_as_half(mxb));
+  const float s32 = __fdiv_rn(__fsub_rn(mx, mn), Qf);
+  const __half s16 = __float2half_rn(s32);
+  meta = (uint32_t)__half_as_ushort(s16) | ((uint32_t)mnb << 16);
+  const float sf = __half2float(s16);
+  const float inv = __fdiv_rn(1.0f, sf);
+  const float nz = -mn;
+  if (!__any_sync(kFull, !(sf >= 6.103515625e-05f))) {  // every s16 normal: t <= Q + 1/8, no clamp needed
+#pragma unroll
+    for (int c = 0; c < NCH; c++) {
+      uint32_t ub[8];
+#pragma unroll
+      for (int w = 0; w < 4; w++)
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++) {
+          const float d = mixed_add_h(hh ? (x[c][w] >> 16) : (x[c][w] & 0xFFFFu), nz);
+          const float a = __fadd_rd(__fmul_rn(d, inv), 0.5f);
+          ub[2 * w + hh] = __float_as_uint(__fadd_rd(a, 8388608.0f));
+        }
+      pk[c] = pack8_codes_ct<BITS>(ub);
+    }
+  } else {
+    const float cap = (sf >= 6.103515625e-05f) ? 3.0e38f : Qf;
+    const uint32_t zmask = sf != 0.0f ? 0xFFFFFFFFu : 0u;
+#pragma unroll
+    for (int c = 0; c < NCH; c++) {
+      uint32_t ub[8];
+#pragma unroll
+      for (int w = 0; w < 4; w++)
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++) {
+          const float d = mixed_add_h(hh ? (x[c][w] >> 16) : (x[c][w] & 0xFFFFu), nz);
+          const float t = fminf(__fmul_rn(d, inv), cap);
+          const float a = __fadd_rd(t, 0.5f);
+          ub[2 * w + hh] = __float_as_uint(__fadd_rd(a, 8388608.0f)) & zmask;
+        }
+      pk[c] = pack8_codes_ct<BITS>(ub);
+    }
+  }
+}
+
+// FP32 input (a dequantized K8V4 token being downgraded, Q9): x[c][e] = element e of chunk c.
+// min/max with fminf/fmaxf (IEEE minimum/maximum, -0 < +0 on sm_100 as the oracle's total order);
+// z = f16(min) may exceed some inputs, so t is clamped to [0, Q] before the exact RD rounding — equal to
+// clamp(round_half_away(t), 0, Q).
+template <int G, int NCH>
+__device__ __forceinline__ void quant_chunks_f32(const float (&x)[NCH][8], int bits, unsigned gmask,
+                                                 uint2 (&pk)[NCH], uint32_t& meta) {
+  const float Qf = (float)((1 << bits) - 1);
+  float mn = x[0][0], mx = x[0][0];
+#pragma unroll
+  for (int c = 0; c < NCH; c++)
+#pragma unroll
+    for (int e = 0; e < 8; e++) { mn = fminf(mn, x[c][e]); mx = fmaxf(mx, x[c][e]); }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(gmask, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(gmask, mx, o));
+  }
+  const float s32 = __fdiv_rn(__fsub_rn(mx, mn), Qf);
+  const __half s16 = __float2half_rn(s32), z16 = __float2half_rn(mn);
+  meta = (uint32_t)__half_as_ushort(s16) | ((uint32_t)__half_as_ushort(z16) << 16);
+  const float sf = __half2float(s16), zf = __half2float(z16);
+  const float inv = __fdiv_rn(1.0f, sf);
+  const uint32_t zmask = sf != 0.0f ? 0xFFFFFFFFu : 0u;
+#pragma unroll
+  for (int c = 0; c < NCH; c++) {
+    uint32_t ub[8];
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      float t = __fmul_rn(__fsub_rn(x[c][e], zf), inv);
+      t = fminf(fmaxf(t, 0.0f), Qf);
+      const float a = __fadd_rd(t, 0.5f);
+      ub[e] = __float_as_uint(__fadd_rd(a, 8388608.0f)) & zmask;
+    }
+    pk[c] = pack8_codes(ub, bits);
+  }
+}
+
+// Dequantize one 8-element chunk (its `bits`-byte code piece) -> fp32 (X^ = s*Q + z).
+__device__ __forceinline__ void dequant_chunk(const uint8_t* row, int chunk, int bits, uint32_t meta, float (&x)[8]) {
+  const float sf = __half2float(__ushort_as_half((unsigned short)(meta & 0xFFFFu)));
+  const float zf = __half2float(__ushort_as_half((unsigned short)(meta >> 16)));
+  const uint8_t* s = row + chunk * bits;
+  uint64_t v;
+  if (bits == 8) { const uint2 t = *reinterpret_cast<const uint2*>(s); v = (uint64_t)t.x | ((uint64_t)t.y << 32); }
+  else if (bits == 4) v = *reinterpret_cast<const uint32_t*>(s);
+  else v = *reinterpret_cast<const uint16_t*>(s);
+  const uint32_t Q = (1u << bits) - 1u;
+#pragma unroll
+  for (int e = 0; e < 8; e++) {
+    const uint32_t q = (uint32_t)(v >> (e * bits)) & Q;
+    x[e] = __fadd_rn(__fmul_rn(sf, __uint_as_float(0x4B000000u | q) - 8388608.0f), zf);
+  }
+}
+
+// ---- runtime-bit-width variants for kernels whose lanes groups hold different classes (decode): the
+// arithmetic is the same; only Q and the packing depend on `bits`; collectives use the group mask.
+template <int E>
+__device__ __forceinline__ int pack_codes_rt(const uint32_t (&ub)[E], int bits, uint32_t (&cw)[E / 4]) {
+  if (bits == 8) {
+#pragma unroll
+    for (int w = 0; w < E / 4; w++) cw[w] = pack4_lo_bytes(ub[4 * w], ub[4 * w + 1], ub[4 * w + 2], ub[4 * w + 3]);
+    return E / 4;
+  }
+  if (bits == 4) {
+#pragma unroll
+    for (int w = 0; w < E / 8; w++) {
+      const uint32_t ev = pack4_lo_bytes(ub[8 * w], ub[8 * w + 2], ub[8 * w + 4], ub[8 * w + 6]);
+      const uint32_t od = pack4_lo_bytes(ub[8 * w + 1], ub[8 * w + 3], ub[8 * w + 5], ub[8 * w + 7]);
+      cw[w] = ev | (od << 4);
+    }
+    return E / 8;
+  }
+#pragma unroll
+  for (int w = 0; w < E / 16; w++) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int m = 0; m < 4; m++)
+      acc |= pack4_lo_bytes(ub[16 * w + m], ub[16 * w + m + 4], ub[16 * w + m + 8], ub[16 * w + m + 12]) << (2 * m);
+    cw[w] = acc;
+  }
+  return E / 16;
+}
+
+template <int NC>
+__device__ __forceinline__ void store_words_rt(uint8_t* dst, const uint32_t (&w)[NC], int n) {
+  if (n >= 4) {
+#pragma unroll
+    for (int i = 0; i < NC; i += 4)
+      if (i < n) reinterpret_cast<uint4*>(dst)[i / 4] = make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]);
+  } else if (n == 2) {
+    *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+  } else {
+    *reinterpret_cast<uint32_t*>(dst) = w[0];
+  }
+}
+
+// FP16 input, runtime bits, group-masked collectives.  Same arithmetic as quant_h16.
+template <int G, int NW>
+__device__ __forceinline__ int quant_h16_rt(const uint32_t (&x)[NW], int bits, unsigned gmask,
+                                            uint32_t (&cw)[NW / 2], uint32_t& meta, bool& ok) {
+  const float Qf = (float)((1 << bits) - 1);
+  __half2 lo = *reinterpret_cast<const __half2*>(&x[0]), hi = lo;
+#pragma unroll
+  for (int i = 1; i < NW; i++) {
+    const __half2 v = *reinterpret_cast<const __half2*>(&x[i]);
+    lo = __hmin2_nan(lo, v);
+    hi = __hmax2_nan(hi, v);
+  }
+  __half2 key = __halves2half2(__hmin_nan(__low2half(lo), __high2half(lo)),
+                               __hneg(__hmax_nan(__low2half(hi), __high2half(hi))));
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    uint32_t k = *reinterpret_cast<uint32_t*>(&key);
+    k = __shfl_xor_sync(gmask, k, o);
+    key = __hmin2_nan(key, *reinterpret_cast<__half2*>(&k));
+  }
+  unsigned short mnb = __half_as_ushort(__low2half(key));
+  const unsigned short mxb = __half_as_ushort(__hneg(__high2half(key)));
+  if ((mnb & 0x7FFFu) == 0) {                           // group-uniform: which zero is the minimum?
+    bool negz = false;
+#pragma unroll
+    for (int i = 0; i < NW; i++) negz |= ((x[i] & 0xFFFFu) == 0x8000u) | ((x[i] >> 16) == 0x8000u);
+    mnb = (__ballot_sync(gmask, negz) & gmask) ? 0x8000u : 0x0000u;
+  }
+  ok = ((mnb & 0x7C00u) != 0x7C00u) && ((mxb & 0x7C00u) != 0x7C00u);
+  const float mn = __half2float(__ushort_as_half(mnb)), mx = __half2float(__ushort_as_half(mxb));
+  const float s32 = __fdiv_rn(__fsub_rn(mx, mn), Qf);
+  const __half s16 = __float2half_rn(s32);
+  meta = (uint32_t)__half_as_ushort(s16) | ((uint32_t)mnb << 16);
+  const float sf = __half2float(s16);
+  const float inv = __fdiv_rn(1.0f, sf);
+  const float nz = -mn;
+  const float cap = (sf >= 6.103515625e-05f) ? 3.0e38f : Qf;
+  uint32_t ub[NW * 2];
+#pragma unroll
+  for (int i = 0; i < NW; i++) {
+#pragma unroll
+    for (int hh = 0; hh < 2; hh++) {
+      const float d = mixed_add_h(hh ? (x[i] >> 16) : (x[i] & 0xFFFFu), nz);
+      float t = __fmul_rn(d, inv);
+      t = fminf(t, cap);
+      const float a = __fadd_rd(t, 0.5f);
+      ub[2 * i + hh] = sf != 0.0f ? __float_as_uint(__fadd_rd(a, 8388608.0f)) : 0u;
+    }
+  }
+  return pack_codes_rt<NW * 2>(ub, bits, cw);
+}
+
+// FP32 input (a dequantized K8V4 token being downgraded, Q9), runtime bits, group-masked collectives.
+// min/max with fminf/fmaxf (IEEE minimum/maximum: -0 < +0 on sm_100, as the oracle's total order);
+// z = f16(min) may exceed some inputs, so t is clamped to [0, Q] before the exact RD rounding — the same
+// result as clamp(round_half_away(t), 0, Q).
+template <int G, int E>
+__device__ __forceinline__ int quant_f32_rt(const float (&x)[E], int bits, unsigned gmask, uint32_t (&cw)[E / 4],
+                                            uint32_t& meta) {
+  const float Qf = (float)((1 << bits) - 1);
+  float mn = x[0], mx = x[0];
+#pragma unroll
+  for (int i = 1; i < E; i++) { mn = fminf(mn, x[i]); mx = fmaxf(mx, x[i]); }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(gmask, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(gmask, mx, o));
+  }
+  const float s32 = __fdiv_rn(__fsub_rn(mx, mn), Qf);
+  const __half s16 = __float2half_rn(s32), z16 = __float2half_rn(mn);
+  meta = (uint32_t)__half_as_ushort(s16) | ((uint32_t)__half_as_ushort(z16) << 16);
+  const float sf = __half2float(s16), zf = __half2float(z16);
+  const float inv = __fdiv_rn(1.0f, sf);
+  uint32_t ub[E];
+#pragma unroll
+  for (int i = 0; i < E; i++) {
+    float t = __fmul_rn(__fsub_rn(x[i], zf), inv);
+    t = fminf(fmaxf(t, 0.0f), Qf);
+    const float a = __fadd_rd(t, 0.5f);
+    ub[i] = sf != 0.0f ? __float_as_uint(__fadd_rd(a, 8388608.0f)) : 0u;
+  }
+  return pack_codes_rt<E>(ub, bits, cw);
+}
+
+// Dequantize E codes (bits each, packed LSB-first in words) -> fp32 (X^ = s*Q + z).
+template <int E>
+__device__ __forceinline__ void dequant_rt(const uint32_t* w, int bits, uint32_t meta, float (&x)[E]) {
+  const float sf = __half2float(__ushort_as_half((unsigned short)(meta & 0xFFFFu)));
+  const float zf = __half2float(__ushort_as_half((unsigned short)(meta >> 16)));
+  const uint32_t Q = (1u << bits) - 1u;
+#pragma unroll
+  for (int i = 0; i < E; i++) {
+    const int bit = i * bits;
+    const uint32_t q = (w[bit >> 5] >> (bit & 31)) & Q;
+    x[i] = __fadd_rn(__fmul_rn(sf, __uint_as_float(0x4B000000u | q) - 8388608.0f), zf);
   }
 }
 

@@ -47,7 +47,6 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 template <int TU>
 __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, int phase) {
   constexpr int NW = TU / 32;
-  __shared__ int s_tile;
   __shared__ unsigned long long s_epoch;
   __shared__ int64_t s_start0, s_free0, s_D, s_F;
   __shared__ int s_status0;
@@ -56,16 +55,28 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Ctrl* ctrl = p.ctrl;
-  if (tid == 0) {
-    const unsigned long long t = atomicAdd(&ctrl->ticket, 1ull);
-    s_tile = (int)(t % (unsigned long long)p.num_tiles);
-    s_epoch = t / (unsigned long long)p.num_tiles;
-    s_start0 = ld_volatile(&ctrl->start);
-    s_free0 = ld_volatile(&ctrl->free);
-    s_status0 = ld_volatile(&ctrl->status);
+  // The launch is cooperative (all tiles co-resident), so tiles take their index from blockIdx and the
+  // look-back always waits on running or finished tiles.  The call's epoch (status-word tag and barrier
+  // target) is ctrl->ticket, which only tile 0 advances, after the barrier every tile crossed having read it.
+  if (tid == 0) s_epoch = *(volatile unsigned long long*)&ctrl->ticket;
+  if (tid == 32) s_start0 = ld_volatile(&ctrl->start);
+  if (tid == 64) s_free0 = ld_volatile(&ctrl->free);
+  if (tid == 96) s_status0 = ld_volatile(&ctrl->status);
+  const int tile = blockIdx.x;
+  // per-unit loads do not depend on the control block: issue them before the first barrier
+  const int u = tile * TU + tid;
+  int st = -1, r = 0, nh = 0, nl = 0;
+  uint32_t dword = 0;
+  int pfh = 0, pfl = 0;
+  if (u < p.U) {
+    r = u / p.LyH;
+    st = p.req_state[r];
+    nh = p.n_h[u];
+    nl = p.n_l[u];
+    if (phase == DKV_PHASE_DECODE) dword = __ldg(reinterpret_cast<const uint32_t*>(dec + u));
+    else { pfh = p.pf_nh[u]; pfl = p.pf_nl[u]; }
   }
   __syncthreads();
-  const int tile = s_tile;
   const unsigned long long epoch = s_epoch;
   const uint32_t tag = (uint32_t)(epoch & 63ull);
   const int64_t start0 = s_start0, free0 = s_free0;
@@ -73,24 +84,18 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   const int P = p.P, L = p.L;
 
   // ---- per-unit demand and freed pages (planning results)
-  const int u = tile * TU + tid;
-  int st = -1, r = 0, nh = 0, nl = 0, grow = 0;
+  int grow = 0;
   uint32_t dem = 0, fr = 0;
   if (u < p.U) {
-    r = u / p.LyH;
-    st = p.req_state[r];
-    nh = p.n_h[u];
-    nl = p.n_l[u];
     if (st == DKV_REQ_PENDING_FREE) fr = ceil_div(nh, p.Ch) + ceil_div(nl, p.Cl);
     if (status0 == 0) {
       if (phase == DKV_PHASE_DECODE) {
         if (st == DKV_REQ_ACTIVE) {
-          const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(dec + u));
-          dem = w >> 24;
-          grow = (w >> 16) & 0xFF;
+          dem = dword >> 24;
+          grow = (dword >> 16) & 0xFF;
         }
       } else if (st == DKV_REQ_ADMITTING) {
-        dem = ceil_div(p.pf_nh[u], p.Ch) + ceil_div(p.pf_nl[u], p.Cl);
+        dem = ceil_div(pfh, p.Ch) + ceil_div(pfl, p.Cl);
       }
     }
   }
@@ -170,19 +175,32 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   }
   __syncthreads();
 
-  // ---- grid barrier: every tile's recycle writes are visible and the totals are known
-  if (tid == 0) {
-    if (tile == p.num_tiles - 1) { ctrl->total_dem = s_incdem; ctrl->total_fr = s_incfr; }
-    __threadfence();
-    atomicAdd(&ctrl->arrive, 1ull);
-    const unsigned long long target = (epoch + 1ull) * (unsigned long long)p.num_tiles;
-    while (ld_acquire(&ctrl->arrive) < target) __nanosleep(40);
-    s_D = ld_volatile(&ctrl->total_dem);
-    s_F = ld_volatile(&ctrl->total_fr);
+  // ---- Fast path (no grid barrier): with an error pending nothing is granted; in a decode step every unit
+  // demands at most one page, so if the free region at entry already holds >= U pages the
+  // all-or-nothing check cannot fail and every grant reads a ring slot of that region, never one recycled
+  // in this call.  Both conditions are read at entry and identical in every tile.
+  const bool fast = (status0 != 0) || (phase == DKV_PHASE_DECODE && free0 >= (int64_t)p.U);
+  bool ok;
+  int64_t D = 0, F = 0;
+  if (fast) {
+    ok = status0 == 0;
+  } else {
+    // grid barrier: every tile's recycle writes are visible and the totals are known
+    if (tid == 0) {
+      if (tile == p.num_tiles - 1) { ctrl->total_dem = s_incdem; ctrl->total_fr = s_incfr; }
+      const unsigned long long bep = *(volatile unsigned long long*)&ctrl->bar_epoch;
+      __threadfence();
+      atomicAdd(&ctrl->arrive, 1ull);
+      const unsigned long long target = (bep + 1ull) * (unsigned long long)p.num_tiles;
+      while (ld_acquire(&ctrl->arrive) < target) __nanosleep(40);
+      s_D = ld_volatile(&ctrl->total_dem);
+      s_F = ld_volatile(&ctrl->total_fr);
+    }
+    __syncthreads();
+    D = s_D;
+    F = s_F;
+    ok = (status0 == 0) && (D <= free0 + F);
   }
-  __syncthreads();
-  const int64_t D = s_D, F = s_F, free_avail = free0 + F;
-  const bool ok = (status0 == 0) && (D <= free_avail);
 
   // ---- grant + bidirectional table write + counts
   if (ok) {
@@ -222,8 +240,9 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
       if (st == DKV_REQ_ADMITTING) { p.n_h[u] = p.pf_nh[u]; p.n_l[u] = p.pf_nl[u]; }
     }
   }
-  // ---- request-level transitions (all tiles read req_state before the barrier)
-  if (u < p.U && u % p.LyH == 0) {
+  // ---- request-level transitions, by the tile owning the request's LAST unit: every other tile holding
+  // units of the request is a predecessor, and has read req_state before publishing its look-back status
+  if (u < p.U && u % p.LyH == p.LyH - 1) {
     if (st == DKV_REQ_PENDING_FREE) {
       p.req_state[r] = DKV_REQ_IDLE; p.seq_len[r] = 0; p.prompt_len[r] = 0;
     } else if (ok && phase == DKV_PHASE_DECODE && st == DKV_REQ_ACTIVE) {
@@ -232,8 +251,11 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
       p.seq_len[r] = p.prompt_len[r];
     }
   }
-  // ---- pointers (every tile read them before arriving at the barrier)
-  if (tile == 0 && tid == 0) {
+  // ---- pointers: every tile read them before publishing its look-back status, so the last tile (whose
+  // inclusive prefix holds the totals) may write them in the fast path; tile 0 after the barrier otherwise
+  if (tid == 0 && (fast ? tile == p.num_tiles - 1 : tile == 0)) {
+    if (fast) { D = s_incdem; F = s_incfr; }
+    const int64_t free_avail = free0 + F;
     if (status0 == 0 && !ok) { set_status(ctrl, DKV_ERR_OOM); ctrl->oom_count += 1; }
     const int64_t ns = ok ? (start0 + D) % P : start0;
     const int64_t nf = ok ? free_avail - D : free_avail;
@@ -241,6 +263,8 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
     ctrl->free = nf;
     ctrl->last_demand = status0 == 0 ? D : 0;
     ctrl->last_freed = F;
+    ctrl->ticket = epoch + 1ull;                       // next call's epoch
+    if (!fast) ctrl->bar_epoch = ctrl->bar_epoch + 1ull;   // every tile read it before arriving
     p.stats[0] = nf;
     p.stats[1] = -(status0 == 0 ? D : 0);
     p.stats[2] = -((int64_t)P - nf);

@@ -21,7 +21,7 @@ __global__ void init_kernel(PoolDev p) {
     Ctrl* c = p.ctrl;
     c->start = 0; c->free = p.P; c->status = 0; c->oom_count = 0;
     c->ticket = 0ull; c->arrive = 0ull; c->last_demand = 0; c->last_freed = 0;
-    c->total_dem = 0; c->total_fr = 0;
+    c->total_dem = 0; c->total_fr = 0; c->bar_epoch = 0ull;
     p.stats[0] = p.P; p.stats[1] = 0; p.stats[2] = 0; p.stats[3] = 0;
   }
 }
