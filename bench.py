@@ -217,7 +217,7 @@ def run_ours(args, rank, world, local):
     dev = torch.device("cuda", local)
     wl = Workload(c, rank, world, dev)
     cfg = D.make_config(wl.R, c["Ly"], wl.Hl, c["d"], c["M"], c["W"], c["Ch"], c["Cl"], P=c["P"],
-                        alpha_h=c["alpha_h"], alpha_l=c["alpha_l"])
+                        alpha_h=c["alpha_h"], alpha_l=c["alpha_l"], tile_units=args.tile_units)
     pool = Pool(cfg, device=dev)
     geom = pool.geom()
     T = c["prompt"]
@@ -256,6 +256,7 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         barrier(world)
         e0, e1 = ev(), ev()
+        torch.cuda._sleep(200_000)                         # see the decode phase: time device execution
         e0.record()
         pool.quant_write_prefill(k16, v16, sig)
         e1.record()
@@ -276,6 +277,18 @@ def run_ours(args, rank, world, local):
     stats_view = pool.views()["stats"]
     red = torch.empty(4, dtype=torch.int64, device=dev)
     comp_us, cls_us, qw_us, step_us, cls_bytes = [], [], [], [], []
+    # launch floor: event -> trivial kernel -> event, measured the same way as the step kernels
+    floor_us = []
+    for _ in range(20):
+        torch.cuda.synchronize()
+        f0, f1 = ev(), ev()
+        torch.cuda._sleep(200_000)
+        f0.record()
+        torch.cuda._sleep(0)
+        f1.record()
+        torch.cuda.synchronize()
+        floor_us.append(f0.elapsed_time(f1) * 1e3)
+    floor = float(np.median(floor_us))
     freed_steps = 0
     total_steps = args.warmup + args.steps
     for s in range(total_steps):
@@ -296,6 +309,10 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         barrier(world)
         e = [ev() for _ in range(4)]
+        # a ~100 µs device-side spin ahead of the step lets the host enqueue all three ABI calls before the
+        # GPU reaches e[0], so the events time device execution, not Python/ctypes submission latency
+        # (e2e below keeps the host path in its timed region)
+        torch.cuda._sleep(200_000)
         e[0].record()
         pool.classify_decode(cand, dec)
         e[1].record()
@@ -402,6 +419,7 @@ def run_ours(args, rank, world, local):
                            "quant_write": round(qw_mean, 3), "step": round(step_mean, 3),
                            "compact_alloc_p50": round(float(np.percentile(comp_us, 50)), 3),
                            "compact_alloc_p99": round(float(np.percentile(comp_us, 99)), 3),
+                           "launch_floor": round(floor, 3),
                            "recycle_steps": freed_steps},
         "quant_write": {"gbs": round(agg_bulk_gbs, 1), "gbs_per_gpu": round(bulk_gbs_rank, 1),
                         "ms": round(bulk_max, 3), "algorithmic_bytes_per_gpu": bbytes, "token_mix": bmix,
@@ -522,6 +540,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="llama3_8b", choices=sorted(CONFIGS))
+    ap.add_argument("--tile-units", type=int, default=0, help="compact_alloc scan tile (0 = library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     assert args.warmup >= 1

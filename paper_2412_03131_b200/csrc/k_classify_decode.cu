@@ -1,0 +1,182 @@
+// k_classify_decode.cu — generation-phase planning (a1-a2; "each attention head independently
+// determines its memory allocation requirements ... perfectly parallelizable").
+//
+// One warp per unit.  Algorithm 1: the class of t_c from the thresholds alpha/N, then the
+// victim t_v = lexicographic (score, position) argmin over the section t_c joins (Q6, Q7).  The section's
+// page IDs are staged in shared memory with one coalesced pass over its table row, then each lane issues
+// kCV 16-B score loads (4 slots each) at once, so a unit costs two dependent memory round trips.  The scan
+// keeps a running unsigned minimum (stored scores are canonical non-negative floats, so bit order is float
+// order) with a tiny update path; whenever the minimum score may be shared by several slots, a rare exact
+// pass re-reads the section and breaks the tie on positions (oldest wins).
+#include "dkv_internal.cuh"
+
+namespace dkv {
+
+constexpr int kCDWarps = 4;                // units (warps) per CTA
+constexpr int kCV = 8;                     // 16-B score vectors per lane per batch (1024 slots per batch)
+
+__device__ __forceinline__ int32_t slot_pos(const PoolDev& p, int cls, int u, int s) {
+  int idx;
+  const uint8_t* pg = slot_page(p, cls, u, s, idx);
+  const int off_pos = cls == DKV_CLS_HIGH ? p.g[1].off_pos : p.g[2].off_pos;
+  return __ldg(reinterpret_cast<const int32_t*>(pg + off_pos) + idx);
+}
+
+__global__ void __launch_bounds__(kCDWarps * 32)
+classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decision_t* __restrict__ dec) {
+  extern __shared__ int32_t s_pid_all[];                         // [kCDWarps][L] page IDs of the scanned sections
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int u = blockIdx.x * kCDWarps + warp;
+  if (u >= p.U) return;                                          // whole warps exit together
+  int32_t* s_pid = s_pid_all + warp * p.L;
+  if (ld_volatile(&p.ctrl->status) != 0) return;                 // sticky error: no-op
+  if (u < (p.U + 31) / 32 && lane == 0) {
+    // warm L2 with the ring window the following dkv_compact_alloc grants from: [start, start + U) holds
+    // every page a decode step can demand (one per unit); one 128-B line per warp
+    const int64_t idx = (ld_volatile(&p.ctrl->start) + 32 * (int64_t)u) % p.P;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p.ring + idx));
+  }
+  const int r = u / p.LyH;
+  uint8_t tc_class = DKV_CLS_NONE, v_action = DKV_V_NONE, grow = DKV_GROW_NONE, demand = 0;
+  int v_slot = -1, tc_slot = -1, v_dst_slot = -1;
+  bool scan = false;
+  int cls = DKV_CLS_NONE, n = 0, nh = 0, nl = 0;
+  float sc = 0.0f, th = 0.0f, tl = 0.0f;
+  {
+    const int8_t st = p.req_state[r];
+    const int N = p.seq_len[r] + 1;                              // Q3: includes this step's token
+    const float s_in = cand_sig[u];
+    const int nh_in = p.n_h[u], nl_in = p.n_l[u];
+    const int pc = N - 1 - p.W;                                  // t_c = earliest window token
+    if (st == DKV_REQ_ACTIVE && pc >= 0) {
+      if (!finite_f(s_in) || s_in < 0.0f) {
+        if (lane == 0) set_status(p.ctrl, DKV_ERR_NONFINITE);
+      } else {
+        sc = canon_zero(s_in);
+        th = __fdiv_rn(p.alpha_h, (float)N);                     // alpha_h / N
+        tl = __fdiv_rn(p.alpha_l, (float)N);                     // alpha_l / N
+        cls = sc >= th ? DKV_CLS_HIGH : (sc >= tl ? DKV_CLS_LOW : DKV_CLS_PRUNED);
+        tc_class = (uint8_t)cls;
+        if (cls != DKV_CLS_PRUNED) {
+          nh = nh_in;
+          nl = nl_in;
+          n = (cls == DKV_CLS_HIGH) ? nh : nl;
+          scan = true;
+        }
+      }
+    }
+  }
+  int vs = -1;                                                   // victim slot, -1 = t_c itself
+  uint32_t vb = 0xFFFFFFFFu;
+  if (scan && n > 0) {                                           // warp-uniform
+    const int C = cls == DKV_CLS_HIGH ? p.g[1].C : p.g[2].C;
+    const int off_score = cls == DKV_CLS_HIGH ? p.g[1].off_score : p.g[2].off_score;
+    const bool pow2 = (C & (C - 1)) == 0;
+    const int csh = __popc(C - 1);
+    const int npages = (n + C - 1) / C;
+    const int32_t* row = p.table + (size_t)u * p.L;
+    for (int k = lane; k < npages; k += 32) s_pid[k] = __ldg(row + (cls == DKV_CLS_HIGH ? k : p.L - 1 - k));
+    __syncwarp();
+    const uint8_t* base_sc = p.pages + off_score;
+    auto vec_addr = [&](int s0) {
+      const int pg = pow2 ? (s0 >> csh) : s0 / C;
+      const int ix = pow2 ? (s0 & (C - 1)) : s0 % C;
+      return base_sc + (size_t)s_pid[pg] * (size_t)p.page_bytes + 4 * ix;
+    };
+    uint32_t best = 0xFFFFFFFFu;
+    int bslot = -1;
+    bool tie = false;                                            // best may be held by more than one slot
+    for (int base = 0; base < n; base += 128 * kCV) {
+      uint4 v[kCV];
+#pragma unroll
+      for (int j = 0; j < kCV; j++) {
+        const int s0 = base + j * 128 + 4 * lane;
+        v[j] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        if (s0 < n) v[j] = ld_nc_v4(vec_addr(s0));
+      }
+#pragma unroll
+      for (int j = 0; j < kCV; j++) {
+        const int s0 = base + j * 128 + 4 * lane;
+        uint32_t a = v[j].x, b = v[j].y, c = v[j].z, d = v[j].w;
+        if (s0 + 3 >= n) {                                       // tail vector: mask slots >= n
+          a = s0 < n ? a : 0xFFFFFFFFu;
+          b = s0 + 1 < n ? b : 0xFFFFFFFFu;
+          c = s0 + 2 < n ? c : 0xFFFFFFFFu;
+          d = 0xFFFFFFFFu;
+        }
+        const uint32_t m4 = min(min(a, b), min(c, d));
+        if (m4 <= best && m4 != 0xFFFFFFFFu) {                   // rare after the first steps
+          if (m4 == best) {
+            tie = true;
+          } else {
+            best = m4;
+            bslot = s0 + (a == m4 ? 0 : (b == m4 ? 1 : (c == m4 ? 2 : 3)));
+            tie = ((a == m4) + (b == m4) + (c == m4) + (d == m4)) > 1;
+          }
+        }
+      }
+    }
+    const uint32_t m = __reduce_min_sync(kFull, best);
+    const unsigned holders = __ballot_sync(kFull, best == m);
+    const bool any_tie = __any_sync(kFull, best == m && tie);
+    if (__popc(holders) == 1 && !any_tie) {
+      vs = __shfl_sync(kFull, bslot, __ffs(holders) - 1);
+    } else {
+      // exact pass: among the slots scoring m, the oldest position wins (Q6)
+      int32_t bp = 0x7FFFFFFF;
+      int bs = -1;
+      for (int s0 = 4 * lane; s0 < n; s0 += 128) {
+        const uint4 x = ld_nc_v4(vec_addr(s0));
+        const uint32_t e4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          if (s0 + e < n && e4[e] == m) {
+            const int32_t ps = slot_pos(p, cls, u, s0 + e);
+            if (ps < bp) { bp = ps; bs = s0 + e; }
+          }
+        }
+      }
+      const uint32_t mp = __reduce_min_sync(kFull, (uint32_t)bp);
+      vs = __shfl_sync(kFull, bs, __ffs(__ballot_sync(kFull, (uint32_t)bp == mp && bs >= 0)) - 1);
+    }
+    vb = m;
+  }
+  if (lane != 0) return;
+  if (scan) {
+    // t_c has the largest position, so a stored token wins every score tie with it
+    if (vs >= 0 && !(vb <= __float_as_uint(sc))) vs = -1;
+    const float sv = __uint_as_float(vb);
+    if (cls == DKV_CLS_HIGH) {
+      if (vs < 0 || sv >= th) {                                  // t_v stays in KV_h
+        v_action = DKV_V_KEEP; grow = DKV_GROW_HIGH; demand = (nh % p.Ch == 0); tc_slot = nh;
+      } else if (sv >= tl) {                                     // line requant_high
+        v_action = DKV_V_DOWN; grow = DKV_GROW_LOW; demand = (nl % p.Cl == 0);
+        v_slot = vs; tc_slot = vs; v_dst_slot = nl;
+      } else {                                                   // prune t_v
+        v_action = DKV_V_PRUNE; v_slot = vs; tc_slot = vs;
+      }
+    } else {
+      if (vs < 0 || sv >= tl) {
+        v_action = DKV_V_KEEP; grow = DKV_GROW_LOW; demand = (nl % p.Cl == 0); tc_slot = nl;
+      } else {                                                   // line prune_low
+        v_action = DKV_V_PRUNE; v_slot = vs; tc_slot = vs;
+      }
+    }
+  }
+  int4 w;
+  w.x = (int)((uint32_t)tc_class | ((uint32_t)v_action << 8) | ((uint32_t)grow << 16) | ((uint32_t)demand << 24));
+  w.y = v_slot; w.z = tc_slot; w.w = v_dst_slot;
+  reinterpret_cast<int4*>(dec)[u] = w;
+}
+
+cudaError_t launch_classify_decode(const PoolDev& p, const float* sig, dkv_decision_t* dec, cudaStream_t s) {
+  const size_t smem = 4 * (size_t)p.L * kCDWarps;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(classify_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  classify_decode_kernel<<<(p.U + kCDWarps - 1) / kCDWarps, kCDWarps * 32, smem, s>>>(p, sig, dec);
+  return cudaGetLastError();
+}
+
+}  // namespace dkv

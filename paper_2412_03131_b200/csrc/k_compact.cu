@@ -17,7 +17,7 @@
 // the grid-wide demand before any grant, and grants may read ring slots recycled by other tiles in this
 // call (Q14), so the kernel then crosses one software grid barrier (arrival counter; the launch is
 // cooperative, which guarantees co-residency) and grants.
-#include <cooperative_groups.h>
+#include <stdlib.h>
 
 #include "dkv_internal.cuh"
 
@@ -152,23 +152,51 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   const uint32_t off_dem = s_exdem + s_wdem[warp] + inc_dem - (phase == DKV_PHASE_DECODE ? (dem != 0) : dem);
   const uint32_t off_fr = s_exfr + s_wfr[warp] + inc_fr - fr;
 
-  // ---- recycle: freed IDs -> ring[(end + off + k) mod P], canonical slot order (Q13); warp-cooperative
+  // ---- recycle: freed IDs -> ring[(end + off + k) mod P], canonical slot order (Q13).  The tile's freed
+  // units are listed in shared memory and dealt round-robin to all warps; a warp copies one unit's slots
+  // with 32 lanes, issuing up to 8 table loads per lane before the dependent ring / table stores.
   {
-    const int64_t end0 = (start0 + free0) % P;
-    unsigned fm = __ballot_sync(kFull, fr != 0);
-    while (fm) {
-      const int src = __ffs(fm) - 1;
-      fm &= fm - 1;
-      const int uu = __shfl_sync(kFull, u, src);
-      const uint32_t off = __shfl_sync(kFull, off_fr, src);
-      const int nfr = (int)__shfl_sync(kFull, fr, src);
-      const int ph = __shfl_sync(kFull, ceil_div(nh, p.Ch), src);
-      int32_t* row = p.table + (size_t)uu * L;
-      for (int k = lane; k < nfr; k += 32) {
-        const int slot = k < ph ? k : L - nfr + k;               // [0, ph) then [L - pl, L)
-        const int32_t pid = row[slot];
-        p.ring[(end0 + off + k) % P] = pid;
-        row[slot] = -1;
+    __shared__ int s_nfu;
+    __shared__ uint32_t s_fu[TU];                                // freed unit, by tile-local rank
+    if (tid == 0) s_nfu = 0;
+    __syncthreads();
+    const unsigned fm = __ballot_sync(kFull, fr != 0);
+    int wbase = 0;
+    if (lane == 0 && fm) wbase = atomicAdd(&s_nfu, __popc(fm));
+    wbase = __shfl_sync(kFull, wbase, 0);
+    if (fr != 0) s_fu[wbase + __popc(fm & ((1u << lane) - 1u))] = (uint32_t)tid;
+    __syncthreads();
+    const int nfu = s_nfu;
+    if (nfu > 0) {
+      const int64_t end0 = (start0 + free0) % P;
+      __shared__ uint32_t s_off[TU];
+      __shared__ int s_nfr[TU], s_ph[TU];
+      s_off[tid] = off_fr; s_nfr[tid] = (int)fr; s_ph[tid] = ceil_div(nh, p.Ch);
+      __syncthreads();
+      for (int i = warp; i < nfu; i += NW) {
+        const int t = (int)s_fu[i];
+        const int uu = tile * TU + t;
+        const uint32_t off = s_off[t];
+        const int nfr = s_nfr[t], ph = s_ph[t];
+        int32_t* row = p.table + (size_t)uu * L;
+        for (int k0 = 0; k0 < nfr; k0 += 32 * 8) {
+          int32_t pid[8];
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            const int k = k0 + 32 * j + lane;
+            const int slot = k < ph ? k : L - nfr + k;           // [0, ph) then [L - pl, L)
+            pid[j] = k < nfr ? __ldcg(row + slot) : -1;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            const int k = k0 + 32 * j + lane;
+            if (k < nfr) {
+              const int slot = k < ph ? k : L - nfr + k;
+              p.ring[(end0 + off + k) % P] = pid[j];
+              row[slot] = -1;
+            }
+          }
+        }
       }
     }
     if (fr != 0) { p.n_h[u] = 0; p.n_l[u] = 0; }
@@ -282,8 +310,9 @@ static cudaError_t launch_tu(const PoolDev& p, const dkv_decision_t* dec, int ph
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
+  static const int coop = getenv("DKV_COMPACT_COOP") ? atoi(getenv("DKV_COMPACT_COOP")) : 1;   // tuning knob
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = coop ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, compact_alloc_kernel<TU>, p, dec, phase);
 }
 

@@ -10,21 +10,22 @@
 //      tc_slot, score = s_c, position = p_c;
 //   3. write the new token into that same window slot (its old row was read into registers first).
 // Every collective is group-masked, so units with different classes / actions in one warp are independent.
+#include <stdlib.h>
+
 #include "dkv_internal.cuh"
 
 namespace dkv {
 
 constexpr int kQDWarps = 4;
-constexpr int kQDG = 4;                                  // lanes per unit
 
-template <int D>
+template <int D, int kQDG>                               // kQDG lanes per unit
 __global__ void __launch_bounds__(kQDWarps * 32)
 quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uint16_t* __restrict__ knew,
                     const uint16_t* __restrict__ vnew, const float* __restrict__ cand_sig) {
-  constexpr int NCH = D / 32;                            // chunks per lane
+  constexpr int NCH = D / (8 * kQDG);                    // chunks per lane
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / kQDG, q = lane % kQDG;
-  const unsigned gmask = 0xFu << (grp * kQDG);
+  const unsigned gmask = ((1u << kQDG) - 1u) << (grp * kQDG);
   const int u = (blockIdx.x * kQDWarps + warp) * (32 / kQDG) + grp;
   if (u >= p.U) return;                                  // whole groups exit together
   if (ld_volatile(&p.ctrl->status) != 0) return;
@@ -120,13 +121,23 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
   }
 }
 
+template <int D, int G>
+static cudaError_t launch_qd(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
+                             const float* sig, cudaStream_t s) {
+  const int units_per_cta = kQDWarps * (32 / G);
+  const int grid = (p.U + units_per_cta - 1) / units_per_cta;
+  quant_decode_kernel<D, G><<<grid, kQDWarps * 32, 0, s>>>(p, dec, k, v, sig);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
                                 const float* sig, cudaStream_t s) {
-  const int units_per_cta = kQDWarps * (32 / kQDG);
-  const int grid = (p.U + units_per_cta - 1) / units_per_cta;
-  if (p.d == 128) quant_decode_kernel<128><<<grid, kQDWarps * 32, 0, s>>>(p, dec, k, v, sig);
-  else quant_decode_kernel<64><<<grid, kQDWarps * 32, 0, s>>>(p, dec, k, v, sig);
-  return cudaGetLastError();
+  static const int g = getenv("DKV_QD_G") ? atoi(getenv("DKV_QD_G")) : 4;   // tuning knob
+  if (p.d == 128) {
+    if (g == 16) return launch_qd<128, 16>(p, dec, k, v, sig, s);
+    return g == 4 ? launch_qd<128, 4>(p, dec, k, v, sig, s) : launch_qd<128, 8>(p, dec, k, v, sig, s);
+  }
+  return g == 4 ? launch_qd<64, 4>(p, dec, k, v, sig, s) : launch_qd<64, 8>(p, dec, k, v, sig, s);
 }
 
 }  // namespace dkv

@@ -127,8 +127,6 @@ struct dkv_pool {
   bool recovering;                   // last query reported an error: frees allowed out of sequence
 };
 
-static dkv_status_t cuda_status(cudaError_t e) { return e == cudaSuccess ? DKV_OK : DKV_ERR_CUDA; }
-
 extern "C" {
 
 const char* dkv_status_string(dkv_status_t st) {

@@ -73,6 +73,7 @@ class Shape:
     H: int
     H_total: int | None = None
     h0: int = 0
+    req_ids: tuple | None = None      # global request id of each local request slot (default: identity)
 
     @property
     def Ht(self) -> int:
@@ -84,7 +85,10 @@ class Shape:
 
     def global_units(self, reqs, device="cpu") -> torch.Tensor:
         """[len(reqs), Ly*H] int64 global unit ids for local request ids `reqs`, local (l, h) order."""
-        r = torch.as_tensor(np.asarray(reqs, dtype=np.int64), device=device).view(-1, 1, 1)
+        rr = np.asarray(reqs, dtype=np.int64)
+        if self.req_ids is not None:
+            rr = np.asarray(self.req_ids, dtype=np.int64)[rr]
+        r = torch.as_tensor(rr, device=device).view(-1, 1, 1)
         l = torch.arange(self.Ly, device=device, dtype=torch.int64).view(1, -1, 1)
         h = torch.arange(self.H, device=device, dtype=torch.int64).view(1, 1, -1) + self.h0
         return ((r * self.Ly + l) * self.Ht + h).reshape(len(reqs), self.Ly * self.H)

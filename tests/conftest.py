@@ -20,6 +20,9 @@ def pytest_collection_modifyitems(config, items):
     except Exception:  # pragma: no cover
         has_gpu = False
     if has_gpu:
+        for it in items:                      # a hung kernel must not eat the GPU budget
+            if "gpu" in it.keywords and not it.get_closest_marker("timeout"):
+                it.add_marker(pytest.mark.timeout(600))
         return
     skip = pytest.mark.skip(reason="no CUDA device")
     for it in items:

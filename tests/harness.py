@@ -40,10 +40,11 @@ class Scenario:
     H_total: int | None = None
     h0: int = 0
     tile_units: int = 0
+    req_ids: tuple | None = None      # global request ids of the local slots (sampled sub-pools)
 
     @property
     def shape(self) -> synth.Shape:
-        return synth.Shape(self.R, self.Ly, self.H, self.H_total, self.h0)
+        return synth.Shape(self.R, self.Ly, self.H, self.H_total, self.h0, self.req_ids)
 
     @property
     def U(self):

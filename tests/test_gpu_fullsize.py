@@ -1,0 +1,140 @@
+"""Parity at BASELINE.json's full size (configs[1]: 64 requests x 32 layers x 8 KV heads, head_dim 128,
+4096-token prompts, 2^22 pages) in the launch configuration bench.py times, on sampled requests the
+oracle recomputes one by one (a sub-pool holding only those requests: their units see the same inputs,
+and every unit's slot contents depend only on its own history), plus pool-wide properties that hold at any
+size (page ownership is a permutation, occupied slots are exactly [0, ph) u [L - pl, L))."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def _unit_records(pages, table_row, n_h, n_l, geom, L):
+    """per-slot (k codes, k meta, v codes, v meta, score bits, pos) of one unit from device tensors"""
+    recs = {}
+    for cls, n in ((1, n_h), (2, n_l)):
+        g = geom[cls]
+        C = g["C"]
+        npg = -(-int(n) // C)
+        if npg == 0:
+            continue
+        cols = list(range(npg)) if cls == 1 else [L - 1 - k for k in range(npg)]
+        pids = table_row[cols].long()
+        pg = pages[pids].cpu().numpy()                                  # [npg, page_bytes]
+        for s in range(int(n)):
+            b = pg[s // C]
+            i = s % C
+            recs[(cls, s)] = (b[g["off_k"] + i * g["k_row"]: g["off_k"] + (i + 1) * g["k_row"]].tobytes(),
+                              b[g["off_kmeta"] + 4 * i: g["off_kmeta"] + 4 * i + 4].tobytes(),
+                              b[g["off_v"] + i * g["v_row"]: g["off_v"] + (i + 1) * g["v_row"]].tobytes(),
+                              b[g["off_vmeta"] + 4 * i: g["off_vmeta"] + 4 * i + 4].tobytes(),
+                              b[g["off_score"] + 4 * i: g["off_score"] + 4 * i + 4].tobytes(),
+                              b[g["off_pos"] + 4 * i: g["off_pos"] + 4 * i + 4].tobytes())
+    return recs
+
+
+def test_llama8b_fullsize_sampled_parity():
+    import bench
+    import synth
+    from paper_2412_03131_b200 import Pool, decisions_to_numpy
+    from paper_2412_03131_b200 import dkv as D
+    from tests import harness as H
+
+    c = bench.CONFIGS["llama3_8b"]
+    dev = torch.device("cuda", 0)
+    wl = bench.Workload(c, 0, 1, dev)
+    T = c["prompt"]
+    cfg = D.make_config(wl.R, c["Ly"], wl.Hl, c["d"], c["M"], c["W"], c["Ch"], c["Cl"], P=c["P"],
+                        alpha_h=c["alpha_h"], alpha_l=c["alpha_l"])
+    pool = Pool(cfg, device=dev)
+    geom, L, LyH = pool.geom(), pool.L, pool.LyH
+    sig, kk, vv = wl.prefill_inputs(T)
+    reqs = list(range(wl.R))
+    pool.classify_prefill(reqs, [T] * wl.R, sig)
+    pool.compact_alloc(None)
+    pool.quant_write_prefill(kk.view(torch.int16), vv.view(torch.int16), sig)
+    del kk, vv
+    dec = pool.new_decisions()
+
+    sample = (0, 37)
+    scn = H.Scenario(R=2, Ly=c["Ly"], H=c["H"], d=c["d"], M=c["M"], W=c["W"], Ch=c["Ch"], Cl=c["Cl"],
+                     P=2 * LyH * (T // c["Ch"] + 8), alpha_h=c["alpha_h"], alpha_l=c["alpha_l"], seed=c["seed"],
+                     mix=c["mix"], req_ids=sample)
+    o = H.OracleBackend(scn)
+    inp = H.Inputs(scn)                                                  # oracle inputs drawn on the host
+    life = H.Lifecycle(scn)
+    H.admit([o], inp, life, [0, 1], [T, T])
+
+    def compare(where, dec_gpu=None, dec_orc=None):
+        torch.cuda.synchronize()
+        v = pool.views()
+        n_h, n_l = v["n_h"].cpu().numpy(), v["n_l"].cpu().numpy()
+        for i, r in enumerate(sample):
+            for j in range(LyH):
+                ug, uo = r * LyH + j, i * LyH + j
+                assert (n_h[ug], n_l[ug]) == (o.pool.n_h[uo], o.pool.n_l[uo]), (where, r, j)
+                if j % 37 == 0 or dec_gpu is not None:
+                    a = _unit_records(v["pages"], v["table"][ug], n_h[ug], n_l[ug], geom, L)
+                    b = {}
+                    for cls, n in ((1, o.pool.n_h[uo]), (2, o.pool.n_l[uo])):
+                        for s in range(int(n)):
+                            kc, km, vc, vm, sg, ps = o.pool.slot_record(cls, uo, s)
+                            b[(cls, s)] = (kc.tobytes(), np.uint32(km).tobytes(), vc.tobytes(),
+                                           np.uint32(vm).tobytes(), np.uint32(sg).tobytes(), np.int32(ps).tobytes())
+                    assert a == b, (where, r, j)
+                    wk = v["win_k"][ug].cpu().numpy().view(np.uint16)
+                    assert np.array_equal(wk, o.pool.win_k[uo]), (where, r, j)
+            if dec_gpu is not None:
+                a = dec_gpu[r * LyH:(r + 1) * LyH]
+                b = dec_orc[i * LyH:(i + 1) * LyH]
+                assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (where, r)
+        # pool-wide properties at full size (on the device)
+        ctrl = v["ctrl"].cpu().numpy()
+        start, free, P = int(ctrl[0]), int(ctrl[1]), c["P"]
+        ring = v["ring"]
+        free_ids = ring[(start + torch.arange(free, device=dev)) % P]
+        tab = v["table"]
+        used = tab[tab >= 0]
+        allids = torch.cat([free_ids, used]).sort().values
+        assert allids.numel() == P and torch.equal(allids, torch.arange(P, device=dev, dtype=allids.dtype)), where
+        ph = (v["n_h"].long() + c["Ch"] - 1) // c["Ch"]
+        pl = (v["n_l"].long() + c["Cl"] - 1) // c["Cl"]
+        k = torch.arange(L, device=dev).view(1, -1)
+        expect = (k < ph.view(-1, 1)) | (k >= (L - pl).view(-1, 1))
+        assert torch.equal(tab >= 0, expect), where
+
+    compare("prefill")
+    seq = np.full(wl.R, T, np.int64)
+    act = np.ones(wl.R, bool)
+    for step in range(3):
+        v = pool.views()
+        synth.apply_drift(c["seed"], step, wl.shape, v["pages"], v["table"], v["n_h"], v["n_l"],
+                          {k_: (geom[k_]["C"], geom[k_]["off_score"], geom[k_]["off_pos"]) for k_ in (1, 2)}, L)
+        cand, nk, nv = wl.decode_inputs(seq, act)
+        pool.classify_decode(cand, dec)
+        pool.compact_alloc(dec)
+        pool.quant_write_decode(dec, nk.view(torch.int16), nv.view(torch.int16), cand)
+        seq += 1
+        decs = H.decode_step([o], inp, life, step)
+        compare(f"decode {step}", decisions_to_numpy(dec), decs[0])
+    st, _ = pool.query()
+    assert st == 0
+
+
+def test_synth_generators_device_independent():
+    """The input generators give bit-identical values on the host and on the device (so the bench may draw
+    its 32 GiB of inputs on the GPU while the oracle draws its sample on the host)."""
+    import synth
+    ug = torch.arange(0, 4096, 7, dtype=torch.int64)
+    a =synth.kv_values(5, synth.S_KEY, ug, 0, 64, 128)
+    b = synth.kv_values(5, synth.S_KEY, ug.cuda(), 0, 64, 128).cpu()
+    assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    mh, ml = synth.unit_mix(5, ug, Ly=32, Ht=8)
+    s1 = synth.prefill_sig(5, ug, 300, 1.0, 0.02, mh, ml)
+    s2 = synth.prefill_sig(5, ug.cuda(), 300, 1.0, 0.02, mh.cuda(), ml.cuda()).cpu()
+    assert torch.equal(s1.view(torch.int32), s2.view(torch.int32))
+    N = torch.full((ug.numel(),), 4500, dtype=torch.int64)
+    d1 = synth.decode_sig(5, ug, N, 64, 1.0, 0.02, mh, ml)
+    d2 = synth.decode_sig(5, ug.cuda(), N.cuda(), 64, 1.0, 0.02, mh.cuda(), ml.cuda()).cpu()
+    assert torch.equal(d1.view(torch.int32), d2.view(torch.int32))
