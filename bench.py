@@ -201,11 +201,20 @@ def load_peaks():
 
 
 def load_traffic():
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch of each kernel, from the committed
+    `ncu --set full` summaries (profiles/traffic.json, written by tools/make_profiles.py)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            return json.load(f)
-    return {}
+    if not os.path.exists(p):
+        return lambda k: None
+    with open(p) as f:
+        j = json.load(f)
+
+    def get(kernel):
+        for name, rec in j.items():
+            if name.split("<")[0] == kernel:
+                return int(rec["bytes_per_launch"])
+        return None
+    return get
 
 
 # ----------------------------------------------------------------------------------------- our arm
@@ -427,11 +436,11 @@ def run_ours(args, rank, world, local):
         "roofline": {"kernel": "quant_prefill_kernel (dkv_quant_write PREFILL, bulk writer)", "bound": "hbm",
                      "achieved": round(bulk_gbs_rank, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": round(bulk_gbs_rank / peak, 4),
-                     "traffic": traffic.get("quant_prefill_kernel")},
+                     "traffic": traffic("quant_prefill_kernel"), "traffic_unit": "bytes per launch"},
         "roofline_decode": {"kernel": "classify_decode_kernel", "bound": "hbm", "achieved": round(cls_gbs, 1),
                             "peak": peak, "unit": "GB/s", "frac": round(cls_gbs / peak, 4),
                             "algorithmic_bytes": int(statistics.mean(cls_bytes)),
-                            "traffic": traffic.get("classify_decode_kernel")},
+                            "traffic": traffic("classify_decode_kernel"), "traffic_unit": "bytes per launch"},
         "e2e": {"value": round(e2e_mean, 3), "unit": "us per decode step (H2D inputs + classify + compact_alloc + "
                                                      "quant_write + D2H decisions)",
                 "h2d_bytes_per_step": wl.U * (4 + 2 * 2 * c["d"]), "d2h_bytes_per_step": wl.U * 16},
