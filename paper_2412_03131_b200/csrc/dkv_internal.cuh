@@ -31,6 +31,38 @@ struct ClassGeom {
   int32_t C, kbits, vbits, k_row, v_row, off_k, off_kmeta, off_v, off_vmeta, off_score, off_pos;
 };
 
+// n / d and n % d for 0 <= n < 2^31 by multiply-high (Granlund-Montgomery): mul = ceil(2^(31+l) / d),
+// l = ceil(log2 d); d = 1 is mul = 0.  Built on the host (make_fastdiv), checked there over every n a
+// kernel can pass (fastdiv_check).
+struct FastDiv {
+  int32_t d;
+  uint32_t mul;
+  int32_t shr;
+};
+__host__ __device__ __forceinline__ int32_t fdiv(const FastDiv& f, int32_t n) {
+#ifdef __CUDA_ARCH__
+  return f.mul == 0 ? n : (int32_t)(__umulhi((uint32_t)n, f.mul) >> f.shr);
+#else
+  return f.mul == 0 ? n : (int32_t)((((uint64_t)(uint32_t)n * f.mul) >> 32) >> f.shr);
+#endif
+}
+__host__ __device__ __forceinline__ int32_t fmod_(const FastDiv& f, int32_t n) { return n - fdiv(f, n) * f.d; }
+inline FastDiv make_fastdiv(int32_t d) {
+  FastDiv f;
+  f.d = d;
+  if (d <= 1) { f.mul = 0; f.shr = 0; return f; }
+  int l = 0;
+  while ((1ll << l) < d) l++;
+  f.mul = (uint32_t)((((uint64_t)1 << (31 + l)) + (uint64_t)d - 1) / (uint64_t)d);
+  f.shr = l - 1;
+  return f;
+}
+inline bool fastdiv_check(const FastDiv& f, int64_t n_max) {
+  for (int64_t n = 0; n <= n_max && n < ((int64_t)1 << 31); n++)
+    if (fdiv(f, (int32_t)n) != (int32_t)(n / f.d)) return false;
+  return true;
+}
+
 // Everything a kernel needs, passed by value.
 struct PoolDev {
   int32_t R, Ly, H, LyH, U, d, M, W, L, P, page_bytes, Ch, Cl;
@@ -54,6 +86,7 @@ struct PoolDev {
   __half* win_v;
   uint8_t* pages;
   int64_t* stats;       // int64[4] admission counters
+  FastDiv div_LyH, div_W, div_Ch, div_Cl;   // u -> request, position -> window slot, slot -> (page, index)
 };
 
 // ------------------------------------------------------------------------------------- memory ops
@@ -76,6 +109,14 @@ __device__ __forceinline__ uint32_t ld_nc_u32(const void* p) {
 __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
   uint4 v;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+// same, with the L2 fetch limited to the 64-B sector pair the load touches (.L2::64B prefetch size)
+__device__ __forceinline__ uint4 ld_nc_v4_64(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
@@ -745,6 +786,45 @@ __device__ __forceinline__ uint8_t* slot_page(const PoolDev& p, int cls, int u, 
 }
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// ---- per-CTA copy of the per-request arrays.  Every unit of a request reads the same state / length
+// word, so thousands of warps loading them (or the control block) directly all queue on the same few L2
+// lines at one slice — measured to dominate the decode kernels.  Persistent CTAs copy the arrays into
+// shared memory once instead (one coalesced pass per CTA).  Above kReqSmemMax requests the kernels read
+// global memory directly.
+constexpr int kReqSmemMax = 4096;
+__host__ __device__ __forceinline__ size_t req_cache_bytes(int R) {
+  return R <= kReqSmemMax ? (size_t)R * 4 + (((size_t)R + 15) & ~(size_t)15) : 0;
+}
+struct ReqCache {
+  const int32_t* len;
+  const int8_t* st;
+};
+// smem: [R] int32 committed lengths, then [R] int8 states (caller provides req_cache_bytes(R) bytes)
+__device__ __forceinline__ ReqCache load_req_cache(const PoolDev& p, void* smem) {
+  ReqCache c;
+  if (p.R <= kReqSmemMax) {
+    int32_t* len = reinterpret_cast<int32_t*>(smem);
+    int8_t* st = reinterpret_cast<int8_t*>(len + p.R);
+    for (int i = threadIdx.x; i < p.R; i += blockDim.x) { len[i] = p.seq_len[i]; st[i] = p.req_state[i]; }
+    c.len = len;
+    c.st = st;
+  } else {
+    c.len = p.seq_len;
+    c.st = p.req_state;
+  }
+  return c;                                            // caller: __syncthreads() before use
+}
+
+// CTAs of a persistent kernel: resident CTAs per SM x SMs (cached per kernel by the caller)
+template <typename K>
+inline int persistent_grid(K kernel, int threads, size_t smem) {
+  int dev = 0, sms = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess) return 0;
+  return sms * (per_sm > 0 ? per_sm : 1);
+}
 
 // ------------------------------------------------------------------------------------- launchers
 // Each returns a cudaError_t from the launch.

@@ -1,122 +1,384 @@
 // k_quant_decode.cu — the KV compressor's generation step behind dkv_quant_write(DECODE).
 //
-// Four lanes per unit, eight units per warp.  A d-vector is handled as d/8 16-byte chunks; lane q of a
-// group owns chunks q, q+4, q+8, ... so each warp-wide 16-B access of a group covers 64 contiguous bytes.
-// Per unit, in the order readings Q8/Q9 fix:
+// One G-lane group per unit, EPL = d/G consecutive elements of K and of V per lane, so each vector is one
+// coalesced row per group and the unit's class (hence its bit widths) is uniform inside the group.  Per
+// unit, in the order readings Q8/Q9 fix:
 //   1. downgrade the victim t_v (v_action == DOWN): dequantize its K8V4 codes from its KV_h slot and
-//      re-quantize at K4V2 (quant_chunks_f32) into KV_l slot v_dst_slot, carrying its score and position —
-//      before t_c overwrites that KV_h slot;
-//   2. quantize t_c out of window slot (N-1) mod W == p_c mod W at its class bits (quant_chunks_h16) into
-//      tc_slot, score = s_c, position = p_c;
-//   3. write the new token into that same window slot (its old row was read into registers first).
-// Every collective is group-masked, so units with different classes / actions in one warp are independent.
+//      re-quantize at K4V2 into KV_l slot v_dst_slot, carrying its score and position — before t_c
+//      overwrites that KV_h slot;
+//   2. quantize t_c out of window slot (N-1) mod W == p_c mod W at its class bits into tc_slot,
+//      score = s_c, position = p_c;
+//   3. write the new token into that same window slot (after its old row has been consumed).
+//
+// What sets the duration (measured, profiles/): the unit count, not the bytes.  A unit is a chain of three
+// dependent memory round trips —
+//   A. everything indexed by u alone: decision word, s_c, the new token's K/V (request state and length
+//      come from a per-CTA shared-memory copy: thousands of warps reading the same word queue at one L2
+//      slice);
+//   B. everything the decision or the length addresses: t_c's window row and the (at most three) table
+//      entries the unit touches, one per lane (t_c's page, the victim's KV_h page, its KV_l page);
+//   C. the victim's K8V4 record (downgrades only), addressed by the page IDs shuffled from B —
+// followed by the per-vector scalar work (min/max reduction, two correctly rounded divisions), which a
+// group does once for all its lanes: several units per warp amortise it.  The window push is issued only
+// after t_c's row has been consumed: a store issued while the same line's load miss is outstanding takes a
+// slow path in L2 (measured: 73 -> 26 us at the Llama-3-8B config).
+// Quantizer arithmetic is the oracle's (c.5 / Q16), expressed as in dkv_internal.cuh's quant_h16 /
+// quant_chunks_f32: packed half2 NaN-propagating min/max, one mixed-precision subtraction, exact
+// round-half-away via two round-down adds.
 #include <stdlib.h>
 
 #include "dkv_internal.cuh"
 
 namespace dkv {
 
-constexpr int kQDWarps = 4;
+constexpr int kQDThreads = 256;
 
-template <int D, int kQDG>                               // kQDG lanes per unit
-__global__ void __launch_bounds__(kQDWarps * 32)
+// EPL codes (low byte of ub[i] = code of element i) -> EPL*bits packed bits, element 0 in the LSBs (Q17)
+template <int EPL>
+__device__ __forceinline__ uint4 pack_codes(const uint32_t (&ub)[EPL], int bits) {
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  if (bits == 8) {
+#pragma unroll
+    for (int i = 0; i < EPL / 4; i++) w[i] = pack4_lo_bytes(ub[4 * i], ub[4 * i + 1], ub[4 * i + 2], ub[4 * i + 3]);
+  } else if (bits == 4) {
+    if constexpr (EPL == 4) {
+      w[0] = __byte_perm(ub[0], ub[2], 0x0040) | (__byte_perm(ub[1], ub[3], 0x0040) << 4);
+    } else {
+#pragma unroll
+      for (int i = 0; i < EPL / 8; i++) {
+        const uint32_t ev = pack4_lo_bytes(ub[8 * i], ub[8 * i + 2], ub[8 * i + 4], ub[8 * i + 6]);
+        const uint32_t od = pack4_lo_bytes(ub[8 * i + 1], ub[8 * i + 3], ub[8 * i + 5], ub[8 * i + 7]);
+        w[i] = ev | (od << 4);
+      }
+    }
+  } else {                                               // 2 bits
+    if constexpr (EPL == 4) {
+      w[0] = (ub[0] & 3u) | ((ub[1] & 3u) << 2) | ((ub[2] & 3u) << 4) | ((ub[3] & 3u) << 6);
+    } else if constexpr (EPL == 8) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int m = 0; m < 4; m++) acc |= __byte_perm(ub[m], ub[m + 4], 0x0040) << (2 * m);
+      w[0] = acc;
+    } else {
+#pragma unroll
+      for (int i = 0; i < EPL / 16; i++) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int m = 0; m < 4; m++)
+          acc |= pack4_lo_bytes(ub[16 * i + m], ub[16 * i + m + 4], ub[16 * i + m + 8], ub[16 * i + m + 12]) << (2 * m);
+        w[i] = acc;
+      }
+    }
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+// store / load this lane's piece (EPL elements = EPL*bits/8 bytes) of a code row
+template <int EPL>
+__device__ __forceinline__ void store_codes_lane(uint8_t* row, int q, int bits, uint4 v) {
+  const int nb = EPL * bits / 8;
+  uint8_t* d = row + q * nb;
+  if (nb == 16) *reinterpret_cast<uint4*>(d) = v;
+  else if (nb == 8) *reinterpret_cast<uint2*>(d) = make_uint2(v.x, v.y);
+  else if (nb == 4) *reinterpret_cast<uint32_t*>(d) = v.x;
+  else if (nb == 2) *reinterpret_cast<uint16_t*>(d) = (uint16_t)v.x;
+  else *d = (uint8_t)v.x;
+}
+template <int EPL>
+__device__ __forceinline__ uint4 load_codes_lane(const uint8_t* row, int q, int bits) {
+  const int nb = EPL * bits / 8;
+  const uint8_t* s = row + q * nb;
+  if (nb == 16) return *reinterpret_cast<const uint4*>(s);
+  if (nb == 8) { const uint2 t = *reinterpret_cast<const uint2*>(s); return make_uint4(t.x, t.y, 0u, 0u); }
+  if (nb == 4) return make_uint4(*reinterpret_cast<const uint32_t*>(s), 0u, 0u, 0u);
+  if (nb == 2) return make_uint4(*reinterpret_cast<const uint16_t*>(s), 0u, 0u, 0u);
+  return make_uint4(*s, 0u, 0u, 0u);
+}
+
+// this lane's EPL fp16 elements as EPL/2 half2 words
+template <int EPL>
+struct HVec {
+  uint32_t w[EPL / 2];
+};
+template <int EPL>
+__device__ __forceinline__ HVec<EPL> load_hvec(const uint16_t* row, int q) {
+  HVec<EPL> h;
+  if constexpr (EPL == 4) {
+    const uint2 t = *reinterpret_cast<const uint2*>(row + q * 4);
+    h.w[0] = t.x; h.w[1] = t.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < EPL / 8; i++) {
+      const uint4 t = *reinterpret_cast<const uint4*>(row + q * EPL + 8 * i);
+      h.w[4 * i] = t.x; h.w[4 * i + 1] = t.y; h.w[4 * i + 2] = t.z; h.w[4 * i + 3] = t.w;
+    }
+  }
+  return h;
+}
+template <int EPL>
+__device__ __forceinline__ HVec<EPL> ldg_hvec(const uint16_t* row, int q) {
+  HVec<EPL> h;
+  if constexpr (EPL == 4) {
+    const uint2 t = __ldg(reinterpret_cast<const uint2*>(row + q * 4));
+    h.w[0] = t.x; h.w[1] = t.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < EPL / 8; i++) {
+      const uint4 t = ld_nc_v4(row + q * EPL + 8 * i);
+      h.w[4 * i] = t.x; h.w[4 * i + 1] = t.y; h.w[4 * i + 2] = t.z; h.w[4 * i + 3] = t.w;
+    }
+  }
+  return h;
+}
+template <int EPL>
+__device__ __forceinline__ void store_hvec(uint16_t* row, int q, const HVec<EPL>& h) {
+  if constexpr (EPL == 4) {
+    *reinterpret_cast<uint2*>(row + q * 4) = make_uint2(h.w[0], h.w[1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < EPL / 8; i++)
+      *reinterpret_cast<uint4*>(row + q * EPL + 8 * i) =
+          make_uint4(h.w[4 * i], h.w[4 * i + 1], h.w[4 * i + 2], h.w[4 * i + 3]);
+  }
+}
+
+// this lane's EPL fp16 elements of a row -> shared memory with cp.async (no registers held while in flight)
+template <int EPL>
+__device__ __forceinline__ void stage_row(uint16_t* sdst, const uint16_t* gsrc) {
+  if constexpr (EPL == 4) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+  } else {
+#pragma unroll
+    for (int i = 0; i < EPL / 8; i++)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst + 8 * i)), "l"(gsrc + 8 * i) : "memory");
+  }
+}
+template <int EPL>
+__device__ __forceinline__ HVec<EPL> lds_hvec(const uint16_t* s) {
+  HVec<EPL> h;
+  if constexpr (EPL == 4) {
+    const uint2 t = *reinterpret_cast<const uint2*>(s);
+    h.w[0] = t.x; h.w[1] = t.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < EPL / 8; i++) {
+      const uint4 t = *reinterpret_cast<const uint4*>(s + 8 * i);
+      h.w[4 * i] = t.x; h.w[4 * i + 1] = t.y; h.w[4 * i + 2] = t.z; h.w[4 * i + 3] = t.w;
+    }
+  }
+  return h;
+}
+
+// FP16 input, one vector per G-lane group.
+template <int G, int EPL>
+__device__ __forceinline__ uint4 quant_h16_lane(const HVec<EPL>& x, int bits, unsigned gmask, uint32_t& meta,
+                                                bool& ok) {
+  const float Qf = (float)((1 << bits) - 1);
+  __half2 lo = *reinterpret_cast<const __half2*>(&x.w[0]), hi = lo;
+#pragma unroll
+  for (int i = 1; i < EPL / 2; i++) {
+    const __half2 v = *reinterpret_cast<const __half2*>(&x.w[i]);
+    lo = __hmin2_nan(lo, v);
+    hi = __hmax2_nan(hi, v);
+  }
+  __half2 key = __halves2half2(__hmin_nan(__low2half(lo), __high2half(lo)),
+                               __hneg(__hmax_nan(__low2half(hi), __high2half(hi))));
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    uint32_t k = *reinterpret_cast<uint32_t*>(&key);
+    k = __shfl_xor_sync(gmask, k, o);
+    key = __hmin2_nan(key, *reinterpret_cast<__half2*>(&k));
+  }
+  unsigned short mnb = __half_as_ushort(__low2half(key));
+  const unsigned short mxb = __half_as_ushort(__hneg(__high2half(key)));
+  if ((mnb & 0x7FFFu) == 0) {                           // group-uniform, rare: which zero is the minimum?
+    bool negz = false;
+#pragma unroll
+    for (int i = 0; i < EPL / 2; i++) negz |= ((x.w[i] & 0xFFFFu) == 0x8000u) | ((x.w[i] >> 16) == 0x8000u);
+    mnb = __any_sync(gmask, negz) ? 0x8000u : 0x0000u;
+  }
+  ok = ((mnb & 0x7C00u) != 0x7C00u) && ((mxb & 0x7C00u) != 0x7C00u);
+  const float mn = __half2float(__ushort_as_half(mnb)), mx = __half2float(__ushort_as_half(mxb));
+  const float s32 = __fdiv_rn(__fsub_rn(mx, mn), Qf);
+  const __half s16 = __float2half_rn(s32);
+  meta = (uint32_t)__half_as_ushort(s16) | ((uint32_t)mnb << 16);
+  const float sf = __half2float(s16);
+  const float inv = __frcp_rn(sf);                      // == fdiv_rn(1, sf)
+  const float nz = -mn;                                 // z = min exactly (FP16 input)
+  const float cap = (sf >= 6.103515625e-05f) ? 3.0e38f : Qf;   // clamp only for a subnormal s16
+  const uint32_t zmask = sf != 0.0f ? 0xFFFFFFFFu : 0u;        // s16 == 0: all codes 0
+  uint32_t ub[EPL];
+#pragma unroll
+  for (int i = 0; i < EPL; i++) {
+    const float d = mixed_add_h((i & 1) ? (x.w[i >> 1] >> 16) : (x.w[i >> 1] & 0xFFFFu), nz);
+    const float t = fminf(__fmul_rn(d, inv), cap);
+    ub[i] = __float_as_uint(__fadd_rd(__fadd_rd(t, 0.5f), 8388608.0f)) & zmask;
+  }
+  return pack_codes<EPL>(ub, bits);
+}
+
+// FP32 input (a dequantized K8V4 token being downgraded, Q9); as quant_chunks_f32.
+template <int G, int EPL>
+__device__ __forceinline__ uint4 quant_f32_lane(const float (&x)[EPL], int bits, unsigned gmask, uint32_t& meta) {
+  const float Qf = (float)((1 << bits) - 1);
+  float mn = x[0], mx = x[0];
+#pragma unroll
+  for (int i = 1; i < EPL; i++) { mn = fminf(mn, x[i]); mx = fmaxf(mx, x[i]); }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(gmask, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(gmask, mx, o));
+  }
+  const float s32 = __fdiv_rn(__fsub_rn(mx, mn), Qf);
+  const __half s16 = __float2half_rn(s32), z16 = __float2half_rn(mn);
+  meta = (uint32_t)__half_as_ushort(s16) | ((uint32_t)__half_as_ushort(z16) << 16);
+  const float sf = __half2float(s16), zf = __half2float(z16);
+  const float inv = __frcp_rn(sf);
+  const uint32_t zmask = sf != 0.0f ? 0xFFFFFFFFu : 0u;
+  uint32_t ub[EPL];
+#pragma unroll
+  for (int i = 0; i < EPL; i++) {
+    const float t = fminf(fmaxf(__fmul_rn(__fsub_rn(x[i], zf), inv), 0.0f), Qf);
+    ub[i] = __float_as_uint(__fadd_rd(__fadd_rd(t, 0.5f), 8388608.0f)) & zmask;
+  }
+  return pack_codes<EPL>(ub, bits);
+}
+
+// X^ = s*Q + z for this lane's EPL codes
+template <int EPL, int BITS>
+__device__ __forceinline__ void dequant_lane_ct(const uint4 c, float sf, float zf, float (&x)[EPL]) {
+  const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+  for (int i = 0; i < EPL; i++) {
+    constexpr uint32_t Q = (1u << BITS) - 1u;
+    const uint32_t q = (w[(i * BITS) >> 5] >> ((i * BITS) & 31)) & Q;
+    x[i] = __fadd_rn(__fmul_rn(sf, __uint_as_float(0x4B000000u | q) - 8388608.0f), zf);
+  }
+}
+template <int EPL>
+__device__ __forceinline__ void dequant_lane(const uint4 c, int bits, uint32_t meta, float (&x)[EPL]) {
+  const float sf = __half2float(__ushort_as_half((unsigned short)(meta & 0xFFFFu)));
+  const float zf = __half2float(__ushort_as_half((unsigned short)(meta >> 16)));
+  if (bits == 8) dequant_lane_ct<EPL, 8>(c, sf, zf, x);
+  else if (bits == 4) dequant_lane_ct<EPL, 4>(c, sf, zf, x);
+  else dequant_lane_ct<EPL, 2>(c, sf, zf, x);
+}
+
+template <int D, int G>
+__global__ void __launch_bounds__(kQDThreads, 4)
 quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uint16_t* __restrict__ knew,
                     const uint16_t* __restrict__ vnew, const float* __restrict__ cand_sig) {
-  constexpr int NCH = D / (8 * kQDG);                    // chunks per lane
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = lane / kQDG, q = lane % kQDG;
-  const unsigned gmask = ((1u << kQDG) - 1u) << (grp * kQDG);
-  const int u = (blockIdx.x * kQDWarps + warp) * (32 / kQDG) + grp;
-  if (u >= p.U) return;                                  // whole groups exit together
-  if (ld_volatile(&p.ctrl->status) != 0) return;
-  const int r = u / p.LyH;
-  if (p.req_state[r] != DKV_REQ_ACTIVE) return;
-  const int N = p.seq_len[r];                            // already includes this step's token (compact_alloc)
-  const int pc = N - 1 - p.W;
-  const int4 dw = reinterpret_cast<const int4*>(dec)[u];
-  const int tc_class = dw.x & 0xFF, v_action = (dw.x >> 8) & 0xFF;
-  const int v_slot = dw.y, tc_slot = dw.z, v_dst = dw.w;
+  constexpr int EPL = D / G;                             // elements per lane per vector
+  constexpr int UPC = kQDThreads / G;                    // units per CTA per iteration
+  extern __shared__ __align__(16) uint8_t qd_smem[];
+  __shared__ __align__(16) uint16_t s_new[2][kQDThreads * EPL];   // the new token's K / V rows, this lane's part
+  __shared__ int32_t s_status;
+  const int lane = threadIdx.x & 31;
+  const int q = lane % G;
+  const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  if (threadIdx.x == 0) s_status = p.ctrl->status;
+  const ReqCache rc = load_req_cache(p, qd_smem);
+  __syncthreads();
+  if (s_status != 0) return;                             // sticky error: no-op
+  uint16_t* const my_nk = &s_new[0][threadIdx.x * EPL];
+  uint16_t* const my_nv = &s_new[1][threadIdx.x * EPL];
 
-  // window row of t_c and the new token (16 x 16 B per lane in flight at d = 128)
-  uint32_t wk[NCH][4], wv[NCH][4], nk[NCH][4], nv[NCH][4];
-  const int ws = p.W > 0 ? (N - 1) % p.W : 0;
-  uint4* wk_row = reinterpret_cast<uint4*>(p.win_k + ((size_t)u * p.W + ws) * D);
-  uint4* wv_row = reinterpret_cast<uint4*>(p.win_v + ((size_t)u * p.W + ws) * D);
-  const uint4* nk_row = reinterpret_cast<const uint4*>(knew + (size_t)u * D);
-  const uint4* nv_row = reinterpret_cast<const uint4*>(vnew + (size_t)u * D);
-#pragma unroll
-  for (int c = 0; c < NCH; c++) {
-    const int ch = q + kQDG * c;
-    const uint4 a = __ldg(nk_row + ch), b = __ldg(nv_row + ch);
-    nk[c][0] = a.x; nk[c][1] = a.y; nk[c][2] = a.z; nk[c][3] = a.w;
-    nv[c][0] = b.x; nv[c][1] = b.y; nv[c][2] = b.z; nv[c][3] = b.w;
-    uint4 x = a, y = b;                                  // W = 0: t_c is the new token itself
-    if (p.W > 0) { x = wk_row[ch]; y = wv_row[ch]; }
-    wk[c][0] = x.x; wk[c][1] = x.y; wk[c][2] = x.z; wk[c][3] = x.w;
-    wv[c][0] = y.x; wv[c][1] = y.y; wv[c][2] = y.z; wv[c][3] = y.w;
-  }
-  // 3. window push, issued early: t_c's row is already in registers (same lanes, same addresses, program order)
-  if (p.W > 0) {
-#pragma unroll
-    for (int c = 0; c < NCH; c++) {
-      const int ch = q + kQDG * c;
-      wk_row[ch] = make_uint4(nk[c][0], nk[c][1], nk[c][2], nk[c][3]);
-      wv_row[ch] = make_uint4(nv[c][0], nv[c][1], nv[c][2], nv[c][3]);
+  for (int ub = blockIdx.x; ub * UPC < p.U; ub += gridDim.x) {
+    const int u = ub * UPC + threadIdx.x / G;
+    if (u >= p.U) break;                                 // whole groups leave together (last block only)
+
+    // ---- A: loads indexed by u only (all in flight together); the new token goes straight to smem
+    const int r = fdiv(p.div_LyH, u);
+    const int8_t st = rc.st[r];
+    const int N = rc.len[r];                             // already includes this step's token (compact_alloc)
+    const int4 dw = __ldg(reinterpret_cast<const int4*>(dec) + u);
+    const float s_in = __ldg(cand_sig + u);
+    stage_row<EPL>(my_nk, knew + (size_t)u * D + q * EPL);
+    stage_row<EPL>(my_nv, vnew + (size_t)u * D + q * EPL);
+    cp_async_commit();
+    const bool live = st == DKV_REQ_ACTIVE;
+
+    // ---- B: window row of t_c + the unit's table entries
+    const int pc = N - 1 - p.W;
+    const int tc_class = dw.x & 0xFF, v_action = (dw.x >> 8) & 0xFF;
+    const int v_slot = dw.y, tc_slot = dw.z, v_dst = dw.w;
+    const bool has_tc = live && (tc_class == DKV_CLS_HIGH || tc_class == DKV_CLS_LOW);
+    const bool down = live && v_action == DKV_V_DOWN;
+    const bool tc_high = tc_class == DKV_CLS_HIGH;
+    const int tc_pg = fdiv(tc_high ? p.div_Ch : p.div_Cl, tc_slot);
+    int tix = -1;                                        // lane 0: t_c's page; 1: victim KV_h; 2: victim KV_l
+    if (q == 0 && has_tc) tix = tc_high ? tc_pg : p.L - 1 - tc_pg;
+    if (q == 1 && down) tix = fdiv(p.div_Ch, v_slot);
+    if (q == 2 && down) tix = p.L - 1 - fdiv(p.div_Cl, v_dst);
+    const int pid = tix >= 0 ? __ldg(p.table + (size_t)u * p.L + tix) : 0;
+    uint16_t* wk_row = nullptr;
+    uint16_t* wv_row = nullptr;
+    HVec<EPL> wk, wv;
+    if (p.W > 0 && live) {
+      const int ws = fmod_(p.div_W, N - 1);
+      wk_row = reinterpret_cast<uint16_t*>(p.win_k) + ((size_t)u * p.W + ws) * D;
+      wv_row = reinterpret_cast<uint16_t*>(p.win_v) + ((size_t)u * p.W + ws) * D;
+      wk = load_hvec<EPL>(wk_row, q);
+      wv = load_hvec<EPL>(wv_row, q);
     }
-  }
+    const int gl = lane & ~(G - 1);
+    const int pid_tc = __shfl_sync(gmask, pid, gl);
+    const int pid_src = __shfl_sync(gmask, pid, gl + 1);
+    const int pid_dst = __shfl_sync(gmask, pid, gl + 2);
 
-  // 1. downgrade t_v: K8V4 -> K4V2 (Q9)
-  if (v_action == DKV_V_DOWN) {
-    const ClassGeom gh = geom_of(p, DKV_CLS_HIGH), go = geom_of(p, DKV_CLS_LOW);
-    int is, id;
-    const uint8_t* src = slot_page(p, DKV_CLS_HIGH, u, v_slot, is);
-    uint8_t* dst = slot_page(p, DKV_CLS_LOW, u, v_dst, id);
+    // ---- C + 1. downgrade t_v: K8V4 -> K4V2 (Q9)
+    if (down) {                                          // group-uniform
+      const ClassGeom gh = p.g[1], go = p.g[2];
+      const int is = fmod_(p.div_Ch, v_slot), id = fmod_(p.div_Cl, v_dst);
+      const uint8_t* src = p.pages + (size_t)pid_src * (size_t)p.page_bytes;
+      uint8_t* dst = p.pages + (size_t)pid_dst * (size_t)p.page_bytes;
+      const uint4 ck = load_codes_lane<EPL>(src + gh.off_k + is * gh.k_row, q, gh.kbits);
+      const uint4 cv = load_codes_lane<EPL>(src + gh.off_v + is * gh.v_row, q, gh.vbits);
+      const uint32_t kmeta = *reinterpret_cast<const uint32_t*>(src + gh.off_kmeta + 4 * is);
+      const uint32_t vmeta = *reinterpret_cast<const uint32_t*>(src + gh.off_vmeta + 4 * is);
+      uint32_t carry = 0;                                // lane 2: score bits, lane 3: position
+      if (q == 2) carry = *reinterpret_cast<const uint32_t*>(src + gh.off_score + 4 * is);
+      if (q == 3) carry = *reinterpret_cast<const uint32_t*>(src + gh.off_pos + 4 * is);
 #pragma unroll 1
-    for (int kvsel = 0; kvsel < 2; kvsel++) {
-      const int sb = kvsel ? gh.vbits : gh.kbits, db = kvsel ? go.vbits : go.kbits;
-      const uint8_t* srow = src + (kvsel ? gh.off_v + is * gh.v_row : gh.off_k + is * gh.k_row);
-      uint8_t* drow = dst + (kvsel ? go.off_v + id * go.v_row : go.off_k + id * go.k_row);
-      const uint32_t meta = *reinterpret_cast<const uint32_t*>(src + (kvsel ? gh.off_vmeta : gh.off_kmeta) + 4 * is);
-      float x[NCH][8];
-#pragma unroll
-      for (int c = 0; c < NCH; c++) dequant_chunk(srow, q + kQDG * c, sb, meta, x[c]);
-      uint2 pk[NCH];
-      uint32_t m2;
-      quant_chunks_f32<kQDG, NCH>(x, db, gmask, pk, m2);
-#pragma unroll
-      for (int c = 0; c < NCH; c++) store_chunk_codes(drow, q + kQDG * c, db, pk[c]);
-      if (q == kvsel) *reinterpret_cast<uint32_t*>(dst + (kvsel ? go.off_vmeta : go.off_kmeta) + 4 * id) = m2;
-    }
-    if (q == 2) *reinterpret_cast<uint32_t*>(dst + go.off_score + 4 * id) =
-        *reinterpret_cast<const uint32_t*>(src + gh.off_score + 4 * is);
-    if (q == 3) *reinterpret_cast<int32_t*>(dst + go.off_pos + 4 * id) =
-        *reinterpret_cast<const int32_t*>(src + gh.off_pos + 4 * is);
-  }
-
-  // 2. t_c -> its section slot at its class bits
-  if (tc_class == DKV_CLS_HIGH || tc_class == DKV_CLS_LOW) {
-    const ClassGeom g = geom_of(p, tc_class);
-    uint2 pkk[NCH], pkv[NCH];
-    uint32_t mk, mv;
-    bool fk, fv;
-    quant_chunks_h16<kQDG, NCH>(wk, g.kbits, gmask, pkk, mk, fk);
-    quant_chunks_h16<kQDG, NCH>(wv, g.vbits, gmask, pkv, mv, fv);
-    if (!(fk && fv)) {
-      if (q == 0) set_status(p.ctrl, DKV_ERR_NONFINITE);
-    } else {
-      int idx;
-      uint8_t* pg = slot_page(p, tc_class, u, tc_slot, idx);
-      uint8_t* krow = pg + g.off_k + idx * g.k_row;
-      uint8_t* vrow = pg + g.off_v + idx * g.v_row;
-#pragma unroll
-      for (int c = 0; c < NCH; c++) {
-        store_chunk_codes(krow, q + kQDG * c, g.kbits, pkk[c]);
-        store_chunk_codes(vrow, q + kQDG * c, g.vbits, pkv[c]);
+      for (int kv = 0; kv < 2; kv++) {
+        float x[EPL];
+        dequant_lane<EPL>(kv ? cv : ck, kv ? gh.vbits : gh.kbits, kv ? vmeta : kmeta, x);
+        uint32_t m2;
+        const int db = kv ? go.vbits : go.kbits;
+        const uint4 pk = quant_f32_lane<G, EPL>(x, db, gmask, m2);
+        store_codes_lane<EPL>(dst + (kv ? go.off_v + id * go.v_row : go.off_k + id * go.k_row), q, db, pk);
+        if (q == kv) *reinterpret_cast<uint32_t*>(dst + (kv ? go.off_vmeta : go.off_kmeta) + 4 * id) = m2;
       }
-      if (q == 0) *reinterpret_cast<uint32_t*>(pg + g.off_kmeta + 4 * idx) = mk;
-      if (q == 1) *reinterpret_cast<uint32_t*>(pg + g.off_vmeta + 4 * idx) = mv;
-      if (q == 2) *reinterpret_cast<float*>(pg + g.off_score + 4 * idx) = canon_zero(cand_sig[u]);
-      if (q == 3) *reinterpret_cast<int32_t*>(pg + g.off_pos + 4 * idx) = pc;
+      if (q == 2) *reinterpret_cast<uint32_t*>(dst + go.off_score + 4 * id) = carry;
+      if (q == 3) *reinterpret_cast<uint32_t*>(dst + go.off_pos + 4 * id) = carry;
+      __syncwarp(gmask);                                 // every lane's read of t_v precedes t_c's stores
+    }
+
+    // ---- 2. t_c -> its section slot at its class bits
+    cp_async_wait<0>();                                  // this lane's part of the new token is in smem
+    if (has_tc) {                                        // group-uniform
+      if (p.W == 0) { wk = lds_hvec<EPL>(my_nk); wv = lds_hvec<EPL>(my_nv); }   // t_c is the new token
+      const ClassGeom g = geom_of(p, tc_class);
+      uint32_t mk, mv;
+      bool fk, fv;
+      const uint4 pk = quant_h16_lane<G, EPL>(wk, g.kbits, gmask, mk, fk);
+      const uint4 pv = quant_h16_lane<G, EPL>(wv, g.vbits, gmask, mv, fv);
+      if (!(fk && fv)) {
+        if (q == 0) set_status(p.ctrl, DKV_ERR_NONFINITE);
+      } else {
+        const int idx = tc_slot - tc_pg * g.C;
+        uint8_t* pg = p.pages + (size_t)pid_tc * (size_t)p.page_bytes;
+        store_codes_lane<EPL>(pg + g.off_k + idx * g.k_row, q, g.kbits, pk);
+        store_codes_lane<EPL>(pg + g.off_v + idx * g.v_row, q, g.vbits, pv);
+        if (q == 0) *reinterpret_cast<uint32_t*>(pg + g.off_kmeta + 4 * idx) = mk;
+        if (q == 1) *reinterpret_cast<uint32_t*>(pg + g.off_vmeta + 4 * idx) = mv;
+        if (q == 2) *reinterpret_cast<float*>(pg + g.off_score + 4 * idx) = canon_zero(s_in);
+        if (q == 3) *reinterpret_cast<int32_t*>(pg + g.off_pos + 4 * idx) = pc;
+      }
+    }
+    // 3. window push, after t_c's row has been consumed
+    if (wk_row != nullptr) {
+      store_hvec<EPL>(wk_row, q, lds_hvec<EPL>(my_nk));
+      store_hvec<EPL>(wv_row, q, lds_hvec<EPL>(my_nv));
     }
   }
 }
@@ -124,20 +386,27 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
 template <int D, int G>
 static cudaError_t launch_qd(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
                              const float* sig, cudaStream_t s) {
-  const int units_per_cta = kQDWarps * (32 / G);
-  const int grid = (p.U + units_per_cta - 1) / units_per_cta;
-  quant_decode_kernel<D, G><<<grid, kQDWarps * 32, 0, s>>>(p, dec, k, v, sig);
+  constexpr int units_per_cta = kQDThreads / G;
+  const size_t smem = req_cache_bytes(p.R);
+  static int cap = 0;                                    // persistent grid (per template instance)
+  if (cap == 0) cap = persistent_grid(quant_decode_kernel<D, G>, kQDThreads, req_cache_bytes(kReqSmemMax));
+  if (cap == 0) return cudaErrorUnknown;
+  const int need = (p.U + units_per_cta - 1) / units_per_cta;
+  quant_decode_kernel<D, G><<<need < cap ? need : cap, kQDThreads, smem, s>>>(p, dec, k, v, sig);
   return cudaGetLastError();
 }
 
 cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
                                 const float* sig, cudaStream_t s) {
-  static const int g = getenv("DKV_QD_G") ? atoi(getenv("DKV_QD_G")) : 4;   // tuning knob
+  static const int g = getenv("DKV_QD_G") ? atoi(getenv("DKV_QD_G")) : 8;   // lanes per unit (tuning knob)
   if (p.d == 128) {
-    if (g == 16) return launch_qd<128, 16>(p, dec, k, v, sig, s);
-    return g == 4 ? launch_qd<128, 4>(p, dec, k, v, sig, s) : launch_qd<128, 8>(p, dec, k, v, sig, s);
+    if (g == 32) return launch_qd<128, 32>(p, dec, k, v, sig, s);
+    if (g == 8) return launch_qd<128, 8>(p, dec, k, v, sig, s);
+    return launch_qd<128, 16>(p, dec, k, v, sig, s);
   }
-  return g == 4 ? launch_qd<64, 4>(p, dec, k, v, sig, s) : launch_qd<64, 8>(p, dec, k, v, sig, s);
+  if (g == 16) return launch_qd<64, 16>(p, dec, k, v, sig, s);
+  if (g == 4) return launch_qd<64, 4>(p, dec, k, v, sig, s);
+  return launch_qd<64, 8>(p, dec, k, v, sig, s);
 }
 
 }  // namespace dkv

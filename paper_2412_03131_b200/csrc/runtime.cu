@@ -173,6 +173,15 @@ dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_
   const int cores = compact_max_coresident(G.tile_units);
   if (cores <= 0) return DKV_ERR_CUDA;
   if (G.num_tiles > cores) return DKV_ERR_INVALID_ARG;   // the scan's grid barrier needs co-residency
+  {
+    // multiply-high division constants, checked over every dividend a kernel can pass (unreachable failure)
+    const int32_t LyH = cfg->num_layers * cfg->num_kv_heads;
+    if (!fastdiv_check(make_fastdiv(LyH), G.U) ||
+        !fastdiv_check(make_fastdiv(cfg->window > 0 ? cfg->window : 1), (int64_t)cfg->max_seq_len + 1) ||
+        !fastdiv_check(make_fastdiv(cfg->page_tokens_high), (int64_t)G.L * cfg->page_tokens_high) ||
+        !fastdiv_check(make_fastdiv(cfg->page_tokens_low), (int64_t)G.L * cfg->page_tokens_low))
+      return DKV_ERR_INVALID_ARG;
+  }
   dkv_pool* p = new dkv_pool();
   p->cfg = *cfg;
   p->G = G;
@@ -197,6 +206,10 @@ dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_
   d.prompt_den = cfg->prompt_denominator; d.num_tiles = G.num_tiles; d.tile_units = G.tile_units; d.nseg = G.nseg;
   d.alpha_h = cfg->alpha_h; d.alpha_l = cfg->alpha_l;
   for (int k = 0; k < 3; k++) d.g[k] = G.g[k];
+  d.div_LyH = make_fastdiv(d.LyH);
+  d.div_W = make_fastdiv(d.W > 0 ? d.W : 1);
+  d.div_Ch = make_fastdiv(d.Ch);
+  d.div_Cl = make_fastdiv(d.Cl);
   uint8_t* b = p->base;
   d.ctrl = (Ctrl*)(b + Lo.off_ctrl);
   d.stats = (int64_t*)(b + Lo.off_stats);
