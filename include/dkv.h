@@ -84,7 +84,14 @@ typedef struct {
   float   alpha_h, alpha_l;    /* thresholds (calibrated values P:702-703) */
   int32_t prompt_denominator;  /* Q4: 0 = 1-indexed position i; 1 = prompt length n */
   int32_t tile_units;          /* scan tile (units per CTA): 0 = default 1024; 256, 512 or 1024 */
-  int32_t reserved[2];         /* must be zero */
+  int32_t prefill_workflow;    /* prompt-phase allocation: 0 = exact (plan, then allocate ceil(n_h/C_h) +
+                                  ceil(n_l/C_l) pages per head); 1 = the paper's workflow (Fig. 5):
+                                  allocate ceil(kept/C_h) pages per head "assuming all tokens are stored at
+                                  high precision", plan, keep high pages from the left and low pages from
+                                  the right of each head's block, reclaim the middle at the end pointer
+                                  (one extra page when the plan needs it, reading Q29).  Same final
+                                  classes, counts and page bytes; different page IDs and ring order. */
+  int32_t reserved[1];         /* must be zero */
 } dkv_config_t;
 
 /* 16-byte per-unit decision written by dkv_classify(DECODE); padding-free, compared byte for byte.
@@ -114,6 +121,7 @@ typedef struct {
           off_stats;
   int32_t units, table_len, page_bytes, num_tiles, tile_units, seg_tokens, num_segs;
   int32_t C[3], k_row[3], v_row[3], off_k[3], off_kmeta[3], off_v[3], off_vmeta[3], off_score[3], off_pos[3];
+  int64_t off_tile_sums;       /* int64[num_tiles][3] scratch of the prompt workflow's scans */
 } dkv_layout_t;
 
 /* Arena size for `cfg`, or 0 if the configuration is invalid. */
@@ -146,7 +154,8 @@ dkv_status_t dkv_classify(dkv_pool_t p, int32_t phase, const int32_t* h_req, con
 /* Coordination.  Recycles every PENDING_FREE request (its pages go to the ring at end = start + free in
  * canonical order, Q13; the request becomes IDLE), then grants the demand of the most recent dkv_classify
  * all-or-nothing (Q15): decode demand from d_dec (device, as written by dkv_classify(DECODE)); prefill
- * demand ceil(n_h/C_h) + ceil(n_l/C_l) from pool scratch (d_dec may be NULL).  Writes the bidirectional
+ * demand ceil(n_h/C_h) + ceil(n_l/C_l) from pool scratch (d_dec may be NULL), or with prefill_workflow = 1
+ * the conservative block ceil(kept/C_h) (+1, Q29) whose unused middle is reclaimed in the same call.  Writes the bidirectional
  * tables (high left-to-right, low right-to-left) and counts, advances start/free.  On OOM: sticky
  * DKV_ERR_OOM, allocation state unchanged, recycling applied.  May be re-issued with the same d_dec
  * after an OOM (only ACTIVE / ADMITTING requests take part). */

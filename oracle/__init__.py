@@ -61,7 +61,8 @@ def build(force: bool = False) -> str:
 
 class Config(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("R", "Ly", "H", "d", "M", "W", "Ch", "Cl", "kbh", "vbh", "kbl", "vbl", "P")] + \
-               [("alpha_h", C.c_float), ("alpha_l", C.c_float), ("prompt_denominator", C.c_int32)]
+               [("alpha_h", C.c_float), ("alpha_l", C.c_float), ("prompt_denominator", C.c_int32),
+                ("prefill_workflow", C.c_int32)]
 
 
 class ClassGeom(C.Structure):
@@ -80,7 +81,8 @@ class _Pool(C.Structure):
                 ("pf_nh", C.POINTER(C.c_int32)), ("pf_nl", C.POINTER(C.c_int32)),
                 ("admit_list", C.POINTER(C.c_int32)), ("n_admit", C.c_int32),
                 ("status", C.c_int32), ("last_phase", C.c_int32),
-                ("last_demand", C.c_int64), ("last_freed", C.c_int64), ("oom_count", C.c_int32)]
+                ("last_demand", C.c_int64), ("last_freed", C.c_int64), ("oom_count", C.c_int32),
+                ("last_reclaimed", C.c_int64)]
 
 
 _lib = None
@@ -166,7 +168,7 @@ def unpack_codes(codes, d: int, bits: int) -> np.ndarray:
 
 def make_config(**kw) -> Config:
     defaults = dict(R=4, Ly=2, H=4, d=64, M=128, W=16, Ch=16, Cl=32, kbh=8, vbh=4, kbl=4, vbl=2, P=1024,
-                    alpha_h=1.0, alpha_l=0.02, prompt_denominator=0)
+                    alpha_h=1.0, alpha_l=0.02, prompt_denominator=0, prefill_workflow=0)
     defaults.update(kw)
     return Config(**defaults)
 
@@ -253,6 +255,10 @@ class OraclePool:
     @property
     def oom_count(self):
         return self._p.contents.oom_count
+
+    @property
+    def last_reclaimed(self):
+        return self._p.contents.last_reclaimed
 
     def take_status(self) -> int:
         return lib().orc_take_status(self._p)

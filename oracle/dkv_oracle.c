@@ -161,7 +161,8 @@ int32_t orc_geometry(const orc_config* c, int32_t* U, int32_t* L, int32_t* page_
   if (c->R < 1 || c->Ly < 1 || c->H < 1 || c->d < 8 || c->d % 8 || c->M < 1 || c->W < 0 ||
       c->Ch < 1 || c->Cl < c->Ch || c->P < 1 || !bits_ok(c->kbh) || !bits_ok(c->vbh) ||
       !bits_ok(c->kbl) || !bits_ok(c->vbl) || !isfinite(c->alpha_h) || !isfinite(c->alpha_l) ||
-      c->alpha_h < 0 || c->alpha_l < 0 || (c->prompt_denominator != 0 && c->prompt_denominator != 1))
+      c->alpha_h < 0 || c->alpha_l < 0 || (c->prompt_denominator != 0 && c->prompt_denominator != 1) ||
+      (c->prefill_workflow != 0 && c->prefill_workflow != 1))
     return ORC_ERR_INVALID;
   orc_class_geom gh, gl;
   class_geom(c->d, c->Ch, c->kbh, c->vbh, &gh);
@@ -418,6 +419,63 @@ int32_t orc_classify_prefill(orc_pool* p, const int32_t* req, const int32_t* len
 }
 
 /* ------------------------------------------------------------------------------------------------
+ * The paper's prompt workflow (NEXT-1, fig:memory_management_flow), selected by
+ * prefill_workflow = 1.  "Memory pages are conservatively allocated for each head, assuming all tokens
+ * are stored at high precision": c_u = ceil(kept/C_h) pages, kept = prompt tokens outside the
+ * window; "the end pointer advances", i.e. the allocation pointer (Q1).  Then "the planning phase
+ * determines ... high-precision and low-precision pages", and each head keeps its high pages
+ * from the left and its low pages from the right of its block while the pages in between are reclaimed
+ * "via a parallel prefix-sum operation" and appended at the end pointer.
+ * Q29 (the paper is silent): with C_l >= C_h, ceil(n_h/C_h) + ceil(n_l/C_l) can exceed c_u by one page
+ * (e.g. one high and one low token in a 16-token block); such a head keeps its whole block and takes one
+ * more page, granted from the start pointer after every conservative block (a second exclusive scan in
+ * canonical order).  Blocks and top-ups are one all-or-nothing allocation (Q15).
+ * ----------------------------------------------------------------------------------------------*/
+static int32_t conservative_pages(const orc_pool* p, int32_t u) {
+  const orc_config* c = &p->c;
+  int32_t r = u / (c->Ly * c->H);
+  int32_t kept = p->prompt_len[r] - c->W > 0 ? p->prompt_len[r] - c->W : 0;
+  return ceil_div(kept, c->Ch);
+}
+static int32_t topup_pages(const orc_pool* p, int32_t u) {
+  const orc_config* c = &p->c;
+  int32_t need = ceil_div(p->pf_nh[u], c->Ch) + ceil_div(p->pf_nl[u], c->Cl);
+  return need > conservative_pages(p, u) ? 1 : 0;
+}
+/* grants D = sum(c_u) + sum(e_u) pages from ring[start..), writes the final tables and appends the
+ * reclaimed middles at end = start + free (before this allocation); sets p->last_reclaimed */
+static void prefill_conservative_grant(orc_pool* p, int64_t D) {
+  const orc_config* c = &p->c;
+  int32_t LyH = c->Ly * c->H, L = p->L, P = c->P;
+  int64_t end = (p->start + p->free) % P;
+  int64_t sum_c = 0;
+  for (int32_t u = 0; u < p->U; u++)
+    if (p->req_state[u / LyH] == ORC_REQ_ADMITTING) sum_c += conservative_pages(p, u);
+  int64_t off_c = 0, off_e = 0, off_m = 0;
+  for (int32_t u = 0; u < p->U; u++) {
+    if (p->req_state[u / LyH] != ORC_REQ_ADMITTING) continue;
+    int32_t* row = &p->table[(size_t)u * L];
+    int32_t cu = conservative_pages(p, u), eu = topup_pages(p, u);
+    int32_t ph = ceil_div(p->pf_nh[u], c->Ch), pl = ceil_div(p->pf_nl[u], c->Cl);
+    if (ph + pl > L) { set_status(p, ORC_ERR_OVERFLOW); off_c += cu; off_e += eu; continue; }
+    /* block'[k]: the conservative block (scan 1), then the top-up page (scan 2) */
+    int64_t base_c = p->start + off_c, pos_e = p->start + sum_c + off_e;
+    int32_t nb = cu + eu;
+#define BLOCK(k) p->ring[((k) < cu ? base_c + (k) : pos_e) % P]
+    for (int32_t k = 0; k < ph; k++) row[k] = BLOCK(k);                  /* high: left to right */
+    for (int32_t k = 0; k < pl; k++) row[L - 1 - k] = BLOCK(nb - 1 - k);  /* low: right to left */
+    for (int32_t k = ph; k < nb - pl; k++) {                             /* reclaim the middle (scan 3) */
+      p->ring[(end + off_m) % P] = BLOCK(k);
+      off_m += 1;
+    }
+#undef BLOCK
+    off_c += cu; off_e += eu;
+  }
+  (void)D;
+  p->last_reclaimed = off_m;
+}
+
+/* ------------------------------------------------------------------------------------------------
  * Coordination (c.3).  P:485-488: "after each head determines the number of pages to be allocated or
  * freed, a parallel prefix sum ... computes a unique offset for each head relative to the start or end
  * pointer ... For memory allocation, each head concurrently retrieves its new page IDs from its
@@ -460,10 +518,12 @@ int32_t orc_compact_alloc(orc_pool* p, const orc_decision* dec) {
     if (p->last_phase == ORC_DECODE) {
       if (p->req_state[r] == ORC_REQ_ACTIVE) D += dec[u].demand;
     } else if (p->req_state[r] == ORC_REQ_ADMITTING) {
-      D += ceil_div(p->pf_nh[u], c->Ch) + ceil_div(p->pf_nl[u], c->Cl);
+      if (c->prefill_workflow == 1) D += conservative_pages(p, u) + topup_pages(p, u);
+      else D += ceil_div(p->pf_nh[u], c->Ch) + ceil_div(p->pf_nl[u], c->Cl);
     }
   }
   p->last_demand = D;
+  p->last_reclaimed = 0;
   if (D > p->free) { set_status(p, ORC_ERR_OOM); p->oom_count++; return ORC_OK; }
   /* 3. grant in canonical order; high IDs left-to-right, low IDs right-to-left */
   int64_t off = 0;
@@ -477,7 +537,7 @@ int32_t orc_compact_alloc(orc_pool* p, const orc_decision* dec) {
       int32_t k = (dec[u].grow == ORC_GROW_HIGH) ? p->n_h[u] / c->Ch : L - 1 - p->n_l[u] / c->Cl;
       row[k] = p->ring[(p->start + off) % P];
       off += 1;
-    } else {
+    } else if (c->prefill_workflow == 0) {
       if (p->req_state[r] != ORC_REQ_ADMITTING) continue;
       int32_t ph = ceil_div(p->pf_nh[u], c->Ch), pl = ceil_div(p->pf_nl[u], c->Cl);
       if (ph + pl > L) { set_status(p, ORC_ERR_OVERFLOW); off += ph + pl; continue; }
@@ -485,8 +545,10 @@ int32_t orc_compact_alloc(orc_pool* p, const orc_decision* dec) {
       for (int32_t k = 0; k < pl; k++) { row[L - 1 - k] = p->ring[(p->start + off) % P]; off += 1; }
     }
   }
+  if (p->last_phase == ORC_PREFILL && c->prefill_workflow == 1) prefill_conservative_grant(p, D);
   p->start = (p->start + D) % P;
   p->free -= D;
+  if (p->last_phase == ORC_PREFILL && c->prefill_workflow == 1) p->free += p->last_reclaimed;
   /* 4. counts (a5) and the request length */
   for (int32_t u = 0; u < p->U; u++) {
     int32_t r = u / LyH;
@@ -600,60 +662,22 @@ int32_t orc_free(orc_pool* p, const int32_t* req, int32_t n) {
 }
 
 /* ------------------------------------------------------------------------------------------------
- * NEXT-1, the paper's prompt workflow (Fig. 5): "conservatively allocate ... assuming all
- * tokens are stored at high precision" (ceil((n-W)/C_h) pages per head into slots 0..c-1), then the
- * planning phase, then keep high pages left-to-right and low pages right-to-left, and "reclaim unused
- * pages ... via a parallel prefix-sum" appended at the end pointer.  The plan's low pages are the last
- * pl pages of the conservative block, moved to the right end of the table (a no-op when c == L, as in
- * Fig. 5); the reclaimed middle is slots [ph, c - pl).  Returns ORC_ERR_OVERFLOW if ph + pl > c.
+ * NEXT-1 convenience entry point (used by the Fig. 5 replay): admit + plan + compact with
+ * prefill_workflow = 1 for this call only; reclaimed_out receives the reclaimed IDs in ring order.
  * ----------------------------------------------------------------------------------------------*/
 int32_t orc_prefill_conservative(orc_pool* p, const int32_t* req, const int32_t* len, int32_t n,
                                  const float* sig, int64_t sig_stride, int32_t* reclaimed_out, int64_t* n_reclaimed) {
-  const orc_config* c = &p->c;
-  int32_t LyH = c->Ly * c->H, L = p->L, P = c->P;
+  int32_t saved = p->c.prefill_workflow;
+  int64_t end = (p->start + p->free) % p->c.P;
   int32_t st = orc_classify_prefill(p, req, len, n, sig, sig_stride, NULL);
+  if (st == ORC_OK) {
+    p->c.prefill_workflow = 1;
+    st = orc_compact_alloc(p, NULL);
+    p->c.prefill_workflow = saved;
+  }
   if (st != ORC_OK) return st;
-  /* conservative allocation */
-  int64_t D = 0;
-  for (int32_t i = 0; i < n; i++) {
-    int32_t kept = len[i] - c->W > 0 ? len[i] - c->W : 0;
-    D += (int64_t)LyH * ceil_div(kept, c->Ch);
-  }
-  if (D > p->free) { set_status(p, ORC_ERR_OOM); return ORC_OK; }
-  int64_t off = 0;
-  for (int32_t i = 0; i < n; i++) {
-    int32_t kept = len[i] - c->W > 0 ? len[i] - c->W : 0, cc = ceil_div(kept, c->Ch);
-    if (cc > L) return ORC_ERR_OVERFLOW;
-    for (int32_t j = 0; j < LyH; j++)
-      for (int32_t k = 0; k < cc; k++) { p->table[(size_t)(req[i] * LyH + j) * L + k] = p->ring[(p->start + off) % P]; off++; }
-  }
-  p->start = (p->start + D) % P;
-  p->free -= D;
-  /* planning result -> keep left ph, move last pl to the right end, reclaim the middle */
-  int64_t nr = 0;
-  for (int32_t i = 0; i < n; i++) {
-    int32_t kept = len[i] - c->W > 0 ? len[i] - c->W : 0, cc = ceil_div(kept, c->Ch);
-    for (int32_t j = 0; j < LyH; j++) {
-      int32_t u = req[i] * LyH + j;
-      int32_t* row = &p->table[(size_t)u * L];
-      int32_t ph = ceil_div(p->pf_nh[u], c->Ch), pl = ceil_div(p->pf_nl[u], c->Cl);
-      if (ph + pl > cc) return ORC_ERR_OVERFLOW;
-      int32_t lows[64];
-      if (pl > 64) return ORC_ERR_INVALID;                                  /* oracle-level helper bound */
-      for (int32_t k = 0; k < pl; k++) lows[k] = row[cc - 1 - k];         /* k-th low page */
-      for (int32_t k = ph; k < cc - pl; k++) {
-        p->ring[(p->start + p->free) % P] = row[k];
-        if (reclaimed_out) reclaimed_out[nr] = row[k];
-        p->free += 1; nr++;
-      }
-      for (int32_t k = ph; k < cc; k++) row[k] = -1;
-      for (int32_t k = 0; k < pl; k++) row[L - 1 - k] = lows[k];
-      p->n_h[u] = p->pf_nh[u];
-      p->n_l[u] = p->pf_nl[u];
-    }
-    p->seq_len[req[i]] = len[i];
-  }
-  if (n_reclaimed) *n_reclaimed = nr;
-  p->last_phase = ORC_PREFILL;
+  for (int64_t k = 0; k < p->last_reclaimed; k++)
+    if (reclaimed_out) reclaimed_out[k] = p->ring[(end + k) % p->c.P];
+  if (n_reclaimed) *n_reclaimed = p->last_reclaimed;
   return ORC_OK;
 }

@@ -36,6 +36,8 @@ typedef struct {
   int32_t P;                    /* pages in the pool */
   float alpha_h, alpha_l;       /* thresholds */
   int32_t prompt_denominator;   /* Q4: 0 = 1-indexed position i, 1 = prompt length n */
+  int32_t prefill_workflow;     /* 0 = exact allocation after planning; 1 = the paper's prompt workflow
+                                   (Fig. 5): conservative allocation, planning, reclaim (Q29) */
 } orc_config;
 
 /* 16-byte decision record per unit (same byte layout the product's ABI documents). */
@@ -67,6 +69,7 @@ typedef struct orc_pool {
   int32_t status;                           /* sticky device-style status, first error wins */
   int32_t last_phase;                       /* phase of the most recent classify */
   int64_t last_demand, last_freed; int32_t oom_count;
+  int64_t last_reclaimed;                   /* prefill_workflow 1: middle pages reclaimed by the last call */
 } orc_pool;
 
 /* --- scalar primitives (exported for the pins) --- */
@@ -95,8 +98,8 @@ int32_t   orc_quant_write_prefill(orc_pool* p, const uint16_t* k, const uint16_t
                                   const float* sig, int64_t sig_stride);
 int32_t   orc_free(orc_pool* p, const int32_t* req, int32_t n);
 int32_t   orc_take_status(orc_pool* p);     /* returns and clears the sticky status */
-/* NEXT-1 (Fig. 5): conservative prompt allocation then reclaim of the unused middle
-   slots; used at oracle level to replay the paper's worked example. */
+/* NEXT-1 (Fig. 5): admit + plan + compact with prefill_workflow = 1 for this call (the
+   pool's own setting is restored); reclaimed_out receives the reclaimed page IDs in ring order. */
 int32_t   orc_prefill_conservative(orc_pool* p, const int32_t* req, const int32_t* len, int32_t n,
                                    const float* sig, int64_t sig_stride, int32_t* reclaimed_out, int64_t* n_reclaimed);
 

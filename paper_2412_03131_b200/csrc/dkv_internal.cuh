@@ -87,6 +87,8 @@ struct PoolDev {
   uint8_t* pages;
   int64_t* stats;       // int64[4] admission counters
   FastDiv div_LyH, div_W, div_Ch, div_Cl;   // u -> request, position -> window slot, slot -> (page, index)
+  int64_t* tile_sums;   // [num_tiles][3] prompt-workflow scan scratch
+  int32_t prefill_wf;   // dkv_config_t.prefill_workflow
 };
 
 // ------------------------------------------------------------------------------------- memory ops
@@ -835,7 +837,9 @@ cudaError_t launch_clear_status(const PoolDev& p, cudaStream_t s);
 cudaError_t launch_classify_decode(const PoolDev& p, const float* sig, dkv_decision_t* dec, cudaStream_t s);
 cudaError_t launch_classify_prefill(const PoolDev& p, int n, const float* sig, int64_t sig_stride, uint8_t* cls,
                                     int max_len, cudaStream_t s);
-cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s);
+cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s,
+                                 bool alloc = true);
+cudaError_t launch_prefill_conservative(const PoolDev& p, cudaStream_t s);
 cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
                                 const float* sig, cudaStream_t s);
 cudaError_t launch_quant_prefill(const PoolDev& p, int n, const uint16_t* k, const uint16_t* v, int64_t kv_stride,

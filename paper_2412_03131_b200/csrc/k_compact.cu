@@ -45,7 +45,7 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 }
 
 template <int TU>
-__global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, int phase) {
+__global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, int phase, int alloc) {
   constexpr int NW = TU / 32;
   __shared__ unsigned long long s_epoch;
   __shared__ int64_t s_start0, s_free0, s_D, s_F;
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
           dem = dword >> 24;
           grow = (dword >> 16) & 0xFF;
         }
-      } else if (st == DKV_REQ_ADMITTING) {
+      } else if (st == DKV_REQ_ADMITTING && alloc) {
         dem = ceil_div(pfh, p.Ch) + ceil_div(pfl, p.Cl);
       }
     }
@@ -193,7 +193,11 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
             if (k < nfr) {
               const int slot = k < ph ? k : L - nfr + k;
               p.ring[(end0 + off + k) % P] = pid[j];
-              row[slot] = -1;
+              // clear the slot only once its load has returned: a store issued while the same line's load
+              // miss is outstanding takes a slow path in L2 (see k_quant_decode.cu)
+              int32_t empty = -1;
+              asm volatile("" : "+r"(empty) : "r"(pid[j]));
+              row[slot] = empty;
             }
           }
         }
@@ -265,7 +269,7 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
           row[slot] = __ldcg(p.ring + (start0 + off + k) % P);
         }
       }
-      if (st == DKV_REQ_ADMITTING) { p.n_h[u] = p.pf_nh[u]; p.n_l[u] = p.pf_nl[u]; }
+      if (st == DKV_REQ_ADMITTING && alloc) { p.n_h[u] = p.pf_nh[u]; p.n_l[u] = p.pf_nl[u]; }
     }
   }
   // ---- request-level transitions, by the tile owning the request's LAST unit: every other tile holding
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
       p.req_state[r] = DKV_REQ_IDLE; p.seq_len[r] = 0; p.prompt_len[r] = 0;
     } else if (ok && phase == DKV_PHASE_DECODE && st == DKV_REQ_ACTIVE) {
       p.seq_len[r] += 1;
-    } else if (ok && phase == DKV_PHASE_PREFILL && st == DKV_REQ_ADMITTING) {
+    } else if (ok && alloc && phase == DKV_PHASE_PREFILL && st == DKV_REQ_ADMITTING) {
       p.seq_len[r] = p.prompt_len[r];
     }
   }
@@ -301,7 +305,7 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
 }
 
 template <int TU>
-static cudaError_t launch_tu(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s) {
+static cudaError_t launch_tu(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s, int alloc) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.num_tiles);
   cfg.blockDim = dim3(TU);
@@ -313,14 +317,14 @@ static cudaError_t launch_tu(const PoolDev& p, const dkv_decision_t* dec, int ph
   static const int coop = getenv("DKV_COMPACT_COOP") ? atoi(getenv("DKV_COMPACT_COOP")) : 1;   // tuning knob
   cfg.attrs = attr;
   cfg.numAttrs = coop ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, compact_alloc_kernel<TU>, p, dec, phase);
+  return cudaLaunchKernelEx(&cfg, compact_alloc_kernel<TU>, p, dec, phase, alloc);
 }
 
-cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s) {
+cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s, bool alloc) {
   switch (p.tile_units) {
-    case 256: return launch_tu<256>(p, dec, phase, s);
-    case 512: return launch_tu<512>(p, dec, phase, s);
-    default: return launch_tu<1024>(p, dec, phase, s);
+    case 256: return launch_tu<256>(p, dec, phase, s, alloc ? 1 : 0);
+    case 512: return launch_tu<512>(p, dec, phase, s, alloc ? 1 : 0);
+    default: return launch_tu<1024>(p, dec, phase, s, alloc ? 1 : 0);
   }
 }
 

@@ -50,7 +50,8 @@ bool validate(const dkv_config_t* c, Geometry& G) {
   if (!(c->alpha_h >= 0.0f && c->alpha_h <= 3.0e38f) || !(c->alpha_l >= 0.0f && c->alpha_l <= 3.0e38f)) return false;
   if (c->prompt_denominator != 0 && c->prompt_denominator != 1) return false;
   if (c->tile_units != 0 && c->tile_units != 256 && c->tile_units != 512 && c->tile_units != 1024) return false;
-  if (c->reserved[0] || c->reserved[1]) return false;
+  if (c->prefill_workflow != 0 && c->prefill_workflow != 1) return false;
+  if (c->reserved[0]) return false;
   const int64_t U = (int64_t)c->max_requests * c->num_layers * c->num_kv_heads;
   if (U >= (1 << 24)) return false;
   G.U = (int32_t)U;
@@ -77,6 +78,7 @@ bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
   Lo.off_ctrl = take(256);
   Lo.off_stats = take(32);
   Lo.off_tile_status = take(8 * (int64_t)G.num_tiles);
+  Lo.off_tile_sums = take(24 * (int64_t)G.num_tiles);
   Lo.off_ring = take(4 * P);
   Lo.off_table = take(4 * U * G.L);
   Lo.off_n_h = take(4 * U);
@@ -214,6 +216,8 @@ dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_
   d.ctrl = (Ctrl*)(b + Lo.off_ctrl);
   d.stats = (int64_t*)(b + Lo.off_stats);
   d.tile_status = (unsigned long long*)(b + Lo.off_tile_status);
+  d.tile_sums = (int64_t*)(b + Lo.off_tile_sums);
+  d.prefill_wf = cfg->prefill_workflow;
   d.ring = (int32_t*)(b + Lo.off_ring);
   d.table = (int32_t*)(b + Lo.off_table);
   d.n_h = (int32_t*)(b + Lo.off_n_h);
@@ -292,7 +296,14 @@ dkv_status_t dkv_compact_alloc(dkv_pool_t p, const dkv_decision_t* d_dec, dkv_st
   if (!p) return DKV_ERR_INVALID_ARG;
   if (p->seq == SEQ_IDLE && !p->recovering) return DKV_ERR_STATE;
   if (p->phase == DKV_PHASE_DECODE && !d_dec) return DKV_ERR_INVALID_ARG;
-  cudaError_t e = launch_compact_alloc(p->dev, d_dec, p->phase, (cudaStream_t)s);
+  cudaError_t e;
+  if (p->phase == DKV_PHASE_PREFILL && p->cfg.prefill_workflow == 1) {
+    // the paper's prompt workflow: recycle (no allocation), then conservative blocks + reclaim
+    e = launch_compact_alloc(p->dev, d_dec, p->phase, (cudaStream_t)s, /*alloc=*/false);
+    if (e == cudaSuccess) e = launch_prefill_conservative(p->dev, (cudaStream_t)s);
+  } else {
+    e = launch_compact_alloc(p->dev, d_dec, p->phase, (cudaStream_t)s, /*alloc=*/true);
+  }
   if (e != cudaSuccess) return DKV_ERR_CUDA;
   const int R = p->cfg.max_requests;
   for (int r = 0; r < R; r++) {

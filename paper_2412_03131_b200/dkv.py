@@ -40,7 +40,7 @@ class dkv_config_t(C.Structure):
         "max_requests", "num_layers", "num_kv_heads", "head_dim", "max_seq_len", "window", "page_tokens_high",
         "page_tokens_low", "kbits_high", "vbits_high", "kbits_low", "vbits_low", "num_pages")] + \
         [("alpha_h", C.c_float), ("alpha_l", C.c_float), ("prompt_denominator", C.c_int32),
-         ("tile_units", C.c_int32), ("reserved", C.c_int32 * 2)]
+         ("tile_units", C.c_int32), ("prefill_workflow", C.c_int32), ("reserved", C.c_int32 * 1)]
 
 
 class dkv_decision_t(C.Structure):
@@ -61,7 +61,7 @@ class dkv_layout_t(C.Structure):
         "off_win_v", "off_pages", "off_stats")] + [(n, C.c_int32) for n in (
         "units", "table_len", "page_bytes", "num_tiles", "tile_units", "seg_tokens", "num_segs")] + \
         [(n, C.c_int32 * 3) for n in ("C", "k_row", "v_row", "off_k", "off_kmeta", "off_v", "off_vmeta",
-                                       "off_score", "off_pos")]
+                                       "off_score", "off_pos")] + [("off_tile_sums", C.c_int64)]
 
 
 assert C.sizeof(dkv_decision_t) == 16
@@ -200,9 +200,10 @@ def dkv_status_string(st) -> str:
 
 
 def make_config(R, Ly, H, d, M, W, Ch=16, Cl=32, kbh=8, vbh=4, kbl=4, vbl=2, P=1024, alpha_h=1.0, alpha_l=0.02,
-                prompt_denominator=0, tile_units=0) -> dkv_config_t:
+                prompt_denominator=0, tile_units=0, prefill_workflow=0) -> dkv_config_t:
     c = dkv_config_t(max_requests=R, num_layers=Ly, num_kv_heads=H, head_dim=d, max_seq_len=M, window=W,
                      page_tokens_high=Ch, page_tokens_low=Cl, kbits_high=kbh, vbits_high=vbh, kbits_low=kbl,
                      vbits_low=vbl, num_pages=P, alpha_h=alpha_h, alpha_l=alpha_l,
-                     prompt_denominator=prompt_denominator, tile_units=tile_units)
+                     prompt_denominator=prompt_denominator, tile_units=tile_units,
+                     prefill_workflow=prefill_workflow)
     return c

@@ -15,7 +15,8 @@ class GpuBackend:
     def __init__(self, scn, device="cuda"):
         self.scn = scn
         cfg = D.make_config(scn.R, scn.Ly, scn.H, scn.d, scn.M, scn.W, scn.Ch, scn.Cl, scn.kbh, scn.vbh, scn.kbl,
-                            scn.vbl, scn.P, scn.alpha_h, scn.alpha_l, scn.prompt_denominator, scn.tile_units)
+                            scn.vbl, scn.P, scn.alpha_h, scn.alpha_l, scn.prompt_denominator, scn.tile_units,
+                            scn.prefill_workflow)
         self.pool = Pool(cfg, device=device)
         self.U, self.L, self.page_bytes = self.pool.U, self.pool.L, self.pool.page_bytes
         self.v = self.pool.views()

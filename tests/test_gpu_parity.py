@@ -92,3 +92,62 @@ def test_tile_size_determinism():
     from tests.gpu_backend import compare_state
     compare_state(snaps[0], snaps[1], where="256 vs 512")
     compare_state(snaps[0], snaps[2], where="256 vs 1024")
+
+
+# ---------------------------------------------------------------- NEXT-1: the paper's prompt workflow
+@pytest.mark.parametrize("tile_units", [256, 1024])
+def test_prompt_workflow_parity(tile_units):
+    # prefill_workflow = 1: conservative blocks, top-ups (Q29), reclaimed middles — ring,
+    # pointers, tables, counts and page bytes bit-exact with the oracle after every call, across several
+    # scan tiles with a ragged tail, frees and re-admission
+    scn = H.TINY.replace(R=7, Ly=5, H=40, d=128, M=1100, W=64, P=60000, seed=23, tile_units=tile_units,
+                         prefill_workflow=1)
+    lens = [300, 64, 517, 40, 0, 1000, 129]
+    _lifecycle(scn, steps=24, prompt_lens=lens, frees=[(7, [0, 2]), (15, [5])], readmit_len=260, pages_every=5)
+
+
+def test_prompt_workflow_tiny_and_wraparound():
+    # the free region ends at the allocation pointer (fresh pool): reclaimed middles wrap onto granted ring
+    # slots, which the kernel must read before the reclaim writes land (second grid barrier)
+    scn = H.TINY.replace(prefill_workflow=1, P=700)
+    _lifecycle(scn, steps=40, prompt_lens=[64, 64, 64, 64], frees=[(20, [1, 3])], readmit_len=48)
+
+
+def test_fig5_on_gpu():
+    """PIN-1 at GPU level: Fig. 5 (P:521-529) with every token doubled (4-token high / 8-token low pages;
+    the CUDA geometry needs C % 4 == 0) — pages 5-8 -> head A, 9-12 -> head B, A keeps 5 + 8, B keeps
+    9, 10 + 12, pages 6, 7, 11 reclaimed at the end pointer, which wraps to the head of the list."""
+    import json
+    import os
+    from paper_2412_03131_b200 import Pool
+    from paper_2412_03131_b200 import dkv as D
+    with open(os.path.join(os.path.dirname(__file__), "golden", "fig5.json")) as f:
+        g = json.load(f)
+    cfg = D.make_config(R=1, Ly=1, H=2, d=64, M=16, W=0, Ch=4, Cl=8, P=16, alpha_h=1.0, alpha_l=0.02,
+                        prefill_workflow=1)
+    pool = Pool(cfg, device="cuda")
+    v = pool.views()
+    v["ctrl"][0] = g["initial"]["start"]                  # pages 0-4 held outside the example (as in Fig. 5)
+    v["ctrl"][1] = g["initial"]["free"]
+    torch.cuda.synchronize()
+    n0 = g["prompt_len"]
+    sig = np.repeat(np.array(g["sig"], np.float32), 2, axis=1)
+    i = np.arange(1, 2 * n0 + 1, dtype=np.float32)
+    base = np.repeat(np.arange(1, n0 + 1, dtype=np.float32), 2)
+    sig = (sig * (base / i)).astype(np.float32).reshape(1, 2, 2 * n0)   # each token keeps its Fig. 5 class
+    pool.classify_prefill([0], [2 * n0], torch.from_numpy(sig).cuda())
+    pool.compact_alloc(None)
+    st, stats = pool.query()
+    assert st == 0
+    e = g["expect"]
+    table = v["table"].cpu().numpy()
+    L = table.shape[1]
+    for head, u in (("A", 0), ("B", 1)):
+        assert list(table[u, :len(e["high_pages"][head])]) == e["high_pages"][head]
+        assert [int(table[u, L - 1 - k]) for k in range(len(e["low_pages"][head]))] == e["low_pages"][head]
+    ring = v["ring"].cpu().numpy()
+    assert list(ring[:3]) == e["ring_head_after"]
+    ctrl = v["ctrl"].cpu().numpy()
+    assert int(ctrl[0]) == e["start_after"] and int(ctrl[1]) == e["free_after"]
+    free_region = [int(ring[(int(ctrl[0]) + k) % 16]) for k in range(int(ctrl[1]))]
+    assert free_region == e["free_region_after"]
