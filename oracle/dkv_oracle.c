@@ -256,6 +256,9 @@ static int32_t slot_pos(orc_pool* p, int cls, int32_t u, int32_t s) {
 static int32_t write_token(orc_pool* p, int cls, int32_t u, int32_t s, const float* k, const float* v,
                            float sig, int32_t pos) {
   const orc_class_geom* g = &p->g[cls];
+  /* Q30: a token with a non-finite K or V element is rejected whole — nothing of it is written */
+  for (int32_t i = 0; i < p->c.d; i++)
+    if (!isfinite(k[i]) || !isfinite(v[i])) return ORC_ERR_NONFINITE;
   int32_t idx; uint8_t* pg = slot_page(p, cls, u, s, &idx);
   uint16_t ks, kz, vs, vz;
   int32_t st = orc_quantize(k, p->c.d, g->kbits, pg + g->off_k + idx * g->k_row, &ks, &kz);
@@ -272,6 +275,9 @@ static int32_t write_token(orc_pool* p, int cls, int32_t u, int32_t s, const flo
 
 static void read_token(orc_pool* p, int cls, int32_t u, int32_t s, float* k, float* v, float* sig, int32_t* pos) {
   const orc_class_geom* g = &p->g[cls];
+  /* Q30: a token with a non-finite K or V element is rejected whole — nothing of it is written */
+  for (int32_t i = 0; i < p->c.d; i++)
+    if (!isfinite(k[i]) || !isfinite(v[i])) return ORC_ERR_NONFINITE;
   int32_t idx; uint8_t* pg = slot_page(p, cls, u, s, &idx);
   uint16_t ks, kz, vs, vz;
   memcpy(&ks, pg + g->off_kmeta + 4 * idx, 2); memcpy(&kz, pg + g->off_kmeta + 4 * idx + 2, 2);

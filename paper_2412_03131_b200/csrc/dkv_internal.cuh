@@ -538,6 +538,95 @@ __device__ __forceinline__ void quant_chunks_h16_ct(const uint32_t (&x)[NCH][4],
   }
 }
 
+// The same quantizer split in two so a caller can validate both vectors of a token before storing
+// either (Q30): qstats_h16_ct = min/max, group reduction, s, z, metadata, finiteness; qencode_h16_ct =
+// the codes.  Arithmetic identical to quant_chunks_h16_ct.
+struct QStats {
+  float nz, inv, cap;
+  uint32_t zmask, meta;
+  bool ok, all_normal;      // all_normal is warp-uniform
+};
+template <int G, int NCH, int BITS>
+__device__ __forceinline__ QStats qstats_h16_ct(const uint32_t (&x)[NCH][4], unsigned gmask) {
+  constexpr float Qf = (float)((1 << BITS) - 1);
+  __half2 lo = *reinterpret_cast<const __half2*>(&x[0][0]), hi = lo;
+#pragma unroll
+  for (int c = 0; c < NCH; c++)
+#pragma unroll
+    for (int w = 0; w < 4; w++) {
+      if (c == 0 && w == 0) continue;
+      const __half2 v = *reinterpret_cast<const __half2*>(&x[c][w]);
+      lo = __hmin2_nan(lo, v);
+      hi = __hmax2_nan(hi, v);
+    }
+  __half2 key = __halves2half2(__hmin_nan(__low2half(lo), __high2half(lo)),
+                               __hneg(__hmax_nan(__low2half(hi), __high2half(hi))));
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    uint32_t k = *reinterpret_cast<uint32_t*>(&key);
+    k = __shfl_xor_sync(kFull, k, o);
+    key = __hmin2_nan(key, *reinterpret_cast<__half2*>(&k));
+  }
+  unsigned short mnb = __half_as_ushort(__low2half(key));
+  const unsigned short mxb = __half_as_ushort(__hneg(__high2half(key)));
+  const bool zmin = (mnb & 0x7FFFu) == 0;
+  if (__any_sync(kFull, zmin)) {                        // rare: which zero is the minimum?
+    bool negz = false;
+#pragma unroll
+    for (int c = 0; c < NCH; c++)
+#pragma unroll
+      for (int w = 0; w < 4; w++) negz |= ((x[c][w] & 0xFFFFu) == 0x8000u) | ((x[c][w] >> 16) == 0x8000u);
+    const unsigned b = __ballot_sync(kFull, negz);
+    if (zmin) mnb = (b & gmask) ? 0x8000u : 0x0000u;
+  }
+  QStats st;
+  st.ok = ((mnb & 0x7C00u) != 0x7C00u) && ((mxb & 0x7C00u) != 0x7C00u);
+  const float mn = __half2float(__ushort_as_half(mnb)), mx = __half2float(__ushort_as_half(mxb));
+  const float s32 = __fdiv_rn(__fsub_rn(mx, mn), Qf);
+  const __half s16 = __float2half_rn(s32);
+  st.meta = (uint32_t)__half_as_ushort(s16) | ((uint32_t)mnb << 16);
+  const float sf = __half2float(s16);
+  st.inv = __fdiv_rn(1.0f, sf);
+  st.nz = -mn;
+  st.all_normal = !__any_sync(kFull, !(sf >= 6.103515625e-05f));
+  st.cap = (sf >= 6.103515625e-05f) ? 3.0e38f : Qf;
+  st.zmask = sf != 0.0f ? 0xFFFFFFFFu : 0u;
+  return st;
+}
+template <int NCH, int BITS>
+__device__ __forceinline__ void qencode_h16_ct(const uint32_t (&x)[NCH][4], const QStats& st, uint2 (&pk)[NCH]) {
+  if (st.all_normal) {                                  // every s16 normal: t <= Q + 1/8, no clamp needed
+#pragma unroll
+    for (int c = 0; c < NCH; c++) {
+      uint32_t ub[8];
+#pragma unroll
+      for (int w = 0; w < 4; w++)
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++) {
+          const float d = mixed_add_h(hh ? (x[c][w] >> 16) : (x[c][w] & 0xFFFFu), st.nz);
+          const float a = __fadd_rd(__fmul_rn(d, st.inv), 0.5f);
+          ub[2 * w + hh] = __float_as_uint(__fadd_rd(a, 8388608.0f));
+        }
+      pk[c] = pack8_codes_ct<BITS>(ub);
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < NCH; c++) {
+      uint32_t ub[8];
+#pragma unroll
+      for (int w = 0; w < 4; w++)
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++) {
+          const float d = mixed_add_h(hh ? (x[c][w] >> 16) : (x[c][w] & 0xFFFFu), st.nz);
+          const float t = fminf(__fmul_rn(d, st.inv), st.cap);
+          const float a = __fadd_rd(t, 0.5f);
+          ub[2 * w + hh] = __float_as_uint(__fadd_rd(a, 8388608.0f)) & st.zmask;
+        }
+      pk[c] = pack8_codes_ct<BITS>(ub);
+    }
+  }
+}
+
 // FP32 input (a dequantized K8V4 token being downgraded, Q9): x[c][e] = element e of chunk c.
 // min/max with fminf/fmaxf (IEEE minimum/maximum, -0 < +0 on sm_100 as the oracle's total order);
 // z = f16(min) may exceed some inputs, so t is clamped to [0, Q] before the exact RD rounding — equal to

@@ -82,35 +82,42 @@ __device__ __forceinline__ void bulk_list(const ListCtx& c, const ClassGeom& g, 
     const int pid = valid ? __ldg(c.row + (c.cls == DKV_CLS_HIGH ? k : c.L - 1 - k)) : 0;
     uint8_t* pg = c.pages + (size_t)pid * (size_t)c.page_bytes;
     uint32_t mk, mv;
-    bool fk, fv;
-    {
+    bool tok_ok;
+    uint8_t* krow = pg + g.off_k + idx * g.k_row;
+    uint8_t* vrow = pg + g.off_v + idx * g.v_row;
+    if constexpr (KB > 0) {
+      // statistics of both vectors first, so a token is validated whole before any store (Q30)
+      const QStats sk = qstats_h16_ct<kBulkG, NCH, KB>(xk, gmask);
+      const QStats sv = qstats_h16_ct<kBulkG, NCH, VB>(xv, gmask);
+      mk = sk.meta; mv = sv.meta;
+      tok_ok = sk.ok && sv.ok;
       uint2 pk[NCH];
-      if constexpr (KB > 0) quant_chunks_h16_ct<kBulkG, NCH, KB>(xk, gmask, pk, mk, fk);
-      else quant_chunks_h16<kBulkG, NCH>(xk, g.kbits, gmask, pk, mk, fk);
-      uint8_t* krow = pg + g.off_k + idx * g.k_row;
-      if (valid) {
+      qencode_h16_ct<NCH, KB>(xk, sk, pk);
+      if (valid && tok_ok) {
+#pragma unroll
+        for (int a = 0; a < NCH; a++) store_chunk_codes_ct<KB>(krow, q + kBulkG * a, pk[a]);
+      }
+      qencode_h16_ct<NCH, VB>(xv, sv, pk);
+      if (valid && tok_ok) {
+#pragma unroll
+        for (int a = 0; a < NCH; a++) store_chunk_codes_ct<VB>(vrow, q + kBulkG * a, pk[a]);
+      }
+    } else {
+      uint2 pkk[NCH], pkv[NCH];
+      bool fk, fv;
+      quant_chunks_h16<kBulkG, NCH>(xk, g.kbits, gmask, pkk, mk, fk);
+      quant_chunks_h16<kBulkG, NCH>(xv, g.vbits, gmask, pkv, mv, fv);
+      tok_ok = fk && fv;
+      if (valid && tok_ok) {
 #pragma unroll
         for (int a = 0; a < NCH; a++) {
-          if constexpr (KB > 0) store_chunk_codes_ct<KB>(krow, q + kBulkG * a, pk[a]);
-          else store_chunk_codes(krow, q + kBulkG * a, g.kbits, pk[a]);
+          store_chunk_codes(krow, q + kBulkG * a, g.kbits, pkk[a]);
+          store_chunk_codes(vrow, q + kBulkG * a, g.vbits, pkv[a]);
         }
       }
     }
-    {
-      uint2 pk[NCH];
-      if constexpr (KB > 0) quant_chunks_h16_ct<kBulkG, NCH, VB>(xv, gmask, pk, mv, fv);
-      else quant_chunks_h16<kBulkG, NCH>(xv, g.vbits, gmask, pk, mv, fv);
-      uint8_t* vrow = pg + g.off_v + idx * g.v_row;
-      if (valid) {
-#pragma unroll
-        for (int a = 0; a < NCH; a++) {
-          if constexpr (KB > 0) store_chunk_codes_ct<VB>(vrow, q + kBulkG * a, pk[a]);
-          else store_chunk_codes(vrow, q + kBulkG * a, g.vbits, pk[a]);
-        }
-      }
-    }
-    if (valid) {
-      bad |= !(fk && fv);
+    if (valid) bad |= !tok_ok;
+    if (valid && tok_ok) {                               // Q30: a non-finite token is rejected whole
       uint32_t* w32 = nullptr;
       uint32_t val = 0;
       if (q == 0) { w32 = reinterpret_cast<uint32_t*>(pg + g.off_kmeta) + idx; val = mk; }

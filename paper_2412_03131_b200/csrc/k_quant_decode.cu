@@ -355,6 +355,7 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
 
     // ---- 2. t_c -> its section slot at its class bits
     cp_async_wait<0>();                                  // this lane's part of the new token is in smem
+    bool rejected = false;                               // Q30: a non-finite t_c leaves slot and window as they are
     if (has_tc) {                                        // group-uniform
       if (p.W == 0) { wk = lds_hvec<EPL>(my_nk); wv = lds_hvec<EPL>(my_nv); }   // t_c is the new token
       const ClassGeom g = geom_of(p, tc_class);
@@ -364,6 +365,7 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
       const uint4 pv = quant_h16_lane<G, EPL>(wv, g.vbits, gmask, mv, fv);
       if (!(fk && fv)) {
         if (q == 0) set_status(p.ctrl, DKV_ERR_NONFINITE);
+        rejected = true;
       } else {
         const int idx = tc_slot - tc_pg * g.C;
         uint8_t* pg = p.pages + (size_t)pid_tc * (size_t)p.page_bytes;
@@ -376,7 +378,7 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
       }
     }
     // 3. window push, after t_c's row has been consumed
-    if (wk_row != nullptr) {
+    if (wk_row != nullptr && !rejected) {
       store_hvec<EPL>(wk_row, q, lds_hvec<EPL>(my_nk));
       store_hvec<EPL>(wv_row, q, lds_hvec<EPL>(my_nv));
     }

@@ -81,7 +81,7 @@ class Inputs:
 
     def prefill(self, reqs, lens, stride=None):
         s = self.scn
-        stride = int(stride if stride is not None else max(max(lens), 1))
+        stride = int(stride if stride is not None else max(max(lens, default=0), 1))
         ridx = torch.as_tensor(np.asarray(reqs, np.int64), device=self.device)
         ug = self.ug[ridx]                                                         # [n, LyH]
         sig = synth.prefill_sig(s.seed, ug, stride, s.alpha_h, s.alpha_l, self.mix_h[ridx], self.mix_l[ridx],
