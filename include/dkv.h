@@ -122,6 +122,7 @@ typedef struct {
   int32_t units, table_len, page_bytes, num_tiles, tile_units, seg_tokens, num_segs;
   int32_t C[3], k_row[3], v_row[3], off_k[3], off_kmeta[3], off_v[3], off_vmeta[3], off_score[3], off_pos[3];
   int64_t off_tile_sums;       /* int64[num_tiles][3] scratch of the prompt workflow's scans */
+  int64_t off_rec;             /* int32[units][3] scratch of the deferred recycle copy */
 } dkv_layout_t;
 
 /* Arena size for `cfg`, or 0 if the configuration is invalid. */

@@ -23,7 +23,10 @@ struct Ctrl {
   int64_t last_demand, last_freed;
   int64_t total_dem, total_fr;   // published by the last scan tile before the barrier
   unsigned long long bar_epoch;  // grid barriers crossed (only calls that take the barrier path)
-  int64_t pad[5];
+  int64_t rec_end0;              // end pointer at entry of the last compact_alloc (deferred recycle)
+  int32_t rec_deferred;          // 1: the last compact_alloc left its recycle copies to recycle_kernel
+  int32_t pad32;
+  int64_t pad[3];
 };
 static_assert(sizeof(Ctrl) <= 256, "ctrl block");
 
@@ -88,6 +91,7 @@ struct PoolDev {
   int64_t* stats;       // int64[4] admission counters
   FastDiv div_LyH, div_W, div_Ch, div_Cl;   // u -> request, position -> window slot, slot -> (page, index)
   int64_t* tile_sums;   // [num_tiles][3] prompt-workflow scan scratch
+  int32_t* rec;         // [U][3] deferred recycle: {ring offset from the end pointer, ph, freed pages}
   int32_t prefill_wf;   // dkv_config_t.prefill_workflow
 };
 
@@ -927,7 +931,8 @@ cudaError_t launch_classify_decode(const PoolDev& p, const float* sig, dkv_decis
 cudaError_t launch_classify_prefill(const PoolDev& p, int n, const float* sig, int64_t sig_stride, uint8_t* cls,
                                     int max_len, cudaStream_t s);
 cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s,
-                                 bool alloc = true);
+                                 bool alloc = true, bool defer_recycle = false);
+cudaError_t launch_recycle(const PoolDev& p, const int32_t* req, int n, cudaStream_t s);
 cudaError_t launch_prefill_conservative(const PoolDev& p, cudaStream_t s);
 cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
                                 const float* sig, cudaStream_t s);

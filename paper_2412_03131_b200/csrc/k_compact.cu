@@ -45,7 +45,7 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 }
 
 template <int TU>
-__global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, int phase, int alloc) {
+__global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, int phase, int alloc, int defer_rec) {
   constexpr int NW = TU / 32;
   __shared__ unsigned long long s_epoch;
   __shared__ int64_t s_start0, s_free0, s_D, s_F;
@@ -153,52 +153,77 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   const uint32_t off_fr = s_exfr + s_wfr[warp] + inc_fr - fr;
 
   // ---- recycle: freed IDs -> ring[(end + off + k) mod P], canonical slot order (Q13).  The tile's freed
-  // units are listed in shared memory and dealt round-robin to all warps; a warp copies one unit's slots
-  // with 32 lanes, issuing up to 8 table loads per lane before the dependent ring / table stores.
+  // slots form one flat list (k = tile-local exclusive scan of the freed counts + slot rank), cut into one
+  // contiguous chunk per warp; lane l of a warp takes k = base + 32 j + l (coalesced table reads and ring
+  // writes), finds its first unit by binary search and then only walks forward.  kRecDepth loads per lane
+  // are in flight before the dependent ring / table stores.  A whole finished request (its units sit in one
+  // or two tiles) is copied by every warp of those tiles at once.
   {
-    __shared__ int s_nfu;
-    __shared__ uint32_t s_fu[TU];                                // freed unit, by tile-local rank
-    if (tid == 0) s_nfu = 0;
-    __syncthreads();
-    const unsigned fm = __ballot_sync(kFull, fr != 0);
-    int wbase = 0;
-    if (lane == 0 && fm) wbase = atomicAdd(&s_nfu, __popc(fm));
-    wbase = __shfl_sync(kFull, wbase, 0);
-    if (fr != 0) s_fu[wbase + __popc(fm & ((1u << lane) - 1u))] = (uint32_t)tid;
-    __syncthreads();
-    const int nfu = s_nfu;
-    if (nfu > 0) {
-      const int64_t end0 = (start0 + free0) % P;
-      __shared__ uint32_t s_off[TU];
-      __shared__ int s_nfr[TU], s_ph[TU];
-      s_off[tid] = off_fr; s_nfr[tid] = (int)fr; s_ph[tid] = ceil_div(nh, p.Ch);
+    constexpr int kRecDepth = 8;
+    __shared__ uint32_t s_loc[TU];                               // tile-local exclusive freed offset
+    __shared__ int s_nfr[TU], s_ph[TU];
+    const uint32_t tile_ex = s_exfr;
+    const uint32_t Ft = s_incfr - tile_ex;                       // freed slots in this tile
+    // deferred: in the decode fast path (grants never read a slot recycled in this call) the copy is left to
+    // recycle_kernel, launched right after; this kernel records each freed unit's offset from the end pointer
+    const bool defer = defer_rec && phase == DKV_PHASE_DECODE && status0 == 0 && free0 >= (int64_t)p.U;
+    if (defer && fr != 0) {
+      p.rec[3 * (size_t)u] = (int32_t)off_fr;
+      p.rec[3 * (size_t)u + 1] = ceil_div(nh, p.Ch);
+      p.rec[3 * (size_t)u + 2] = (int32_t)fr;
+    }
+    if (tid == 0 && tile == 0 && defer_rec) {
+      int64_t e0 = start0 + free0;
+      ctrl->rec_end0 = e0 >= P ? e0 - P : e0;
+      ctrl->rec_deferred = defer ? 1 : 0;
+    }
+    if (Ft > 0 && !defer) {                                      // tile-uniform
+      int64_t ring0 = start0 + free0;                            // end pointer + this tile's offset
+      ring0 -= ring0 >= P ? P : 0;
+      ring0 += tile_ex;
+      s_loc[tid] = off_fr - tile_ex; s_nfr[tid] = (int)fr; s_ph[tid] = ceil_div(nh, p.Ch);
       __syncthreads();
-      for (int i = warp; i < nfu; i += NW) {
-        const int t = (int)s_fu[i];
-        const int uu = tile * TU + t;
-        const uint32_t off = s_off[t];
-        const int nfr = s_nfr[t], ph = s_ph[t];
-        int32_t* row = p.table + (size_t)uu * L;
-        for (int k0 = 0; k0 < nfr; k0 += 32 * 8) {
-          int32_t pid[8];
+      const uint32_t per = ((Ft + NW - 1) / NW + 31) & ~31u;     // per-warp chunk, a multiple of 32
+      const uint32_t w0 = (uint32_t)warp * per, w1 = min(w0 + per, Ft);
+      int t = 0;
+      if (w0 + lane < w1) {                                      // last t with s_loc[t] <= k
+        const uint32_t k = w0 + lane;
+        int lo = 0, hi = TU;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_loc[mid] <= k) lo = mid; else hi = mid;
+        }
+        t = lo;
+      }
+      const uint32_t row0 = (uint32_t)(tile * TU) * (uint32_t)L;
+      for (uint32_t base = w0; base < w1; base += 32 * kRecDepth) {
+        uint32_t tix[kRecDepth];                                 // table index (unit * L + slot)
 #pragma unroll
-          for (int j = 0; j < 8; j++) {
-            const int k = k0 + 32 * j + lane;
-            const int slot = k < ph ? k : L - nfr + k;           // [0, ph) then [L - pl, L)
-            pid[j] = k < nfr ? __ldcg(row + slot) : -1;
+        for (int j = 0; j < kRecDepth; j++) {
+          const uint32_t k = base + 32 * j + lane;
+          tix[j] = 0xFFFFFFFFu;
+          if (k < w1) {
+            while (k >= s_loc[t] + (uint32_t)s_nfr[t]) t++;
+            const int jj = (int)(k - s_loc[t]), nfr_t = s_nfr[t];
+            const int slot = jj < s_ph[t] ? jj : L - nfr_t + jj;  // [0, ph) then [L - pl, L)
+            tix[j] = row0 + (uint32_t)t * (uint32_t)L + (uint32_t)slot;
           }
+        }
+        int32_t pid[kRecDepth];
 #pragma unroll
-          for (int j = 0; j < 8; j++) {
-            const int k = k0 + 32 * j + lane;
-            if (k < nfr) {
-              const int slot = k < ph ? k : L - nfr + k;
-              p.ring[(end0 + off + k) % P] = pid[j];
-              // clear the slot only once its load has returned: a store issued while the same line's load
-              // miss is outstanding takes a slow path in L2 (see k_quant_decode.cu)
-              int32_t empty = -1;
-              asm volatile("" : "+r"(empty) : "r"(pid[j]));
-              row[slot] = empty;
-            }
+        for (int j = 0; j < kRecDepth; j++) pid[j] = tix[j] != 0xFFFFFFFFu ? __ldcg(p.table + tix[j]) : -1;
+#pragma unroll
+        for (int j = 0; j < kRecDepth; j++) {
+          if (tix[j] != 0xFFFFFFFFu) {
+            int64_t pos = ring0 + base + 32 * j + lane;            // < 3P: two conditional wraps, no division
+            pos -= pos >= P ? P : 0;
+            pos -= pos >= P ? P : 0;
+            p.ring[pos] = pid[j];
+            // clear the slot only once its load has returned: a store issued while the same line's load
+            // miss is outstanding takes a slow path in L2 (see k_quant_decode.cu)
+            int32_t empty = -1;
+            asm volatile("" : "+r"(empty) : "r"(pid[j]));
+            p.table[tix[j]] = empty;
           }
         }
       }
@@ -243,7 +268,9 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
           set_status(ctrl, DKV_ERR_OVERFLOW);
         } else {
           const int slot = (grow == DKV_GROW_HIGH) ? nh / p.Ch : L - 1 - nl / p.Cl;
-          p.table[(size_t)u * L + slot] = __ldcg(p.ring + (start0 + off_dem) % P);
+          int64_t pos = start0 + off_dem;                        // < 2P (off_dem < D <= free)
+          pos -= pos >= P ? P : 0;
+          p.table[(size_t)u * L + slot] = __ldcg(p.ring + pos);
         }
       }
       if (st == DKV_REQ_ACTIVE) {
@@ -266,7 +293,9 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
         int32_t* row = p.table + (size_t)uu * L;
         for (int k = lane; k < nd; k += 32) {
           const int slot = k < ph ? k : L - 1 - (k - ph);       // high left-to-right, low right-to-left
-          row[slot] = __ldcg(p.ring + (start0 + off + k) % P);
+          int64_t pos = start0 + off + k;                        // < 2P
+          pos -= pos >= P ? P : 0;
+          row[slot] = __ldcg(p.ring + pos);
         }
       }
       if (st == DKV_REQ_ADMITTING && alloc) { p.n_h[u] = p.pf_nh[u]; p.n_l[u] = p.pf_nl[u]; }
@@ -305,7 +334,8 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
 }
 
 template <int TU>
-static cudaError_t launch_tu(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s, int alloc) {
+static cudaError_t launch_tu(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s, int alloc,
+                             int defer) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.num_tiles);
   cfg.blockDim = dim3(TU);
@@ -317,14 +347,16 @@ static cudaError_t launch_tu(const PoolDev& p, const dkv_decision_t* dec, int ph
   static const int coop = getenv("DKV_COMPACT_COOP") ? atoi(getenv("DKV_COMPACT_COOP")) : 1;   // tuning knob
   cfg.attrs = attr;
   cfg.numAttrs = coop ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, compact_alloc_kernel<TU>, p, dec, phase, alloc);
+  return cudaLaunchKernelEx(&cfg, compact_alloc_kernel<TU>, p, dec, phase, alloc, defer);
 }
 
-cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s, bool alloc) {
+cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s, bool alloc,
+                                 bool defer_recycle) {
+  const int a = alloc ? 1 : 0, d = defer_recycle ? 1 : 0;
   switch (p.tile_units) {
-    case 256: return launch_tu<256>(p, dec, phase, s, alloc ? 1 : 0);
-    case 512: return launch_tu<512>(p, dec, phase, s, alloc ? 1 : 0);
-    default: return launch_tu<1024>(p, dec, phase, s, alloc ? 1 : 0);
+    case 256: return launch_tu<256>(p, dec, phase, s, a, d);
+    case 512: return launch_tu<512>(p, dec, phase, s, a, d);
+    default: return launch_tu<1024>(p, dec, phase, s, a, d);
   }
 }
 
@@ -340,6 +372,64 @@ int compact_max_coresident(int tile_units) {
   }
   if (e != cudaSuccess) return 0;
   return per * sms;
+}
+
+// ---- deferred recycle copy (decode steps that free requests): one warp per unit of the freed requests,
+// ring[(end0 + off + k) mod P] = table slot k of the unit in canonical slot order (Q13), then the slot is
+// cleared.  Runs right after compact_alloc_kernel recorded {off, ph, freed} per unit in p.rec; a no-op if
+// that call took the barrier path (it then copied in place).
+constexpr int kRecMaxReq = 64;
+struct RecList {
+  int32_t n;
+  int32_t req[kRecMaxReq];
+};
+
+__global__ void __launch_bounds__(256) recycle_kernel(PoolDev p, RecList l) {
+  if (ld_volatile(&p.ctrl->rec_deferred) == 0) return;
+  const int lane = threadIdx.x & 31;
+  const int wu = (blockIdx.x * 256 + threadIdx.x) >> 5;         // index over the freed requests' units
+  if (wu >= l.n * p.LyH) return;
+  const int u = l.req[wu / p.LyH] * p.LyH + wu % p.LyH;
+  const int32_t off = p.rec[3 * (size_t)u], ph = p.rec[3 * (size_t)u + 1], nfr = p.rec[3 * (size_t)u + 2];
+  const int P = p.P, L = p.L;
+  const int64_t ring0 = p.ctrl->rec_end0 + off;                  // < 2P
+  int32_t* row = p.table + (size_t)u * L;
+  for (int k0 = 0; k0 < nfr; k0 += 32 * 8) {
+    int32_t pid[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const int k = k0 + 32 * j + lane;
+      const int slot = k < ph ? k : L - nfr + k;                 // [0, ph) then [L - pl, L)
+      pid[j] = k < nfr ? __ldcg(row + slot) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const int k = k0 + 32 * j + lane;
+      if (k < nfr) {
+        const int slot = k < ph ? k : L - nfr + k;
+        int64_t pos = ring0 + k;                                 // < 3P
+        pos -= pos >= P ? P : 0;
+        pos -= pos >= P ? P : 0;
+        p.ring[pos] = pid[j];
+        int32_t empty = -1;                                      // clear only after the load returned
+        asm volatile("" : "+r"(empty) : "r"(pid[j]));
+        row[slot] = empty;
+      }
+    }
+  }
+}
+
+cudaError_t launch_recycle(const PoolDev& p, const int32_t* req, int n, cudaStream_t s) {
+  for (int i0 = 0; i0 < n; i0 += kRecMaxReq) {
+    RecList l;
+    l.n = n - i0 < kRecMaxReq ? n - i0 : kRecMaxReq;
+    for (int i = 0; i < l.n; i++) l.req[i] = req[i0 + i];
+    const long warps = (long)l.n * p.LyH;
+    recycle_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(p, l);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace dkv

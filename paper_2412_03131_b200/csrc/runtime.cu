@@ -79,6 +79,7 @@ bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
   Lo.off_stats = take(32);
   Lo.off_tile_status = take(8 * (int64_t)G.num_tiles);
   Lo.off_tile_sums = take(24 * (int64_t)G.num_tiles);
+  Lo.off_rec = take(12 * (int64_t)G.U);
   Lo.off_ring = take(4 * P);
   Lo.off_table = take(4 * U * G.L);
   Lo.off_n_h = take(4 * U);
@@ -217,6 +218,7 @@ dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_
   d.stats = (int64_t*)(b + Lo.off_stats);
   d.tile_status = (unsigned long long*)(b + Lo.off_tile_status);
   d.tile_sums = (int64_t*)(b + Lo.off_tile_sums);
+  d.rec = (int32_t*)(b + Lo.off_rec);
   d.prefill_wf = cfg->prefill_workflow;
   d.ring = (int32_t*)(b + Lo.off_ring);
   d.table = (int32_t*)(b + Lo.off_table);
@@ -302,7 +304,16 @@ dkv_status_t dkv_compact_alloc(dkv_pool_t p, const dkv_decision_t* d_dec, dkv_st
     e = launch_compact_alloc(p->dev, d_dec, p->phase, (cudaStream_t)s, /*alloc=*/false);
     if (e == cudaSuccess) e = launch_prefill_conservative(p->dev, (cudaStream_t)s);
   } else {
-    e = launch_compact_alloc(p->dev, d_dec, p->phase, (cudaStream_t)s, /*alloc=*/true);
+    // decode steps that recycle finished requests: the scan kernel only records each freed unit's ring
+    // offset, and a second, wide kernel copies the page IDs (one warp per freed unit, all SMs) — the copy
+    // would otherwise run on the one or two CTAs whose tile holds the request
+    std::vector<int32_t> freed;
+    if (p->phase == DKV_PHASE_DECODE)
+      for (int r = 0; r < p->cfg.max_requests; r++)
+        if (p->req_state[r] == DKV_REQ_PENDING_FREE) freed.push_back(r);
+    e = launch_compact_alloc(p->dev, d_dec, p->phase, (cudaStream_t)s, /*alloc=*/true, !freed.empty());
+    if (e == cudaSuccess && !freed.empty())
+      e = launch_recycle(p->dev, freed.data(), (int)freed.size(), (cudaStream_t)s);
   }
   if (e != cudaSuccess) return DKV_ERR_CUDA;
   const int R = p->cfg.max_requests;

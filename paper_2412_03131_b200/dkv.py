@@ -61,7 +61,7 @@ class dkv_layout_t(C.Structure):
         "off_win_v", "off_pages", "off_stats")] + [(n, C.c_int32) for n in (
         "units", "table_len", "page_bytes", "num_tiles", "tile_units", "seg_tokens", "num_segs")] + \
         [(n, C.c_int32 * 3) for n in ("C", "k_row", "v_row", "off_k", "off_kmeta", "off_v", "off_vmeta",
-                                       "off_score", "off_pos")] + [("off_tile_sums", C.c_int64)]
+                                       "off_score", "off_pos")] + [("off_tile_sums", C.c_int64), ("off_rec", C.c_int64)]
 
 
 assert C.sizeof(dkv_decision_t) == 16

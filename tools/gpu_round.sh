@@ -12,5 +12,5 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 K='regex:quant_prefill|classify_decode|compact_alloc|quant_decode|classify_prefill|finish_prefill|set_requests|init_kernel'
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/launches_bench_$TAG.log 2>&1; echo "ncu launches rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:quant_prefill -s 1 -c 1 -o gpurun_out/prof_bulk_$TAG python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/prof_bulk_$TAG.log 2>&1; echo "ncu bulk rc=$?"
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"classify_decode|compact_alloc|quant_decode" -s 6 -c 6 -o gpurun_out/prof_decode_$TAG python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/prof_decode_$TAG.log 2>&1; echo "ncu decode rc=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"classify_decode|compact_alloc|quant_decode" -s 12 -c 3 -o gpurun_out/prof_decode_$TAG python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/prof_decode_$TAG.log 2>&1; echo "ncu decode rc=$?"
 ls -la gpurun_out
