@@ -348,7 +348,7 @@ def run_ours(args, rank, world, local):
             comp_us.append(e[1].elapsed_time(e[2]) * 1e3)
             qw_us.append(e[2].elapsed_time(e[3]) * 1e3)
             step_us.append(e[0].elapsed_time(e[3]) * 1e3)
-            launches += 3                                   # classify, compact_alloc, quant_decode kernels
+            launches += 3 + (1 if churn else 0)             # classify, compact_alloc, quant_decode (+ recycle)
             tc = dec.view(torch.uint8).view(-1, 16)[:, 0].cpu().numpy()
             sec = np.where(tc == 1, nh0.cpu().numpy(), np.where(tc == 2, nl0.cpu().numpy(), 0)).astype(np.int64)
             C = np.where(tc == 1, geom[1]["C"], geom[2]["C"])

@@ -16,7 +16,7 @@ __global__ void init_kernel(PoolDev p) {
   for (size_t i = tid; i < (size_t)p.R; i += nth) {
     p.req_state[i] = DKV_REQ_IDLE; p.seq_len[i] = 0; p.prompt_len[i] = 0; p.admit[i] = 0;
   }
-  for (size_t i = tid; i < (size_t)2 * p.num_tiles; i += nth) p.tile_status[i] = 0ull;
+  for (size_t i = tid; i < (size_t)p.num_tiles; i += nth) p.tile_status[i] = 0ull;
   if (tid == 0) {
     Ctrl* c = p.ctrl;
     c->start = 0; c->free = p.P; c->status = 0; c->oom_count = 0;

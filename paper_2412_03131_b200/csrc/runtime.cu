@@ -237,6 +237,9 @@ dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_
   cudaError_t e = cudaMemsetAsync(b + Lo.off_pages, 0, (size_t)(Lo.arena_bytes - Lo.off_pages), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(b + Lo.off_win_k, 0, (size_t)(Lo.off_pages - Lo.off_win_k), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(b + Lo.off_pf_seg, 0, (size_t)(Lo.off_win_k - Lo.off_pf_seg), s);
+  // control block, counters and scan / workflow / recycle scratch start zeroed (every byte initialised)
+  if (e == cudaSuccess) e = cudaMemsetAsync(b, 0, (size_t)Lo.off_ring, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(b + Lo.off_rec, 0, 12 * (size_t)G.U, s);
   if (e == cudaSuccess) e = launch_init(d, s);
   if (e != cudaSuccess) {
     dkv_pool_destroy(p);
