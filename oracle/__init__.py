@@ -62,7 +62,7 @@ def build(force: bool = False) -> str:
 class Config(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("R", "Ly", "H", "d", "M", "W", "Ch", "Cl", "kbh", "vbh", "kbl", "vbl", "P")] + \
                [("alpha_h", C.c_float), ("alpha_l", C.c_float), ("prompt_denominator", C.c_int32),
-                ("prefill_workflow", C.c_int32)]
+                ("prefill_workflow", C.c_int32), ("q_per_kv", C.c_int32)]
 
 
 class ClassGeom(C.Structure):
@@ -82,7 +82,7 @@ class _Pool(C.Structure):
                 ("admit_list", C.POINTER(C.c_int32)), ("n_admit", C.c_int32),
                 ("status", C.c_int32), ("last_phase", C.c_int32),
                 ("last_demand", C.c_int64), ("last_freed", C.c_int64), ("oom_count", C.c_int32),
-                ("last_reclaimed", C.c_int64)]
+                ("last_reclaimed", C.c_int64), ("win_sig", C.POINTER(C.c_float))]
 
 
 _lib = None
@@ -115,8 +115,10 @@ def lib():
         L.orc_take_status.argtypes = [P(_Pool)]
         L.orc_prefill_conservative.argtypes = [P(_Pool), C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64,
                                                C.c_void_p, P(C.c_int64)]
+        L.orc_attend.argtypes = [P(_Pool), C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_exp.argtypes = [C.c_float]; L.orc_exp.restype = C.c_float
         for f in ("orc_classify_decode", "orc_classify_prefill", "orc_compact_alloc", "orc_quant_write_decode",
-                  "orc_quant_write_prefill", "orc_free", "orc_take_status", "orc_prefill_conservative"):
+                  "orc_quant_write_prefill", "orc_free", "orc_take_status", "orc_prefill_conservative", "orc_attend"):
             getattr(L, f).restype = C.c_int32
         _lib = L
     return _lib
@@ -168,7 +170,7 @@ def unpack_codes(codes, d: int, bits: int) -> np.ndarray:
 
 def make_config(**kw) -> Config:
     defaults = dict(R=4, Ly=2, H=4, d=64, M=128, W=16, Ch=16, Cl=32, kbh=8, vbh=4, kbl=4, vbl=2, P=1024,
-                    alpha_h=1.0, alpha_l=0.02, prompt_denominator=0, prefill_workflow=0)
+                    alpha_h=1.0, alpha_l=0.02, prompt_denominator=0, prefill_workflow=0, q_per_kv=0)
     defaults.update(kw)
     return Config(**defaults)
 
@@ -213,6 +215,7 @@ class OraclePool:
         self.pages = view(s.pages, (c.P, self.page_bytes), C.c_uint8)
         self.win_k = view(s.win_k, (self.U, c.W, c.d), C.c_uint16)
         self.win_v = view(s.win_v, (self.U, c.W, c.d), C.c_uint16)
+        self.win_sig = view(s.win_sig, (self.U, c.W), C.c_float)
 
     def __del__(self):
         p = getattr(self, "_p", None)
@@ -265,8 +268,10 @@ class OraclePool:
 
     # calls
     def classify_decode(self, cand_sig):
-        cand_sig = np.ascontiguousarray(cand_sig, dtype=np.float32)
-        assert cand_sig.shape == (self.U,)
+        """cand_sig None: t_c's significance is taken from the window (NEXT-2)"""
+        if cand_sig is not None:
+            cand_sig = np.ascontiguousarray(cand_sig, dtype=np.float32)
+            assert cand_sig.shape == (self.U,)
         dec = np.zeros(self.U, dtype=DECISION_DTYPE)
         st = lib().orc_classify_decode(self._p, _ptr(cand_sig), _ptr(dec))
         return st, dec
@@ -289,9 +294,20 @@ class OraclePool:
         dec = np.ascontiguousarray(dec, dtype=DECISION_DTYPE)
         k_new = np.ascontiguousarray(k_new).view(np.uint16)
         v_new = np.ascontiguousarray(v_new).view(np.uint16)
-        cand_sig = np.ascontiguousarray(cand_sig, dtype=np.float32)
+        if cand_sig is not None:
+            cand_sig = np.ascontiguousarray(cand_sig, dtype=np.float32)
         assert k_new.shape == (self.U, self.cfg.d)
         return lib().orc_quant_write_decode(self._p, _ptr(dec), _ptr(k_new), _ptr(v_new), _ptr(cand_sig))
+
+    def attend(self, q, want_out=True, want_probs=False):
+        """NEXT-2: q = fp16 [U][G][d]; returns (status, out fp32 [U][G][d] or None, probs [U][M] or None)"""
+        G = self.cfg.q_per_kv
+        q = np.ascontiguousarray(q).view(np.uint16)
+        assert q.shape == (self.U, G, self.cfg.d)
+        out = np.zeros((self.U, G, self.cfg.d), np.float32) if want_out else None
+        probs = np.zeros((self.U, self.cfg.M), np.float32) if want_probs else None
+        st = lib().orc_attend(self._p, _ptr(q), _ptr(out), _ptr(probs))
+        return st, out, probs
 
     def quant_write_prefill(self, k, v, sig):
         k = np.ascontiguousarray(k).view(np.uint16)

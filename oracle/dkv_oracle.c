@@ -162,7 +162,7 @@ int32_t orc_geometry(const orc_config* c, int32_t* U, int32_t* L, int32_t* page_
       c->Ch < 1 || c->Cl < c->Ch || c->P < 1 || !bits_ok(c->kbh) || !bits_ok(c->vbh) ||
       !bits_ok(c->kbl) || !bits_ok(c->vbl) || !isfinite(c->alpha_h) || !isfinite(c->alpha_l) ||
       c->alpha_h < 0 || c->alpha_l < 0 || (c->prompt_denominator != 0 && c->prompt_denominator != 1) ||
-      (c->prefill_workflow != 0 && c->prefill_workflow != 1))
+      (c->prefill_workflow != 0 && c->prefill_workflow != 1) || c->q_per_kv < 0 || c->q_per_kv > 16)
     return ORC_ERR_INVALID;
   orc_class_geom gh, gl;
   class_geom(c->d, c->Ch, c->kbh, c->vbh, &gh);
@@ -204,11 +204,13 @@ orc_pool* orc_pool_new(const orc_config* c) {
   size_t wn = U * (size_t)c->W * (size_t)c->d;
   p->win_k = (uint16_t*)calloc(wn ? wn : 1, 2);
   p->win_v = (uint16_t*)calloc(wn ? wn : 1, 2);
+  const size_t wsn = U * (size_t)c->W;
+  p->win_sig = (float*)calloc(wsn ? wsn : 1, 4);
   p->pf_nh = (int32_t*)calloc(U, 4);
   p->pf_nl = (int32_t*)calloc(U, 4);
   p->admit_list = (int32_t*)calloc(R, 4);
   if (!p->ring || !p->table || !p->n_h || !p->n_l || !p->req_state || !p->seq_len || !p->prompt_len ||
-      !p->pages || !p->win_k || !p->win_v || !p->pf_nh || !p->pf_nl || !p->admit_list) {
+      !p->pages || !p->win_k || !p->win_v || !p->win_sig || !p->pf_nh || !p->pf_nl || !p->admit_list) {
     orc_pool_delete(p);
     return NULL;
   }
@@ -224,7 +226,7 @@ void orc_pool_delete(orc_pool* p) {
   if (!p) return;
   free(p->ring); free(p->table); free(p->n_h); free(p->n_l); free(p->req_state); free(p->seq_len);
   free(p->prompt_len); free(p->pages); free(p->win_k); free(p->win_v); free(p->pf_nh); free(p->pf_nl);
-  free(p->admit_list);
+  free(p->admit_list); free(p->win_sig);
   free(p);
 }
 
@@ -259,6 +261,9 @@ static int32_t write_token(orc_pool* p, int cls, int32_t u, int32_t s, const flo
   /* Q30: a token with a non-finite K or V element is rejected whole — nothing of it is written */
   for (int32_t i = 0; i < p->c.d; i++)
     if (!isfinite(k[i]) || !isfinite(v[i])) return ORC_ERR_NONFINITE;
+  /* Q30: a token with a non-finite K or V element is rejected whole — nothing of it is written */
+  for (int32_t i = 0; i < p->c.d; i++)
+    if (!isfinite(k[i]) || !isfinite(v[i])) return ORC_ERR_NONFINITE;
   int32_t idx; uint8_t* pg = slot_page(p, cls, u, s, &idx);
   uint16_t ks, kz, vs, vz;
   int32_t st = orc_quantize(k, p->c.d, g->kbits, pg + g->off_k + idx * g->k_row, &ks, &kz);
@@ -275,9 +280,6 @@ static int32_t write_token(orc_pool* p, int cls, int32_t u, int32_t s, const flo
 
 static void read_token(orc_pool* p, int cls, int32_t u, int32_t s, float* k, float* v, float* sig, int32_t* pos) {
   const orc_class_geom* g = &p->g[cls];
-  /* Q30: a token with a non-finite K or V element is rejected whole — nothing of it is written */
-  for (int32_t i = 0; i < p->c.d; i++)
-    if (!isfinite(k[i]) || !isfinite(v[i])) return ORC_ERR_NONFINITE;
   int32_t idx; uint8_t* pg = slot_page(p, cls, u, s, &idx);
   uint16_t ks, kz, vs, vz;
   memcpy(&ks, pg + g->off_kmeta + 4 * idx, 2); memcpy(&kz, pg + g->off_kmeta + 4 * idx + 2, 2);
@@ -318,7 +320,8 @@ int32_t orc_classify_decode(orc_pool* p, const float* cand_sig, orc_decision* de
     int32_t N = p->seq_len[r] + 1;
     int32_t pc = N - 1 - c->W;
     if (pc < 0) continue;                                     /* no token leaves the window yet */
-    float sc = cand_sig[u];
+    /* NULL cand_sig (NEXT-2): t_c's significance is the running average kept for its window slot */
+    float sc = cand_sig ? cand_sig[u] : (c->W ? p->win_sig[(size_t)u * c->W + (size_t)(pc % c->W)] : 0.0f);
     if (!isfinite(sc) || sc < 0.0f) { set_status(p, ORC_ERR_NONFINITE); continue; }
     if (sc == 0.0f) sc = 0.0f;                                /* canonicalise -0 -> +0 (Q6) */
     float th = c->alpha_h / (float)N;                         /* alpha_h / N */
@@ -603,12 +606,15 @@ int32_t orc_quant_write_decode(orc_pool* p, const orc_decision* dec, const uint1
       /* t_c sits in window slot p_c mod W == (N-1) mod W; read it before the push overwrites it */
       const uint16_t* sk = W ? wk : kn; const uint16_t* sv = W ? wv : vn;
       for (int32_t i = 0; i < d; i++) { kx[i] = orc_f32_from_f16(sk[i]); vx[i] = orc_f32_from_f16(sv[i]); }
-      float sc = cand_sig[u];
+      float sc = cand_sig ? cand_sig[u] : (W ? p->win_sig[(size_t)u * W + (size_t)((N - 1) % W)] : 0.0f);
       if (sc == 0.0f) sc = 0.0f;
       int32_t st = write_token(p, D->tc_class, u, D->tc_slot, kx, vx, sc, pc);
       if (st != ORC_OK) { set_status(p, st); continue; }
     }
-    if (W) { memcpy(wk, kn, (size_t)d * 2); memcpy(wv, vn, (size_t)d * 2); }
+    if (W) {
+      memcpy(wk, kn, (size_t)d * 2); memcpy(wv, vn, (size_t)d * 2);
+      p->win_sig[(size_t)u * W + (size_t)((N - 1) % W)] = 0.0f;   /* the new token: no later query yet (Q33) */
+    }
   }
   free(kx); free(vx);
   return ORC_OK;
@@ -643,6 +649,9 @@ int32_t orc_quant_write_prefill(orc_pool* p, const uint16_t* k, const uint16_t* 
         } else {
           memcpy(p->win_k + ((size_t)u * W + (size_t)(t % W)) * d, kr, (size_t)d * 2);
           memcpy(p->win_v + ((size_t)u * W + (size_t)(t % W)) * d, vr, (size_t)d * 2);
+          float ws = sig[((int64_t)i * LyH + j) * sig_stride + t];
+          if (ws == 0.0f) ws = 0.0f;
+          p->win_sig[(size_t)u * W + (size_t)(t % W)] = ws;     /* the prompt phase's significance */
         }
       }
     }
@@ -664,6 +673,145 @@ int32_t orc_free(orc_pool* p, const int32_t* req, int32_t n) {
     for (int32_t j = 0; j < i; j++) if (req[j] == req[i]) return ORC_ERR_STATE;
   }
   for (int32_t i = 0; i < n; i++) p->req_state[req[i]] = ORC_REQ_PENDING_FREE;
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------------------------------
+ * NEXT-2: decode attention over the compressed cache and the significance update.
+ * Eq. 1 for the query of the newest token (position N-1) of every ACTIVE unit, G = q_per_kv
+ * query heads sharing the KV head (GQA), over the unit's stored tokens (keys dequantized,
+ * X^ = s*Q + z) and its FP16 window; every floating-point result is fixed by readings Q31-Q34:
+ *   Q31 logit = fmul(dot, 1/sqrt(d)) with dot = serial sum over elements e = 0..d-1 of fmul(q_e, k_e);
+ *       tokens in the order: high slots 0..n_h-1, low slots 0..n_l-1, window oldest -> newest;
+ *   Q32 p = exp(logit - max) with orc_exp (round-to-nearest range reduction + degree-6 polynomial, fixed
+ *       operation order); Z = sum over pages in that order of the serial in-page sums (the window counts as
+ *       one page); a = fdiv(p, Z); the output row = serial sum over tokens of fmul(a, v_e);
+ *   Q33 a token's significance is the mean of the scores it received from later tokens; a decode
+ *       step adds the score of query N-1 (max over the G heads) to every token p < N-1:
+ *       sig' = fdiv(fadd(fmul(sig, c), a), c + 1), c = N-2-p scores so far; a new token starts at 0;
+ *   Q34 pages keep the updated significance in their score segment, the window in win_sig.
+ * ----------------------------------------------------------------------------------------------*/
+float orc_exp(float x) {
+  const float log2e = 1.44269504088896341f;
+  float t = x * log2e;                                   /* fmul_rn */
+  if (t < -125.0f) return 0.0f;
+  float n = rintf(t);                                    /* round to nearest even */
+  float f = t - n;                                       /* exact, |f| <= 1/2 */
+  /* 2^f = sum (ln2)^k f^k / k!, Horner, k = 0..6 */
+  float r = 1.54035304e-4f;
+  r = r * f + 1.33335581e-3f;
+  r = r * f + 9.61812911e-3f;
+  r = r * f + 5.55041087e-2f;
+  r = r * f + 2.40226507e-1f;
+  r = r * f + 6.93147181e-1f;
+  r = r * f + 1.0f;
+  uint32_t eb = (uint32_t)((int32_t)n + 127) << 23;      /* 2^n, n in [-125, 0] */
+  float two_n;
+  memcpy(&two_n, &eb, 4);
+  return r * two_n;
+}
+
+typedef struct { const uint8_t* pg; int cls; int32_t idx; float* sig; int32_t pos; const uint16_t* wk;
+                 const uint16_t* wv; } att_tok;
+
+static void att_key(const orc_pool* p, const att_tok* t, float* k) {
+  int32_t d = p->c.d;
+  if (t->wk) { for (int32_t e = 0; e < d; e++) k[e] = orc_f32_from_f16(t->wk[e]); return; }
+  const orc_class_geom* g = &p->g[t->cls];
+  uint16_t s16, z16;
+  memcpy(&s16, t->pg + g->off_kmeta + 4 * t->idx, 2); memcpy(&z16, t->pg + g->off_kmeta + 4 * t->idx + 2, 2);
+  orc_dequantize(t->pg + g->off_k + t->idx * g->k_row, d, g->kbits, s16, z16, k);
+}
+static void att_val(const orc_pool* p, const att_tok* t, float* v) {
+  int32_t d = p->c.d;
+  if (t->wv) { for (int32_t e = 0; e < d; e++) v[e] = orc_f32_from_f16(t->wv[e]); return; }
+  const orc_class_geom* g = &p->g[t->cls];
+  uint16_t s16, z16;
+  memcpy(&s16, t->pg + g->off_vmeta + 4 * t->idx, 2); memcpy(&z16, t->pg + g->off_vmeta + 4 * t->idx + 2, 2);
+  orc_dequantize(t->pg + g->off_v + t->idx * g->v_row, d, g->vbits, s16, z16, v);
+}
+
+int32_t orc_attend(orc_pool* p, const uint16_t* q, float* out, float* probs) {
+  const orc_config* c = &p->c;
+  if (c->q_per_kv < 1) return ORC_ERR_INVALID;
+  if (p->status != ORC_OK) return ORC_OK;
+  const int32_t LyH = c->Ly * c->H, d = c->d, W = c->W, G = c->q_per_kv, M = c->M;
+  att_tok* tok = (att_tok*)malloc(sizeof(att_tok) * (size_t)M);
+  int32_t* tpage = (int32_t*)malloc(4 * (size_t)M);       /* page index of each token (window = last) */
+  float* lg = (float*)malloc(4 * (size_t)M * (size_t)G);
+  float* a = (float*)malloc(4 * (size_t)M);
+  float* kx = (float*)malloc(4 * (size_t)d);
+  float* vx = (float*)malloc(4 * (size_t)d);
+  const float scale = 1.0f / sqrtf((float)d);
+  for (int32_t u = 0; u < p->U; u++) {
+    int32_t r = u / LyH;
+    if (p->req_state[r] != ORC_REQ_ACTIVE) continue;
+    int32_t N = p->seq_len[r];
+    /* token list (Q31 order) */
+    int32_t n = 0, npage = 0;
+    for (int cls = ORC_CLS_HIGH; cls <= ORC_CLS_LOW; cls++) {
+      int32_t cnt = cls == ORC_CLS_HIGH ? p->n_h[u] : p->n_l[u], C = p->g[cls].C;
+      for (int32_t s = 0; s < cnt; s++) {
+        att_tok* t = &tok[n];
+        int32_t idx;
+        t->pg = slot_page(p, cls, u, s, &idx);
+        t->cls = cls; t->idx = idx; t->wk = NULL; t->wv = NULL;
+        t->sig = (float*)(t->pg + p->g[cls].off_score + 4 * idx);
+        memcpy(&t->pos, t->pg + p->g[cls].off_pos + 4 * idx, 4);
+        tpage[n] = npage + s / C;
+        n++;
+      }
+      npage += (cnt + C - 1) / C;
+    }
+    for (int32_t ps = (N - W > 0 ? N - W : 0); ps < N; ps++) {
+      att_tok* t = &tok[n];
+      size_t ws = (size_t)u * W + (size_t)(ps % W);
+      t->pg = NULL; t->cls = 0; t->idx = 0; t->pos = ps;
+      t->wk = p->win_k + ws * d; t->wv = p->win_v + ws * d; t->sig = &p->win_sig[ws];
+      tpage[n] = npage;
+      n++;
+    }
+    for (int32_t i = 0; i < n; i++) a[i] = 0.0f;
+    for (int32_t g = 0; g < G; g++) {
+      const uint16_t* qg = q + ((size_t)u * G + g) * d;
+      float m = -INFINITY;
+      for (int32_t i = 0; i < n; i++) {
+        att_key(p, &tok[i], kx);
+        float dot = 0.0f;
+        for (int32_t e = 0; e < d; e++) dot = dot + orc_f32_from_f16(qg[e]) * kx[e];   /* fadd(fmul) */
+        float l = dot * scale;
+        lg[(size_t)g * M + i] = l;
+        if (l > m) m = l;
+      }
+      float Z = 0.0f, part = 0.0f;
+      for (int32_t i = 0; i < n; i++) {
+        float e = orc_exp(lg[(size_t)g * M + i] - m);
+        lg[(size_t)g * M + i] = e;
+        part = part + e;
+        if (i == n - 1 || tpage[i + 1] != tpage[i]) { Z = Z + part; part = 0.0f; }
+      }
+      float* og = out ? out + ((size_t)u * G + g) * d : NULL;
+      if (og) for (int32_t e = 0; e < d; e++) og[e] = 0.0f;
+      for (int32_t i = 0; i < n; i++) {
+        float ai = lg[(size_t)g * M + i] / Z;                /* fdiv_rn */
+        if (ai > a[i]) a[i] = ai;                            /* GQA: max over the group */
+        if (og) {
+          att_val(p, &tok[i], vx);
+          for (int32_t e = 0; e < d; e++) og[e] = og[e] + ai * vx[e];
+        }
+      }
+    }
+    if (probs) for (int32_t i = 0; i < M; i++) probs[(size_t)u * M + i] = i < n ? a[i] : 0.0f;
+    for (int32_t i = 0; i < n; i++) {                        /* Q33: running mean over later queries */
+      int32_t cnt = N - 2 - tok[i].pos;
+      if (cnt < 0) continue;                                 /* the query's own token */
+      float sg;
+      memcpy(&sg, tok[i].sig, 4);
+      sg = (sg * (float)cnt + a[i]) / (float)(cnt + 1);
+      memcpy(tok[i].sig, &sg, 4);
+    }
+  }
+  free(tok); free(tpage); free(lg); free(a); free(kx); free(vx);
   return ORC_OK;
 }
 

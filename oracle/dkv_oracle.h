@@ -38,6 +38,7 @@ typedef struct {
   int32_t prompt_denominator;   /* Q4: 0 = 1-indexed position i, 1 = prompt length n */
   int32_t prefill_workflow;     /* 0 = exact allocation after planning; 1 = the paper's prompt workflow
                                    (Fig. 5): conservative allocation, planning, reclaim (Q29) */
+  int32_t q_per_kv;             /* NEXT-2: query heads per KV head (GQA group); 0 = no attention */
 } orc_config;
 
 /* 16-byte decision record per unit (same byte layout the product's ABI documents). */
@@ -70,6 +71,7 @@ typedef struct orc_pool {
   int32_t last_phase;                       /* phase of the most recent classify */
   int64_t last_demand, last_freed; int32_t oom_count;
   int64_t last_reclaimed;                   /* prefill_workflow 1: middle pages reclaimed by the last call */
+  float   *win_sig;                         /* [U][W] significance of the window tokens (running averages) */
 } orc_pool;
 
 /* --- scalar primitives (exported for the pins) --- */
@@ -98,6 +100,13 @@ int32_t   orc_quant_write_prefill(orc_pool* p, const uint16_t* k, const uint16_t
                                   const float* sig, int64_t sig_stride);
 int32_t   orc_free(orc_pool* p, const int32_t* req, int32_t n);
 int32_t   orc_take_status(orc_pool* p);     /* returns and clears the sticky status */
+/* NEXT-2: decode attention of every ACTIVE unit's G query heads over its stored
+   (dequantized) tokens and its FP16 window, then the running-average significance update (Q31-Q34).
+   q = fp16 bits [U][G][d]; out = fp32 [U][G][d] (may be NULL); probs (may be NULL) = fp32 [U][M] per-token
+   attention (max over the G heads) in token order (high slots, low slots, window oldest first). */
+int32_t   orc_attend(orc_pool* p, const uint16_t* q, float* out, float* probs);
+float     orc_exp(float x);                 /* the normative exp of Q32 (x <= 0) */
+
 /* NEXT-1 (Fig. 5): admit + plan + compact with prefill_workflow = 1 for this call (the
    pool's own setting is restored); reclaimed_out receives the reclaimed page IDs in ring order. */
 int32_t   orc_prefill_conservative(orc_pool* p, const int32_t* req, const int32_t* len, int32_t n,
