@@ -36,6 +36,7 @@ class Scenario:
     alpha_l: float = 0.02
     prompt_denominator: int = 0
     prefill_workflow: int = 0
+    q_per_kv: int = 0
     seed: int = 1
     mix: tuple = (0.35, 0.45, 0.20)
     H_total: int | None = None
@@ -58,7 +59,7 @@ class Scenario:
     def config_dict(self):
         return {k: getattr(self, k) for k in ("R", "Ly", "H", "d", "M", "W", "Ch", "Cl", "kbh", "vbh", "kbl", "vbl",
                                               "P", "alpha_h", "alpha_l", "prompt_denominator",
-                                              "prefill_workflow")}
+                                              "prefill_workflow", "q_per_kv")}
 
     def replace(self, **kw):
         return dataclasses.replace(self, **kw)
