@@ -91,7 +91,8 @@ typedef struct {
                                   the right of each head's block, reclaim the middle at the end pointer
                                   (one extra page when the plan needs it, reading Q29).  Same final
                                   classes, counts and page bytes; different page IDs and ring order. */
-  int32_t reserved[1];         /* must be zero */
+  int32_t q_per_kv;            /* NEXT-2 (dkv_attend): query heads per KV head, the GQA group;
+                                  0 = no attention; supported: 1, 2, 4, 5, 7, 8 */
 } dkv_config_t;
 
 /* 16-byte per-unit decision written by dkv_classify(DECODE); padding-free, compared byte for byte.
@@ -123,6 +124,9 @@ typedef struct {
   int32_t C[3], k_row[3], v_row[3], off_k[3], off_kmeta[3], off_v[3], off_vmeta[3], off_score[3], off_pos[3];
   int64_t off_tile_sums;       /* int64[num_tiles][3] scratch of the prompt workflow's scans */
   int64_t off_rec;             /* int32[units][3] scratch of the deferred recycle copy */
+  int64_t off_win_sig;         /* fp32[units][window]: significance of the window tokens (NEXT-2) */
+  int64_t off_secmin;          /* int32[units][8]: per-section (significance, position, slot) minima written by
+                                  dkv_attend, consumed by the next dkv_classify(DECODE) (NEXT-2) */
 } dkv_layout_t;
 
 /* Arena size for `cfg`, or 0 if the configuration is invalid. */
@@ -140,7 +144,8 @@ dkv_status_t dkv_pool_destroy(dkv_pool_t p);
 
 /* Planning.
  * DECODE : every ACTIVE request appends one token this step.  d_sig = device fp32[U]: significance of
- *          each unit's t_c (values for non-ACTIVE units are ignored).  Writes d_dec[U] (device).
+ *          each unit's t_c (values for non-ACTIVE units are ignored), or NULL: t_c's significance is the one
+ *          kept for its window slot (NEXT-2, maintained by dkv_attend).  Writes d_dec[U] (device).
  *          h_req/h_len/n/sig_stride/d_token_class unused (NULL/0).  DKV_ERR_STATE if an ACTIVE request
  *          already holds max_seq_len tokens.
  * PREFILL: admits host arrays h_req[0..n) (IDLE -> ADMITTING) with prompt lengths h_len[0..n) <= M.
@@ -173,6 +178,22 @@ dkv_status_t dkv_compact_alloc(dkv_pool_t p, const dkv_decision_t* d_dec, dkv_st
 dkv_status_t dkv_quant_write(dkv_pool_t p, int32_t phase, const dkv_decision_t* d_dec, const uint16_t* d_k,
                              const uint16_t* d_v, int64_t kv_stride, const float* d_sig, int64_t sig_stride,
                              dkv_stream_t s);
+
+/* NEXT-2 — decode attention over the compressed cache with the significance update (P:360-361, P:573-608,
+ * readings Q31-Q34 of DESIGN.md).  For every ACTIVE unit: the q_per_kv query heads d_q (device fp16 bits
+ * [U][q_per_kv][d], the newest token's queries) attend over the unit's stored tokens (keys and values
+ * dequantized from their pages, X^ = s*Q + z) and its FP16 window (which holds the newest token after
+ * dkv_quant_write(DECODE)); softmax(q.k / sqrt(d)); every token's significance becomes the running mean of
+ * the (max over the group) scores it received from later queries — in place, in the page score segments
+ * and the window's significance array — and each section's (significance, position) minimum is recorded so
+ * the next dkv_classify(DECODE) needs no scan.  d_out (device fp32 [U][q_per_kv][d]) receives the attention
+ * output, d_probs (device fp32 [U][max_seq_len]) the per-token scores (max over the group) in token order
+ * (high slots, low slots, window oldest first); either may be NULL.  Deterministic: every floating-point
+ * result is fixed by Q31-Q34 (bit-identical to the oracle).  Allowed between sequences; DKV_ERR_INVALID_ARG
+ * if q_per_kv is 0 / unsupported or q_per_kv * max_seq_len * 4 B of logits exceed shared memory.
+ * With NEXT-2 the decode step passes d_sig = NULL to dkv_classify / dkv_quant_write: t_c's significance is
+ * then read from the window. */
+dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* d_probs, dkv_stream_t s);
 
 /* Release: host array h_req[0..n) of ACTIVE requests -> PENDING_FREE (double free / not active ->
  * DKV_ERR_STATE).  Allowed between sequences only (after dkv_quant_write, before dkv_classify).  Pages are

@@ -92,6 +92,9 @@ struct PoolDev {
   FastDiv div_LyH, div_W, div_Ch, div_Cl;   // u -> request, position -> window slot, slot -> (page, index)
   int64_t* tile_sums;   // [num_tiles][3] prompt-workflow scan scratch
   int32_t* rec;         // [U][3] deferred recycle: {ring offset from the end pointer, ph, freed pages}
+  float* win_sig;       // [U][W] significance of the window tokens (NEXT-2)
+  int32_t* secmin;      // [U][8] {sig_h, pos_h, slot_h, sig_l, pos_l, slot_l, valid, 0} from dkv_attend
+  int32_t G;            // q_per_kv
   int32_t prefill_wf;   // dkv_config_t.prefill_workflow
 };
 
@@ -933,6 +936,8 @@ cudaError_t launch_classify_prefill(const PoolDev& p, int n, const float* sig, i
 cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s,
                                  bool alloc = true, bool defer_recycle = false);
 cudaError_t launch_recycle(const PoolDev& p, const int32_t* req, int n, cudaStream_t s);
+cudaError_t launch_attend(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s);
+size_t attend_smem_bytes(const PoolDev& p);
 cudaError_t launch_prefill_conservative(const PoolDev& p, cudaStream_t s);
 cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
                                 const float* sig, cudaStream_t s);

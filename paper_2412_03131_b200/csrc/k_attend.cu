@@ -1,0 +1,311 @@
+// k_attend.cu — NEXT-2: decode attention over the compressed cache with the significance update and the
+// victim search of the next step fused into its epilogue (readings Q31-Q34).
+//
+// One CTA per unit (request, layer, KV head), the paper's "one thread block per (head, sequence)".
+// The unit's tokens are taken in the normative order of Q31 — high section slots, low section slots, the
+// FP16 window oldest first — and every floating-point result is fixed by Q31-Q34, so the kernel matches the
+// oracle bit for bit:
+//   1. logits: one thread per token dequantizes its key (X^ = s*Q + z) and accumulates the G dot
+//      products serially over the d elements; logit = dot * (1/sqrt(d));
+//   2. softmax: max per head (order-free), p = dkv_exp(logit - max), Z = pages summed in order of their
+//      serial in-page sums (the window is one page), a = p / Z, score = max over the G heads;
+//   3. significance: sig' = (sig * c + score) / (c + 1), c = N - 2 - position (Q33), written in place
+//      (page score segment / window array, Q34); each section's (sig', position) minimum goes to the unit's
+//      secmin record, which lets the next dkv_classify(DECODE) pick its victim without a scan;
+//   4. output (optional): one thread per element e, serial over the tokens, all G heads at once.
+// Logits / probabilities live in shared memory (q_per_kv * max_seq_len floats).
+#include "dkv_internal.cuh"
+
+namespace dkv {
+
+constexpr int kAttThreads = 256;
+
+// Q32: exp for x <= 0 — 2^t, t = x*log2(e), n = rint(t), f = t - n, degree-6 Taylor polynomial of 2^f in
+// Horner form, times 2^n; 0 below t = -125.  Every step one IEEE binary32 operation (as the oracle's orc_exp).
+__device__ __forceinline__ float dkv_exp(float x) {
+  const float t = __fmul_rn(x, 1.44269504088896341f);
+  if (t < -125.0f) return 0.0f;
+  const float n = rintf(t);
+  const float f = __fsub_rn(t, n);
+  float r = 1.54035304e-4f;
+  r = __fadd_rn(__fmul_rn(r, f), 1.33335581e-3f);
+  r = __fadd_rn(__fmul_rn(r, f), 9.61812911e-3f);
+  r = __fadd_rn(__fmul_rn(r, f), 5.55041087e-2f);
+  r = __fadd_rn(__fmul_rn(r, f), 2.40226507e-1f);
+  r = __fadd_rn(__fmul_rn(r, f), 6.93147181e-1f);
+  r = __fadd_rn(__fmul_rn(r, f), 1.0f);
+  return __fmul_rn(r, __int_as_float(((int)n + 127) << 23));
+}
+
+__device__ __forceinline__ float dq(uint32_t code, float sf, float zf) {      // X^ = s*Q + z
+  return __fadd_rn(__fmul_rn(sf, __uint_as_float(0x4B000000u | code) - 8388608.0f), zf);
+}
+
+struct AttShared {
+  float* qf;        // [G][D]
+  float* lg;        // [G][M]  logits -> exp -> probabilities
+  float* part;      // [G][npage]
+  int32_t* pid;     // [ph + pl] page IDs, section order
+  uint32_t* vmeta;  // [M] value metadata of stored tokens
+};
+
+// Accumulate the G dot products of the query heads with one stored key of BITS-bit codes (serial over e).
+template <int D, int G, int BITS>
+__device__ __forceinline__ void dot_stored(const float* __restrict__ qf, const uint8_t* row, uint32_t kmeta,
+                                           float (&acc)[G]) {
+  const float sf = __half2float(__ushort_as_half((unsigned short)(kmeta & 0xFFFFu)));
+  const float zf = __half2float(__ushort_as_half((unsigned short)(kmeta >> 16)));
+  constexpr int PER = 32 / BITS;                                  // codes per 32-bit word
+  constexpr uint32_t Q = (1u << BITS) - 1u;
+#pragma unroll 1
+  for (int w = 0; w < D / PER; w += 4) {
+    const uint4 v = *reinterpret_cast<const uint4*>(row + 4 * w);
+    const uint32_t words[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+#pragma unroll
+      for (int j = 0; j < PER; j++) {
+        const int e = (w + k) * PER + j;
+        const float x = dq((words[k] >> (j * BITS)) & Q, sf, zf);
+#pragma unroll
+        for (int g = 0; g < G; g++) acc[g] = __fadd_rn(acc[g], __fmul_rn(qf[g * D + e], x));
+      }
+    }
+  }
+}
+
+template <int D, int G>
+__global__ void __launch_bounds__(kAttThreads)
+attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs) {
+  extern __shared__ __align__(16) float att_smem[];
+  __shared__ float s_red[kAttThreads / 32][G];
+  __shared__ float s_m[G], s_Z[G];
+  __shared__ unsigned long long s_min[2];
+  __shared__ int s_slot[2];
+  const int u = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (ld_volatile(&p.ctrl->status) != 0) return;                  // sticky error: no-op
+  const int r = fdiv(p.div_LyH, u);
+  if (p.req_state[r] != DKV_REQ_ACTIVE) return;
+  const int M = p.M, L = p.L, W = p.W;
+  const int N = p.seq_len[r];                                     // includes the newest token
+  const int nh = p.n_h[u], nl = p.n_l[u];
+  const int nw = min(W, N);
+  const int T = nh + nl + nw;
+  const int Ch = p.g[1].C, Cl = p.g[2].C;
+  const int ph = ceil_div(nh, Ch), pl = ceil_div(nl, Cl);
+  const int npage = ph + pl + (nw > 0 ? 1 : 0);
+  AttShared S;
+  S.qf = att_smem;
+  S.lg = S.qf + G * D;
+  S.part = S.lg + (size_t)G * M;
+  S.pid = reinterpret_cast<int32_t*>(S.part + (size_t)G * (L + 1));
+  S.vmeta = reinterpret_cast<uint32_t*>(S.pid + L);
+  const int32_t* row = p.table + (size_t)u * L;
+  for (int k = tid; k < ph + pl; k += kAttThreads) S.pid[k] = k < ph ? row[k] : row[L - 1 - (k - ph)];
+  for (int k = tid; k < G * D; k += kAttThreads)
+    S.qf[k] = __half2float(__ushort_as_half(q[(size_t)u * G * D + k]));
+  if (tid < 2) { s_min[tid] = ~0ull; s_slot[tid] = -1; }
+  __syncthreads();
+  const float scale = __fdiv_rn(1.0f, __fsqrt_rn((float)D));
+  const ClassGeom gh = p.g[1], gl = p.g[2];
+
+  // ---- 1. logits (Q31)
+  float mx[G];
+#pragma unroll
+  for (int g = 0; g < G; g++) mx[g] = -INFINITY;
+  for (int i = tid; i < T; i += kAttThreads) {
+    float acc[G];
+#pragma unroll
+    for (int g = 0; g < G; g++) acc[g] = 0.0f;
+    if (i < nh + nl) {
+      const bool hi = i < nh;
+      const ClassGeom& gg = hi ? gh : gl;
+      const int s = hi ? i : i - nh;
+      const int pg = hi ? fdiv(p.div_Ch, s) : ph + fdiv(p.div_Cl, s);
+      const int idx = hi ? s - (pg * Ch) : s - (pg - ph) * Cl;
+      const uint8_t* page = p.pages + (size_t)S.pid[pg] * (size_t)p.page_bytes;
+      const uint32_t km = *reinterpret_cast<const uint32_t*>(page + gg.off_kmeta + 4 * idx);
+      S.vmeta[i] = *reinterpret_cast<const uint32_t*>(page + gg.off_vmeta + 4 * idx);
+      const uint8_t* krow = page + gg.off_k + idx * gg.k_row;
+      if (gg.kbits == 8) dot_stored<D, G, 8>(S.qf, krow, km, acc);
+      else if (gg.kbits == 4) dot_stored<D, G, 4>(S.qf, krow, km, acc);
+      else dot_stored<D, G, 2>(S.qf, krow, km, acc);
+    } else {
+      const int pos = N - nw + (i - nh - nl);
+      const uint16_t* wk = reinterpret_cast<const uint16_t*>(p.win_k) + ((size_t)u * W + fmod_(p.div_W, pos)) * D;
+#pragma unroll 1
+      for (int e0 = 0; e0 < D; e0 += 8) {
+        const uint4 v = *reinterpret_cast<const uint4*>(wk + e0);
+        const uint32_t hw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const float x = __half2float(__ushort_as_half((unsigned short)(hw[k >> 1] >> (16 * (k & 1)))));
+#pragma unroll
+          for (int g = 0; g < G; g++) acc[g] = __fadd_rn(acc[g], __fmul_rn(S.qf[g * D + e0 + k], x));
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; g++) {
+      const float l = __fmul_rn(acc[g], scale);
+      S.lg[(size_t)g * M + i] = l;
+      mx[g] = fmaxf(mx[g], l);
+    }
+  }
+  // ---- 2. softmax (Q32)
+#pragma unroll
+  for (int g = 0; g < G; g++) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx[g] = fmaxf(mx[g], __shfl_xor_sync(kFull, mx[g], o));
+    if (lane == 0) s_red[warp][g] = mx[g];
+  }
+  __syncthreads();
+  if (tid < G) {
+    float m = -INFINITY;
+    for (int w = 0; w < kAttThreads / 32; w++) m = fmaxf(m, s_red[w][tid]);
+    s_m[tid] = m;
+  }
+  __syncthreads();
+  for (int i = tid; i < T; i += kAttThreads)
+#pragma unroll
+    for (int g = 0; g < G; g++) S.lg[(size_t)g * M + i] = dkv_exp(__fsub_rn(S.lg[(size_t)g * M + i], s_m[g]));
+  __syncthreads();
+  for (int it = tid; it < G * npage; it += kAttThreads) {          // serial in-page sums
+    const int g = it / npage, k = it % npage;
+    int t0, t1;
+    if (k < ph) { t0 = k * Ch; t1 = min(t0 + Ch, nh); }
+    else if (k < ph + pl) { t0 = nh + (k - ph) * Cl; t1 = min(t0 + Cl, nh + nl); }
+    else { t0 = nh + nl; t1 = T; }
+    float sum = 0.0f;
+    for (int i = t0; i < t1; i++) sum = __fadd_rn(sum, S.lg[(size_t)g * M + i]);
+    S.part[g * (L + 1) + k] = sum;
+  }
+  __syncthreads();
+  if (tid < G) {                                                  // pages in order
+    float Z = 0.0f;
+    for (int k = 0; k < npage; k++) Z = __fadd_rn(Z, S.part[tid * (L + 1) + k]);
+    s_Z[tid] = Z;
+  }
+  __syncthreads();
+
+  // ---- 3. scores, significance (Q33, Q34), section minima
+  for (int i = tid; i < T; i += kAttThreads) {
+    float a = 0.0f;
+#pragma unroll
+    for (int g = 0; g < G; g++) {
+      const float ag = __fdiv_rn(S.lg[(size_t)g * M + i], s_Z[g]);
+      S.lg[(size_t)g * M + i] = ag;
+      a = fmaxf(a, ag);                                           // GQA: max over the group
+    }
+    if (probs) probs[(size_t)u * M + i] = a;
+    float* sp;
+    int pos, cls = 0, slot = 0;
+    if (i < nh + nl) {
+      const bool hi = i < nh;
+      const ClassGeom& gg = hi ? gh : gl;
+      slot = hi ? i : i - nh;
+      const int pg = hi ? fdiv(p.div_Ch, slot) : ph + fdiv(p.div_Cl, slot);
+      const int idx = hi ? slot - pg * Ch : slot - (pg - ph) * Cl;
+      uint8_t* page = p.pages + (size_t)S.pid[pg] * (size_t)p.page_bytes;
+      sp = reinterpret_cast<float*>(page + gg.off_score + 4 * idx);
+      pos = *reinterpret_cast<const int32_t*>(page + gg.off_pos + 4 * idx);
+      cls = hi ? 1 : 2;
+    } else {
+      pos = N - nw + (i - nh - nl);
+      sp = p.win_sig + (size_t)u * W + fmod_(p.div_W, pos);
+    }
+    float sg = *sp;
+    const int c = N - 2 - pos;                                    // later queries so far
+    if (c >= 0) {
+      sg = __fdiv_rn(__fadd_rn(__fmul_rn(sg, (float)c), a), (float)(c + 1));
+      *sp = sg;
+    }
+    if (cls) atomicMin(&s_min[cls - 1], ((unsigned long long)__float_as_uint(sg) << 32) | (uint32_t)pos);
+  }
+  __syncthreads();
+  for (int i = tid; i < nh + nl; i += kAttThreads) {             // slot of each section's minimum
+    const bool hi = i < nh;
+    const int slot = hi ? i : i - nh;
+    const int pg = hi ? fdiv(p.div_Ch, slot) : ph + fdiv(p.div_Cl, slot);
+    const ClassGeom& gg = hi ? gh : gl;
+    const int idx = hi ? slot - pg * Ch : slot - (pg - ph) * Cl;
+    const uint8_t* page = p.pages + (size_t)S.pid[pg] * (size_t)p.page_bytes;
+    const int pos = *reinterpret_cast<const int32_t*>(page + gg.off_pos + 4 * idx);
+    if ((uint32_t)pos == (uint32_t)(s_min[hi ? 0 : 1] & 0xFFFFFFFFull)) s_slot[hi ? 0 : 1] = slot;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int32_t* m = p.secmin + 8 * (size_t)u;
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      m[3 * c] = (int32_t)(uint32_t)(s_min[c] >> 32);
+      m[3 * c + 1] = (int32_t)(uint32_t)(s_min[c] & 0xFFFFFFFFull);
+      m[3 * c + 2] = s_slot[c];
+    }
+    m[6] = 1;
+  }
+  // ---- 4. output (Q32): serial over tokens, one thread per element, all heads
+  if (out != nullptr && tid < D) {
+    const int e = tid;
+    float acc[G];
+#pragma unroll
+    for (int g = 0; g < G; g++) acc[g] = 0.0f;
+    for (int i = 0; i < T; i++) {
+      float x;
+      if (i < nh + nl) {
+        const bool hi = i < nh;
+        const ClassGeom& gg = hi ? gh : gl;
+        const int slot = hi ? i : i - nh;
+        const int pg = hi ? fdiv(p.div_Ch, slot) : ph + fdiv(p.div_Cl, slot);
+        const int idx = hi ? slot - pg * Ch : slot - (pg - ph) * Cl;
+        const uint8_t* vrow = p.pages + (size_t)S.pid[pg] * (size_t)p.page_bytes + gg.off_v + idx * gg.v_row;
+        const int bit = e * gg.vbits;
+        const uint32_t code = ((uint32_t)vrow[bit >> 3] >> (bit & 7)) & ((1u << gg.vbits) - 1u);
+        const uint32_t vm = S.vmeta[i];
+        x = dq(code, __half2float(__ushort_as_half((unsigned short)(vm & 0xFFFFu))),
+               __half2float(__ushort_as_half((unsigned short)(vm >> 16))));
+      } else {
+        const int pos = N - nw + (i - nh - nl);
+        x = __half2float(p.win_v[((size_t)u * W + fmod_(p.div_W, pos)) * D + e]);
+      }
+#pragma unroll
+      for (int g = 0; g < G; g++) acc[g] = __fadd_rn(acc[g], __fmul_rn(S.lg[(size_t)g * M + i], x));
+    }
+#pragma unroll
+    for (int g = 0; g < G; g++) out[((size_t)u * G + g) * D + e] = acc[g];
+  }
+}
+
+size_t attend_smem_bytes(const PoolDev& p) {
+  const size_t G = p.G > 0 ? p.G : 1;
+  return 4 * (G * p.d + G * (size_t)p.M + G * (size_t)(p.L + 1) + (size_t)p.L + (size_t)p.M);
+}
+
+template <int D, int G>
+static cudaError_t launch_att(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s) {
+  const size_t smem = attend_smem_bytes(p);
+  cudaError_t e = cudaFuncSetAttribute(attend_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  attend_kernel<D, G><<<p.U, kAttThreads, smem, s>>>(p, q, out, probs);
+  return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_att_d(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s) {
+  switch (p.G) {
+    case 1: return launch_att<D, 1>(p, q, out, probs, s);
+    case 2: return launch_att<D, 2>(p, q, out, probs, s);
+    case 4: return launch_att<D, 4>(p, q, out, probs, s);
+    case 5: return launch_att<D, 5>(p, q, out, probs, s);
+    case 7: return launch_att<D, 7>(p, q, out, probs, s);
+    case 8: return launch_att<D, 8>(p, q, out, probs, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_attend(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s) {
+  return p.d == 128 ? launch_att_d<128>(p, q, out, probs, s) : launch_att_d<64>(p, q, out, probs, s);
+}
+
+}  // namespace dkv

@@ -327,8 +327,10 @@ quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const u
       const size_t w = ((size_t)u * p.W + (t % p.W)) * D + cc * 8;
       *reinterpret_cast<uint4*>(p.win_k + w) = a;
       *reinterpret_cast<uint4*>(p.win_v + w) = b;
+      if (cc == 0) p.win_sig[(size_t)u * p.W + (t % p.W)] = canon_zero(__ldg(srow + t));   // P:360, Q33
     }
   }
+  if (seg == 0 && lane == 0) p.secmin[8 * (size_t)u + 6] = 0;   // no dkv_attend minima for a new prompt
   if (__any_sync(kFull, bad) && lane == 0) set_status(p.ctrl, DKV_ERR_NONFINITE);
 }
 

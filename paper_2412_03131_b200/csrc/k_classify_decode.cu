@@ -45,7 +45,9 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   {
     const int8_t st = p.req_state[r];
     const int N = p.seq_len[r] + 1;                              // Q3: includes this step's token
-    const float s_in = cand_sig[u];
+    // t_c's significance: given, or (NEXT-2, cand_sig NULL) the running mean kept for its window slot
+    const float s_in = cand_sig ? cand_sig[u]
+                                : (p.W > 0 && N - 1 - p.W >= 0 ? p.win_sig[(size_t)u * p.W + (N - 1 - p.W) % p.W] : 0.0f);
     const int nh_in = p.n_h[u], nl_in = p.n_l[u];
     const int pc = N - 1 - p.W;                                  // t_c = earliest window token
     if (st == DKV_REQ_ACTIVE && pc >= 0) {
@@ -68,7 +70,14 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   }
   int vs = -1;                                                   // victim slot, -1 = t_c itself
   uint32_t vb = 0xFFFFFFFFu;
-  if (scan && n > 0) {                                           // warp-uniform
+  // NEXT-2: dkv_attend recorded each section's (significance, position) minimum after its update and no
+  // section changed since (quant_write clears the flag): the victim needs no scan
+  const bool fused = scan && n > 0 && p.secmin[8 * (size_t)u + 6] == 1;
+  if (fused) {
+    const int b = cls == DKV_CLS_HIGH ? 0 : 3;
+    vb = (uint32_t)p.secmin[8 * (size_t)u + b];
+    vs = p.secmin[8 * (size_t)u + b + 2];
+  } else if (scan && n > 0) {                                    // warp-uniform
     const int C = cls == DKV_CLS_HIGH ? p.g[1].C : p.g[2].C;
     const int off_score = cls == DKV_CLS_HIGH ? p.g[1].off_score : p.g[2].off_score;
     const bool pow2 = (C & (C - 1)) == 0;

@@ -291,7 +291,7 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
     const int8_t st = rc.st[r];
     const int N = rc.len[r];                             // already includes this step's token (compact_alloc)
     const int4 dw = __ldg(reinterpret_cast<const int4*>(dec) + u);
-    const float s_in = __ldg(cand_sig + u);
+    const float s_in_given = cand_sig ? __ldg(cand_sig + u) : 0.0f;
     stage_row<EPL>(my_nk, knew + (size_t)u * D + q * EPL);
     stage_row<EPL>(my_nv, vnew + (size_t)u * D + q * EPL);
     cp_async_commit();
@@ -320,6 +320,8 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
       wk = load_hvec<EPL>(wk_row, q);
       wv = load_hvec<EPL>(wv_row, q);
     }
+    // t_c's significance: given, or (NEXT-2, cand_sig NULL) the running mean kept for its window slot
+    const float s_in = cand_sig ? s_in_given : (p.W > 0 && live ? p.win_sig[(size_t)u * p.W + fmod_(p.div_W, N - 1)] : 0.0f);
     const int gl = lane & ~(G - 1);
     const int pid_tc = __shfl_sync(gmask, pid, gl);
     const int pid_src = __shfl_sync(gmask, pid, gl + 1);
@@ -378,9 +380,11 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
       }
     }
     // 3. window push, after t_c's row has been consumed
+    if (live && q == 0) p.secmin[8 * (size_t)u + 6] = 0;    // section minima of dkv_attend no longer valid
     if (wk_row != nullptr && !rejected) {
       store_hvec<EPL>(wk_row, q, lds_hvec<EPL>(my_nk));
       store_hvec<EPL>(wv_row, q, lds_hvec<EPL>(my_nv));
+      if (q == 0) p.win_sig[(size_t)u * p.W + fmod_(p.div_W, N - 1)] = 0.0f;   // the new token (Q33)
     }
   }
 }

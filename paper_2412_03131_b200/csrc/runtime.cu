@@ -51,7 +51,7 @@ bool validate(const dkv_config_t* c, Geometry& G) {
   if (c->prompt_denominator != 0 && c->prompt_denominator != 1) return false;
   if (c->tile_units != 0 && c->tile_units != 256 && c->tile_units != 512 && c->tile_units != 1024) return false;
   if (c->prefill_workflow != 0 && c->prefill_workflow != 1) return false;
-  if (c->reserved[0]) return false;
+  if (c->q_per_kv < 0 || c->q_per_kv > 16) return false;
   const int64_t U = (int64_t)c->max_requests * c->num_layers * c->num_kv_heads;
   if (U >= (1 << 24)) return false;
   G.U = (int32_t)U;
@@ -80,6 +80,8 @@ bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
   Lo.off_tile_status = take(8 * (int64_t)G.num_tiles);
   Lo.off_tile_sums = take(24 * (int64_t)G.num_tiles);
   Lo.off_rec = take(12 * (int64_t)G.U);
+  Lo.off_win_sig = take(4 * (int64_t)G.U * c->window);
+  Lo.off_secmin = take(32 * (int64_t)G.U);
   Lo.off_ring = take(4 * P);
   Lo.off_table = take(4 * U * G.L);
   Lo.off_n_h = take(4 * U);
@@ -219,6 +221,9 @@ dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_
   d.tile_status = (unsigned long long*)(b + Lo.off_tile_status);
   d.tile_sums = (int64_t*)(b + Lo.off_tile_sums);
   d.rec = (int32_t*)(b + Lo.off_rec);
+  d.win_sig = (float*)(b + Lo.off_win_sig);
+  d.secmin = (int32_t*)(b + Lo.off_secmin);
+  d.G = cfg->q_per_kv;
   d.prefill_wf = cfg->prefill_workflow;
   d.ring = (int32_t*)(b + Lo.off_ring);
   d.table = (int32_t*)(b + Lo.off_table);
@@ -237,9 +242,9 @@ dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_
   cudaError_t e = cudaMemsetAsync(b + Lo.off_pages, 0, (size_t)(Lo.arena_bytes - Lo.off_pages), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(b + Lo.off_win_k, 0, (size_t)(Lo.off_pages - Lo.off_win_k), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(b + Lo.off_pf_seg, 0, (size_t)(Lo.off_win_k - Lo.off_pf_seg), s);
-  // control block, counters and scan / workflow / recycle scratch start zeroed (every byte initialised)
+  // control block, counters, scan / workflow / recycle scratch, window significance and section minima
+  // (everything laid out before the ring) start zeroed: every byte initialised
   if (e == cudaSuccess) e = cudaMemsetAsync(b, 0, (size_t)Lo.off_ring, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(b + Lo.off_rec, 0, 12 * (size_t)G.U, s);
   if (e == cudaSuccess) e = launch_init(d, s);
   if (e != cudaSuccess) {
     dkv_pool_destroy(p);
@@ -266,7 +271,7 @@ dkv_status_t dkv_classify(dkv_pool_t p, int32_t phase, const int32_t* h_req, con
   if (p->seq != SEQ_IDLE && !(p->recovering && p->phase == DKV_PHASE_DECODE)) return DKV_ERR_STATE;
   const int R = p->cfg.max_requests;
   if (phase == DKV_PHASE_DECODE) {
-    if (!d_sig || !d_dec) return DKV_ERR_INVALID_ARG;
+    if (!d_dec) return DKV_ERR_INVALID_ARG;              // d_sig NULL: t_c's significance from the window
     for (int r = 0; r < R; r++)
       if (p->req_state[r] == DKV_REQ_ACTIVE && p->seq_len[r] >= p->cfg.max_seq_len) return DKV_ERR_STATE;
     cudaError_t e = launch_classify_decode(p->dev, d_sig, d_dec, (cudaStream_t)s);
@@ -337,7 +342,7 @@ dkv_status_t dkv_quant_write(dkv_pool_t p, int32_t phase, const dkv_decision_t* 
   if (p->seq != SEQ_COMPACTED || phase != p->phase) return DKV_ERR_STATE;
   cudaError_t e;
   if (phase == DKV_PHASE_DECODE) {
-    if (!d_dec || !d_k || !d_v || !d_sig) return DKV_ERR_INVALID_ARG;
+    if (!d_dec || !d_k || !d_v) return DKV_ERR_INVALID_ARG;
     e = launch_quant_decode(p->dev, d_dec, d_k, d_v, d_sig, (cudaStream_t)s);
   } else {
     const int n = (int)p->admitted.size();
@@ -353,6 +358,20 @@ dkv_status_t dkv_quant_write(dkv_pool_t p, int32_t phase, const dkv_decision_t* 
   p->seq = SEQ_IDLE;
   p->recovering = false;
   return DKV_OK;
+}
+
+dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* d_probs, dkv_stream_t s) {
+  if (!p || !d_q) return DKV_ERR_INVALID_ARG;
+  if (p->seq != SEQ_IDLE) return DKV_ERR_STATE;                // between sequences only
+  const int G = p->cfg.q_per_kv;
+  if (!(G == 1 || G == 2 || G == 4 || G == 5 || G == 7 || G == 8)) return DKV_ERR_INVALID_ARG;
+  int dev = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+    return DKV_ERR_CUDA;
+  if (attend_smem_bytes(p->dev) > (size_t)optin) return DKV_ERR_INVALID_ARG;
+  cudaError_t e = launch_attend(p->dev, d_q, d_out, d_probs, (cudaStream_t)s);
+  return e == cudaSuccess ? DKV_OK : DKV_ERR_CUDA;
 }
 
 dkv_status_t dkv_free(dkv_pool_t p, const int32_t* h_req, int32_t n, dkv_stream_t s) {

@@ -26,7 +26,7 @@ DKV_REQ_IDLE, DKV_REQ_ADMITTING, DKV_REQ_ACTIVE, DKV_REQ_PENDING_FREE = 0, 1, 2,
 
 EXPORTED = ("dkv_arena_bytes", "dkv_pool_layout", "dkv_pool_init", "dkv_pool_destroy", "dkv_classify",
             "dkv_compact_alloc", "dkv_quant_write", "dkv_free", "dkv_pool_query", "dkv_pool_stats_device_ptr",
-            "dkv_status_string")
+            "dkv_status_string", "dkv_attend")
 
 
 class DkvError(RuntimeError):
@@ -40,7 +40,7 @@ class dkv_config_t(C.Structure):
         "max_requests", "num_layers", "num_kv_heads", "head_dim", "max_seq_len", "window", "page_tokens_high",
         "page_tokens_low", "kbits_high", "vbits_high", "kbits_low", "vbits_low", "num_pages")] + \
         [("alpha_h", C.c_float), ("alpha_l", C.c_float), ("prompt_denominator", C.c_int32),
-         ("tile_units", C.c_int32), ("prefill_workflow", C.c_int32), ("reserved", C.c_int32 * 1)]
+         ("tile_units", C.c_int32), ("prefill_workflow", C.c_int32), ("q_per_kv", C.c_int32)]
 
 
 class dkv_decision_t(C.Structure):
@@ -61,7 +61,8 @@ class dkv_layout_t(C.Structure):
         "off_win_v", "off_pages", "off_stats")] + [(n, C.c_int32) for n in (
         "units", "table_len", "page_bytes", "num_tiles", "tile_units", "seg_tokens", "num_segs")] + \
         [(n, C.c_int32 * 3) for n in ("C", "k_row", "v_row", "off_k", "off_kmeta", "off_v", "off_vmeta",
-                                       "off_score", "off_pos")] + [("off_tile_sums", C.c_int64), ("off_rec", C.c_int64)]
+                                       "off_score", "off_pos")] + [("off_tile_sums", C.c_int64), ("off_rec", C.c_int64),
+                                                                  ("off_win_sig", C.c_int64), ("off_secmin", C.c_int64)]
 
 
 assert C.sizeof(dkv_decision_t) == 16
@@ -84,13 +85,14 @@ _lib.dkv_classify.argtypes = [_vp, C.c_int32, _vp, _vp, C.c_int32, _vp, C.c_int6
 _lib.dkv_compact_alloc.argtypes = [_vp, _vp, _vp]
 _lib.dkv_quant_write.argtypes = [_vp, C.c_int32, _vp, _vp, _vp, C.c_int64, _vp, C.c_int64, _vp]
 _lib.dkv_free.argtypes = [_vp, _vp, C.c_int32, _vp]
+_lib.dkv_attend.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _lib.dkv_pool_query.argtypes = [_vp, _P(dkv_stats_t), _vp]
 _lib.dkv_pool_stats_device_ptr.argtypes = [_vp]
 _lib.dkv_pool_stats_device_ptr.restype = _vp
 _lib.dkv_status_string.argtypes = [C.c_int32]
 _lib.dkv_status_string.restype = C.c_char_p
 for _f in ("dkv_pool_layout", "dkv_pool_init", "dkv_pool_destroy", "dkv_classify", "dkv_compact_alloc",
-           "dkv_quant_write", "dkv_free", "dkv_pool_query"):
+           "dkv_quant_write", "dkv_free", "dkv_pool_query", "dkv_attend"):
     getattr(_lib, _f).restype = C.c_int32
 
 
@@ -177,6 +179,10 @@ def dkv_quant_write(pool, phase, d_dec, d_k, d_v, kv_stride, d_sig, sig_stride, 
                                                           _dev(d_sig), sig_stride, _stream(stream)))
 
 
+def dkv_attend(pool, d_q, d_out, d_probs, stream=None) -> int:
+    return _check("dkv_attend", _lib.dkv_attend(pool, _dev(d_q), _dev(d_out), _dev(d_probs), _stream(stream)))
+
+
 def dkv_free(pool, h_req, n, stream=None) -> int:
     req, preq = _host_i32(h_req)
     return _check("dkv_free", _lib.dkv_free(pool, preq, n, _stream(stream)))
@@ -200,10 +206,10 @@ def dkv_status_string(st) -> str:
 
 
 def make_config(R, Ly, H, d, M, W, Ch=16, Cl=32, kbh=8, vbh=4, kbl=4, vbl=2, P=1024, alpha_h=1.0, alpha_l=0.02,
-                prompt_denominator=0, tile_units=0, prefill_workflow=0) -> dkv_config_t:
+                prompt_denominator=0, tile_units=0, prefill_workflow=0, q_per_kv=0) -> dkv_config_t:
     c = dkv_config_t(max_requests=R, num_layers=Ly, num_kv_heads=H, head_dim=d, max_seq_len=M, window=W,
                      page_tokens_high=Ch, page_tokens_low=Cl, kbits_high=kbh, vbits_high=vbh, kbits_low=kbl,
                      vbits_low=vbl, num_pages=P, alpha_h=alpha_h, alpha_l=alpha_l,
                      prompt_denominator=prompt_denominator, tile_units=tile_units,
-                     prefill_workflow=prefill_workflow)
+                     prefill_workflow=prefill_workflow, q_per_kv=q_per_kv)
     return c

@@ -55,6 +55,10 @@ class Pool:
         return _d.dkv_quant_write(self.handle, _d.DKV_PHASE_PREFILL, None, k, v, k.shape[-2], sig, sig.shape[-1],
                                   stream or self.stream)
 
+    def attend(self, q, out=None, probs=None, stream=None):
+        """NEXT-2: q = fp16 (as int16) [U][q_per_kv][d] CUDA tensor; out fp32 [U][G][d] / probs fp32 [U][M] or None"""
+        return _d.dkv_attend(self.handle, q, out, probs, stream or self.stream)
+
     def free(self, reqs, stream=None):
         return _d.dkv_free(self.handle, reqs, len(reqs), stream or self.stream)
 
@@ -85,6 +89,8 @@ class Pool:
             win_v=self._view(L.off_win_v, 2 * U * W * d, torch.int16, (U, W, d)),
             pages=self._view(L.off_pages, P * self.page_bytes, torch.uint8, (P, self.page_bytes)),
             stats=self._view(L.off_stats, 32, torch.int64, (4,)),
+            win_sig=self._view(L.off_win_sig, 4 * U * W, torch.float32, (U, W)),
+            secmin=self._view(L.off_secmin, 32 * U, torch.int32, (U, 8)),
         )
 
     def geom(self):

@@ -16,7 +16,7 @@ class GpuBackend:
         self.scn = scn
         cfg = D.make_config(scn.R, scn.Ly, scn.H, scn.d, scn.M, scn.W, scn.Ch, scn.Cl, scn.kbh, scn.vbh, scn.kbl,
                             scn.vbl, scn.P, scn.alpha_h, scn.alpha_l, scn.prompt_denominator, scn.tile_units,
-                            scn.prefill_workflow)
+                            scn.prefill_workflow, scn.q_per_kv)
         self.pool = Pool(cfg, device=device)
         self.U, self.L, self.page_bytes = self.pool.U, self.pool.L, self.pool.page_bytes
         self.v = self.pool.views()
@@ -30,7 +30,7 @@ class GpuBackend:
         return x.to(self.device).contiguous()
 
     def classify_decode(self, cand):
-        self._cand = self._cuda(cand.float() if isinstance(cand, torch.Tensor) else cand)
+        self._cand = None if cand is None else self._cuda(cand.float() if isinstance(cand, torch.Tensor) else cand)
         self.pool.classify_decode(self._cand, self.dec)
         return 0, self.dec
 
@@ -45,8 +45,17 @@ class GpuBackend:
 
     def quant_write_decode(self, dec, k, v, cand):
         k, v = self._cuda(k).view(torch.int16), self._cuda(v).view(torch.int16)
-        self.pool.quant_write_decode(dec, k, v, self._cuda(cand))
+        self.pool.quant_write_decode(dec, k, v, None if cand is None else self._cuda(cand))
         return 0
+
+    def attend(self, q, want_out=True, want_probs=False):
+        G, d, M = self.scn.q_per_kv, self.scn.d, self.scn.M
+        qd = self._cuda(np.ascontiguousarray(q).view(np.int16))
+        out = torch.zeros((self.U, G, d), dtype=torch.float32, device=self.device) if want_out else None
+        probs = torch.zeros((self.U, M), dtype=torch.float32, device=self.device) if want_probs else None
+        self.pool.attend(qd, out, probs)
+        torch.cuda.synchronize()
+        return 0, (out.cpu().numpy() if want_out else None), (probs.cpu().numpy() if want_probs else None)
 
     def quant_write_prefill(self, k, v, sig):
         k, v = self._cuda(k).view(torch.int16), self._cuda(v).view(torch.int16)
@@ -75,7 +84,7 @@ class GpuBackend:
                  status=int(ctrl[2] & 0xFFFFFFFF), table=v["table"].cpu().numpy(), n_h=v["n_h"].cpu().numpy(),
                  n_l=v["n_l"].cpu().numpy(), req_state=v["req_state"].cpu().numpy(),
                  seq_len=v["seq_len"].cpu().numpy(), win_k=v["win_k"].cpu().numpy().view(np.uint16),
-                 win_v=v["win_v"].cpu().numpy().view(np.uint16))
+                 win_v=v["win_v"].cpu().numpy().view(np.uint16), win_sig=v["win_sig"].cpu().numpy())
         if pages:
             s["pages"] = v["pages"].cpu().numpy()
         return s
@@ -88,6 +97,7 @@ def dec_np(dec):
 
 
 def compare_state(a, b, keys=("ring", "start", "free", "table", "n_h", "n_l", "req_state", "seq_len", "win_k", "win_v",
+                              "win_sig",
                               "pages"), where=""):
     for k in keys:
         if k not in a or k not in b:

@@ -117,7 +117,7 @@ class OracleBackend:
                              off_score=g[c].off_score, off_pos=g[c].off_pos) for c in (1, 2)}
 
     def classify_decode(self, cand):
-        return self.pool.classify_decode(_np(cand))
+        return self.pool.classify_decode(None if cand is None else _np(cand))
 
     def classify_prefill(self, reqs, lens, sig):
         st, _ = self.pool.classify_prefill(reqs, lens, _np(sig), want_classes=False)
@@ -127,7 +127,10 @@ class OracleBackend:
         return self.pool.compact_alloc(None if dec is None else _np(dec))
 
     def quant_write_decode(self, dec, k, v, cand):
-        return self.pool.quant_write_decode(_np(dec), _np(k), _np(v), _np(cand))
+        return self.pool.quant_write_decode(_np(dec), _np(k), _np(v), None if cand is None else _np(cand))
+
+    def attend(self, q, want_out=True, want_probs=False):
+        return self.pool.attend(q, want_out=want_out, want_probs=want_probs)
 
     def quant_write_prefill(self, k, v, sig):
         return self.pool.quant_write_prefill(_np(k), _np(v), _np(sig))
@@ -149,7 +152,7 @@ class OracleBackend:
         p = self.pool
         s = dict(ring=p.ring.copy(), start=int(p.start), free=int(p.free), table=p.table.copy(),
                  n_h=p.n_h.copy(), n_l=p.n_l.copy(), req_state=p.req_state.copy(), seq_len=p.seq_len.copy(),
-                 win_k=p.win_k.copy(), win_v=p.win_v.copy())
+                 win_k=p.win_k.copy(), win_v=p.win_v.copy(), win_sig=p.win_sig.copy())
         if pages:
             s["pages"] = p.pages.copy()
         return s
