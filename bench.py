@@ -39,9 +39,9 @@ import synth  # noqa: E402
 
 CONFIGS = {
     "llama3_8b": dict(R=64, Ly=32, H=8, d=128, prompt=4096, M=8192, W=64, Ch=16, Cl=32, P=1 << 22,
-                      alpha_h=1.0, alpha_l=0.02, mix=(0.35, 0.45, 0.20), seed=2),
+                      alpha_h=1.0, alpha_l=0.02, mix=(0.35, 0.45, 0.20), seed=2, G=4),
     "tiny": dict(R=4, Ly=2, H=4, d=64, prompt=64, M=128, W=16, Ch=16, Cl=32, P=1024,
-                 alpha_h=1.0, alpha_l=0.02, mix=(0.35, 0.45, 0.20), seed=1),
+                 alpha_h=1.0, alpha_l=0.02, mix=(0.35, 0.45, 0.20), seed=1, G=4),
 }
 METRIC = "µs per decode-step compact+alloc (64 req×32L×8H); quant-write GB/s vs HBM peak, 1/2/4/8 GPU"
 
@@ -226,7 +226,8 @@ def run_ours(args, rank, world, local):
     dev = torch.device("cuda", local)
     wl = Workload(c, rank, world, dev)
     cfg = D.make_config(wl.R, c["Ly"], wl.Hl, c["d"], c["M"], c["W"], c["Ch"], c["Cl"], P=c["P"],
-                        alpha_h=c["alpha_h"], alpha_l=c["alpha_l"], tile_units=args.tile_units)
+                        alpha_h=c["alpha_h"], alpha_l=c["alpha_l"], tile_units=args.tile_units,
+                        q_per_kv=c.get("G", 0))
     pool = Pool(cfg, device=dev)
     geom = pool.geom()
     T = c["prompt"]
@@ -391,6 +392,67 @@ def run_ours(args, rank, world, local):
     st, stats = pool.query()
     assert st == 0, f"device status {st} after e2e"
 
+    # ---------------- NEXT-2: decode steps driven by the attention kernel's significance
+    next2 = None
+    if args.next2 and c.get("G", 0) > 0:
+        G, d = c["G"], c["d"]
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(c["seed"] + rank)
+        qbuf = torch.empty((wl.U, G, d), dtype=torch.float16, device=dev)
+        obuf = torch.empty((wl.U, G, d), dtype=torch.float32, device=dev)
+        att_us, cls2_us, step2_us, att_bytes = [], [], [], []
+        v = pool.views()
+        qbuf.normal_(generator=gen)
+        pool.attend(qbuf.view(torch.int16), obuf)                 # primes the window significance + minima
+        for s in range(args.warmup + args.steps):
+            timed = s >= args.warmup
+            cand, nk, nv = wl.decode_inputs(seq, active)
+            qbuf.normal_(generator=gen)
+            nh0, nl0 = v["n_h"].clone(), v["n_l"].clone()
+            flush.zero_()
+            torch.cuda.synchronize()
+            barrier(world)
+            e = [ev() for _ in range(5)]
+            torch.cuda._sleep(200_000)
+            e[0].record()
+            pool.classify_decode(None, dec)
+            e[1].record()
+            pool.compact_alloc(dec)
+            e[2].record()
+            pool.quant_write_decode(dec, nk.view(torch.int16), nv.view(torch.int16), None)
+            e[3].record()
+            pool.attend(qbuf.view(torch.int16), obuf)
+            e[4].record()
+            torch.cuda.synchronize()
+            seq[active] += 1
+            if timed:
+                cls2_us.append(e[0].elapsed_time(e[1]) * 1e3)
+                att_us.append(e[3].elapsed_time(e[4]) * 1e3)
+                step2_us.append(e[0].elapsed_time(e[4]) * 1e3)
+                launches += 4
+                # algorithmic bytes of one attention pass: every stored token's K/V codes, metadata, position and
+                # score (read + write back), every window token's fp16 K/V and significance (read + write),
+                # the queries and the output
+                nh1, nl1 = v["n_h"].long(), v["n_l"].long()
+                gh_, gl_ = geom[1], geom[2]
+                per_h = gh_["k_row"] + gh_["v_row"] + 8 + 4 + 4 + 4
+                per_l = gl_["k_row"] + gl_["v_row"] + 8 + 4 + 4 + 4
+                nwin = min(c["W"], int(seq.max()))
+                att_bytes.append(int((nh1.sum() * per_h + nl1.sum() * per_l).item())
+                                 + wl.U * (nwin * (4 * d + 8) + G * d * 2 + G * d * 4))
+        st, _ = pool.query()
+        assert st == 0, f"device status {st} after the NEXT-2 steps"
+        att_mean = max_over_ranks(statistics.mean(att_us), world)
+        att_gbs = statistics.mean(att_bytes) / (statistics.mean(att_us) * 1e-6) / 1e9
+        next2 = {"attend_us": round(att_mean, 1), "attend_gbs": round(att_gbs, 1),
+                 "attend_frac_of_hbm_peak": round(att_gbs / load_peaks()[0], 4),
+                 "attend_algorithmic_bytes": int(statistics.mean(att_bytes)),
+                 "classify_fused_us": round(max_over_ranks(statistics.mean(cls2_us), world), 3),
+                 "step_us": round(max_over_ranks(statistics.mean(step2_us), world), 1),
+                 "q_per_kv": G,
+                 "note": "dkv_attend (NEXT-2) supplies significance; classify takes its victims from the "
+                         "attention kernel's section minima (no scan)"}
+
     # ---------------- aggregate (max over ranks)
     comp_mean = max_over_ranks(statistics.mean(comp_us), world)
     step_mean = max_over_ranks(statistics.mean(step_us), world)
@@ -444,6 +506,7 @@ def run_ours(args, rank, world, local):
         "e2e": {"value": round(e2e_mean, 3), "unit": "us per decode step (H2D inputs + classify + compact_alloc + "
                                                      "quant_write + D2H decisions)",
                 "h2d_bytes_per_step": wl.U * (4 + 2 * 2 * c["d"]), "d2h_bytes_per_step": wl.U * 16},
+        "next2": next2,
         "gpu_launches": launches,
         "clocks": clocks,
         "wall_s": round(wall, 1),
@@ -551,6 +614,7 @@ def main():
     ap.add_argument("--config", default="llama3_8b", choices=sorted(CONFIGS))
     ap.add_argument("--tile-units", type=int, default=0, help="compact_alloc scan tile (0 = library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--next2", type=int, default=1, help="also time NEXT-2 decode steps (dkv_attend)")
     args = ap.parse_args()
     assert args.warmup >= 1
     if args.impl == "reference":

@@ -681,11 +681,12 @@ int32_t orc_free(orc_pool* p, const int32_t* req, int32_t n) {
  * Eq. 1 for the query of the newest token (position N-1) of every ACTIVE unit, G = q_per_kv
  * query heads sharing the KV head (GQA), over the unit's stored tokens (keys dequantized,
  * X^ = s*Q + z) and its FP16 window; every floating-point result is fixed by readings Q31-Q34:
- *   Q31 logit = fmul(dot, 1/sqrt(d)) with dot = serial sum over elements e = 0..d-1 of fmul(q_e, k_e);
+ *   Q31 logit = fmul(dot, 1/sqrt(d)) with dot = serial fused multiply-add chain over elements e = 0..d-1,
+ *       dot = fma(q_e, k_e, dot) from 0 (one rounding per element);
  *       tokens in the order: high slots 0..n_h-1, low slots 0..n_l-1, window oldest -> newest;
  *   Q32 p = exp(logit - max) with orc_exp (round-to-nearest range reduction + degree-6 polynomial, fixed
  *       operation order); Z = sum over pages in that order of the serial in-page sums (the window counts as
- *       one page); a = fdiv(p, Z); the output row = serial sum over tokens of fmul(a, v_e);
+ *       one page); a = fdiv(p, Z); the output row = serial fma chain over tokens, o = fma(a, v_e, o);
  *   Q33 a token's significance is the mean of the scores it received from later tokens; a decode
  *       step adds the score of query N-1 (max over the G heads) to every token p < N-1:
  *       sig' = fdiv(fadd(fmul(sig, c), a), c + 1), c = N-2-p scores so far; a new token starts at 0;
@@ -778,7 +779,7 @@ int32_t orc_attend(orc_pool* p, const uint16_t* q, float* out, float* probs) {
       for (int32_t i = 0; i < n; i++) {
         att_key(p, &tok[i], kx);
         float dot = 0.0f;
-        for (int32_t e = 0; e < d; e++) dot = dot + orc_f32_from_f16(qg[e]) * kx[e];   /* fadd(fmul) */
+        for (int32_t e = 0; e < d; e++) dot = fmaf(orc_f32_from_f16(qg[e]), kx[e], dot);   /* Q31 */
         float l = dot * scale;
         lg[(size_t)g * M + i] = l;
         if (l > m) m = l;
@@ -797,7 +798,7 @@ int32_t orc_attend(orc_pool* p, const uint16_t* q, float* out, float* probs) {
         if (ai > a[i]) a[i] = ai;                            /* GQA: max over the group */
         if (og) {
           att_val(p, &tok[i], vx);
-          for (int32_t e = 0; e < d; e++) og[e] = og[e] + ai * vx[e];
+          for (int32_t e = 0; e < d; e++) og[e] = fmaf(ai, vx[e], og[e]);              /* Q32 */
         }
       }
     }

@@ -936,8 +936,8 @@ cudaError_t launch_classify_prefill(const PoolDev& p, int n, const float* sig, i
 cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s,
                                  bool alloc = true, bool defer_recycle = false);
 cudaError_t launch_recycle(const PoolDev& p, const int32_t* req, int n, cudaStream_t s);
-cudaError_t launch_attend(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s);
-size_t attend_smem_bytes(const PoolDev& p);
+cudaError_t launch_attend(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s);
+size_t attend_smem_bytes(const PoolDev& p, int TS);
 cudaError_t launch_prefill_conservative(const PoolDev& p, cudaStream_t s);
 cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
                                 const float* sig, cudaStream_t s);

@@ -13,12 +13,13 @@
 //      (page score segment / window array, Q34); each section's (sig', position) minimum goes to the unit's
 //      secmin record, which lets the next dkv_classify(DECODE) pick its victim without a scan;
 //   4. output (optional): one thread per element e, serial over the tokens, all G heads at once.
-// Logits / probabilities live in shared memory (q_per_kv * max_seq_len floats).
+// Logits / probabilities live in shared memory: q_per_kv floats per token, sized by the longest ACTIVE request
+// (the host mirror knows every request's length; a unit holds at most that many tokens).
 #include "dkv_internal.cuh"
 
 namespace dkv {
 
-constexpr int kAttThreads = 256;
+constexpr int kAttThreads = 512;
 
 // Q32: exp for x <= 0 — 2^t, t = x*log2(e), n = rint(t), f = t - n, degree-6 Taylor polynomial of 2^f in
 // Horner form, times 2^n; 0 below t = -125.  Every step one IEEE binary32 operation (as the oracle's orc_exp).
@@ -37,8 +38,10 @@ __device__ __forceinline__ float dkv_exp(float x) {
   return __fmul_rn(r, __int_as_float(((int)n + 127) << 23));
 }
 
-__device__ __forceinline__ float dq(uint32_t code, float sf, float zf) {      // X^ = s*Q + z
-  return __fadd_rn(__fmul_rn(sf, __uint_as_float(0x4B000000u | code) - 8388608.0f), zf);
+// X^ = s*Q + z.  s is binary16 and Q < 2^8, so s*Q is exact in binary32 and fma(s, Q, z) rounds once,
+// exactly like the oracle's fadd(fmul(s, Q), z).
+__device__ __forceinline__ float dq(uint32_t code, float sf, float zf) {
+  return __fmaf_rn(sf, __uint_as_float(0x4B000000u | code) - 8388608.0f, zf);
 }
 
 struct AttShared {
@@ -46,29 +49,40 @@ struct AttShared {
   float* lg;        // [G][M]  logits -> exp -> probabilities
   float* part;      // [G][npage]
   int32_t* pid;     // [ph + pl] page IDs, section order
-  uint32_t* vmeta;  // [M] value metadata of stored tokens
+  float2* vsz;      // [M] value (s, z) of stored tokens as fp32
 };
 
-// Accumulate the G dot products of the query heads with one stored key of BITS-bit codes (serial over e).
+// Accumulate the G dot products of the query heads with one stored key of BITS-bit codes: the whole code
+// row is loaded first, then one fma chain per head over e = 0..d-1 (Q31).
 template <int D, int G, int BITS>
 __device__ __forceinline__ void dot_stored(const float* __restrict__ qf, const uint8_t* row, uint32_t kmeta,
                                            float (&acc)[G]) {
   const float sf = __half2float(__ushort_as_half((unsigned short)(kmeta & 0xFFFFu)));
   const float zf = __half2float(__ushort_as_half((unsigned short)(kmeta >> 16)));
   constexpr int PER = 32 / BITS;                                  // codes per 32-bit word
+  constexpr int NW = D / PER;                                     // words per row
   constexpr uint32_t Q = (1u << BITS) - 1u;
-#pragma unroll 1
-  for (int w = 0; w < D / PER; w += 4) {
-    const uint4 v = *reinterpret_cast<const uint4*>(row + 4 * w);
-    const uint32_t words[4] = {v.x, v.y, v.z, v.w};
+  uint32_t w[NW];
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
+  for (int k = 0; k < NW / 4; k++) {
+    const uint4 v = *reinterpret_cast<const uint4*>(row + 16 * k);
+    w[4 * k] = v.x; w[4 * k + 1] = v.y; w[4 * k + 2] = v.z; w[4 * k + 3] = v.w;
+  }
 #pragma unroll
-      for (int j = 0; j < PER; j++) {
-        const int e = (w + k) * PER + j;
-        const float x = dq((words[k] >> (j * BITS)) & Q, sf, zf);
+  for (int k = 0; k < NW; k++) {
 #pragma unroll
-        for (int g = 0; g < G; g++) acc[g] = __fadd_rn(acc[g], __fmul_rn(qf[g * D + e], x));
+    for (int j = 0; j < PER; j += 4) {
+      float x[4];
+#pragma unroll
+      for (int jj = 0; jj < 4; jj++) x[jj] = dq((w[k] >> ((j + jj) * BITS)) & Q, sf, zf);
+      const int e = k * PER + j;
+#pragma unroll
+      for (int g = 0; g < G; g++) {
+        const float4 qv = *reinterpret_cast<const float4*>(qf + g * D + e);
+        acc[g] = __fmaf_rn(qv.x, x[0], acc[g]);
+        acc[g] = __fmaf_rn(qv.y, x[1], acc[g]);
+        acc[g] = __fmaf_rn(qv.z, x[2], acc[g]);
+        acc[g] = __fmaf_rn(qv.w, x[3], acc[g]);
       }
     }
   }
@@ -76,7 +90,8 @@ __device__ __forceinline__ void dot_stored(const float* __restrict__ qf, const u
 
 template <int D, int G>
 __global__ void __launch_bounds__(kAttThreads)
-attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs) {
+attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs,
+              int TS) {                                          // TS: shared-memory token capacity (>= any T)
   extern __shared__ __align__(16) float att_smem[];
   __shared__ float s_red[kAttThreads / 32][G];
   __shared__ float s_m[G], s_Z[G];
@@ -87,7 +102,7 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
   if (ld_volatile(&p.ctrl->status) != 0) return;                  // sticky error: no-op
   const int r = fdiv(p.div_LyH, u);
   if (p.req_state[r] != DKV_REQ_ACTIVE) return;
-  const int M = p.M, L = p.L, W = p.W;
+  const int M = TS, L = p.L, W = p.W;                            // M: per-head logit stride in shared memory
   const int N = p.seq_len[r];                                     // includes the newest token
   const int nh = p.n_h[u], nl = p.n_l[u];
   const int nw = min(W, N);
@@ -100,7 +115,7 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
   S.lg = S.qf + G * D;
   S.part = S.lg + (size_t)G * M;
   S.pid = reinterpret_cast<int32_t*>(S.part + (size_t)G * (L + 1));
-  S.vmeta = reinterpret_cast<uint32_t*>(S.pid + L);
+  S.vsz = reinterpret_cast<float2*>(((uintptr_t)(S.pid + L) + 7) & ~(uintptr_t)7);
   const int32_t* row = p.table + (size_t)u * L;
   for (int k = tid; k < ph + pl; k += kAttThreads) S.pid[k] = k < ph ? row[k] : row[L - 1 - (k - ph)];
   for (int k = tid; k < G * D; k += kAttThreads)
@@ -126,7 +141,9 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
       const int idx = hi ? s - (pg * Ch) : s - (pg - ph) * Cl;
       const uint8_t* page = p.pages + (size_t)S.pid[pg] * (size_t)p.page_bytes;
       const uint32_t km = *reinterpret_cast<const uint32_t*>(page + gg.off_kmeta + 4 * idx);
-      S.vmeta[i] = *reinterpret_cast<const uint32_t*>(page + gg.off_vmeta + 4 * idx);
+      const uint32_t vm = *reinterpret_cast<const uint32_t*>(page + gg.off_vmeta + 4 * idx);
+      S.vsz[i] = make_float2(__half2float(__ushort_as_half((unsigned short)(vm & 0xFFFFu))),
+                             __half2float(__ushort_as_half((unsigned short)(vm >> 16))));
       const uint8_t* krow = page + gg.off_k + idx * gg.k_row;
       if (gg.kbits == 8) dot_stored<D, G, 8>(S.qf, krow, km, acc);
       else if (gg.kbits == 4) dot_stored<D, G, 4>(S.qf, krow, km, acc);
@@ -134,7 +151,7 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
     } else {
       const int pos = N - nw + (i - nh - nl);
       const uint16_t* wk = reinterpret_cast<const uint16_t*>(p.win_k) + ((size_t)u * W + fmod_(p.div_W, pos)) * D;
-#pragma unroll 1
+#pragma unroll 2
       for (int e0 = 0; e0 < D; e0 += 8) {
         const uint4 v = *reinterpret_cast<const uint4*>(wk + e0);
         const uint32_t hw[4] = {v.x, v.y, v.z, v.w};
@@ -142,7 +159,7 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
         for (int k = 0; k < 8; k++) {
           const float x = __half2float(__ushort_as_half((unsigned short)(hw[k >> 1] >> (16 * (k & 1)))));
 #pragma unroll
-          for (int g = 0; g < G; g++) acc[g] = __fadd_rn(acc[g], __fmul_rn(S.qf[g * D + e0 + k], x));
+          for (int g = 0; g < G; g++) acc[g] = __fmaf_rn(S.qf[g * D + e0 + k], x, acc[g]);
         }
       }
     }
@@ -198,7 +215,7 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
       S.lg[(size_t)g * M + i] = ag;
       a = fmaxf(a, ag);                                           // GQA: max over the group
     }
-    if (probs) probs[(size_t)u * M + i] = a;
+    if (probs) probs[(size_t)u * p.M + i] = a;
     float* sp;
     int pos, cls = 0, slot = 0;
     if (i < nh + nl) {
@@ -245,67 +262,121 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
     }
     m[6] = 1;
   }
-  // ---- 4. output (Q32): serial over tokens, one thread per element, all heads
-  if (out != nullptr && tid < D) {
-    const int e = tid;
-    float acc[G];
+  // ---- 4. output (Q32): thread (e, head subset), one fma chain over the tokens in order.  Tiles of kVT
+  // tokens' value rows are staged in shared memory by all threads with 16-B loads (double-buffered); within
+  // a tile the high / low / window tokens are walked in separate loops with the element's byte and shift
+  // hoisted, so a token costs one shared load + shift, one dequant and one fma per head.
+  if (out != nullptr) {
+    constexpr int HS = (G >= 2 && kAttThreads / D >= 2) ? 2 : 1;  // head subsets (threads per element)
+    constexpr int GPS = (G + HS - 1) / HS;                        // heads per thread
+    constexpr int RB = 2 * D;                                     // staged row bytes (an fp16 window row)
+    constexpr int CPR = RB / 16;                                  // 16-B chunks per row
+    constexpr int kVT = kAttThreads / CPR;                        // tokens per tile
+    uint8_t* tile = reinterpret_cast<uint8_t*>(((uintptr_t)(S.vsz + M) + 15) & ~(uintptr_t)15);   // [2][kVT][RB]
+    const bool worker = tid < HS * D;
+    const int e = tid % D, hs = tid / D;
+    float acc[GPS];
 #pragma unroll
-    for (int g = 0; g < G; g++) acc[g] = 0.0f;
-    for (int i = 0; i < T; i++) {
-      float x;
-      if (i < nh + nl) {
-        const bool hi = i < nh;
-        const ClassGeom& gg = hi ? gh : gl;
-        const int slot = hi ? i : i - nh;
-        const int pg = hi ? fdiv(p.div_Ch, slot) : ph + fdiv(p.div_Cl, slot);
-        const int idx = hi ? slot - pg * Ch : slot - (pg - ph) * Cl;
-        const uint8_t* vrow = p.pages + (size_t)S.pid[pg] * (size_t)p.page_bytes + gg.off_v + idx * gg.v_row;
-        const int bit = e * gg.vbits;
-        const uint32_t code = ((uint32_t)vrow[bit >> 3] >> (bit & 7)) & ((1u << gg.vbits) - 1u);
-        const uint32_t vm = S.vmeta[i];
-        x = dq(code, __half2float(__ushort_as_half((unsigned short)(vm & 0xFFFFu))),
-               __half2float(__ushort_as_half((unsigned short)(vm >> 16))));
-      } else {
-        const int pos = N - nw + (i - nh - nl);
-        x = __half2float(p.win_v[((size_t)u * W + fmod_(p.div_W, pos)) * D + e]);
+    for (int j = 0; j < GPS; j++) acc[j] = 0.0f;
+    const int bh = e * gh.vbits, bl = e * gl.vbits;
+    const int byh = bh >> 3, shh = bh & 7, byl = bl >> 3, shl = bl & 7;
+    const uint32_t mkh = (1u << gh.vbits) - 1u, mkl = (1u << gl.vbits) - 1u;
+    auto stage = [&](int t0, int buf) {                           // token rows [t0, t0 + kVT) -> tile[buf]
+      const int j = tid / CPR, c = tid % CPR;
+      const int i = t0 + j;
+      if (i < T) {
+        const uint8_t* src = nullptr;
+        int rb;
+        if (i < nh + nl) {
+          const bool hi = i < nh;
+          const ClassGeom& gg = hi ? gh : gl;
+          const int slot = hi ? i : i - nh;
+          const int pg = hi ? fdiv(p.div_Ch, slot) : ph + fdiv(p.div_Cl, slot);
+          const int idx = hi ? slot - pg * Ch : slot - (pg - ph) * Cl;
+          src = p.pages + (size_t)S.pid[pg] * (size_t)p.page_bytes + gg.off_v + idx * gg.v_row;
+          rb = gg.v_row;
+        } else {
+          const int pos = N - nw + (i - nh - nl);
+          src = reinterpret_cast<const uint8_t*>(p.win_v + ((size_t)u * W + fmod_(p.div_W, pos)) * D);
+          rb = RB;
+        }
+        if (16 * c < rb) cp_async16(tile + ((size_t)buf * kVT + j) * RB + 16 * c, src + 16 * c, true);
       }
+      cp_async_commit();
+    };
+    auto fma_heads = [&](int i, float x) {
 #pragma unroll
-      for (int g = 0; g < G; g++) acc[g] = __fadd_rn(acc[g], __fmul_rn(S.lg[(size_t)g * M + i], x));
+      for (int jj = 0; jj < GPS; jj++) {
+        const int g = hs + jj * HS;
+        if (g < G) acc[jj] = __fmaf_rn(S.lg[(size_t)g * M + i], x, acc[jj]);
+      }
+    };
+    const int ntiles = (T + kVT - 1) / kVT;
+    stage(0, 0);
+    for (int tt = 0; tt < ntiles; tt++) {
+      if (tt + 1 < ntiles) stage((tt + 1) * kVT, (tt + 1) & 1);
+      else cp_async_commit();
+      cp_async_wait<1>();
+      __syncthreads();
+      if (worker) {
+        const uint8_t* tb = tile + (size_t)(tt & 1) * kVT * RB;
+        const int t0 = tt * kVT, t1 = min(t0 + kVT, T);
+        int i = t0;
+        for (; i < min(t1, nh); i++) {                            // high section
+          const uint32_t code = ((uint32_t)tb[(size_t)(i - t0) * RB + byh] >> shh) & mkh;
+          const float2 sz = S.vsz[i];
+          fma_heads(i, dq(code, sz.x, sz.y));
+        }
+        for (; i < min(t1, nh + nl); i++) {                       // low section
+          const uint32_t code = ((uint32_t)tb[(size_t)(i - t0) * RB + byl] >> shl) & mkl;
+          const float2 sz = S.vsz[i];
+          fma_heads(i, dq(code, sz.x, sz.y));
+        }
+        for (; i < t1; i++)                                       // window, oldest first
+          fma_heads(i, __half2float(reinterpret_cast<const __half*>(tb + (size_t)(i - t0) * RB)[e]));
+      }
+      __syncthreads();                                            // this buffer is restaged two tiles on
     }
+    if (worker) {
 #pragma unroll
-    for (int g = 0; g < G; g++) out[((size_t)u * G + g) * D + e] = acc[g];
+      for (int jj = 0; jj < GPS; jj++) {
+        const int g = hs + jj * HS;
+        if (g < G) out[((size_t)u * G + g) * D + e] = acc[jj];
+      }
+    }
   }
 }
 
-size_t attend_smem_bytes(const PoolDev& p) {
+size_t attend_smem_bytes(const PoolDev& p, int TS) {
   const size_t G = p.G > 0 ? p.G : 1;
-  return 4 * (G * p.d + G * (size_t)p.M + G * (size_t)(p.L + 1) + (size_t)p.L + (size_t)p.M);
+  const size_t tile = 2 * (size_t)kAttThreads * 16 + 16;         // two staged value tiles (+ alignment)
+  return 4 * (G * p.d + G * (size_t)TS + G * (size_t)(p.L + 1) + (size_t)p.L) + 8 + 8 * (size_t)TS + tile;
 }
 
 template <int D, int G>
-static cudaError_t launch_att(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s) {
-  const size_t smem = attend_smem_bytes(p);
+static cudaError_t launch_att(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s) {
+  const size_t smem = attend_smem_bytes(p, TS);
   cudaError_t e = cudaFuncSetAttribute(attend_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  attend_kernel<D, G><<<p.U, kAttThreads, smem, s>>>(p, q, out, probs);
+  attend_kernel<D, G><<<p.U, kAttThreads, smem, s>>>(p, q, out, probs, TS);
   return cudaGetLastError();
 }
 
 template <int D>
-static cudaError_t launch_att_d(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s) {
+static cudaError_t launch_att_d(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s) {
   switch (p.G) {
-    case 1: return launch_att<D, 1>(p, q, out, probs, s);
-    case 2: return launch_att<D, 2>(p, q, out, probs, s);
-    case 4: return launch_att<D, 4>(p, q, out, probs, s);
-    case 5: return launch_att<D, 5>(p, q, out, probs, s);
-    case 7: return launch_att<D, 7>(p, q, out, probs, s);
-    case 8: return launch_att<D, 8>(p, q, out, probs, s);
+    case 1: return launch_att<D, 1>(p, q, out, probs, TS, s);
+    case 2: return launch_att<D, 2>(p, q, out, probs, TS, s);
+    case 4: return launch_att<D, 4>(p, q, out, probs, TS, s);
+    case 5: return launch_att<D, 5>(p, q, out, probs, TS, s);
+    case 7: return launch_att<D, 7>(p, q, out, probs, TS, s);
+    case 8: return launch_att<D, 8>(p, q, out, probs, TS, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_attend(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s) {
-  return p.d == 128 ? launch_att_d<128>(p, q, out, probs, s) : launch_att_d<64>(p, q, out, probs, s);
+cudaError_t launch_attend(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s) {
+  return p.d == 128 ? launch_att_d<128>(p, q, out, probs, TS, s) : launch_att_d<64>(p, q, out, probs, TS, s);
 }
 
 }  // namespace dkv

@@ -369,8 +369,12 @@ dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* 
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
     return DKV_ERR_CUDA;
-  if (attend_smem_bytes(p->dev) > (size_t)optin) return DKV_ERR_INVALID_ARG;
-  cudaError_t e = launch_attend(p->dev, d_q, d_out, d_probs, (cudaStream_t)s);
+  int TS = 1;                                                    // tokens a unit can hold: <= its length
+  for (int r = 0; r < p->cfg.max_requests; r++)
+    if (p->req_state[r] == DKV_REQ_ACTIVE && p->seq_len[r] > TS) TS = p->seq_len[r];
+  TS = (TS + 31) & ~31;
+  if (attend_smem_bytes(p->dev, TS) > (size_t)optin) return DKV_ERR_INVALID_ARG;
+  cudaError_t e = launch_attend(p->dev, d_q, d_out, d_probs, TS, (cudaStream_t)s);
   return e == cudaSuccess ? DKV_OK : DKV_ERR_CUDA;
 }
 
