@@ -1,7 +1,7 @@
 # B200 (sm_100a) build of the DiffKV memory-manager C-ABI library + the CPU oracle (test infrastructure).
 NVCC    ?= nvcc
 ARCH    := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $(EXTRA) \
            --expt-relaxed-constexpr -Iinclude -Xptxas -v
 PKG     := paper_2412_03131_b200
 SRCS    := $(wildcard $(PKG)/csrc/*.cu)

@@ -56,7 +56,13 @@ struct ListCtx {
   uint32_t* phase;           // PF == 2: parity bit per stage (warp-uniform)
 };
 
-constexpr int kBulkStages = 3;
+#ifndef DKV_BULK_STAGES
+#define DKV_BULK_STAGES 2
+#endif
+#ifndef DKV_BULK_MINB
+#define DKV_BULK_MINB 4
+#endif
+constexpr int kBulkStages = DKV_BULK_STAGES;               // staging depth (tuning: tools/sweep_bulk.sh)
 
 // Walk one class list.  KB/VB > 0: compile-time widths; KB == 0: runtime widths from g.
 // PF: 0 = rows loaded into registers right before use; 1 = register ping-pong; 2 = 1-D TMA
@@ -239,7 +245,7 @@ template <int D>
 constexpr size_t bulk_ring_bytes() { return (size_t)kBulkWarps * kBulkStages * kBulkTPS * 2 * D * 2; }
 
 template <int D, int PF>
-__global__ void __launch_bounds__(kBulkWarps * 32, PF == 1 ? 4 : (PF >= 2 ? 4 : 6))
+__global__ void __launch_bounds__(kBulkWarps * 32, PF == 1 ? 4 : (PF >= 2 ? DKV_BULK_MINB : 6))
 quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const uint16_t* __restrict__ vin,
                      int64_t kv_stride, const float* __restrict__ sig, int64_t sig_stride, int nseg_max) {
   __shared__ uint32_t s_ent[kBulkWarps][kSegTokens];   // (t - t0) | slot << 8; high from the front, low from the back
