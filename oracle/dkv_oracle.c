@@ -686,7 +686,8 @@ int32_t orc_free(orc_pool* p, const int32_t* req, int32_t n) {
  *       tokens in the order: high slots 0..n_h-1, low slots 0..n_l-1, window oldest -> newest;
  *   Q32 p = exp(logit - max) with orc_exp (round-to-nearest range reduction + degree-6 polynomial, fixed
  *       operation order); Z = sum over pages in that order of the serial in-page sums (the window counts as
- *       one page); a = fdiv(p, Z); the output row = serial fma chain over tokens, o = fma(a, v_e, o);
+ *       one page); a = fdiv(p, Z); the output row = the serial sum over pages (same order) of each page's
+ *       fma chain over its tokens, o_page = fma(a, v_e, o_page) from 0;
  *   Q33 a token's significance is the mean of the scores it received from later tokens; a decode
  *       step adds the score of query N-1 (max over the G heads) to every token p < N-1:
  *       sig' = fdiv(fadd(fmul(sig, c), a), c + 1), c = N-2-p scores so far; a new token starts at 0;
@@ -743,6 +744,7 @@ int32_t orc_attend(orc_pool* p, const uint16_t* q, float* out, float* probs) {
   float* a = (float*)malloc(4 * (size_t)M);
   float* kx = (float*)malloc(4 * (size_t)d);
   float* vx = (float*)malloc(4 * (size_t)d);
+  float* pv = (float*)malloc(4 * (size_t)d);                  /* the current page's partial output row */
   const float scale = 1.0f / sqrtf((float)d);
   for (int32_t u = 0; u < p->U; u++) {
     int32_t r = u / LyH;
@@ -792,13 +794,15 @@ int32_t orc_attend(orc_pool* p, const uint16_t* q, float* out, float* probs) {
         if (i == n - 1 || tpage[i + 1] != tpage[i]) { Z = Z + part; part = 0.0f; }
       }
       float* og = out ? out + ((size_t)u * G + g) * d : NULL;
-      if (og) for (int32_t e = 0; e < d; e++) og[e] = 0.0f;
+      if (og) for (int32_t e = 0; e < d; e++) { og[e] = 0.0f; pv[e] = 0.0f; }
       for (int32_t i = 0; i < n; i++) {
         float ai = lg[(size_t)g * M + i] / Z;                /* fdiv_rn */
         if (ai > a[i]) a[i] = ai;                            /* GQA: max over the group */
-        if (og) {
+        if (og) {                                            /* Q32: pages in order of in-page fma chains */
           att_val(p, &tok[i], vx);
-          for (int32_t e = 0; e < d; e++) og[e] = fmaf(ai, vx[e], og[e]);              /* Q32 */
+          for (int32_t e = 0; e < d; e++) pv[e] = fmaf(ai, vx[e], pv[e]);
+          if (i == n - 1 || tpage[i + 1] != tpage[i])
+            for (int32_t e = 0; e < d; e++) { og[e] = og[e] + pv[e]; pv[e] = 0.0f; }
         }
       }
     }
@@ -812,7 +816,7 @@ int32_t orc_attend(orc_pool* p, const uint16_t* q, float* out, float* probs) {
       memcpy(tok[i].sig, &sg, 4);
     }
   }
-  free(tok); free(tpage); free(lg); free(a); free(kx); free(vx);
+  free(tok); free(tpage); free(lg); free(a); free(kx); free(vx); free(pv);
   return ORC_OK;
 }
 

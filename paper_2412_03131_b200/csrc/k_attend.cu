@@ -12,9 +12,12 @@
 //   3. significance: sig' = (sig * c + score) / (c + 1), c = N - 2 - position (Q33), written in place
 //      (page score segment / window array, Q34); each section's (sig', position) minimum goes to the unit's
 //      secmin record, which lets the next dkv_classify(DECODE) pick its victim without a scan;
-//   4. output (optional): one thread per element e, serial over the tokens, all G heads at once.
+//   4. output (optional): pages in order of their in-page fma chains; a warp per page, a lane per element
+//      set with all G heads, partials added in page order by (head, element) threads.
 // Logits / probabilities live in shared memory: q_per_kv floats per token, sized by the longest ACTIVE request
 // (the host mirror knows every request's length; a unit holds at most that many tokens).
+#include <algorithm>
+
 #include "dkv_internal.cuh"
 
 namespace dkv {
@@ -44,9 +47,12 @@ __device__ __forceinline__ float dq(uint32_t code, float sf, float zf) {
   return __fmaf_rn(sf, __uint_as_float(0x4B000000u | code) - 8388608.0f, zf);
 }
 
+template <int G>
+constexpr int padded_heads() { return (G + 3) / 4 * 4; }          // lg row stride: 16-B aligned per token
+
 struct AttShared {
   float* qf;        // [G][D]
-  float* lg;        // [G][M]  logits -> exp -> probabilities
+  float* lg;        // [M][GP] logits -> exp -> probabilities, token-major (one 16-B load per 4 heads)
   float* part;      // [G][npage]
   int32_t* pid;     // [ph + pl] page IDs, section order
   float2* vsz;      // [M] value (s, z) of stored tokens as fp32
@@ -111,11 +117,17 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
   const int ph = ceil_div(nh, Ch), pl = ceil_div(nl, Cl);
   const int npage = ph + pl + (nw > 0 ? 1 : 0);
   AttShared S;
+  constexpr int GP = padded_heads<G>();
+  // every region is carved by float offsets from the shared base (keeps the compiler on shared-space loads)
+  const int off_lg = G * D;                                       // multiple of 4 floats
+  const int off_part = off_lg + GP * M;
+  const int off_pid = off_part + G * (L + 1);
+  const int off_vsz = (off_pid + L + 1) & ~1;                     // 8-B aligned
   S.qf = att_smem;
-  S.lg = S.qf + G * D;
-  S.part = S.lg + (size_t)G * M;
-  S.pid = reinterpret_cast<int32_t*>(S.part + (size_t)G * (L + 1));
-  S.vsz = reinterpret_cast<float2*>(((uintptr_t)(S.pid + L) + 7) & ~(uintptr_t)7);
+  S.lg = att_smem + off_lg;
+  S.part = att_smem + off_part;
+  S.pid = reinterpret_cast<int32_t*>(att_smem + off_pid);
+  S.vsz = reinterpret_cast<float2*>(att_smem + off_vsz);
   const int32_t* row = p.table + (size_t)u * L;
   for (int k = tid; k < ph + pl; k += kAttThreads) S.pid[k] = k < ph ? row[k] : row[L - 1 - (k - ph)];
   for (int k = tid; k < G * D; k += kAttThreads)
@@ -166,7 +178,7 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
 #pragma unroll
     for (int g = 0; g < G; g++) {
       const float l = __fmul_rn(acc[g], scale);
-      S.lg[(size_t)g * M + i] = l;
+      S.lg[(size_t)i * GP + g] = l;
       mx[g] = fmaxf(mx[g], l);
     }
   }
@@ -186,7 +198,7 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
   __syncthreads();
   for (int i = tid; i < T; i += kAttThreads)
 #pragma unroll
-    for (int g = 0; g < G; g++) S.lg[(size_t)g * M + i] = dkv_exp(__fsub_rn(S.lg[(size_t)g * M + i], s_m[g]));
+    for (int g = 0; g < G; g++) S.lg[(size_t)i * GP + g] = dkv_exp(__fsub_rn(S.lg[(size_t)i * GP + g], s_m[g]));
   __syncthreads();
   for (int it = tid; it < G * npage; it += kAttThreads) {          // serial in-page sums
     const int g = it / npage, k = it % npage;
@@ -195,7 +207,7 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
     else if (k < ph + pl) { t0 = nh + (k - ph) * Cl; t1 = min(t0 + Cl, nh + nl); }
     else { t0 = nh + nl; t1 = T; }
     float sum = 0.0f;
-    for (int i = t0; i < t1; i++) sum = __fadd_rn(sum, S.lg[(size_t)g * M + i]);
+    for (int i = t0; i < t1; i++) sum = __fadd_rn(sum, S.lg[(size_t)i * GP + g]);
     S.part[g * (L + 1) + k] = sum;
   }
   __syncthreads();
@@ -211,8 +223,8 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
     float a = 0.0f;
 #pragma unroll
     for (int g = 0; g < G; g++) {
-      const float ag = __fdiv_rn(S.lg[(size_t)g * M + i], s_Z[g]);
-      S.lg[(size_t)g * M + i] = ag;
+      const float ag = __fdiv_rn(S.lg[(size_t)i * GP + g], s_Z[g]);
+      S.lg[(size_t)i * GP + g] = ag;
       a = fmaxf(a, ag);                                           // GQA: max over the group
     }
     if (probs) probs[(size_t)u * p.M + i] = a;
@@ -262,95 +274,106 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
     }
     m[6] = 1;
   }
-  // ---- 4. output (Q32): thread (e, head subset), one fma chain over the tokens in order.  Tiles of kVT
-  // tokens' value rows are staged in shared memory by all threads with 16-B loads (double-buffered); within
-  // a tile the high / low / window tokens are walked in separate loops with the element's byte and shift
-  // hoisted, so a token costs one shared load + shift, one dequant and one fma per head.
+  // ---- 4. output (Q32): pages in order, each page's partial a fma chain over its tokens.  Rounds of PPR
+  // pages: warp w computes page (round * PPR + w) for every (element, head) — lane owns elements lane + 32k,
+  // all heads, so its 16-32 chains are independent — from the page's value segment staged in shared memory;
+  // then thread (head, element) adds the round's partials to its running sum in page order.
   if (out != nullptr) {
-    constexpr int HS = (G >= 2 && kAttThreads / D >= 2) ? 2 : 1;  // head subsets (threads per element)
-    constexpr int GPS = (G + HS - 1) / HS;                        // heads per thread
-    constexpr int RB = 2 * D;                                     // staged row bytes (an fp16 window row)
-    constexpr int CPR = RB / 16;                                  // 16-B chunks per row
-    constexpr int kVT = kAttThreads / CPR;                        // tokens per tile
-    uint8_t* tile = reinterpret_cast<uint8_t*>(((uintptr_t)(S.vsz + M) + 15) & ~(uintptr_t)15);   // [2][kVT][RB]
-    const bool worker = tid < HS * D;
-    const int e = tid % D, hs = tid / D;
-    float acc[GPS];
+    constexpr int PPR = G <= 4 ? 16 : 8;                          // pages per round
+    constexpr int EPL = D / 32;                                   // elements per lane
+    const int vseg = max(Ch * gh.v_row, Cl * gl.v_row);           // bytes of one page's value segment
+    const int off_part4 = ((off_vsz + 2 * M) + 3) & ~3;           // [PPR][G][D] page partials
+    float* part4 = att_smem + off_part4;
+    uint8_t* seg = reinterpret_cast<uint8_t*>(att_smem + off_part4 + PPR * G * D) + (size_t)warp * ((vseg + 15) & ~15);
+    float run[(G * D + kAttThreads - 1) / kAttThreads];
 #pragma unroll
-    for (int j = 0; j < GPS; j++) acc[j] = 0.0f;
-    const int bh = e * gh.vbits, bl = e * gl.vbits;
-    const int byh = bh >> 3, shh = bh & 7, byl = bl >> 3, shl = bl & 7;
-    const uint32_t mkh = (1u << gh.vbits) - 1u, mkl = (1u << gl.vbits) - 1u;
-    auto stage = [&](int t0, int buf) {                           // token rows [t0, t0 + kVT) -> tile[buf]
-      const int j = tid / CPR, c = tid % CPR;
-      const int i = t0 + j;
-      if (i < T) {
-        const uint8_t* src = nullptr;
-        int rb;
-        if (i < nh + nl) {
-          const bool hi = i < nh;
+    for (int j = 0; j < (G * D + kAttThreads - 1) / kAttThreads; j++) run[j] = 0.0f;
+    for (int r0 = 0; r0 < npage; r0 += PPR) {
+      const int k = r0 + warp;
+      if (warp < PPR && k < npage) {
+        float acc[EPL][G];
+#pragma unroll
+        for (int x = 0; x < EPL; x++)
+#pragma unroll
+          for (int g = 0; g < G; g++) acc[x][g] = 0.0f;
+        if (k < ph + pl) {                                        // a stored page
+          const bool hi = k < ph;
           const ClassGeom& gg = hi ? gh : gl;
-          const int slot = hi ? i : i - nh;
-          const int pg = hi ? fdiv(p.div_Ch, slot) : ph + fdiv(p.div_Cl, slot);
-          const int idx = hi ? slot - pg * Ch : slot - (pg - ph) * Cl;
-          src = p.pages + (size_t)S.pid[pg] * (size_t)p.page_bytes + gg.off_v + idx * gg.v_row;
-          rb = gg.v_row;
-        } else {
-          const int pos = N - nw + (i - nh - nl);
-          src = reinterpret_cast<const uint8_t*>(p.win_v + ((size_t)u * W + fmod_(p.div_W, pos)) * D);
-          rb = RB;
-        }
-        if (16 * c < rb) cp_async16(tile + ((size_t)buf * kVT + j) * RB + 16 * c, src + 16 * c, true);
-      }
-      cp_async_commit();
-    };
-    auto fma_heads = [&](int i, float x) {
+          const int t0 = hi ? k * Ch : nh + (k - ph) * Cl;
+          const int cnt = min(hi ? Ch : Cl, (hi ? nh : nh + nl) - t0);
+          const uint8_t* src = p.pages + (size_t)S.pid[k] * (size_t)p.page_bytes + gg.off_v;
+          const int nbytes = cnt * gg.v_row;
+          for (int o = 16 * lane; o < nbytes; o += 512)
+            *reinterpret_cast<uint4*>(seg + o) = *reinterpret_cast<const uint4*>(src + o);
+          __syncwarp();
+          const int vb = gg.vbits;
+          const uint32_t mk = (1u << vb) - 1u;
+          for (int j = 0; j < cnt; j++) {
+            const int i = t0 + j;
+            const float2 sz = S.vsz[i];
+            float av[G];
 #pragma unroll
-      for (int jj = 0; jj < GPS; jj++) {
-        const int g = hs + jj * HS;
-        if (g < G) acc[jj] = __fmaf_rn(S.lg[(size_t)g * M + i], x, acc[jj]);
+            for (int g4 = 0; g4 < GP; g4 += 4) {
+              const float4 a4 = *reinterpret_cast<const float4*>(S.lg + (size_t)i * GP + g4);
+              if (g4 < G) av[g4] = a4.x;
+              if (g4 + 1 < G) av[g4 + 1] = a4.y;
+              if (g4 + 2 < G) av[g4 + 2] = a4.z;
+              if (g4 + 3 < G) av[g4 + 3] = a4.w;
+            }
+            const uint8_t* rowp = seg + j * gg.v_row;
+#pragma unroll
+            for (int x = 0; x < EPL; x++) {
+              const int bit = (lane + 32 * x) * vb;
+              const float v = dq(((uint32_t)rowp[bit >> 3] >> (bit & 7)) & mk, sz.x, sz.y);
+#pragma unroll
+              for (int g = 0; g < G; g++) acc[x][g] = __fmaf_rn(av[g], v, acc[x][g]);
+            }
+          }
+          __syncwarp();                                           // seg is reused by this warp's next page
+        } else {                                                  // the window page, oldest first
+          for (int i = nh + nl; i < T; i++) {
+            const int pos = N - nw + (i - nh - nl);
+            const __half* vr = p.win_v + ((size_t)u * W + fmod_(p.div_W, pos)) * D;
+            float av[G];
+#pragma unroll
+            for (int g = 0; g < G; g++) av[g] = S.lg[(size_t)i * GP + g];
+#pragma unroll
+            for (int x = 0; x < EPL; x++) {
+              const float v = __half2float(vr[lane + 32 * x]);
+#pragma unroll
+              for (int g = 0; g < G; g++) acc[x][g] = __fmaf_rn(av[g], v, acc[x][g]);
+            }
+          }
+        }
+#pragma unroll
+        for (int x = 0; x < EPL; x++)
+#pragma unroll
+          for (int g = 0; g < G; g++) part4[(warp * G + g) * D + lane + 32 * x] = acc[x][g];
       }
-    };
-    const int ntiles = (T + kVT - 1) / kVT;
-    stage(0, 0);
-    for (int tt = 0; tt < ntiles; tt++) {
-      if (tt + 1 < ntiles) stage((tt + 1) * kVT, (tt + 1) & 1);
-      else cp_async_commit();
-      cp_async_wait<1>();
       __syncthreads();
-      if (worker) {
-        const uint8_t* tb = tile + (size_t)(tt & 1) * kVT * RB;
-        const int t0 = tt * kVT, t1 = min(t0 + kVT, T);
-        int i = t0;
-        for (; i < min(t1, nh); i++) {                            // high section
-          const uint32_t code = ((uint32_t)tb[(size_t)(i - t0) * RB + byh] >> shh) & mkh;
-          const float2 sz = S.vsz[i];
-          fma_heads(i, dq(code, sz.x, sz.y));
-        }
-        for (; i < min(t1, nh + nl); i++) {                       // low section
-          const uint32_t code = ((uint32_t)tb[(size_t)(i - t0) * RB + byl] >> shl) & mkl;
-          const float2 sz = S.vsz[i];
-          fma_heads(i, dq(code, sz.x, sz.y));
-        }
-        for (; i < t1; i++)                                       // window, oldest first
-          fma_heads(i, __half2float(reinterpret_cast<const __half*>(tb + (size_t)(i - t0) * RB)[e]));
-      }
-      __syncthreads();                                            // this buffer is restaged two tiles on
-    }
-    if (worker) {
 #pragma unroll
-      for (int jj = 0; jj < GPS; jj++) {
-        const int g = hs + jj * HS;
-        if (g < G) out[((size_t)u * G + g) * D + e] = acc[jj];
+      for (int j = 0; j < (G * D + kAttThreads - 1) / kAttThreads; j++) {
+        const int t = tid + j * kAttThreads;                      // (head, element) = (t / D, t % D)
+        if (t < G * D)
+          for (int w = 0; w < PPR && r0 + w < npage; w++) run[j] = __fadd_rn(run[j], part4[w * G * D + t]);
       }
+      __syncthreads();                                            // partials are rewritten next round
+    }
+#pragma unroll
+    for (int j = 0; j < (G * D + kAttThreads - 1) / kAttThreads; j++) {
+      const int t = tid + j * kAttThreads;
+      if (t < G * D) out[(size_t)u * G * D + t] = run[j];
     }
   }
 }
 
 size_t attend_smem_bytes(const PoolDev& p, int TS) {
-  const size_t G = p.G > 0 ? p.G : 1;
-  const size_t tile = 2 * (size_t)kAttThreads * 16 + 16;         // two staged value tiles (+ alignment)
-  return 4 * (G * p.d + G * (size_t)TS + G * (size_t)(p.L + 1) + (size_t)p.L) + 8 + 8 * (size_t)TS + tile;
+  const size_t G = p.G > 0 ? p.G : 1, GP = (G + 3) / 4 * 4, PPR = G <= 4 ? 16 : 8;
+  const size_t vseg = (size_t)std::max(p.g[1].C * p.g[1].v_row, p.g[2].C * p.g[2].v_row);
+  const size_t segs = (size_t)(kAttThreads / 32) * ((vseg + 15) & ~(size_t)15);   // per-warp value segments
+  // floats: q, logits, Z page partials, page IDs, (s, z) pairs, output page partials, + alignment slack
+  return 4 * (G * p.d + GP * (size_t)TS + G * (size_t)(p.L + 1) + (size_t)p.L + 2 + 2 * (size_t)TS + 4 +
+              PPR * G * (size_t)p.d) + segs;
 }
 
 template <int D, int G>
