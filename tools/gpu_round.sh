@@ -9,8 +9,9 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$TAG.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke_$TAG.log
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?"; tail -1 gpurun_out/bench_$TAG.json
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$TAG.json 2>&1; echo "ref rc=$?"; tail -1 gpurun_out/bench_ref_$TAG.json
-K='regex:quant_prefill|classify_decode|compact_alloc|quant_decode|classify_prefill|finish_prefill|set_requests|init_kernel|recycle_kernel'
+K='regex:quant_prefill|classify_decode|compact_alloc|quant_decode|classify_prefill|finish_prefill|set_requests|init_kernel|recycle_kernel|attend_kernel'
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/launches_bench_$TAG.log 2>&1; echo "ncu launches rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:quant_prefill -s 1 -c 1 -o gpurun_out/prof_bulk_$TAG python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/prof_bulk_$TAG.log 2>&1; echo "ncu bulk rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"classify_decode|compact_alloc|quant_decode" -s 12 -c 3 -o gpurun_out/prof_decode_$TAG python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/prof_decode_$TAG.log 2>&1; echo "ncu decode rc=$?"
 ls -la gpurun_out
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:attend_kernel -s 2 -c 1 -o gpurun_out/prof_attend_$TAG python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/prof_attend_$TAG.log 2>&1; echo "ncu attend rc=$?"
