@@ -56,7 +56,8 @@ def launches(tag, path):
             f.write(f"{i},{k},{us:.3f}\n")
     # decode-phase launches: the trailing run of decode kernels (after the last bulk/prefill launch)
     last_bulk = max((i for i, k, _ in order if "prefill" in k), default=-1)
-    dec = [(k, us) for i, k, us in order if i > last_bulk]
+    # the memory manager's decode step (NEXT-2's attention is model compute, reported on its own)
+    dec = [(k, us) for i, k, us in order if i > last_bulk and "attend" not in k]
     dper = {}
     for k, us in dec:
         dper.setdefault(k, []).append(us)
