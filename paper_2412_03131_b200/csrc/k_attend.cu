@@ -275,9 +275,10 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
     m[6] = 1;
   }
   // ---- 4. output (Q32): pages in order, each page's partial a fma chain over its tokens.  Rounds of PPR
-  // pages: warp w computes page (round * PPR + w) for every (element, head) — lane owns elements lane + 32k,
-  // all heads, so its 16-32 chains are independent — from the page's value segment staged in shared memory;
-  // then thread (head, element) adds the round's partials to its running sum in page order.
+  // pages: warp w computes page (round * PPR + w) for every (element, head) — lane owns EPL elements and all
+  // heads, so its 16-32 chains are independent — from the page's value segment staged in shared memory;
+  // then thread (head, element) adds the round's partials to its running sum in page order.  A lane owns
+  // EPL consecutive elements, so one aligned 32-bit shared load yields all of its codes of a token.
   if (out != nullptr) {
     constexpr int PPR = G <= 4 ? 16 : 8;                          // pages per round
     constexpr int EPL = D / 32;                                   // elements per lane
@@ -320,11 +321,13 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
               if (g4 + 2 < G) av[g4 + 2] = a4.z;
               if (g4 + 3 < G) av[g4 + 3] = a4.w;
             }
+            // this lane's EPL consecutive elements: EPL * vb bits (4..32, a divisor of 32) in one aligned word
             const uint8_t* rowp = seg + j * gg.v_row;
+            const int bit0 = lane * EPL * vb;
+            const uint32_t word = *reinterpret_cast<const uint32_t*>(rowp + ((bit0 >> 5) << 2)) >> (bit0 & 31);
 #pragma unroll
             for (int x = 0; x < EPL; x++) {
-              const int bit = (lane + 32 * x) * vb;
-              const float v = dq(((uint32_t)rowp[bit >> 3] >> (bit & 7)) & mk, sz.x, sz.y);
+              const float v = dq((word >> (x * vb)) & mk, sz.x, sz.y);
 #pragma unroll
               for (int g = 0; g < G; g++) acc[x][g] = __fmaf_rn(av[g], v, acc[x][g]);
             }
@@ -339,7 +342,7 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
             for (int g = 0; g < G; g++) av[g] = S.lg[(size_t)i * GP + g];
 #pragma unroll
             for (int x = 0; x < EPL; x++) {
-              const float v = __half2float(vr[lane + 32 * x]);
+              const float v = __half2float(vr[EPL * lane + x]);
 #pragma unroll
               for (int g = 0; g < G; g++) acc[x][g] = __fmaf_rn(av[g], v, acc[x][g]);
             }
@@ -348,7 +351,7 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
 #pragma unroll
         for (int x = 0; x < EPL; x++)
 #pragma unroll
-          for (int g = 0; g < G; g++) part4[(warp * G + g) * D + lane + 32 * x] = acc[x][g];
+          for (int g = 0; g < G; g++) part4[(warp * G + g) * D + EPL * lane + x] = acc[x][g];
       }
       __syncthreads();
 #pragma unroll
