@@ -127,6 +127,7 @@ typedef struct {
   int64_t off_win_sig;         /* fp32[units][window]: significance of the window tokens (NEXT-2) */
   int64_t off_secmin;          /* int32[units][8]: per-section (significance, position, slot) minima written by
                                   dkv_attend, consumed by the next dkv_classify(DECODE) (NEXT-2) */
+  int64_t off_head_alpha;      /* fp32[layers * kv_heads][2]: per-head (alpha_h, alpha_l) (NEXT-4) */
 } dkv_layout_t;
 
 /* Arena size for `cfg`, or 0 if the configuration is invalid. */
@@ -194,6 +195,14 @@ dkv_status_t dkv_quant_write(dkv_pool_t p, int32_t phase, const dkv_decision_t* 
  * With NEXT-2 the decode step passes d_sig = NULL to dkv_classify / dkv_quant_write: t_c's significance is
  * then read from the window. */
 dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* d_probs, dkv_stream_t s);
+
+/* NEXT-4 — per-head thresholds ("a shared set of thresholds for all attention heads" is the
+ * paper's choice; per-head thresholds its stated extension; reading Q35).  h_alpha_h / h_alpha_l: host
+ * arrays of num_layers * num_kv_heads finite values >= 0 in (layer, this pool's head) order; unit u uses
+ * entry u mod (num_layers * num_kv_heads) in every classification (prompt thresholds alpha / i, Algorithm 1
+ * thresholds alpha / N).  NULL restores the pool-wide alpha_h / alpha_l.  Between sequences only; the
+ * values are copied on `s` (the host arrays may be reused once the call returns). */
+dkv_status_t dkv_set_head_thresholds(dkv_pool_t p, const float* h_alpha_h, const float* h_alpha_l, dkv_stream_t s);
 
 /* Release: host array h_req[0..n) of ACTIVE requests -> PENDING_FREE (double free / not active ->
  * DKV_ERR_STATE).  Allowed between sequences only (after dkv_quant_write, before dkv_classify).  Pages are

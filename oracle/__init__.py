@@ -82,7 +82,8 @@ class _Pool(C.Structure):
                 ("admit_list", C.POINTER(C.c_int32)), ("n_admit", C.c_int32),
                 ("status", C.c_int32), ("last_phase", C.c_int32),
                 ("last_demand", C.c_int64), ("last_freed", C.c_int64), ("oom_count", C.c_int32),
-                ("last_reclaimed", C.c_int64), ("win_sig", C.POINTER(C.c_float))]
+                ("last_reclaimed", C.c_int64), ("win_sig", C.POINTER(C.c_float)),
+                ("head_ah", C.POINTER(C.c_float)), ("head_al", C.POINTER(C.c_float)), ("use_head", C.c_int32)]
 
 
 _lib = None
@@ -117,6 +118,8 @@ def lib():
                                                C.c_void_p, P(C.c_int64)]
         L.orc_attend.argtypes = [P(_Pool), C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_exp.argtypes = [C.c_float]; L.orc_exp.restype = C.c_float
+        L.orc_set_head_thresholds.argtypes = [P(_Pool), C.c_void_p, C.c_void_p]
+        L.orc_set_head_thresholds.restype = C.c_int32
         for f in ("orc_classify_decode", "orc_classify_prefill", "orc_compact_alloc", "orc_quant_write_decode",
                   "orc_quant_write_prefill", "orc_free", "orc_take_status", "orc_prefill_conservative", "orc_attend"):
             getattr(L, f).restype = C.c_int32
@@ -298,6 +301,15 @@ class OraclePool:
             cand_sig = np.ascontiguousarray(cand_sig, dtype=np.float32)
         assert k_new.shape == (self.U, self.cfg.d)
         return lib().orc_quant_write_decode(self._p, _ptr(dec), _ptr(k_new), _ptr(v_new), _ptr(cand_sig))
+
+    def set_head_thresholds(self, alpha_h, alpha_l):
+        """NEXT-4: per-(layer, head) thresholds [Ly*H] each, or None to restore the pool-wide pair"""
+        if alpha_h is None:
+            return lib().orc_set_head_thresholds(self._p, None, None)
+        ah = np.ascontiguousarray(alpha_h, dtype=np.float32)
+        al = np.ascontiguousarray(alpha_l, dtype=np.float32)
+        assert ah.shape == (self.LyH,) and al.shape == (self.LyH,)
+        return lib().orc_set_head_thresholds(self._p, _ptr(ah), _ptr(al))
 
     def attend(self, q, want_out=True, want_probs=False):
         """NEXT-2: q = fp16 [U][G][d]; returns (status, out fp32 [U][G][d] or None, probs [U][M] or None)"""

@@ -226,7 +226,7 @@ void orc_pool_delete(orc_pool* p) {
   if (!p) return;
   free(p->ring); free(p->table); free(p->n_h); free(p->n_l); free(p->req_state); free(p->seq_len);
   free(p->prompt_len); free(p->pages); free(p->win_k); free(p->win_v); free(p->pf_nh); free(p->pf_nl);
-  free(p->admit_list); free(p->win_sig);
+  free(p->admit_list); free(p->win_sig); free(p->head_ah); free(p->head_al);
   free(p);
 }
 
@@ -300,6 +300,14 @@ static int32_t ceil_div(int32_t a, int32_t b) { return (a + b - 1) / b; }
  *   victim = lexicographic argmin of (score, position) over the section t_c joins, t_c included (Q6, Q7)
  *   t_c takes the victim's slot when the victim leaves; a downgraded victim goes to the KV_l tail (Q8)
  * ----------------------------------------------------------------------------------------------*/
+/* Q35 (NEXT-4): the thresholds of unit u's (layer, head) — per head when set, else the pool-wide pair */
+static float unit_ah(const orc_pool* p, int32_t u) {
+  return p->use_head ? p->head_ah[u % (p->c.Ly * p->c.H)] : p->c.alpha_h;
+}
+static float unit_al(const orc_pool* p, int32_t u) {
+  return p->use_head ? p->head_al[u % (p->c.Ly * p->c.H)] : p->c.alpha_l;
+}
+
 static void empty_decision(orc_decision* d) {
   memset(d, 0, sizeof(*d));
   d->v_slot = d->tc_slot = d->v_dst_slot = -1;
@@ -324,8 +332,8 @@ int32_t orc_classify_decode(orc_pool* p, const float* cand_sig, orc_decision* de
     float sc = cand_sig ? cand_sig[u] : (c->W ? p->win_sig[(size_t)u * c->W + (size_t)(pc % c->W)] : 0.0f);
     if (!isfinite(sc) || sc < 0.0f) { set_status(p, ORC_ERR_NONFINITE); continue; }
     if (sc == 0.0f) sc = 0.0f;                                /* canonicalise -0 -> +0 (Q6) */
-    float th = c->alpha_h / (float)N;                         /* alpha_h / N */
-    float tl = c->alpha_l / (float)N;                         /* alpha_l / N */
+    float th = unit_ah(p, u) / (float)N;                      /* alpha_h / N */
+    float tl = unit_al(p, u) / (float)N;                      /* alpha_l / N */
     int cls;
     if (sc >= th) cls = ORC_CLS_HIGH;                         /* line q_high */
     else if (sc >= tl) cls = ORC_CLS_LOW;                     /* line q_low  */
@@ -386,9 +394,23 @@ static int32_t admit(orc_pool* p, const int32_t* req, const int32_t* len, int32_
   return ORC_OK;
 }
 
-static int prompt_class(const orc_config* c, float s, int32_t t, int32_t n) {
+int32_t orc_set_head_thresholds(orc_pool* p, const float* alpha_h, const float* alpha_l) {
+  int32_t LyH = p->c.Ly * p->c.H;
+  if (!alpha_h || !alpha_l) { p->use_head = 0; return ORC_OK; }
+  for (int32_t i = 0; i < LyH; i++)
+    if (!isfinite(alpha_h[i]) || !isfinite(alpha_l[i]) || alpha_h[i] < 0 || alpha_l[i] < 0) return ORC_ERR_INVALID;
+  if (!p->head_ah) { p->head_ah = (float*)malloc(4 * (size_t)LyH); p->head_al = (float*)malloc(4 * (size_t)LyH); }
+  if (!p->head_ah || !p->head_al) return ORC_ERR_INVALID;
+  memcpy(p->head_ah, alpha_h, 4 * (size_t)LyH);
+  memcpy(p->head_al, alpha_l, 4 * (size_t)LyH);
+  p->use_head = 1;
+  return ORC_OK;
+}
+
+static int prompt_class(const orc_pool* p, int32_t u, float s, int32_t t, int32_t n) {
+  const orc_config* c = &p->c;
   float den = (c->prompt_denominator == 0) ? (float)(t + 1) : (float)n;
-  float th = c->alpha_h / den, tl = c->alpha_l / den;
+  float th = unit_ah(p, u) / den, tl = unit_al(p, u) / den;
   if (s >= th) return ORC_CLS_HIGH;
   if (s >= tl) return ORC_CLS_LOW;
   return ORC_CLS_PRUNED;
@@ -414,7 +436,7 @@ int32_t orc_classify_prefill(orc_pool* p, const int32_t* req, const int32_t* len
         if (t < T - c->W && p->status == ORC_OK) {
           float s = row[t];
           if (!isfinite(s) || s < 0.0f) { set_status(p, ORC_ERR_NONFINITE); s = 0.0f; }
-          cls = prompt_class(c, s, t, T);
+          cls = prompt_class(p, u, s, t, T);
           if (cls == ORC_CLS_HIGH) nh++;
           if (cls == ORC_CLS_LOW) nl++;
         }
@@ -640,7 +662,7 @@ int32_t orc_quant_write_prefill(orc_pool* p, const uint16_t* k, const uint16_t* 
         if (t < T - W) {
           float s = sig[((int64_t)i * LyH + j) * sig_stride + t];
           if (s == 0.0f) s = 0.0f;
-          int cls = prompt_class(c, s, t, T);
+          int cls = prompt_class(p, u, s, t, T);
           if (cls == ORC_CLS_PRUNED) continue;
           for (int32_t e = 0; e < d; e++) { kx[e] = orc_f32_from_f16(kr[e]); vx[e] = orc_f32_from_f16(vr[e]); }
           int32_t slot = (cls == ORC_CLS_HIGH) ? h++ : l++;

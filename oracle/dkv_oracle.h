@@ -72,6 +72,8 @@ typedef struct orc_pool {
   int64_t last_demand, last_freed; int32_t oom_count;
   int64_t last_reclaimed;                   /* prefill_workflow 1: middle pages reclaimed by the last call */
   float   *win_sig;                         /* [U][W] significance of the window tokens (running averages) */
+  float   *head_ah, *head_al;               /* NEXT-4: [Ly*H] per-(layer, head) thresholds (Q35) */
+  int32_t use_head;                         /* 1: the per-head thresholds replace alpha_h / alpha_l */
 } orc_pool;
 
 /* --- scalar primitives (exported for the pins) --- */
@@ -106,6 +108,9 @@ int32_t   orc_take_status(orc_pool* p);     /* returns and clears the sticky sta
    attention (max over the G heads) in token order (high slots, low slots, window oldest first). */
 int32_t   orc_attend(orc_pool* p, const uint16_t* q, float* out, float* probs);
 float     orc_exp(float x);                 /* the normative exp of Q32 (x <= 0) */
+/* NEXT-4: per-(layer, KV head) thresholds, arrays of Ly*H finite values >= 0 in (l, h) order;
+   NULL restores the pool-wide alpha_h / alpha_l.  Allowed between sequences. */
+int32_t   orc_set_head_thresholds(orc_pool* p, const float* alpha_h, const float* alpha_l);
 
 /* NEXT-1 (Fig. 5): admit + plan + compact with prefill_workflow = 1 for this call (the
    pool's own setting is restored); reclaimed_out receives the reclaimed page IDs in ring order. */

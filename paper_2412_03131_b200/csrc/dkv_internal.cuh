@@ -95,6 +95,8 @@ struct PoolDev {
   float* win_sig;       // [U][W] significance of the window tokens (NEXT-2)
   int32_t* secmin;      // [U][8] {sig_h, pos_h, slot_h, sig_l, pos_l, slot_l, valid, 0} from dkv_attend
   int32_t G;            // q_per_kv
+  float* head_alpha;    // [LyH][2] per-head (alpha_h, alpha_l) (NEXT-4)
+  int32_t use_head_alpha;   // 1: head_alpha replaces alpha_h / alpha_l
   int32_t prefill_wf;   // dkv_config_t.prefill_workflow
 };
 
@@ -884,6 +886,14 @@ __device__ __forceinline__ uint8_t* slot_page(const PoolDev& p, int cls, int u, 
 }
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Q35 (NEXT-4): the thresholds of unit u's (layer, head)
+__device__ __forceinline__ float unit_alpha_h(const PoolDev& p, int u) {
+  return p.use_head_alpha ? p.head_alpha[2 * fmod_(p.div_LyH, u)] : p.alpha_h;
+}
+__device__ __forceinline__ float unit_alpha_l(const PoolDev& p, int u) {
+  return p.use_head_alpha ? p.head_alpha[2 * fmod_(p.div_LyH, u) + 1] : p.alpha_l;
+}
 
 // ---- per-CTA copy of the per-request arrays.  Every unit of a request reads the same state / length
 // word, so thousands of warps loading them (or the control block) directly all queue on the same few L2

@@ -21,9 +21,9 @@ constexpr int kBulkWarps = 4;
 constexpr int kBulkG = 4;                                // lanes per token
 constexpr int kBulkTPS = 32 / kBulkG;                    // tokens per warp step
 
-__device__ __forceinline__ int prompt_class_q(const PoolDev& p, float s, int t, int T) {
-  const float den = (p.prompt_den == 0) ? (float)(t + 1) : (float)T;
-  const float th = __fdiv_rn(p.alpha_h, den), tl = __fdiv_rn(p.alpha_l, den);
+__device__ __forceinline__ int prompt_class_q(float ah, float al, int prompt_den, float s, int t, int T) {
+  const float den = (prompt_den == 0) ? (float)(t + 1) : (float)T;
+  const float th = __fdiv_rn(ah, den), tl = __fdiv_rn(al, den);
   return s >= th ? DKV_CLS_HIGH : (s >= tl ? DKV_CLS_LOW : DKV_CLS_PRUNED);
 }
 
@@ -270,6 +270,7 @@ quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const u
   const int i = (int)(wi / p.LyH), j = (int)(wi % p.LyH);
   const int r = p.admit[i];
   const int u = r * p.LyH + j;
+  const float ah = unit_alpha_h(p, u), al = unit_alpha_l(p, u);  // Q35
   const int T = p.prompt_len[r];
   const int t0 = seg * kSegTokens;
   if (t0 >= T) return;
@@ -291,7 +292,7 @@ quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const u
     float s = 0.0f;
     if (t < ke) {
       s = canon_zero(__ldcs(srow + t));
-      cl = prompt_class_q(p, s, t, T);
+      cl = prompt_class_q(ah, al, p.prompt_den, s, t, T);
     }
     const unsigned hm = __ballot_sync(kFull, cl == DKV_CLS_HIGH);
     const unsigned lm = __ballot_sync(kFull, cl == DKV_CLS_LOW);

@@ -55,8 +55,8 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
         if (lane == 0) set_status(p.ctrl, DKV_ERR_NONFINITE);
       } else {
         sc = canon_zero(s_in);
-        th = __fdiv_rn(p.alpha_h, (float)N);                     // alpha_h / N
-        tl = __fdiv_rn(p.alpha_l, (float)N);                     // alpha_l / N
+        th = __fdiv_rn(unit_alpha_h(p, u), (float)N);            // alpha_h / N (per head: Q35)
+        tl = __fdiv_rn(unit_alpha_l(p, u), (float)N);            // alpha_l / N
         cls = sc >= th ? DKV_CLS_HIGH : (sc >= tl ? DKV_CLS_LOW : DKV_CLS_PRUNED);
         tc_class = (uint8_t)cls;
         if (cls != DKV_CLS_PRUNED) {

@@ -8,9 +8,9 @@ namespace dkv {
 // ------------------------------------------------------------------------------------------- prefill
 constexpr int kPrefillWarps = 4;
 
-__device__ __forceinline__ int prompt_class(const PoolDev& p, float s, int t, int T) {
-  const float den = (p.prompt_den == 0) ? (float)(t + 1) : (float)T;
-  const float th = __fdiv_rn(p.alpha_h, den), tl = __fdiv_rn(p.alpha_l, den);
+__device__ __forceinline__ int prompt_class(float ah, float al, int prompt_den, float s, int t, int T) {
+  const float den = (prompt_den == 0) ? (float)(t + 1) : (float)T;
+  const float th = __fdiv_rn(ah, den), tl = __fdiv_rn(al, den);
   return s >= th ? DKV_CLS_HIGH : (s >= tl ? DKV_CLS_LOW : DKV_CLS_PRUNED);
 }
 
@@ -25,6 +25,7 @@ classify_prefill_kernel(PoolDev p, int n, const float* __restrict__ sig, int64_t
   const int i = w / p.LyH, j = w % p.LyH;
   const int r = p.admit[i];
   const int u = r * p.LyH + j;
+  const float ah = unit_alpha_h(p, u), al = unit_alpha_l(p, u);  // Q35
   const int T = p.prompt_len[r];
   const int kept = max(T - p.W, 0);
   const float* row = sig + (int64_t)w * sig_stride;
@@ -65,7 +66,7 @@ classify_prefill_kernel(PoolDev p, int n, const float* __restrict__ sig, int64_t
         if (t < kept) {
           float s = sv[k][e];
           if (!finite_f(s) || s < 0.0f) { bad = true; s = 0.0f; }
-          c = prompt_class(p, canon_zero(s), t, T);
+          c = prompt_class(ah, al, p.prompt_den, canon_zero(s), t, T);
         }
         ch += c == DKV_CLS_HIGH;
         cl += c == DKV_CLS_LOW;

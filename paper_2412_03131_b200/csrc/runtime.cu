@@ -82,6 +82,7 @@ bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
   Lo.off_rec = take(12 * (int64_t)G.U);
   Lo.off_win_sig = take(4 * (int64_t)G.U * c->window);
   Lo.off_secmin = take(32 * (int64_t)G.U);
+  Lo.off_head_alpha = take(8 * (int64_t)c->num_layers * c->num_kv_heads);
   Lo.off_ring = take(4 * P);
   Lo.off_table = take(4 * U * G.L);
   Lo.off_n_h = take(4 * U);
@@ -223,6 +224,8 @@ dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_
   d.rec = (int32_t*)(b + Lo.off_rec);
   d.win_sig = (float*)(b + Lo.off_win_sig);
   d.secmin = (int32_t*)(b + Lo.off_secmin);
+  d.head_alpha = (float*)(b + Lo.off_head_alpha);
+  d.use_head_alpha = 0;
   d.G = cfg->q_per_kv;
   d.prefill_wf = cfg->prefill_workflow;
   d.ring = (int32_t*)(b + Lo.off_ring);
@@ -376,6 +379,29 @@ dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* 
   if (attend_smem_bytes(p->dev, TS) > (size_t)optin) return DKV_ERR_INVALID_ARG;
   cudaError_t e = launch_attend(p->dev, d_q, d_out, d_probs, TS, (cudaStream_t)s);
   return e == cudaSuccess ? DKV_OK : DKV_ERR_CUDA;
+}
+
+dkv_status_t dkv_set_head_thresholds(dkv_pool_t p, const float* h_alpha_h, const float* h_alpha_l, dkv_stream_t s) {
+  if (!p) return DKV_ERR_INVALID_ARG;
+  if (p->seq != SEQ_IDLE) return DKV_ERR_STATE;
+  if (!h_alpha_h || !h_alpha_l) {
+    p->dev.use_head_alpha = 0;
+    return DKV_OK;
+  }
+  const int LyH = p->dev.LyH;
+  std::vector<float> v(2 * (size_t)LyH);
+  for (int i = 0; i < LyH; i++) {
+    const float a = h_alpha_h[i], b = h_alpha_l[i];
+    if (!(a >= 0.0f && a <= 3.0e38f) || !(b >= 0.0f && b <= 3.0e38f)) return DKV_ERR_INVALID_ARG;
+    v[2 * i] = a;
+    v[2 * i + 1] = b;
+  }
+  // pageable source: cudaMemcpyAsync stages it before returning, so the host arrays may be reused
+  cudaError_t e = cudaMemcpyAsync(p->dev.head_alpha, v.data(), 8 * (size_t)LyH, cudaMemcpyHostToDevice,
+                                  (cudaStream_t)s);
+  if (e != cudaSuccess) return DKV_ERR_CUDA;
+  p->dev.use_head_alpha = 1;
+  return DKV_OK;
 }
 
 dkv_status_t dkv_free(dkv_pool_t p, const int32_t* h_req, int32_t n, dkv_stream_t s) {

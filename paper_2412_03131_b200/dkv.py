@@ -26,7 +26,7 @@ DKV_REQ_IDLE, DKV_REQ_ADMITTING, DKV_REQ_ACTIVE, DKV_REQ_PENDING_FREE = 0, 1, 2,
 
 EXPORTED = ("dkv_arena_bytes", "dkv_pool_layout", "dkv_pool_init", "dkv_pool_destroy", "dkv_classify",
             "dkv_compact_alloc", "dkv_quant_write", "dkv_free", "dkv_pool_query", "dkv_pool_stats_device_ptr",
-            "dkv_status_string", "dkv_attend")
+            "dkv_status_string", "dkv_attend", "dkv_set_head_thresholds")
 
 
 class DkvError(RuntimeError):
@@ -62,7 +62,8 @@ class dkv_layout_t(C.Structure):
         "units", "table_len", "page_bytes", "num_tiles", "tile_units", "seg_tokens", "num_segs")] + \
         [(n, C.c_int32 * 3) for n in ("C", "k_row", "v_row", "off_k", "off_kmeta", "off_v", "off_vmeta",
                                        "off_score", "off_pos")] + [("off_tile_sums", C.c_int64), ("off_rec", C.c_int64),
-                                                                  ("off_win_sig", C.c_int64), ("off_secmin", C.c_int64)]
+                                                                  ("off_win_sig", C.c_int64), ("off_secmin", C.c_int64),
+                                                                  ("off_head_alpha", C.c_int64)]
 
 
 assert C.sizeof(dkv_decision_t) == 16
@@ -86,13 +87,14 @@ _lib.dkv_compact_alloc.argtypes = [_vp, _vp, _vp]
 _lib.dkv_quant_write.argtypes = [_vp, C.c_int32, _vp, _vp, _vp, C.c_int64, _vp, C.c_int64, _vp]
 _lib.dkv_free.argtypes = [_vp, _vp, C.c_int32, _vp]
 _lib.dkv_attend.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_lib.dkv_set_head_thresholds.argtypes = [_vp, _vp, _vp, _vp]
 _lib.dkv_pool_query.argtypes = [_vp, _P(dkv_stats_t), _vp]
 _lib.dkv_pool_stats_device_ptr.argtypes = [_vp]
 _lib.dkv_pool_stats_device_ptr.restype = _vp
 _lib.dkv_status_string.argtypes = [C.c_int32]
 _lib.dkv_status_string.restype = C.c_char_p
 for _f in ("dkv_pool_layout", "dkv_pool_init", "dkv_pool_destroy", "dkv_classify", "dkv_compact_alloc",
-           "dkv_quant_write", "dkv_free", "dkv_pool_query", "dkv_attend"):
+           "dkv_quant_write", "dkv_free", "dkv_pool_query", "dkv_attend", "dkv_set_head_thresholds"):
     getattr(_lib, _f).restype = C.c_int32
 
 
@@ -181,6 +183,15 @@ def dkv_quant_write(pool, phase, d_dec, d_k, d_v, kv_stride, d_sig, sig_stride, 
 
 def dkv_attend(pool, d_q, d_out, d_probs, stream=None) -> int:
     return _check("dkv_attend", _lib.dkv_attend(pool, _dev(d_q), _dev(d_out), _dev(d_probs), _stream(stream)))
+
+
+def dkv_set_head_thresholds(pool, alpha_h, alpha_l, stream=None) -> int:
+    if alpha_h is None:
+        return _check("dkv_set_head_thresholds", _lib.dkv_set_head_thresholds(pool, None, None, _stream(stream)))
+    ah = np.ascontiguousarray(np.asarray(alpha_h, dtype=np.float32))
+    al = np.ascontiguousarray(np.asarray(alpha_l, dtype=np.float32))
+    return _check("dkv_set_head_thresholds", _lib.dkv_set_head_thresholds(
+        pool, ah.ctypes.data_as(_vp), al.ctypes.data_as(_vp), _stream(stream)))
 
 
 def dkv_free(pool, h_req, n, stream=None) -> int:

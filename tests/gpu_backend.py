@@ -48,6 +48,10 @@ class GpuBackend:
         self.pool.quant_write_decode(dec, k, v, None if cand is None else self._cuda(cand))
         return 0
 
+    def set_head_thresholds(self, ah, al):
+        self.pool.set_head_thresholds(ah, al)
+        return 0
+
     def attend(self, q, want_out=True, want_probs=False):
         G, d, M = self.scn.q_per_kv, self.scn.d, self.scn.M
         qd = self._cuda(np.ascontiguousarray(q).view(np.int16))

@@ -132,6 +132,9 @@ class OracleBackend:
     def attend(self, q, want_out=True, want_probs=False):
         return self.pool.attend(q, want_out=want_out, want_probs=want_probs)
 
+    def set_head_thresholds(self, ah, al):
+        return self.pool.set_head_thresholds(ah, al)
+
     def quant_write_prefill(self, k, v, sig):
         return self.pool.quant_write_prefill(_np(k), _np(v), _np(sig))
 

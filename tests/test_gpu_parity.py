@@ -15,9 +15,11 @@ def _mk(scn):
     return H.OracleBackend(scn), GpuBackend(scn)
 
 
-def _lifecycle(scn, steps, prompt_lens, frees=(), readmit_len=None, pages_every=1, tol_steps=None):
+def _lifecycle(scn, steps, prompt_lens, frees=(), readmit_len=None, pages_every=1, tol_steps=None, head=None):
     from tests.gpu_backend import compare_state, dec_np
     o, g = _mk(scn)
+    if head is not None:                                         # NEXT-4: per-head thresholds on both sides
+        assert o.set_head_thresholds(*head) == 0 and g.set_head_thresholds(*head) == 0
     inp = H.Inputs(scn)
     life = H.Lifecycle(scn)
     counter = {"n": 0}
@@ -151,3 +153,16 @@ def test_fig5_on_gpu():
     assert int(ctrl[0]) == e["start_after"] and int(ctrl[1]) == e["free_after"]
     free_region = [int(ring[(int(ctrl[0]) + k) % 16]) for k in range(int(ctrl[1]))]
     assert free_region == e["free_region_after"]
+
+
+# ---------------------------------------------------------------- NEXT-4: per-head thresholds (Q35)
+@pytest.mark.parametrize("workflow", [0, 1])
+def test_per_head_thresholds_parity(workflow):
+    scn = H.TINY.replace(R=5, Ly=3, H=6, d=128, M=700, W=32, P=30000, seed=41, tile_units=256,
+                         prefill_workflow=workflow)
+    rng = np.random.default_rng(41)
+    n = scn.Ly * scn.H
+    ah = rng.choice([0.5, 1.0, 3.0, 1e30], size=n).astype(np.float32)
+    al = rng.choice([0.0, 0.02, 0.1, 1e30], size=n).astype(np.float32)
+    _lifecycle(scn, steps=20, prompt_lens=[300, 64, 200, 17, 450], frees=[(8, [1, 3])], readmit_len=150,
+               pages_every=4, head=(ah, al))
