@@ -128,6 +128,8 @@ typedef struct {
   int64_t off_secmin;          /* int32[units][8]: per-section (significance, position, slot) minima written by
                                   dkv_attend, consumed by the next dkv_classify(DECODE) (NEXT-2) */
   int64_t off_head_alpha;      /* fp32[layers * kv_heads][2]: per-head (alpha_h, alpha_l) (NEXT-4) */
+  int64_t off_att_scratch;     /* NEXT-2 long contexts: 296 slots of (ceil4(q_per_kv) + 2) * max_seq_len fp32 when
+                                  those do not fit in shared memory (0 bytes otherwise) */
 } dkv_layout_t;
 
 /* Arena size for `cfg`, or 0 if the configuration is invalid. */
@@ -191,7 +193,8 @@ dkv_status_t dkv_quant_write(dkv_pool_t p, int32_t phase, const dkv_decision_t* 
  * output, d_probs (device fp32 [U][max_seq_len]) the per-token scores (max over the group) in token order
  * (high slots, low slots, window oldest first); either may be NULL.  Deterministic: every floating-point
  * result is fixed by Q31-Q34 (bit-identical to the oracle).  Allowed between sequences; DKV_ERR_INVALID_ARG
- * if q_per_kv is 0 / unsupported or q_per_kv * max_seq_len * 4 B of logits exceed shared memory.
+ * if q_per_kv is 0 / unsupported.  Long contexts (logits beyond shared memory) run a persistent form whose
+ * logits live in the arena's scratch slots (off_att_scratch).
  * With NEXT-2 the decode step passes d_sig = NULL to dkv_classify / dkv_quant_write: t_c's significance is
  * then read from the window. */
 dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* d_probs, dkv_stream_t s);

@@ -96,6 +96,8 @@ struct PoolDev {
   int32_t* secmin;      // [U][8] {sig_h, pos_h, slot_h, sig_l, pos_l, slot_l, valid, 0} from dkv_attend
   int32_t G;            // q_per_kv
   float* head_alpha;    // [LyH][2] per-head (alpha_h, alpha_l) (NEXT-4)
+  float* att_scratch;   // [att_slots][GP + 2][M] long-context attention scratch (NEXT-2), or null
+  int32_t att_slots;
   int32_t use_head_alpha;   // 1: head_alpha replaces alpha_h / alpha_l
   int32_t prefill_wf;   // dkv_config_t.prefill_workflow
 };
@@ -948,6 +950,7 @@ cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, in
 cudaError_t launch_recycle(const PoolDev& p, const int32_t* req, int n, cudaStream_t s);
 cudaError_t launch_attend(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s);
 size_t attend_smem_bytes(const PoolDev& p, int TS);
+size_t attend_long_smem_bytes(const PoolDev& p);
 cudaError_t launch_prefill_conservative(const PoolDev& p, cudaStream_t s);
 cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
                                 const float* sig, cudaStream_t s);

@@ -94,16 +94,16 @@ __device__ __forceinline__ void dot_stored(const float* __restrict__ qf, const u
   }
 }
 
-template <int D, int G>
-__global__ void __launch_bounds__(kAttThreads)
-attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs,
-              int TS) {                                          // TS: shared-memory token capacity (>= any T)
+// One unit.  LONG: the logits and (s, z) pairs live in a per-CTA slot of HBM scratch instead of shared memory
+// (contexts whose q_per_kv * length floats exceed shared memory; the kernel is then persistent).
+template <int D, int G, bool LONG>
+__device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __restrict__ q, float* __restrict__ out,
+                                            float* __restrict__ probs, int TS, int u, float* g_lg, float2* g_vsz) {
   extern __shared__ __align__(16) float att_smem[];
   __shared__ float s_red[kAttThreads / 32][G];
   __shared__ float s_m[G], s_Z[G];
   __shared__ unsigned long long s_min[2];
   __shared__ int s_slot[2];
-  const int u = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (ld_volatile(&p.ctrl->status) != 0) return;                  // sticky error: no-op
   const int r = fdiv(p.div_LyH, u);
@@ -120,14 +120,14 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
   constexpr int GP = padded_heads<G>();
   // every region is carved by float offsets from the shared base (keeps the compiler on shared-space loads)
   const int off_lg = G * D;                                       // multiple of 4 floats
-  const int off_part = off_lg + GP * M;
+  const int off_part = off_lg + (LONG ? 0 : GP * M);
   const int off_pid = off_part + G * (L + 1);
   const int off_vsz = (off_pid + L + 1) & ~1;                     // 8-B aligned
   S.qf = att_smem;
-  S.lg = att_smem + off_lg;
+  S.lg = LONG ? g_lg : att_smem + off_lg;
   S.part = att_smem + off_part;
   S.pid = reinterpret_cast<int32_t*>(att_smem + off_pid);
-  S.vsz = reinterpret_cast<float2*>(att_smem + off_vsz);
+  S.vsz = LONG ? g_vsz : reinterpret_cast<float2*>(att_smem + off_vsz);
   const int32_t* row = p.table + (size_t)u * L;
   for (int k = tid; k < ph + pl; k += kAttThreads) S.pid[k] = k < ph ? row[k] : row[L - 1 - (k - ph)];
   for (int k = tid; k < G * D; k += kAttThreads)
@@ -283,7 +283,7 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
     constexpr int PPR = G <= 4 ? 16 : 8;                          // pages per round
     constexpr int EPL = D / 32;                                   // elements per lane
     const int vseg = max(Ch * gh.v_row, Cl * gl.v_row);           // bytes of one page's value segment
-    const int off_part4 = ((off_vsz + 2 * M) + 3) & ~3;           // [PPR][G][D] page partials
+    const int off_part4 = ((off_vsz + (LONG ? 0 : 2 * M)) + 3) & ~3;   // [PPR][G][D] page partials
     float* part4 = att_smem + off_part4;
     uint8_t* seg = reinterpret_cast<uint8_t*>(att_smem + off_part4 + PPR * G * D) + (size_t)warp * ((vseg + 15) & ~15);
     float run[(G * D + kAttThreads - 1) / kAttThreads];
@@ -370,6 +370,33 @@ attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out
   }
 }
 
+template <int D, int G>
+__global__ void __launch_bounds__(kAttThreads)
+attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs, int TS) {
+  attend_unit<D, G, false>(p, q, out, probs, TS, blockIdx.x, nullptr, nullptr);
+}
+
+// persistent form for long contexts: CTA b owns scratch slot b and walks units b, b + grid, ...
+template <int D, int G>
+__global__ void __launch_bounds__(kAttThreads)
+attend_long_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs,
+                   int TS) {
+  constexpr int GP = padded_heads<G>();
+  float* lg = p.att_scratch + (size_t)blockIdx.x * (GP + 2) * (size_t)TS;
+  float2* vsz = reinterpret_cast<float2*>(lg + (size_t)GP * TS);
+  for (int u = blockIdx.x; u < p.U; u += gridDim.x) {
+    attend_unit<D, G, true>(p, q, out, probs, TS, u, lg, vsz);
+    __syncthreads();                                              // shared state is reused by the next unit
+  }
+}
+
+size_t attend_long_smem_bytes(const PoolDev& p) {
+  const size_t G = p.G > 0 ? p.G : 1, PPR = G <= 4 ? 16 : 8;
+  const size_t vseg = (size_t)std::max(p.g[1].C * p.g[1].v_row, p.g[2].C * p.g[2].v_row);
+  const size_t segs = (size_t)(kAttThreads / 32) * ((vseg + 15) & ~(size_t)15);
+  return 4 * (G * p.d + G * (size_t)(p.L + 1) + (size_t)p.L + 2 + 4 + PPR * G * (size_t)p.d) + segs;
+}
+
 size_t attend_smem_bytes(const PoolDev& p, int TS) {
   const size_t G = p.G > 0 ? p.G : 1, GP = (G + 3) / 4 * 4, PPR = G <= 4 ? 16 : 8;
   const size_t vseg = (size_t)std::max(p.g[1].C * p.g[1].v_row, p.g[2].C * p.g[2].v_row);
@@ -381,6 +408,16 @@ size_t attend_smem_bytes(const PoolDev& p, int TS) {
 
 template <int D, int G>
 static cudaError_t launch_att(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s) {
+  if (TS < 0) {                                                   // long-context form (scratch slots in HBM)
+    const int ts = -TS;
+    const size_t smem = attend_long_smem_bytes(p);
+    cudaError_t e = cudaFuncSetAttribute(attend_long_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    const int grid = p.U < p.att_slots ? p.U : p.att_slots;
+    attend_long_kernel<D, G><<<grid, kAttThreads, smem, s>>>(p, q, out, probs, ts);
+    return cudaGetLastError();
+  }
   const size_t smem = attend_smem_bytes(p, TS);
   cudaError_t e = cudaFuncSetAttribute(attend_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -31,6 +31,9 @@ void class_geom(int d, int C, int kb, int vb, ClassGeom& g) {
 }
 int class_end(const ClassGeom& g) { return g.off_pos + 4 * g.C; }
 
+constexpr int kAttSlots = 296;                               // 2 x 148 SMs
+constexpr int64_t kAttSmemLongThreshold = 160 * 1024;         // logits + (s, z) bytes beyond which HBM slots exist
+
 struct Geometry {
   int32_t U, L, page_bytes, num_tiles, tile_units, nseg;
   ClassGeom g[3];
@@ -83,6 +86,13 @@ bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
   Lo.off_win_sig = take(4 * (int64_t)G.U * c->window);
   Lo.off_secmin = take(32 * (int64_t)G.U);
   Lo.off_head_alpha = take(8 * (int64_t)c->num_layers * c->num_kv_heads);
+  // NEXT-2 long contexts: when q_per_kv * max_seq_len logits + (s, z) pairs cannot stay in shared memory
+  // (227 KB per CTA on sm_100), kAttSlots persistent CTAs keep them in HBM slots
+  {
+    const int64_t GP = (c->q_per_kv + 3) / 4 * 4, Mp = (c->max_seq_len + 31) / 32 * 32;
+    const bool need = c->q_per_kv > 0 && (GP + 2) * Mp * 4 > kAttSmemLongThreshold;
+    Lo.off_att_scratch = take(need ? (int64_t)kAttSlots * (GP + 2) * Mp * 4 : 0);
+  }
   Lo.off_ring = take(4 * P);
   Lo.off_table = take(4 * U * G.L);
   Lo.off_n_h = take(4 * U);
@@ -225,6 +235,12 @@ dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_
   d.win_sig = (float*)(b + Lo.off_win_sig);
   d.secmin = (int32_t*)(b + Lo.off_secmin);
   d.head_alpha = (float*)(b + Lo.off_head_alpha);
+  {
+    const int64_t GP = (cfg->q_per_kv + 3) / 4 * 4, Mp = (cfg->max_seq_len + 31) / 32 * 32;
+    const bool need = cfg->q_per_kv > 0 && (GP + 2) * Mp * 4 > kAttSmemLongThreshold;
+    d.att_scratch = need ? (float*)(b + Lo.off_att_scratch) : nullptr;
+    d.att_slots = need ? kAttSlots : 0;
+  }
   d.use_head_alpha = 0;
   d.G = cfg->q_per_kv;
   d.prefill_wf = cfg->prefill_workflow;
@@ -376,7 +392,11 @@ dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* 
   for (int r = 0; r < p->cfg.max_requests; r++)
     if (p->req_state[r] == DKV_REQ_ACTIVE && p->seq_len[r] > TS) TS = p->seq_len[r];
   TS = (TS + 31) & ~31;
-  if (attend_smem_bytes(p->dev, TS) > (size_t)optin) return DKV_ERR_INVALID_ARG;
+  if (attend_smem_bytes(p->dev, TS) > (size_t)optin) {
+    // long context: logits in the HBM scratch slots (persistent kernel), token capacity = max_seq_len
+    if (!p->dev.att_scratch || attend_long_smem_bytes(p->dev) > (size_t)optin) return DKV_ERR_INVALID_ARG;
+    TS = -((p->cfg.max_seq_len + 31) & ~31);
+  }
   cudaError_t e = launch_attend(p->dev, d_q, d_out, d_probs, TS, (cudaStream_t)s);
   return e == cudaSuccess ? DKV_OK : DKV_ERR_CUDA;
 }

@@ -63,7 +63,8 @@ class dkv_layout_t(C.Structure):
         [(n, C.c_int32 * 3) for n in ("C", "k_row", "v_row", "off_k", "off_kmeta", "off_v", "off_vmeta",
                                        "off_score", "off_pos")] + [("off_tile_sums", C.c_int64), ("off_rec", C.c_int64),
                                                                   ("off_win_sig", C.c_int64), ("off_secmin", C.c_int64),
-                                                                  ("off_head_alpha", C.c_int64)]
+                                                                  ("off_head_alpha", C.c_int64),
+                                                                  ("off_att_scratch", C.c_int64)]
 
 
 assert C.sizeof(dkv_decision_t) == 16

@@ -94,3 +94,11 @@ def test_fused_victim_matches_scan():
         _, d = g.classify_decode(None)
         decs.append(dec_np(d).copy())
     assert np.array_equal(decs[0].view(np.uint8), decs[1].view(np.uint8))
+
+
+def test_attention_parity_long_context():
+    # Qwen-32B-style thinking shard (BASELINE configs[2] shape): 33k max length, GQA group of 5, alpha (3, 0):
+    # the logits of a 20k-token request do not fit in shared memory -> the persistent form with HBM slots
+    scn = H.TINY.replace(R=2, Ly=2, H=2, d=128, M=33792, W=64, P=8000, seed=13, q_per_kv=5,
+                         alpha_h=3.0, alpha_l=0.0, mix=(0.4, 0.6, 0.0))
+    _run(scn, [20000, 6000], steps=3, seed=7)
