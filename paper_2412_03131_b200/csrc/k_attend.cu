@@ -47,6 +47,14 @@ __device__ __forceinline__ float dq(uint32_t code, float sf, float zf) {
   return __fmaf_rn(sf, __uint_as_float(0x4B000000u | code) - 8388608.0f, zf);
 }
 
+// one output warp's shared-memory area: a page's value codes + value (s, z) pairs (the contiguous span from
+// off_v), later overwritten by the warp's [G][D] fp32 page partial
+__host__ __device__ inline int attend_warp_area(const ClassGeom& a, const ClassGeom& b, int G, int D) {
+  const int sa = a.off_vmeta - a.off_v + 4 * a.C, sb = b.off_vmeta - b.off_v + 4 * b.C;
+  const int span = ((sa > sb ? sa : sb) + 15) & ~15;
+  return span > 4 * G * D ? span : 4 * G * D;
+}
+
 template <int G>
 constexpr int padded_heads() { return (G + 3) / 4 * 4; }          // lg row stride: 16-B aligned per token
 
@@ -55,7 +63,6 @@ struct AttShared {
   float* lg;        // [M][GP] logits -> exp -> probabilities, token-major (one 16-B load per 4 heads)
   float* part;      // [G][npage]
   int32_t* pid;     // [ph + pl] page IDs, section order
-  float2* vsz;      // [M] value (s, z) of stored tokens as fp32
 };
 
 // Accumulate the G dot products of the query heads with one stored key of BITS-bit codes: the whole code
@@ -98,7 +105,7 @@ __device__ __forceinline__ void dot_stored(const float* __restrict__ qf, const u
 // (contexts whose q_per_kv * length floats exceed shared memory; the kernel is then persistent).
 template <int D, int G, bool LONG>
 __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __restrict__ q, float* __restrict__ out,
-                                            float* __restrict__ probs, int TS, int u, float* g_lg, float2* g_vsz) {
+                                            float* __restrict__ probs, int TS, int u, float* g_lg) {
   extern __shared__ __align__(16) float att_smem[];
   __shared__ float s_red[kAttThreads / 32][G];
   __shared__ float s_m[G], s_Z[G];
@@ -122,12 +129,10 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
   const int off_lg = G * D;                                       // multiple of 4 floats
   const int off_part = off_lg + (LONG ? 0 : GP * M);
   const int off_pid = off_part + G * (L + 1);
-  const int off_vsz = (off_pid + L + 1) & ~1;                     // 8-B aligned
   S.qf = att_smem;
   S.lg = LONG ? g_lg : att_smem + off_lg;
   S.part = att_smem + off_part;
   S.pid = reinterpret_cast<int32_t*>(att_smem + off_pid);
-  S.vsz = LONG ? g_vsz : reinterpret_cast<float2*>(att_smem + off_vsz);
   const int32_t* row = p.table + (size_t)u * L;
   for (int k = tid; k < ph + pl; k += kAttThreads) S.pid[k] = k < ph ? row[k] : row[L - 1 - (k - ph)];
   for (int k = tid; k < G * D; k += kAttThreads)
@@ -153,9 +158,6 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
       const int idx = hi ? s - (pg * Ch) : s - (pg - ph) * Cl;
       const uint8_t* page = p.pages + (size_t)S.pid[pg] * (size_t)p.page_bytes;
       const uint32_t km = *reinterpret_cast<const uint32_t*>(page + gg.off_kmeta + 4 * idx);
-      const uint32_t vm = *reinterpret_cast<const uint32_t*>(page + gg.off_vmeta + 4 * idx);
-      S.vsz[i] = make_float2(__half2float(__ushort_as_half((unsigned short)(vm & 0xFFFFu))),
-                             __half2float(__ushort_as_half((unsigned short)(vm >> 16))));
       const uint8_t* krow = page + gg.off_k + idx * gg.k_row;
       if (gg.kbits == 8) dot_stored<D, G, 8>(S.qf, krow, km, acc);
       else if (gg.kbits == 4) dot_stored<D, G, 4>(S.qf, krow, km, acc);
@@ -275,17 +277,19 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
     m[6] = 1;
   }
   // ---- 4. output (Q32): pages in order, each page's partial a fma chain over its tokens.  Rounds of PPR
-  // pages: warp w computes page (round * PPR + w) for every (element, head) — lane owns EPL elements and all
-  // heads, so its 16-32 chains are independent — from the page's value segment staged in shared memory;
-  // then thread (head, element) adds the round's partials to its running sum in page order.  A lane owns
-  // EPL consecutive elements, so one aligned 32-bit shared load yields all of its codes of a token.
+  // pages: warp w < PPR computes page (round * PPR + w) for every (element, head) — lane owns EPL elements and
+  // all heads, so its 16-32 chains are independent — from the page's value codes and value (s, z) pairs (one
+  // contiguous span of the page) staged in the warp's shared-memory area; the warp then overwrites that area
+  // with its [G][D] page partial, and thread (head, element) adds the round's partials to its running sum in
+  // page order.  A lane owns EPL consecutive elements, so one aligned 32-bit shared load yields all of its
+  // codes of a token.
   if (out != nullptr) {
     constexpr int PPR = G <= 4 ? 16 : 8;                          // pages per round
     constexpr int EPL = D / 32;                                   // elements per lane
-    const int vseg = max(Ch * gh.v_row, Cl * gl.v_row);           // bytes of one page's value segment
-    const int off_part4 = ((off_vsz + (LONG ? 0 : 2 * M)) + 3) & ~3;   // [PPR][G][D] page partials
-    float* part4 = att_smem + off_part4;
-    uint8_t* seg = reinterpret_cast<uint8_t*>(att_smem + off_part4 + PPR * G * D) + (size_t)warp * ((vseg + 15) & ~15);
+    const int wbytes = attend_warp_area(gh, gl, G, D);
+    uint8_t* seg0 = reinterpret_cast<uint8_t*>(att_smem + ((off_pid + L + 1 + 3) & ~3));   // PPR warp areas
+    uint8_t* seg = seg0 + (size_t)warp * wbytes;
+    float* part4 = reinterpret_cast<float*>(seg);                 // [G][D], after the page is consumed
     float run[(G * D + kAttThreads - 1) / kAttThreads];
 #pragma unroll
     for (int j = 0; j < (G * D + kAttThreads - 1) / kAttThreads; j++) run[j] = 0.0f;
@@ -303,7 +307,8 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
           const int t0 = hi ? k * Ch : nh + (k - ph) * Cl;
           const int cnt = min(hi ? Ch : Cl, (hi ? nh : nh + nl) - t0);
           const uint8_t* src = p.pages + (size_t)S.pid[k] * (size_t)p.page_bytes + gg.off_v;
-          const int nbytes = cnt * gg.v_row;
+          const int mbase = gg.off_vmeta - gg.off_v;              // value (s, z) pairs follow the codes
+          const int nbytes = mbase + 4 * cnt;
           for (int o = 16 * lane; o < nbytes; o += 512)
             *reinterpret_cast<uint4*>(seg + o) = *reinterpret_cast<const uint4*>(src + o);
           __syncwarp();
@@ -311,7 +316,9 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
           const uint32_t mk = (1u << vb) - 1u;
           for (int j = 0; j < cnt; j++) {
             const int i = t0 + j;
-            const float2 sz = S.vsz[i];
+            const uint32_t vm = *reinterpret_cast<const uint32_t*>(seg + mbase + 4 * j);
+            const float2 sz = make_float2(__half2float(__ushort_as_half((unsigned short)(vm & 0xFFFFu))),
+                                          __half2float(__ushort_as_half((unsigned short)(vm >> 16))));
             float av[G];
 #pragma unroll
             for (int g4 = 0; g4 < GP; g4 += 4) {
@@ -332,7 +339,7 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
               for (int g = 0; g < G; g++) acc[x][g] = __fmaf_rn(av[g], v, acc[x][g]);
             }
           }
-          __syncwarp();                                           // seg is reused by this warp's next page
+          __syncwarp();                                           // seg now takes the page partial
         } else {                                                  // the window page, oldest first
           for (int i = nh + nl; i < T; i++) {
             const int pos = N - nw + (i - nh - nl);
@@ -351,14 +358,15 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
 #pragma unroll
         for (int x = 0; x < EPL; x++)
 #pragma unroll
-          for (int g = 0; g < G; g++) part4[(warp * G + g) * D + EPL * lane + x] = acc[x][g];
+          for (int g = 0; g < G; g++) part4[g * D + EPL * lane + x] = acc[x][g];
       }
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < (G * D + kAttThreads - 1) / kAttThreads; j++) {
         const int t = tid + j * kAttThreads;                      // (head, element) = (t / D, t % D)
         if (t < G * D)
-          for (int w = 0; w < PPR && r0 + w < npage; w++) run[j] = __fadd_rn(run[j], part4[w * G * D + t]);
+          for (int w = 0; w < PPR && r0 + w < npage; w++)
+            run[j] = __fadd_rn(run[j], reinterpret_cast<const float*>(seg0 + (size_t)w * wbytes)[t]);
       }
       __syncthreads();                                            // partials are rewritten next round
     }
@@ -371,39 +379,37 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
 }
 
 template <int D, int G>
-__global__ void __launch_bounds__(kAttThreads)
+__global__ void __launch_bounds__(kAttThreads, 2)
 attend_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs, int TS) {
-  attend_unit<D, G, false>(p, q, out, probs, TS, blockIdx.x, nullptr, nullptr);
+  attend_unit<D, G, false>(p, q, out, probs, TS, blockIdx.x, nullptr);
 }
 
 // persistent form for long contexts: CTA b owns scratch slot b and walks units b, b + grid, ...
 template <int D, int G>
-__global__ void __launch_bounds__(kAttThreads)
+__global__ void __launch_bounds__(kAttThreads, 2)
 attend_long_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs,
                    int TS) {
   constexpr int GP = padded_heads<G>();
   float* lg = p.att_scratch + (size_t)blockIdx.x * (GP + 2) * (size_t)TS;
-  float2* vsz = reinterpret_cast<float2*>(lg + (size_t)GP * TS);
   for (int u = blockIdx.x; u < p.U; u += gridDim.x) {
-    attend_unit<D, G, true>(p, q, out, probs, TS, u, lg, vsz);
+    attend_unit<D, G, true>(p, q, out, probs, TS, u, lg);
     __syncthreads();                                              // shared state is reused by the next unit
   }
 }
 
-size_t attend_long_smem_bytes(const PoolDev& p) {
+// bytes of shared memory per unit besides the logits: q, Z page partials, page IDs (+ alignment), and PPR warp
+// areas, each holding one page's value codes + (s, z) pairs, then that page's [G][D] output partial
+static size_t attend_fixed_bytes(const PoolDev& p) {
   const size_t G = p.G > 0 ? p.G : 1, PPR = G <= 4 ? 16 : 8;
-  const size_t vseg = (size_t)std::max(p.g[1].C * p.g[1].v_row, p.g[2].C * p.g[2].v_row);
-  const size_t segs = (size_t)(kAttThreads / 32) * ((vseg + 15) & ~(size_t)15);
-  return 4 * (G * p.d + G * (size_t)(p.L + 1) + (size_t)p.L + 2 + 4 + PPR * G * (size_t)p.d) + segs;
+  return 4 * (G * p.d + G * (size_t)(p.L + 1) + (size_t)p.L + 1 + 3) +
+         PPR * (size_t)attend_warp_area(p.g[1], p.g[2], (int)G, p.d);
 }
 
+size_t attend_long_smem_bytes(const PoolDev& p) { return attend_fixed_bytes(p); }
+
 size_t attend_smem_bytes(const PoolDev& p, int TS) {
-  const size_t G = p.G > 0 ? p.G : 1, GP = (G + 3) / 4 * 4, PPR = G <= 4 ? 16 : 8;
-  const size_t vseg = (size_t)std::max(p.g[1].C * p.g[1].v_row, p.g[2].C * p.g[2].v_row);
-  const size_t segs = (size_t)(kAttThreads / 32) * ((vseg + 15) & ~(size_t)15);   // per-warp value segments
-  // floats: q, logits, Z page partials, page IDs, (s, z) pairs, output page partials, + alignment slack
-  return 4 * (G * p.d + GP * (size_t)TS + G * (size_t)(p.L + 1) + (size_t)p.L + 2 + 2 * (size_t)TS + 4 +
-              PPR * G * (size_t)p.d) + segs;
+  const size_t G = p.G > 0 ? p.G : 1, GP = (G + 3) / 4 * 4;
+  return attend_fixed_bytes(p) + 4 * GP * (size_t)TS;             // + the logits, token-major
 }
 
 template <int D, int G>
