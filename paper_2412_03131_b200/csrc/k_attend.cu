@@ -22,7 +22,14 @@
 
 namespace dkv {
 
-constexpr int kAttThreads = 512;
+#ifndef DKV_ATT_THREADS
+#define DKV_ATT_THREADS 512
+#endif
+constexpr int kAttThreads = DKV_ATT_THREADS;                      // 2 CTAs per SM (launch bounds)
+// output pages per round: one per warp, at most 16 (G <= 4) / 8 page partials of [G][D] floats
+__host__ __device__ constexpr int att_ppr(int G) {
+  return (G <= 4 ? 16 : 8) < kAttThreads / 32 ? (G <= 4 ? 16 : 8) : kAttThreads / 32;
+}
 
 // Q32: exp for x <= 0 — 2^t, t = x*log2(e), n = rint(t), f = t - n, degree-6 Taylor polynomial of 2^f in
 // Horner form, times 2^n; 0 below t = -125.  Every step one IEEE binary32 operation (as the oracle's orc_exp).
@@ -81,13 +88,24 @@ __device__ __forceinline__ void dot_stored(const float* __restrict__ qf, const u
     const uint4 v = *reinterpret_cast<const uint4*>(row + 16 * k);
     w[4 * k] = v.x; w[4 * k + 1] = v.y; w[4 * k + 2] = v.z; w[4 * k + 3] = v.w;
   }
+  constexpr int PB = 8 / BITS;                                    // codes per byte
+  constexpr uint32_t MB = Q * (0x01010101u);                      // the code mask in every byte
 #pragma unroll
   for (int k = 0; k < NW; k++) {
+    // part[i] byte b = code (b * PB + i) of the word (Q17: lowest element in the least-significant bits); one
+    // byte permute then yields the float 2^23 + code (exact), and the subtraction of 2^23 is exact too
+    uint32_t part[PB];
+#pragma unroll
+    for (int i = 0; i < PB; i++) part[i] = (w[k] >> (i * BITS)) & MB;
 #pragma unroll
     for (int j = 0; j < PER; j += 4) {
       float x[4];
 #pragma unroll
-      for (int jj = 0; jj < 4; jj++) x[jj] = dq((w[k] >> ((j + jj) * BITS)) & Q, sf, zf);
+      for (int jj = 0; jj < 4; jj++) {
+        const int e = j + jj;
+        const float c = __uint_as_float(__byte_perm(part[e % PB], 0x4B000000u, 0x7540u | (uint32_t)(e / PB)));
+        x[jj] = __fmaf_rn(sf, __fsub_rn(c, 8388608.0f), zf);
+      }
       const int e = k * PER + j;
 #pragma unroll
       for (int g = 0; g < G; g++) {
@@ -97,6 +115,45 @@ __device__ __forceinline__ void dot_stored(const float* __restrict__ qf, const u
         acc[g] = __fmaf_rn(qv.z, x[2], acc[g]);
         acc[g] = __fmaf_rn(qv.w, x[3], acc[g]);
       }
+    }
+  }
+}
+
+// The output chains of one staged page (Q32): for each of its cnt tokens in slot order, this lane's EPL
+// consecutive value elements (EPL * VB bits of one aligned shared word) dequantized with the token's (s, z)
+// and accumulated into the G heads' chains.  Codes become floats as in dot_stored (byte permute, exact).
+template <int D, int G, int VB>
+__device__ __forceinline__ void value_tokens(const uint8_t* seg, int mbase, int v_row, int lane, const float* lg,
+                                             int cnt, float (&acc)[D / 32][G]) {
+  constexpr int EPL = D / 32, GP = padded_heads<G>();
+  constexpr int PB = 8 / VB;
+  constexpr uint32_t MB = ((1u << VB) - 1u) * 0x01010101u;
+  const int bit0 = lane * EPL * VB;
+  const uint8_t* wp = seg + ((bit0 >> 5) << 2);
+  const int sh = bit0 & 31;
+  for (int j = 0; j < cnt; j++) {
+    const uint32_t vm = *reinterpret_cast<const uint32_t*>(seg + mbase + 4 * j);
+    const float sf = __half2float(__ushort_as_half((unsigned short)(vm & 0xFFFFu)));
+    const float zf = __half2float(__ushort_as_half((unsigned short)(vm >> 16)));
+    float av[G];
+#pragma unroll
+    for (int g4 = 0; g4 < GP; g4 += 4) {
+      const float4 a4 = *reinterpret_cast<const float4*>(lg + (size_t)j * GP + g4);
+      if (g4 < G) av[g4] = a4.x;
+      if (g4 + 1 < G) av[g4 + 1] = a4.y;
+      if (g4 + 2 < G) av[g4 + 2] = a4.z;
+      if (g4 + 3 < G) av[g4 + 3] = a4.w;
+    }
+    const uint32_t word = *reinterpret_cast<const uint32_t*>(wp + j * v_row) >> sh;
+    uint32_t part[PB];
+#pragma unroll
+    for (int i = 0; i < PB; i++) part[i] = (word >> (i * VB)) & MB;
+#pragma unroll
+    for (int x = 0; x < EPL; x++) {
+      const float c = __uint_as_float(__byte_perm(part[x % PB], 0x4B000000u, 0x7540u | (uint32_t)(x / PB)));
+      const float v = __fmaf_rn(sf, __fsub_rn(c, 8388608.0f), zf);
+#pragma unroll
+      for (int g = 0; g < G; g++) acc[x][g] = __fmaf_rn(av[g], v, acc[x][g]);
     }
   }
 }
@@ -184,6 +241,12 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
       mx[g] = fmaxf(mx[g], l);
     }
   }
+  // the output phase reads the unit's FP16 window value rows last: pull them into L2 now
+  if (out != nullptr) {
+    const char* wv = reinterpret_cast<const char*>(p.win_v + (size_t)u * W * D);
+    for (int o = tid * 128; o < W * D * 2; o += kAttThreads * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(wv + o));
+  }
   // ---- 2. softmax (Q32)
 #pragma unroll
   for (int g = 0; g < G; g++) {
@@ -220,18 +283,12 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
   }
   __syncthreads();
 
-  // ---- 3. scores, significance (Q33, Q34), section minima
-  for (int i = tid; i < T; i += kAttThreads) {
-    float a = 0.0f;
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-      const float ag = __fdiv_rn(S.lg[(size_t)i * GP + g], s_Z[g]);
-      S.lg[(size_t)i * GP + g] = ag;
-      a = fmaxf(a, ag);                                           // GQA: max over the group (P:361)
-    }
-    if (probs) probs[(size_t)u * p.M + i] = a;
-    float* sp;
-    int pos, cls = 0, slot = 0;
+  // ---- 3. scores, significance (Q33, Q34), section minima.  Two tokens per trip so their score / position
+  // loads overlap; each thread keeps its running (sig, position) minimum and slot per section, so the section
+  // minimum's slot is found without a second pass over the positions.
+  unsigned long long mkey[2] = {~0ull, ~0ull};
+  int mslot[2] = {-1, -1};
+  auto locate = [&](int i, float*& sp, int& pos, int& cls, int& slot) {
     if (i < nh + nl) {
       const bool hi = i < nh;
       const ClassGeom& gg = hi ? gh : gl;
@@ -245,26 +302,46 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
     } else {
       pos = N - nw + (i - nh - nl);
       sp = p.win_sig + (size_t)u * W + fmod_(p.div_W, pos);
+      cls = 0; slot = 0;
     }
-    float sg = *sp;
+  };
+  auto update = [&](int i, float* sp, int pos, int cls, int slot, float sg) {
+    float a = 0.0f;
+#pragma unroll
+    for (int g = 0; g < G; g++) {
+      const float ag = __fdiv_rn(S.lg[(size_t)i * GP + g], s_Z[g]);
+      S.lg[(size_t)i * GP + g] = ag;
+      a = fmaxf(a, ag);                                           // GQA: max over the group (P:361)
+    }
+    if (probs) probs[(size_t)u * p.M + i] = a;
     const int c = N - 2 - pos;                                    // later queries so far
     if (c >= 0) {
       sg = __fdiv_rn(__fadd_rn(__fmul_rn(sg, (float)c), a), (float)(c + 1));
       *sp = sg;
     }
-    if (cls) atomicMin(&s_min[cls - 1], ((unsigned long long)__float_as_uint(sg) << 32) | (uint32_t)pos);
+    if (cls) {
+      const unsigned long long key = ((unsigned long long)__float_as_uint(sg) << 32) | (uint32_t)pos;
+      if (key < mkey[cls - 1]) { mkey[cls - 1] = key; mslot[cls - 1] = slot; }
+    }
+  };
+  for (int i = tid; i < T; i += 2 * kAttThreads) {
+    const int i2 = i + kAttThreads;
+    float *sp1, *sp2 = nullptr;
+    int pos1, cls1, slot1, pos2 = 0, cls2 = 0, slot2 = 0;
+    locate(i, sp1, pos1, cls1, slot1);
+    if (i2 < T) locate(i2, sp2, pos2, cls2, slot2);
+    const float sg1 = *sp1;
+    const float sg2 = i2 < T ? *sp2 : 0.0f;
+    update(i, sp1, pos1, cls1, slot1, sg1);
+    if (i2 < T) update(i2, sp2, pos2, cls2, slot2, sg2);
   }
+#pragma unroll
+  for (int c = 0; c < 2; c++)
+    if (mkey[c] != ~0ull) atomicMin(&s_min[c], mkey[c]);
   __syncthreads();
-  for (int i = tid; i < nh + nl; i += kAttThreads) {             // slot of each section's minimum
-    const bool hi = i < nh;
-    const int slot = hi ? i : i - nh;
-    const int pg = hi ? fdiv(p.div_Ch, slot) : ph + fdiv(p.div_Cl, slot);
-    const ClassGeom& gg = hi ? gh : gl;
-    const int idx = hi ? slot - pg * Ch : slot - (pg - ph) * Cl;
-    const uint8_t* page = p.pages + (size_t)S.pid[pg] * (size_t)p.page_bytes;
-    const int pos = *reinterpret_cast<const int32_t*>(page + gg.off_pos + 4 * idx);
-    if ((uint32_t)pos == (uint32_t)(s_min[hi ? 0 : 1] & 0xFFFFFFFFull)) s_slot[hi ? 0 : 1] = slot;
-  }
+#pragma unroll
+  for (int c = 0; c < 2; c++)
+    if (mkey[c] != ~0ull && mkey[c] == s_min[c]) s_slot[c] = mslot[c];   // positions are unique: one winner
   __syncthreads();
   if (tid == 0) {
     int32_t* m = p.secmin + 8 * (size_t)u;
@@ -284,7 +361,7 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
   // page order.  A lane owns EPL consecutive elements, so one aligned 32-bit shared load yields all of its
   // codes of a token.
   if (out != nullptr) {
-    constexpr int PPR = G <= 4 ? 16 : 8;                          // pages per round
+    constexpr int PPR = att_ppr(G);                               // pages per round
     constexpr int EPL = D / 32;                                   // elements per lane
     const int wbytes = attend_warp_area(gh, gl, G, D);
     uint8_t* seg0 = reinterpret_cast<uint8_t*>(att_smem + ((off_pid + L + 1 + 3) & ~3));   // PPR warp areas
@@ -312,46 +389,42 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
           for (int o = 16 * lane; o < nbytes; o += 512)
             *reinterpret_cast<uint4*>(seg + o) = *reinterpret_cast<const uint4*>(src + o);
           __syncwarp();
-          const int vb = gg.vbits;
-          const uint32_t mk = (1u << vb) - 1u;
-          for (int j = 0; j < cnt; j++) {
-            const int i = t0 + j;
-            const uint32_t vm = *reinterpret_cast<const uint32_t*>(seg + mbase + 4 * j);
-            const float2 sz = make_float2(__half2float(__ushort_as_half((unsigned short)(vm & 0xFFFFu))),
-                                          __half2float(__ushort_as_half((unsigned short)(vm >> 16))));
-            float av[G];
-#pragma unroll
-            for (int g4 = 0; g4 < GP; g4 += 4) {
-              const float4 a4 = *reinterpret_cast<const float4*>(S.lg + (size_t)i * GP + g4);
-              if (g4 < G) av[g4] = a4.x;
-              if (g4 + 1 < G) av[g4 + 1] = a4.y;
-              if (g4 + 2 < G) av[g4 + 2] = a4.z;
-              if (g4 + 3 < G) av[g4 + 3] = a4.w;
-            }
-            // this lane's EPL consecutive elements: EPL * vb bits (4..32, a divisor of 32) in one aligned word
-            const uint8_t* rowp = seg + j * gg.v_row;
-            const int bit0 = lane * EPL * vb;
-            const uint32_t word = *reinterpret_cast<const uint32_t*>(rowp + ((bit0 >> 5) << 2)) >> (bit0 & 31);
-#pragma unroll
-            for (int x = 0; x < EPL; x++) {
-              const float v = dq((word >> (x * vb)) & mk, sz.x, sz.y);
-#pragma unroll
-              for (int g = 0; g < G; g++) acc[x][g] = __fmaf_rn(av[g], v, acc[x][g]);
-            }
-          }
+          if (gg.vbits == 4) value_tokens<D, G, 4>(seg, mbase, gg.v_row, lane, S.lg + (size_t)t0 * GP, cnt, acc);
+          else if (gg.vbits == 2) value_tokens<D, G, 2>(seg, mbase, gg.v_row, lane, S.lg + (size_t)t0 * GP, cnt, acc);
+          else value_tokens<D, G, 8>(seg, mbase, gg.v_row, lane, S.lg + (size_t)t0 * GP, cnt, acc);
           __syncwarp();                                           // seg now takes the page partial
         } else {                                                  // the window page, oldest first
-          for (int i = nh + nl; i < T; i++) {
-            const int pos = N - nw + (i - nh - nl);
-            const __half* vr = p.win_v + ((size_t)u * W + fmod_(p.div_W, pos)) * D;
-            float av[G];
+          constexpr int WB = 8;                                   // window rows in flight per lane
+          for (int i0 = nh + nl; i0 < T; i0 += WB) {
+            uint32_t raw[WB][EPL / 2];
 #pragma unroll
-            for (int g = 0; g < G; g++) av[g] = S.lg[(size_t)i * GP + g];
+            for (int b = 0; b < WB; b++) {
+              const int pos = N - nw + (i0 + b - nh - nl);
+              if (i0 + b < T) {
+                const uint32_t* vr = reinterpret_cast<const uint32_t*>(
+                    p.win_v + ((size_t)u * W + fmod_(p.div_W, pos)) * D) + lane * (EPL / 2);
+                if constexpr (EPL == 4) {
+                  const uint2 t2 = *reinterpret_cast<const uint2*>(vr);
+                  raw[b][0] = t2.x; raw[b][EPL / 2 - 1] = t2.y;
+                } else {
+                  raw[b][0] = vr[0];
+                }
+              }
+            }
 #pragma unroll
-            for (int x = 0; x < EPL; x++) {
-              const float v = __half2float(vr[EPL * lane + x]);
+            for (int b = 0; b < WB; b++) {
+              const int i = i0 + b;
+              if (i < T) {
+                float av[G];
 #pragma unroll
-              for (int g = 0; g < G; g++) acc[x][g] = __fmaf_rn(av[g], v, acc[x][g]);
+                for (int g = 0; g < G; g++) av[g] = S.lg[(size_t)i * GP + g];
+#pragma unroll
+                for (int x = 0; x < EPL; x++) {
+                  const float v = __half2float(__ushort_as_half((unsigned short)(raw[b][x >> 1] >> (16 * (x & 1)))));
+#pragma unroll
+                  for (int g = 0; g < G; g++) acc[x][g] = __fmaf_rn(av[g], v, acc[x][g]);
+                }
+              }
             }
           }
         }
@@ -364,9 +437,19 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
 #pragma unroll
       for (int j = 0; j < (G * D + kAttThreads - 1) / kAttThreads; j++) {
         const int t = tid + j * kAttThreads;                      // (head, element) = (t / D, t % D)
-        if (t < G * D)
-          for (int w = 0; w < PPR && r0 + w < npage; w++)
-            run[j] = __fadd_rn(run[j], reinterpret_cast<const float*>(seg0 + (size_t)w * wbytes)[t]);
+        if (t < G * D) {
+          const float* pp = reinterpret_cast<const float*>(seg0) + t;
+          const int ws = wbytes / 4;
+          if (r0 + PPR <= npage) {                                // full round: all loads first, then the chain
+            float v[PPR];
+#pragma unroll
+            for (int w = 0; w < PPR; w++) v[w] = pp[w * ws];
+#pragma unroll
+            for (int w = 0; w < PPR; w++) run[j] = __fadd_rn(run[j], v[w]);
+          } else {
+            for (int w = 0; r0 + w < npage; w++) run[j] = __fadd_rn(run[j], pp[w * ws]);
+          }
+        }
       }
       __syncthreads();                                            // partials are rewritten next round
     }
@@ -400,7 +483,7 @@ attend_long_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict_
 // bytes of shared memory per unit besides the logits: q, Z page partials, page IDs (+ alignment), and PPR warp
 // areas, each holding one page's value codes + (s, z) pairs, then that page's [G][D] output partial
 static size_t attend_fixed_bytes(const PoolDev& p) {
-  const size_t G = p.G > 0 ? p.G : 1, PPR = G <= 4 ? 16 : 8;
+  const size_t G = p.G > 0 ? p.G : 1, PPR = att_ppr((int)G);
   return 4 * (G * p.d + G * (size_t)(p.L + 1) + (size_t)p.L + 1 + 3) +
          PPR * (size_t)attend_warp_area(p.g[1], p.g[2], (int)G, p.d);
 }
