@@ -200,6 +200,16 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def load_fp32_peak():
+    """FP32 FFMA peak for the attention kernel's ALU roofline: measured by tools/fmabench.cu on a B200
+    (profiles/fp32_peak.json), else the nominal 148 SMs x 128 FMA/clk x 2 x 1.965 GHz."""
+    p = os.path.join(ROOT, "profiles", "fp32_peak.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["fp32_tflops"]), "measured (profiles/fp32_peak.json, tools/fmabench.cu)"
+    return 148 * 128 * 2 * 1.965e9 / 1e12, "nominal (148 SMs x 128 FP32 lanes x 2 x 1965 MHz)"
+
+
 def load_traffic():
     """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch of each kernel, from the committed
     `ncu --set full` summaries (profiles/traffic.json, written by tools/make_profiles.py)."""
@@ -400,7 +410,7 @@ def run_ours(args, rank, world, local):
         gen.manual_seed(c["seed"] + rank)
         qbuf = torch.empty((wl.U, G, d), dtype=torch.float16, device=dev)
         obuf = torch.empty((wl.U, G, d), dtype=torch.float32, device=dev)
-        att_us, cls2_us, step2_us, att_bytes = [], [], [], []
+        att_us, cls2_us, step2_us, att_bytes, att_flops = [], [], [], [], []
         v = pool.views()
         qbuf.normal_(generator=gen)
         pool.attend(qbuf.view(torch.int16), obuf)                 # primes the window significance + minima
@@ -440,6 +450,11 @@ def run_ours(args, rank, world, local):
                 nwin = min(c["W"], int(seq.max()))
                 att_bytes.append(int((nh1.sum() * per_h + nl1.sum() * per_l).item())
                                  + wl.U * (nwin * (4 * d + 8) + G * d * 2 + G * d * 4))
+                # algorithmic fp32 flops (Q31/Q32 arithmetic): per token the G logit and G output fma chains over
+                # d elements (2 G d fma); a stored token's key and value dequantization adds 2 d fma
+                n_stored = int((nh1.sum() + nl1.sum()).item())
+                n_win = wl.U * nwin
+                att_flops.append(2 * ((n_stored + n_win) * 2 * G * d + n_stored * 2 * d))
         st, _ = pool.query()
         assert st == 0, f"device status {st} after the NEXT-2 steps"
         att_mean = max_over_ranks(statistics.mean(att_us), world)
@@ -450,6 +465,16 @@ def run_ours(args, rank, world, local):
                  "classify_fused_us": round(max_over_ranks(statistics.mean(cls2_us), world), 3),
                  "step_us": round(max_over_ranks(statistics.mean(step2_us), world), 1),
                  "q_per_kv": G,
+                 "roofline": {"kernel": "attend_kernel", "bound": "alu",
+                              "achieved": round(statistics.mean(att_flops) / (statistics.mean(att_us) * 1e-6) / 1e12, 2),
+                              "peak": round(load_fp32_peak()[0], 2), "peak_source": load_fp32_peak()[1],
+                              "unit": "TFLOP/s",
+                              "frac": round(statistics.mean(att_flops) / (statistics.mean(att_us) * 1e-6) / 1e12
+                                            / load_fp32_peak()[0], 4),
+                              "algorithmic_flops": int(statistics.mean(att_flops)),
+                              "note": "exact fp32 fma chains (Q31/Q32) on CUDA cores; the kernel also issues the "
+                                      "code->float conversions, softmax and significance work, so it is bound by "
+                                      "instruction issue (ncu: profiles/*prof_attend*)"},
                  "note": "dkv_attend (NEXT-2) supplies significance; classify takes its victims from the "
                          "attention kernel's section minima (no scan)"}
 
