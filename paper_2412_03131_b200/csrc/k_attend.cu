@@ -144,13 +144,23 @@ __device__ __forceinline__ void value_tokens(const uint8_t* seg, int mbase, int 
       if (g4 + 2 < G) av[g4 + 2] = a4.z;
       if (g4 + 3 < G) av[g4 + 3] = a4.w;
     }
-    const uint32_t word = *reinterpret_cast<const uint32_t*>(wp + j * v_row) >> sh;
+    // the lane's EPL * VB code bits: a byte / half-word / word load when they are byte-aligned (no shift)
+    constexpr int LB = EPL * VB;
+    uint32_t word;
+    if constexpr (LB == 8) word = seg[j * v_row + (bit0 >> 3)];
+    else if constexpr (LB == 16) word = *reinterpret_cast<const uint16_t*>(seg + j * v_row + (bit0 >> 3));
+    else if constexpr (LB == 32) word = *reinterpret_cast<const uint32_t*>(seg + j * v_row + (bit0 >> 3));
+    else word = *reinterpret_cast<const uint32_t*>(wp + j * v_row) >> sh;
     uint32_t part[PB];
+    if constexpr (VB != 2) {
 #pragma unroll
-    for (int i = 0; i < PB; i++) part[i] = (word >> (i * VB)) & MB;
+      for (int i = 0; i < PB; i++) part[i] = (word >> (i * VB)) & MB;
+    }
 #pragma unroll
     for (int x = 0; x < EPL; x++) {
-      const float c = __uint_as_float(__byte_perm(part[x % PB], 0x4B000000u, 0x7540u | (uint32_t)(x / PB)));
+      // 2-bit codes: shift + one LOP3 ((w >> s) & 3 | 2^23 bits) per code beats four byte-wise masks
+      const float c = VB == 2 ? __uint_as_float(((word >> (2 * x)) & 3u) | 0x4B000000u)
+                              : __uint_as_float(__byte_perm(part[x % PB], 0x4B000000u, 0x7540u | (uint32_t)(x / PB)));
       const float v = __fmaf_rn(sf, __fsub_rn(c, 8388608.0f), zf);
 #pragma unroll
       for (int g = 0; g < G; g++) acc[x][g] = __fmaf_rn(av[g], v, acc[x][g]);
