@@ -34,6 +34,20 @@ def _unit_records(pages, table_row, n_h, n_l, geom, L):
     return recs
 
 
+def _section(pages, table_row, n, C, off_score, off_pos, cls, L):
+    """score bits (u32) and positions of a section's n slots in slot order, from a device tensor or a host array"""
+    npg = -(-n // C)
+    cols = np.arange(npg) if cls == 1 else L - 1 - np.arange(npg)
+    pids = np.asarray(table_row)[cols].astype(np.int64)
+    if isinstance(pages, torch.Tensor):
+        pg = pages[torch.from_numpy(pids).to(pages.device)].cpu().numpy()
+    else:
+        pg = pages[pids]
+    sc = np.ascontiguousarray(pg[:, off_score:off_score + 4 * C]).view(np.uint32).reshape(-1)[:n]
+    ps = np.ascontiguousarray(pg[:, off_pos:off_pos + 4 * C]).view(np.int32).reshape(-1)[:n]
+    return sc, ps
+
+
 def test_llama8b_fullsize_sampled_parity():
     import bench
     import synth
@@ -138,3 +152,102 @@ def test_synth_generators_device_independent():
     d1 = synth.decode_sig(5, ug, N, 64, 1.0, 0.02, mh, ml)
     d2 = synth.decode_sig(5, ug.cuda(), N.cuda(), 64, 1.0, 0.02, mh.cuda(), ml.cuda()).cpu()
     assert torch.equal(d1.view(torch.int32), d2.view(torch.int32))
+
+
+def test_llama8b_fullsize_attention_sampled_parity():
+    """NEXT-2 at the bench's full size and launch configuration (configs[1], q_per_kv 4 as bench.py times it):
+    dkv_attend over all 16384 units, then a decode step whose classify takes t_c's significance from the window
+    and its victims from the attention kernel's section minima (d_sig NULL).  Two sampled requests (512 units)
+    are recomputed by the oracle one by one: attention outputs, the significance written back (every stored
+    slot's score bits, the window significance), the section minima and the following decisions are bit-exact."""
+    import bench
+    from paper_2412_03131_b200 import Pool, decisions_to_numpy
+    from paper_2412_03131_b200 import dkv as D
+    from tests import harness as H
+    from tests.gpu_backend import dec_np
+
+    c = bench.CONFIGS["llama3_8b"]
+    G, d = c["G"], c["d"]
+    dev = torch.device("cuda", 0)
+    wl = bench.Workload(c, 0, 1, dev)
+    T = c["prompt"]
+    cfg = D.make_config(wl.R, c["Ly"], wl.Hl, d, c["M"], c["W"], c["Ch"], c["Cl"], P=c["P"],
+                        alpha_h=c["alpha_h"], alpha_l=c["alpha_l"], q_per_kv=G)
+    pool = Pool(cfg, device=dev)
+    geom, L, LyH = pool.geom(), pool.L, pool.LyH
+    sig, kk, vv = wl.prefill_inputs(T)
+    reqs = list(range(wl.R))
+    pool.classify_prefill(reqs, [T] * wl.R, sig)
+    pool.compact_alloc(None)
+    pool.quant_write_prefill(kk.view(torch.int16), vv.view(torch.int16), sig)
+    del kk, vv, sig
+
+    sample = (5, 62)
+    scn = H.Scenario(R=2, Ly=c["Ly"], H=c["H"], d=d, M=c["M"], W=c["W"], Ch=c["Ch"], Cl=c["Cl"],
+                     P=2 * LyH * (T // c["Ch"] + 8), alpha_h=c["alpha_h"], alpha_l=c["alpha_l"], seed=c["seed"],
+                     mix=c["mix"], req_ids=sample, q_per_kv=G)
+    o = H.OracleBackend(scn)
+    inp, life = H.Inputs(scn), H.Lifecycle(scn)
+    H.admit([o], inp, life, [0, 1], [T, T])
+    rows = np.concatenate([np.arange(r * LyH, (r + 1) * LyH) for r in sample])
+    rng = np.random.default_rng(11)
+
+    def attend_and_compare(where):
+        q = rng.normal(0, 1, size=(wl.U, G, d)).astype(np.float16)
+        out = torch.empty((wl.U, G, d), dtype=torch.float32, device=dev)
+        assert pool.attend(torch.from_numpy(q.view(np.int16)).to(dev), out) == 0
+        st, oo, _ = o.attend(q[rows], want_out=True, want_probs=False)
+        assert st == 0
+        og = out.cpu().numpy()[rows]
+        assert np.array_equal(oo.view(np.uint32), og.view(np.uint32)), f"[{where}] attention outputs differ"
+        v = pool.views()
+        n_h, n_l = v["n_h"].cpu().numpy(), v["n_l"].cpu().numpy()
+        secmin = v["secmin"].cpu().numpy()
+        win_sig = v["win_sig"].cpu().numpy()
+        gtab = v["table"][torch.from_numpy(rows).to(dev)].cpu().numpy()
+        for i, r in enumerate(sample):
+            for j in range(LyH):
+                ug, uo = r * LyH + j, i * LyH + j
+                assert (n_h[ug], n_l[ug]) == (o.pool.n_h[uo], o.pool.n_l[uo]), (where, r, j)
+                for k, cls in enumerate((1, 2)):
+                    n = int(o.pool.n_h[uo] if cls == 1 else o.pool.n_l[uo])
+                    if n == 0:
+                        continue
+                    # every stored slot's significance (score bits) and position after the write-back
+                    gs, gp = _section(v["pages"], gtab[i * LyH + j], n, geom[cls]["C"], geom[cls]["off_score"],
+                                      geom[cls]["off_pos"], cls, L)
+                    og_ = o.pool.geom[cls]
+                    os_, op_ = _section(o.pool.pages, o.pool.table[uo], n, og_.C, og_.off_score, og_.off_pos, cls, L)
+                    assert np.array_equal(gs, os_) and np.array_equal(gp, op_), (where, r, j, cls)
+                    # the section minimum the next classify uses: (significance bits, position, slot)
+                    key = (os_.astype(np.uint64) << np.uint64(32)) | op_.astype(np.uint32).astype(np.uint64)
+                    s_min = int(np.argmin(key))
+                    want = (int(os_[s_min].view(np.int32)), int(op_[s_min]), s_min)
+                    assert tuple(int(x) for x in secmin[ug][3 * k:3 * k + 3]) == want, (where, r, j, cls)
+                assert np.array_equal(win_sig[ug].view(np.uint32), o.pool.win_sig[uo].view(np.uint32)), (where, r, j)
+
+    attend_and_compare("prefill")
+    dec = pool.new_decisions()
+    seq = np.full(wl.R, T, np.int64)
+    act = np.ones(wl.R, bool)
+    for step in range(2):
+        _, nk, nv = wl.decode_inputs(seq, act)
+        pool.classify_decode(None, dec)
+        pool.compact_alloc(dec)
+        pool.quant_write_decode(dec, nk.view(torch.int16), nv.view(torch.int16), None)
+        seq += 1
+        active = life.state == H.REQ_ACTIVE
+        N = np.where(active, life.seq + 1, 0)
+        _, k, v_ = inp.decode(N)
+        st, do = o.classify_decode(None)
+        assert st == 0
+        assert o.compact_alloc(do) == 0 and o.quant_write_decode(do, k, v_, None) == 0
+        life.seq[active] += 1
+        dg, dor = dec_np(decisions_to_numpy(dec)), dec_np(do)
+        for i, r in enumerate(sample):
+            a = np.ascontiguousarray(dg[r * LyH:(r + 1) * LyH])
+            b = np.ascontiguousarray(dor[i * LyH:(i + 1) * LyH])
+            assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (step, r)
+        attend_and_compare(f"decode {step}")
+    st, _ = pool.query()
+    assert st == 0
