@@ -708,8 +708,9 @@ int32_t orc_free(orc_pool* p, const int32_t* req, int32_t n) {
  *       tokens in the order: high slots 0..n_h-1, low slots 0..n_l-1, window oldest -> newest;
  *   Q32 p = exp(logit - max) with orc_exp (round-to-nearest range reduction + degree-6 polynomial, fixed
  *       operation order); Z = sum over pages in that order of the serial in-page sums (the window counts as
- *       one page); a = fdiv(p, Z); the output row = the serial sum over pages (same order) of each page's
- *       fma chain over its tokens, o_page = fma(a, v_e, o_page) from 0;
+ *       pages of C_h tokens, oldest first, the last one possibly partial); a = fdiv(p, Z); the output row =
+ *       the serial sum over pages (same order) of each page's fma chain over its tokens,
+ *       o_page = fma(a, v_e, o_page) from 0;
  *   Q33 a token's significance is the mean of the scores it received from later tokens; a decode
  *       step adds the score of query N-1 (max over the G heads) to every token p < N-1:
  *       sig' = fdiv(fadd(fmul(sig, c), a), c + 1), c = N-2-p scores so far; a new token starts at 0;
@@ -761,7 +762,7 @@ int32_t orc_attend(orc_pool* p, const uint16_t* q, float* out, float* probs) {
   if (p->status != ORC_OK) return ORC_OK;
   const int32_t LyH = c->Ly * c->H, d = c->d, W = c->W, G = c->q_per_kv, M = c->M;
   att_tok* tok = (att_tok*)malloc(sizeof(att_tok) * (size_t)M);
-  int32_t* tpage = (int32_t*)malloc(4 * (size_t)M);       /* page index of each token (window = last) */
+  int32_t* tpage = (int32_t*)malloc(4 * (size_t)M);       /* page index of each token (window pages last) */
   float* lg = (float*)malloc(4 * (size_t)M * (size_t)G);
   float* a = (float*)malloc(4 * (size_t)M);
   float* kx = (float*)malloc(4 * (size_t)d);
@@ -788,12 +789,13 @@ int32_t orc_attend(orc_pool* p, const uint16_t* q, float* out, float* probs) {
       }
       npage += (cnt + C - 1) / C;
     }
-    for (int32_t ps = (N - W > 0 ? N - W : 0); ps < N; ps++) {
+    const int32_t first = N - W > 0 ? N - W : 0, Cw = p->g[ORC_CLS_HIGH].C;
+    for (int32_t ps = first; ps < N; ps++) {
       att_tok* t = &tok[n];
       size_t ws = (size_t)u * W + (size_t)(ps % W);
       t->pg = NULL; t->cls = 0; t->idx = 0; t->pos = ps;
       t->wk = p->win_k + ws * d; t->wv = p->win_v + ws * d; t->sig = &p->win_sig[ws];
-      tpage[n] = npage;
+      tpage[n] = npage + (ps - first) / Cw;                  /* Q32: window pages of C_h tokens, oldest first */
       n++;
     }
     for (int32_t i = 0; i < n; i++) a[i] = 0.0f;

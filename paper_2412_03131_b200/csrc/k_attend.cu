@@ -8,7 +8,7 @@
 //   1. logits: one thread per token dequantizes its key (X^ = s*Q + z) and accumulates the G dot
 //      products serially over the d elements; logit = dot * (1/sqrt(d));
 //   2. softmax: max per head (order-free), p = dkv_exp(logit - max), Z = pages summed in order of their
-//      serial in-page sums (the window is one page), a = p / Z, score = max over the G heads;
+//      serial in-page sums (the window as pages of C_h tokens), a = p / Z, score = max over the G heads;
 //   3. significance: sig' = (sig * c + score) / (c + 1), c = N - 2 - position (Q33), written in place
 //      (page score segment / window array, Q34); each section's (sig', position) minimum goes to the unit's
 //      secmin record, which lets the next dkv_classify(DECODE) pick its victim without a scan;
@@ -189,13 +189,14 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
   const int T = nh + nl + nw;
   const int Ch = p.g[1].C, Cl = p.g[2].C;
   const int ph = ceil_div(nh, Ch), pl = ceil_div(nl, Cl);
-  const int npage = ph + pl + (nw > 0 ? 1 : 0);
+  const int npage = ph + pl + ceil_div(nw, Ch);                  // Q32: the window as pages of C_h tokens
+  const int PS = L + ceil_div(W, Ch);                            // page-partial stride (pages a unit can have)
   AttShared S;
   constexpr int GP = padded_heads<G>();
   // every region is carved by float offsets from the shared base (keeps the compiler on shared-space loads)
   const int off_lg = G * D;                                       // multiple of 4 floats
   const int off_part = off_lg + (LONG ? 0 : GP * M);
-  const int off_pid = off_part + G * (L + 1);
+  const int off_pid = off_part + G * PS;
   S.qf = att_smem;
   S.lg = LONG ? g_lg : att_smem + off_lg;
   S.part = att_smem + off_part;
@@ -280,15 +281,15 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
     int t0, t1;
     if (k < ph) { t0 = k * Ch; t1 = min(t0 + Ch, nh); }
     else if (k < ph + pl) { t0 = nh + (k - ph) * Cl; t1 = min(t0 + Cl, nh + nl); }
-    else { t0 = nh + nl; t1 = T; }
+    else { t0 = nh + nl + (k - ph - pl) * Ch; t1 = min(t0 + Ch, T); }
     float sum = 0.0f;
     for (int i = t0; i < t1; i++) sum = __fadd_rn(sum, S.lg[(size_t)i * GP + g]);
-    S.part[g * (L + 1) + k] = sum;
+    S.part[g * PS + k] = sum;
   }
   __syncthreads();
   if (tid < G) {                                                  // pages in order
     float Z = 0.0f;
-    for (int k = 0; k < npage; k++) Z = __fadd_rn(Z, S.part[tid * (L + 1) + k]);
+    for (int k = 0; k < npage; k++) Z = __fadd_rn(Z, S.part[tid * PS + k]);
     s_Z[tid] = Z;
   }
   __syncthreads();
@@ -403,14 +404,15 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
           else if (gg.vbits == 2) value_tokens<D, G, 2>(seg, mbase, gg.v_row, lane, S.lg + (size_t)t0 * GP, cnt, acc);
           else value_tokens<D, G, 8>(seg, mbase, gg.v_row, lane, S.lg + (size_t)t0 * GP, cnt, acc);
           __syncwarp();                                           // seg now takes the page partial
-        } else {                                                  // the window page, oldest first
+        } else {                                                  // a window page (C_h tokens, oldest first)
           constexpr int WB = 8;                                   // window rows in flight per lane
-          for (int i0 = nh + nl; i0 < T; i0 += WB) {
+          const int w0 = nh + nl + (k - ph - pl) * Ch, w1 = min(w0 + Ch, T);   // this window page
+          for (int i0 = w0; i0 < w1; i0 += WB) {
             uint32_t raw[WB][EPL / 2];
 #pragma unroll
             for (int b = 0; b < WB; b++) {
               const int pos = N - nw + (i0 + b - nh - nl);
-              if (i0 + b < T) {
+              if (i0 + b < w1) {
                 const uint32_t* vr = reinterpret_cast<const uint32_t*>(
                     p.win_v + ((size_t)u * W + fmod_(p.div_W, pos)) * D) + lane * (EPL / 2);
                 if constexpr (EPL == 4) {
@@ -424,7 +426,7 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
 #pragma unroll
             for (int b = 0; b < WB; b++) {
               const int i = i0 + b;
-              if (i < T) {
+              if (i < w1) {
                 float av[G];
 #pragma unroll
                 for (int g = 0; g < G; g++) av[g] = S.lg[(size_t)i * GP + g];
@@ -494,7 +496,8 @@ attend_long_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict_
 // areas, each holding one page's value codes + (s, z) pairs, then that page's [G][D] output partial
 static size_t attend_fixed_bytes(const PoolDev& p) {
   const size_t G = p.G > 0 ? p.G : 1, PPR = att_ppr((int)G);
-  return 4 * (G * p.d + G * (size_t)(p.L + 1) + (size_t)p.L + 1 + 3) +
+  const size_t PS = (size_t)p.L + (size_t)((p.W + p.g[1].C - 1) / p.g[1].C);   // page partials per head
+  return 4 * (G * p.d + G * PS + (size_t)p.L + 1 + 3) +
          PPR * (size_t)attend_warp_area(p.g[1], p.g[2], (int)G, p.d);
 }
 
