@@ -65,12 +65,21 @@ def test_attention_parity_tiny():
     _run(scn, [64, 64, 64, 64], steps=30, frees=[(10, [2])], readmit=40)
 
 
-@pytest.mark.parametrize("G", [1, 5, 8])
+@pytest.mark.parametrize("G", [1, 2, 4, 5, 7, 8])
 def test_attention_parity_multi_page_d128(G):
     # d = 128, K8V4 / K4V2, several pages per section, ragged prompts, GQA groups of 1 / 5 / 8 heads
     scn = H.TINY.replace(R=3, Ly=2, H=3, d=128, M=700, W=64, P=6000, seed=21, q_per_kv=G,
                          alpha_h=1.0, alpha_l=0.02)
     _run(scn, [520, 70, 300], steps=12, frees=[(4, [1])], readmit=200, seed=G)
+
+
+@pytest.mark.parametrize("G", [2, 7])
+def test_attention_parity_d64_ragged_windows(G):
+    # d = 64 (half-width pages), K8V4 / K4V2, a 16-token window (one window page) next to prompts shorter than
+    # the window, ragged multi-page sections, frees and re-admission
+    scn = H.TINY.replace(R=4, Ly=2, H=2, d=64, M=900, W=16, P=6000, seed=31 + G, q_per_kv=G,
+                         alpha_h=1.0, alpha_l=0.02)
+    _run(scn, [700, 9, 130, 16], steps=10, frees=[(3, [0])], readmit=333, seed=G)
 
 
 def test_fused_victim_matches_scan():
