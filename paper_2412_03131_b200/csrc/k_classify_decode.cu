@@ -6,21 +6,16 @@
 // page IDs are staged in shared memory with one coalesced pass over its table row, then each lane issues
 // kCV 16-B score loads (4 slots each) at once, so a unit costs two dependent memory round trips.  The scan
 // keeps a running unsigned minimum (stored scores are canonical non-negative floats, so bit order is float
-// order) with a tiny update path; whenever the minimum score may be shared by several slots, a rare exact
-// pass re-reads the section and breaks the tie on positions (oldest wins).
+// order) with a tiny update path; whenever the minimum score may be shared by several slots, an exact pass
+// re-reads the section (batched, with the positions of the vectors holding the minimum) and breaks the tie on
+// positions (oldest wins).
 #include "dkv_internal.cuh"
 
 namespace dkv {
 
 constexpr int kCDWarps = 4;                // units (warps) per CTA
 constexpr int kCV = 8;                     // 16-B score vectors per lane per batch (1024 slots per batch)
-
-__device__ __forceinline__ int32_t slot_pos(const PoolDev& p, int cls, int u, int s) {
-  int idx;
-  const uint8_t* pg = slot_page(p, cls, u, s, idx);
-  const int off_pos = cls == DKV_CLS_HIGH ? p.g[1].off_pos : p.g[2].off_pos;
-  return __ldg(reinterpret_cast<const int32_t*>(pg + off_pos) + idx);
-}
+constexpr int kXV = 4;                     // the same for the exact (tie-breaking) pass, which also holds positions
 
 __global__ void __launch_bounds__(kCDWarps * 32)
 classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decision_t* __restrict__ dec) {
@@ -131,18 +126,35 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
     if (__popc(holders) == 1 && !any_tie) {
       vs = __shfl_sync(kFull, bslot, __ffs(holders) - 1);
     } else {
-      // exact pass: among the slots scoring m, the oldest position wins (Q6)
+      // exact pass: among the slots scoring m, the oldest position wins (Q6).  Batched: kXV score vectors
+      // in flight per lane, then one 16-B position vector (the same 4 slots' positions, contiguous in the
+      // page) for every score vector holding m — a section whose minimum is shared by hundreds of slots
+      // (exact zeros when nothing is pruned) costs two round trips per batch, not one per tied slot
+      const int off_pos = cls == DKV_CLS_HIGH ? p.g[1].off_pos : p.g[2].off_pos;
       int32_t bp = 0x7FFFFFFF;
       int bs = -1;
-      for (int s0 = 4 * lane; s0 < n; s0 += 128) {
-        const uint4 x = ld_nc_v4(vec_addr(s0));
-        const uint32_t e4[4] = {x.x, x.y, x.z, x.w};
+      for (int base = 0; base < n; base += 128 * kXV) {
+        uint4 v[kXV], q[kXV];
 #pragma unroll
-        for (int e = 0; e < 4; e++) {
-          if (s0 + e < n && e4[e] == m) {
-            const int32_t ps = slot_pos(p, cls, u, s0 + e);
-            if (ps < bp) { bp = ps; bs = s0 + e; }
-          }
+        for (int j = 0; j < kXV; j++) {
+          const int s0 = base + j * 128 + 4 * lane;
+          v[j] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+          if (s0 < n) v[j] = ld_nc_v4(vec_addr(s0));
+        }
+#pragma unroll
+        for (int j = 0; j < kXV; j++) {
+          const int s0 = base + j * 128 + 4 * lane;
+          if (v[j].x == m || v[j].y == m || v[j].z == m || v[j].w == m)
+            q[j] = ld_nc_v4(vec_addr(s0) - off_score + off_pos);
+        }
+#pragma unroll
+        for (int j = 0; j < kXV; j++) {
+          const int s0 = base + j * 128 + 4 * lane;
+          const uint32_t e4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+          const int32_t p4[4] = {(int32_t)q[j].x, (int32_t)q[j].y, (int32_t)q[j].z, (int32_t)q[j].w};
+#pragma unroll
+          for (int e = 0; e < 4; e++)
+            if (s0 + e < n && e4[e] == m && p4[e] < bp) { bp = p4[e]; bs = s0 + e; }
         }
       }
       const uint32_t mp = __reduce_min_sync(kFull, (uint32_t)bp);
