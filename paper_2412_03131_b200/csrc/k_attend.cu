@@ -56,10 +56,15 @@ __device__ __forceinline__ float dq(uint32_t code, float sf, float zf) {
 
 // one output warp's shared-memory area: a page's value codes + value (s, z) pairs (the contiguous span from
 // off_v), later overwritten by the warp's [G][D] fp32 page partial
-__host__ __device__ inline int attend_warp_area(const ClassGeom& a, const ClassGeom& b, int G, int D) {
+// (long-context form: followed by the page's probabilities, staged from the HBM logit slot)
+__host__ __device__ inline int attend_span(const ClassGeom& a, const ClassGeom& b) {
   const int sa = a.off_vmeta - a.off_v + 4 * a.C, sb = b.off_vmeta - b.off_v + 4 * b.C;
-  const int span = ((sa > sb ? sa : sb) + 15) & ~15;
-  return span > 4 * G * D ? span : 4 * G * D;
+  return ((sa > sb ? sa : sb) + 15) & ~15;
+}
+__host__ __device__ inline int attend_warp_area(const ClassGeom& a, const ClassGeom& b, int G, int D) {
+  const int GP = (G + 3) / 4 * 4, C = a.C > b.C ? a.C : b.C;
+  const int staged = attend_span(a, b) + 4 * GP * C;
+  return staged > 4 * G * D ? staged : 4 * G * D;
 }
 
 template <int G>
@@ -399,10 +404,17 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
           const int nbytes = mbase + 4 * cnt;
           for (int o = 16 * lane; o < nbytes; o += 512)
             *reinterpret_cast<uint4*>(seg + o) = *reinterpret_cast<const uint4*>(src + o);
+          const float* lgp = S.lg + (size_t)t0 * GP;
+          if (LONG) {                                             // the page's probabilities, HBM slot -> shared
+            float* sa = reinterpret_cast<float*>(seg + attend_span(gh, gl));
+            for (int o = 4 * lane; o < cnt * GP; o += 128)
+              *reinterpret_cast<float4*>(sa + o) = *reinterpret_cast<const float4*>(lgp + o);
+            lgp = sa;
+          }
           __syncwarp();
-          if (gg.vbits == 4) value_tokens<D, G, 4>(seg, mbase, gg.v_row, lane, S.lg + (size_t)t0 * GP, cnt, acc);
-          else if (gg.vbits == 2) value_tokens<D, G, 2>(seg, mbase, gg.v_row, lane, S.lg + (size_t)t0 * GP, cnt, acc);
-          else value_tokens<D, G, 8>(seg, mbase, gg.v_row, lane, S.lg + (size_t)t0 * GP, cnt, acc);
+          if (gg.vbits == 4) value_tokens<D, G, 4>(seg, mbase, gg.v_row, lane, lgp, cnt, acc);
+          else if (gg.vbits == 2) value_tokens<D, G, 2>(seg, mbase, gg.v_row, lane, lgp, cnt, acc);
+          else value_tokens<D, G, 8>(seg, mbase, gg.v_row, lane, lgp, cnt, acc);
           __syncwarp();                                           // seg now takes the page partial
         } else {                                                  // a window page (C_h tokens, oldest first)
           constexpr int WB = 8;                                   // window rows in flight per lane
