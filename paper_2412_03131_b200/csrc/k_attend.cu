@@ -215,6 +215,19 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
   const float scale = __fdiv_rn(1.0f, __fsqrt_rn((float)D));
   const ClassGeom gh = p.g[1], gl = p.g[2];
 
+  // a token's GP-float logit / probability row (G heads + zero padding) moves as 16-B vectors
+  auto store_row = [&](int i, const float (&row)[GP]) {
+#pragma unroll
+    for (int g4 = 0; g4 < GP; g4 += 4)
+      *reinterpret_cast<float4*>(S.lg + (size_t)i * GP + g4) = make_float4(row[g4], row[g4 + 1], row[g4 + 2], row[g4 + 3]);
+  };
+  auto load_row = [&](int i, float (&row)[GP]) {
+#pragma unroll
+    for (int g4 = 0; g4 < GP; g4 += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(S.lg + (size_t)i * GP + g4);
+      row[g4] = v.x; row[g4 + 1] = v.y; row[g4 + 2] = v.z; row[g4 + 3] = v.w;
+    }
+  };
   // ---- 1. logits (Q31)
   float mx[G];
 #pragma unroll
@@ -250,12 +263,16 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
         }
       }
     }
+    float row[GP];
 #pragma unroll
-    for (int g = 0; g < G; g++) {
-      const float l = __fmul_rn(acc[g], scale);
-      S.lg[(size_t)i * GP + g] = l;
-      mx[g] = fmaxf(mx[g], l);
+    for (int g = 0; g < GP; g++) {
+      row[g] = 0.0f;
+      if (g < G) {
+        row[g] = __fmul_rn(acc[g], scale);
+        mx[g] = fmaxf(mx[g], row[g]);
+      }
     }
+    store_row(i, row);
   }
   // the output phase reads the unit's FP16 window value rows last: pull them into L2 now
   if (out != nullptr) {
@@ -277,9 +294,13 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
     s_m[tid] = m;
   }
   __syncthreads();
-  for (int i = tid; i < T; i += kAttThreads)
+  for (int i = tid; i < T; i += kAttThreads) {
+    float row[GP];
+    load_row(i, row);
 #pragma unroll
-    for (int g = 0; g < G; g++) S.lg[(size_t)i * GP + g] = dkv_exp(__fsub_rn(S.lg[(size_t)i * GP + g], s_m[g]));
+    for (int g = 0; g < G; g++) row[g] = dkv_exp(__fsub_rn(row[g], s_m[g]));
+    store_row(i, row);
+  }
   __syncthreads();
   for (int it = tid; it < G * npage; it += kAttThreads) {          // serial in-page sums
     const int g = it / npage, k = it % npage;
@@ -322,13 +343,14 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
     }
   };
   auto update = [&](int i, float* sp, int pos, int cls, int slot, float sg) {
-    float a = 0.0f;
+    float a = 0.0f, row[GP];
+    load_row(i, row);
 #pragma unroll
     for (int g = 0; g < G; g++) {
-      const float ag = __fdiv_rn(S.lg[(size_t)i * GP + g], s_Z[g]);
-      S.lg[(size_t)i * GP + g] = ag;
-      a = fmaxf(a, ag);                                           // GQA: max over the group
+      row[g] = __fdiv_rn(row[g], s_Z[g]);
+      a = fmaxf(a, row[g]);                                       // GQA: max over the group
     }
+    store_row(i, row);
     if (probs) probs[(size_t)u * p.M + i] = a;
     const int c = N - 2 - pos;                                    // later queries so far
     if (c >= 0) {
