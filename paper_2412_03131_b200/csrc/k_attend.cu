@@ -302,15 +302,37 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
     store_row(i, row);
   }
   __syncthreads();
-  for (int it = tid; it < G * npage; it += kAttThreads) {          // serial in-page sums
-    const int g = it / npage, k = it % npage;
-    int t0, t1;
+  auto page_range = [&](int k, int& t0, int& t1) {
     if (k < ph) { t0 = k * Ch; t1 = min(t0 + Ch, nh); }
     else if (k < ph + pl) { t0 = nh + (k - ph) * Cl; t1 = min(t0 + Cl, nh + nl); }
     else { t0 = nh + nl + (k - ph - pl) * Ch; t1 = min(t0 + Ch, T); }
-    float sum = 0.0f;
-    for (int i = t0; i < t1; i++) sum = __fadd_rn(sum, S.lg[(size_t)i * GP + g]);
-    S.part[g * PS + k] = sum;
+  };
+  if (LONG) {                                                     // serial in-page sums, a thread per page:
+    for (int k = tid; k < npage; k += kAttThreads) {              // whole rows from the HBM slot, G chains
+      int t0, t1;
+      page_range(k, t0, t1);
+      float sum[GP];
+#pragma unroll
+      for (int g = 0; g < GP; g++) sum[g] = 0.0f;
+#pragma unroll 4
+      for (int i = t0; i < t1; i++) {
+        float row[GP];
+        load_row(i, row);
+#pragma unroll
+        for (int g = 0; g < G; g++) sum[g] = __fadd_rn(sum[g], row[g]);
+      }
+#pragma unroll
+      for (int g = 0; g < G; g++) S.part[g * PS + k] = sum[g];
+    }
+  } else {
+    for (int it = tid; it < G * npage; it += kAttThreads) {        // serial in-page sums
+      const int g = it / npage, k = it % npage;
+      int t0, t1;
+      page_range(k, t0, t1);
+      float sum = 0.0f;
+      for (int i = t0; i < t1; i++) sum = __fadd_rn(sum, S.lg[(size_t)i * GP + g]);
+      S.part[g * PS + k] = sum;
+    }
   }
   __syncthreads();
   if (tid < G) {                                                  // pages in order
