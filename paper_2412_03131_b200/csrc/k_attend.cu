@@ -432,6 +432,15 @@ __device__ __forceinline__ void attend_unit(const PoolDev& p, const uint16_t* __
     for (int j = 0; j < (G * D + kAttThreads - 1) / kAttThreads; j++) run[j] = 0.0f;
     for (int r0 = 0; r0 < npage; r0 += PPR) {
       const int k = r0 + warp;
+      {                                                           // pull the next round's value span into L2
+        const int kn = k + PPR;
+        if (warp < PPR && kn < ph + pl) {
+          const ClassGeom& gn = kn < ph ? gh : gl;
+          const int span = gn.off_vmeta - gn.off_v + 4 * gn.C;
+          const char* src = reinterpret_cast<const char*>(p.pages + (size_t)S.pid[kn] * (size_t)p.page_bytes + gn.off_v);
+          if (lane * 128 < span) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + lane * 128));
+        }
+      }
       if (warp < PPR && k < npage) {
         float acc[EPL][G];
 #pragma unroll
