@@ -136,12 +136,14 @@ class ClockSampler:
 class Workload:
     """Synthetic inputs of one GPU's shard, generated on the device from counters (synth/)."""
 
-    def __init__(self, c, rank, world, device):
+    def __init__(self, c, rank, world, device, strong=False):
         self.c = c
         self.world = world
         assert c["H"] % world == 0
         self.Hl = c["H"] // world
-        self.R = c["R"] * world                      # weak scaling: global batch grows with N
+        # weak scaling (default): the global batch grows with N, per-GPU units fixed; strong: the global batch is
+        # fixed and each GPU's pool holds H/N of its heads
+        self.R = c["R"] if strong else c["R"] * world
         self.shape = synth.Shape(self.R, c["Ly"], self.Hl, H_total=c["H"], h0=rank * self.Hl)
         self.LyH = c["Ly"] * self.Hl
         self.U = self.R * self.LyH
@@ -234,7 +236,7 @@ def run_ours(args, rank, world, local):
 
     c = CONFIGS[args.config]
     dev = torch.device("cuda", local)
-    wl = Workload(c, rank, world, dev)
+    wl = Workload(c, rank, world, dev, strong=args.strong)
     cfg = D.make_config(wl.R, c["Ly"], wl.Hl, c["d"], c["M"], c["W"], c["Ch"], c["Cl"], P=c["P"],
                         alpha_h=c["alpha_h"], alpha_l=c["alpha_l"], tile_units=args.tile_units,
                         q_per_kv=c.get("G", 0))
@@ -297,6 +299,7 @@ def run_ours(args, rank, world, local):
     stats_view = pool.views()["stats"]
     red = torch.empty(4, dtype=torch.int64, device=dev)
     comp_us, cls_us, qw_us, step_us, cls_bytes = [], [], [], [], []
+    ar_us, ar_hidden = [], []
     # launch floor: event -> trivial kernel -> event, measured the same way as the step kernels
     floor_us = []
     for _ in range(20):
@@ -329,6 +332,7 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         barrier(world)
         e = [ev() for _ in range(4)]
+        ar = [ev(), ev()]
         # a ~100 µs device-side spin ahead of the step lets the host enqueue all three ABI calls before the
         # GPU reaches e[0], so the events time device execution, not Python/ctypes submission latency
         # (e2e below keeps the host path in its timed region)
@@ -342,8 +346,10 @@ def run_ours(args, rank, world, local):
             import torch.distributed as dist
             side.wait_event(e[2])
             with torch.cuda.stream(side):
+                ar[0].record(side)
                 red.copy_(stats_view)
                 dist.all_reduce(red, op=dist.ReduceOp.MIN)
+                ar[1].record(side)
         pool.quant_write_decode(dec, nk.view(torch.int16), nv.view(torch.int16), cand)
         e[3].record()
         torch.cuda.synchronize()
@@ -360,6 +366,9 @@ def run_ours(args, rank, world, local):
             qw_us.append(e[2].elapsed_time(e[3]) * 1e3)
             step_us.append(e[0].elapsed_time(e[3]) * 1e3)
             launches += 3 + (1 if churn else 0)             # classify, compact_alloc, quant_decode (+ recycle)
+            if side is not None:                            # count all-reduce latency; hidden if it ended in the step
+                ar_us.append(ar[0].elapsed_time(ar[1]) * 1e3)
+                ar_hidden.append(e[0].elapsed_time(ar[1]) <= e[0].elapsed_time(e[3]))
             tc = dec.view(torch.uint8).view(-1, 16)[:, 0].cpu().numpy()
             sec = np.where(tc == 1, nh0.cpu().numpy(), np.where(tc == 2, nl0.cpu().numpy(), 0)).astype(np.int64)
             C = np.where(tc == 1, geom[1]["C"], geom[2]["C"])
@@ -510,7 +519,7 @@ def run_ours(args, rank, world, local):
         "warmup": args.warmup,
         "ms_per_step": round(step_mean / 1e3, 6),
         "higher_is_better": False,
-        "scaling": "weak",
+        "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None,
         "dtype": "fp16 in / u8 codes (fp32 quantizer arithmetic, int32 scans)",
         "data": "synthetic (seeded counter-based significance / K / V, synth/)",
@@ -544,6 +553,11 @@ def run_ours(args, rank, world, local):
                                                      "quant_write + D2H decisions)",
                 "h2d_bytes_per_step": wl.U * (4 + 2 * 2 * c["d"]), "d2h_bytes_per_step": wl.U * 16},
         "next2": next2,
+        # §8e: the per-step MIN all-reduce of the admission counters (N > 1): its latency on the side stream and
+        # the fraction of steps in which it finished inside the step (hidden behind quant_write)
+        "allreduce": ({"us": round(max_over_ranks(statistics.mean(ar_us), world), 2),
+                       "hidden_frac": round(sum(ar_hidden) / len(ar_hidden), 3), "bytes": 32}
+                      if ar_us else None),
         "gpu_launches": launches,
         "clocks": clocks,
         "wall_s": round(wall, 1),
@@ -652,6 +666,8 @@ def main():
     ap.add_argument("--tile-units", type=int, default=0, help="compact_alloc scan tile (0 = library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--next2", type=int, default=1, help="also time NEXT-2 decode steps (dkv_attend)")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: fixed global batch (configs[1]'s 64 requests), heads sharded N-way")
     args = ap.parse_args()
     assert args.warmup >= 1
     if args.impl == "reference":
