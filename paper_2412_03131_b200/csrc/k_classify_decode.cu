@@ -17,6 +17,12 @@ constexpr int kCDWarps = 4;                // units (warps) per CTA
 constexpr int kCV = 8;                     // 16-B score vectors per lane per batch (1024 slots per batch)
 constexpr int kXV = 4;                     // the same for the exact (tie-breaking) pass, which also holds positions
 
+#ifdef DKV_CD_64B   // A/B knob: limit the L2 fetch of a score load to the 64-B segment it touches
+#define CD_LD ld_nc_v4_64
+#else
+#define CD_LD ld_nc_v4
+#endif
+
 __global__ void __launch_bounds__(kCDWarps * 32)
 classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decision_t* __restrict__ dec) {
   extern __shared__ int32_t s_pid_all[];                         // [kCDWarps][L] page IDs of the scanned sections
@@ -96,7 +102,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
       for (int j = 0; j < kCV; j++) {
         const int s0 = base + j * 128 + 4 * lane;
         v[j] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        if (s0 < n) v[j] = ld_nc_v4(vec_addr(s0));
+        if (s0 < n) v[j] = CD_LD(vec_addr(s0));
       }
 #pragma unroll
       for (int j = 0; j < kCV; j++) {
@@ -139,7 +145,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
         for (int j = 0; j < kXV; j++) {
           const int s0 = base + j * 128 + 4 * lane;
           v[j] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-          if (s0 < n) v[j] = ld_nc_v4(vec_addr(s0));
+          if (s0 < n) v[j] = CD_LD(vec_addr(s0));
         }
 #pragma unroll
         for (int j = 0; j < kXV; j++) {

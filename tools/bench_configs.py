@@ -241,6 +241,10 @@ def warm_up(seconds=3.0):
 if __name__ == "__main__":
     names = sys.argv[1:] or list(SHAPES)
     warm_up()
+    # throwaway pass of the first config: the first pool of the process measured 20-70 % slow (first touch of
+    # its pages, module load), profiles/r1f_configs.jsonl
+    run(names[0])
+    torch.cuda.empty_cache()
     for n in names:
         print(json.dumps(run(n)), flush=True)
         torch.cuda.empty_cache()
