@@ -13,8 +13,17 @@
 
 namespace dkv {
 
-constexpr int kCDWarps = 4;                // units (warps) per CTA
-constexpr int kCV = 8;                     // 16-B score vectors per lane per batch (1024 slots per batch)
+#ifndef DKV_CD_WARPS
+#define DKV_CD_WARPS 4
+#endif
+#ifndef DKV_CD_MINB
+#define DKV_CD_MINB 1
+#endif
+#ifndef DKV_CD_KCV
+#define DKV_CD_KCV 8
+#endif
+constexpr int kCDWarps = DKV_CD_WARPS;     // units (warps) per CTA
+constexpr int kCV = DKV_CD_KCV;            // 16-B score vectors per lane per batch (1024 slots per batch)
 constexpr int kXV = 4;                     // the same for the exact (tie-breaking) pass, which also holds positions
 
 #ifdef DKV_CD_64B   // A/B knob: limit the L2 fetch of a score load to the 64-B segment it touches
@@ -23,7 +32,7 @@ constexpr int kXV = 4;                     // the same for the exact (tie-breaki
 #define CD_LD ld_nc_v4
 #endif
 
-__global__ void __launch_bounds__(kCDWarps * 32)
+__global__ void __launch_bounds__(kCDWarps * 32, DKV_CD_MINB)
 classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decision_t* __restrict__ dec) {
   extern __shared__ int32_t s_pid_all[];                         // [kCDWarps][L] page IDs of the scanned sections
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
