@@ -16,8 +16,11 @@ namespace dkv {
 #ifndef DKV_CD_WARPS
 #define DKV_CD_WARPS 4
 #endif
+#ifndef DKV_CD_SPEC
+#define DKV_CD_SPEC 1      // u-addressed loads (status, section minima, first table entries) in one round trip
+#endif
 #ifndef DKV_CD_MINB
-#define DKV_CD_MINB 1
+#define DKV_CD_MINB 10     // 10 CTAs (40 warps) per SM: 48 registers, a few spilled
 #endif
 #ifndef DKV_CD_KCV
 #define DKV_CD_KCV 8
@@ -26,7 +29,14 @@ constexpr int kCDWarps = DKV_CD_WARPS;     // units (warps) per CTA
 constexpr int kCV = DKV_CD_KCV;            // 16-B score vectors per lane per batch (1024 slots per batch)
 constexpr int kXV = 4;                     // the same for the exact (tie-breaking) pass, which also holds positions
 
-#ifdef DKV_CD_64B   // A/B knob: limit the L2 fetch of a score load to the 64-B segment it touches
+// Build knobs, measured by tools/classify_ab.sh at the Llama-3-8B config (classify scan µs, two runs each):
+// baseline 44.5; DKV_CD_64B 43.6; DKV_CD_SPEC 42.8; SPEC + 64B 42.4; SPEC + MINB 10 40.8; kCV 16 59.8;
+// kCV 4 45.2; 8 warps per CTA 49.6 — the scan is latency-bound, so fewer dependent round trips and more
+// resident warps win, and more loads in flight per warp (at the cost of occupancy) lose.
+#ifndef DKV_CD_64B
+#define DKV_CD_64B 1
+#endif
+#if DKV_CD_64B      // limit the L2 fetch of a score load to the 64-B segment it touches
 #define CD_LD ld_nc_v4_64
 #else
 #define CD_LD ld_nc_v4
@@ -39,7 +49,20 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   const int u = blockIdx.x * kCDWarps + warp;
   if (u >= p.U) return;                                          // whole warps exit together
   int32_t* s_pid = s_pid_all + warp * p.L;
+#if DKV_CD_SPEC
+  // One round trip for everything u alone addresses: the sticky status (read through L1 — 16k warps reading
+  // the word at one L2 slice queue there; a status set during this call is seen or not, as before), the
+  // section minima of dkv_attend, and the first table entries at both ends of the row (64 high pages, 32 low
+  // pages: the first scan batch's page IDs whichever class t_c takes)
+  const int32_t* row = p.table + (size_t)u * p.L;
+  const int32_t sm_w = lane < 8 ? __ldg(p.secmin + 8 * (size_t)u + lane) : 0;
+  const int32_t sp_h0 = lane < p.L ? __ldg(row + lane) : 0;
+  const int32_t sp_h1 = lane + 32 < p.L ? __ldg(row + lane + 32) : 0;
+  const int32_t sp_l0 = lane < p.L ? __ldg(row + p.L - 1 - lane) : 0;
+  if (__ldg(&p.ctrl->status) != 0) return;                       // sticky error: no-op
+#else
   if (ld_volatile(&p.ctrl->status) != 0) return;                 // sticky error: no-op
+#endif
   if (u < (p.U + 31) / 32 && lane == 0) {
     // warm L2 with the ring window the following dkv_compact_alloc grants from: [start, start + U) holds
     // every page a decode step can demand (one per unit); one 128-B line per warp
@@ -82,19 +105,38 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   uint32_t vb = 0xFFFFFFFFu;
   // NEXT-2: dkv_attend recorded each section's (significance, position) minimum after its update and no
   // section changed since (quant_write clears the flag): the victim needs no scan
+#if DKV_CD_SPEC
+  const bool fused = scan && n > 0 && __shfl_sync(kFull, sm_w, 6) == 1;
+  if (fused) {
+    const int b = cls == DKV_CLS_HIGH ? 0 : 3;
+    vb = (uint32_t)__shfl_sync(kFull, sm_w, b);
+    vs = __shfl_sync(kFull, sm_w, b + 2);
+  } else if
+#else
   const bool fused = scan && n > 0 && p.secmin[8 * (size_t)u + 6] == 1;
   if (fused) {
     const int b = cls == DKV_CLS_HIGH ? 0 : 3;
     vb = (uint32_t)p.secmin[8 * (size_t)u + b];
     vs = p.secmin[8 * (size_t)u + b + 2];
-  } else if (scan && n > 0) {                                    // warp-uniform
+  } else if
+#endif
+  (scan && n > 0) {                                    // warp-uniform
     const int C = cls == DKV_CLS_HIGH ? p.g[1].C : p.g[2].C;
     const int off_score = cls == DKV_CLS_HIGH ? p.g[1].off_score : p.g[2].off_score;
     const bool pow2 = (C & (C - 1)) == 0;
     const int csh = __popc(C - 1);
     const int npages = (n + C - 1) / C;
+#if DKV_CD_SPEC
+    for (int k = lane; k < npages; k += 32) {
+      int32_t pid;
+      if (cls == DKV_CLS_HIGH) pid = k < 32 ? sp_h0 : (k < 64 ? sp_h1 : __ldg(row + k));
+      else pid = k < 32 ? sp_l0 : __ldg(row + p.L - 1 - k);
+      s_pid[k] = pid;
+    }
+#else
     const int32_t* row = p.table + (size_t)u * p.L;
     for (int k = lane; k < npages; k += 32) s_pid[k] = __ldg(row + (cls == DKV_CLS_HIGH ? k : p.L - 1 - k));
+#endif
     __syncwarp();
     const uint8_t* base_sc = p.pages + off_score;
     auto vec_addr = [&](int s0) {
