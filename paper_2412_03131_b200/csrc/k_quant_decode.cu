@@ -32,6 +32,9 @@
 namespace dkv {
 
 constexpr int kQDThreads = 256;
+#ifndef DKV_QD_MINB
+#define DKV_QD_MINB 4      // CTAs per SM the register budget is sized for (the persistent grid follows it)
+#endif
 
 // EPL codes (low byte of ub[i] = code of element i) -> EPL*bits packed bits, element 0 in the LSBs (Q17)
 template <int EPL>
@@ -264,7 +267,7 @@ __device__ __forceinline__ void dequant_lane(const uint4 c, int bits, uint32_t m
 }
 
 template <int D, int G>
-__global__ void __launch_bounds__(kQDThreads, 4)
+__global__ void __launch_bounds__(kQDThreads, DKV_QD_MINB)
 quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uint16_t* __restrict__ knew,
                     const uint16_t* __restrict__ vnew, const float* __restrict__ cand_sig) {
   constexpr int EPL = D / G;                             // elements per lane per vector
