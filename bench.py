@@ -14,8 +14,8 @@ Phases (each bracketed by barrier + synchronize, every kernel timed with CUDA ev
            steps (untimed) the significance drift (attention stand-in), next-step inputs and a 256 MiB L2
            flush; every 10th step frees one request first (its compact_alloc recycles ~37k pages) and
            re-admits it after.  value = mean µs of dkv_compact_alloc per decode step (max over ranks).
-  e2e    : K decode steps through the same C-ABI with pinned HOST inputs (cand_sig, new K/V) copied in and
-           the decisions copied out inside the timed region.
+  e2e    : K decode steps, each ONE C-ABI call with pinned HOST buffers (dkv_decode_step_host: cand_sig and new K/V copied in,
+           the decisions copied out, all inside the timed region).
 At N > 1 each step also all-reduces the pool's int64[4] admission counters (MIN) over NCCL on a side
 stream (one-step lag), the only collective of the path.
 """
@@ -381,39 +381,25 @@ def run_ours(args, rank, world, local):
     # ---------------- e2e: same decode step through the C ABI with host buffers
     e2e_us = []
     pin_c = torch.empty((args.steps, wl.U), dtype=torch.float32).pin_memory()
-    pin_k = torch.empty((args.steps, wl.U, c["d"]), dtype=torch.int16).pin_memory()
-    pin_v = torch.empty_like(pin_k).pin_memory()
+    # K and V of a step side by side in one pinned buffer: one 8.4 MB H2D copy per step instead of two
+    pin_kv = torch.empty((args.steps, 2, wl.U, c["d"]), dtype=torch.int16).pin_memory()
+    pin_k, pin_v = pin_kv[:, 0], pin_kv[:, 1]
     pin_dec = torch.empty((wl.U, 4), dtype=torch.int32).pin_memory()
     for i in range(args.steps):
         cand, nk, nv = wl.decode_inputs(seq + i, active)
         pin_c[i].copy_(cand)
         pin_k[i].copy_(nk.view(torch.int16))
         pin_v[i].copy_(nv.view(torch.int16))
-    d_c = torch.empty(wl.U, dtype=torch.float32, device=dev)
-    d_k = torch.empty((wl.U, c["d"]), dtype=torch.int16, device=dev)
-    d_v = torch.empty_like(d_k)
-    # the new tokens' K/V (8.4 MB at this config, the bulk of the H2D bytes) travel on a copy stream while
-    # classify + compact_alloc run on the pool's stream; quant_write, the first call that reads them, waits
-    copy_stream = torch.cuda.Stream(device=dev)
+    # one C-ABI call per step with HOST buffers (dkv_decode_step_host): the library copies the significance
+    # and the new tokens' K/V (8.4 MB at this config; on its own copy stream, overlapping classify +
+    # compact_alloc; quant_write waits for it), runs the three kernels' calls and copies the decisions back
     for i in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         barrier(world)
-        e0, e1, ekv = ev(), ev(), ev()
+        e0, e1 = ev(), ev()
         e0.record()
-        d_c.copy_(pin_c[i], non_blocking=True)
-        ec = ev()
-        ec.record()
-        copy_stream.wait_event(ec)                        # the 64 KB significance copy goes first
-        with torch.cuda.stream(copy_stream):
-            d_k.copy_(pin_k[i], non_blocking=True)
-            d_v.copy_(pin_v[i], non_blocking=True)
-            ekv.record(copy_stream)
-        pool.classify_decode(d_c, dec)
-        pool.compact_alloc(dec)
-        torch.cuda.current_stream().wait_event(ekv)
-        pool.quant_write_decode(dec, d_k, d_v, d_c)
-        pin_dec.copy_(dec, non_blocking=True)
+        pool.decode_step_host(pin_c[i], pin_kv[i], pin_dec)
         e1.record()
         torch.cuda.synchronize()
         e2e_us.append(e0.elapsed_time(e1) * 1e3)
@@ -549,7 +535,7 @@ def run_ours(args, rank, world, local):
                             "peak": peak, "unit": "GB/s", "frac": round(cls_gbs / peak, 4),
                             "algorithmic_bytes": int(statistics.mean(cls_bytes)),
                             "traffic": traffic("classify_decode_kernel"), "traffic_unit": "bytes per launch"},
-        "e2e": {"value": round(e2e_mean, 3), "unit": "us per decode step (H2D inputs + classify + compact_alloc + "
+        "e2e": {"value": round(e2e_mean, 3), "unit": "us per decode step, one dkv_decode_step_host call (H2D inputs + classify + compact_alloc + "
                                                      "quant_write + D2H decisions)",
                 "h2d_bytes_per_step": wl.U * (4 + 2 * 2 * c["d"]), "d2h_bytes_per_step": wl.U * 16},
         "next2": next2,

@@ -207,6 +207,21 @@ dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* 
  * values are copied on `s` (the host arrays may be reused once the call returns). */
 dkv_status_t dkv_set_head_thresholds(dkv_pool_t p, const float* h_alpha_h, const float* h_alpha_l, dkv_stream_t s);
 
+/* The whole decode step from HOST buffers — the e2e path (P:457-459 planning, P:485-488 coordination,
+ * P:557 compressor; the three calls above in order).  h_sig: host fp32 [U] cand_sig as for
+ * dkv_classify(DECODE), or NULL (NEXT-2: significance from the window); h_kv: host fp16 bits [2][U][d],
+ * the new tokens' keys then values; h_dec: host dkv_decision_t[U] receiving the decisions, or NULL.
+ * Host buffers should be pinned (page-locked) for the copies to be asynchronous.  d_stage: caller-owned
+ * device staging of at least dkv_decode_stage_bytes(p) bytes (decisions, significance, K/V; it must
+ * outlive the step's work on s).  The K/V copy runs on a library-owned copy stream (created on first use,
+ * destroyed with the handle), ordered after the work already on s and overlapping classify +
+ * compact_alloc; quant_write waits for it.  Asynchronous like the other calls: h_dec is valid once s has
+ * completed.  Errors: DKV_ERR_INVALID_ARG (NULL handle / h_kv / d_stage, staging too small), otherwise
+ * those of dkv_classify / dkv_compact_alloc / dkv_quant_write (the step stops at the first failing one). */
+size_t dkv_decode_stage_bytes(dkv_pool_t p);
+dkv_status_t dkv_decode_step_host(dkv_pool_t p, const float* h_sig, const uint16_t* h_kv, dkv_decision_t* h_dec,
+                                  void* d_stage, size_t stage_bytes, dkv_stream_t s);
+
 /* Release: host array h_req[0..n) of ACTIVE requests -> PENDING_FREE (double free / not active ->
  * DKV_ERR_STATE).  Allowed between sequences only (after dkv_quant_write, before dkv_classify).  Pages are
  * recycled by the next dkv_compact_alloc; the slot is IDLE (re-admissible) after that call. */

@@ -141,6 +141,8 @@ struct dkv_pool {
   int8_t* h_req;
   int32_t* h_seq;
   bool recovering;                   // last query reported an error: frees allowed out of sequence
+  cudaStream_t copy_stream;          // dkv_decode_step_host: the new tokens' K/V H2D copy (created on first use)
+  cudaEvent_t ev_ready, ev_kv;       // ... ordered after prior work on the caller's stream / copy done
 };
 
 extern "C" {
@@ -278,6 +280,9 @@ dkv_status_t dkv_pool_destroy(dkv_pool_t p) {
   if (p->h_ctrl) cudaFreeHost(p->h_ctrl);
   if (p->h_req) cudaFreeHost(p->h_req);
   if (p->h_seq) cudaFreeHost(p->h_seq);
+  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  if (p->ev_ready) cudaEventDestroy(p->ev_ready);
+  if (p->ev_kv) cudaEventDestroy(p->ev_kv);
   delete p;
   return DKV_OK;
 }
@@ -472,5 +477,51 @@ dkv_status_t dkv_pool_query(dkv_pool_t p, dkv_stats_t* out, dkv_stream_t s) {
 }
 
 int64_t* dkv_pool_stats_device_ptr(dkv_pool_t p) { return p ? p->dev.stats : nullptr; }
+
+// ---- the whole decode step from host buffers (the e2e path; include/dkv.h)
+static size_t stage_align(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t dkv_decode_stage_bytes(dkv_pool_t p) {
+  if (!p) return 0;
+  const size_t U = (size_t)p->G.U;
+  return stage_align(U * sizeof(dkv_decision_t)) + stage_align(U * 4) + 2 * U * (size_t)p->cfg.head_dim * 2;
+}
+
+dkv_status_t dkv_decode_step_host(dkv_pool_t p, const float* h_sig, const uint16_t* h_kv, dkv_decision_t* h_dec,
+                                  void* d_stage, size_t stage_bytes, dkv_stream_t st) {
+  if (!p || !h_kv || !d_stage || stage_bytes < dkv_decode_stage_bytes(p)) return DKV_ERR_INVALID_ARG;
+  if (p->seq != SEQ_IDLE && !(p->recovering && p->phase == DKV_PHASE_DECODE)) return DKV_ERR_STATE;
+  cudaStream_t s = (cudaStream_t)st;
+  if (!p->copy_stream) {
+    if (cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_kv, cudaEventDisableTiming) != cudaSuccess)
+      return DKV_ERR_CUDA;
+  }
+  const size_t U = (size_t)p->G.U, d = (size_t)p->cfg.head_dim;
+  uint8_t* b = (uint8_t*)d_stage;
+  dkv_decision_t* d_dec = (dkv_decision_t*)b;
+  float* d_sig = h_sig ? (float*)(b + stage_align(U * sizeof(dkv_decision_t))) : nullptr;
+  uint16_t* d_k = (uint16_t*)(b + stage_align(U * sizeof(dkv_decision_t)) + stage_align(U * 4));
+  uint16_t* d_v = d_k + U * d;
+  // the significance (U floats) first on s; the K/V copy (2·U·d halves) on the copy stream, ordered after
+  // everything already on s (the previous step's quant_write still reads the staging), overlapping
+  // classify + compact_alloc, which do not read it
+  if (h_sig && cudaMemcpyAsync(d_sig, h_sig, U * 4, cudaMemcpyHostToDevice, s) != cudaSuccess) return DKV_ERR_CUDA;
+  if (cudaEventRecord(p->ev_ready, s) != cudaSuccess || cudaStreamWaitEvent(p->copy_stream, p->ev_ready, 0) != cudaSuccess ||
+      cudaMemcpyAsync(d_k, h_kv, 2 * U * d * 2, cudaMemcpyHostToDevice, p->copy_stream) != cudaSuccess ||
+      cudaEventRecord(p->ev_kv, p->copy_stream) != cudaSuccess)
+    return DKV_ERR_CUDA;
+  dkv_status_t r = dkv_classify(p, DKV_PHASE_DECODE, nullptr, nullptr, 0, d_sig, 0, d_dec, nullptr, st);
+  if (r == DKV_OK) r = dkv_compact_alloc(p, d_dec, st);
+  // s takes over the copy in every case, so the next call's staging writes stay ordered
+  if (cudaStreamWaitEvent(s, p->ev_kv, 0) != cudaSuccess) return DKV_ERR_CUDA;
+  if (r != DKV_OK) return r;
+  r = dkv_quant_write(p, DKV_PHASE_DECODE, d_dec, d_k, d_v, 0, d_sig, 0, st);
+  if (r != DKV_OK) return r;
+  if (h_dec && cudaMemcpyAsync(h_dec, d_dec, U * sizeof(dkv_decision_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return DKV_ERR_CUDA;
+  return DKV_OK;
+}
 
 }  // extern "C"

@@ -26,7 +26,8 @@ DKV_REQ_IDLE, DKV_REQ_ADMITTING, DKV_REQ_ACTIVE, DKV_REQ_PENDING_FREE = 0, 1, 2,
 
 EXPORTED = ("dkv_arena_bytes", "dkv_pool_layout", "dkv_pool_init", "dkv_pool_destroy", "dkv_classify",
             "dkv_compact_alloc", "dkv_quant_write", "dkv_free", "dkv_pool_query", "dkv_pool_stats_device_ptr",
-            "dkv_status_string", "dkv_attend", "dkv_set_head_thresholds")
+            "dkv_status_string", "dkv_attend", "dkv_set_head_thresholds", "dkv_decode_stage_bytes",
+            "dkv_decode_step_host")
 
 
 class DkvError(RuntimeError):
@@ -90,12 +91,16 @@ _lib.dkv_free.argtypes = [_vp, _vp, C.c_int32, _vp]
 _lib.dkv_attend.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _lib.dkv_set_head_thresholds.argtypes = [_vp, _vp, _vp, _vp]
 _lib.dkv_pool_query.argtypes = [_vp, _P(dkv_stats_t), _vp]
+_lib.dkv_decode_stage_bytes.argtypes = [_vp]
+_lib.dkv_decode_stage_bytes.restype = C.c_size_t
+_lib.dkv_decode_step_host.argtypes = [_vp, _vp, _vp, _vp, _vp, C.c_size_t, _vp]
 _lib.dkv_pool_stats_device_ptr.argtypes = [_vp]
 _lib.dkv_pool_stats_device_ptr.restype = _vp
 _lib.dkv_status_string.argtypes = [C.c_int32]
 _lib.dkv_status_string.restype = C.c_char_p
 for _f in ("dkv_pool_layout", "dkv_pool_init", "dkv_pool_destroy", "dkv_classify", "dkv_compact_alloc",
-           "dkv_quant_write", "dkv_free", "dkv_pool_query", "dkv_attend", "dkv_set_head_thresholds"):
+           "dkv_quant_write", "dkv_free", "dkv_pool_query", "dkv_attend", "dkv_set_head_thresholds",
+           "dkv_decode_step_host"):
     getattr(_lib, _f).restype = C.c_int32
 
 
@@ -193,6 +198,28 @@ def dkv_set_head_thresholds(pool, alpha_h, alpha_l, stream=None) -> int:
     al = np.ascontiguousarray(np.asarray(alpha_l, dtype=np.float32))
     return _check("dkv_set_head_thresholds", _lib.dkv_set_head_thresholds(
         pool, ah.ctypes.data_as(_vp), al.ctypes.data_as(_vp), _stream(stream)))
+
+
+def dkv_decode_stage_bytes(pool) -> int:
+    return int(_lib.dkv_decode_stage_bytes(pool))
+
+
+def _hostp(x):
+    """Host address of a CPU torch tensor / numpy array / None (pinned CPU tensors give asynchronous copies)."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        if x.is_cuda or not x.is_contiguous():
+            raise ValueError("expected a contiguous host (CPU) tensor")
+        return x.data_ptr()
+    if not x.flags["C_CONTIGUOUS"]:
+        raise ValueError("expected a C-contiguous host array")
+    return x.ctypes.data
+
+
+def dkv_decode_step_host(pool, h_sig, h_kv, h_dec, d_stage, stage_bytes, stream=None) -> int:
+    return _check("dkv_decode_step_host", _lib.dkv_decode_step_host(pool, _hostp(h_sig), _hostp(h_kv), _hostp(h_dec),
+                                                                    _dev(d_stage), stage_bytes, _stream(stream)))
 
 
 def dkv_free(pool, h_req, n, stream=None) -> int:

@@ -51,6 +51,15 @@ class Pool:
     def quant_write_decode(self, dec, k, v, sig, stream=None):
         return _d.dkv_quant_write(self.handle, _d.DKV_PHASE_DECODE, dec, k, v, 0, sig, 0, stream or self.stream)
 
+    def decode_step_host(self, h_sig, h_kv, h_dec=None, stream=None):
+        """The whole decode step from host buffers (dkv_decode_step_host): h_sig fp32 [U] or None, h_kv int16
+        [2][U][d] (keys then values), h_dec int32 [U][4] or None — CPU tensors, pinned for async copies."""
+        if getattr(self, "_stage", None) is None:
+            self._stage_bytes = _d.dkv_decode_stage_bytes(self.handle)
+            self._stage = torch.empty(self._stage_bytes, dtype=torch.uint8, device=self.device)
+        return _d.dkv_decode_step_host(self.handle, h_sig, h_kv, h_dec, self._stage, self._stage_bytes,
+                                       stream or self.stream)
+
     def quant_write_prefill(self, k, v, sig, stream=None):
         return _d.dkv_quant_write(self.handle, _d.DKV_PHASE_PREFILL, None, k, v, k.shape[-2], sig, sig.shape[-1],
                                   stream or self.stream)
