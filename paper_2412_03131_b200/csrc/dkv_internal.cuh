@@ -942,7 +942,7 @@ cudaError_t launch_init(const PoolDev& p, cudaStream_t s);
 cudaError_t launch_set_requests(const PoolDev& p, const int32_t* req, const int32_t* len, int n, int mode,
                                 cudaStream_t s);
 cudaError_t launch_clear_status(const PoolDev& p, cudaStream_t s);
-cudaError_t launch_classify_decode(const PoolDev& p, const float* sig, dkv_decision_t* dec, cudaStream_t s);
+cudaError_t launch_classify_decode(const PoolDev& p, const float* sig, dkv_decision_t* dec, int max_len, cudaStream_t s);
 cudaError_t launch_classify_prefill(const PoolDev& p, int n, const float* sig, int64_t sig_stride, uint8_t* cls,
                                     int max_len, cudaStream_t s);
 cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s,

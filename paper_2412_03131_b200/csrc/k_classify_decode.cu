@@ -9,6 +9,8 @@
 // order) with a tiny update path; whenever the minimum score may be shared by several slots, an exact pass
 // re-reads the section (batched, with the positions of the vectors holding the minimum) and breaks the tie on
 // positions (oldest wins).
+#include <stdlib.h>
+
 #include "dkv_internal.cuh"
 
 namespace dkv {
@@ -42,7 +44,8 @@ constexpr int kXV = 4;                     // the same for the exact (tie-breaki
 #define CD_LD ld_nc_v4
 #endif
 
-__global__ void __launch_bounds__(kCDWarps * 32, DKV_CD_MINB)
+template <int MINB>
+__global__ void __launch_bounds__(kCDWarps * 32, MINB)
 classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decision_t* __restrict__ dec) {
   extern __shared__ int32_t s_pid_all[];                         // [kCDWarps][L] page IDs of the scanned sections
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -247,14 +250,24 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   reinterpret_cast<int4*>(dec)[u] = w;
 }
 
-cudaError_t launch_classify_decode(const PoolDev& p, const float* sig, dkv_decision_t* dec, cudaStream_t s) {
+template <int MINB>
+static cudaError_t launch_cd(const PoolDev& p, const float* sig, dkv_decision_t* dec, cudaStream_t s) {
   const size_t smem = 4 * (size_t)p.L * kCDWarps;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(classify_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(classify_decode_kernel<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  classify_decode_kernel<<<(p.U + kCDWarps - 1) / kCDWarps, kCDWarps * 32, smem, s>>>(p, sig, dec);
+  classify_decode_kernel<MINB><<<(p.U + kCDWarps - 1) / kCDWarps, kCDWarps * 32, smem, s>>>(p, sig, dec);
   return cudaGetLastError();
+}
+
+// max_len: the longest ACTIVE request (host mirror).  Long sections run the instantiation with the full
+// register budget: their scans take many batches and, when the minimum is shared, the exact pass, which
+// spills at the 10-CTA budget (measured: profiles/r1j_classify_long_ab.log)
+cudaError_t launch_classify_decode(const PoolDev& p, const float* sig, dkv_decision_t* dec, int max_len, cudaStream_t s) {
+  static const int long_len = getenv("DKV_CD_LONG") ? atoi(getenv("DKV_CD_LONG")) : (1 << 30);   // tuning knob
+  if (max_len > long_len) return launch_cd<1>(p, sig, dec, s);
+  return launch_cd<DKV_CD_MINB>(p, sig, dec, s);
 }
 
 }  // namespace dkv

@@ -296,9 +296,13 @@ dkv_status_t dkv_classify(dkv_pool_t p, int32_t phase, const int32_t* h_req, con
   const int R = p->cfg.max_requests;
   if (phase == DKV_PHASE_DECODE) {
     if (!d_dec) return DKV_ERR_INVALID_ARG;              // d_sig NULL: t_c's significance from the window
-    for (int r = 0; r < R; r++)
-      if (p->req_state[r] == DKV_REQ_ACTIVE && p->seq_len[r] >= p->cfg.max_seq_len) return DKV_ERR_STATE;
-    cudaError_t e = launch_classify_decode(p->dev, d_sig, d_dec, (cudaStream_t)s);
+    int max_len = 0;
+    for (int r = 0; r < R; r++) {
+      if (p->req_state[r] != DKV_REQ_ACTIVE) continue;
+      if (p->seq_len[r] >= p->cfg.max_seq_len) return DKV_ERR_STATE;
+      max_len = p->seq_len[r] > max_len ? p->seq_len[r] : max_len;
+    }
+    cudaError_t e = launch_classify_decode(p->dev, d_sig, d_dec, max_len, (cudaStream_t)s);
     if (e != cudaSuccess) return DKV_ERR_CUDA;
   } else if (phase == DKV_PHASE_PREFILL) {
     if (n < 0 || n > R || (n > 0 && (!h_req || !h_len || !d_sig))) return DKV_ERR_INVALID_ARG;

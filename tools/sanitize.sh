@@ -15,3 +15,9 @@ for tool in memcheck racecheck synccheck; do
     python -m pytest tests/test_gpu_attention.py -x -q -k "tiny or multi_page_d128" > gpurun_out/sanitize_attend_$tool.log 2>&1
   echo "attend $tool rc=$? $(grep -E 'ERROR SUMMARY|passed|failed' gpurun_out/sanitize_attend_$tool.log | tr '\n' ' ')"
 done
+# the host-buffer decode step (library copy stream + events) and both classify instantiations
+for tool in memcheck racecheck synccheck; do
+  DKV_CD_LONG=${DKV_CD_LONG_SAN:-100} timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 \
+    python -m pytest tests/test_gpu_host_step.py -x -q > gpurun_out/sanitize_host_step_$tool.log 2>&1
+  echo "host step $tool rc=$? $(grep -E 'ERROR SUMMARY|passed|failed' gpurun_out/sanitize_host_step_$tool.log | tr '\n' ' ')"
+done
