@@ -265,7 +265,7 @@ static cudaError_t launch_cd(const PoolDev& p, const float* sig, dkv_decision_t*
 // register budget: their scans take many batches and, when the minimum is shared, the exact pass, which
 // spills at the 10-CTA budget (measured: profiles/r1j_classify_long_ab.log)
 cudaError_t launch_classify_decode(const PoolDev& p, const float* sig, dkv_decision_t* dec, int max_len, cudaStream_t s) {
-  static const int long_len = getenv("DKV_CD_LONG") ? atoi(getenv("DKV_CD_LONG")) : (1 << 30);   // tuning knob
+  static const int long_len = getenv("DKV_CD_LONG") ? atoi(getenv("DKV_CD_LONG")) : 12288;   // tuning knob
   if (max_len > long_len) return launch_cd<1>(p, sig, dec, s);
   return launch_cd<DKV_CD_MINB>(p, sig, dec, s);
 }
