@@ -952,8 +952,9 @@ cudaError_t launch_attend(const PoolDev& p, const uint16_t* q, float* out, float
 size_t attend_smem_bytes(const PoolDev& p, int TS);
 size_t attend_long_smem_bytes(const PoolDev& p);
 cudaError_t launch_prefill_conservative(const PoolDev& p, cudaStream_t s);
+// units [u0, u1) (u1 < 0: all U)
 cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
-                                const float* sig, cudaStream_t s);
+                                const float* sig, cudaStream_t s, int u0 = 0, int u1 = -1);
 cudaError_t launch_quant_prefill(const PoolDev& p, int n, const uint16_t* k, const uint16_t* v, int64_t kv_stride,
                                  const float* sig, int64_t sig_stride, int max_len, cudaStream_t s);
 int compact_max_coresident(int tile_units);

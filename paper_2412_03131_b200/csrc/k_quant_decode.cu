@@ -269,7 +269,7 @@ __device__ __forceinline__ void dequant_lane(const uint4 c, int bits, uint32_t m
 template <int D, int G>
 __global__ void __launch_bounds__(kQDThreads, DKV_QD_MINB)
 quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uint16_t* __restrict__ knew,
-                    const uint16_t* __restrict__ vnew, const float* __restrict__ cand_sig) {
+                    const uint16_t* __restrict__ vnew, const float* __restrict__ cand_sig, int u0, int u1) {
   constexpr int EPL = D / G;                             // elements per lane per vector
   constexpr int UPC = kQDThreads / G;                    // units per CTA per iteration
   extern __shared__ __align__(16) uint8_t qd_smem[];
@@ -285,9 +285,9 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
   uint16_t* const my_nk = &s_new[0][threadIdx.x * EPL];
   uint16_t* const my_nv = &s_new[1][threadIdx.x * EPL];
 
-  for (int ub = blockIdx.x; ub * UPC < p.U; ub += gridDim.x) {
-    const int u = ub * UPC + threadIdx.x / G;
-    if (u >= p.U) break;                                 // whole groups leave together (last block only)
+  for (int ub = blockIdx.x; u0 + ub * UPC < u1; ub += gridDim.x) {   // units [u0, u1)
+    const int u = u0 + ub * UPC + threadIdx.x / G;
+    if (u >= u1) break;                                  // whole groups leave together (last block only)
 
     // ---- A: loads indexed by u only (all in flight together); the new token goes straight to smem
     const int r = fdiv(p.div_LyH, u);
@@ -394,28 +394,30 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
 
 template <int D, int G>
 static cudaError_t launch_qd(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
-                             const float* sig, cudaStream_t s) {
+                             const float* sig, int u0, int u1, cudaStream_t s) {
   constexpr int units_per_cta = kQDThreads / G;
   const size_t smem = req_cache_bytes(p.R);
   static int cap = 0;                                    // persistent grid (per template instance)
   if (cap == 0) cap = persistent_grid(quant_decode_kernel<D, G>, kQDThreads, req_cache_bytes(kReqSmemMax));
   if (cap == 0) return cudaErrorUnknown;
-  const int need = (p.U + units_per_cta - 1) / units_per_cta;
-  quant_decode_kernel<D, G><<<need < cap ? need : cap, kQDThreads, smem, s>>>(p, dec, k, v, sig);
+  if (u1 <= u0) return cudaSuccess;
+  const int need = (u1 - u0 + units_per_cta - 1) / units_per_cta;
+  quant_decode_kernel<D, G><<<need < cap ? need : cap, kQDThreads, smem, s>>>(p, dec, k, v, sig, u0, u1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
-                                const float* sig, cudaStream_t s) {
+                                const float* sig, cudaStream_t s, int u0, int u1) {
+  if (u1 < 0) u1 = p.U;
   static const int g = getenv("DKV_QD_G") ? atoi(getenv("DKV_QD_G")) : 8;   // lanes per unit (tuning knob)
   if (p.d == 128) {
-    if (g == 32) return launch_qd<128, 32>(p, dec, k, v, sig, s);
-    if (g == 8) return launch_qd<128, 8>(p, dec, k, v, sig, s);
-    return launch_qd<128, 16>(p, dec, k, v, sig, s);
+    if (g == 32) return launch_qd<128, 32>(p, dec, k, v, sig, u0, u1, s);
+    if (g == 8) return launch_qd<128, 8>(p, dec, k, v, sig, u0, u1, s);
+    return launch_qd<128, 16>(p, dec, k, v, sig, u0, u1, s);
   }
-  if (g == 16) return launch_qd<64, 16>(p, dec, k, v, sig, s);
-  if (g == 4) return launch_qd<64, 4>(p, dec, k, v, sig, s);
-  return launch_qd<64, 8>(p, dec, k, v, sig, s);
+  if (g == 16) return launch_qd<64, 16>(p, dec, k, v, sig, u0, u1, s);
+  if (g == 4) return launch_qd<64, 4>(p, dec, k, v, sig, u0, u1, s);
+  return launch_qd<64, 8>(p, dec, k, v, sig, u0, u1, s);
 }
 
 }  // namespace dkv

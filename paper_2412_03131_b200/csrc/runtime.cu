@@ -142,7 +142,8 @@ struct dkv_pool {
   int32_t* h_seq;
   bool recovering;                   // last query reported an error: frees allowed out of sequence
   cudaStream_t copy_stream;          // dkv_decode_step_host: the new tokens' K/V H2D copy (created on first use)
-  cudaEvent_t ev_ready, ev_kv;       // ... ordered after prior work on the caller's stream / copy done
+  cudaEvent_t ev_ready;              // ... ordered after prior work on the caller's stream
+  cudaEvent_t ev_kv[8];              // ... unit chunk c of the K/V copy done
 };
 
 extern "C" {
@@ -282,7 +283,8 @@ dkv_status_t dkv_pool_destroy(dkv_pool_t p) {
   if (p->h_seq) cudaFreeHost(p->h_seq);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   if (p->ev_ready) cudaEventDestroy(p->ev_ready);
-  if (p->ev_kv) cudaEventDestroy(p->ev_kv);
+  for (cudaEvent_t e : p->ev_kv)
+    if (e) cudaEventDestroy(e);
   delete p;
   return DKV_OK;
 }
@@ -496,11 +498,17 @@ dkv_status_t dkv_decode_step_host(dkv_pool_t p, const float* h_sig, const uint16
   if (!p || !h_kv || !d_stage || stage_bytes < dkv_decode_stage_bytes(p)) return DKV_ERR_INVALID_ARG;
   if (p->seq != SEQ_IDLE && !(p->recovering && p->phase == DKV_PHASE_DECODE)) return DKV_ERR_STATE;
   cudaStream_t s = (cudaStream_t)st;
+  // the K/V copy and quant_write may go in unit chunks (quant_write of chunk c overlapping the copy of chunk
+  // c + 1); measured at the Llama-3-8B config (profiles/r1l_e2e_chunks.log): 1 chunk 219.7 us, 2: 220.9,
+  // 4: 244.4, 8: 278.4 — smaller copies lose more than the overlap gains, so one chunk is the default
+  static const int nch_env = getenv("DKV_E2E_CHUNKS") ? atoi(getenv("DKV_E2E_CHUNKS")) : 1;   // tuning knob (measured: 1 best)
+  const int nch = nch_env < 1 ? 1 : (nch_env > 8 ? 8 : nch_env);
   if (!p->copy_stream) {
     if (cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->ev_kv, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&p->ev_ready, cudaEventDisableTiming) != cudaSuccess)
       return DKV_ERR_CUDA;
+    for (cudaEvent_t& e : p->ev_kv)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return DKV_ERR_CUDA;
   }
   const size_t U = (size_t)p->G.U, d = (size_t)p->cfg.head_dim;
   uint8_t* b = (uint8_t*)d_stage;
@@ -508,21 +516,34 @@ dkv_status_t dkv_decode_step_host(dkv_pool_t p, const float* h_sig, const uint16
   float* d_sig = h_sig ? (float*)(b + stage_align(U * sizeof(dkv_decision_t))) : nullptr;
   uint16_t* d_k = (uint16_t*)(b + stage_align(U * sizeof(dkv_decision_t)) + stage_align(U * 4));
   uint16_t* d_v = d_k + U * d;
+  size_t cut[9];                                         // chunk boundaries, multiples of 32 units
+  for (int c = 0; c <= nch; c++) cut[c] = c == nch ? U : ((U * c / nch) & ~(size_t)31);
   // the significance (U floats) first on s; the K/V copy (2·U·d halves) on the copy stream, ordered after
   // everything already on s (the previous step's quant_write still reads the staging), overlapping
   // classify + compact_alloc, which do not read it
   if (h_sig && cudaMemcpyAsync(d_sig, h_sig, U * 4, cudaMemcpyHostToDevice, s) != cudaSuccess) return DKV_ERR_CUDA;
-  if (cudaEventRecord(p->ev_ready, s) != cudaSuccess || cudaStreamWaitEvent(p->copy_stream, p->ev_ready, 0) != cudaSuccess ||
-      cudaMemcpyAsync(d_k, h_kv, 2 * U * d * 2, cudaMemcpyHostToDevice, p->copy_stream) != cudaSuccess ||
-      cudaEventRecord(p->ev_kv, p->copy_stream) != cudaSuccess)
+  if (cudaEventRecord(p->ev_ready, s) != cudaSuccess || cudaStreamWaitEvent(p->copy_stream, p->ev_ready, 0) != cudaSuccess)
     return DKV_ERR_CUDA;
+  for (int c = 0; c < nch; c++) {
+    const size_t n = (cut[c + 1] - cut[c]) * d * 2;
+    if ((n && (cudaMemcpyAsync(d_k + cut[c] * d, h_kv + cut[c] * d, n, cudaMemcpyHostToDevice, p->copy_stream) != cudaSuccess ||
+               cudaMemcpyAsync(d_v + cut[c] * d, h_kv + (U + cut[c]) * d, n, cudaMemcpyHostToDevice, p->copy_stream) != cudaSuccess)) ||
+        cudaEventRecord(p->ev_kv[c], p->copy_stream) != cudaSuccess)
+      return DKV_ERR_CUDA;
+  }
   dkv_status_t r = dkv_classify(p, DKV_PHASE_DECODE, nullptr, nullptr, 0, d_sig, 0, d_dec, nullptr, st);
   if (r == DKV_OK) r = dkv_compact_alloc(p, d_dec, st);
-  // s takes over the copy in every case, so the next call's staging writes stay ordered
-  if (cudaStreamWaitEvent(s, p->ev_kv, 0) != cudaSuccess) return DKV_ERR_CUDA;
-  if (r != DKV_OK) return r;
-  r = dkv_quant_write(p, DKV_PHASE_DECODE, d_dec, d_k, d_v, 0, d_sig, 0, st);
-  if (r != DKV_OK) return r;
+  if (r != DKV_OK) {                                     // s takes over the whole copy: later staging writes stay ordered
+    return cudaStreamWaitEvent(s, p->ev_kv[nch - 1], 0) == cudaSuccess ? r : DKV_ERR_CUDA;
+  }
+  // dkv_quant_write(DECODE), chunk by chunk as the K/V arrive
+  for (int c = 0; c < nch; c++) {
+    if (cudaStreamWaitEvent(s, p->ev_kv[c], 0) != cudaSuccess) return DKV_ERR_CUDA;
+    if (launch_quant_decode(p->dev, d_dec, d_k, d_v, d_sig, s, (int)cut[c], (int)cut[c + 1]) != cudaSuccess)
+      return DKV_ERR_CUDA;
+  }
+  p->seq = SEQ_IDLE;
+  p->recovering = false;
   if (h_dec && cudaMemcpyAsync(h_dec, d_dec, U * sizeof(dkv_decision_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
     return DKV_ERR_CUDA;
   return DKV_OK;
