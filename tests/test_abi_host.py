@@ -79,6 +79,10 @@ def test_no_device_fails_loudly(D):
     st = D.lib().dkv_pool_init(C.byref(cfg), C.c_void_p(1 << 20), n, None, C.byref(h))
     assert st == D.DKV_ERR_CUDA and not h.value
     assert D.lib().dkv_classify(None, 0, None, None, 0, None, 0, None, None, None) == D.DKV_ERR_INVALID_ARG
+    # the host-buffer decode step validates its arguments before any CUDA call
+    assert D.lib().dkv_decode_stage_bytes(None) == 0
+    buf = (C.c_uint16 * 8)()
+    assert D.lib().dkv_decode_step_host(None, None, buf, None, C.c_void_p(1 << 20), 1 << 20, None) == D.DKV_ERR_INVALID_ARG
 
 
 def test_status_strings(D):
