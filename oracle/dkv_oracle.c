@@ -261,9 +261,6 @@ static int32_t write_token(orc_pool* p, int cls, int32_t u, int32_t s, const flo
   /* Q30: a token with a non-finite K or V element is rejected whole — nothing of it is written */
   for (int32_t i = 0; i < p->c.d; i++)
     if (!isfinite(k[i]) || !isfinite(v[i])) return ORC_ERR_NONFINITE;
-  /* Q30: a token with a non-finite K or V element is rejected whole — nothing of it is written */
-  for (int32_t i = 0; i < p->c.d; i++)
-    if (!isfinite(k[i]) || !isfinite(v[i])) return ORC_ERR_NONFINITE;
   int32_t idx; uint8_t* pg = slot_page(p, cls, u, s, &idx);
   uint16_t ks, kz, vs, vz;
   int32_t st = orc_quantize(k, p->c.d, g->kbits, pg + g->off_k + idx * g->k_row, &ks, &kz);

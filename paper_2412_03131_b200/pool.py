@@ -107,8 +107,9 @@ class Pool:
         )
 
     def geom(self):
-        L = self.layout
-        return {c: dict(C=L.C[c], k_row=L.k_row[c], v_row=L.v_row[c], off_k=L.off_k[c], off_kmeta=L.off_kmeta[c],
+        L, cf = self.layout, self.cfg
+        bits = {1: (cf.kbits_high, cf.vbits_high), 2: (cf.kbits_low, cf.vbits_low)}
+        return {c: dict(C=L.C[c], kbits=bits[c][0], vbits=bits[c][1], k_row=L.k_row[c], v_row=L.v_row[c], off_k=L.off_k[c], off_kmeta=L.off_kmeta[c],
                         off_v=L.off_v[c], off_vmeta=L.off_vmeta[c], off_score=L.off_score[c], off_pos=L.off_pos[c])
                 for c in (1, 2)}
 

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 import torch
 
+from tests import eq1
 from tests import harness as H
 
 pytestmark = pytest.mark.gpu
@@ -28,6 +29,10 @@ def _run(scn, lens, steps, frees=(), readmit=None, seed=0):
         _, og, pg = g.attend(q, want_out=True, want_probs=True)
         assert np.array_equal(po.view(np.uint32), pg.view(np.uint32)), f"[{where}] per-token scores differ"
         assert np.array_equal(oo.view(np.uint32), og.view(np.uint32)), f"[{where}] attention outputs differ"
+        # the GPU result pinned to the paper's formula itself: Eq. 1 in float64 from the GPU pool's page bytes
+        sg = g.snapshot()
+        units = range(scn.U) if scn.U * scn.M <= 200000 else range(0, scn.U, max(1, scn.U // 16))
+        eq1.check_units(sg, g.geom, g.L, scn.W, d, scn.LyH, q, og, pg, units, where=where)
         same(where + " attend")
 
     H.admit([o, g], inp, life, list(range(len(lens))), lens)

@@ -201,6 +201,12 @@ def test_llama8b_fullsize_attention_sampled_parity():
         og = out.cpu().numpy()[rows]
         assert np.array_equal(oo.view(np.uint32), og.view(np.uint32)), f"[{where}] attention outputs differ"
         v = pool.views()
+        # the GPU outputs of 64 sampled units pinned to Eq. 1 evaluated in float64 from the GPU's page bytes
+        from tests import eq1
+        snap = dict(pages=v["pages"], table=v["table"], n_h=v["n_h"], n_l=v["n_l"], seq_len=v["seq_len"],
+                    win_k=v["win_k"], win_v=v["win_v"])
+        out_np = out.cpu().numpy()
+        eq1.check_units(snap, geom, L, c["W"], d, LyH, q, out_np, None, range(0, wl.U, wl.U // 64), where=where)
         n_h, n_l = v["n_h"].cpu().numpy(), v["n_l"].cpu().numpy()
         secmin = v["secmin"].cpu().numpy()
         win_sig = v["win_sig"].cpu().numpy()

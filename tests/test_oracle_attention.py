@@ -161,3 +161,23 @@ def test_lifecycle_with_window_significance():
         assert p.status == 0
         H.check_invariants(o.snapshot(), scn, o.L, o.geom)
     assert {1, 2, 11} <= seen and (12 in seen or 13 in seen), seen   # H, L, keep and a victim leaving
+
+
+def test_eq1_helper_agrees_with_independent_unpacker():
+    """tests/eq1.py (the float64 Eq. 1 the GPU attention is pinned to) against this file's own unpacker and
+    float64 evaluation on an oracle pool: the same tokens, and the oracle's attention within the same bound."""
+    from tests import eq1
+    scn, o, inp, life = _pool_after_prefill(G=4, seed=5)
+    p = o.pool
+    geom = {c: dict(o.geom[c], kbits=p.geom[c].kbits, vbits=p.geom[c].vbits) for c in (1, 2)}
+    snap = o.snapshot()
+    q = np.random.default_rng(8).normal(0, 1, size=(p.U, 4, scn.d)).astype(np.float16)
+    for u in range(p.U):
+        k1, v1, p1 = _tokens64(p, u)
+        k2, v2, p2 = eq1.unit_tokens64(snap["pages"], snap["table"][u], snap["n_h"][u], snap["n_l"][u],
+                                       snap["seq_len"][u // p.LyH], snap["win_k"][u], snap["win_v"][u],
+                                       geom, o.L, scn.W, scn.d)
+        assert np.array_equal(k1, k2) and np.array_equal(v1, v2) and np.array_equal(p1, p2), u
+    st, out, probs = p.attend(q, want_out=True, want_probs=True)
+    assert st == 0
+    eq1.check_units(snap, geom, o.L, scn.W, scn.d, p.LyH, q, out, probs, range(p.U), where="oracle")
