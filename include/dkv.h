@@ -215,9 +215,8 @@ dkv_status_t dkv_set_head_thresholds(dkv_pool_t p, const float* h_alpha_h, const
  * device staging of at least dkv_decode_stage_bytes(p) bytes (decisions, significance, K/V; it must
  * outlive the step's work on s).  The K/V copy runs on a library-owned copy stream (created on first use,
  * destroyed with the handle), ordered after the work already on s and overlapping classify +
- * compact_alloc; quant_write waits for it (env DKV_E2E_CHUNKS > 1 splits the copy and quant_write into
- * unit chunks that overlap; measured slower at the Llama-3-8B config).  Results are identical to the three
- * separate calls.  Asynchronous like the other calls: h_dec is valid once s has
+ * compact_alloc; quant_write waits for it.  Every host-detectable error (call order, an ACTIVE request at
+ * max_seq_len) is reported before anything is queued.  Results are identical to the three separate calls.  Asynchronous like the other calls: h_dec is valid once s has
  * completed.  Errors: DKV_ERR_INVALID_ARG (NULL handle / h_kv / d_stage, staging too small), otherwise
  * those of dkv_classify / dkv_compact_alloc / dkv_quant_write (the step stops at the first failing one). */
 size_t dkv_decode_stage_bytes(dkv_pool_t p);
@@ -234,7 +233,7 @@ dkv_status_t dkv_free(dkv_pool_t p, const int32_t* h_req, int32_t n, dkv_stream_
 dkv_status_t dkv_pool_query(dkv_pool_t p, dkv_stats_t* out, dkv_stream_t s);
 
 /* Device address of the pool's int64[4] admission counters {free_pages, -last_demand, -used_pages,
- * -status}, rewritten by every dkv_compact_alloc — the payload of the per-step count all-reduce (MIN). */
+ * status} (status <= 0, so the MIN shows an error on any GPU), rewritten by every dkv_compact_alloc — the payload of the per-step count all-reduce (MIN). */
 int64_t* dkv_pool_stats_device_ptr(dkv_pool_t p);
 
 const char* dkv_status_string(dkv_status_t st);

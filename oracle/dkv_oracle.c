@@ -316,10 +316,11 @@ int32_t orc_classify_decode(orc_pool* p, const float* cand_sig, orc_decision* de
     if (p->req_state[r] == ORC_REQ_ACTIVE && p->seq_len[r] >= c->M) return ORC_ERR_STATE;
   p->last_phase = ORC_DECODE;
   int32_t LyH = c->Ly * c->H;
+  const int32_t st0 = p->status;                             /* Q36: the status is taken once, at entry */
   for (int32_t u = 0; u < p->U; u++) {
     orc_decision* D = &dec[u];
     empty_decision(D);
-    if (p->status != ORC_OK) continue;                       /* sticky error: no-op */
+    if (st0 != ORC_OK) continue;                             /* sticky error: no-op */
     int32_t r = u / LyH;
     if (p->req_state[r] != ORC_REQ_ACTIVE) continue;
     int32_t N = p->seq_len[r] + 1;
@@ -421,6 +422,7 @@ int32_t orc_classify_prefill(orc_pool* p, const int32_t* req, const int32_t* len
   if (st != ORC_OK) return st;
   p->last_phase = ORC_PREFILL;
   int32_t LyH = c->Ly * c->H;
+  const int32_t st0 = p->status;                             /* Q36: the status is taken once, at entry */
   for (int32_t i = 0; i < n; i++) {
     int32_t r = req[i], T = len[i];
     for (int32_t j = 0; j < LyH; j++) {
@@ -430,7 +432,7 @@ int32_t orc_classify_prefill(orc_pool* p, const int32_t* req, const int32_t* len
       int32_t nh = 0, nl = 0;
       for (int32_t t = 0; t < T; t++) {
         int cls = ORC_CLS_NONE;                               /* window token */
-        if (t < T - c->W && p->status == ORC_OK) {
+        if (t < T - c->W && st0 == ORC_OK) {
           float s = row[t];
           if (!isfinite(s) || s < 0.0f) { set_status(p, ORC_ERR_NONFINITE); s = 0.0f; }
           cls = prompt_class(p, u, s, t, T);
@@ -643,7 +645,17 @@ int32_t orc_quant_write_decode(orc_pool* p, const orc_decision* dec, const uint1
    the newest min(W, n) tokens go to the window at slot pos mod W; then ADMITTING -> ACTIVE. */
 int32_t orc_quant_write_prefill(orc_pool* p, const uint16_t* k, const uint16_t* v, int64_t kv_stride,
                                 const float* sig, int64_t sig_stride) {
-  if (p->status != ORC_OK) return ORC_OK;
+  if (p->status != ORC_OK) {
+    /* Q36/Q37: an error at entry means this admission's planning or allocation did not happen (no pages
+       were granted): the admission is rolled back, ADMITTING -> IDLE */
+    for (int32_t i = 0; i < p->n_admit; i++) {
+      int32_t r = p->admit_list[i];
+      if (p->req_state[r] != ORC_REQ_ADMITTING) continue;
+      p->req_state[r] = ORC_REQ_IDLE; p->seq_len[r] = 0; p->prompt_len[r] = 0;
+    }
+    p->n_admit = 0;
+    return ORC_OK;
+  }
   const orc_config* c = &p->c;
   int32_t LyH = c->Ly * c->H, d = c->d, W = c->W;
   float* kx = (float*)malloc((size_t)d * 4); float* vx = (float*)malloc((size_t)d * 4);
@@ -676,7 +688,8 @@ int32_t orc_quant_write_prefill(orc_pool* p, const uint16_t* k, const uint16_t* 
     }
   }
   free(kx); free(vx);
-  if (p->status != ORC_OK) return ORC_OK;
+  /* Q30/Q37: a token rejected by this call does not stop the others; the request becomes ACTIVE (and can be
+     freed) with the sticky status reporting the error */
   for (int32_t i = 0; i < p->n_admit; i++)
     if (p->req_state[p->admit_list[i]] == ORC_REQ_ADMITTING) p->req_state[p->admit_list[i]] = ORC_REQ_ACTIVE;
   p->n_admit = 0;

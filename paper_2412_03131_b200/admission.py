@@ -3,7 +3,7 @@
 P:555-556: "each worker includes a dedicated memory manager that oversees the KV cache for its assigned
 attention heads" — GPU g owns KV heads [g*H/G, (g+1)*H/G) of every request and layer, in an independent
 pool; no KV byte crosses GPUs.  The only exchange is one all-reduce (MIN) of the pools' int64[4]
-admission counters {free_pages, -last_demand, -used_pages, -status} per step, which the scheduler
+admission counters {free_pages, -last_demand, -used_pages, status} per step, which the scheduler
 (it "batches as many requests as possible within the available GPU memory") uses to admit a
 request only if EVERY GPU has room for its shard.  torch.distributed (NCCL on GPUs, gloo in CPU tests)
 carries it on a side stream; the counters are written by dkv_compact_alloc inside the arena.
@@ -48,7 +48,7 @@ class Admission:
         return int(reduced[0])
 
     def healthy(self, reduced) -> bool:
-        return int(reduced[3]) == 0                     # -status MIN == 0 <=> no GPU has a pending error
+        return int(reduced[3]) == 0                     # status <= 0: MIN == 0 <=> no GPU has a pending error
 
     def admit(self, reduced, prefill_pages: int) -> bool:
         return self.healthy(reduced) and self.free_min(reduced) >= prefill_pages + self.decode_reserve

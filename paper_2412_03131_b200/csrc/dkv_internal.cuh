@@ -25,8 +25,14 @@ struct Ctrl {
   unsigned long long bar_epoch;  // grid barriers crossed (only calls that take the barrier path)
   int64_t rec_end0;              // end pointer at entry of the last compact_alloc (deferred recycle)
   int32_t rec_deferred;          // 1: the last compact_alloc left its recycle copies to recycle_kernel
+  // Status snapshots (reading Q36: every call takes the status once, at entry).  dkv_classify's kernels
+  // never write `status` (their errors go to `pending`), so every classify warp sees the same entry value;
+  // dkv_compact_alloc merges `pending` into `status` and leaves its final status in `qw_status`, the entry
+  // status of the following dkv_quant_write, whose kernels read only that word.
+  int32_t pending;
+  int32_t qw_status;
   int32_t pad32;
-  int64_t pad[3];
+  int64_t pad[2];
 };
 static_assert(sizeof(Ctrl) <= 256, "ctrl block");
 
@@ -144,6 +150,8 @@ __device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
 }
 
 __device__ __forceinline__ void set_status(Ctrl* c, int32_t st) { atomicCAS(&c->status, 0, st); }
+// an error found by a dkv_classify kernel (Q36): merged into `status` by the next dkv_compact_alloc
+__device__ __forceinline__ void set_pending(Ctrl* c, int32_t st) { atomicCAS(&c->pending, 0, st); }
 
 // ------------------------------------------------------------------------------------- async bulk copies
 // 1-D TMA (cp.async.bulk) global -> shared with mbarrier transaction counting (sm_90+ / sm_100a).

@@ -266,7 +266,7 @@ quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const u
   const int seg = (int)(item % nseg_max);
   const long wi = item / nseg_max;                     // admitted unit index (i * LyH + j)
   if (wi >= (long)n * p.LyH) return;
-  if (ld_volatile(&p.ctrl->status) != 0) return;
+  if (ld_volatile(&p.ctrl->qw_status) != 0) return;   // entry status (Q36), left by dkv_compact_alloc
   const int i = (int)(wi / p.LyH), j = (int)(wi % p.LyH);
   const int r = p.admit[i];
   const int u = r * p.LyH + j;
@@ -341,14 +341,22 @@ quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const u
   if (__any_sync(kFull, bad) && lane == 0) set_status(p.ctrl, DKV_ERR_NONFINITE);
 }
 
-// ADMITTING -> ACTIVE once every prompt token is written (skipped while an error is pending)
+// ADMITTING -> ACTIVE once every prompt token is written.  With an error at entry (Q36/Q37: the admission's
+// planning or allocation failed, so it holds no pages) the admission is rolled back: ADMITTING -> IDLE.  A
+// token rejected by this call (Q30) does not stop the others; the request becomes ACTIVE and can be freed.
 __global__ void finish_prefill_kernel(PoolDev p, int n) {
-  if (ld_volatile(&p.ctrl->status) != 0) return;
+  const bool rollback = ld_volatile(&p.ctrl->qw_status) != 0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int r = p.admit[i];
-    if (p.req_state[r] == DKV_REQ_ADMITTING) p.req_state[r] = DKV_REQ_ACTIVE;
+    if (p.req_state[r] != DKV_REQ_ADMITTING) continue;
+    if (rollback) { p.req_state[r] = DKV_REQ_IDLE; p.seq_len[r] = 0; p.prompt_len[r] = 0; }
+    else p.req_state[r] = DKV_REQ_ACTIVE;
   }
 }
+
+#ifndef DKV_BULK_PF
+#define DKV_BULK_PF 3
+#endif
 
 cudaError_t launch_quant_prefill(const PoolDev& p, int n, const uint16_t* k, const uint16_t* v, int64_t kv_stride,
                                  const float* sig, int64_t sig_stride, int max_len, cudaStream_t s) {
@@ -356,7 +364,7 @@ cudaError_t launch_quant_prefill(const PoolDev& p, int n, const uint16_t* k, con
   const long items = (long)n * p.LyH * nseg_max;
   if (items > 0) {
     const long grid = (items + kBulkWarps - 1) / kBulkWarps;
-    static const int pf = getenv("DKV_BULK_PF") ? atoi(getenv("DKV_BULK_PF")) : 3;   // tuning knob
+    constexpr int pf = DKV_BULK_PF;                   // staging form (build-time choice; 3 measured best)
     if (p.d == 128) {
       if (pf == 2 || pf == 3) {
         constexpr size_t sm = bulk_ring_bytes<128>();

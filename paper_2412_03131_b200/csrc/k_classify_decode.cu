@@ -62,10 +62,16 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   const int32_t sp_h0 = lane < p.L ? __ldg(row + lane) : 0;
   const int32_t sp_h1 = lane + 32 < p.L ? __ldg(row + lane + 32) : 0;
   const int32_t sp_l0 = lane < p.L ? __ldg(row + p.L - 1 - lane) : 0;
-  if (__ldg(&p.ctrl->status) != 0) return;                       // sticky error: no-op
+  const bool dead = __ldg(&p.ctrl->status) != 0;
 #else
-  if (ld_volatile(&p.ctrl->status) != 0) return;                 // sticky error: no-op
+  const bool dead = ld_volatile(&p.ctrl->status) != 0;
 #endif
+  // sticky error at entry (Q36: one snapshot per call; classify kernels never write `status`): the unit's
+  // decision is the empty one, nothing else happens
+  if (dead) {
+    if (lane == 0) reinterpret_cast<int4*>(dec)[u] = make_int4(0, -1, -1, -1);
+    return;
+  }
   if (u < (p.U + 31) / 32 && lane == 0) {
     // warm L2 with the ring window the following dkv_compact_alloc grants from: [start, start + U) holds
     // every page a decode step can demand (one per unit); one 128-B line per warp
@@ -88,7 +94,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
     const int pc = N - 1 - p.W;                                  // t_c = earliest window token
     if (st == DKV_REQ_ACTIVE && pc >= 0) {
       if (!finite_f(s_in) || s_in < 0.0f) {
-        if (lane == 0) set_status(p.ctrl, DKV_ERR_NONFINITE);
+        if (lane == 0) set_pending(p.ctrl, DKV_ERR_NONFINITE);   // Q36: merged by compact_alloc
       } else {
         sc = canon_zero(s_in);
         th = __fdiv_rn(unit_alpha_h(p, u), (float)N);            // alpha_h / N (per head: Q35)
@@ -250,6 +256,10 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   reinterpret_cast<int4*>(dec)[u] = w;
 }
 
+#ifndef DKV_CD_LONG_LEN
+#define DKV_CD_LONG_LEN 12288   // longest active request above which the full-register instantiation runs
+#endif
+
 template <int MINB>
 static cudaError_t launch_cd(const PoolDev& p, const float* sig, dkv_decision_t* dec, cudaStream_t s) {
   const size_t smem = 4 * (size_t)p.L * kCDWarps;
@@ -265,8 +275,7 @@ static cudaError_t launch_cd(const PoolDev& p, const float* sig, dkv_decision_t*
 // register budget: their scans take many batches and, when the minimum is shared, the exact pass, which
 // spills at the 10-CTA budget (measured: profiles/r1j_classify_long_ab.log)
 cudaError_t launch_classify_decode(const PoolDev& p, const float* sig, dkv_decision_t* dec, int max_len, cudaStream_t s) {
-  static const int long_len = getenv("DKV_CD_LONG") ? atoi(getenv("DKV_CD_LONG")) : 12288;   // tuning knob
-  if (max_len > long_len) return launch_cd<1>(p, sig, dec, s);
+  if (max_len > DKV_CD_LONG_LEN) return launch_cd<1>(p, sig, dec, s);
   return launch_cd<DKV_CD_MINB>(p, sig, dec, s);
 }
 

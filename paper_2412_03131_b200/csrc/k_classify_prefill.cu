@@ -21,7 +21,6 @@ classify_prefill_kernel(PoolDev p, int n, const float* __restrict__ sig, int64_t
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int w = blockIdx.x * kPrefillWarps + warp;               // (admitted index, unit-in-request)
   if (w >= n * p.LyH) return;
-  if (ld_volatile(&p.ctrl->status) != 0) return;
   const int i = w / p.LyH, j = w % p.LyH;
   const int r = p.admit[i];
   const int u = r * p.LyH + j;
@@ -30,6 +29,12 @@ classify_prefill_kernel(PoolDev p, int n, const float* __restrict__ sig, int64_t
   const int kept = max(T - p.W, 0);
   const float* row = sig + (int64_t)w * sig_stride;
   uint8_t* crow = cls_out ? cls_out + (int64_t)w * sig_stride : nullptr;
+  if (ld_volatile(&p.ctrl->status) != 0) {              // sticky error at entry (Q36): no classes, no counts
+    if (crow)
+      for (int t = lane; t < T; t += 32) crow[t] = DKV_CLS_NONE;
+    if (lane == 0) { p.pf_nh[u] = 0; p.pf_nl[u] = 0; }
+    return;
+  }
   int32_t* seg = p.pf_seg + (size_t)u * p.nseg * 2;
   int nh = 0, nl = 0;
   bool bad = false;
@@ -85,7 +90,7 @@ classify_prefill_kernel(PoolDev p, int n, const float* __restrict__ sig, int64_t
       }
     }
   }
-  if (__any_sync(kFull, bad) && lane == 0) set_status(p.ctrl, DKV_ERR_NONFINITE);
+  if (__any_sync(kFull, bad) && lane == 0) set_pending(p.ctrl, DKV_ERR_NONFINITE);   // Q36
   if (lane == 0) { p.pf_nh[u] = nh; p.pf_nl[u] = nl; }
 }
 

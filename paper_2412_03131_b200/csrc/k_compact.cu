@@ -61,7 +61,10 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   if (tid == 0) s_epoch = *(volatile unsigned long long*)&ctrl->ticket;
   if (tid == 32) s_start0 = ld_volatile(&ctrl->start);
   if (tid == 64) s_free0 = ld_volatile(&ctrl->free);
-  if (tid == 96) s_status0 = ld_volatile(&ctrl->status);
+  if (tid == 96) {                                   // entry status (Q36): sticky status, else classify's error
+    const int a = ld_volatile(&ctrl->status);
+    s_status0 = a != 0 ? a : ld_volatile(&ctrl->pending);
+  }
   const int tile = blockIdx.x;
   // per-unit loads do not depend on the control block: issue them before the first barrier
   const int u = tile * TU + tid;
@@ -317,6 +320,8 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   if (tid == 0 && (fast ? tile == p.num_tiles - 1 : tile == 0)) {
     if (fast) { D = s_incdem; F = s_incfr; }
     const int64_t free_avail = free0 + F;
+    if (status0 != 0) set_status(ctrl, status0);      // classify's pending error becomes the sticky status
+    ctrl->pending = 0;
     if (status0 == 0 && !ok) { set_status(ctrl, DKV_ERR_OOM); ctrl->oom_count += 1; }
     const int64_t ns = ok ? (start0 + D) % P : start0;
     const int64_t nf = ok ? free_avail - D : free_avail;
@@ -329,7 +334,9 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
     p.stats[0] = nf;
     p.stats[1] = -(status0 == 0 ? D : 0);
     p.stats[2] = -((int64_t)P - nf);
-    p.stats[3] = -(int64_t)ld_volatile(&ctrl->status);
+    const int fin = ld_volatile(&ctrl->status);
+    ctrl->qw_status = fin;                             // entry status of the following dkv_quant_write (Q36)
+    p.stats[3] = (int64_t)fin;                         // <= 0: the MIN over GPUs shows any error
   }
 }
 
@@ -344,9 +351,8 @@ static cudaError_t launch_tu(const PoolDev& p, const dkv_decision_t* dec, int ph
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
-  static const int coop = getenv("DKV_COMPACT_COOP") ? atoi(getenv("DKV_COMPACT_COOP")) : 1;   // tuning knob
   cfg.attrs = attr;
-  cfg.numAttrs = coop ? 1 : 0;
+  cfg.numAttrs = 1;                                    // always cooperative: the grid barrier needs co-residency
   return cudaLaunchKernelEx(&cfg, compact_alloc_kernel<TU>, p, dec, phase, alloc, defer);
 }
 

@@ -49,7 +49,7 @@ __global__ void set_requests_kernel(PoolDev p, ReqList l) {
     p.req_state[r] = DKV_REQ_ADMITTING;
     p.prompt_len[r] = l.len[i];
     p.admit[l.base + i] = r;
-  } else {
+  } else if (p.req_state[r] == DKV_REQ_ACTIVE) {      // an admission rolled back on the device (Q37) stays IDLE
     p.req_state[r] = DKV_REQ_PENDING_FREE;
   }
 }
@@ -72,7 +72,11 @@ cudaError_t launch_set_requests(const PoolDev& p, const int32_t* req, const int3
   return cudaSuccess;
 }
 
-__global__ void clear_status_kernel(PoolDev p) { p.ctrl->status = 0; }
+__global__ void clear_status_kernel(PoolDev p) {
+  p.ctrl->status = 0;
+  p.ctrl->pending = 0;
+  p.ctrl->qw_status = 0;
+}
 
 cudaError_t launch_clear_status(const PoolDev& p, cudaStream_t s) {
   clear_status_kernel<<<1, 1, 0, s>>>(p);

@@ -185,7 +185,9 @@ __global__ void __launch_bounds__(TU) prefill_conservative_kernel(PoolDev p) {
     p.stats[0] = nf;
     p.stats[1] = -(status0 == 0 ? D : 0);
     p.stats[2] = -((int64_t)P - nf);
-    p.stats[3] = -(int64_t)ld_volatile(&ctrl->status);
+    const int fin = ld_volatile(&ctrl->status);
+    ctrl->qw_status = fin;                             // entry status of the following dkv_quant_write (Q36)
+    p.stats[3] = (int64_t)fin;                         // <= 0: the MIN over GPUs shows any error
   }
 }
 

@@ -32,6 +32,9 @@
 namespace dkv {
 
 constexpr int kQDThreads = 256;
+#ifndef DKV_QD_LANES
+#define DKV_QD_LANES 8     // lanes per unit; measured best at d = 128 (profiles/r1g_quant_decode_compact_ab.log)
+#endif
 #ifndef DKV_QD_MINB
 #define DKV_QD_MINB 4      // CTAs per SM the register budget is sized for (the persistent grid follows it)
 #endif
@@ -278,10 +281,10 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
   const int lane = threadIdx.x & 31;
   const int q = lane % G;
   const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
-  if (threadIdx.x == 0) s_status = p.ctrl->status;
+  if (threadIdx.x == 0) s_status = p.ctrl->qw_status;    // entry status (Q36), left by dkv_compact_alloc
   const ReqCache rc = load_req_cache(p, qd_smem);
   __syncthreads();
-  if (s_status != 0) return;                             // sticky error: no-op
+  if (s_status != 0) return;                             // error at entry: no-op
   uint16_t* const my_nk = &s_new[0][threadIdx.x * EPL];
   uint16_t* const my_nv = &s_new[1][threadIdx.x * EPL];
 
@@ -409,7 +412,7 @@ static cudaError_t launch_qd(const PoolDev& p, const dkv_decision_t* dec, const 
 cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
                                 const float* sig, cudaStream_t s, int u0, int u1) {
   if (u1 < 0) u1 = p.U;
-  static const int g = getenv("DKV_QD_G") ? atoi(getenv("DKV_QD_G")) : 8;   // lanes per unit (tuning knob)
+  constexpr int g = DKV_QD_LANES;                       // lanes per unit (build-time choice)
   if (p.d == 128) {
     if (g == 32) return launch_qd<128, 32>(p, dec, k, v, sig, u0, u1, s);
     if (g == 8) return launch_qd<128, 8>(p, dec, k, v, sig, u0, u1, s);

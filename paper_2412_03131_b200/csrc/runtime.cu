@@ -143,7 +143,7 @@ struct dkv_pool {
   bool recovering;                   // last query reported an error: frees allowed out of sequence
   cudaStream_t copy_stream;          // dkv_decode_step_host: the new tokens' K/V H2D copy (created on first use)
   cudaEvent_t ev_ready;              // ... ordered after prior work on the caller's stream
-  cudaEvent_t ev_kv[8];              // ... unit chunk c of the K/V copy done
+  cudaEvent_t ev_kv;                 // ... the K/V copy done
 };
 
 extern "C" {
@@ -283,9 +283,23 @@ dkv_status_t dkv_pool_destroy(dkv_pool_t p) {
   if (p->h_seq) cudaFreeHost(p->h_seq);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   if (p->ev_ready) cudaEventDestroy(p->ev_ready);
-  for (cudaEvent_t e : p->ev_kv)
-    if (e) cudaEventDestroy(e);
+  if (p->ev_kv) cudaEventDestroy(p->ev_kv);
   delete p;
+  return DKV_OK;
+}
+
+// The host-detectable conditions of a decode dkv_classify: call order (a decode step interrupted by a device
+// error may be abandoned: its compact_alloc applied nothing) and no ACTIVE request at max_seq_len.  *max_len
+// receives the longest ACTIVE request.
+static dkv_status_t decode_precheck(const dkv_pool* p, int* max_len) {
+  if (p->seq != SEQ_IDLE && !(p->recovering && p->phase == DKV_PHASE_DECODE)) return DKV_ERR_STATE;
+  int m = 0;
+  for (int r = 0; r < p->cfg.max_requests; r++) {
+    if (p->req_state[r] != DKV_REQ_ACTIVE) continue;
+    if (p->seq_len[r] >= p->cfg.max_seq_len) return DKV_ERR_STATE;
+    m = p->seq_len[r] > m ? p->seq_len[r] : m;
+  }
+  *max_len = m;
   return DKV_OK;
 }
 
@@ -293,20 +307,16 @@ dkv_status_t dkv_classify(dkv_pool_t p, int32_t phase, const int32_t* h_req, con
                           const float* d_sig, int64_t sig_stride, dkv_decision_t* d_dec, uint8_t* d_token_class,
                           dkv_stream_t s) {
   if (!p) return DKV_ERR_INVALID_ARG;
-  // a decode step interrupted by a device error may be abandoned (its compact_alloc applied nothing)
-  if (p->seq != SEQ_IDLE && !(p->recovering && p->phase == DKV_PHASE_DECODE)) return DKV_ERR_STATE;
   const int R = p->cfg.max_requests;
   if (phase == DKV_PHASE_DECODE) {
     if (!d_dec) return DKV_ERR_INVALID_ARG;              // d_sig NULL: t_c's significance from the window
     int max_len = 0;
-    for (int r = 0; r < R; r++) {
-      if (p->req_state[r] != DKV_REQ_ACTIVE) continue;
-      if (p->seq_len[r] >= p->cfg.max_seq_len) return DKV_ERR_STATE;
-      max_len = p->seq_len[r] > max_len ? p->seq_len[r] : max_len;
-    }
+    const dkv_status_t pre = decode_precheck(p, &max_len);
+    if (pre != DKV_OK) return pre;
     cudaError_t e = launch_classify_decode(p->dev, d_sig, d_dec, max_len, (cudaStream_t)s);
     if (e != cudaSuccess) return DKV_ERR_CUDA;
   } else if (phase == DKV_PHASE_PREFILL) {
+    if (p->seq != SEQ_IDLE && !(p->recovering && p->phase == DKV_PHASE_DECODE)) return DKV_ERR_STATE;
     if (n < 0 || n > R || (n > 0 && (!h_req || !h_len || !d_sig))) return DKV_ERR_INVALID_ARG;
     int max_len = 0;
     std::vector<char> seen(R, 0);
@@ -463,7 +473,8 @@ dkv_status_t dkv_pool_query(dkv_pool_t p, dkv_stats_t* out, dkv_stream_t s) {
   if (e == cudaSuccess) e = launch_clear_status(p->dev, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return DKV_ERR_CUDA;
-  const Ctrl& c = *p->h_ctrl;
+  Ctrl& c = *p->h_ctrl;
+  if (c.status == DKV_OK) c.status = c.pending;         // an error classify found, not yet merged (Q36)
   if (out) {
     out->free_pages = c.free;
     out->used_pages = (int64_t)p->cfg.num_pages - c.free;
@@ -496,54 +507,49 @@ size_t dkv_decode_stage_bytes(dkv_pool_t p) {
 dkv_status_t dkv_decode_step_host(dkv_pool_t p, const float* h_sig, const uint16_t* h_kv, dkv_decision_t* h_dec,
                                   void* d_stage, size_t stage_bytes, dkv_stream_t st) {
   if (!p || !h_kv || !d_stage || stage_bytes < dkv_decode_stage_bytes(p)) return DKV_ERR_INVALID_ARG;
-  if (p->seq != SEQ_IDLE && !(p->recovering && p->phase == DKV_PHASE_DECODE)) return DKV_ERR_STATE;
+  // every host-detectable error before anything is queued (dkv.h: such errors enqueue nothing)
+  int max_len = 0;
+  const dkv_status_t pre = decode_precheck(p, &max_len);
+  if (pre != DKV_OK) return pre;
   cudaStream_t s = (cudaStream_t)st;
-  // the K/V copy and quant_write may go in unit chunks (quant_write of chunk c overlapping the copy of chunk
-  // c + 1); measured at the Llama-3-8B config (profiles/r1l_e2e_chunks.log): 1 chunk 219.7 us, 2: 220.9,
-  // 4: 244.4, 8: 278.4 — smaller copies lose more than the overlap gains, so one chunk is the default
-  static const int nch_env = getenv("DKV_E2E_CHUNKS") ? atoi(getenv("DKV_E2E_CHUNKS")) : 1;   // tuning knob (measured: 1 best)
-  const int nch = nch_env < 1 ? 1 : (nch_env > 8 ? 8 : nch_env);
-  if (!p->copy_stream) {
-    if (cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->ev_ready, cudaEventDisableTiming) != cudaSuccess)
+  if (!p->copy_stream) {                                 // created all-or-nothing on first use
+    cudaStream_t cs = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e0, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) != cudaSuccess) {
+      if (cs) cudaStreamDestroy(cs);
+      if (e0) cudaEventDestroy(e0);
+      if (e1) cudaEventDestroy(e1);
       return DKV_ERR_CUDA;
-    for (cudaEvent_t& e : p->ev_kv)
-      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return DKV_ERR_CUDA;
+    }
+    p->copy_stream = cs; p->ev_ready = e0; p->ev_kv = e1;
   }
   const size_t U = (size_t)p->G.U, d = (size_t)p->cfg.head_dim;
   uint8_t* b = (uint8_t*)d_stage;
   dkv_decision_t* d_dec = (dkv_decision_t*)b;
   float* d_sig = h_sig ? (float*)(b + stage_align(U * sizeof(dkv_decision_t))) : nullptr;
-  uint16_t* d_k = (uint16_t*)(b + stage_align(U * sizeof(dkv_decision_t)) + stage_align(U * 4));
-  uint16_t* d_v = d_k + U * d;
-  size_t cut[9];                                         // chunk boundaries, multiples of 32 units
-  for (int c = 0; c <= nch; c++) cut[c] = c == nch ? U : ((U * c / nch) & ~(size_t)31);
-  // the significance (U floats) first on s; the K/V copy (2·U·d halves) on the copy stream, ordered after
-  // everything already on s (the previous step's quant_write still reads the staging), overlapping
-  // classify + compact_alloc, which do not read it
+  uint16_t* d_kv = (uint16_t*)(b + stage_align(U * sizeof(dkv_decision_t)) + stage_align(U * 4));
+  // the significance (U floats) first on s; the K/V copy (2·U·d halves, one transfer) on the copy stream,
+  // ordered after everything already on s (the previous step's quant_write still reads the staging) and
+  // overlapping classify + compact_alloc, which do not read it.  Measured (profiles/r1l_e2e_chunks.log):
+  // splitting it into unit chunks that overlap quant_write is slower (2 / 4 / 8 chunks: 221 / 244 / 278 us
+  // vs 220 us at the Llama-3-8B config), so it is one copy.
   if (h_sig && cudaMemcpyAsync(d_sig, h_sig, U * 4, cudaMemcpyHostToDevice, s) != cudaSuccess) return DKV_ERR_CUDA;
   if (cudaEventRecord(p->ev_ready, s) != cudaSuccess || cudaStreamWaitEvent(p->copy_stream, p->ev_ready, 0) != cudaSuccess)
     return DKV_ERR_CUDA;
-  for (int c = 0; c < nch; c++) {
-    const size_t n = (cut[c + 1] - cut[c]) * d * 2;
-    if ((n && (cudaMemcpyAsync(d_k + cut[c] * d, h_kv + cut[c] * d, n, cudaMemcpyHostToDevice, p->copy_stream) != cudaSuccess ||
-               cudaMemcpyAsync(d_v + cut[c] * d, h_kv + (U + cut[c]) * d, n, cudaMemcpyHostToDevice, p->copy_stream) != cudaSuccess)) ||
-        cudaEventRecord(p->ev_kv[c], p->copy_stream) != cudaSuccess)
-      return DKV_ERR_CUDA;
+  const cudaError_t ce = cudaMemcpyAsync(d_kv, h_kv, 2 * U * d * 2, cudaMemcpyHostToDevice, p->copy_stream);
+  if (cudaEventRecord(p->ev_kv, p->copy_stream) != cudaSuccess) return DKV_ERR_CUDA;
+  if (ce != cudaSuccess) {
+    cudaStreamWaitEvent(s, p->ev_kv, 0);
+    return DKV_ERR_CUDA;
   }
   dkv_status_t r = dkv_classify(p, DKV_PHASE_DECODE, nullptr, nullptr, 0, d_sig, 0, d_dec, nullptr, st);
   if (r == DKV_OK) r = dkv_compact_alloc(p, d_dec, st);
-  if (r != DKV_OK) {                                     // s takes over the whole copy: later staging writes stay ordered
-    return cudaStreamWaitEvent(s, p->ev_kv[nch - 1], 0) == cudaSuccess ? r : DKV_ERR_CUDA;
-  }
-  // dkv_quant_write(DECODE), chunk by chunk as the K/V arrive
-  for (int c = 0; c < nch; c++) {
-    if (cudaStreamWaitEvent(s, p->ev_kv[c], 0) != cudaSuccess) return DKV_ERR_CUDA;
-    if (launch_quant_decode(p->dev, d_dec, d_k, d_v, d_sig, s, (int)cut[c], (int)cut[c + 1]) != cudaSuccess)
-      return DKV_ERR_CUDA;
-  }
-  p->seq = SEQ_IDLE;
-  p->recovering = false;
+  // s waits for the copy on every path from here, so later writes to the staging stay ordered after it
+  if (cudaStreamWaitEvent(s, p->ev_kv, 0) != cudaSuccess) return DKV_ERR_CUDA;
+  if (r == DKV_OK) r = dkv_quant_write(p, DKV_PHASE_DECODE, d_dec, d_kv, d_kv + U * d, 0, d_sig, 0, st);
+  if (r != DKV_OK) return r;
   if (h_dec && cudaMemcpyAsync(h_dec, d_dec, U * sizeof(dkv_decision_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
     return DKV_ERR_CUDA;
   return DKV_OK;

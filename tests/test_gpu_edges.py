@@ -195,3 +195,107 @@ def test_alpha_special_cases(alphas):
         _step(o, g, inp, life, step)
     if alphas[1] > 1e20:
         assert o.pool.free == scn.P
+
+
+@pytest.mark.parametrize("workflow", [0, 1])
+def test_prefill_error_rolls_back_admission_then_readmit(workflow):
+    """a dkv_quant_write(PREFILL) that finds an error at entry (here the admission's OOM)
+    rolls the admission back (ADMITTING -> IDLE, no pages held), so after dkv_pool_query the slots are
+    re-admissible; GPU and oracle agree at every step."""
+    scn = H.TINY.replace(prefill_workflow=workflow)
+    used, _, _, _ = _used_after_prefill(scn, [64, 64])
+    scn = scn.replace(P=used + 5)
+    o, g = _pair(scn)
+    inp, life = H.Inputs(scn), H.Lifecycle(scn)
+    H.admit([o, g], inp, life, [0, 1], [64, 64])
+    sig, k, v = inp.prefill([2, 3], [64, 64])
+    for b in (o, g):
+        assert b.classify_prefill([2, 3], [64, 64], sig) == 0
+        assert b.compact_alloc(None) == 0
+        assert b.quant_write_prefill(k, v, sig) == 0
+    _same(o, g, "rolled back")
+    assert list(o.pool.req_state[2:4]) == [H.REQ_IDLE, H.REQ_IDLE]
+    assert o.take_status() == oracle.ERR_OOM and g.take_status() == oracle.ERR_OOM
+    H.free([o, g], life, [0])                                  # make room, then admit a short prompt
+    for step in range(2):
+        _step(o, g, inp, life, step)
+    H.admit([o, g], inp, life, [2], [40])
+    _same(o, g, "re-admitted")
+    for step in range(2, 6):
+        _step(o, g, inp, life, step)
+
+
+def test_prefill_nonfinite_token_request_active_and_freeable():
+    """Q30/Q37: a non-finite K element found by the bulk writer rejects that token only; the requests become
+    ACTIVE (sticky NONFINITE), so after the query they can be freed and their pages recycled."""
+    scn = H.TINY
+    o, g = _pair(scn)
+    inp, life = H.Inputs(scn), H.Lifecycle(scn)
+    sig, k, v = inp.prefill([0, 1], [64, 64])
+    k = k.clone()
+    k.view(torch.int16)[1, 2, 3, 5] = 0x7E00
+    for b in (o, g):
+        assert b.classify_prefill([0, 1], [64, 64], sig) == 0
+        assert b.compact_alloc(None) == 0
+        assert b.quant_write_prefill(k, v, sig) == 0
+    _same(o, g, "prefill with a NaN key")
+    assert list(o.pool.req_state[:2]) == [H.REQ_ACTIVE, H.REQ_ACTIVE]
+    assert o.take_status() == oracle.ERR_NONFINITE and g.take_status() == oracle.ERR_NONFINITE
+    for b in (o, g):
+        assert b.free([0, 1]) == 0
+    life.state[:] = H.REQ_IDLE
+    H.decode_step([o, g], inp, life, 0)                          # recycles both requests
+    _same(o, g, "freed")
+    assert o.pool.free == scn.P
+    H.admit([o, g], inp, life, [0, 1], [64, 50])
+    _same(o, g, "re-admitted")
+
+
+def test_nonfinite_multi_cta_units_keep_going():
+    """the status is one snapshot per call, so an error found in one unit (one CTA) does not
+    stop the units of CTAs that start later: a pool spanning many CTAs of every decode / prefill kernel, with
+    non-finite significance and K/V in units far apart, matches the oracle in every byte."""
+    scn = H.TINY.replace(R=16, Ly=4, H=8, d=64, M=256, W=16, P=40000, seed=17)
+    for where in ("decode_kv", "decode_sig", "prefill_kv"):
+        o, g = _pair(scn)
+        inp, life = H.Inputs(scn), H.Lifecycle(scn)
+        reqs = list(range(scn.R))
+        lens = [80 + 7 * r for r in reqs]
+        if where == "prefill_kv":
+            sig, k, v = inp.prefill(reqs, lens)
+            k = k.clone()
+            for (i, j, t) in ((0, 1, 3), (7, 30, 40), (15, 31, 60)):
+                k.view(torch.int16)[i, j, t, 9] = 0x7C00
+            for b in (o, g):
+                assert b.classify_prefill(reqs, lens, sig) == 0
+                assert b.compact_alloc(None) == 0
+                assert b.quant_write_prefill(k, v, sig) == 0
+            _same(o, g, where)
+            assert o.pool.status == oracle.ERR_NONFINITE
+            continue
+        H.admit([o, g], inp, life, reqs, lens)
+        N = life.seq + 1
+        cand, k, v = inp.decode(N)
+        bad = [3, scn.U // 2 + 5, scn.U - 2]
+        if where == "decode_sig":
+            cand = cand.clone()
+            cand[bad] = float("nan")
+        else:
+            k = k.clone()
+            for u in bad:
+                k.view(torch.int16)[u, 7] = 0x7E00              # reaches t_c W steps later
+        from tests.gpu_backend import dec_np
+        for step in range(scn.W + 2):
+            (_, do), (_, dg) = o.classify_decode(cand), g.classify_decode(cand)
+            assert np.array_equal(dec_np(do).view(np.uint8), dec_np(dg).view(np.uint8)), (where, step)
+            for b, d in ((o, do), (g, dg)):
+                assert b.compact_alloc(d) == 0
+                assert b.quant_write_decode(d, k, v, cand) == 0
+            _same(o, g, f"{where} step {step}", pages=True)
+            if o.pool.status != 0:
+                break
+            life.seq += 1
+            cand, k2, v2 = inp.decode(life.seq + 1)
+            k = k2 if where != "decode_kv" else k
+            v = v2
+        assert o.pool.status == oracle.ERR_NONFINITE, where

@@ -60,7 +60,7 @@ def _worker(rank, world, port, q):
         o = _run(scn, steps=12)
         mine = _unit_contents(o, scn)
         # count all-reduce over the two pools
-        stats = torch.tensor([o.pool.free, -o.pool.last_demand, -(scn.P - o.pool.free), -o.pool.status],
+        stats = torch.tensor([o.pool.free, -o.pool.last_demand, -(scn.P - o.pool.free), o.pool.status],
                              dtype=torch.int64)
         red, _ = count_allreduce(stats)
         gathered = [None] * world
@@ -86,6 +86,39 @@ def test_head_sharded_pools_match_single_pool_and_count_allreduce():
     assert res["same"], "sharded pools differ from the single pool (PIN-13)"
     s0, s1 = res["stats"]
     assert res["red"] == res["red1"] == [min(a, b) for a, b in zip(s0, s1)]
+
+
+def _error_worker(rank, world, port, q):
+    """rank 1's pool runs out of pages at admission (a real sticky OOM); rank 0's is healthy"""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        scn = H.TINY.replace(R=2, Ly=2, H=2, d=32, W=8, Ch=4, Cl=8, M=96, P=600 if rank == 0 else 20, seed=5)
+        o = H.OracleBackend(scn)
+        inp = H.Inputs(scn)
+        sig, k, v = inp.prefill([0, 1], [60, 60])
+        assert o.classify_prefill([0, 1], [60, 60], sig) == 0
+        o.compact_alloc(None)
+        p = o.pool
+        stats = torch.tensor([p.free, -p.last_demand, -(scn.P - p.free), p.status], dtype=torch.int64)
+        red, _ = count_allreduce(stats)
+        adm = Admission(decode_reserve=0)
+        q.put((rank, int(p.status), red.tolist(), adm.healthy(red), adm.admit(red, 0)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_count_allreduce_shows_an_error_on_one_rank():
+    """the counters carry status itself (<= 0), so the MIN is negative when any one GPU has a pending
+    error and admission stops on every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    mp.spawn(_error_worker, args=(2, _free_port(), q), nprocs=2, join=True)
+    res = sorted([q.get(), q.get()])
+    assert res[0][1] == 0 and res[1][1] == -3                            # rank 1: DKV_ERR_OOM
+    for _, _, red, healthy, admit in res:
+        assert red[3] == -3 and not healthy and not admit
 
 
 def test_shard_heads_and_admission_rule():
