@@ -44,20 +44,35 @@ CONFIGS = {
                  alpha_h=1.0, alpha_l=0.02, mix=(0.35, 0.45, 0.20), seed=1, G=4),
 }
 METRIC = "µs per decode-step compact+alloc (64 req×32L×8H); quant-write GB/s vs HBM peak, 1/2/4/8 GPU"
+# the e2e key of both arms: one whole decode step (classify + compact_alloc + quant_write) through the public API
+E2E_UNIT = "us per decode step (classify + compact_alloc + quant_write through the public API)"
 
 
 # ----------------------------------------------------------------------------------------- distributed
-def dist_init():
+DIST = {"backend": None, "red_device": "cuda"}
+
+
+def dist_init(shared_device=False):
+    """One rank per GPU from the torchrun environment (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_*).  NCCL carries
+    the per-step count all-reduce (NCCL_DEBUG=INFO, subsystem INIT, prints each communicator's nranks to
+    stderr); with --shared-device (more ranks than GPUs) the ranks share GPUs and reduce over gloo."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    dev = local % max(ndev, 1) if shared_device else local
+    torch.cuda.set_device(dev)
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
-    return rank, world, local
+        if shared_device and ndev < world:
+            dist.init_process_group("gloo")
+            DIST.update(backend="gloo", red_device="cpu")
+        else:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+            DIST.update(backend="nccl", red_device="cuda")
+    return rank, world, dev
 
 
 def barrier(world):
@@ -66,22 +81,23 @@ def barrier(world):
         dist.barrier()
 
 
-def max_over_ranks(x: float, world: int) -> float:
+def _reduce(x: float, world: int, op) -> float:
     if world == 1:
         return x
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = torch.tensor([x], dtype=torch.float64, device=DIST["red_device"])
+    dist.all_reduce(t, op=op)
     return float(t.item())
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    import torch.distributed as dist
+    return _reduce(x, world, dist.ReduceOp.MAX if world > 1 else None)
 
 
 def sum_over_ranks(x: float, world: int) -> float:
-    if world == 1:
-        return x
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    return _reduce(x, world, dist.ReduceOp.SUM if world > 1 else None)
 
 
 # ----------------------------------------------------------------------------------------- clocks
@@ -179,18 +195,22 @@ class Workload:
         return cand.contiguous(), k.contiguous(), v.contiguous()
 
 
+def bulk_bytes_counts(nh, nl, kept, nw, geom, d):
+    """Algorithmic bytes of one dkv_quant_write(PREFILL), SURVEY §8(d) accounting: a kept token reads its K and
+    V (2·d fp16 = 512 B at d = 128) and writes its codes + {s, z} K/V metadata + score + position (High K8V4:
+    128 + 64 + 4 + 4 + 4 + 4 = 208 B -> 720 B; Low K4V2: 112 B -> 624 B); a pruned token moves nothing; a
+    window token reads 2·d fp16 and writes them to the window (1024 B at d = 128)."""
+    hb = 4 * d + geom[1]["k_row"] + geom[1]["v_row"] + 16
+    lb = 4 * d + geom[2]["k_row"] + geom[2]["v_row"] + 16
+    return nh * hb + nl * lb + nw * 8 * d, dict(high=nh, low=nl, pruned=kept - nh - nl, window=nw)
+
+
 def bulk_bytes(pool, geom, W, d, T, units):
-    """Algorithmic bytes of one dkv_quant_write(PREFILL) of `units` prompts of T tokens."""
+    """bulk_bytes_counts for the pool's current contents after an admission of `units` prompts of T tokens"""
     v = pool.views()
     nh = int(v["n_h"].sum().item())
     nl = int(v["n_l"].sum().item())
-    kept = units * max(T - W, 0)
-    npr = kept - nh - nl
-    nw = units * min(W, T)
-    rd = 2 * d * 2 + 4
-    hb = rd + geom[1]["k_row"] + geom[1]["v_row"] + 16
-    lb = rd + geom[2]["k_row"] + geom[2]["v_row"] + 16
-    return nh * hb + nl * lb + npr * 4 + nw * 4 * d, dict(high=nh, low=nl, pruned=npr, window=nw)
+    return bulk_bytes_counts(nh, nl, units * max(T - W, 0), units * min(W, T), geom, d)
 
 
 def load_peaks():
@@ -293,13 +313,22 @@ def run_ours(args, rank, world, local):
     bulk_max = max_over_ranks(bulk_mean, world)
 
     # ---------------- decode phase
+    from paper_2412_03131_b200.admission import Admission, prefill_page_bound
     seq = np.full(wl.R, T, np.int64)
     active = np.ones(wl.R, bool)
-    side = torch.cuda.Stream(device=dev) if world > 1 else None
-    stats_view = pool.views()["stats"]
-    red = torch.empty(4, dtype=torch.int64, device=dev)
+    nccl = DIST["backend"] == "nccl"
+    side = torch.cuda.Stream(device=dev) if world > 1 and nccl else None
+    v0 = pool.views()
+    stats_view = v0["stats"]
+    red = torch.empty(4, dtype=torch.int64, device=dev if nccl else "cpu")
     comp_us, cls_us, qw_us, step_us, cls_bytes = [], [], [], [], []
     ar_us, ar_hidden = [], []
+    realized = {"demand": [], "freed": [], "downgrades": [], "pruned_victims": [], "oom": 0}
+    # SURVEY §8e admission: a freed request's slot is re-admitted only when EVERY GPU has room for its shard's
+    # prefill bound plus the decode reserve (one page per unit), judged on the MIN-reduced counters
+    adm = Admission(decode_reserve=wl.U)
+    bound = prefill_page_bound(T, c["W"], c["Ch"], wl.LyH)
+    waiting, admitted_n, deferred_n = [], 0, 0
     # launch floor: event -> trivial kernel -> event, measured the same way as the step kernels
     floor_us = []
     for _ in range(20):
@@ -325,6 +354,7 @@ def run_ours(args, rank, world, local):
             r = (s * 7) % wl.R
             pool.free([r])
             active[r] = False
+            waiting.append(r)
             freed_steps += 1
         cand, nk, nv = wl.decode_inputs(seq, active)
         nh0, nl0 = v["n_h"].clone(), v["n_l"].clone()
@@ -342,7 +372,7 @@ def run_ours(args, rank, world, local):
         e[1].record()
         pool.compact_alloc(dec)
         e[2].record()
-        if side is not None:                                # count all-reduce, overlapped (one-step lag)
+        if side is not None:                                # count all-reduce over NCCL, overlapped with quant_write
             import torch.distributed as dist
             side.wait_event(e[2])
             with torch.cuda.stream(side):
@@ -353,13 +383,24 @@ def run_ours(args, rank, world, local):
         pool.quant_write_decode(dec, nk.view(torch.int16), nv.view(torch.int16), cand)
         e[3].record()
         torch.cuda.synchronize()
+        if side is None:                                    # one rank, or gloo (--shared-device): after the step
+            red.copy_(stats_view)
+            if world > 1:
+                import torch.distributed as dist
+                dist.all_reduce(red, op=dist.ReduceOp.MIN)
         seq[active] += 1
-        if churn:                                           # re-admit (untimed prefill of 4096 tokens)
-            pool.classify_prefill([r], [T], sig[r:r + 1])
-            pool.compact_alloc(None)
-            pool.quant_write_prefill(k16[r:r + 1], v16[r:r + 1], sig[r:r + 1])
-            seq[r] = T
-            active[r] = True
+        # admission on the reduced counters (identical on every rank, so every rank decides the same)
+        for r in list(waiting):
+            if adm.admit(red.cpu(), bound):
+                pool.classify_prefill([r], [T], sig[r:r + 1])   # re-admit (untimed prefill of a 4096-token prompt)
+                pool.compact_alloc(None)
+                pool.quant_write_prefill(k16[r:r + 1], v16[r:r + 1], sig[r:r + 1])
+                seq[r] = T
+                active[r] = True
+                waiting.remove(r)
+                admitted_n += 1
+            else:
+                deferred_n += 1
         if timed:
             cls_us.append(e[0].elapsed_time(e[1]) * 1e3)
             comp_us.append(e[1].elapsed_time(e[2]) * 1e3)
@@ -369,10 +410,18 @@ def run_ours(args, rank, world, local):
             if side is not None:                            # count all-reduce latency; hidden if it ended in the step
                 ar_us.append(ar[0].elapsed_time(ar[1]) * 1e3)
                 ar_hidden.append(e[0].elapsed_time(ar[1]) <= e[0].elapsed_time(e[3]))
-            tc = dec.view(torch.uint8).view(-1, 16)[:, 0].cpu().numpy()
+            d16 = dec.view(torch.uint8).view(-1, 16).cpu().numpy()
+            tc = d16[:, 0]
             sec = np.where(tc == 1, nh0.cpu().numpy(), np.where(tc == 2, nl0.cpu().numpy(), 0)).astype(np.int64)
             C = np.where(tc == 1, geom[1]["C"], geom[2]["C"])
             cls_bytes.append(int((4 * sec + 4 * ((sec + C - 1) // C)).sum() + 28 * wl.U))
+            # Ctrl as int64: start, free, {status, oom_count}, ticket, arrive, last_demand, last_freed
+            ct = pool.arena[int(pool.layout.off_ctrl):int(pool.layout.off_ctrl) + 56].view(torch.int64).cpu().numpy()
+            realized["demand"].append(int(ct[5]))
+            realized["freed"].append(int(ct[6]))
+            realized["downgrades"].append(int((d16[:, 1] == 2).sum()))
+            realized["pruned_victims"].append(int((d16[:, 1] == 3).sum()))
+            realized["oom"] += int(int(ct[2]) & 0xFFFFFFFF == (-3 & 0xFFFFFFFF))
     st, stats = pool.query()
     assert st == 0, f"device status {st} after decode"
     wall = time.time() - t_wall0
@@ -485,6 +534,42 @@ def run_ours(args, rank, world, local):
                  "note": "dkv_attend (NEXT-2) supplies significance; classify takes its victims from the "
                          "attention kernel's section minima (no scan)"}
 
+    # ---------------- recycle micro-benchmark: free 1 / 8 / 32 requests, then one decode step whose
+    # dkv_compact_alloc recycles all their pages (~37k / 300k / 1.2M page IDs at this config)
+    recycle = {}
+    if wl.R >= 32:
+        for kq in (1, 8, 32):
+            reqs_k = [r for r in range(wl.R) if active[r]][:kq]
+            r0 = reqs_k[0]
+            if reqs_k != list(range(r0, r0 + kq)):
+                continue
+            pool.free(reqs_k)
+            active[reqs_k] = False
+            cand, nk, nv = wl.decode_inputs(seq, active)
+            flush.zero_()
+            torch.cuda.synchronize()
+            e = [ev() for _ in range(3)]
+            torch.cuda._sleep(200_000)
+            e[0].record()
+            pool.classify_decode(cand, dec)
+            e[1].record()
+            pool.compact_alloc(dec)
+            e[2].record()
+            pool.quant_write_decode(dec, nk.view(torch.int16), nv.view(torch.int16), cand)
+            torch.cuda.synchronize()
+            launches += 4
+            seq[active] += 1
+            ct = pool.arena[int(pool.layout.off_ctrl):int(pool.layout.off_ctrl) + 56].view(torch.int64).cpu().numpy()
+            recycle[str(kq)] = {"compact_alloc_us": round(e[1].elapsed_time(e[2]) * 1e3, 2),
+                                "recycled_pages": int(ct[6])}
+            pool.classify_prefill(reqs_k, [T] * kq, sig[r0:r0 + kq])
+            pool.compact_alloc(None)
+            pool.quant_write_prefill(k16[r0:r0 + kq], v16[r0:r0 + kq], sig[r0:r0 + kq])
+            seq[reqs_k] = T
+            active[reqs_k] = True
+        st, _ = pool.query()
+        assert st == 0, f"device status {st} after the recycle micro-benchmark"
+
     # ---------------- aggregate (max over ranks)
     comp_mean = max_over_ranks(statistics.mean(comp_us), world)
     step_mean = max_over_ranks(statistics.mean(step_us), world)
@@ -520,10 +605,23 @@ def run_ours(args, rank, world, local):
         },
         "decode_step_us": {"classify": round(cls_mean, 3), "compact_alloc": round(comp_mean, 3),
                            "quant_write": round(qw_mean, 3), "step": round(step_mean, 3),
-                           "compact_alloc_p50": round(float(np.percentile(comp_us, 50)), 3),
-                           "compact_alloc_p99": round(float(np.percentile(comp_us, 99)), 3),
+                           **{f"{name}_p{q}": round(float(np.percentile(xs, q)), 3)
+                              for name, xs in (("classify", cls_us), ("compact_alloc", comp_us), ("quant_write", qw_us))
+                              for q in (50, 99)},
+                           "percentile_note": f"over {len(comp_us)} timed steps (p99 of so few samples is near the max)",
                            "launch_floor": round(floor, 3),
                            "recycle_steps": freed_steps},
+        # what each step actually did (means over the timed steps)
+        "realized_per_step": {"demand_pages": round(statistics.mean(realized["demand"]), 1),
+                              "freed_pages": round(statistics.mean(realized["freed"]), 1),
+                              "downgrades": round(statistics.mean(realized["downgrades"]), 1),
+                              "pruned_victims": round(statistics.mean(realized["pruned_victims"]), 1),
+                              "oom_steps": realized["oom"]},
+        "admission": {"rule": "admit iff MIN over GPUs of free pages >= prefill bound + one page per unit "
+                              "(paper_2412_03131_b200/admission.py, on the all-reduced counters)",
+                      "admitted": admitted_n, "deferred_checks": deferred_n, "prefill_bound_pages": bound},
+        "dist": {"backend": DIST["backend"], "world": world,
+                 "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if DIST["backend"] == "nccl" else None},
         "quant_write": {"gbs": round(agg_bulk_gbs, 1), "gbs_per_gpu": round(bulk_gbs_rank, 1),
                         "ms": round(bulk_max, 3), "algorithmic_bytes_per_gpu": bbytes, "token_mix": bmix,
                         "frac_of_hbm_peak": round(bulk_gbs_rank / peak, 4)},
@@ -535,8 +633,7 @@ def run_ours(args, rank, world, local):
                             "peak": peak, "unit": "GB/s", "frac": round(cls_gbs / peak, 4),
                             "algorithmic_bytes": int(statistics.mean(cls_bytes)),
                             "traffic": traffic("classify_decode_kernel"), "traffic_unit": "bytes per launch"},
-        "e2e": {"value": round(e2e_mean, 3), "unit": "us per decode step, one dkv_decode_step_host call (H2D inputs + classify + compact_alloc + "
-                                                     "quant_write + D2H decisions)",
+        "e2e": {"value": round(e2e_mean, 3), "unit": E2E_UNIT,
                 "h2d_bytes_per_step": wl.U * (4 + 2 * 2 * c["d"]), "d2h_bytes_per_step": wl.U * 16},
         "next2": next2,
         # §8e: the per-step MIN all-reduce of the admission counters (N > 1): its latency on the side stream and
@@ -544,6 +641,11 @@ def run_ours(args, rank, world, local):
         "allreduce": ({"us": round(max_over_ranks(statistics.mean(ar_us), world), 2),
                        "hidden_frac": round(sum(ar_hidden) / len(ar_hidden), 3), "bytes": 32}
                       if ar_us else None),
+        "recycle_microbench": recycle,
+        # the paper's own figure for this path (other hardware: context, not a target): the whole memory manager
+        # is < 0.2 % (prompt) / < 0.9 % (generation) of step latency on L40 inside vLLM
+        "paper_context": {"manager_share_of_step_L40": {"prompt": "< 0.2 %", "generation": "< 0.9 %"},
+                          "cite": "PAPER.md:853-859 (§7.2 Memory Management Overhead)"},
         "gpu_launches": launches,
         "clocks": clocks,
         "wall_s": round(wall, 1),
@@ -558,6 +660,33 @@ def run_oracle_sample(args, sample_requests=1, steps=None):
     full per-GPU batch by the unit ratio."""
     import oracle  # test infrastructure: bench's cpu_baseline / --impl reference legs only
 
+    host = host_cpu()
+    saved = os.sched_getaffinity(0)
+    core = min(saved)
+    os.sched_setaffinity(0, {core})                       # SURVEY §8(d): the serial oracle pinned to one core
+    try:
+        o = _oracle_sample(args, oracle, sample_requests, steps)
+    finally:
+        os.sched_setaffinity(0, saved)
+    o.update(cores=1, core=core, cpu_model=host["cpu_model"], nproc=host["nproc"],
+             pinning=f"sched_setaffinity to core {core} (1 of {host['nproc']} cores)")
+    return o
+
+
+def host_cpu():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def _oracle_sample(args, oracle, sample_requests, steps):
     c = CONFIGS[args.config]
     Rs = sample_requests
     T = c["prompt"]
@@ -577,12 +706,10 @@ def run_oracle_sample(args, sample_requests=1, steps=None):
     t2 = time.perf_counter()
     units = Rs * c["Ly"] * c["H"]
     # algorithmic bytes of the sample's bulk write (same accounting as the GPU)
-    nh, nl = int(pool.n_h.sum()), int(pool.n_l.sum())
-    kept = units * (T - c["W"])
     g = pool.geom
-    rd = 2 * c["d"] * 2 + 4
-    bb = nh * (rd + g[1].k_row + g[1].v_row + 16) + nl * (rd + g[2].k_row + g[2].v_row + 16) + \
-        (kept - nh - nl) * 4 + units * c["W"] * 4 * c["d"]
+    geom = {k: dict(k_row=g[k].k_row, v_row=g[k].v_row) for k in (1, 2)}
+    bb, _ = bulk_bytes_counts(int(pool.n_h.sum()), int(pool.n_l.sum()), units * (T - c["W"]), units * c["W"],
+                              geom, c["d"])
     seq = np.full(Rs, T, np.int64)
     act = np.ones(Rs, bool)
     comp, cls, qw = [], [], []
@@ -605,12 +732,19 @@ def run_oracle_sample(args, sample_requests=1, steps=None):
         "compact_us": statistics.mean(comp) * 1e6 * scale,
         "classify_us": statistics.mean(cls) * 1e6 * scale,
         "quant_us": statistics.mean(qw) * 1e6 * scale,
+        "step_us": statistics.mean([a + b + q for a, b, q in zip(cls, comp, qw)]) * 1e6 * scale,
         "bulk_gbs": bb / (t2 - t1) / 1e9,
         "prefill_classify_s": t1 - t0,
         "sample": f"{Rs} of {c['R']} requests ({units} of {c['R'] * c['Ly'] * c['H']} units), prompt {T}, "
                   f"{steps} decode steps; µs scaled by the unit ratio x{scale:g}",
-        "cores": 1,
     }
+
+
+def cpu_baseline_obj(o):
+    return {"value": round(o["compact_us"], 3), "unit": "us", "cores": o["cores"], "kind": "oracle",
+            "sample": o["sample"], "cpu_model": o["cpu_model"], "nproc": o["nproc"], "pinning": o["pinning"],
+            "quant_write_gbs": round(o["bulk_gbs"], 3), "classify_us": round(o["classify_us"], 1),
+            "quant_write_decode_us": round(o["quant_us"], 1), "step_us": round(o["step_us"], 1)}
 
 
 def run_reference(args, rank, world):
@@ -634,12 +768,38 @@ def run_reference(args, rank, world):
         "dtype": "fp16 in / u8 codes (fp32 quantizer arithmetic)",
         "data": "synthetic (seeded counter-based, synth/)",
         "config": {"workload": f"{args.config} (oracle sample)", "global_batch": c["R"]},
-        "cpu_baseline": {"value": round(o["compact_us"], 3), "unit": "us", "cores": o["cores"], "kind": "oracle",
-                         "sample": o["sample"], "quant_write_gbs": round(o["bulk_gbs"], 3),
-                         "classify_us": round(o["classify_us"], 1), "quant_write_decode_us": round(o["quant_us"], 1)},
-        "e2e": {"value": round(o["compact_us"], 3), "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": cpu_baseline_obj(o),
+        # the oracle's whole decode step, in our e2e unit (it runs on host buffers: no copies)
+        "e2e": {"value": round(o["step_us"], 3), "unit": E2E_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": round(time.time() - t0, 1),
     }
+
+
+def _spawned_rank(local, world, port, argv):
+    """one rank of `bench.py --gpus N` started without torchrun: the torchrun environment, then main()"""
+    os.environ.update(RANK=str(local), LOCAL_RANK=str(local), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
+                      MASTER_PORT=str(port))
+    sys.argv = [sys.argv[0]] + argv
+    main()
+
+
+def launch_ranks(args, argv):
+    """`--gpus N` without WORLD_SIZE: spawn N ranks here, one per GPU (the same processes torchrun would start).
+    Fails loudly when the node has fewer GPUs, unless --shared-device maps several ranks onto each GPU (a
+    functional check of the N-rank path only: the ranks then share one GPU's SMs and HBM, and the counter
+    all-reduce runs over gloo because NCCL refuses two ranks on one device)."""
+    import socket
+
+    import torch.multiprocessing as mp
+    ndev = torch.cuda.device_count()
+    if ndev < args.gpus and not args.shared_device:
+        sys.exit(f"bench.py --gpus {args.gpus}: this node has {ndev} CUDA device(s); run on an {args.gpus}-GPU node "
+                 f"(or pass --shared-device for a functional run of the {args.gpus}-rank path on fewer GPUs)")
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    mp.spawn(_spawned_rank, args=(args.gpus, port, argv), nprocs=args.gpus, join=True)
 
 
 def main():
@@ -654,25 +814,29 @@ def main():
     ap.add_argument("--next2", type=int, default=1, help="also time NEXT-2 decode steps (dkv_attend)")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: fixed global batch (configs[1]'s 64 requests), heads sharded N-way")
+    ap.add_argument("--shared-device", action="store_true",
+                    help="allow more ranks than GPUs (functional check; counters over gloo)")
+    argv = sys.argv[1:]
     args = ap.parse_args()
-    assert args.warmup >= 1
+    assert args.warmup >= 3, "the driver's timing rules need >= 3 warm-up steps"
+    env_world = os.environ.get("WORLD_SIZE")
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
-        world = int(os.environ.get("WORLD_SIZE", "1"))
+        world = int(env_world or args.gpus)
         out = run_reference(args, rank, world)
         if out is not None:
             print(json.dumps(out), flush=True)
         return
-    rank, world, local = dist_init()
+    if env_world is None and args.gpus > 1:
+        launch_ranks(args, argv)
+        return
+    if env_world is not None and int(env_world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}")
+    rank, world, local = dist_init(args.shared_device)
     out = run_ours(args, rank, world, local)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            o = run_oracle_sample(args)
-            out["cpu_baseline"] = {"value": round(o["compact_us"], 3), "unit": "us", "cores": o["cores"],
-                                   "kind": "oracle", "sample": o["sample"],
-                                   "quant_write_gbs": round(o["bulk_gbs"], 3),
-                                   "classify_us": round(o["classify_us"], 1),
-                                   "quant_write_decode_us": round(o["quant_us"], 1)}
+            out["cpu_baseline"] = cpu_baseline_obj(run_oracle_sample(args))
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -47,6 +47,13 @@ def _used_after_prefill(scn, lens):
     return (1 << 16) - o.pool.free, o, inp, life
 
 
+def _pool_pages_for_second_oom(scn, lens):
+    """pages for which an admission of `lens` succeeds and a second, identical one runs out: the first needs
+    its transient demand (the prompt workflow's conservative blocks exceed what it keeps, Fig. 5)"""
+    used, o, _, _ = _used_after_prefill(scn, lens)
+    return max(used + 5, int(o.pool.last_demand) + 2)
+
+
 def test_decode_oom_all_or_nothing_then_recover():
     from tests.gpu_backend import dec_np
     scn = H.TINY
@@ -84,12 +91,12 @@ def test_decode_oom_all_or_nothing_then_recover():
 @pytest.mark.parametrize("workflow", [0, 1])
 def test_prefill_oom_leaves_allocation_untouched(workflow):
     scn = H.TINY.replace(prefill_workflow=workflow)
-    used, _, _, _ = _used_after_prefill(scn, [64, 64])
-    scn = scn.replace(P=used + 5)
+    scn = scn.replace(P=_pool_pages_for_second_oom(scn, [64, 64]))
     o, g = _pair(scn)
     inp, life = H.Inputs(scn), H.Lifecycle(scn)
     H.admit([o, g], inp, life, [0, 1], [64, 64])
     _same(o, g, "first admission")
+    assert o.pool.status == 0
     sig, k, v = inp.prefill([2, 3], [64, 64])
     for b in (o, g):
         assert b.classify_prefill([2, 3], [64, 64], sig) == 0
@@ -203,11 +210,11 @@ def test_prefill_error_rolls_back_admission_then_readmit(workflow):
     rolls the admission back (ADMITTING -> IDLE, no pages held), so after dkv_pool_query the slots are
     re-admissible; GPU and oracle agree at every step."""
     scn = H.TINY.replace(prefill_workflow=workflow)
-    used, _, _, _ = _used_after_prefill(scn, [64, 64])
-    scn = scn.replace(P=used + 5)
+    scn = scn.replace(P=_pool_pages_for_second_oom(scn, [64, 64]))
     o, g = _pair(scn)
     inp, life = H.Inputs(scn), H.Lifecycle(scn)
     H.admit([o, g], inp, life, [0, 1], [64, 64])
+    assert o.pool.status == 0
     sig, k, v = inp.prefill([2, 3], [64, 64])
     for b in (o, g):
         assert b.classify_prefill([2, 3], [64, 64], sig) == 0
