@@ -389,6 +389,8 @@ def run_ours(args, rank, world, local):
                 import torch.distributed as dist
                 dist.all_reduce(red, op=dist.ReduceOp.MIN)
         seq[active] += 1
+        # Ctrl as int64: start, free, {status, oom_count}, ticket, arrive, last_demand, last_freed
+        ct = pool.arena[int(pool.layout.off_ctrl):int(pool.layout.off_ctrl) + 56].view(torch.int64).cpu().numpy()
         # admission on the reduced counters (identical on every rank, so every rank decides the same)
         for r in list(waiting):
             if adm.admit(red.cpu(), bound):
@@ -415,8 +417,6 @@ def run_ours(args, rank, world, local):
             sec = np.where(tc == 1, nh0.cpu().numpy(), np.where(tc == 2, nl0.cpu().numpy(), 0)).astype(np.int64)
             C = np.where(tc == 1, geom[1]["C"], geom[2]["C"])
             cls_bytes.append(int((4 * sec + 4 * ((sec + C - 1) // C)).sum() + 28 * wl.U))
-            # Ctrl as int64: start, free, {status, oom_count}, ticket, arrive, last_demand, last_freed
-            ct = pool.arena[int(pool.layout.off_ctrl):int(pool.layout.off_ctrl) + 56].view(torch.int64).cpu().numpy()
             realized["demand"].append(int(ct[5]))
             realized["freed"].append(int(ct[6]))
             realized["downgrades"].append(int((d16[:, 1] == 2).sum()))

@@ -130,6 +130,10 @@ typedef struct {
   int64_t off_head_alpha;      /* fp32[layers * kv_heads][2]: per-head (alpha_h, alpha_l) (NEXT-4) */
   int64_t off_att_scratch;     /* NEXT-2 long contexts: 296 slots of (ceil4(q_per_kv) + 2) * max_seq_len fp32 when
                                   those do not fit in shared memory (0 bytes otherwise) */
+  int64_t off_qpid;            /* int32[units][2] {page of t_c's slot (= the victim's KV_h page when it is
+                                  downgraded), page of a downgraded victim's KV_l slot}: written by
+                                  dkv_classify(DECODE) for existing pages and by dkv_compact_alloc for granted
+                                  ones, read by dkv_quant_write(DECODE) instead of the tables */
 } dkv_layout_t;
 
 /* Arena size for `cfg`, or 0 if the configuration is invalid. */

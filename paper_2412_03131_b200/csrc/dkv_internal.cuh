@@ -106,6 +106,7 @@ struct PoolDev {
   int32_t att_slots;
   int32_t use_head_alpha;   // 1: head_alpha replaces alpha_h / alpha_l
   int32_t prefill_wf;   // dkv_config_t.prefill_workflow
+  int2* qpid;           // [U] {t_c's page, downgraded victim's KV_l page} for dkv_quant_write(DECODE)
 };
 
 // ------------------------------------------------------------------------------------- memory ops

@@ -254,6 +254,23 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   w.x = (int)((uint32_t)tc_class | ((uint32_t)v_action << 8) | ((uint32_t)grow << 16) | ((uint32_t)demand << 24));
   w.y = v_slot; w.z = tc_slot; w.w = v_dst_slot;
   reinterpret_cast<int4*>(dec)[u] = w;
+  // The page IDs dkv_quant_write(DECODE) will touch, so that it reads no table: t_c's page (which is also the
+  // victim's KV_h page when the victim is downgraded, since t_c takes its slot, Q8) and the KV_l page a
+  // downgraded victim moves to.  A page the growing section receives this step is not known yet: -1 here,
+  // written by dkv_compact_alloc when it grants it.  The scanned section's IDs are in shared memory already.
+  if (scan) {
+    const bool hi = cls == DKV_CLS_HIGH;
+    const int C = hi ? p.Ch : p.Cl;
+    const int32_t* trow = p.table + (size_t)u * p.L;
+    const bool have = n > 0 && !fused;                          // s_pid holds the section's pages
+    int pa = -1, pb = -1;
+    if (!(v_action == DKV_V_KEEP && demand)) {
+      const int k = tc_slot / C;
+      pa = have ? s_pid[k] : __ldg(trow + (hi ? k : p.L - 1 - k));
+    }
+    if (v_action == DKV_V_DOWN && !demand) pb = __ldg(trow + p.L - 1 - nl / p.Cl);
+    p.qpid[u] = make_int2(pa, pb);
+  }
 }
 
 #ifndef DKV_CD_LONG_LEN

@@ -273,7 +273,10 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
           const int slot = (grow == DKV_GROW_HIGH) ? nh / p.Ch : L - 1 - nl / p.Cl;
           int64_t pos = start0 + off_dem;                        // < 2P (off_dem < D <= free)
           pos -= pos >= P ? P : 0;
-          p.table[(size_t)u * L + slot] = __ldcg(p.ring + pos);
+          const int32_t pid = __ldcg(p.ring + pos);
+          p.table[(size_t)u * L + slot] = pid;
+          // for dkv_quant_write: the granted page is t_c's (KEEP) or the downgraded victim's KV_l page (DOWN)
+          reinterpret_cast<int32_t*>(p.qpid + u)[((dword >> 8) & 0xFF) == DKV_V_DOWN ? 1 : 0] = pid;
         }
       }
       if (st == DKV_REQ_ACTIVE) {

@@ -10,18 +10,17 @@
 //      score = s_c, position = p_c;
 //   3. write the new token into that same window slot (after its old row has been consumed).
 //
-// What sets the duration (measured, profiles/): the unit count, not the bytes.  A unit is a chain of three
-// dependent memory round trips —
-//   A. everything indexed by u alone: decision word, s_c, the new token's K/V (request state and length
-//      come from a per-CTA shared-memory copy: thousands of warps reading the same word queue at one L2
-//      slice);
-//   B. everything the decision or the length addresses: t_c's window row and the (at most three) table
-//      entries the unit touches, one per lane (t_c's page, the victim's KV_h page, its KV_l page);
-//   C. the victim's K8V4 record (downgrades only), addressed by the page IDs shuffled from B —
-// followed by the per-vector scalar work (min/max reduction, two correctly rounded divisions), which a
-// group does once for all its lanes: several units per warp amortise it.  The window push is issued only
-// after t_c's row has been consumed: a store issued while the same line's load miss is outstanding takes a
-// slow path in L2 (measured: 73 -> 26 us at the Llama-3-8B config).
+// What sets the duration (measured, profiles/): the unit count, not the bytes — each unit is a chain of
+// dependent memory round trips, followed by the per-vector scalar work (min/max reduction, two correctly
+// rounded divisions) that a group does once for all its lanes (several units per warp amortise it):
+//   A. everything indexed by u alone: decision word, the page IDs it touches (qpid: dkv_classify recorded
+//      the existing pages, dkv_compact_alloc the granted one — in round 1 this kernel read them from the
+//      tables, a second dependent trip), s_c, t_c's window row (its slot follows from the request length,
+//      which comes from a per-CTA shared-memory copy: thousands of warps reading the same word queue at one
+//      L2 slice) and the new token's K/V;
+//   C. the victim's K8V4 record (downgrades only), addressed by the page ID from A.
+// The window push is issued only after t_c's row has been consumed: a store issued while the same line's
+// load miss is outstanding takes a slow path in L2 (measured: 73 -> 26 us at the Llama-3-8B config).
 // Quantizer arithmetic is the oracle's (c.5 / Q16), expressed as in dkv_internal.cuh's quant_h16 /
 // quant_chunks_f32: packed half2 NaN-propagating min/max, one mixed-precision subtraction, exact
 // round-half-away via two round-down adds.
@@ -292,18 +291,32 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
     const int u = u0 + ub * UPC + threadIdx.x / G;
     if (u >= u1) break;                                  // whole groups leave together (last block only)
 
-    // ---- A: loads indexed by u only (all in flight together); the new token goes straight to smem
+    // ---- A: every load indexed by u (or by the request length, from shared memory) — all in flight together:
+    // the decision, the page IDs it needs (classify / compact_alloc left them in qpid, so no table read),
+    // t_c's significance, t_c's window row, and the new token (straight to shared memory)
     const int r = fdiv(p.div_LyH, u);
     const int8_t st = rc.st[r];
     const int N = rc.len[r];                             // already includes this step's token (compact_alloc)
+    const bool live = st == DKV_REQ_ACTIVE;
     const int4 dw = __ldg(reinterpret_cast<const int4*>(dec) + u);
+    const int2 qp = __ldg(p.qpid + u);
     const float s_in_given = cand_sig ? __ldg(cand_sig + u) : 0.0f;
     stage_row<EPL>(my_nk, knew + (size_t)u * D + q * EPL);
     stage_row<EPL>(my_nv, vnew + (size_t)u * D + q * EPL);
     cp_async_commit();
-    const bool live = st == DKV_REQ_ACTIVE;
-
-    // ---- B: window row of t_c + the unit's table entries
+    uint16_t* wk_row = nullptr;
+    uint16_t* wv_row = nullptr;
+    HVec<EPL> wk, wv;
+    int ws = 0;
+    if (p.W > 0 && live) {
+      ws = fmod_(p.div_W, N - 1);
+      wk_row = reinterpret_cast<uint16_t*>(p.win_k) + ((size_t)u * p.W + ws) * D;
+      wv_row = reinterpret_cast<uint16_t*>(p.win_v) + ((size_t)u * p.W + ws) * D;
+      wk = load_hvec<EPL>(wk_row, q);
+      wv = load_hvec<EPL>(wv_row, q);
+    }
+    // t_c's significance: given, or (NEXT-2, cand_sig NULL) the running mean kept for its window slot
+    const float s_in = cand_sig ? s_in_given : (p.W > 0 && live ? p.win_sig[(size_t)u * p.W + ws] : 0.0f);
     const int pc = N - 1 - p.W;
     const int tc_class = dw.x & 0xFF, v_action = (dw.x >> 8) & 0xFF;
     const int v_slot = dw.y, tc_slot = dw.z, v_dst = dw.w;
@@ -311,27 +324,8 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
     const bool down = live && v_action == DKV_V_DOWN;
     const bool tc_high = tc_class == DKV_CLS_HIGH;
     const int tc_pg = fdiv(tc_high ? p.div_Ch : p.div_Cl, tc_slot);
-    int tix = -1;                                        // lane 0: t_c's page; 1: victim KV_h; 2: victim KV_l
-    if (q == 0 && has_tc) tix = tc_high ? tc_pg : p.L - 1 - tc_pg;
-    if (q == 1 && down) tix = fdiv(p.div_Ch, v_slot);
-    if (q == 2 && down) tix = p.L - 1 - fdiv(p.div_Cl, v_dst);
-    const int pid = tix >= 0 ? __ldg(p.table + (size_t)u * p.L + tix) : 0;
-    uint16_t* wk_row = nullptr;
-    uint16_t* wv_row = nullptr;
-    HVec<EPL> wk, wv;
-    if (p.W > 0 && live) {
-      const int ws = fmod_(p.div_W, N - 1);
-      wk_row = reinterpret_cast<uint16_t*>(p.win_k) + ((size_t)u * p.W + ws) * D;
-      wv_row = reinterpret_cast<uint16_t*>(p.win_v) + ((size_t)u * p.W + ws) * D;
-      wk = load_hvec<EPL>(wk_row, q);
-      wv = load_hvec<EPL>(wv_row, q);
-    }
-    // t_c's significance: given, or (NEXT-2, cand_sig NULL) the running mean kept for its window slot
-    const float s_in = cand_sig ? s_in_given : (p.W > 0 && live ? p.win_sig[(size_t)u * p.W + fmod_(p.div_W, N - 1)] : 0.0f);
-    const int gl = lane & ~(G - 1);
-    const int pid_tc = __shfl_sync(gmask, pid, gl);
-    const int pid_src = __shfl_sync(gmask, pid, gl + 1);
-    const int pid_dst = __shfl_sync(gmask, pid, gl + 2);
+    const int pid_tc = qp.x, pid_src = qp.x, pid_dst = qp.y;   // the victim's KV_h slot is t_c's slot (Q8)
+
 
     // ---- C + 1. downgrade t_v: K8V4 -> K4V2 (Q9)
     if (down) {                                          // group-uniform

@@ -93,6 +93,7 @@ bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
     const bool need = c->q_per_kv > 0 && (GP + 2) * Mp * 4 > kAttSmemLongThreshold;
     Lo.off_att_scratch = take(need ? (int64_t)kAttSlots * (GP + 2) * Mp * 4 : 0);
   }
+  Lo.off_qpid = take(8 * U);
   Lo.off_ring = take(4 * P);
   Lo.off_table = take(4 * U * G.L);
   Lo.off_n_h = take(4 * U);
@@ -237,6 +238,7 @@ dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_
   d.rec = (int32_t*)(b + Lo.off_rec);
   d.win_sig = (float*)(b + Lo.off_win_sig);
   d.secmin = (int32_t*)(b + Lo.off_secmin);
+  d.qpid = (int2*)(b + Lo.off_qpid);
   d.head_alpha = (float*)(b + Lo.off_head_alpha);
   {
     const int64_t GP = (cfg->q_per_kv + 3) / 4 * 4, Mp = (cfg->max_seq_len + 31) / 32 * 32;

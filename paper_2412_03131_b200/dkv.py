@@ -65,7 +65,7 @@ class dkv_layout_t(C.Structure):
                                        "off_score", "off_pos")] + [("off_tile_sums", C.c_int64), ("off_rec", C.c_int64),
                                                                   ("off_win_sig", C.c_int64), ("off_secmin", C.c_int64),
                                                                   ("off_head_alpha", C.c_int64),
-                                                                  ("off_att_scratch", C.c_int64)]
+                                                                  ("off_att_scratch", C.c_int64), ("off_qpid", C.c_int64)]
 
 
 assert C.sizeof(dkv_decision_t) == 16

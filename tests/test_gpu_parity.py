@@ -166,3 +166,27 @@ def test_per_head_thresholds_parity(workflow):
     al = rng.choice([0.0, 0.02, 0.1, 1e30], size=n).astype(np.float32)
     _lifecycle(scn, steps=20, prompt_lens=[300, 64, 200, 17, 450], frees=[(8, [1, 3])], readmit_len=150,
                pages_every=4, head=(ah, al))
+
+
+@pytest.mark.parametrize("path", ["fast", "barrier"])
+def test_many_tiles_lookback_window_parity(path):
+    """the decoupled look-back slides its 32-predecessor window (`look -= 32`) only when more
+    than 33 tiles precede a tile.  U = 12 x 32 x 32 = 12288 units at 256-unit tiles = 48 tiles; the whole ring,
+    both pointers, every table and count compared with the oracle after every call.  "fast": free >= U, the
+    decode scan has no grid barrier; "barrier": a pool tight enough that free < U, so every decode call takes
+    the all-or-nothing barrier path (prefill always does).  Frees of several requests in one step."""
+    base = H.TINY.replace(R=12, Ly=32, H=32, d=64, M=160, W=16, seed=41, tile_units=256)
+    assert base.U // 256 >= 34
+    lens = [40, 24, 56, 33, 17, 48, 60, 29, 44, 36, 52, 20]
+    if path == "fast":
+        scn = base.replace(P=200000)
+    else:
+        probe = H.OracleBackend(base.replace(P=200000))
+        inp, life = H.Inputs(base), H.Lifecycle(base)
+        H.admit([probe], inp, life, list(range(12)), lens)
+        used = 200000 - probe.pool.free
+        scn = base.replace(P=used + base.U // 2)               # free < U from the first decode step
+    o, g, life = _lifecycle(scn, steps=12, prompt_lens=lens, frees=[(3, [2, 7]), (6, [0, 5, 11])],
+                            readmit_len=30, pages_every=5)
+    if path == "barrier":
+        assert o.pool.free < scn.U
