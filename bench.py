@@ -454,6 +454,59 @@ def run_ours(args, rank, world, local):
         e2e_us.append(e0.elapsed_time(e1) * 1e3)
     st, stats = pool.query()
     assert st == 0, f"device status {st} after e2e"
+    seq[active] += args.steps
+
+    # ---------------- CUDA graph: GRAPH_STEPS decode steps captured once (dkv_decode_graph_create) and replayed;
+    # per-step inputs [GRAPH_STEPS][U][d] (840 MB at this config, >> L2) already in HBM.  No L2 flush between the
+    # steps of a replay: it is the steady state of back-to-back decode steps.
+    from paper_2412_03131_b200 import dkv as D
+    GS = 100
+    gsig = torch.empty((GS, wl.U), dtype=torch.float32, device=dev)
+    gk = torch.empty((GS, wl.U, c["d"]), dtype=torch.int16, device=dev)
+    gv = torch.empty_like(gk)
+    for t in range(GS):
+        cand, nk, nv = wl.decode_inputs(seq + t, active)
+        gsig[t].copy_(cand)
+        gk[t].copy_(nk.view(torch.int16))
+        gv[t].copy_(nv.view(torch.int16))
+    gdec = pool.new_decisions()
+    graph_pdl = pool.decode_graph(GS, gsig, gk, gv, gdec, D.DKV_GRAPH_PDL)
+    graph_ev = pool.decode_graph(GS, gsig, gk, gv, gdec, D.DKV_GRAPH_EVENTS)
+    graph_plain = pool.decode_graph(GS, gsig, gk, gv, gdec, 0)
+    graph_us = {}
+    for name, gr in (("pdl", graph_pdl), ("plain", graph_plain)):
+        for rep in range(2):                                 # one untimed replay, one timed
+            flush.zero_()
+            torch.cuda.synchronize()
+            barrier(world)
+            g0, g1 = ev(), ev()
+            torch.cuda._sleep(200_000)
+            g0.record()
+            gr.launch()
+            g1.record()
+            torch.cuda.synchronize()
+            seq[active] += GS
+            launches += 3 * GS if rep else 0
+        graph_us[name] = g0.elapsed_time(g1) * 1e3 / GS
+    flush.zero_()
+    graph_ev.launch()
+    torch.cuda.synchronize()
+    seq[active] += GS
+    kms = graph_ev.kernel_ms() * 1e3                         # [GS][3] us: classify, compact_alloc, quant_write
+    st, _ = pool.query()
+    assert st == 0, f"device status {st} after the graph replays"
+    for gr in (graph_pdl, graph_ev, graph_plain):
+        gr.close()
+    del gsig, gk, gv
+    graph = {"steps_per_graph": GS, "graph_step_us": round(max_over_ranks(graph_us["pdl"], world), 3),
+             "graph_step_us_no_pdl": round(max_over_ranks(graph_us["plain"], world), 3),
+             "in_graph_kernel_us": {nm: {"mean": round(float(kms[:, j].mean()), 3),
+                                         "p50": round(float(np.percentile(kms[:, j], 50)), 3),
+                                         "p99": round(float(np.percentile(kms[:, j], 99)), 3)}
+                                    for j, nm in enumerate(("classify", "compact_alloc", "quant_write"))},
+             "note": "graph_step_us = device time of one replay of a 100-step graph (PDL between kernels) / 100; "
+                     "in_graph_kernel_us from a graph with an event node around every kernel (no PDL); no L2 flush "
+                     "inside a replay (steady state), inputs 840 MB per replay"}
 
     # ---------------- NEXT-2: decode steps driven by the attention kernel's significance
     next2 = None
@@ -635,6 +688,7 @@ def run_ours(args, rank, world, local):
                             "traffic": traffic("classify_decode_kernel"), "traffic_unit": "bytes per launch"},
         "e2e": {"value": round(e2e_mean, 3), "unit": E2E_UNIT,
                 "h2d_bytes_per_step": wl.U * (4 + 2 * 2 * c["d"]), "d2h_bytes_per_step": wl.U * 16},
+        "graph": graph,
         "next2": next2,
         # §8e: the per-step MIN all-reduce of the admission counters (N > 1): its latency on the side stream and
         # the fraction of steps in which it finished inside the step (hidden behind quant_write)

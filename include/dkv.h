@@ -227,6 +227,31 @@ size_t dkv_decode_stage_bytes(dkv_pool_t p);
 dkv_status_t dkv_decode_step_host(dkv_pool_t p, const float* h_sig, const uint16_t* h_kv, dkv_decision_t* h_dec,
                                   void* d_stage, size_t stage_bytes, dkv_stream_t s);
 
+/* The decode step as a CUDA graph (launch-bound inner loop).  Captures `steps` consecutive
+ * decode steps — each dkv_classify(DECODE) -> dkv_compact_alloc -> dkv_quant_write(DECODE), the same kernels and
+ * results as the eager calls — into one CUDA graph replayed by dkv_decode_graph_launch.  Step t reads the
+ * caller's device buffers d_sig + t*sig_step (fp32 [U], or d_sig NULL: significance from the window, NEXT-2),
+ * d_k + t*kv_step and d_v + t*kv_step (fp16 bits [U][d]); a step of 0 reuses one buffer (update it between
+ * launches).  Decisions go to d_dec (device [U]).  The buffers must outlive the graph.  Nothing in the step
+ * depends on host state: a freed request's pages are recycled by the first step after dkv_free (its copies
+ * done by that step's quant_write kernel), and the classify kernel form follows max_seq_len.
+ * flags: DKV_GRAPH_PDL — programmatic dependent launch between the kernels (each kernel's launch and
+ * prologue overlap its predecessor; every kernel waits (griddepcontrol.wait) before reading its predecessor's
+ * output); DKV_GRAPH_EVENTS — an event node around each kernel for per-kernel times
+ * (dkv_decode_graph_kernel_ms: h_ms[steps][3] = classify, compact_alloc, quant_write in ms; disables PDL).
+ * Create: between sequences (DKV_ERR_STATE otherwise); DKV_ERR_CUDA if capture fails.  Launch: between
+ * sequences, with every ACTIVE request at most max_seq_len - steps long (DKV_ERR_STATE otherwise, nothing
+ * enqueued); asynchronous on `s`; the host mirror advances by `steps` steps.  Device errors follow the sticky
+ * status rules above (dkv_pool_query after the launch reports them). */
+typedef struct dkv_graph* dkv_graph_t;
+enum { DKV_GRAPH_PDL = 1, DKV_GRAPH_EVENTS = 2 };
+dkv_status_t dkv_decode_graph_create(dkv_pool_t p, int32_t steps, const float* d_sig, int64_t sig_step,
+                                     const uint16_t* d_k, const uint16_t* d_v, int64_t kv_step, dkv_decision_t* d_dec,
+                                     int32_t flags, dkv_graph_t* out);
+dkv_status_t dkv_decode_graph_launch(dkv_graph_t g, dkv_stream_t s);
+dkv_status_t dkv_decode_graph_kernel_ms(dkv_graph_t g, float* h_ms);
+dkv_status_t dkv_decode_graph_destroy(dkv_graph_t g);
+
 /* Release: host array h_req[0..n) of ACTIVE requests -> PENDING_FREE (double free / not active ->
  * DKV_ERR_STATE).  Allowed between sequences only (after dkv_quant_write, before dkv_classify).  Pages are
  * recycled by the next dkv_compact_alloc; the slot is IDLE (re-admissible) after that call. */

@@ -107,7 +107,25 @@ struct PoolDev {
   int32_t use_head_alpha;   // 1: head_alpha replaces alpha_h / alpha_l
   int32_t prefill_wf;   // dkv_config_t.prefill_workflow
   int2* qpid;           // [U] {t_c's page, downgraded victim's KV_l page} for dkv_quant_write(DECODE)
+  int32_t pdl;          // launch option: 1 = programmatic dependent launch (decode-step CUDA graphs)
 };
+
+// kernel launch with optional programmatic dependent launch (cudaLaunchKernelEx)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                             Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
 
 // ------------------------------------------------------------------------------------- memory ops
 __device__ __forceinline__ int32_t ld_volatile(const int32_t* p) { return *(volatile const int32_t*)p; }
@@ -153,6 +171,14 @@ __device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
 __device__ __forceinline__ void set_status(Ctrl* c, int32_t st) { atomicCAS(&c->status, 0, st); }
 // an error found by a dkv_classify kernel (Q36): merged into `status` by the next dkv_compact_alloc
 __device__ __forceinline__ void set_pending(Ctrl* c, int32_t st) { atomicCAS(&c->pending, 0, st); }
+
+// Programmatic dependent launch (sm_90+): a kernel launched with the programmatic-serialization attribute
+// may start while its predecessor runs; pdl_wait() blocks until the predecessor grid has completed and its
+// writes are visible, pdl_trigger() lets the successor launch.  Both are no-ops without the attribute.  Every
+// kernel of the decode step triggers only after its own wait, so when a kernel starts, the kernel two back
+// has completed: code before pdl_wait() may read anything the immediate predecessor does not write.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ------------------------------------------------------------------------------------- async bulk copies
 // 1-D TMA (cp.async.bulk) global -> shared with mbarrier transaction counting (sm_90+ / sm_100a).
@@ -956,7 +982,6 @@ cudaError_t launch_classify_prefill(const PoolDev& p, int n, const float* sig, i
                                     int max_len, cudaStream_t s);
 cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s,
                                  bool alloc = true, bool defer_recycle = false);
-cudaError_t launch_recycle(const PoolDev& p, const int32_t* req, int n, cudaStream_t s);
 cudaError_t launch_attend(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s);
 size_t attend_smem_bytes(const PoolDev& p, int TS);
 size_t attend_long_smem_bytes(const PoolDev& p);

@@ -51,6 +51,8 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int u = blockIdx.x * kCDWarps + warp;
   if (u >= p.U) return;                                          // whole warps exit together
+  pdl_wait();                                                    // (PDL) the previous quant_write's writes
+  pdl_trigger();
   int32_t* s_pid = s_pid_all + warp * p.L;
 #if DKV_CD_SPEC
   // One round trip for everything u alone addresses: the sticky status (read through L1 — 16k warps reading
@@ -284,8 +286,8 @@ static cudaError_t launch_cd(const PoolDev& p, const float* sig, dkv_decision_t*
     cudaError_t e = cudaFuncSetAttribute(classify_decode_kernel<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  classify_decode_kernel<MINB><<<(p.U + kCDWarps - 1) / kCDWarps, kCDWarps * 32, smem, s>>>(p, sig, dec);
-  return cudaGetLastError();
+  return launch_ex(classify_decode_kernel<MINB>, dim3((p.U + kCDWarps - 1) / kCDWarps), dim3(kCDWarps * 32), smem, s,
+                   p.pdl != 0, p, sig, dec);
 }
 
 // max_len: the longest ACTIVE request (host mirror).  Long sections run the instantiation with the full

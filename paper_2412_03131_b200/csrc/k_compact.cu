@@ -58,15 +58,9 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   // The launch is cooperative (all tiles co-resident), so tiles take their index from blockIdx and the
   // look-back always waits on running or finished tiles.  The call's epoch (status-word tag and barrier
   // target) is ctrl->ticket, which only tile 0 advances, after the barrier every tile crossed having read it.
-  if (tid == 0) s_epoch = *(volatile unsigned long long*)&ctrl->ticket;
-  if (tid == 32) s_start0 = ld_volatile(&ctrl->start);
-  if (tid == 64) s_free0 = ld_volatile(&ctrl->free);
-  if (tid == 96) {                                   // entry status (Q36): sticky status, else classify's error
-    const int a = ld_volatile(&ctrl->status);
-    s_status0 = a != 0 ? a : ld_volatile(&ctrl->pending);
-  }
   const int tile = blockIdx.x;
-  // per-unit loads do not depend on the control block: issue them before the first barrier
+  // per-unit loads do not depend on the control block: issue them before the first barrier; the request
+  // state and counts are not written by dkv_classify, so they may be read before the PDL wait
   const int u = tile * TU + tid;
   int st = -1, r = 0, nh = 0, nl = 0;
   uint32_t dword = 0;
@@ -76,6 +70,17 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
     st = p.req_state[r];
     nh = p.n_h[u];
     nl = p.n_l[u];
+  }
+  pdl_wait();                                        // (PDL) the decisions and classify's pending error
+  pdl_trigger();
+  if (tid == 0) s_epoch = *(volatile unsigned long long*)&ctrl->ticket;
+  if (tid == 32) s_start0 = ld_volatile(&ctrl->start);
+  if (tid == 64) s_free0 = ld_volatile(&ctrl->free);
+  if (tid == 96) {                                   // entry status (Q36): sticky status, else classify's error
+    const int a = ld_volatile(&ctrl->status);
+    s_status0 = a != 0 ? a : ld_volatile(&ctrl->pending);
+  }
+  if (u < p.U) {
     if (phase == DKV_PHASE_DECODE) dword = __ldg(reinterpret_cast<const uint32_t*>(dec + u));
     else { pfh = p.pf_nh[u]; pfl = p.pf_nl[u]; }
   }
@@ -168,7 +173,9 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
     const uint32_t tile_ex = s_exfr;
     const uint32_t Ft = s_incfr - tile_ex;                       // freed slots in this tile
     // deferred: in the decode fast path (grants never read a slot recycled in this call) the copy is left to
-    // recycle_kernel, launched right after; this kernel records each freed unit's offset from the end pointer
+    // the following dkv_quant_write(DECODE) (quant_decode_kernel, over all SMs — here it would run on the one
+    // or two CTAs whose tile holds the request); this kernel records each freed unit's offset from the end
+    // pointer
     const bool defer = defer_rec && phase == DKV_PHASE_DECODE && status0 == 0 && free0 >= (int64_t)p.U;
     if (defer && fr != 0) {
       p.rec[3 * (size_t)u] = (int32_t)off_fr;
@@ -351,11 +358,13 @@ static cudaError_t launch_tu(const PoolDev& p, const dkv_decision_t* dec, int ph
   cfg.blockDim = dim3(TU);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;         // always cooperative: the grid barrier needs co-residency
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;                                    // always cooperative: the grid barrier needs co-residency
+  cfg.numAttrs = p.pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, compact_alloc_kernel<TU>, p, dec, phase, alloc, defer);
 }
 
@@ -381,64 +390,6 @@ int compact_max_coresident(int tile_units) {
   }
   if (e != cudaSuccess) return 0;
   return per * sms;
-}
-
-// ---- deferred recycle copy (decode steps that free requests): one warp per unit of the freed requests,
-// ring[(end0 + off + k) mod P] = table slot k of the unit in canonical slot order (Q13), then the slot is
-// cleared.  Runs right after compact_alloc_kernel recorded {off, ph, freed} per unit in p.rec; a no-op if
-// that call took the barrier path (it then copied in place).
-constexpr int kRecMaxReq = 64;
-struct RecList {
-  int32_t n;
-  int32_t req[kRecMaxReq];
-};
-
-__global__ void __launch_bounds__(256) recycle_kernel(PoolDev p, RecList l) {
-  if (ld_volatile(&p.ctrl->rec_deferred) == 0) return;
-  const int lane = threadIdx.x & 31;
-  const int wu = (blockIdx.x * 256 + threadIdx.x) >> 5;         // index over the freed requests' units
-  if (wu >= l.n * p.LyH) return;
-  const int u = l.req[wu / p.LyH] * p.LyH + wu % p.LyH;
-  const int32_t off = p.rec[3 * (size_t)u], ph = p.rec[3 * (size_t)u + 1], nfr = p.rec[3 * (size_t)u + 2];
-  const int P = p.P, L = p.L;
-  const int64_t ring0 = p.ctrl->rec_end0 + off;                  // < 2P
-  int32_t* row = p.table + (size_t)u * L;
-  for (int k0 = 0; k0 < nfr; k0 += 32 * 8) {
-    int32_t pid[8];
-#pragma unroll
-    for (int j = 0; j < 8; j++) {
-      const int k = k0 + 32 * j + lane;
-      const int slot = k < ph ? k : L - nfr + k;                 // [0, ph) then [L - pl, L)
-      pid[j] = k < nfr ? __ldcg(row + slot) : -1;
-    }
-#pragma unroll
-    for (int j = 0; j < 8; j++) {
-      const int k = k0 + 32 * j + lane;
-      if (k < nfr) {
-        const int slot = k < ph ? k : L - nfr + k;
-        int64_t pos = ring0 + k;                                 // < 3P
-        pos -= pos >= P ? P : 0;
-        pos -= pos >= P ? P : 0;
-        p.ring[pos] = pid[j];
-        int32_t empty = -1;                                      // clear only after the load returned
-        asm volatile("" : "+r"(empty) : "r"(pid[j]));
-        row[slot] = empty;
-      }
-    }
-  }
-}
-
-cudaError_t launch_recycle(const PoolDev& p, const int32_t* req, int n, cudaStream_t s) {
-  for (int i0 = 0; i0 < n; i0 += kRecMaxReq) {
-    RecList l;
-    l.n = n - i0 < kRecMaxReq ? n - i0 : kRecMaxReq;
-    for (int i = 0; i < l.n; i++) l.req[i] = req[i0 + i];
-    const long warps = (long)l.n * p.LyH;
-    recycle_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(p, l);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
 }
 
 }  // namespace dkv

@@ -268,6 +268,46 @@ __device__ __forceinline__ void dequant_lane(const uint4 c, int bits, uint32_t m
   else dequant_lane_ct<EPL, 2>(c, sf, zf, x);
 }
 
+// Deferred recycle copy of one freed unit by its G-lane group (decode steps that free requests):
+// ring[(end0 + off + k) mod P] = table slot k of the unit in canonical slot order (Q13) — slots [0, ph) then
+// [L - pl, L) — and the slot is cleared; {off, ph, freed} were recorded by compact_alloc_kernel in p.rec,
+// whose marker (freed != 0) is consumed here.
+template <int G>
+__device__ __forceinline__ void recycle_unit(const PoolDev& p, int u, int q, unsigned gmask, int64_t end0) {
+  const int32_t nfr = p.rec[3 * (size_t)u + 2];
+  if (nfr == 0) return;                                  // group-uniform
+  const int32_t off = p.rec[3 * (size_t)u], ph = p.rec[3 * (size_t)u + 1];
+  const int P = p.P, L = p.L;
+  const int64_t ring0 = end0 + off;                      // < 2P
+  int32_t* row = p.table + (size_t)u * L;
+  constexpr int kDepth = 8;
+  for (int k0 = 0; k0 < nfr; k0 += G * kDepth) {
+    int32_t pid[kDepth];
+#pragma unroll
+    for (int j = 0; j < kDepth; j++) {
+      const int k = k0 + G * j + q;
+      const int slot = k < ph ? k : L - nfr + k;
+      pid[j] = k < nfr ? __ldcg(row + slot) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < kDepth; j++) {
+      const int k = k0 + G * j + q;
+      if (k < nfr) {
+        const int slot = k < ph ? k : L - nfr + k;
+        int64_t pos = ring0 + k;                         // < 3P: two conditional wraps, no division
+        pos -= pos >= P ? P : 0;
+        pos -= pos >= P ? P : 0;
+        p.ring[pos] = pid[j];
+        int32_t empty = -1;                              // clear only after the load returned (see the header)
+        asm volatile("" : "+r"(empty) : "r"(pid[j]));
+        row[slot] = empty;
+      }
+    }
+  }
+  __syncwarp(gmask);
+  if (q == 0) p.rec[3 * (size_t)u + 2] = 0;
+}
+
 template <int D, int G>
 __global__ void __launch_bounds__(kQDThreads, DKV_QD_MINB)
 quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uint16_t* __restrict__ knew,
@@ -280,24 +320,41 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
   const int lane = threadIdx.x & 31;
   const int q = lane % G;
   const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
-  if (threadIdx.x == 0) s_status = p.ctrl->qw_status;    // entry status (Q36), left by dkv_compact_alloc
+  __shared__ int32_t s_rec;
+  __shared__ int64_t s_end0;
+  pdl_wait();                                            // (PDL) everything below reads what compact_alloc wrote
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    s_status = p.ctrl->qw_status;                        // entry status (Q36), left by dkv_compact_alloc
+    s_rec = ld_volatile(&p.ctrl->rec_deferred);          // compact_alloc left this step's recycle copies to us
+    s_end0 = ld_volatile(&p.ctrl->rec_end0);
+  }
   const ReqCache rc = load_req_cache(p, qd_smem);
   __syncthreads();
-  if (s_status != 0) return;                             // error at entry: no-op
+  const bool dead = s_status != 0;                       // error at entry: no quantization, no window push
+  const bool rec_on = s_rec != 0;
+  if (dead && !rec_on) return;
   uint16_t* const my_nk = &s_new[0][threadIdx.x * EPL];
   uint16_t* const my_nv = &s_new[1][threadIdx.x * EPL];
 
   for (int ub = blockIdx.x; u0 + ub * UPC < u1; ub += gridDim.x) {   // units [u0, u1)
     const int u = u0 + ub * UPC + threadIdx.x / G;
     if (u >= u1) break;                                  // whole groups leave together (last block only)
+    const int r = fdiv(p.div_LyH, u);
+    const int8_t st = rc.st[r];
+    const bool live = st == DKV_REQ_ACTIVE;
+    if (!live) {
+      // a unit of a request this step's dkv_compact_alloc recycled without copying (decode fast path): its
+      // page IDs go to the ring here, at the offsets the scan assigned (Q13 order), and its slots are cleared
+      if (rec_on) recycle_unit<G>(p, u, q, gmask, s_end0);
+      continue;
+    }
+    if (dead) continue;
 
     // ---- A: every load indexed by u (or by the request length, from shared memory) — all in flight together:
     // the decision, the page IDs it needs (classify / compact_alloc left them in qpid, so no table read),
     // t_c's significance, t_c's window row, and the new token (straight to shared memory)
-    const int r = fdiv(p.div_LyH, u);
-    const int8_t st = rc.st[r];
     const int N = rc.len[r];                             // already includes this step's token (compact_alloc)
-    const bool live = st == DKV_REQ_ACTIVE;
     const int4 dw = __ldg(reinterpret_cast<const int4*>(dec) + u);
     const int2 qp = __ldg(p.qpid + u);
     const float s_in_given = cand_sig ? __ldg(cand_sig + u) : 0.0f;
@@ -399,8 +456,8 @@ static cudaError_t launch_qd(const PoolDev& p, const dkv_decision_t* dec, const 
   if (cap == 0) return cudaErrorUnknown;
   if (u1 <= u0) return cudaSuccess;
   const int need = (u1 - u0 + units_per_cta - 1) / units_per_cta;
-  quant_decode_kernel<D, G><<<need < cap ? need : cap, kQDThreads, smem, s>>>(p, dec, k, v, sig, u0, u1);
-  return cudaGetLastError();
+  return launch_ex(quant_decode_kernel<D, G>, dim3(need < cap ? need : cap), dim3(kQDThreads), smem, s, p.pdl != 0, p,
+                   dec, k, v, sig, u0, u1);
 }
 
 cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,

@@ -354,16 +354,12 @@ dkv_status_t dkv_compact_alloc(dkv_pool_t p, const dkv_decision_t* d_dec, dkv_st
     e = launch_compact_alloc(p->dev, d_dec, p->phase, (cudaStream_t)s, /*alloc=*/false);
     if (e == cudaSuccess) e = launch_prefill_conservative(p->dev, (cudaStream_t)s);
   } else {
-    // decode steps that recycle finished requests: the scan kernel only records each freed unit's ring
-    // offset, and a second, wide kernel copies the page IDs (one warp per freed unit, all SMs) — the copy
-    // would otherwise run on the one or two CTAs whose tile holds the request
-    std::vector<int32_t> freed;
-    if (p->phase == DKV_PHASE_DECODE)
-      for (int r = 0; r < p->cfg.max_requests; r++)
-        if (p->req_state[r] == DKV_REQ_PENDING_FREE) freed.push_back(r);
-    e = launch_compact_alloc(p->dev, d_dec, p->phase, (cudaStream_t)s, /*alloc=*/true, !freed.empty());
-    if (e == cudaSuccess && !freed.empty())
-      e = launch_recycle(p->dev, freed.data(), (int)freed.size(), (cudaStream_t)s);
+    // decode steps that recycle finished requests: in the fast path the scan kernel only records each freed
+    // unit's ring offset and the following dkv_quant_write(DECODE) copies the page IDs over all SMs (inside
+    // this kernel the copy would run on the one or two CTAs whose tile holds the request).  Nothing here
+    // depends on the host mirror, so the step can be captured in a CUDA graph (dkv_decode_graph_create).
+    e = launch_compact_alloc(p->dev, d_dec, p->phase, (cudaStream_t)s, /*alloc=*/true,
+                             /*defer_recycle=*/p->phase == DKV_PHASE_DECODE);
   }
   if (e != cudaSuccess) return DKV_ERR_CUDA;
   const int R = p->cfg.max_requests;
@@ -554,6 +550,107 @@ dkv_status_t dkv_decode_step_host(dkv_pool_t p, const float* h_sig, const uint16
   if (r != DKV_OK) return r;
   if (h_dec && cudaMemcpyAsync(h_dec, d_dec, U * sizeof(dkv_decision_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
     return DKV_ERR_CUDA;
+  return DKV_OK;
+}
+
+// ---- the decode step as a CUDA graph (dkv.h: dkv_decode_graph_*)
+struct dkv_graph {
+  dkv_pool* pool;
+  int32_t steps, flags;
+  cudaStream_t cap;                  // capture stream (library-owned)
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  std::vector<cudaEvent_t> ev;       // DKV_GRAPH_EVENTS: [steps][4] boundaries of classify / compact / quant
+};
+
+dkv_status_t dkv_decode_graph_destroy(dkv_graph_t g) {
+  if (!g) return DKV_ERR_INVALID_ARG;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  if (g->cap) cudaStreamDestroy(g->cap);
+  for (cudaEvent_t e : g->ev)
+    if (e) cudaEventDestroy(e);
+  delete g;
+  return DKV_OK;
+}
+
+dkv_status_t dkv_decode_graph_create(dkv_pool_t p, int32_t steps, const float* d_sig, int64_t sig_step,
+                                     const uint16_t* d_k, const uint16_t* d_v, int64_t kv_step, dkv_decision_t* d_dec,
+                                     int32_t flags, dkv_graph_t* out) {
+  if (!out) return DKV_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!p || steps < 1 || !d_k || !d_v || !d_dec || sig_step < 0 || kv_step < 0 || (flags & ~3)) return DKV_ERR_INVALID_ARG;
+  if (p->seq != SEQ_IDLE) return DKV_ERR_STATE;
+  dkv_graph* g = new dkv_graph();
+  g->pool = p; g->steps = steps; g->flags = flags;
+  g->cap = nullptr; g->graph = nullptr; g->exec = nullptr;
+  const bool events = (flags & DKV_GRAPH_EVENTS) != 0;
+  PoolDev d = p->dev;
+  d.pdl = ((flags & DKV_GRAPH_PDL) && !events) ? 1 : 0;    // event nodes between kernels would break the PDL edges
+  if (cudaStreamCreateWithFlags(&g->cap, cudaStreamNonBlocking) != cudaSuccess) {
+    dkv_decode_graph_destroy(g);
+    return DKV_ERR_CUDA;
+  }
+  if (events) {
+    g->ev.assign((size_t)steps * 4, nullptr);
+    for (cudaEvent_t& e : g->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) { dkv_decode_graph_destroy(g); return DKV_ERR_CUDA; }
+  }
+  const size_t U = (size_t)p->G.U, D = (size_t)p->cfg.head_dim;
+  // the classify instantiation cannot follow the longest active request inside a graph: it follows max_seq_len
+  const int max_len = p->cfg.max_seq_len;
+  cudaError_t e = cudaStreamBeginCapture(g->cap, cudaStreamCaptureModeThreadLocal);
+  for (int32_t t = 0; t < steps && e == cudaSuccess; t++) {
+    const float* sig = d_sig ? d_sig + (size_t)t * (size_t)sig_step : nullptr;
+    const uint16_t* k = d_k + (size_t)t * (size_t)kv_step;
+    const uint16_t* v = d_v + (size_t)t * (size_t)kv_step;
+    cudaEvent_t* ev = events ? &g->ev[4 * (size_t)t] : nullptr;
+    if (ev) e = cudaEventRecordWithFlags(ev[0], g->cap, cudaEventRecordExternal);
+    if (e == cudaSuccess) e = launch_classify_decode(d, sig, d_dec, max_len, g->cap);
+    if (e == cudaSuccess && ev) e = cudaEventRecordWithFlags(ev[1], g->cap, cudaEventRecordExternal);
+    if (e == cudaSuccess) e = launch_compact_alloc(d, d_dec, DKV_PHASE_DECODE, g->cap, true, true);
+    if (e == cudaSuccess && ev) e = cudaEventRecordWithFlags(ev[2], g->cap, cudaEventRecordExternal);
+    if (e == cudaSuccess) e = launch_quant_decode(d, d_dec, k, v, sig, g->cap);
+    if (e == cudaSuccess && ev) e = cudaEventRecordWithFlags(ev[3], g->cap, cudaEventRecordExternal);
+  }
+  const cudaError_t e2 = cudaStreamEndCapture(g->cap, &g->graph);
+  if (e == cudaSuccess) e = e2;
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+  (void)U; (void)D;
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    dkv_decode_graph_destroy(g);
+    return DKV_ERR_CUDA;
+  }
+  *out = g;
+  return DKV_OK;
+}
+
+dkv_status_t dkv_decode_graph_launch(dkv_graph_t g, dkv_stream_t s) {
+  if (!g) return DKV_ERR_INVALID_ARG;
+  dkv_pool* p = g->pool;
+  if (p->seq != SEQ_IDLE) return DKV_ERR_STATE;
+  // every step's dkv_classify needs the ACTIVE requests below max_seq_len
+  for (int r = 0; r < p->cfg.max_requests; r++)
+    if (p->req_state[r] == DKV_REQ_ACTIVE && p->seq_len[r] + g->steps > p->cfg.max_seq_len) return DKV_ERR_STATE;
+  if (cudaGraphLaunch(g->exec, (cudaStream_t)s) != cudaSuccess) return DKV_ERR_CUDA;
+  // the host mirror after `steps` decode steps: the first step recycles the freed requests
+  for (int r = 0; r < p->cfg.max_requests; r++) {
+    if (p->req_state[r] == DKV_REQ_PENDING_FREE) { p->req_state[r] = DKV_REQ_IDLE; p->seq_len[r] = 0; }
+    else if (p->req_state[r] == DKV_REQ_ACTIVE) p->seq_len[r] += g->steps;
+  }
+  p->phase = DKV_PHASE_DECODE;
+  p->recovering = false;
+  return DKV_OK;
+}
+
+dkv_status_t dkv_decode_graph_kernel_ms(dkv_graph_t g, float* h_ms) {
+  if (!g || !h_ms || !(g->flags & DKV_GRAPH_EVENTS)) return DKV_ERR_INVALID_ARG;
+  for (int32_t t = 0; t < g->steps; t++)
+    for (int k = 0; k < 3; k++)
+      if (cudaEventElapsedTime(&h_ms[3 * (size_t)t + k], g->ev[4 * (size_t)t + k], g->ev[4 * (size_t)t + k + 1]) !=
+          cudaSuccess)
+        return DKV_ERR_CUDA;
   return DKV_OK;
 }
 

@@ -27,7 +27,8 @@ DKV_REQ_IDLE, DKV_REQ_ADMITTING, DKV_REQ_ACTIVE, DKV_REQ_PENDING_FREE = 0, 1, 2,
 EXPORTED = ("dkv_arena_bytes", "dkv_pool_layout", "dkv_pool_init", "dkv_pool_destroy", "dkv_classify",
             "dkv_compact_alloc", "dkv_quant_write", "dkv_free", "dkv_pool_query", "dkv_pool_stats_device_ptr",
             "dkv_status_string", "dkv_attend", "dkv_set_head_thresholds", "dkv_decode_stage_bytes",
-            "dkv_decode_step_host")
+            "dkv_decode_step_host", "dkv_decode_graph_create", "dkv_decode_graph_launch",
+            "dkv_decode_graph_kernel_ms", "dkv_decode_graph_destroy")
 
 
 class DkvError(RuntimeError):
@@ -96,11 +97,16 @@ _lib.dkv_decode_stage_bytes.restype = C.c_size_t
 _lib.dkv_decode_step_host.argtypes = [_vp, _vp, _vp, _vp, _vp, C.c_size_t, _vp]
 _lib.dkv_pool_stats_device_ptr.argtypes = [_vp]
 _lib.dkv_pool_stats_device_ptr.restype = _vp
+_lib.dkv_decode_graph_create.argtypes = [_vp, C.c_int32, _vp, C.c_int64, _vp, _vp, C.c_int64, _vp, C.c_int32, _P(_vp)]
+_lib.dkv_decode_graph_launch.argtypes = [_vp, _vp]
+_lib.dkv_decode_graph_kernel_ms.argtypes = [_vp, _vp]
+_lib.dkv_decode_graph_destroy.argtypes = [_vp]
 _lib.dkv_status_string.argtypes = [C.c_int32]
 _lib.dkv_status_string.restype = C.c_char_p
 for _f in ("dkv_pool_layout", "dkv_pool_init", "dkv_pool_destroy", "dkv_classify", "dkv_compact_alloc",
            "dkv_quant_write", "dkv_free", "dkv_pool_query", "dkv_attend", "dkv_set_head_thresholds",
-           "dkv_decode_step_host"):
+           "dkv_decode_step_host", "dkv_decode_graph_create", "dkv_decode_graph_launch", "dkv_decode_graph_kernel_ms",
+           "dkv_decode_graph_destroy"):
     getattr(_lib, _f).restype = C.c_int32
 
 
@@ -220,6 +226,30 @@ def _hostp(x):
 def dkv_decode_step_host(pool, h_sig, h_kv, h_dec, d_stage, stage_bytes, stream=None) -> int:
     return _check("dkv_decode_step_host", _lib.dkv_decode_step_host(pool, _hostp(h_sig), _hostp(h_kv), _hostp(h_dec),
                                                                     _dev(d_stage), stage_bytes, _stream(stream)))
+
+
+DKV_GRAPH_PDL, DKV_GRAPH_EVENTS = 1, 2
+
+
+def dkv_decode_graph_create(pool, steps, d_sig, sig_step, d_k, d_v, kv_step, d_dec, flags) -> int:
+    h = _vp()
+    _check("dkv_decode_graph_create", _lib.dkv_decode_graph_create(pool, steps, _dev(d_sig), sig_step, _dev(d_k),
+                                                                   _dev(d_v), kv_step, _dev(d_dec), flags, C.byref(h)))
+    return h.value
+
+
+def dkv_decode_graph_launch(graph, stream=None) -> int:
+    return _check("dkv_decode_graph_launch", _lib.dkv_decode_graph_launch(graph, _stream(stream)))
+
+
+def dkv_decode_graph_kernel_ms(graph, steps) -> np.ndarray:
+    out = np.zeros((steps, 3), np.float32)
+    _check("dkv_decode_graph_kernel_ms", _lib.dkv_decode_graph_kernel_ms(graph, out.ctypes.data_as(_vp)))
+    return out
+
+
+def dkv_decode_graph_destroy(graph) -> int:
+    return _check("dkv_decode_graph_destroy", _lib.dkv_decode_graph_destroy(graph))
 
 
 def dkv_free(pool, h_req, n, stream=None) -> int:

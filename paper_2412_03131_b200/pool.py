@@ -60,6 +60,16 @@ class Pool:
         return _d.dkv_decode_step_host(self.handle, h_sig, h_kv, h_dec, self._stage, self._stage_bytes,
                                        stream or self.stream)
 
+    def decode_graph(self, steps, sig, k, v, dec, flags=_d.DKV_GRAPH_PDL):
+        """dkv_decode_graph_create: `steps` decode steps captured as one CUDA graph.  sig fp32 [steps][U] (or
+        [U] reused, or None: window significance), k / v int16 [steps][U][d] (or [U][d] reused), dec int32
+        [U][4]: CUDA tensors that must outlive the graph.  Returns a DecodeGraph."""
+        U, d = self.U, self.cfg.head_dim
+        sig_step = U if (sig is not None and sig.dim() == 2) else 0
+        kv_step = U * d if k.dim() == 3 else 0
+        h = _d.dkv_decode_graph_create(self.handle, steps, sig, sig_step, k, v, kv_step, dec, flags)
+        return DecodeGraph(h, steps, (sig, k, v, dec))
+
     def quant_write_prefill(self, k, v, sig, stream=None):
         return _d.dkv_quant_write(self.handle, _d.DKV_PHASE_PREFILL, None, k, v, k.shape[-2], sig, sig.shape[-1],
                                   stream or self.stream)
@@ -112,6 +122,31 @@ class Pool:
         return {c: dict(C=L.C[c], kbits=bits[c][0], vbits=bits[c][1], k_row=L.k_row[c], v_row=L.v_row[c], off_k=L.off_k[c], off_kmeta=L.off_kmeta[c],
                         off_v=L.off_v[c], off_vmeta=L.off_vmeta[c], off_score=L.off_score[c], off_pos=L.off_pos[c])
                 for c in (1, 2)}
+
+
+class DecodeGraph:
+    """A captured decode-step graph (keeps its buffers alive); launch() replays it on the current stream."""
+
+    def __init__(self, handle, steps, buffers):
+        self.handle, self.steps, self._buffers = handle, steps, buffers
+
+    def launch(self, stream=None):
+        return _d.dkv_decode_graph_launch(self.handle, stream)
+
+    def kernel_ms(self):
+        """[steps][3] classify / compact_alloc / quant_write ms of the last replay (DKV_GRAPH_EVENTS graphs)"""
+        return _d.dkv_decode_graph_kernel_ms(self.handle, self.steps)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _d.dkv_decode_graph_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def decisions_to_numpy(dec: torch.Tensor) -> np.ndarray:

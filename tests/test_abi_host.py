@@ -83,6 +83,13 @@ def test_no_device_fails_loudly(D):
     assert D.lib().dkv_decode_stage_bytes(None) == 0
     buf = (C.c_uint16 * 8)()
     assert D.lib().dkv_decode_step_host(None, None, buf, None, C.c_void_p(1 << 20), 1 << 20, None) == D.DKV_ERR_INVALID_ARG
+    # the decode-graph calls reject a NULL handle / output without touching CUDA
+    g = C.c_void_p()
+    assert D.lib().dkv_decode_graph_create(None, 1, None, 0, buf, buf, 0, buf, 0, C.byref(g)) == D.DKV_ERR_INVALID_ARG
+    assert not g.value
+    assert D.lib().dkv_decode_graph_launch(None, None) == D.DKV_ERR_INVALID_ARG
+    assert D.lib().dkv_decode_graph_kernel_ms(None, buf) == D.DKV_ERR_INVALID_ARG
+    assert D.lib().dkv_decode_graph_destroy(None) == D.DKV_ERR_INVALID_ARG
 
 
 def test_status_strings(D):
