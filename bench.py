@@ -516,53 +516,66 @@ def run_ours(args, rank, world, local):
         gen.manual_seed(c["seed"] + rank)
         qbuf = torch.empty((wl.U, G, d), dtype=torch.float16, device=dev)
         obuf = torch.empty((wl.U, G, d), dtype=torch.float32, device=dev)
-        att_us, cls2_us, step2_us, att_bytes, att_flops = [], [], [], [], []
         v = pool.views()
         qbuf.normal_(generator=gen)
         pool.attend(qbuf.view(torch.int16), obuf)                 # primes the window significance + minima
-        for s in range(args.warmup + args.steps):
-            timed = s >= args.warmup
-            cand, nk, nv = wl.decode_inputs(seq, active)
-            qbuf.normal_(generator=gen)
-            nh0, nl0 = v["n_h"].clone(), v["n_l"].clone()
-            flush.zero_()
-            torch.cuda.synchronize()
-            barrier(world)
-            e = [ev() for _ in range(5)]
-            torch.cuda._sleep(200_000)
-            e[0].record()
-            pool.classify_decode(None, dec)
-            e[1].record()
-            pool.compact_alloc(dec)
-            e[2].record()
-            pool.quant_write_decode(dec, nk.view(torch.int16), nv.view(torch.int16), None)
-            e[3].record()
-            pool.attend(qbuf.view(torch.int16), obuf)
-            e[4].record()
-            torch.cuda.synchronize()
-            seq[active] += 1
-            if timed:
-                cls2_us.append(e[0].elapsed_time(e[1]) * 1e3)
-                att_us.append(e[3].elapsed_time(e[4]) * 1e3)
-                step2_us.append(e[0].elapsed_time(e[4]) * 1e3)
-                launches += 4
-                # algorithmic bytes of one attention pass: every stored token's K/V codes, metadata, position and
-                # score (read + write back), every window token's fp16 K/V and significance (read + write),
-                # the queries and the output
-                nh1, nl1 = v["n_h"].long(), v["n_l"].long()
-                gh_, gl_ = geom[1], geom[2]
-                per_h = gh_["k_row"] + gh_["v_row"] + 8 + 4 + 4 + 4
-                per_l = gl_["k_row"] + gl_["v_row"] + 8 + 4 + 4 + 4
-                nwin = min(c["W"], int(seq.max()))
-                att_bytes.append(int((nh1.sum() * per_h + nl1.sum() * per_l).item())
-                                 + wl.U * (nwin * (4 * d + 8) + G * d * 2 + G * d * 4))
-                # algorithmic fp32 flops (Q31/Q32 arithmetic): per token the G logit and G output fma chains over
-                # d elements (2 G d fma); a stored token's key and value dequantization adds 2 d fma
-                n_stored = int((nh1.sum() + nl1.sum()).item())
-                n_win = wl.U * nwin
-                att_flops.append(2 * ((n_stored + n_win) * 2 * G * d + n_stored * 2 * d))
-        st, _ = pool.query()
-        assert st == 0, f"device status {st} after the NEXT-2 steps"
+
+        def run_next2(attend_fn):
+            nonlocal launches
+            att_us, cls2_us, step2_us, att_bytes, att_flops = [], [], [], [], []
+            for s in range(args.warmup + args.steps):
+                timed = s >= args.warmup
+                cand, nk, nv = wl.decode_inputs(seq, active)
+                qbuf.normal_(generator=gen)
+                flush.zero_()
+                torch.cuda.synchronize()
+                barrier(world)
+                e = [ev() for _ in range(5)]
+                torch.cuda._sleep(200_000)
+                e[0].record()
+                pool.classify_decode(None, dec)
+                e[1].record()
+                pool.compact_alloc(dec)
+                e[2].record()
+                pool.quant_write_decode(dec, nk.view(torch.int16), nv.view(torch.int16), None)
+                e[3].record()
+                attend_fn(qbuf.view(torch.int16), obuf)
+                e[4].record()
+                torch.cuda.synchronize()
+                seq[active] += 1
+                if timed:
+                    cls2_us.append(e[0].elapsed_time(e[1]) * 1e3)
+                    att_us.append(e[3].elapsed_time(e[4]) * 1e3)
+                    step2_us.append(e[0].elapsed_time(e[4]) * 1e3)
+                    launches += 4
+                    # algorithmic bytes of one attention pass: every stored token's K/V codes, metadata, position and
+                    # score (read + write back), every window token's fp16 K/V and significance (read + write),
+                    # the queries and the output
+                    nh1, nl1 = v["n_h"].long(), v["n_l"].long()
+                    gh_, gl_ = geom[1], geom[2]
+                    per_h = gh_["k_row"] + gh_["v_row"] + 8 + 4 + 4 + 4
+                    per_l = gl_["k_row"] + gl_["v_row"] + 8 + 4 + 4 + 4
+                    nwin = min(c["W"], int(seq.max()))
+                    att_bytes.append(int((nh1.sum() * per_h + nl1.sum() * per_l).item())
+                                     + wl.U * (nwin * (4 * d + 8) + G * d * 2 + G * d * 4))
+                    # algorithmic flops: per token the G logit and G output dot products over d elements (2 G d
+                    # fma); a stored token's key and value dequantization adds 2 d fma
+                    n_stored = int((nh1.sum() + nl1.sum()).item())
+                    n_win = wl.U * nwin
+                    att_flops.append(2 * ((n_stored + n_win) * 2 * G * d + n_stored * 2 * d))
+            st, _ = pool.query()
+            assert st == 0, f"device status {st} after the NEXT-2 steps"
+            return att_us, cls2_us, step2_us, att_bytes, att_flops
+
+        att_us, cls2_us, step2_us, att_bytes, att_flops = run_next2(lambda q_, o_: pool.attend(q_, o_))
+        tc_us, tc_cls_us, tc_step_us, tc_bytes, _ = run_next2(lambda q_, o_: pool.attend_tc(q_, o_))
+        tc_mean = max_over_ranks(statistics.mean(tc_us), world)
+        tc_gbs = statistics.mean(tc_bytes) / (statistics.mean(tc_us) * 1e-6) / 1e9
+        # the same batch's KV as FP16 (2 x d x 2 bytes per stored or window token) read at the measured HBM peak: the
+        # time an FP16 attention needs at roofline (the paper's comparison)
+        fp16_bytes = (int((v["n_h"].long().sum() + v["n_l"].long().sum()).item())
+                      + wl.U * min(c["W"], int(seq.max()))) * 4 * d
+        fp16_us = fp16_bytes / (load_peaks()[0] * 1e9) * 1e6
         att_mean = max_over_ranks(statistics.mean(att_us), world)
         att_gbs = statistics.mean(att_bytes) / (statistics.mean(att_us) * 1e-6) / 1e9
         next2 = {"attend_us": round(att_mean, 1), "attend_gbs": round(att_gbs, 1),
@@ -586,6 +599,19 @@ def run_ours(args, rank, world, local):
                                       "instruction issue (ncu: profiles/*prof_attend*)"},
                  "note": "dkv_attend (NEXT-2) supplies significance; classify takes its victims from the "
                          "attention kernel's section minima (no scan)"}
+        next2["tc"] = {"kernel": "attend_tc_kernel (dkv_attend_tc: mma.sync on the integer codes, fp32 accumulation)",
+                       "attend_us": round(tc_mean, 1),
+                       "classify_fused_us": round(max_over_ranks(statistics.mean(tc_cls_us), world), 3),
+                       "step_us": round(max_over_ranks(statistics.mean(tc_step_us), world), 1),
+                       "manager_share_of_step": round(1.0 - statistics.mean(tc_us) / statistics.mean(tc_step_us), 4),
+                       "roofline": {"bound": "hbm", "achieved": round(tc_gbs, 1), "peak": load_peaks()[0],
+                                    "unit": "GB/s", "frac": round(tc_gbs / load_peaks()[0], 4),
+                                    "algorithmic_bytes": int(statistics.mean(tc_bytes)),
+                                    "traffic": load_traffic()("attend_tc_kernel"), "traffic_unit": "bytes per launch"},
+                       "fp16_attention_at_roofline_us": round(fp16_us, 1),
+                       "speedup_vs_fp16_roofline": round(fp16_us / statistics.mean(tc_us), 3),
+                       "note": "FP16 reference: the same tokens' K and V as fp16 (4 d bytes each) read at the measured "
+                               "HBM peak; the paper reports 1.7x for K8V8 over FP16 (P:896-900)"}
 
     # ---------------- recycle micro-benchmark: free 1 / 8 / 32 requests, then one decode step whose
     # dkv_compact_alloc recycles all their pages (~37k / 300k / 1.2M page IDs at this config)

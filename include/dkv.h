@@ -203,6 +203,16 @@ dkv_status_t dkv_quant_write(dkv_pool_t p, int32_t phase, const dkv_decision_t* 
  * then read from the window. */
 dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* d_probs, dkv_stream_t s);
 
+/* NEXT-2 on tensor cores — the same operation as dkv_attend (Eq. 1 with GQA max, the running-mean significance
+ * written back, the section minima for the next dkv_classify), computed with mma.sync tensor-core contractions on
+ * the integer codes: logit = (s * q.codes + z * sum(q)) / sqrt(d), out = sum_t (a s) codes + sum_t a z, fp32
+ * accumulation, the window on CUDA cores.  Not bit-identical to dkv_attend / the oracle: results agree with
+ * Eq. 1 evaluated in float64 to the tolerances of tests/test_gpu_attention_tc.py (outputs rtol 2e-4 / atol 2e-5,
+ * scores rtol 2e-5 / atol 1e-7); the section minima are exact for the significance values it writes.  Same
+ * arguments and errors as dkv_attend.  Falls back to dkv_attend when the longest active request's logits do not
+ * fit in shared memory or a class's pages are not whole 16-token tiles. */
+dkv_status_t dkv_attend_tc(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* d_probs, dkv_stream_t s);
+
 /* NEXT-4 — per-head thresholds ("a shared set of thresholds for all attention heads" is the
  * paper's choice; per-head thresholds its stated extension; reading Q35).  h_alpha_h / h_alpha_l: host
  * arrays of num_layers * num_kv_heads finite values >= 0 in (layer, this pool's head) order; unit u uses

@@ -982,9 +982,13 @@ cudaError_t launch_classify_prefill(const PoolDev& p, int n, const float* sig, i
                                     int max_len, cudaStream_t s);
 cudaError_t launch_compact_alloc(const PoolDev& p, const dkv_decision_t* dec, int phase, cudaStream_t s,
                                  bool alloc = true, bool defer_recycle = false);
+cudaError_t launch_recycle(const PoolDev& p, const int32_t* req, int n, cudaStream_t s);
 cudaError_t launch_attend(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s);
 size_t attend_smem_bytes(const PoolDev& p, int TS);
 size_t attend_long_smem_bytes(const PoolDev& p);
+cudaError_t launch_attend_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s);
+size_t attend_tc_smem_bytes(const PoolDev& p, int TS);
+bool attend_tc_supported(const PoolDev& p);
 cudaError_t launch_prefill_conservative(const PoolDev& p, cudaStream_t s);
 // units [u0, u1) (u1 < 0: all U)
 cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,

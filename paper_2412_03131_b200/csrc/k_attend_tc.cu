@@ -1,0 +1,549 @@
+// k_attend_tc.cu — NEXT-2 on tensor cores: decode attention over the compressed cache (Eq. 1; GQA
+// score = max over the group), the running-mean significance update (Q33/Q34) and the section
+// minima for the next dkv_classify, with the two contractions (QK^T, PV) on the tensor cores
+// (mma.sync.m16n8k16, fp32 accumulation).  Behind dkv_attend_tc; the exact path (k_attend.cu, bit-identical to
+// the oracle) stays the parity mode.
+//
+// The contractions are taken on the integer codes, not on dequantized values, so the tensor-core operands are
+// exact and only fp32 accumulation rounds:
+//   logit(t, h) = (s_t * sum_f q_hf code_tf + z_t * sum_f q_hf) / sqrt(d)       (X^ = s*Q + z)
+//   out(h, f)   = sum_t (a_ht s_t) code_tf + sum_t a_ht z_t
+// Codes are < 2^8, so they are exact in fp16 and bf16; the queries are fp16 inputs (exact); a_ht s_t is an fp32
+// value split into bf16 hi + lo (16 significant bits, two MMAs).  The FP16 window (<= W tokens) runs on CUDA
+// cores in fp32.
+//
+// One CTA per unit (the paper's "one thread block per head"), kTcWarps warps; pages go round-robin to
+// the warps, high pages first, then low, each staged into shared memory by per-thread 16-B cp.async
+// copies (two stages per warp).  The MMA fragments are read straight from the staged code rows; the paper's
+// tiled K/V layouts (NEXT-3) exist to make per-thread vector loads coalesce in global memory — here
+// whole page segments are copied (contiguous 1-2 KB runs, coalesced by construction) and the tiling happens in
+// shared memory: a 16-B XOR swizzle of each code row so that the fragment reads are bank-conflict free, and a
+// permutation of the MMA k index (k = 2j, 2j+1, 2j+8, 2j+9 <-> features / tokens 4j .. 4j+3) so that a thread's
+// four codes are adjacent in a row.
+//   phase 1: logits of every token (stored pages by MMA, window on CUDA cores) into shared memory;
+//   phase 2: per-head max, p = exp(l - max), Z (order-free fp32 sums);
+//   phase 3: PV by MMA page by page with a = p / Z, the significance of each stored token (page score
+//            segments) and window token, the section minima; the warps' partial outputs are added in a fixed
+//            order (deterministic for a given launch).
+#include <cuda_bf16.h>
+
+#include "dkv_internal.cuh"
+
+namespace dkv {
+
+constexpr int kTcWarps = 4;
+constexpr int kTcThreads = kTcWarps * 32;
+constexpr int kTcStages = 2;
+constexpr int kTcStage = 2304;                 // bytes per warp per stage: >= C*k_row + 4C and C*v_row + 12C
+
+__device__ __forceinline__ void mma_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// two integer codes (< 1024) -> fp16x2 {c0, c1} exactly: 0x6400 | c = 1024 + c, minus 1024
+__device__ __forceinline__ uint32_t h2_codes(uint32_t c0, uint32_t c1) {
+  const uint32_t w = c0 | (c1 << 16) | 0x64006400u;
+  const __half2 r = __hsub2(*reinterpret_cast<const __half2*>(&w), __halves2half2(__ushort_as_half(0x6400), __ushort_as_half(0x6400)));
+  return *reinterpret_cast<const uint32_t*>(&r);
+}
+// two integer codes (< 256) -> bf16x2 exactly: 0x4300 | c = 128 + c, minus 128
+__device__ __forceinline__ uint32_t bf2_codes(uint32_t c0, uint32_t c1) {
+  const uint32_t w = c0 | (c1 << 16) | 0x43004300u;
+  const uint32_t k = 0x43004300u;
+  const __nv_bfloat162 r = __hsub2(*reinterpret_cast<const __nv_bfloat162*>(&w), *reinterpret_cast<const __nv_bfloat162*>(&k));
+  return *reinterpret_cast<const uint32_t*>(&r);
+}
+// fp32 pair -> bf16x2 hi parts and the bf16x2 of the remainders (x = hi + lo to 16 significant bits)
+__device__ __forceinline__ void bf2_split(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+  const float2 hf = __bfloat1622float2(h);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+// 16-B chunk swizzle of a staged code row: chunk c of row `row` sits at chunk c ^ ((row >> sh) & (kc - 1))
+__device__ __forceinline__ int swz(int row, int c, int sh, int kc) { return c ^ ((row >> sh) & (kc - 1)); }
+
+struct TcGeom {
+  int C, kbits, vbits, k_row, v_row, off_k, off_kmeta, off_v, off_vmeta, off_score, off_pos;
+  int kc, ksh, vc, vsh;                        // chunks per code row and swizzle shifts (K, V)
+};
+__device__ __forceinline__ int ilog2(int x) { return 31 - __clz(x); }
+__device__ __forceinline__ TcGeom tc_geom(const ClassGeom& g) {
+  TcGeom t;
+  t.C = g.C; t.kbits = g.kbits; t.vbits = g.vbits; t.k_row = g.k_row; t.v_row = g.v_row;
+  t.off_k = g.off_k; t.off_kmeta = g.off_kmeta; t.off_v = g.off_v; t.off_vmeta = g.off_vmeta;
+  t.off_score = g.off_score; t.off_pos = g.off_pos;
+  t.kc = g.k_row / 16 > 0 ? g.k_row / 16 : 1;
+  t.ksh = g.k_row >= 128 ? 0 : ilog2(128 / g.k_row);          // rows r..r+7 of a fragment read spread over banks
+  t.vc = g.v_row / 16 > 0 ? g.v_row / 16 : 1;
+  t.vsh = 2;                                                    // fragment rows are tokens 4j .. 4j+3
+  return t;
+}
+
+// stage `bytes` of a code segment (rows of `row` bytes, kc chunks, swizzled) with per-thread 16-B cp.async
+__device__ __forceinline__ void stage_rows(uint8_t* dst, const uint8_t* src, int rows, int row, int kc, int sh,
+                                           int lane) {
+  const int n = rows * kc;
+  if (row >= 16) {
+    for (int j = lane; j < n; j += 32) {
+      const int r = j / kc, c = j - r * kc;
+      cp_async16(dst + r * row + swz(r, c, sh, kc) * 16, src + (size_t)j * 16, true);
+    }
+  } else {                                                      // rows narrower than a chunk: plain copy
+    for (int j = lane; j * 16 < rows * row; j += 32) cp_async16(dst + j * 16, src + (size_t)j * 16, true);
+  }
+}
+__device__ __forceinline__ void stage_plain(uint8_t* dst, const uint8_t* src, int bytes, int lane) {
+  for (int o = 16 * lane; o < bytes; o += 512) cp_async16(dst + o, src + o, true);
+}
+// byte offset of byte `b` of row `r` in a swizzled staged segment
+__device__ __forceinline__ int sw_off(int r, int b, int row, int kc, int sh) {
+  if (row < 16) return r * row + b;
+  return r * row + swz(r, b >> 4, sh, kc) * 16 + (b & 15);
+}
+
+// codes of features 4j .. 4j+3 (group g of 16 features) of key row r -> two fp16x2 (features 4j, 4j+1 | 4j+2, 4j+3)
+__device__ __forceinline__ void key_frag(const uint8_t* kseg, const TcGeom& G_, int r, int g, int j, uint32_t& lo,
+                                         uint32_t& hi) {
+  const int b = g * 2 * G_.kbits + j * (G_.kbits / 2);          // byte of feature 16g + 4j
+  const int o = sw_off(r, b, G_.k_row, G_.kc, G_.ksh);
+  if (G_.kbits == 8) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(kseg + o);
+    lo = h2_codes(w & 0xFFu, (w >> 8) & 0xFFu);
+    hi = h2_codes((w >> 16) & 0xFFu, w >> 24);
+  } else if (G_.kbits == 4) {
+    const uint32_t w = *reinterpret_cast<const uint16_t*>(kseg + o);
+    lo = h2_codes(w & 0xFu, (w >> 4) & 0xFu);
+    hi = h2_codes((w >> 8) & 0xFu, (w >> 12) & 0xFu);
+  } else {
+    const uint32_t w = kseg[o];
+    lo = h2_codes(w & 3u, (w >> 2) & 3u);
+    hi = h2_codes((w >> 4) & 3u, (w >> 6) & 3u);
+  }
+}
+// codes of features f, f+1 (f even) of value row r -> (c_f, c_f+1)
+__device__ __forceinline__ void val_pair(const uint8_t* vseg, const TcGeom& G_, int r, int f, uint32_t& c0, uint32_t& c1) {
+  const int bit = f * G_.vbits;
+  const int o = sw_off(r, bit >> 3, G_.v_row, G_.vc, G_.vsh);
+  const uint32_t Q = (1u << G_.vbits) - 1u;
+  if (G_.vbits == 8) {
+    const uint32_t w = *reinterpret_cast<const uint16_t*>(vseg + o);
+    c0 = w & 0xFFu; c1 = w >> 8;
+  } else {
+    const uint32_t w = vseg[o] >> (bit & 7);
+    c0 = w & Q; c1 = (w >> G_.vbits) & Q;
+  }
+}
+
+template <int D, int G>
+__global__ void __launch_bounds__(kTcThreads)
+attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs, int TS) {
+  constexpr int GP = G <= 4 ? 4 : 8;                             // logit row: GP floats per token
+  constexpr int NG = D / 16;                                      // 16-feature groups (QK k-steps, PV m-tiles)
+  extern __shared__ __align__(16) uint8_t tc_smem[];
+  __shared__ float s_q[G][D];
+  __shared__ float s_qsum[G], s_m[G], s_iz[G];
+  __shared__ float s_red[kTcWarps][G];
+  __shared__ unsigned long long s_min[2];
+  __shared__ int s_slot[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = lane >> 2, tig = lane & 3;
+  const int u = blockIdx.x;
+  if (ld_volatile(&p.ctrl->status) != 0) return;                  // sticky error: no-op
+  const int r = fdiv(p.div_LyH, u);
+  if (p.req_state[r] != DKV_REQ_ACTIVE) return;
+  const int L = p.L, W = p.W;
+  const int N = p.seq_len[r];
+  const int nh = p.n_h[u], nl = p.n_l[u];
+  const int nw = min(W, N);
+  const int T = nh + nl + nw;
+  const TcGeom gh = tc_geom(p.g[1]), gl = tc_geom(p.g[2]);
+  const int ph = ceil_div(nh, gh.C), pl = ceil_div(nl, gl.C);
+  const int npg = ph + pl;
+  float* lg = reinterpret_cast<float*>(tc_smem);                   // [TS][GP]
+  int32_t* pid = reinterpret_cast<int32_t*>(tc_smem + (size_t)TS * GP * 4);
+  uint8_t* stage0 = tc_smem + (size_t)TS * GP * 4 + (size_t)((L + 4) & ~3) * 4;
+  uint8_t* mystage = stage0 + (size_t)warp * kTcStages * kTcStage;
+  const int32_t* trow = p.table + (size_t)u * L;
+  for (int k = tid; k < npg; k += kTcThreads) pid[k] = k < ph ? trow[k] : trow[L - 1 - (k - ph)];
+  for (int k = tid; k < G * D; k += kTcThreads)
+    s_q[k / D][k % D] = __half2float(__ushort_as_half(q[(size_t)u * G * D + k]));
+  if (tid < 2) { s_min[tid] = ~0ull; s_slot[tid] = -1; }
+  __syncthreads();
+  if (tid < G) {
+    float sacc = 0.0f;
+    for (int f = 0; f < D; f++) sacc += s_q[tid][f];
+    s_qsum[tid] = sacc;
+  }
+  const float scale = rsqrtf((float)D);
+  // B fragments of the queries (k = features, permuted; n = head = grp): group g, b0 = features 4j, 4j+1 and
+  // b1 = 4j+2, 4j+3 (j = tig) of head grp
+  uint32_t qb[NG][2];
+#pragma unroll
+  for (int g = 0; g < NG; g++) {
+    const int f = 16 * g + 4 * tig;
+    uint32_t w0 = 0, w1 = 0;
+    if (grp < G) {
+      const uint16_t* qh = q + ((size_t)u * G + grp) * D;
+      w0 = (uint32_t)qh[f] | ((uint32_t)qh[f + 1] << 16);
+      w1 = (uint32_t)qh[f + 2] | ((uint32_t)qh[f + 3] << 16);
+    }
+    qb[g][0] = w0; qb[g][1] = w1;
+  }
+  __syncthreads();
+
+  auto page_geom = [&](int k, TcGeom& g, int& t0, int& cnt) {
+    const bool hi = k < ph;
+    g = hi ? gh : gl;
+    t0 = hi ? k * gh.C : nh + (k - ph) * gl.C;
+    cnt = min(g.C, (hi ? nh : nh + nl) - t0);
+  };
+  auto page_ptr = [&](int k) { return p.pages + (size_t)pid[k] * (size_t)p.page_bytes; };
+
+  // ---- phase 1: logits.  Stored pages: each warp its pages, staged (K codes swizzled + K meta) two ahead.
+  float mx[2] = {-INFINITY, -INFINITY};                           // heads 2*tig, 2*tig + 1
+  auto stage_k = [&](int k, int slot) {
+    TcGeom g; int t0, cnt;
+    page_geom(k, g, t0, cnt);
+    const uint8_t* pg = page_ptr(k);
+    uint8_t* dst = mystage + slot * kTcStage;
+    stage_rows(dst, pg + g.off_k, g.C, g.k_row, g.kc, g.ksh, lane);
+    stage_plain(dst + g.C * g.k_row, pg + g.off_kmeta, 4 * g.C, lane);
+  };
+  {
+    int k = warp, slot = 0;
+    if (k < npg) stage_k(k, 0);
+    cp_async_commit();
+    for (; k < npg; k += kTcWarps, slot ^= 1) {
+      if (k + kTcWarps < npg) stage_k(k + kTcWarps, slot ^ 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncwarp();
+      TcGeom g; int t0, cnt;
+      page_geom(k, g, t0, cnt);
+      const uint8_t* kseg = mystage + slot * kTcStage;
+      const uint32_t* kmeta = reinterpret_cast<const uint32_t*>(kseg + g.C * g.k_row);
+      for (int tile = 0; tile * 16 < cnt; tile++) {
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int gg = 0; gg < NG; gg++) {
+          uint32_t a[4];
+          key_frag(kseg, g, tile * 16 + grp, gg, tig, a[0], a[2]);
+          key_frag(kseg, g, tile * 16 + grp + 8, gg, tig, a[1], a[3]);
+          mma_f16(acc, a, qb[gg][0], qb[gg][1]);
+        }
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++) {                          // rows grp, grp + 8
+          const int j = tile * 16 + grp + 8 * hh;
+          if (j < cnt) {
+            const uint32_t km = kmeta[j];
+            const float sf = __half2float(__ushort_as_half((unsigned short)(km & 0xFFFFu)));
+            const float zf = __half2float(__ushort_as_half((unsigned short)(km >> 16)));
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+              const int h = 2 * tig + c;
+              if (h < G) {
+                const float l = (sf * acc[2 * hh + c] + zf * s_qsum[h]) * scale;
+                lg[(size_t)(t0 + j) * GP + h] = l;
+                mx[c] = fmaxf(mx[c], l);
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    cp_async_wait<0>();
+  }
+  // window tokens (FP16 keys), a thread per token on CUDA cores
+  float wmx[G];
+#pragma unroll
+  for (int h = 0; h < G; h++) wmx[h] = -INFINITY;
+  for (int i = tid; i < nw; i += kTcThreads) {
+    const int pos = N - nw + i;
+    const uint16_t* wk = reinterpret_cast<const uint16_t*>(p.win_k) + ((size_t)u * W + fmod_(p.div_W, pos)) * D;
+    float acc[G];
+#pragma unroll
+    for (int h = 0; h < G; h++) acc[h] = 0.0f;
+    for (int e0 = 0; e0 < D; e0 += 8) {
+      const uint4 v = *reinterpret_cast<const uint4*>(wk + e0);
+      const uint32_t hw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int kk = 0; kk < 8; kk++) {
+        const float x = __half2float(__ushort_as_half((unsigned short)(hw[kk >> 1] >> (16 * (kk & 1)))));
+#pragma unroll
+        for (int h = 0; h < G; h++) acc[h] = fmaf(s_q[h][e0 + kk], x, acc[h]);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < G; h++) {
+      const float l = acc[h] * scale;
+      lg[(size_t)(nh + nl + i) * GP + h] = l;
+      wmx[h] = fmaxf(wmx[h], l);
+    }
+  }
+  // ---- phase 2: per-head max, p = exp(l - max), Z
+  {
+    float m[G];
+#pragma unroll
+    for (int h = 0; h < G; h++) m[h] = wmx[h];
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      float v = mx[c];                                            // reduce over the 8 lanes of this tig
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+      mx[c] = v;
+    }
+#pragma unroll
+    for (int h = 0; h < G; h++) {
+      float v = m[h];
+      // head h's MMA maximum is held by lanes with tig == h / 2
+      const float mm = __shfl_sync(kFull, mx[h & 1], (h >> 1) & 3);
+      v = fmaxf(v, (h >> 1) < 4 ? mm : -INFINITY);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+      if (lane == 0) s_red[warp][h] = v;
+    }
+    __syncthreads();
+    if (tid < G) {
+      float v = -INFINITY;
+      for (int w = 0; w < kTcWarps; w++) v = fmaxf(v, s_red[w][tid]);
+      s_m[tid] = v;
+    }
+    __syncthreads();
+    float zs[G];
+#pragma unroll
+    for (int h = 0; h < G; h++) zs[h] = 0.0f;
+    for (int i = tid; i < T; i += kTcThreads) {
+#pragma unroll
+      for (int h = 0; h < G; h++) {
+        const float e = __expf(lg[(size_t)i * GP + h] - s_m[h]);
+        lg[(size_t)i * GP + h] = e;
+        zs[h] += e;
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < G; h++) {
+      float v = zs[h];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+      if (lane == 0) s_red[warp][h] = v;
+    }
+    __syncthreads();
+    if (tid < G) {
+      float v = 0.0f;
+      for (int w = 0; w < kTcWarps; w++) v += s_red[w][tid];
+      s_iz[tid] = 1.0f / v;
+    }
+    __syncthreads();
+  }
+  // ---- phase 3: PV by MMA (A = value codes^T: m = features f0 = 16g + 2*grp, f0 + 1; k = tokens 4j .. 4j+3;
+  // B = (a * s_v) split bf16 hi / lo: k = tokens, n = head grp), significance + minima, page by page
+  float acc[NG][4];
+#pragma unroll
+  for (int g = 0; g < NG; g++) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.0f;
+  float zsum = 0.0f;                                              // sum_t a_t z_t of head grp (this lane's tokens)
+  unsigned long long mkey[2] = {~0ull, ~0ull};
+  int mslot[2] = {-1, -1};
+  auto stage_v = [&](int k, int slot) {
+    TcGeom g; int t0, cnt;
+    page_geom(k, g, t0, cnt);
+    const uint8_t* pg = page_ptr(k);
+    uint8_t* dst = mystage + slot * kTcStage;
+    stage_rows(dst, pg + g.off_v, g.C, g.v_row, g.vc, g.vsh, lane);
+    uint8_t* d2 = dst + g.C * g.v_row;
+    stage_plain(d2, pg + g.off_vmeta, 4 * g.C, lane);
+    stage_plain(d2 + 4 * g.C, pg + g.off_score, 4 * g.C, lane);
+    stage_plain(d2 + 8 * g.C, pg + g.off_pos, 4 * g.C, lane);
+  };
+  const float iz = grp < G ? s_iz[grp] : 0.0f;
+  {
+    int k = warp, slot = 0;
+    if (k < npg) stage_v(k, 0);
+    cp_async_commit();
+    for (; k < npg; k += kTcWarps, slot ^= 1) {
+      if (k + kTcWarps < npg) stage_v(k + kTcWarps, slot ^ 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncwarp();
+      TcGeom g; int t0, cnt;
+      page_geom(k, g, t0, cnt);
+      const uint8_t* vseg = mystage + slot * kTcStage;
+      const uint32_t* vmeta = reinterpret_cast<const uint32_t*>(vseg + g.C * g.v_row);
+      const float* ssc = reinterpret_cast<const float*>(vseg + g.C * g.v_row + 4 * g.C);
+      const int32_t* spos = reinterpret_cast<const int32_t*>(vseg + g.C * g.v_row + 8 * g.C);
+      for (int tile = 0; tile * 16 < cnt; tile++) {
+        float bv[4];
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) {
+          const int j = tile * 16 + 4 * tig + jj;
+          float b = 0.0f;
+          if (j < cnt && grp < G) {
+            const uint32_t vm = vmeta[j];
+            const float sf = __half2float(__ushort_as_half((unsigned short)(vm & 0xFFFFu)));
+            const float zf = __half2float(__ushort_as_half((unsigned short)(vm >> 16)));
+            const float a = lg[(size_t)(t0 + j) * GP + grp] * iz;
+            b = a * sf;
+            zsum = fmaf(a, zf, zsum);
+          }
+          bv[jj] = b;
+        }
+        uint32_t bh0, bl0, bh1, bl1;
+        bf2_split(bv[0], bv[1], bh0, bl0);
+        bf2_split(bv[2], bv[3], bh1, bl1);
+#pragma unroll
+        for (int gg = 0; gg < NG; gg++) {
+          const int f0 = 16 * gg + 2 * grp;
+          uint32_t c[4][2];
+#pragma unroll
+          for (int jj = 0; jj < 4; jj++) val_pair(vseg, g, tile * 16 + 4 * tig + jj, f0, c[jj][0], c[jj][1]);
+          uint32_t a[4];
+          a[0] = bf2_codes(c[0][0], c[1][0]);                     // feature f0, tokens 4j, 4j+1
+          a[1] = bf2_codes(c[0][1], c[1][1]);                     // feature f0 + 1
+          a[2] = bf2_codes(c[2][0], c[3][0]);                     // feature f0, tokens 4j+2, 4j+3
+          a[3] = bf2_codes(c[2][1], c[3][1]);
+          mma_bf16(acc[gg], a, bh0, bh1);
+          mma_bf16(acc[gg], a, bl0, bl1);
+        }
+      }
+      // significance (Q33) of the page's tokens: a lane per token
+      for (int j = lane; j < cnt; j += 32) {
+        const int i = t0 + j;
+        float a = 0.0f;
+#pragma unroll
+        for (int h = 0; h < G; h++) a = fmaxf(a, lg[(size_t)i * GP + h] * s_iz[h]);
+        if (probs) probs[(size_t)u * p.M + i] = a;
+        const int pos = spos[j];
+        float sg = ssc[j];
+        const int c = N - 2 - pos;
+        if (c >= 0) {
+          sg = __fdiv_rn(__fadd_rn(__fmul_rn(sg, (float)c), a), (float)(c + 1));
+          *reinterpret_cast<float*>(page_ptr(k) + g.off_score + 4 * j) = sg;
+        }
+        const int cls = k < ph ? 0 : 1;
+        const int slotj = k < ph ? t0 + j : t0 - nh + j;
+        const unsigned long long key = ((unsigned long long)__float_as_uint(sg) << 32) | (uint32_t)pos;
+        if (key < mkey[cls]) { mkey[cls] = key; mslot[cls] = slotj; }
+      }
+      __syncwarp();
+    }
+    cp_async_wait<0>();
+  }
+  // window: significance + PV partial on CUDA cores (thread = feature)
+  for (int i = tid; i < nw; i += kTcThreads) {
+    const int pos = N - nw + i;
+    float a = 0.0f;
+#pragma unroll
+    for (int h = 0; h < G; h++) a = fmaxf(a, lg[(size_t)(nh + nl + i) * GP + h] * s_iz[h]);
+    if (probs) probs[(size_t)u * p.M + nh + nl + i] = a;
+    const int c = N - 2 - pos;
+    float* sp = p.win_sig + (size_t)u * W + fmod_(p.div_W, pos);
+    if (c >= 0) *sp = __fdiv_rn(__fadd_rn(__fmul_rn(*sp, (float)c), a), (float)(c + 1));
+  }
+  __syncthreads();                                                // staging areas are free: reuse for the reduction
+  float* part = reinterpret_cast<float*>(stage0);                 // [kTcWarps][G][D] MMA partials, then window
+  float* zred = part + kTcWarps * G * D;                          // [kTcWarps][G]
+#pragma unroll
+  for (int gg = 0; gg < NG; gg++) {
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+      const int h = 2 * tig + (c & 1);
+      const int f = 16 * gg + 2 * grp + (c >> 1);
+      if (h < G) part[((size_t)warp * G + h) * D + f] = acc[gg][c];
+    }
+  }
+  {
+    float v = zsum;                                               // lanes of head grp: tig = 0..3
+    v += __shfl_xor_sync(kFull, v, 1);
+    v += __shfl_xor_sync(kFull, v, 2);
+    if (tig == 0 && grp < G) zred[warp * G + grp] = v;
+  }
+  __syncthreads();
+  if (out != nullptr) {
+    for (int e = tid; e < G * D; e += kTcThreads) {
+      const int h = e / D, f = e % D;
+      float o = 0.0f, z = 0.0f;
+      for (int w = 0; w < kTcWarps; w++) { o += part[((size_t)w * G + h) * D + f]; z += zred[w * G + h]; }
+      float wsum = 0.0f;                                          // the window's values
+      for (int i = 0; i < nw; i++) {
+        const int pos = N - nw + i;
+        const uint16_t* wv = reinterpret_cast<const uint16_t*>(p.win_v) + ((size_t)u * W + fmod_(p.div_W, pos)) * D;
+        wsum = fmaf(lg[(size_t)(nh + nl + i) * GP + h] * s_iz[h], __half2float(__ushort_as_half(wv[f])), wsum);
+      }
+      out[((size_t)u * G + h) * D + f] = o + z + wsum;
+    }
+  }
+  // section minima (stored sections only; keys are unique: positions differ)
+#pragma unroll
+  for (int c = 0; c < 2; c++)
+    if (mkey[c] != ~0ull) atomicMin(&s_min[c], mkey[c]);
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 2; c++)
+    if (mkey[c] != ~0ull && mkey[c] == s_min[c]) s_slot[c] = mslot[c];
+  __syncthreads();
+  if (tid == 0) {
+    int32_t* m = p.secmin + 8 * (size_t)u;
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      m[3 * c] = (int32_t)(uint32_t)(s_min[c] >> 32);
+      m[3 * c + 1] = (int32_t)(uint32_t)(s_min[c] & 0xFFFFFFFFull);
+      m[3 * c + 2] = s_slot[c];
+    }
+    m[6] = 1;
+  }
+}
+
+// the staged page segments of every class fit one stage and every class holds whole 16-token tiles
+bool attend_tc_supported(const PoolDev& p) {
+  for (int k = 1; k <= 2; k++) {
+    const ClassGeom& g = p.g[k];
+    if (g.C % 16 != 0 || g.C * g.k_row + 4 * g.C > kTcStage || g.C * g.v_row + 12 * g.C > kTcStage) return false;
+  }
+  return p.G >= 1 && p.G <= 8;
+}
+
+size_t attend_tc_smem_bytes(const PoolDev& p, int TS) {
+  const int GP = p.G <= 4 ? 4 : 8;
+  const size_t red = (size_t)kTcWarps * p.G * p.d * 4 + (size_t)kTcWarps * p.G * 4;
+  const size_t stage = (size_t)kTcWarps * kTcStages * kTcStage;
+  return (size_t)TS * GP * 4 + (size_t)((p.L + 4) & ~3) * 4 + (stage > red ? stage : red);
+}
+
+template <int D, int G>
+static cudaError_t launch_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s) {
+  const size_t smem = attend_tc_smem_bytes(p, TS);
+  cudaError_t e = cudaFuncSetAttribute(attend_tc_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  attend_tc_kernel<D, G><<<p.U, kTcThreads, smem, s>>>(p, q, out, probs, TS);
+  return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_tc_d(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s) {
+  switch (p.G) {
+    case 1: return launch_tc<D, 1>(p, q, out, probs, TS, s);
+    case 2: return launch_tc<D, 2>(p, q, out, probs, TS, s);
+    case 4: return launch_tc<D, 4>(p, q, out, probs, TS, s);
+    case 5: return launch_tc<D, 5>(p, q, out, probs, TS, s);
+    case 7: return launch_tc<D, 7>(p, q, out, probs, TS, s);
+    default: return launch_tc<D, 8>(p, q, out, probs, TS, s);
+  }
+}
+
+cudaError_t launch_attend_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s) {
+  return p.d == 128 ? launch_tc_d<128>(p, q, out, probs, TS, s) : launch_tc_d<64>(p, q, out, probs, TS, s);
+}
+
+}  // namespace dkv

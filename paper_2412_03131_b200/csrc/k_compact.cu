@@ -392,4 +392,67 @@ int compact_max_coresident(int tile_units) {
   return per * sms;
 }
 
+// ---- deferred recycle copy, eager form (dkv_compact_alloc of a decode step that frees requests): one warp per
+// unit of the freed requests (host list), ring[(end0 + off + k) mod P] = table slot k of the unit in canonical
+// slot order (Q13), then the slot is cleared and the unit's marker consumed — so the pool state is complete when
+// dkv_compact_alloc returns.  Inside a decode-step CUDA graph (no host list) the following quant_write kernel
+// does the same copies from the markers instead (k_quant_decode.cu).  A no-op if the scan took the barrier path
+// (it then copied in place and left no marker).
+constexpr int kRecMaxReq = 64;
+struct RecList {
+  int32_t n;
+  int32_t req[kRecMaxReq];
+};
+
+__global__ void __launch_bounds__(256) recycle_kernel(PoolDev p, RecList l) {
+  const int lane = threadIdx.x & 31;
+  const int wu = (blockIdx.x * 256 + threadIdx.x) >> 5;         // index over the freed requests' units
+  if (wu >= l.n * p.LyH) return;
+  const int u = l.req[wu / p.LyH] * p.LyH + wu % p.LyH;
+  const int32_t nfr = p.rec[3 * (size_t)u + 2];
+  if (nfr == 0) return;                                         // warp-uniform
+  const int32_t off = p.rec[3 * (size_t)u], ph = p.rec[3 * (size_t)u + 1];
+  const int P = p.P, L = p.L;
+  const int64_t ring0 = p.ctrl->rec_end0 + off;                  // < 2P
+  int32_t* row = p.table + (size_t)u * L;
+  for (int k0 = 0; k0 < nfr; k0 += 32 * 8) {
+    int32_t pid[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const int k = k0 + 32 * j + lane;
+      const int slot = k < ph ? k : L - nfr + k;                 // [0, ph) then [L - pl, L)
+      pid[j] = k < nfr ? __ldcg(row + slot) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const int k = k0 + 32 * j + lane;
+      if (k < nfr) {
+        const int slot = k < ph ? k : L - nfr + k;
+        int64_t pos = ring0 + k;                                 // < 3P
+        pos -= pos >= P ? P : 0;
+        pos -= pos >= P ? P : 0;
+        p.ring[pos] = pid[j];
+        int32_t empty = -1;                                      // clear only after the load returned
+        asm volatile("" : "+r"(empty) : "r"(pid[j]));
+        row[slot] = empty;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) p.rec[3 * (size_t)u + 2] = 0;                  // marker consumed
+}
+
+cudaError_t launch_recycle(const PoolDev& p, const int32_t* req, int n, cudaStream_t s) {
+  for (int i0 = 0; i0 < n; i0 += kRecMaxReq) {
+    RecList l;
+    l.n = n - i0 < kRecMaxReq ? n - i0 : kRecMaxReq;
+    for (int i = 0; i < l.n; i++) l.req[i] = req[i0 + i];
+    const long warps = (long)l.n * p.LyH;
+    recycle_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(p, l);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace dkv

@@ -355,11 +355,17 @@ dkv_status_t dkv_compact_alloc(dkv_pool_t p, const dkv_decision_t* d_dec, dkv_st
     if (e == cudaSuccess) e = launch_prefill_conservative(p->dev, (cudaStream_t)s);
   } else {
     // decode steps that recycle finished requests: in the fast path the scan kernel only records each freed
-    // unit's ring offset and the following dkv_quant_write(DECODE) copies the page IDs over all SMs (inside
-    // this kernel the copy would run on the one or two CTAs whose tile holds the request).  Nothing here
-    // depends on the host mirror, so the step can be captured in a CUDA graph (dkv_decode_graph_create).
+    // unit's ring offset and a second, wide kernel copies the page IDs (one warp per freed unit, all SMs) —
+    // inside the scan kernel the copy would run on the one or two CTAs whose tile holds the request.  (In a
+    // decode-step CUDA graph, which has no host list, the quant_write kernel does these copies.)
+    std::vector<int32_t> freed;
+    if (p->phase == DKV_PHASE_DECODE)
+      for (int r = 0; r < p->cfg.max_requests; r++)
+        if (p->req_state[r] == DKV_REQ_PENDING_FREE) freed.push_back(r);
     e = launch_compact_alloc(p->dev, d_dec, p->phase, (cudaStream_t)s, /*alloc=*/true,
                              /*defer_recycle=*/p->phase == DKV_PHASE_DECODE);
+    if (e == cudaSuccess && !freed.empty())
+      e = launch_recycle(p->dev, freed.data(), (int)freed.size(), (cudaStream_t)s);
   }
   if (e != cudaSuccess) return DKV_ERR_CUDA;
   const int R = p->cfg.max_requests;
@@ -418,6 +424,26 @@ dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* 
   }
   cudaError_t e = launch_attend(p->dev, d_q, d_out, d_probs, TS, (cudaStream_t)s);
   return e == cudaSuccess ? DKV_OK : DKV_ERR_CUDA;
+}
+
+dkv_status_t dkv_attend_tc(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* d_probs, dkv_stream_t s) {
+  if (!p || !d_q) return DKV_ERR_INVALID_ARG;
+  if (p->seq != SEQ_IDLE) return DKV_ERR_STATE;
+  const int G = p->cfg.q_per_kv;
+  if (!(G == 1 || G == 2 || G == 4 || G == 5 || G == 7 || G == 8)) return DKV_ERR_INVALID_ARG;
+  int dev = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+    return DKV_ERR_CUDA;
+  int TS = 1;
+  for (int r = 0; r < p->cfg.max_requests; r++)
+    if (p->req_state[r] == DKV_REQ_ACTIVE && p->seq_len[r] > TS) TS = p->seq_len[r];
+  TS = (TS + 31) & ~31;
+  // contexts whose logits do not fit in shared memory, and page geometries the kernel does not tile, take the
+  // exact path (documented in dkv.h)
+  if (!attend_tc_supported(p->dev) || attend_tc_smem_bytes(p->dev, TS) > (size_t)optin)
+    return dkv_attend(p, d_q, d_out, d_probs, s);
+  return launch_attend_tc(p->dev, d_q, d_out, d_probs, TS, (cudaStream_t)s) == cudaSuccess ? DKV_OK : DKV_ERR_CUDA;
 }
 
 dkv_status_t dkv_set_head_thresholds(dkv_pool_t p, const float* h_alpha_h, const float* h_alpha_l, dkv_stream_t s) {

@@ -78,6 +78,10 @@ class Pool:
         """NEXT-2: q = fp16 (as int16) [U][q_per_kv][d] CUDA tensor; out fp32 [U][G][d] / probs fp32 [U][M] or None"""
         return _d.dkv_attend(self.handle, q, out, probs, stream or self.stream)
 
+    def attend_tc(self, q, out=None, probs=None, stream=None):
+        """NEXT-2 on tensor cores (dkv_attend_tc): same buffers as attend()"""
+        return _d.dkv_attend_tc(self.handle, q, out, probs, stream or self.stream)
+
     def set_head_thresholds(self, alpha_h, alpha_l, stream=None):
         """NEXT-4: per-(layer, head) thresholds (host sequences of Ly*H floats), or None for the pool-wide pair"""
         return _d.dkv_set_head_thresholds(self.handle, alpha_h, alpha_l, stream or self.stream)

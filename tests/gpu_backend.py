@@ -61,6 +61,16 @@ class GpuBackend:
         torch.cuda.synchronize()
         return 0, (out.cpu().numpy() if want_out else None), (probs.cpu().numpy() if want_probs else None)
 
+    def attend_tc(self, q, want_out=True, want_probs=False):
+        """NEXT-2 on tensor cores (dkv_attend_tc); same buffers as attend()"""
+        G, d, M = self.scn.q_per_kv, self.scn.d, self.scn.M
+        qd = self._cuda(np.ascontiguousarray(q).view(np.int16))
+        out = torch.zeros((self.U, G, d), dtype=torch.float32, device=self.device) if want_out else None
+        probs = torch.zeros((self.U, M), dtype=torch.float32, device=self.device) if want_probs else None
+        self.pool.attend_tc(qd, out, probs)
+        torch.cuda.synchronize()
+        return 0, (out.cpu().numpy() if want_out else None), (probs.cpu().numpy() if want_probs else None)
+
     def quant_write_prefill(self, k, v, sig):
         k, v = self._cuda(k).view(torch.int16), self._cuda(v).view(torch.int16)
         self.pool.quant_write_prefill(k, v, self._cuda(sig))
