@@ -460,7 +460,8 @@ def run_ours(args, rank, world, local):
     # per-step inputs [GRAPH_STEPS][U][d] (840 MB at this config, >> L2) already in HBM.  No L2 flush between the
     # steps of a replay: it is the steady state of back-to-back decode steps.
     from paper_2412_03131_b200 import dkv as D
-    GS = 100
+    # the replays (two per PDL / plain graph, one event graph) must stay within max_seq_len
+    GS = max(1, min(100, (c["M"] - int(seq.max()) - 4 * (args.warmup + args.steps) - 8) // 6))
     gsig = torch.empty((GS, wl.U), dtype=torch.float32, device=dev)
     gk = torch.empty((GS, wl.U, c["d"]), dtype=torch.int16, device=dev)
     gv = torch.empty_like(gk)
@@ -749,7 +750,7 @@ def run_ours(args, rank, world, local):
                             "traffic": traffic("classify_decode_kernel"), "traffic_unit": "bytes per launch"},
         "e2e": {"value": round(e2e_mean, 3), "unit": E2E_UNIT,
                 "h2d_bytes_per_step": wl.U * (4 + 2 * 2 * c["d"]), "d2h_bytes_per_step": wl.U * 16},
-        "graph": graph,
+        "graph": graph if GS >= 10 else None,
         "next2": next2,
         # §8e: the per-step MIN all-reduce of the admission counters (N > 1): its latency on the side stream and
         # the fraction of steps in which it finished inside the step (hidden behind quant_write)

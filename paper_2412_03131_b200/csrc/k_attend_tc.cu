@@ -33,7 +33,7 @@ namespace dkv {
 
 constexpr int kTcWarps = 4;
 constexpr int kTcThreads = kTcWarps * 32;
-constexpr int kTcStages = 2;
+constexpr int kTcStages = 4;                   // pages in flight per warp (cp.async groups)
 constexpr int kTcStage = 2304;                 // bytes per warp per stage: >= C*k_row + 4C and C*v_row + 12C
 
 __device__ __forceinline__ void mma_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -221,14 +221,18 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     stage_rows(dst, pg + g.off_k, g.C, g.k_row, g.kc, g.ksh, lane);
     stage_plain(dst + g.C * g.k_row, pg + g.off_kmeta, 4 * g.C, lane);
   };
+  const int my_n = npg > warp ? (npg - warp + kTcWarps - 1) / kTcWarps : 0;   // this warp's pages
   {
-    int k = warp, slot = 0;
-    if (k < npg) stage_k(k, 0);
-    cp_async_commit();
-    for (; k < npg; k += kTcWarps, slot ^= 1) {
-      if (k + kTcWarps < npg) stage_k(k + kTcWarps, slot ^ 1);
+#pragma unroll
+    for (int i = 0; i < kTcStages - 1; i++) {
+      if (i < my_n) stage_k(warp + i * kTcWarps, i);
       cp_async_commit();
-      cp_async_wait<1>();
+    }
+    for (int i = 0; i < my_n; i++) {
+      const int k = warp + i * kTcWarps, slot = i % kTcStages;
+      if (i + kTcStages - 1 < my_n) stage_k(warp + (i + kTcStages - 1) * kTcWarps, (i + kTcStages - 1) % kTcStages);
+      cp_async_commit();
+      cp_async_wait<kTcStages - 1>();
       __syncwarp();
       TcGeom g; int t0, cnt;
       page_geom(k, g, t0, cnt);
@@ -369,13 +373,16 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   };
   const float iz = grp < G ? s_iz[grp] : 0.0f;
   {
-    int k = warp, slot = 0;
-    if (k < npg) stage_v(k, 0);
-    cp_async_commit();
-    for (; k < npg; k += kTcWarps, slot ^= 1) {
-      if (k + kTcWarps < npg) stage_v(k + kTcWarps, slot ^ 1);
+#pragma unroll
+    for (int i = 0; i < kTcStages - 1; i++) {
+      if (i < my_n) stage_v(warp + i * kTcWarps, i);
       cp_async_commit();
-      cp_async_wait<1>();
+    }
+    for (int i = 0; i < my_n; i++) {
+      const int k = warp + i * kTcWarps, slot = i % kTcStages;
+      if (i + kTcStages - 1 < my_n) stage_v(warp + (i + kTcStages - 1) * kTcWarps, (i + kTcStages - 1) % kTcStages);
+      cp_async_commit();
+      cp_async_wait<kTcStages - 1>();
       __syncwarp();
       TcGeom g; int t0, cnt;
       page_geom(k, g, t0, cnt);

@@ -79,7 +79,8 @@ def _run(scn, lens, steps, seed=0, frees=()):
         q = rng.normal(0, 1, size=(scn.U, G, d)).astype(np.float16)
         snap = g.snapshot()
         _, og, pg = g.attend_tc(q, want_out=True, want_probs=True)
-        eq1.check_units(snap, g.geom, L, W, d, scn.LyH, q, og, pg, range(scn.U), where=f"tc step {step}")
+        live = [u for u in range(scn.U) if snap["req_state"][u // scn.LyH] == H.REQ_ACTIVE]
+        eq1.check_units(snap, g.geom, L, W, d, scn.LyH, q, og, pg, live, where=f"tc step {step}")
         after = g.snapshot()
         for u in range(scn.U):
             r = u // scn.LyH
