@@ -14,7 +14,7 @@
 //
 // One CTA per unit (the paper's "one thread block per head"), kTcWarps warps; pages go round-robin to
 // the warps, high pages first, then low, each staged into shared memory by per-thread 16-B cp.async
-// copies (two stages per warp).  The MMA fragments are read straight from the staged code rows; the paper's
+// copies (kTcStages pages in flight per warp).  The MMA fragments are read straight from the staged code rows; the paper's
 // tiled K/V layouts (NEXT-3) exist to make per-thread vector loads coalesce in global memory — here
 // whole page segments are copied (contiguous 1-2 KB runs, coalesced by construction) and the tiling happens in
 // shared memory: a 16-B XOR swizzle of each code row so that the fragment reads are bank-conflict free, and a
@@ -31,9 +31,9 @@
 
 namespace dkv {
 
-constexpr int kTcWarps = 4;
+constexpr int kTcWarps = 8;
 constexpr int kTcThreads = kTcWarps * 32;
-constexpr int kTcStages = 4;                   // pages in flight per warp (cp.async groups)
+constexpr int kTcStages = 2;                   // pages in flight per warp (cp.async groups)
 constexpr int kTcStage = 2304;                 // bytes per warp per stage: >= C*k_row + 4C and C*v_row + 12C
 
 __device__ __forceinline__ void mma_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -71,78 +71,147 @@ __device__ __forceinline__ void bf2_split(float x0, float x1, uint32_t& hi, uint
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
-// 16-B chunk swizzle of a staged code row: chunk c of row `row` sits at chunk c ^ ((row >> sh) & (kc - 1))
-__device__ __forceinline__ int swz(int row, int c, int sh, int kc) { return c ^ ((row >> sh) & (kc - 1)); }
-
-struct TcGeom {
-  int C, kbits, vbits, k_row, v_row, off_k, off_kmeta, off_v, off_vmeta, off_score, off_pos;
-  int kc, ksh, vc, vsh;                        // chunks per code row and swizzle shifts (K, V)
+// Compile-time geometry of one precision class (the paper's K8V4 high / K4V2 low pages): tokens per
+// page, bit widths, code row bytes, 16-B chunks per row and the row swizzle shifts of the staged copies.
+template <int D, int C_, int KB, int VB>
+struct TcCls {
+  static constexpr int C = C_, kbits = KB, vbits = VB;
+  static constexpr int k_row = D * KB / 8, v_row = D * VB / 8;
+  static constexpr int kc = k_row / 16, vc = v_row / 16;               // chunks per row (>= 1 for D >= 64)
+  // fragment reads touch rows grp (8 consecutive) at the same byte: shift so those rows' chunks differ
+  static constexpr int ksh = k_row >= 128 ? 0 : (k_row == 64 ? 1 : (k_row == 32 ? 2 : 3));
+  static constexpr int vsh = 2;                                        // V fragment rows: tokens 4j .. 4j+3
+  static_assert(k_row >= 16 && v_row >= 16, "rows of at least one 16-B chunk");
 };
-__device__ __forceinline__ int ilog2(int x) { return 31 - __clz(x); }
-__device__ __forceinline__ TcGeom tc_geom(const ClassGeom& g) {
-  TcGeom t;
-  t.C = g.C; t.kbits = g.kbits; t.vbits = g.vbits; t.k_row = g.k_row; t.v_row = g.v_row;
-  t.off_k = g.off_k; t.off_kmeta = g.off_kmeta; t.off_v = g.off_v; t.off_vmeta = g.off_vmeta;
-  t.off_score = g.off_score; t.off_pos = g.off_pos;
-  t.kc = g.k_row / 16 > 0 ? g.k_row / 16 : 1;
-  t.ksh = g.k_row >= 128 ? 0 : ilog2(128 / g.k_row);          // rows r..r+7 of a fragment read spread over banks
-  t.vc = g.v_row / 16 > 0 ? g.v_row / 16 : 1;
-  t.vsh = 2;                                                    // fragment rows are tokens 4j .. 4j+3
-  return t;
+template <int KC, int SH>
+__device__ __forceinline__ int swz_off(int row, int byte, int row_bytes) {
+  return row * row_bytes + ((((byte >> 4) ^ ((row >> SH) & (KC - 1)))) << 4) + (byte & 15);
 }
 
-// stage `bytes` of a code segment (rows of `row` bytes, kc chunks, swizzled) with per-thread 16-B cp.async
-__device__ __forceinline__ void stage_rows(uint8_t* dst, const uint8_t* src, int rows, int row, int kc, int sh,
-                                           int lane) {
-  const int n = rows * kc;
-  if (row >= 16) {
-    for (int j = lane; j < n; j += 32) {
-      const int r = j / kc, c = j - r * kc;
-      cp_async16(dst + r * row + swz(r, c, sh, kc) * 16, src + (size_t)j * 16, true);
+// a page's staged segments: codes (rows swizzled) + 4C-byte segments, per-thread 16-B cp.async
+template <int ROW, int KC, int SH, int C>
+__device__ __forceinline__ void stage_codes(uint8_t* dst, const uint8_t* src, int lane) {
+  constexpr int n = C * KC;
+#pragma unroll
+  for (int j = lane; j < n; j += 32) {
+    const int r = j / KC, c = j % KC;
+    cp_async16(dst + r * ROW + ((c ^ ((r >> SH) & (KC - 1))) << 4), src + (size_t)j * 16, true);
+  }
+}
+template <int BYTES>
+__device__ __forceinline__ void stage_seg(uint8_t* dst, const uint8_t* src, int lane) {
+#pragma unroll
+  for (int o = 16 * lane; o < BYTES; o += 512) cp_async16(dst + o, src + o, true);
+}
+
+// QK^T of one staged page: logits of its tokens (all G heads) into lg; running max of this lane's two heads
+template <int D, int G, int GP, class CL>
+__device__ __forceinline__ void qk_page(const uint8_t* kseg, int t0, int cnt, const uint32_t (&qb)[D / 16][2],
+                                        const float* qsum, float scale, float* lg, float (&mx)[2], int grp, int tig) {
+  const uint32_t* kmeta = reinterpret_cast<const uint32_t*>(kseg + CL::C * CL::k_row);
+#pragma unroll
+  for (int tile = 0; tile < CL::C / 16; tile++) {
+    if (tile * 16 >= cnt) break;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const int r0 = tile * 16 + grp, r1 = r0 + 8;
+#pragma unroll
+    for (int g = 0; g < D / 16; g++) {
+      const int b = g * 2 * CL::kbits + tig * (CL::kbits / 2);  // byte of feature 16g + 4 tig
+      uint32_t a[4];
+#pragma unroll
+      for (int rr = 0; rr < 2; rr++) {
+        const int o = swz_off<CL::kc, CL::ksh>(rr ? r1 : r0, b, CL::k_row);
+        uint32_t lo, hi;
+        if constexpr (CL::kbits == 8) {
+          const uint32_t w = *reinterpret_cast<const uint32_t*>(kseg + o);
+          lo = h2_codes(w & 0xFFu, (w >> 8) & 0xFFu);
+          hi = h2_codes((w >> 16) & 0xFFu, w >> 24);
+        } else if constexpr (CL::kbits == 4) {
+          const uint32_t w = *reinterpret_cast<const uint16_t*>(kseg + o);
+          lo = h2_codes(w & 0xFu, (w >> 4) & 0xFu);
+          hi = h2_codes((w >> 8) & 0xFu, (w >> 12) & 0xFu);
+        } else {
+          const uint32_t w = kseg[o];
+          lo = h2_codes(w & 3u, (w >> 2) & 3u);
+          hi = h2_codes((w >> 4) & 3u, (w >> 6) & 3u);
+        }
+        a[rr] = lo;                                              // a0 / a1: k = 2 tig, 2 tig + 1
+        a[2 + rr] = hi;                                          // a2 / a3: k = 2 tig + 8, 2 tig + 9
+      }
+      mma_f16(acc, a, qb[g][0], qb[g][1]);
     }
-  } else {                                                      // rows narrower than a chunk: plain copy
-    for (int j = lane; j * 16 < rows * row; j += 32) cp_async16(dst + j * 16, src + (size_t)j * 16, true);
+#pragma unroll
+    for (int hh = 0; hh < 2; hh++) {                             // rows grp, grp + 8
+      const int j = tile * 16 + grp + 8 * hh;
+      if (j < cnt) {
+        const uint32_t km = kmeta[j];
+        const float sf = __half2float(__ushort_as_half((unsigned short)(km & 0xFFFFu)));
+        const float zf = __half2float(__ushort_as_half((unsigned short)(km >> 16)));
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+          const int h = 2 * tig + c;
+          if (h < G) {
+            const float l = (sf * acc[2 * hh + c] + zf * qsum[h]) * scale;
+            lg[(size_t)(t0 + j) * GP + h] = l;
+            mx[c] = fmaxf(mx[c], l);
+          }
+        }
+      }
+    }
   }
-}
-__device__ __forceinline__ void stage_plain(uint8_t* dst, const uint8_t* src, int bytes, int lane) {
-  for (int o = 16 * lane; o < bytes; o += 512) cp_async16(dst + o, src + o, true);
-}
-// byte offset of byte `b` of row `r` in a swizzled staged segment
-__device__ __forceinline__ int sw_off(int r, int b, int row, int kc, int sh) {
-  if (row < 16) return r * row + b;
-  return r * row + swz(r, b >> 4, sh, kc) * 16 + (b & 15);
 }
 
-// codes of features 4j .. 4j+3 (group g of 16 features) of key row r -> two fp16x2 (features 4j, 4j+1 | 4j+2, 4j+3)
-__device__ __forceinline__ void key_frag(const uint8_t* kseg, const TcGeom& G_, int r, int g, int j, uint32_t& lo,
-                                         uint32_t& hi) {
-  const int b = g * 2 * G_.kbits + j * (G_.kbits / 2);          // byte of feature 16g + 4j
-  const int o = sw_off(r, b, G_.k_row, G_.kc, G_.ksh);
-  if (G_.kbits == 8) {
-    const uint32_t w = *reinterpret_cast<const uint32_t*>(kseg + o);
-    lo = h2_codes(w & 0xFFu, (w >> 8) & 0xFFu);
-    hi = h2_codes((w >> 16) & 0xFFu, w >> 24);
-  } else if (G_.kbits == 4) {
-    const uint32_t w = *reinterpret_cast<const uint16_t*>(kseg + o);
-    lo = h2_codes(w & 0xFu, (w >> 4) & 0xFu);
-    hi = h2_codes((w >> 8) & 0xFu, (w >> 12) & 0xFu);
-  } else {
-    const uint32_t w = kseg[o];
-    lo = h2_codes(w & 3u, (w >> 2) & 3u);
-    hi = h2_codes((w >> 4) & 3u, (w >> 6) & 3u);
-  }
-}
-// codes of features f, f+1 (f even) of value row r -> (c_f, c_f+1)
-__device__ __forceinline__ void val_pair(const uint8_t* vseg, const TcGeom& G_, int r, int f, uint32_t& c0, uint32_t& c1) {
-  const int bit = f * G_.vbits;
-  const int o = sw_off(r, bit >> 3, G_.v_row, G_.vc, G_.vsh);
-  const uint32_t Q = (1u << G_.vbits) - 1u;
-  if (G_.vbits == 8) {
-    const uint32_t w = *reinterpret_cast<const uint16_t*>(vseg + o);
-    c0 = w & 0xFFu; c1 = w >> 8;
-  } else {
-    const uint32_t w = vseg[o] >> (bit & 7);
-    c0 = w & Q; c1 = (w >> G_.vbits) & Q;
+// PV of one staged page into the warp's accumulators (m = features 16g + 2 grp (+1), n = heads) + the z term
+template <int D, int G, int GP, class CL>
+__device__ __forceinline__ void pv_page(const uint8_t* vseg, int t0, int cnt, const float* lg, float iz,
+                                        float (&acc)[D / 16][4], float& zsum, int grp, int tig) {
+  const uint32_t* vmeta = reinterpret_cast<const uint32_t*>(vseg + CL::C * CL::v_row);
+#pragma unroll
+  for (int tile = 0; tile < CL::C / 16; tile++) {
+    if (tile * 16 >= cnt) break;
+    float bv[4];
+#pragma unroll
+    for (int jj = 0; jj < 4; jj++) {
+      const int j = tile * 16 + 4 * tig + jj;
+      float b = 0.0f;
+      if (j < cnt && grp < G) {
+        const uint32_t vm = vmeta[j];
+        const float sf = __half2float(__ushort_as_half((unsigned short)(vm & 0xFFFFu)));
+        const float zf = __half2float(__ushort_as_half((unsigned short)(vm >> 16)));
+        const float a = lg[(size_t)(t0 + j) * GP + grp] * iz;
+        b = a * sf;
+        zsum = fmaf(a, zf, zsum);
+      }
+      bv[jj] = b;
+    }
+    uint32_t bh0, bl0, bh1, bl1;
+    bf2_split(bv[0], bv[1], bh0, bl0);
+    bf2_split(bv[2], bv[3], bh1, bl1);
+    const int rbase = tile * 16 + 4 * tig;
+#pragma unroll
+    for (int g = 0; g < D / 16; g++) {
+      const int bit = (16 * g + 2 * grp) * CL::vbits;          // features f0 = 16 g + 2 grp, f0 + 1
+      uint32_t c0[4], c1[4];
+#pragma unroll
+      for (int jj = 0; jj < 4; jj++) {
+        const int o = swz_off<CL::vc, CL::vsh>(rbase + jj, bit >> 3, CL::v_row);
+        if constexpr (CL::vbits == 8) {
+          const uint32_t w = *reinterpret_cast<const uint16_t*>(vseg + o);
+          c0[jj] = w & 0xFFu; c1[jj] = w >> 8;
+        } else {
+          constexpr uint32_t Q = (1u << CL::vbits) - 1u;
+          const uint32_t w = (uint32_t)vseg[o] >> (bit & 7);
+          c0[jj] = w & Q; c1[jj] = (w >> CL::vbits) & Q;
+        }
+      }
+      uint32_t a[4];
+      a[0] = bf2_codes(c0[0], c0[1]);                          // feature f0, tokens 4 tig, 4 tig + 1
+      a[1] = bf2_codes(c1[0], c1[1]);                          // feature f0 + 1
+      a[2] = bf2_codes(c0[2], c0[3]);                          // feature f0, tokens 4 tig + 2, 4 tig + 3
+      a[3] = bf2_codes(c1[2], c1[3]);
+      mma_bf16(acc[g], a, bh0, bh1);
+      mma_bf16(acc[g], a, bl0, bl1);
+    }
   }
 }
 
@@ -151,6 +220,8 @@ __global__ void __launch_bounds__(kTcThreads)
 attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs, int TS) {
   constexpr int GP = G <= 4 ? 4 : 8;                             // logit row: GP floats per token
   constexpr int NG = D / 16;                                      // 16-feature groups (QK k-steps, PV m-tiles)
+  using HI = TcCls<D, 16, 8, 4>;                                  // K8V4, 16-token pages
+  using LO = TcCls<D, 32, 4, 2>;                                  // K4V2, 32-token pages
   extern __shared__ __align__(16) uint8_t tc_smem[];
   __shared__ float s_q[G][D];
   __shared__ float s_qsum[G], s_m[G], s_iz[G];
@@ -168,9 +239,9 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   const int nh = p.n_h[u], nl = p.n_l[u];
   const int nw = min(W, N);
   const int T = nh + nl + nw;
-  const TcGeom gh = tc_geom(p.g[1]), gl = tc_geom(p.g[2]);
-  const int ph = ceil_div(nh, gh.C), pl = ceil_div(nl, gl.C);
+  const int ph = ceil_div(nh, HI::C), pl = ceil_div(nl, LO::C);
   const int npg = ph + pl;
+  const ClassGeom gh = p.g[1], gl = p.g[2];                       // segment offsets inside a page
   float* lg = reinterpret_cast<float*>(tc_smem);                   // [TS][GP]
   int32_t* pid = reinterpret_cast<int32_t*>(tc_smem + (size_t)TS * GP * 4);
   uint8_t* stage0 = tc_smem + (size_t)TS * GP * 4 + (size_t)((L + 4) & ~3) * 4;
@@ -187,41 +258,37 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     s_qsum[tid] = sacc;
   }
   const float scale = rsqrtf((float)D);
-  // B fragments of the queries (k = features, permuted; n = head = grp): group g, b0 = features 4j, 4j+1 and
-  // b1 = 4j+2, 4j+3 (j = tig) of head grp
+  // B fragments of the queries (k = features, permuted; n = head = grp): group g, b0 = features 4 tig, 4 tig + 1
+  // and b1 = 4 tig + 2, 4 tig + 3 of head grp
   uint32_t qb[NG][2];
 #pragma unroll
   for (int g = 0; g < NG; g++) {
-    const int f = 16 * g + 4 * tig;
     uint32_t w0 = 0, w1 = 0;
     if (grp < G) {
-      const uint16_t* qh = q + ((size_t)u * G + grp) * D;
-      w0 = (uint32_t)qh[f] | ((uint32_t)qh[f + 1] << 16);
-      w1 = (uint32_t)qh[f + 2] | ((uint32_t)qh[f + 3] << 16);
+      const uint2 v = *reinterpret_cast<const uint2*>(q + ((size_t)u * G + grp) * D + 16 * g + 4 * tig);
+      w0 = v.x; w1 = v.y;
     }
     qb[g][0] = w0; qb[g][1] = w1;
   }
   __syncthreads();
 
-  auto page_geom = [&](int k, TcGeom& g, int& t0, int& cnt) {
-    const bool hi = k < ph;
-    g = hi ? gh : gl;
-    t0 = hi ? k * gh.C : nh + (k - ph) * gl.C;
-    cnt = min(g.C, (hi ? nh : nh + nl) - t0);
-  };
   auto page_ptr = [&](int k) { return p.pages + (size_t)pid[k] * (size_t)p.page_bytes; };
+  const int my_n = npg > warp ? (npg - warp + kTcWarps - 1) / kTcWarps : 0;   // this warp's pages
 
-  // ---- phase 1: logits.  Stored pages: each warp its pages, staged (K codes swizzled + K meta) two ahead.
-  float mx[2] = {-INFINITY, -INFINITY};                           // heads 2*tig, 2*tig + 1
+  // ---- phase 1: logits.  Stored pages: each warp its pages (k = warp + i * kTcWarps), K codes (swizzled) + K
+  // meta staged kTcStages - 1 pages ahead
+  float mx[2] = {-INFINITY, -INFINITY};                           // heads 2 tig, 2 tig + 1
   auto stage_k = [&](int k, int slot) {
-    TcGeom g; int t0, cnt;
-    page_geom(k, g, t0, cnt);
     const uint8_t* pg = page_ptr(k);
     uint8_t* dst = mystage + slot * kTcStage;
-    stage_rows(dst, pg + g.off_k, g.C, g.k_row, g.kc, g.ksh, lane);
-    stage_plain(dst + g.C * g.k_row, pg + g.off_kmeta, 4 * g.C, lane);
+    if (k < ph) {
+      stage_codes<HI::k_row, HI::kc, HI::ksh, HI::C>(dst, pg + gh.off_k, lane);
+      stage_seg<4 * HI::C>(dst + HI::C * HI::k_row, pg + gh.off_kmeta, lane);
+    } else {
+      stage_codes<LO::k_row, LO::kc, LO::ksh, LO::C>(dst, pg + gl.off_k, lane);
+      stage_seg<4 * LO::C>(dst + LO::C * LO::k_row, pg + gl.off_kmeta, lane);
+    }
   };
-  const int my_n = npg > warp ? (npg - warp + kTcWarps - 1) / kTcWarps : 0;   // this warp's pages
   {
 #pragma unroll
     for (int i = 0; i < kTcStages - 1; i++) {
@@ -234,37 +301,13 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
       cp_async_commit();
       cp_async_wait<kTcStages - 1>();
       __syncwarp();
-      TcGeom g; int t0, cnt;
-      page_geom(k, g, t0, cnt);
       const uint8_t* kseg = mystage + slot * kTcStage;
-      const uint32_t* kmeta = reinterpret_cast<const uint32_t*>(kseg + g.C * g.k_row);
-      for (int tile = 0; tile * 16 < cnt; tile++) {
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int gg = 0; gg < NG; gg++) {
-          uint32_t a[4];
-          key_frag(kseg, g, tile * 16 + grp, gg, tig, a[0], a[2]);
-          key_frag(kseg, g, tile * 16 + grp + 8, gg, tig, a[1], a[3]);
-          mma_f16(acc, a, qb[gg][0], qb[gg][1]);
-        }
-#pragma unroll
-        for (int hh = 0; hh < 2; hh++) {                          // rows grp, grp + 8
-          const int j = tile * 16 + grp + 8 * hh;
-          if (j < cnt) {
-            const uint32_t km = kmeta[j];
-            const float sf = __half2float(__ushort_as_half((unsigned short)(km & 0xFFFFu)));
-            const float zf = __half2float(__ushort_as_half((unsigned short)(km >> 16)));
-#pragma unroll
-            for (int c = 0; c < 2; c++) {
-              const int h = 2 * tig + c;
-              if (h < G) {
-                const float l = (sf * acc[2 * hh + c] + zf * s_qsum[h]) * scale;
-                lg[(size_t)(t0 + j) * GP + h] = l;
-                mx[c] = fmaxf(mx[c], l);
-              }
-            }
-          }
-        }
+      if (k < ph) {
+        const int t0 = k * HI::C;
+        qk_page<D, G, GP, HI>(kseg, t0, min(HI::C, nh - t0), qb, s_qsum, scale, lg, mx, grp, tig);
+      } else {
+        const int t0 = nh + (k - ph) * LO::C;
+        qk_page<D, G, GP, LO>(kseg, t0, min(LO::C, nh + nl - t0), qb, s_qsum, scale, lg, mx, grp, tig);
       }
       __syncwarp();
     }
@@ -299,9 +342,6 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   }
   // ---- phase 2: per-head max, p = exp(l - max), Z
   {
-    float m[G];
-#pragma unroll
-    for (int h = 0; h < G; h++) m[h] = wmx[h];
 #pragma unroll
     for (int c = 0; c < 2; c++) {
       float v = mx[c];                                            // reduce over the 8 lanes of this tig
@@ -311,10 +351,8 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     }
 #pragma unroll
     for (int h = 0; h < G; h++) {
-      float v = m[h];
-      // head h's MMA maximum is held by lanes with tig == h / 2
-      const float mm = __shfl_sync(kFull, mx[h & 1], (h >> 1) & 3);
-      v = fmaxf(v, (h >> 1) < 4 ? mm : -INFINITY);
+      // head h's MMA maximum is held by the lanes with tig == h / 2
+      float v = fmaxf(wmx[h], __shfl_sync(kFull, mx[h & 1], (h >> 1) & 3));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
       if (lane == 0) s_red[warp][h] = v;
@@ -326,14 +364,15 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
       s_m[tid] = v;
     }
     __syncthreads();
-    float zs[G];
+    float m[G], zs[G];
 #pragma unroll
-    for (int h = 0; h < G; h++) zs[h] = 0.0f;
+    for (int h = 0; h < G; h++) { m[h] = s_m[h]; zs[h] = 0.0f; }
     for (int i = tid; i < T; i += kTcThreads) {
+      float* row = lg + (size_t)i * GP;
 #pragma unroll
       for (int h = 0; h < G; h++) {
-        const float e = __expf(lg[(size_t)i * GP + h] - s_m[h]);
-        lg[(size_t)i * GP + h] = e;
+        const float e = __expf(row[h] - m[h]);
+        row[h] = e;
         zs[h] += e;
       }
     }
@@ -352,7 +391,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     }
     __syncthreads();
   }
-  // ---- phase 3: PV by MMA (A = value codes^T: m = features f0 = 16g + 2*grp, f0 + 1; k = tokens 4j .. 4j+3;
+  // ---- phase 3: PV by MMA (A = value codes^T: m = features f0 = 16g + 2 grp, f0 + 1; k = tokens 4 tig .. +3;
   // B = (a * s_v) split bf16 hi / lo: k = tokens, n = head grp), significance + minima, page by page
   float acc[NG][4];
 #pragma unroll
@@ -360,16 +399,25 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   float zsum = 0.0f;                                              // sum_t a_t z_t of head grp (this lane's tokens)
   unsigned long long mkey[2] = {~0ull, ~0ull};
   int mslot[2] = {-1, -1};
+  float izr[G];
+#pragma unroll
+  for (int h = 0; h < G; h++) izr[h] = s_iz[h];
   auto stage_v = [&](int k, int slot) {
-    TcGeom g; int t0, cnt;
-    page_geom(k, g, t0, cnt);
     const uint8_t* pg = page_ptr(k);
     uint8_t* dst = mystage + slot * kTcStage;
-    stage_rows(dst, pg + g.off_v, g.C, g.v_row, g.vc, g.vsh, lane);
-    uint8_t* d2 = dst + g.C * g.v_row;
-    stage_plain(d2, pg + g.off_vmeta, 4 * g.C, lane);
-    stage_plain(d2 + 4 * g.C, pg + g.off_score, 4 * g.C, lane);
-    stage_plain(d2 + 8 * g.C, pg + g.off_pos, 4 * g.C, lane);
+    if (k < ph) {
+      stage_codes<HI::v_row, HI::vc, HI::vsh, HI::C>(dst, pg + gh.off_v, lane);
+      uint8_t* d2 = dst + HI::C * HI::v_row;
+      stage_seg<4 * HI::C>(d2, pg + gh.off_vmeta, lane);
+      stage_seg<4 * HI::C>(d2 + 4 * HI::C, pg + gh.off_score, lane);
+      stage_seg<4 * HI::C>(d2 + 8 * HI::C, pg + gh.off_pos, lane);
+    } else {
+      stage_codes<LO::v_row, LO::vc, LO::vsh, LO::C>(dst, pg + gl.off_v, lane);
+      uint8_t* d2 = dst + LO::C * LO::v_row;
+      stage_seg<4 * LO::C>(d2, pg + gl.off_vmeta, lane);
+      stage_seg<4 * LO::C>(d2 + 4 * LO::C, pg + gl.off_score, lane);
+      stage_seg<4 * LO::C>(d2 + 8 * LO::C, pg + gl.off_pos, lane);
+    }
   };
   const float iz = grp < G ? s_iz[grp] : 0.0f;
   {
@@ -384,62 +432,34 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
       cp_async_commit();
       cp_async_wait<kTcStages - 1>();
       __syncwarp();
-      TcGeom g; int t0, cnt;
-      page_geom(k, g, t0, cnt);
       const uint8_t* vseg = mystage + slot * kTcStage;
-      const uint32_t* vmeta = reinterpret_cast<const uint32_t*>(vseg + g.C * g.v_row);
-      const float* ssc = reinterpret_cast<const float*>(vseg + g.C * g.v_row + 4 * g.C);
-      const int32_t* spos = reinterpret_cast<const int32_t*>(vseg + g.C * g.v_row + 8 * g.C);
-      for (int tile = 0; tile * 16 < cnt; tile++) {
-        float bv[4];
-#pragma unroll
-        for (int jj = 0; jj < 4; jj++) {
-          const int j = tile * 16 + 4 * tig + jj;
-          float b = 0.0f;
-          if (j < cnt && grp < G) {
-            const uint32_t vm = vmeta[j];
-            const float sf = __half2float(__ushort_as_half((unsigned short)(vm & 0xFFFFu)));
-            const float zf = __half2float(__ushort_as_half((unsigned short)(vm >> 16)));
-            const float a = lg[(size_t)(t0 + j) * GP + grp] * iz;
-            b = a * sf;
-            zsum = fmaf(a, zf, zsum);
-          }
-          bv[jj] = b;
-        }
-        uint32_t bh0, bl0, bh1, bl1;
-        bf2_split(bv[0], bv[1], bh0, bl0);
-        bf2_split(bv[2], bv[3], bh1, bl1);
-#pragma unroll
-        for (int gg = 0; gg < NG; gg++) {
-          const int f0 = 16 * gg + 2 * grp;
-          uint32_t c[4][2];
-#pragma unroll
-          for (int jj = 0; jj < 4; jj++) val_pair(vseg, g, tile * 16 + 4 * tig + jj, f0, c[jj][0], c[jj][1]);
-          uint32_t a[4];
-          a[0] = bf2_codes(c[0][0], c[1][0]);                     // feature f0, tokens 4j, 4j+1
-          a[1] = bf2_codes(c[0][1], c[1][1]);                     // feature f0 + 1
-          a[2] = bf2_codes(c[2][0], c[3][0]);                     // feature f0, tokens 4j+2, 4j+3
-          a[3] = bf2_codes(c[2][1], c[3][1]);
-          mma_bf16(acc[gg], a, bh0, bh1);
-          mma_bf16(acc[gg], a, bl0, bl1);
-        }
-      }
+      const bool hi = k < ph;
+      const int C = hi ? HI::C : LO::C;
+      const int t0 = hi ? k * HI::C : nh + (k - ph) * LO::C;
+      const int cnt = min(C, (hi ? nh : nh + nl) - t0);
+      const int vrow = hi ? HI::v_row : LO::v_row;
+      if (hi) pv_page<D, G, GP, HI>(vseg, t0, cnt, lg, iz, acc, zsum, grp, tig);
+      else pv_page<D, G, GP, LO>(vseg, t0, cnt, lg, iz, acc, zsum, grp, tig);
       // significance (Q33) of the page's tokens: a lane per token
+      const float* ssc = reinterpret_cast<const float*>(vseg + C * vrow + 4 * C);
+      const int32_t* spos = reinterpret_cast<const int32_t*>(vseg + C * vrow + 8 * C);
+      float* gsc = reinterpret_cast<float*>(page_ptr(k) + (hi ? gh.off_score : gl.off_score));
       for (int j = lane; j < cnt; j += 32) {
-        const int i = t0 + j;
+        const int i2 = t0 + j;
+        const float* row = lg + (size_t)i2 * GP;
         float a = 0.0f;
 #pragma unroll
-        for (int h = 0; h < G; h++) a = fmaxf(a, lg[(size_t)i * GP + h] * s_iz[h]);
-        if (probs) probs[(size_t)u * p.M + i] = a;
+        for (int h = 0; h < G; h++) a = fmaxf(a, row[h] * izr[h]);
+        if (probs) probs[(size_t)u * p.M + i2] = a;
         const int pos = spos[j];
         float sg = ssc[j];
         const int c = N - 2 - pos;
         if (c >= 0) {
-          sg = __fdiv_rn(__fadd_rn(__fmul_rn(sg, (float)c), a), (float)(c + 1));
-          *reinterpret_cast<float*>(page_ptr(k) + g.off_score + 4 * j) = sg;
+          sg = (sg * (float)c + a) * __frcp_rn((float)(c + 1));
+          gsc[j] = sg;
         }
-        const int cls = k < ph ? 0 : 1;
-        const int slotj = k < ph ? t0 + j : t0 - nh + j;
+        const int cls = hi ? 0 : 1;
+        const int slotj = hi ? t0 + j : t0 - nh + j;
         const unsigned long long key = ((unsigned long long)__float_as_uint(sg) << 32) | (uint32_t)pos;
         if (key < mkey[cls]) { mkey[cls] = key; mslot[cls] = slotj; }
       }
@@ -447,19 +467,20 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     }
     cp_async_wait<0>();
   }
-  // window: significance + PV partial on CUDA cores (thread = feature)
+  // window: significance on CUDA cores
   for (int i = tid; i < nw; i += kTcThreads) {
     const int pos = N - nw + i;
+    const float* row = lg + (size_t)(nh + nl + i) * GP;
     float a = 0.0f;
 #pragma unroll
-    for (int h = 0; h < G; h++) a = fmaxf(a, lg[(size_t)(nh + nl + i) * GP + h] * s_iz[h]);
+    for (int h = 0; h < G; h++) a = fmaxf(a, row[h] * izr[h]);
     if (probs) probs[(size_t)u * p.M + nh + nl + i] = a;
     const int c = N - 2 - pos;
     float* sp = p.win_sig + (size_t)u * W + fmod_(p.div_W, pos);
-    if (c >= 0) *sp = __fdiv_rn(__fadd_rn(__fmul_rn(*sp, (float)c), a), (float)(c + 1));
+    if (c >= 0) *sp = (*sp * (float)c + a) * __frcp_rn((float)(c + 1));
   }
   __syncthreads();                                                // staging areas are free: reuse for the reduction
-  float* part = reinterpret_cast<float*>(stage0);                 // [kTcWarps][G][D] MMA partials, then window
+  float* part = reinterpret_cast<float*>(stage0);                 // [kTcWarps][G][D] MMA partials
   float* zred = part + kTcWarps * G * D;                          // [kTcWarps][G]
 #pragma unroll
   for (int gg = 0; gg < NG; gg++) {
@@ -482,11 +503,11 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
       const int h = e / D, f = e % D;
       float o = 0.0f, z = 0.0f;
       for (int w = 0; w < kTcWarps; w++) { o += part[((size_t)w * G + h) * D + f]; z += zred[w * G + h]; }
-      float wsum = 0.0f;                                          // the window's values
+      float wsum = 0.0f;                                          // the window's values (FP16) on CUDA cores
       for (int i = 0; i < nw; i++) {
         const int pos = N - nw + i;
         const uint16_t* wv = reinterpret_cast<const uint16_t*>(p.win_v) + ((size_t)u * W + fmod_(p.div_W, pos)) * D;
-        wsum = fmaf(lg[(size_t)(nh + nl + i) * GP + h] * s_iz[h], __half2float(__ushort_as_half(wv[f])), wsum);
+        wsum = fmaf(lg[(size_t)(nh + nl + i) * GP + h] * izr[h], __half2float(__ushort_as_half(wv[f])), wsum);
       }
       out[((size_t)u * G + h) * D + f] = o + z + wsum;
     }
@@ -512,13 +533,12 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   }
 }
 
-// the staged page segments of every class fit one stage and every class holds whole 16-token tiles
+// the kernel is specialised for the paper's classes: K8V4 in 16-token pages, K4V2 in 32-token pages;
+// other geometries take the exact path
 bool attend_tc_supported(const PoolDev& p) {
-  for (int k = 1; k <= 2; k++) {
-    const ClassGeom& g = p.g[k];
-    if (g.C % 16 != 0 || g.C * g.k_row + 4 * g.C > kTcStage || g.C * g.v_row + 12 * g.C > kTcStage) return false;
-  }
-  return p.G >= 1 && p.G <= 8;
+  const ClassGeom &h = p.g[1], &l = p.g[2];
+  return h.C == 16 && h.kbits == 8 && h.vbits == 4 && l.C == 32 && l.kbits == 4 && l.vbits == 2 && p.G >= 1 &&
+         p.G <= 8 && (p.d == 64 || p.d == 128);
 }
 
 size_t attend_tc_smem_bytes(const PoolDev& p, int TS) {
