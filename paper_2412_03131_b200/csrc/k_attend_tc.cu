@@ -104,39 +104,53 @@ __device__ __forceinline__ void stage_seg(uint8_t* dst, const uint8_t* src, int 
   for (int o = 16 * lane; o < BYTES; o += 512) cp_async16(dst + o, src + o, true);
 }
 
-// QK^T of one staged page: logits of its tokens (all G heads) into lg; running max of this lane's two heads
+// Loads `BYTES` contiguous bytes of a staged, swizzled row starting at byte `b0` (a multiple of BYTES, BYTES in
+// {2, 4, 8, 16, 32}) into 32-bit words.
+template <int BYTES, int KC, int SH>
+__device__ __forceinline__ void lds_row(const uint8_t* seg, int row, int row_bytes, int b0, uint32_t (&w)[(BYTES + 3) / 4]) {
+  if constexpr (BYTES >= 16) {
+#pragma unroll
+    for (int c = 0; c < BYTES / 16; c++) {
+      const uint4 v = *reinterpret_cast<const uint4*>(seg + swz_off<KC, SH>(row, b0 + 16 * c, row_bytes));
+      w[4 * c] = v.x; w[4 * c + 1] = v.y; w[4 * c + 2] = v.z; w[4 * c + 3] = v.w;
+    }
+  } else if constexpr (BYTES == 8) {
+    const uint2 v = *reinterpret_cast<const uint2*>(seg + swz_off<KC, SH>(row, b0, row_bytes));
+    w[0] = v.x; w[1] = v.y;
+  } else if constexpr (BYTES == 4) {
+    w[0] = *reinterpret_cast<const uint32_t*>(seg + swz_off<KC, SH>(row, b0, row_bytes));
+  } else {
+    w[0] = *reinterpret_cast<const uint16_t*>(seg + swz_off<KC, SH>(row, b0, row_bytes));
+  }
+}
+
+// QK^T of one staged page: logits of its tokens (all G heads) into lg; running max of this lane's two heads.
+// MMA k index <-> feature: in group g, lane tig supplies features FPK*tig + 4g + {0,1 | 2,3} (k = 2 tig, 2 tig + 1 |
+// 2 tig + 8, 2 tig + 9), FPK = D/4, so a lane's codes for all groups are one contiguous run of its key row.
 template <int D, int G, int GP, class CL>
 __device__ __forceinline__ void qk_page(const uint8_t* kseg, int t0, int cnt, const uint32_t (&qb)[D / 16][2],
                                         const float* qsum, float scale, float* lg, float (&mx)[2], int grp, int tig) {
+  constexpr int FPK = D / 4, RB = FPK * CL::kbits / 8;           // features / bytes per lane per key row
+  constexpr int NW = (RB + 3) / 4;
   const uint32_t* kmeta = reinterpret_cast<const uint32_t*>(kseg + CL::C * CL::k_row);
 #pragma unroll
   for (int tile = 0; tile < CL::C / 16; tile++) {
     if (tile * 16 >= cnt) break;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    const int r0 = tile * 16 + grp, r1 = r0 + 8;
+    uint32_t w[2][NW];
+    lds_row<RB, CL::kc, CL::ksh>(kseg, tile * 16 + grp, CL::k_row, RB * tig, w[0]);
+    lds_row<RB, CL::kc, CL::ksh>(kseg, tile * 16 + grp + 8, CL::k_row, RB * tig, w[1]);
 #pragma unroll
     for (int g = 0; g < D / 16; g++) {
-      const int b = g * 2 * CL::kbits + tig * (CL::kbits / 2);  // byte of feature 16g + 4 tig
       uint32_t a[4];
 #pragma unroll
       for (int rr = 0; rr < 2; rr++) {
-        const int o = swz_off<CL::kc, CL::ksh>(rr ? r1 : r0, b, CL::k_row);
-        uint32_t lo, hi;
-        if constexpr (CL::kbits == 8) {
-          const uint32_t w = *reinterpret_cast<const uint32_t*>(kseg + o);
-          lo = h2_codes(w & 0xFFu, (w >> 8) & 0xFFu);
-          hi = h2_codes((w >> 16) & 0xFFu, w >> 24);
-        } else if constexpr (CL::kbits == 4) {
-          const uint32_t w = *reinterpret_cast<const uint16_t*>(kseg + o);
-          lo = h2_codes(w & 0xFu, (w >> 4) & 0xFu);
-          hi = h2_codes((w >> 8) & 0xFu, (w >> 12) & 0xFu);
-        } else {
-          const uint32_t w = kseg[o];
-          lo = h2_codes(w & 3u, (w >> 2) & 3u);
-          hi = h2_codes((w >> 4) & 3u, (w >> 6) & 3u);
-        }
-        a[rr] = lo;                                              // a0 / a1: k = 2 tig, 2 tig + 1
-        a[2 + rr] = hi;                                          // a2 / a3: k = 2 tig + 8, 2 tig + 9
+        constexpr int KB = CL::kbits;
+        const int bit = 4 * g * KB;                              // features 4g .. 4g+3 of the lane's run
+        const uint32_t x = w[rr][bit >> 5] >> (bit & 31);
+        constexpr uint32_t Q = (1u << KB) - 1u;
+        a[rr] = h2_codes(x & Q, (x >> KB) & Q);                  // a0 / a1: k = 2 tig, 2 tig + 1
+        a[2 + rr] = h2_codes((x >> (2 * KB)) & Q, (x >> (3 * KB)) & Q);   // a2 / a3: k = 2 tig + 8, 2 tig + 9
       }
       mma_f16(acc, a, qb[g][0], qb[g][1]);
     }
@@ -161,10 +175,14 @@ __device__ __forceinline__ void qk_page(const uint8_t* kseg, int t0, int cnt, co
   }
 }
 
-// PV of one staged page into the warp's accumulators (m = features 16g + 2 grp (+1), n = heads) + the z term
+// PV of one staged page into the warp's accumulators + the z term.  MMA m index <-> feature: in m-tile g, row grp
+// is feature FPV*grp + 2g and row grp + 8 is FPV*grp + 2g + 1 (FPV = D/8), so a lane's value codes for all
+// m-tiles are one contiguous run of each value row; k = tokens 4 tig .. 4 tig + 3; n = head.
 template <int D, int G, int GP, class CL>
 __device__ __forceinline__ void pv_page(const uint8_t* vseg, int t0, int cnt, const float* lg, float iz,
                                         float (&acc)[D / 16][4], float& zsum, int grp, int tig) {
+  constexpr int FPV = D / 8, RB = FPV * CL::vbits / 8;           // features / bytes per lane per value row
+  constexpr int NW = (RB + 3) / 4;
   const uint32_t* vmeta = reinterpret_cast<const uint32_t*>(vseg + CL::C * CL::v_row);
 #pragma unroll
   for (int tile = 0; tile < CL::C / 16; tile++) {
@@ -187,27 +205,25 @@ __device__ __forceinline__ void pv_page(const uint8_t* vseg, int t0, int cnt, co
     uint32_t bh0, bl0, bh1, bl1;
     bf2_split(bv[0], bv[1], bh0, bl0);
     bf2_split(bv[2], bv[3], bh1, bl1);
-    const int rbase = tile * 16 + 4 * tig;
+    uint32_t w[4][NW];
+#pragma unroll
+    for (int jj = 0; jj < 4; jj++) lds_row<RB, CL::vc, CL::vsh>(vseg, tile * 16 + 4 * tig + jj, CL::v_row, RB * grp, w[jj]);
 #pragma unroll
     for (int g = 0; g < D / 16; g++) {
-      const int bit = (16 * g + 2 * grp) * CL::vbits;          // features f0 = 16 g + 2 grp, f0 + 1
+      constexpr int VB = CL::vbits;
+      constexpr uint32_t Q = (1u << VB) - 1u;
+      const int bit = 2 * g * VB;                                // features 2g, 2g + 1 of the lane's run
       uint32_t c0[4], c1[4];
 #pragma unroll
       for (int jj = 0; jj < 4; jj++) {
-        const int o = swz_off<CL::vc, CL::vsh>(rbase + jj, bit >> 3, CL::v_row);
-        if constexpr (CL::vbits == 8) {
-          const uint32_t w = *reinterpret_cast<const uint16_t*>(vseg + o);
-          c0[jj] = w & 0xFFu; c1[jj] = w >> 8;
-        } else {
-          constexpr uint32_t Q = (1u << CL::vbits) - 1u;
-          const uint32_t w = (uint32_t)vseg[o] >> (bit & 7);
-          c0[jj] = w & Q; c1[jj] = (w >> CL::vbits) & Q;
-        }
+        const uint32_t x = w[jj][bit >> 5] >> (bit & 31);
+        c0[jj] = x & Q;
+        c1[jj] = (x >> VB) & Q;
       }
       uint32_t a[4];
-      a[0] = bf2_codes(c0[0], c0[1]);                          // feature f0, tokens 4 tig, 4 tig + 1
-      a[1] = bf2_codes(c1[0], c1[1]);                          // feature f0 + 1
-      a[2] = bf2_codes(c0[2], c0[3]);                          // feature f0, tokens 4 tig + 2, 4 tig + 3
+      a[0] = bf2_codes(c0[0], c0[1]);                          // feature row grp, tokens 4 tig, 4 tig + 1
+      a[1] = bf2_codes(c1[0], c1[1]);                          // feature row grp + 8
+      a[2] = bf2_codes(c0[2], c0[3]);                          // feature row grp, tokens 4 tig + 2, 4 tig + 3
       a[3] = bf2_codes(c1[2], c1[3]);
       mma_bf16(acc[g], a, bh0, bh1);
       mma_bf16(acc[g], a, bl0, bl1);
@@ -258,14 +274,14 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     s_qsum[tid] = sacc;
   }
   const float scale = rsqrtf((float)D);
-  // B fragments of the queries (k = features, permuted; n = head = grp): group g, b0 = features 4 tig, 4 tig + 1
-  // and b1 = 4 tig + 2, 4 tig + 3 of head grp
+  // B fragments of the queries (k = features, permuted as in qk_page; n = head = grp): group g, b0 = features
+  // (D/4) tig + 4g + {0, 1}, b1 = + {2, 3} of head grp
   uint32_t qb[NG][2];
 #pragma unroll
   for (int g = 0; g < NG; g++) {
     uint32_t w0 = 0, w1 = 0;
     if (grp < G) {
-      const uint2 v = *reinterpret_cast<const uint2*>(q + ((size_t)u * G + grp) * D + 16 * g + 4 * tig);
+      const uint2 v = *reinterpret_cast<const uint2*>(q + ((size_t)u * G + grp) * D + (D / 4) * tig + 4 * g);
       w0 = v.x; w1 = v.y;
     }
     qb[g][0] = w0; qb[g][1] = w1;
@@ -313,32 +329,37 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     }
     cp_async_wait<0>();
   }
-  // window tokens (FP16 keys), a thread per token on CUDA cores
+  // window tokens (FP16 keys): rows staged into shared memory (the page stages are free now), then one
+  // (token, head) dot product per thread on CUDA cores
+  __syncthreads();
+  const uint16_t* wkg = reinterpret_cast<const uint16_t*>(p.win_k) + (size_t)u * W * D;
+  const uint16_t* wvg = reinterpret_cast<const uint16_t*>(p.win_v) + (size_t)u * W * D;
+  uint16_t* wks = reinterpret_cast<uint16_t*>(stage0);            // [nw][D] fp16, oldest first
+  for (int c = tid; c < nw * (D / 8); c += kTcThreads) {
+    const int i = c / (D / 8), e = c % (D / 8);
+    cp_async16(wks + (size_t)i * D + 8 * e, wkg + (size_t)fmod_(p.div_W, N - nw + i) * D + 8 * e, true);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
   float wmx[G];
 #pragma unroll
   for (int h = 0; h < G; h++) wmx[h] = -INFINITY;
-  for (int i = tid; i < nw; i += kTcThreads) {
-    const int pos = N - nw + i;
-    const uint16_t* wk = reinterpret_cast<const uint16_t*>(p.win_k) + ((size_t)u * W + fmod_(p.div_W, pos)) * D;
-    float acc[G];
-#pragma unroll
-    for (int h = 0; h < G; h++) acc[h] = 0.0f;
-    for (int e0 = 0; e0 < D; e0 += 8) {
-      const uint4 v = *reinterpret_cast<const uint4*>(wk + e0);
-      const uint32_t hw[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int kk = 0; kk < 8; kk++) {
-        const float x = __half2float(__ushort_as_half((unsigned short)(hw[kk >> 1] >> (16 * (kk & 1)))));
-#pragma unroll
-        for (int h = 0; h < G; h++) acc[h] = fmaf(s_q[h][e0 + kk], x, acc[h]);
-      }
+  for (int x = tid; x < nw * G; x += kTcThreads) {
+    const int i = x / G, h = x % G;
+    const __half2* kr = reinterpret_cast<const __half2*>(wks + (size_t)i * D);
+    float acc0 = 0.0f, acc1 = 0.0f;
+#pragma unroll 8
+    for (int e = 0; e < D / 2; e++) {
+      const float2 kv = __half22float2(kr[e]);
+      acc0 = fmaf(s_q[h][2 * e], kv.x, acc0);
+      acc1 = fmaf(s_q[h][2 * e + 1], kv.y, acc1);
     }
+    const float l = (acc0 + acc1) * scale;
+    lg[(size_t)(nh + nl + i) * GP + h] = l;
 #pragma unroll
-    for (int h = 0; h < G; h++) {
-      const float l = acc[h] * scale;
-      lg[(size_t)(nh + nl + i) * GP + h] = l;
-      wmx[h] = fmaxf(wmx[h], l);
-    }
+    for (int hh = 0; hh < G; hh++)
+      if (hh == h) wmx[hh] = fmaxf(wmx[hh], l);
   }
   // ---- phase 2: per-head max, p = exp(l - max), Z
   {
@@ -467,6 +488,15 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     }
     cp_async_wait<0>();
   }
+  __syncthreads();                                                // staging areas are free: reuse for the reduction
+  float* part = reinterpret_cast<float*>(stage0);                 // [kTcWarps][G][D] MMA partials
+  float* zred = part + kTcWarps * G * D;                          // [kTcWarps][G]
+  uint16_t* wvs = reinterpret_cast<uint16_t*>(zred + ((kTcWarps * G + 3) & ~3));   // [nw][D] window values
+  for (int c = tid; c < nw * (D / 8); c += kTcThreads) {
+    const int i = c / (D / 8), e = c % (D / 8);
+    cp_async16(wvs + (size_t)i * D + 8 * e, wvg + (size_t)fmod_(p.div_W, N - nw + i) * D + 8 * e, true);
+  }
+  cp_async_commit();
   // window: significance on CUDA cores
   for (int i = tid; i < nw; i += kTcThreads) {
     const int pos = N - nw + i;
@@ -479,15 +509,12 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     float* sp = p.win_sig + (size_t)u * W + fmod_(p.div_W, pos);
     if (c >= 0) *sp = (*sp * (float)c + a) * __frcp_rn((float)(c + 1));
   }
-  __syncthreads();                                                // staging areas are free: reuse for the reduction
-  float* part = reinterpret_cast<float*>(stage0);                 // [kTcWarps][G][D] MMA partials
-  float* zred = part + kTcWarps * G * D;                          // [kTcWarps][G]
 #pragma unroll
   for (int gg = 0; gg < NG; gg++) {
 #pragma unroll
     for (int c = 0; c < 4; c++) {
       const int h = 2 * tig + (c & 1);
-      const int f = 16 * gg + 2 * grp + (c >> 1);
+      const int f = (D / 8) * grp + 2 * gg + (c >> 1);          // pv_page's feature mapping
       if (h < G) part[((size_t)warp * G + h) * D + f] = acc[gg][c];
     }
   }
@@ -497,6 +524,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     v += __shfl_xor_sync(kFull, v, 2);
     if (tig == 0 && grp < G) zred[warp * G + grp] = v;
   }
+  cp_async_wait<0>();
   __syncthreads();
   if (out != nullptr) {
     for (int e = tid; e < G * D; e += kTcThreads) {
@@ -504,11 +532,8 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
       float o = 0.0f, z = 0.0f;
       for (int w = 0; w < kTcWarps; w++) { o += part[((size_t)w * G + h) * D + f]; z += zred[w * G + h]; }
       float wsum = 0.0f;                                          // the window's values (FP16) on CUDA cores
-      for (int i = 0; i < nw; i++) {
-        const int pos = N - nw + i;
-        const uint16_t* wv = reinterpret_cast<const uint16_t*>(p.win_v) + ((size_t)u * W + fmod_(p.div_W, pos)) * D;
-        wsum = fmaf(lg[(size_t)(nh + nl + i) * GP + h] * izr[h], __half2float(__ushort_as_half(wv[f])), wsum);
-      }
+      for (int i = 0; i < nw; i++)
+        wsum = fmaf(lg[(size_t)(nh + nl + i) * GP + h] * izr[h], __half2float(__ushort_as_half(wvs[(size_t)i * D + f])), wsum);
       out[((size_t)u * G + h) * D + f] = o + z + wsum;
     }
   }
@@ -543,7 +568,9 @@ bool attend_tc_supported(const PoolDev& p) {
 
 size_t attend_tc_smem_bytes(const PoolDev& p, int TS) {
   const int GP = p.G <= 4 ? 4 : 8;
-  const size_t red = (size_t)kTcWarps * p.G * p.d * 4 + (size_t)kTcWarps * p.G * 4;
+  // phase 3's reduction area: warp partials, z sums, the staged window values (phase 1 stages the window keys)
+  const size_t red = (size_t)kTcWarps * p.G * p.d * 4 + (size_t)((kTcWarps * p.G + 3) & ~3) * 4 +
+                     (size_t)p.W * p.d * 2;
   const size_t stage = (size_t)kTcWarps * kTcStages * kTcStage;
   return (size_t)TS * GP * 4 + (size_t)((p.L + 4) & ~3) * 4 + (stage > red ? stage : red);
 }
