@@ -36,9 +36,9 @@ _lock = threading.Lock()
 
 OK, ERR_INVALID, ERR_STATE, ERR_OOM, ERR_NONFINITE, ERR_OVERFLOW = 0, -1, -2, -3, -4, -5
 DECODE, PREFILL = 0, 1
-CLS_NONE, CLS_HIGH, CLS_LOW, CLS_PRUNED = 0, 1, 2, 3
+CLS_NONE, CLS_HIGH, CLS_LOW, CLS_PRUNED, CLS_TOP = 0, 1, 2, 3, 4
 V_NONE, V_KEEP, V_DOWN, V_PRUNE = 0, 1, 2, 3
-GROW_NONE, GROW_HIGH, GROW_LOW = 0, 1, 2
+GROW_NONE, GROW_HIGH, GROW_LOW, GROW_TOP = 0, 1, 2, 3
 REQ_IDLE, REQ_ADMITTING, REQ_ACTIVE, REQ_PENDING_FREE = 0, 1, 2, 3
 
 DECISION_DTYPE = np.dtype([("tc_class", "u1"), ("v_action", "u1"), ("grow", "u1"), ("demand", "u1"),
@@ -62,7 +62,8 @@ def build(force: bool = False) -> str:
 class Config(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("R", "Ly", "H", "d", "M", "W", "Ch", "Cl", "kbh", "vbh", "kbl", "vbl", "P")] + \
                [("alpha_h", C.c_float), ("alpha_l", C.c_float), ("prompt_denominator", C.c_int32),
-                ("prefill_workflow", C.c_int32), ("q_per_kv", C.c_int32)]
+                ("prefill_workflow", C.c_int32), ("q_per_kv", C.c_int32),
+                ("top_tier", C.c_int32), ("alpha_t", C.c_float), ("Ct", C.c_int32)]
 
 
 class ClassGeom(C.Structure):
@@ -72,7 +73,7 @@ class ClassGeom(C.Structure):
 
 class _Pool(C.Structure):
     _fields_ = [("c", Config), ("U", C.c_int32), ("L", C.c_int32), ("page_bytes", C.c_int32),
-                ("g", ClassGeom * 3),
+                ("g", ClassGeom * 5),
                 ("ring", C.POINTER(C.c_int32)), ("start", C.c_int64), ("free", C.c_int64),
                 ("table", C.POINTER(C.c_int32)), ("n_h", C.POINTER(C.c_int32)), ("n_l", C.POINTER(C.c_int32)),
                 ("req_state", C.POINTER(C.c_int8)), ("seq_len", C.POINTER(C.c_int32)),
@@ -83,7 +84,9 @@ class _Pool(C.Structure):
                 ("status", C.c_int32), ("last_phase", C.c_int32),
                 ("last_demand", C.c_int64), ("last_freed", C.c_int64), ("oom_count", C.c_int32),
                 ("last_reclaimed", C.c_int64), ("win_sig", C.POINTER(C.c_float)),
-                ("head_ah", C.POINTER(C.c_float)), ("head_al", C.POINTER(C.c_float)), ("use_head", C.c_int32)]
+                ("head_ah", C.POINTER(C.c_float)), ("head_al", C.POINTER(C.c_float)), ("use_head", C.c_int32),
+                ("Lt", C.c_int32), ("ttable", C.POINTER(C.c_int32)), ("n_t", C.POINTER(C.c_int32)),
+                ("pf_nt", C.POINTER(C.c_int32))]
 
 
 _lib = None
@@ -173,7 +176,8 @@ def unpack_codes(codes, d: int, bits: int) -> np.ndarray:
 
 def make_config(**kw) -> Config:
     defaults = dict(R=4, Ly=2, H=4, d=64, M=128, W=16, Ch=16, Cl=32, kbh=8, vbh=4, kbl=4, vbl=2, P=1024,
-                    alpha_h=1.0, alpha_l=0.02, prompt_denominator=0, prefill_workflow=0, q_per_kv=0)
+                    alpha_h=1.0, alpha_l=0.02, prompt_denominator=0, prefill_workflow=0, q_per_kv=0,
+                    top_tier=0, alpha_t=0.0, Ct=4)
     defaults.update(kw)
     return Config(**defaults)
 
@@ -202,6 +206,9 @@ class OraclePool:
         s = self._p.contents
         self.U, self.L, self.page_bytes = s.U, s.L, s.page_bytes
         self.geom = {CLS_HIGH: s.g[CLS_HIGH], CLS_LOW: s.g[CLS_LOW]}
+        if self.cfg.top_tier:
+            self.geom[CLS_TOP] = s.g[CLS_TOP]
+        self.Lt = s.Lt
         c = self.cfg
         self.LyH = c.Ly * c.H
 
@@ -219,6 +226,8 @@ class OraclePool:
         self.win_k = view(s.win_k, (self.U, c.W, c.d), C.c_uint16)
         self.win_v = view(s.win_v, (self.U, c.W, c.d), C.c_uint16)
         self.win_sig = view(s.win_sig, (self.U, c.W), C.c_float)
+        self.ttable = view(s.ttable, (self.U, self.Lt), C.c_int32)      # NEXT-4 TOP table
+        self.n_t = view(s.n_t, (self.U,), C.c_int32)
 
     def __del__(self):
         p = getattr(self, "_p", None)
@@ -344,6 +353,8 @@ class OraclePool:
     # --- read helpers for tests (plain indexing of the documented layout) ---
     def slot_location(self, cls, u, s):
         g = self.geom[cls]
+        if cls == CLS_TOP:
+            return int(self.ttable[u, s // g.C]), s % g.C
         k = s // g.C if cls == CLS_HIGH else self.L - 1 - s // g.C
         return int(self.table[u, k]), s % g.C
 
@@ -354,8 +365,8 @@ class OraclePool:
         pg = self.pages[pid]
         kc = pg[g.off_k + idx * g.k_row: g.off_k + (idx + 1) * g.k_row].copy()
         vc = pg[g.off_v + idx * g.v_row: g.off_v + (idx + 1) * g.v_row].copy()
-        km = int(pg[g.off_kmeta + 4 * idx: g.off_kmeta + 4 * idx + 4].view("<u4")[0])
-        vm = int(pg[g.off_vmeta + 4 * idx: g.off_vmeta + 4 * idx + 4].view("<u4")[0])
+        km = int(pg[g.off_kmeta + 4 * idx: g.off_kmeta + 4 * idx + 4].view("<u4")[0]) if cls != CLS_TOP else 0
+        vm = int(pg[g.off_vmeta + 4 * idx: g.off_vmeta + 4 * idx + 4].view("<u4")[0]) if cls != CLS_TOP else 0
         sg = int(pg[g.off_score + 4 * idx: g.off_score + 4 * idx + 4].view("<u4")[0])
         ps = int(pg[g.off_pos + 4 * idx: g.off_pos + 4 * idx + 4].view("<i4")[0])
         return kc, km, vc, vm, sg, ps

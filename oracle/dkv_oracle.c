@@ -154,6 +154,21 @@ static void class_geom(int32_t d, int32_t C, int32_t kb, int32_t vb, orc_class_g
   g->end = g->off_pos + 4 * C;
 }
 
+/* NEXT-4 (Q40): an FP16 (TOP) page holds Ct tokens as plain fp16 K and V rows (2d bytes each), no quantization
+   metadata, then the fp32 scores and int32 positions; segments 16-byte aligned in the same order. */
+static void class_geom_fp16(int32_t d, int32_t C, orc_class_geom* g) {
+  g->C = C; g->kbits = 16; g->vbits = 16;
+  g->k_row = 2 * d;
+  g->v_row = 2 * d;
+  g->off_k = 0;
+  g->off_kmeta = g->off_k + C * g->k_row;              /* empty */
+  g->off_v = align_up(g->off_kmeta, 16);
+  g->off_vmeta = g->off_v + C * g->v_row;              /* empty */
+  g->off_score = align_up(g->off_vmeta, 16);
+  g->off_pos = align_up(g->off_score + 4 * C, 16);
+  g->end = g->off_pos + 4 * C;
+}
+
 static int bits_ok(int32_t b) { return b == 2 || b == 4 || b == 8; }
 
 int32_t orc_geometry(const orc_config* c, int32_t* U, int32_t* L, int32_t* page_bytes,
@@ -164,12 +179,21 @@ int32_t orc_geometry(const orc_config* c, int32_t* U, int32_t* L, int32_t* page_
       c->alpha_h < 0 || c->alpha_l < 0 || (c->prompt_denominator != 0 && c->prompt_denominator != 1) ||
       (c->prefill_workflow != 0 && c->prefill_workflow != 1) || c->q_per_kv < 0 || c->q_per_kv > 16)
     return ORC_ERR_INVALID;
-  orc_class_geom gh, gl;
+  /* NEXT-4 (Q38, Q43): alpha_t >= alpha_h, the exact prompt workflow only */
+  if (c->top_tier != 0 && (c->top_tier != 1 || c->Ct < 1 || !isfinite(c->alpha_t) || c->alpha_t < c->alpha_h ||
+                           c->prefill_workflow != 0))
+    return ORC_ERR_INVALID;
+  orc_class_geom gh, gl, gt;
   class_geom(c->d, c->Ch, c->kbh, c->vbh, &gh);
   class_geom(c->d, c->Cl, c->kbl, c->vbl, &gl);
+  int32_t end = gh.end > gl.end ? gh.end : gl.end;
+  if (c->top_tier) {
+    class_geom_fp16(c->d, c->Ct, &gt);
+    if (gt.end > end) end = gt.end;
+  }
   if (U) *U = c->R * c->Ly * c->H;
   if (L) *L = (c->M + c->Ch - 1) / c->Ch + (c->W < c->Ch ? 1 : 0);
-  if (page_bytes) *page_bytes = align_up(gh.end > gl.end ? gh.end : gl.end, 128);
+  if (page_bytes) *page_bytes = align_up(end, 128);
   if (high) *high = gh;
   if (low) *low = gl;
   return ORC_OK;
@@ -193,6 +217,11 @@ orc_pool* orc_pool_new(const orc_config* c) {
     return NULL;
   }
   size_t U = (size_t)p->U, L = (size_t)p->L, P = (size_t)c->P, R = (size_t)c->R;
+  if (c->top_tier) class_geom_fp16(c->d, c->Ct, &p->g[ORC_CLS_TOP]);
+  p->Lt = c->top_tier ? (c->M + c->Ct - 1) / c->Ct : 1;         /* Q41: at most M tokens in the TOP section */
+  p->ttable = (int32_t*)malloc(U * (size_t)p->Lt * 4);
+  p->n_t = (int32_t*)calloc(U, 4);
+  p->pf_nt = (int32_t*)calloc(U, 4);
   p->ring = (int32_t*)malloc(P * 4);
   p->table = (int32_t*)malloc(U * L * 4);
   p->n_h = (int32_t*)calloc(U, 4);
@@ -210,12 +239,14 @@ orc_pool* orc_pool_new(const orc_config* c) {
   p->pf_nl = (int32_t*)calloc(U, 4);
   p->admit_list = (int32_t*)calloc(R, 4);
   if (!p->ring || !p->table || !p->n_h || !p->n_l || !p->req_state || !p->seq_len || !p->prompt_len ||
-      !p->pages || !p->win_k || !p->win_v || !p->win_sig || !p->pf_nh || !p->pf_nl || !p->admit_list) {
+      !p->pages || !p->win_k || !p->win_v || !p->win_sig || !p->pf_nh || !p->pf_nl || !p->admit_list ||
+      !p->ttable || !p->n_t || !p->pf_nt) {
     orc_pool_delete(p);
     return NULL;
   }
   for (size_t i = 0; i < P; i++) p->ring[i] = (int32_t)i;
   for (size_t i = 0; i < U * L; i++) p->table[i] = -1;
+  for (size_t i = 0; i < U * (size_t)p->Lt; i++) p->ttable[i] = -1;
   p->start = 0;
   p->free = c->P;
   p->last_phase = -1;
@@ -227,6 +258,7 @@ void orc_pool_delete(orc_pool* p) {
   free(p->ring); free(p->table); free(p->n_h); free(p->n_l); free(p->req_state); free(p->seq_len);
   free(p->prompt_len); free(p->pages); free(p->win_k); free(p->win_v); free(p->pf_nh); free(p->pf_nl);
   free(p->admit_list); free(p->win_sig); free(p->head_ah); free(p->head_al);
+  free(p->ttable); free(p->n_t); free(p->pf_nt);
   free(p);
 }
 
@@ -238,8 +270,13 @@ int32_t orc_take_status(orc_pool* p) { int32_t s = p->status; p->status = ORC_OK
    right), index s mod C (c.1). */
 static uint8_t* slot_page(orc_pool* p, int cls, int32_t u, int32_t s, int32_t* idx) {
   const orc_class_geom* g = &p->g[cls];
-  int32_t k = (cls == ORC_CLS_HIGH) ? s / g->C : p->L - 1 - s / g->C;
-  int32_t pid = p->table[(size_t)u * p->L + k];
+  int32_t pid;
+  if (cls == ORC_CLS_TOP) {                              /* Q41: TOP slot s at ttable[u][s / Ct] */
+    pid = p->ttable[(size_t)u * p->Lt + s / g->C];
+  } else {
+    int32_t k = (cls == ORC_CLS_HIGH) ? s / g->C : p->L - 1 - s / g->C;
+    pid = p->table[(size_t)u * p->L + k];
+  }
   *idx = s % g->C;
   return p->pages + (size_t)pid * (size_t)p->page_bytes;
 }
@@ -275,7 +312,34 @@ static int32_t write_token(orc_pool* p, int cls, int32_t u, int32_t s, const flo
   return ORC_OK;
 }
 
+/* NEXT-4 (Q40): a TOP token is stored as its fp16 K and V rows as given (no quantization); Q30 applies. */
+static int32_t write_token_top(orc_pool* p, int32_t u, int32_t s, const uint16_t* k, const uint16_t* v, float sig,
+                               int32_t pos) {
+  const orc_class_geom* g = &p->g[ORC_CLS_TOP];
+  for (int32_t i = 0; i < p->c.d; i++)
+    if (!isfinite(orc_f32_from_f16(k[i])) || !isfinite(orc_f32_from_f16(v[i]))) return ORC_ERR_NONFINITE;
+  int32_t idx; uint8_t* pg = slot_page(p, ORC_CLS_TOP, u, s, &idx);
+  memcpy(pg + g->off_k + idx * g->k_row, k, (size_t)g->k_row);
+  memcpy(pg + g->off_v + idx * g->v_row, v, (size_t)g->v_row);
+  memcpy(pg + g->off_score + 4 * idx, &sig, 4);
+  memcpy(pg + g->off_pos + 4 * idx, &pos, 4);
+  return ORC_OK;
+}
+
 static void read_token(orc_pool* p, int cls, int32_t u, int32_t s, float* k, float* v, float* sig, int32_t* pos) {
+  if (cls == ORC_CLS_TOP) {                              /* fp16 values, exactly */
+    const orc_class_geom* g = &p->g[ORC_CLS_TOP];
+    int32_t idx; uint8_t* pg = slot_page(p, cls, u, s, &idx);
+    for (int32_t i = 0; i < p->c.d; i++) {
+      uint16_t hk, hv;
+      memcpy(&hk, pg + g->off_k + idx * g->k_row + 2 * i, 2);
+      memcpy(&hv, pg + g->off_v + idx * g->v_row + 2 * i, 2);
+      k[i] = orc_f32_from_f16(hk); v[i] = orc_f32_from_f16(hv);
+    }
+    memcpy(sig, pg + g->off_score + 4 * idx, 4);
+    memcpy(pos, pg + g->off_pos + 4 * idx, 4);
+    return;
+  }
   const orc_class_geom* g = &p->g[cls];
   int32_t idx; uint8_t* pg = slot_page(p, cls, u, s, &idx);
   uint16_t ks, kz, vs, vz;
@@ -332,11 +396,15 @@ int32_t orc_classify_decode(orc_pool* p, const float* cand_sig, orc_decision* de
     if (sc == 0.0f) sc = 0.0f;                                /* canonicalise -0 -> +0 (Q6) */
     float th = unit_ah(p, u) / (float)N;                      /* alpha_h / N */
     float tl = unit_al(p, u) / (float)N;                      /* alpha_l / N */
+    /* NEXT-4 (Q38, Q39): with the FP16 tier, t_c at or above alpha_t / N is TOP */
+    const int top = c->top_tier != 0;
+    float tt = top ? c->alpha_t / (float)N : 0.0f;
     int cls;
-    if (sc >= th) cls = ORC_CLS_HIGH;                         /* line q_high */
+    if (top && sc >= tt) cls = ORC_CLS_TOP;
+    else if (sc >= th) cls = ORC_CLS_HIGH;                    /* line q_high */
     else if (sc >= tl) cls = ORC_CLS_LOW;                     /* line q_low  */
     else { D->tc_class = ORC_CLS_PRUNED; continue; }          /* t_c pruned */
-    int32_t n = (cls == ORC_CLS_HIGH) ? p->n_h[u] : p->n_l[u];
+    int32_t n = cls == ORC_CLS_TOP ? p->n_t[u] : ((cls == ORC_CLS_HIGH) ? p->n_h[u] : p->n_l[u]);
     /* t_v = argmin over the section with t_c added (lines v_high / v_low). */
     int32_t vslot = -1; float vs = sc; int32_t vp = pc;       /* start from t_c itself */
     for (int32_t s = 0; s < n; s++) {
@@ -345,7 +413,23 @@ int32_t orc_classify_decode(orc_pool* p, const float* cand_sig, orc_decision* de
       if (sg < vs || (sg == vs && ps < vp)) { vs = sg; vp = ps; vslot = s; }
     }
     D->tc_class = (uint8_t)cls;
-    if (cls == ORC_CLS_HIGH) {
+    if (cls == ORC_CLS_TOP) {                                 /* Q39: Algorithm 1 one level up */
+      if (vslot < 0 || vs >= tt) {                            /* t_v stays in KV_t */
+        D->v_action = ORC_V_KEEP; D->grow = ORC_GROW_TOP;
+        D->demand = (p->n_t[u] % c->Ct == 0); D->tc_slot = p->n_t[u];
+      } else if (vs >= th) {                                  /* t_v moves to KV_h (re-quantized at P_h) */
+        D->v_action = ORC_V_DOWN; D->grow = ORC_GROW_HIGH;
+        D->demand = (p->n_h[u] % c->Ch == 0);
+        D->v_slot = vslot; D->tc_slot = vslot; D->v_dst_slot = p->n_h[u];
+      } else if (vs >= tl) {                                  /* t_v moves to KV_l (re-quantized at P_l) */
+        D->v_action = ORC_V_DOWN; D->grow = ORC_GROW_LOW;
+        D->demand = (p->n_l[u] % c->Cl == 0);
+        D->v_slot = vslot; D->tc_slot = vslot; D->v_dst_slot = p->n_l[u];
+      } else {                                                /* prune t_v */
+        D->v_action = ORC_V_PRUNE; D->grow = ORC_GROW_NONE; D->demand = 0;
+        D->v_slot = vslot; D->tc_slot = vslot;
+      }
+    } else if (cls == ORC_CLS_HIGH) {
       if (vslot < 0 || vs >= th) {                            /* t_v stays in KV_h */
         D->v_action = ORC_V_KEEP; D->grow = ORC_GROW_HIGH;
         D->demand = (p->n_h[u] % c->Ch == 0); D->tc_slot = p->n_h[u];
@@ -396,7 +480,9 @@ int32_t orc_set_head_thresholds(orc_pool* p, const float* alpha_h, const float* 
   int32_t LyH = p->c.Ly * p->c.H;
   if (!alpha_h || !alpha_l) { p->use_head = 0; return ORC_OK; }
   for (int32_t i = 0; i < LyH; i++)
-    if (!isfinite(alpha_h[i]) || !isfinite(alpha_l[i]) || alpha_h[i] < 0 || alpha_l[i] < 0) return ORC_ERR_INVALID;
+    if (!isfinite(alpha_h[i]) || !isfinite(alpha_l[i]) || alpha_h[i] < 0 || alpha_l[i] < 0 ||
+        (p->c.top_tier && alpha_h[i] > p->c.alpha_t))                 /* Q38: alpha_t >= alpha_h */
+      return ORC_ERR_INVALID;
   if (!p->head_ah) { p->head_ah = (float*)malloc(4 * (size_t)LyH); p->head_al = (float*)malloc(4 * (size_t)LyH); }
   if (!p->head_ah || !p->head_al) return ORC_ERR_INVALID;
   memcpy(p->head_ah, alpha_h, 4 * (size_t)LyH);
@@ -409,6 +495,7 @@ static int prompt_class(const orc_pool* p, int32_t u, float s, int32_t t, int32_
   const orc_config* c = &p->c;
   float den = (c->prompt_denominator == 0) ? (float)(t + 1) : (float)n;
   float th = unit_ah(p, u) / den, tl = unit_al(p, u) / den;
+  if (c->top_tier && s >= c->alpha_t / den) return ORC_CLS_TOP;     /* NEXT-4 (Q38) */
   if (s >= th) return ORC_CLS_HIGH;
   if (s >= tl) return ORC_CLS_LOW;
   return ORC_CLS_PRUNED;
@@ -429,7 +516,7 @@ int32_t orc_classify_prefill(orc_pool* p, const int32_t* req, const int32_t* len
       int32_t u = r * LyH + j;
       const float* row = sig + ((int64_t)i * LyH + j) * sig_stride;
       uint8_t* crow = token_class ? token_class + ((int64_t)i * LyH + j) * sig_stride : NULL;
-      int32_t nh = 0, nl = 0;
+      int32_t nh = 0, nl = 0, nt = 0;
       for (int32_t t = 0; t < T; t++) {
         int cls = ORC_CLS_NONE;                               /* window token */
         if (t < T - c->W && st0 == ORC_OK) {
@@ -438,11 +525,13 @@ int32_t orc_classify_prefill(orc_pool* p, const int32_t* req, const int32_t* len
           cls = prompt_class(p, u, s, t, T);
           if (cls == ORC_CLS_HIGH) nh++;
           if (cls == ORC_CLS_LOW) nl++;
+          if (cls == ORC_CLS_TOP) nt++;
         }
         if (crow) crow[t] = (uint8_t)cls;
       }
       p->pf_nh[u] = nh;
       p->pf_nl[u] = nl;
+      p->pf_nt[u] = nt;
     }
   }
   return ORC_OK;
@@ -525,6 +614,15 @@ int32_t orc_compact_alloc(orc_pool* p, const orc_decision* dec) {
     if (p->req_state[r] != ORC_REQ_PENDING_FREE) continue;
     for (int32_t j = 0; j < LyH; j++) {
       int32_t u = r * LyH + j;
+      for (int32_t k = 0; k < p->Lt; k++) {                     /* NEXT-4 (Q41): the TOP table's slots first */
+        int32_t* slot = &p->ttable[(size_t)u * p->Lt + k];
+        if (*slot != -1) {
+          p->ring[(p->start + p->free) % P] = *slot;
+          p->free += 1; freed += 1;
+          *slot = -1;
+        }
+      }
+      p->n_t[u] = 0;
       for (int32_t k = 0; k < L; k++) {
         int32_t* slot = &p->table[(size_t)u * L + k];
         if (*slot != -1) {
@@ -549,7 +647,8 @@ int32_t orc_compact_alloc(orc_pool* p, const orc_decision* dec) {
       if (p->req_state[r] == ORC_REQ_ACTIVE) D += dec[u].demand;
     } else if (p->req_state[r] == ORC_REQ_ADMITTING) {
       if (c->prefill_workflow == 1) D += conservative_pages(p, u) + topup_pages(p, u);
-      else D += ceil_div(p->pf_nh[u], c->Ch) + ceil_div(p->pf_nl[u], c->Cl);
+      else D += ceil_div(p->pf_nh[u], c->Ch) + ceil_div(p->pf_nl[u], c->Cl) +
+                (c->top_tier ? ceil_div(p->pf_nt[u], c->Ct) : 0);
     }
   }
   p->last_demand = D;
@@ -562,6 +661,12 @@ int32_t orc_compact_alloc(orc_pool* p, const orc_decision* dec) {
     int32_t* row = &p->table[(size_t)u * L];
     if (p->last_phase == ORC_DECODE) {
       if (p->req_state[r] != ORC_REQ_ACTIVE || !dec[u].demand) continue;
+      if (dec[u].grow == ORC_GROW_TOP) {                        /* NEXT-4: the TOP table, left to right */
+        if (p->n_t[u] / c->Ct >= p->Lt) { set_status(p, ORC_ERR_OVERFLOW); continue; }
+        p->ttable[(size_t)u * p->Lt + p->n_t[u] / c->Ct] = p->ring[(p->start + off) % P];
+        off += 1;
+        continue;
+      }
       int32_t ph = ceil_div(p->n_h[u], c->Ch), pl = ceil_div(p->n_l[u], c->Cl);
       if (ph + pl + 1 > L) { set_status(p, ORC_ERR_OVERFLOW); continue; }
       int32_t k = (dec[u].grow == ORC_GROW_HIGH) ? p->n_h[u] / c->Ch : L - 1 - p->n_l[u] / c->Cl;
@@ -569,6 +674,10 @@ int32_t orc_compact_alloc(orc_pool* p, const orc_decision* dec) {
       off += 1;
     } else if (c->prefill_workflow == 0) {
       if (p->req_state[r] != ORC_REQ_ADMITTING) continue;
+      if (c->top_tier) {                                         /* Q41/Q43: a unit's TOP pages come first */
+        int32_t pt = ceil_div(p->pf_nt[u], c->Ct);
+        for (int32_t k = 0; k < pt; k++) { p->ttable[(size_t)u * p->Lt + k] = p->ring[(p->start + off) % P]; off += 1; }
+      }
       int32_t ph = ceil_div(p->pf_nh[u], c->Ch), pl = ceil_div(p->pf_nl[u], c->Cl);
       if (ph + pl > L) { set_status(p, ORC_ERR_OVERFLOW); off += ph + pl; continue; }
       for (int32_t k = 0; k < ph; k++) { row[k] = p->ring[(p->start + off) % P]; off += 1; }
@@ -586,9 +695,11 @@ int32_t orc_compact_alloc(orc_pool* p, const orc_decision* dec) {
       if (p->req_state[r] != ORC_REQ_ACTIVE) continue;
       if (dec[u].grow == ORC_GROW_HIGH) p->n_h[u] += 1;
       if (dec[u].grow == ORC_GROW_LOW) p->n_l[u] += 1;       /* DOWN: n_h unchanged, n_l + 1 */
+      if (dec[u].grow == ORC_GROW_TOP) p->n_t[u] += 1;
     } else if (p->req_state[r] == ORC_REQ_ADMITTING) {
       p->n_h[u] = p->pf_nh[u];
       p->n_l[u] = p->pf_nl[u];
+      p->n_t[u] = c->top_tier ? p->pf_nt[u] : 0;
     }
   }
   for (int32_t r = 0; r < c->R; r++) {
@@ -615,15 +726,23 @@ int32_t orc_quant_write_decode(orc_pool* p, const orc_decision* dec, const uint1
     int32_t N = p->seq_len[r];                      /* already includes the new token */
     int32_t pc = N - 1 - W;
     if (D->v_action == ORC_V_DOWN) {
+      /* the victim leaves the section t_c joins for the class `grow` (Q9; NEXT-4 Q42: a TOP victim's fp16
+         values are quantized as they are) */
       float sg; int32_t ps;
-      read_token(p, ORC_CLS_HIGH, u, D->v_slot, kx, vx, &sg, &ps);
-      int32_t st = write_token(p, ORC_CLS_LOW, u, D->v_dst_slot, kx, vx, sg, ps);
+      read_token(p, D->tc_class, u, D->v_slot, kx, vx, &sg, &ps);
+      int32_t st = write_token(p, D->grow, u, D->v_dst_slot, kx, vx, sg, ps);
       if (st != ORC_OK) { set_status(p, st); continue; }
     }
     const uint16_t* kn = k_new + (size_t)u * d; const uint16_t* vn = v_new + (size_t)u * d;
     uint16_t* wk = W ? p->win_k + ((size_t)u * W + (size_t)((N - 1) % W)) * d : NULL;
     uint16_t* wv = W ? p->win_v + ((size_t)u * W + (size_t)((N - 1) % W)) * d : NULL;
-    if (D->tc_class == ORC_CLS_HIGH || D->tc_class == ORC_CLS_LOW) {
+    if (D->tc_class == ORC_CLS_TOP) {                         /* NEXT-4: t_c kept in FP16 */
+      const uint16_t* sk = W ? wk : kn; const uint16_t* sv = W ? wv : vn;
+      float sc = cand_sig ? cand_sig[u] : (W ? p->win_sig[(size_t)u * W + (size_t)((N - 1) % W)] : 0.0f);
+      if (sc == 0.0f) sc = 0.0f;
+      int32_t st = write_token_top(p, u, D->tc_slot, sk, sv, sc, pc);
+      if (st != ORC_OK) { set_status(p, st); continue; }
+    } else if (D->tc_class == ORC_CLS_HIGH || D->tc_class == ORC_CLS_LOW) {
       /* t_c sits in window slot p_c mod W == (N-1) mod W; read it before the push overwrites it */
       const uint16_t* sk = W ? wk : kn; const uint16_t* sv = W ? wv : vn;
       for (int32_t i = 0; i < d; i++) { kx[i] = orc_f32_from_f16(sk[i]); vx[i] = orc_f32_from_f16(sv[i]); }
@@ -664,7 +783,7 @@ int32_t orc_quant_write_prefill(orc_pool* p, const uint16_t* k, const uint16_t* 
     if (p->req_state[r] != ORC_REQ_ADMITTING) continue;
     for (int32_t j = 0; j < LyH; j++) {
       int32_t u = r * LyH + j;
-      int32_t h = 0, l = 0;
+      int32_t h = 0, l = 0, tp = 0;
       for (int32_t t = 0; t < T; t++) {
         const uint16_t* kr = k + (((int64_t)i * LyH + j) * kv_stride + t) * d;
         const uint16_t* vr = v + (((int64_t)i * LyH + j) * kv_stride + t) * d;
@@ -673,6 +792,11 @@ int32_t orc_quant_write_prefill(orc_pool* p, const uint16_t* k, const uint16_t* 
           if (s == 0.0f) s = 0.0f;
           int cls = prompt_class(p, u, s, t, T);
           if (cls == ORC_CLS_PRUNED) continue;
+          if (cls == ORC_CLS_TOP) {                             /* NEXT-4: FP16 rows as given */
+            int32_t st = write_token_top(p, u, tp++, kr, vr, s, t);
+            if (st != ORC_OK) set_status(p, st);
+            continue;
+          }
           for (int32_t e = 0; e < d; e++) { kx[e] = orc_f32_from_f16(kr[e]); vx[e] = orc_f32_from_f16(vr[e]); }
           int32_t slot = (cls == ORC_CLS_HIGH) ? h++ : l++;
           int32_t st = write_token(p, cls, u, slot, kx, vx, s, t);
@@ -768,7 +892,7 @@ static void att_val(const orc_pool* p, const att_tok* t, float* v) {
 
 int32_t orc_attend(orc_pool* p, const uint16_t* q, float* out, float* probs) {
   const orc_config* c = &p->c;
-  if (c->q_per_kv < 1) return ORC_ERR_INVALID;
+  if (c->q_per_kv < 1 || c->top_tier) return ORC_ERR_INVALID;     /* NEXT-4 tier: no attention (Q44) */
   if (p->status != ORC_OK) return ORC_OK;
   const int32_t LyH = c->Ly * c->H, d = c->d, W = c->W, G = c->q_per_kv, M = c->M;
   att_tok* tok = (att_tok*)malloc(sizeof(att_tok) * (size_t)M);

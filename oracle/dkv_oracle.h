@@ -23,9 +23,9 @@ extern "C" {
 enum { ORC_OK = 0, ORC_ERR_INVALID = -1, ORC_ERR_STATE = -2, ORC_ERR_OOM = -3,
        ORC_ERR_NONFINITE = -4, ORC_ERR_OVERFLOW = -5 };
 enum { ORC_DECODE = 0, ORC_PREFILL = 1 };
-enum { ORC_CLS_NONE = 0, ORC_CLS_HIGH = 1, ORC_CLS_LOW = 2, ORC_CLS_PRUNED = 3 };
+enum { ORC_CLS_NONE = 0, ORC_CLS_HIGH = 1, ORC_CLS_LOW = 2, ORC_CLS_PRUNED = 3, ORC_CLS_TOP = 4 };   /* TOP: NEXT-4 FP16 tier */
 enum { ORC_V_NONE = 0, ORC_V_KEEP = 1, ORC_V_DOWN = 2, ORC_V_PRUNE = 3 };
-enum { ORC_GROW_NONE = 0, ORC_GROW_HIGH = 1, ORC_GROW_LOW = 2 };
+enum { ORC_GROW_NONE = 0, ORC_GROW_HIGH = 1, ORC_GROW_LOW = 2, ORC_GROW_TOP = 3 };
 enum { ORC_REQ_IDLE = 0, ORC_REQ_ADMITTING = 1, ORC_REQ_ACTIVE = 2, ORC_REQ_PENDING_FREE = 3 };
 
 typedef struct {
@@ -39,6 +39,11 @@ typedef struct {
   int32_t prefill_workflow;     /* 0 = exact allocation after planning; 1 = the paper's prompt workflow
                                    (Fig. 5): conservative allocation, planning, reclaim (Q29) */
   int32_t q_per_kv;             /* NEXT-2: query heads per KV head (GQA group); 0 = no attention */
+  /* NEXT-4 three-level tier FP16-K8V4-K4V2 (readings Q38-Q44): 1 adds the FP16 class TOP
+     above High, threshold alpha_t >= alpha_h, pages of Ct FP16 tokens in a unidirectional table */
+  int32_t top_tier;
+  float alpha_t;
+  int32_t Ct;
 } orc_config;
 
 /* 16-byte decision record per unit (same byte layout the product's ABI documents). */
@@ -57,7 +62,7 @@ typedef struct {
 typedef struct orc_pool {
   orc_config c;
   int32_t U, L, page_bytes;
-  orc_class_geom g[3];                      /* index ORC_CLS_HIGH / ORC_CLS_LOW */
+  orc_class_geom g[5];                      /* index ORC_CLS_HIGH / ORC_CLS_LOW / ORC_CLS_TOP */
   int32_t *ring; int64_t start, free;       /* circular free page list */
   int32_t *table;                           /* [U][L] bidirectional page table */
   int32_t *n_h, *n_l;                       /* [U] stored tokens per section */
@@ -74,6 +79,9 @@ typedef struct orc_pool {
   float   *win_sig;                         /* [U][W] significance of the window tokens (running averages) */
   float   *head_ah, *head_al;               /* NEXT-4: [Ly*H] per-(layer, head) thresholds (Q35) */
   int32_t use_head;                         /* 1: the per-head thresholds replace alpha_h / alpha_l */
+  int32_t Lt;                               /* NEXT-4: slots of the unidirectional FP16 (TOP) table */
+  int32_t *ttable;                          /* [U][Lt] TOP page table, filled left to right (Q41) */
+  int32_t *n_t, *pf_nt;                     /* [U] stored TOP tokens; prefill TOP counts */
 } orc_pool;
 
 /* --- scalar primitives (exported for the pins) --- */

@@ -71,6 +71,44 @@ __device__ __forceinline__ void bf2_split(float x0, float x1, uint32_t& hi, uint
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
+// Exact code -> fp16 / bf16 conversion with byte permutes: a w-bit field whose lowest bit sits at mantissa bit b
+// of a half with exponent chosen so that that bit weighs exactly 1 (magic M) holds the value M + code; one
+// subtraction of M (exact) leaves the code.  x2 = [f0 in the low half | f1 in the high half] after masking.
+__device__ __forceinline__ uint32_t hsub2_u(uint32_t x, uint32_t m) {
+  const __half2 r = __hsub2(*reinterpret_cast<const __half2*>(&x), *reinterpret_cast<const __half2*>(&m));
+  return *reinterpret_cast<const uint32_t*>(&r);
+}
+__device__ __forceinline__ uint32_t bsub2_u(uint32_t x, uint32_t m) {
+  const __nv_bfloat162 r = __hsub2(*reinterpret_cast<const __nv_bfloat162*>(&x), *reinterpret_cast<const __nv_bfloat162*>(&m));
+  return *reinterpret_cast<const uint32_t*>(&r);
+}
+// K8: bytes (c0, c1, c2, c3) of x -> fp16x2 (c0, c1) and (c2, c3): 0x64XX = 1024 + XX
+__device__ __forceinline__ void k8_pairs(uint32_t x, uint32_t& lo, uint32_t& hi) {
+  lo = hsub2_u(__byte_perm(x, 0x64646464u, 0x4140), 0x64006400u);
+  hi = hsub2_u(__byte_perm(x, 0x64646464u, 0x4342), 0x64006400u);
+}
+// K4: the two bytes at byte index KB0 (codes n0 | n1 << 4) and KB0 + 1 (n2 | n3 << 4) of x -> fp16x2 (n0, n1),
+// (n2, n3): n0 in bits 0-3 with 0x6400 (1024, ulp 1), n1 in bits 20-23 = bits 4-7 of the high half with 0x5400
+// (64, ulp 1/16)
+template <int KB0>
+__device__ __forceinline__ void k4_pairs(uint32_t x, uint32_t& lo, uint32_t& hi) {
+  constexpr uint32_t s0 = KB0 * 0x1111u, s1 = (KB0 + 1) * 0x1111u;
+  lo = hsub2_u((__byte_perm(x, 0u, s0) & 0x00F0000Fu) | 0x54006400u, 0x54006400u);
+  hi = hsub2_u((__byte_perm(x, 0u, s1) & 0x00F0000Fu) | 0x54006400u, 0x54006400u);
+}
+// V: byte K of x (token j0) and of y (token j1) -> bf16x2 (field of j0, field of j1) for the field at bits
+// [SH, SH + VB) of that byte; the magic makes bit SH weigh 1 in bf16 (7 mantissa bits)
+template <int K, int SH, int VB>
+__device__ __forceinline__ uint32_t v_pair(uint32_t x, uint32_t y) {
+  constexpr uint32_t sel = K | (K << 4) | ((4 + K) << 8) | ((4 + K) << 12);
+  constexpr uint32_t mask = (((1u << VB) - 1u) << SH) * 0x00010001u;
+  // bf16 with 7 explicit mantissa bits: a value in [2^e, 2^(e+1)) has ulp 2^(e-7); bit SH weighs 1 when
+  // 2^(e-7) * 2^SH = 1, i.e. e = 7 - SH: 128.0 (0x4300) for SH = 0, 8.0 (0x4100) for 4, 32.0 (0x4200) for 2,
+  // 2.0 (0x4000) for 6
+  constexpr uint32_t magic = (SH == 0 ? 0x4300u : SH == 2 ? 0x4200u : SH == 4 ? 0x4100u : 0x4000u) * 0x00010001u;
+  return bsub2_u((__byte_perm(x, y, sel) & mask) | magic, magic);
+}
+
 // Compile-time geometry of one precision class (the paper's K8V4 high / K4V2 low pages): tokens per
 // page, bit widths, code row bytes, 16-B chunks per row and the row swizzle shifts of the staged copies.
 template <int D, int C_, int KB, int VB>
@@ -142,15 +180,16 @@ __device__ __forceinline__ void qk_page(const uint8_t* kseg, int t0, int cnt, co
     lds_row<RB, CL::kc, CL::ksh>(kseg, tile * 16 + grp + 8, CL::k_row, RB * tig, w[1]);
 #pragma unroll
     for (int g = 0; g < D / 16; g++) {
-      uint32_t a[4];
-#pragma unroll
+      uint32_t a[4];                                             // a0 / a1: k = 2 tig, 2 tig + 1 (rows grp, grp + 8)
+#pragma unroll                                                   // a2 / a3: k = 2 tig + 8, 2 tig + 9
       for (int rr = 0; rr < 2; rr++) {
-        constexpr int KB = CL::kbits;
-        const int bit = 4 * g * KB;                              // features 4g .. 4g+3 of the lane's run
-        const uint32_t x = w[rr][bit >> 5] >> (bit & 31);
-        constexpr uint32_t Q = (1u << KB) - 1u;
-        a[rr] = h2_codes(x & Q, (x >> KB) & Q);                  // a0 / a1: k = 2 tig, 2 tig + 1
-        a[2 + rr] = h2_codes((x >> (2 * KB)) & Q, (x >> (3 * KB)) & Q);   // a2 / a3: k = 2 tig + 8, 2 tig + 9
+        if constexpr (CL::kbits == 8) {
+          k8_pairs(w[rr][g], a[rr], a[2 + rr]);                  // features 4g .. 4g+3 = word g of the run
+        } else {
+          static_assert(CL::kbits == 4, "tensor-core path: K8 or K4 keys");
+          if (g & 1) k4_pairs<2>(w[rr][g >> 1], a[rr], a[2 + rr]);   // bytes 2g, 2g+1 of the run
+          else k4_pairs<0>(w[rr][g >> 1], a[rr], a[2 + rr]);
+        }
       }
       mma_f16(acc, a, qb[g][0], qb[g][1]);
     }
@@ -210,21 +249,36 @@ __device__ __forceinline__ void pv_page(const uint8_t* vseg, int t0, int cnt, co
     for (int jj = 0; jj < 4; jj++) lds_row<RB, CL::vc, CL::vsh>(vseg, tile * 16 + 4 * tig + jj, CL::v_row, RB * grp, w[jj]);
 #pragma unroll
     for (int g = 0; g < D / 16; g++) {
-      constexpr int VB = CL::vbits;
-      constexpr uint32_t Q = (1u << VB) - 1u;
-      const int bit = 2 * g * VB;                                // features 2g, 2g + 1 of the lane's run
-      uint32_t c0[4], c1[4];
-#pragma unroll
-      for (int jj = 0; jj < 4; jj++) {
-        const uint32_t x = w[jj][bit >> 5] >> (bit & 31);
-        c0[jj] = x & Q;
-        c1[jj] = (x >> VB) & Q;
-      }
+      // features 2g, 2g + 1 of the lane's run: V4 -> byte g (low / high nibble); V2 -> byte g/2, crumbs at bits
+      // 4(g&1) and 4(g&1) + 2.  a0 / a2: feature row grp (f0), tokens (4 tig, 4 tig+1) / (4 tig+2, 4 tig+3);
+      // a1 / a3: feature row grp + 8 (f0 + 1)
       uint32_t a[4];
-      a[0] = bf2_codes(c0[0], c0[1]);                          // feature row grp, tokens 4 tig, 4 tig + 1
-      a[1] = bf2_codes(c1[0], c1[1]);                          // feature row grp + 8
-      a[2] = bf2_codes(c0[2], c0[3]);                          // feature row grp, tokens 4 tig + 2, 4 tig + 3
-      a[3] = bf2_codes(c1[2], c1[3]);
+      if constexpr (CL::vbits == 4) {
+        const int wi = g >> 2;
+        switch (g & 3) {
+#define DKV_V4(K)                                                                             \
+          case K:                                                                             \
+            a[0] = v_pair<K, 0, 4>(w[0][wi], w[1][wi]); a[1] = v_pair<K, 4, 4>(w[0][wi], w[1][wi]); \
+            a[2] = v_pair<K, 0, 4>(w[2][wi], w[3][wi]); a[3] = v_pair<K, 4, 4>(w[2][wi], w[3][wi]); \
+            break;
+          DKV_V4(0) DKV_V4(1) DKV_V4(2) DKV_V4(3)
+#undef DKV_V4
+        }
+      } else {
+        static_assert(CL::vbits == 2, "tensor-core path: V4 or V2 values");
+        const int wi = g >> 3;
+        switch (g & 7) {
+#define DKV_V2(G8)                                                                                      \
+          case G8:                                                                                      \
+            a[0] = v_pair<(G8 & 7) / 2, 4 * (G8 & 1), 2>(w[0][wi], w[1][wi]);                          \
+            a[1] = v_pair<(G8 & 7) / 2, 4 * (G8 & 1) + 2, 2>(w[0][wi], w[1][wi]);                      \
+            a[2] = v_pair<(G8 & 7) / 2, 4 * (G8 & 1), 2>(w[2][wi], w[3][wi]);                          \
+            a[3] = v_pair<(G8 & 7) / 2, 4 * (G8 & 1) + 2, 2>(w[2][wi], w[3][wi]);                      \
+            break;
+          DKV_V2(0) DKV_V2(1) DKV_V2(2) DKV_V2(3) DKV_V2(4) DKV_V2(5) DKV_V2(6) DKV_V2(7)
+#undef DKV_V2
+        }
+      }
       mma_bf16(acc[g], a, bh0, bh1);
       mma_bf16(acc[g], a, bl0, bl1);
     }

@@ -43,6 +43,9 @@ class Scenario:
     h0: int = 0
     tile_units: int = 0
     req_ids: tuple | None = None      # global request ids of the local slots (sampled sub-pools)
+    top_tier: int = 0                 # NEXT-4: FP16 tier above K8V4 (Q38-Q44)
+    alpha_t: float = 0.0
+    Ct: int = 4
 
     @property
     def shape(self) -> synth.Shape:
@@ -59,7 +62,7 @@ class Scenario:
     def config_dict(self):
         return {k: getattr(self, k) for k in ("R", "Ly", "H", "d", "M", "W", "Ch", "Cl", "kbh", "vbh", "kbl", "vbl",
                                               "P", "alpha_h", "alpha_l", "prompt_denominator",
-                                              "prefill_workflow", "q_per_kv")}
+                                              "prefill_workflow", "q_per_kv", "top_tier", "alpha_t", "Ct")}
 
     def replace(self, **kw):
         return dataclasses.replace(self, **kw)
@@ -114,7 +117,7 @@ class OracleBackend:
         g = self.pool.geom
         self.geom = {c: dict(C=g[c].C, k_row=g[c].k_row, v_row=g[c].v_row, off_k=g[c].off_k,
                              off_kmeta=g[c].off_kmeta, off_v=g[c].off_v, off_vmeta=g[c].off_vmeta,
-                             off_score=g[c].off_score, off_pos=g[c].off_pos) for c in (1, 2)}
+                             off_score=g[c].off_score, off_pos=g[c].off_pos) for c in g}
 
     def classify_decode(self, cand):
         return self.pool.classify_decode(None if cand is None else _np(cand))
@@ -156,6 +159,8 @@ class OracleBackend:
         s = dict(ring=p.ring.copy(), start=int(p.start), free=int(p.free), table=p.table.copy(),
                  n_h=p.n_h.copy(), n_l=p.n_l.copy(), req_state=p.req_state.copy(), seq_len=p.seq_len.copy(),
                  win_k=p.win_k.copy(), win_v=p.win_v.copy(), win_sig=p.win_sig.copy())
+        if self.scn.top_tier:
+            s.update(ttable=p.ttable.copy(), n_t=p.n_t.copy())
         if pages:
             s["pages"] = p.pages.copy()
         return s
@@ -265,6 +270,11 @@ def check_invariants(snap, scn: Scenario, L: int, geom, life: Lifecycle | None =
     assert 0 <= free <= P and 0 <= start < P
     free_ids = ring[(start + np.arange(free)) % P]
     used = table[table >= 0]
+    if "ttable" in snap:                              # NEXT-4: the TOP table's pages, slots [0, pt) occupied
+        tt = snap["ttable"]
+        used = np.concatenate([used, tt[tt >= 0]])
+        pt = ceil_div(snap["n_t"], scn.Ct)
+        assert np.array_equal(tt >= 0, np.arange(tt.shape[1])[None, :] < pt[:, None]), "TOP slots not [0, pt)"
     allids = np.concatenate([free_ids, used])
     assert allids.size == P, f"used + free = {allids.size} != P = {P}"
     assert np.array_equal(np.sort(allids), np.arange(P)), "a page is owned twice or lost"
@@ -283,15 +293,20 @@ def check_invariants(snap, scn: Scenario, L: int, geom, life: Lifecycle | None =
                 continue
             N = int(snap["seq_len"][r])
             poss = []
-            for cls, n in ((1, n_h[u]), (2, n_l[u])):
+            secs = ((1, n_h[u]), (2, n_l[u])) + (((4, snap["n_t"][u]),) if "ttable" in snap else ())
+            for cls, n in secs:
                 g = geom[cls]
                 for s in range(int(n)):
-                    kk = s // g["C"] if cls == 1 else L - 1 - s // g["C"]
-                    pid = table[u, kk]
+                    if cls == 4:
+                        pid = snap["ttable"][u, s // g["C"]]
+                    else:
+                        kk = s // g["C"] if cls == 1 else L - 1 - s // g["C"]
+                        pid = table[u, kk]
                     idx = s % g["C"]
                     poss.append(int(pages[pid, g["off_pos"] + 4 * idx: g["off_pos"] + 4 * idx + 4].view("<i4")[0]))
             poss = np.array(poss, np.int64)
             assert len(np.unique(poss)) == len(poss), f"unit {u}: duplicate stored position"
             assert (poss < max(N - scn.W, 0)).all() and (poss >= 0).all()
             if life is not None and life.pruned is not None:
-                assert int(n_h[u] + n_l[u]) + min(scn.W, N) + int(life.pruned[u]) == N, f"I4 fails at unit {u}"
+                nt = int(snap["n_t"][u]) if "n_t" in snap else 0
+                assert int(n_h[u] + n_l[u]) + nt + min(scn.W, N) + int(life.pruned[u]) == N, f"I4 fails at unit {u}"
