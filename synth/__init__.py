@@ -214,12 +214,14 @@ def drift_factor(seed: int, step: int, ug: torch.Tensor, pos: torch.Tensor) -> t
 
 
 def apply_drift(seed: int, step: int, shape: Shape, pages_u8: torch.Tensor, table: torch.Tensor,
-                n_h: torch.Tensor, n_l: torch.Tensor, geom: dict, L: int, active_units=None, chunk: int = 1 << 22):
+                n_h: torch.Tensor, n_l: torch.Tensor, geom: dict, L: int, active_units=None, chunk: int = 1 << 22,
+                ttable=None, n_t=None):
     """sig <- sig * m (one fp32 multiply) for every stored token of every unit, in place on page bytes.
 
     `pages_u8` is a contiguous uint8 [P, page_bytes] tensor (oracle numpy view via torch.from_numpy, or
-    the CUDA arena); `geom` = {cls: (C, off_score, off_pos)} for cls 1 (high) and 2 (low).  Pure harness:
-    stands in for the attention epilogue."""
+    the CUDA arena); `geom` = {cls: (C, off_score, off_pos)} for cls 1 (high) and 2 (low), and 4 (the NEXT-4
+    FP16 tier, pages in `ttable` with `n_t` tokens) when given.  Pure harness: stands in for the attention
+    epilogue."""
     dev = pages_u8.device
     U = table.shape[0]
     pb = pages_u8.shape[1]
@@ -227,7 +229,8 @@ def apply_drift(seed: int, step: int, shape: Shape, pages_u8: torch.Tensor, tabl
     words_i = pages_u8.view(-1).view(torch.int32)
     ug_all = shape.global_units(list(range(shape.R)), device=dev).reshape(-1)
     table = table.to(dev)
-    for cls, n in ((1, n_h), (2, n_l)):
+    secs = ((1, n_h), (2, n_l)) + (((4, n_t),) if ttable is not None else ())
+    for cls, n in secs:
         C, off_s, off_p = geom[cls]
         n64 = n.to(dev).to(torch.int64)
         if active_units is not None:
@@ -242,8 +245,8 @@ def apply_drift(seed: int, step: int, shape: Shape, pages_u8: torch.Tensor, tabl
         uu, pk = vp.nonzero(as_tuple=True)
         for a in range(0, uu.numel(), chunk):
             u1, p1 = uu[a:a + chunk], pk[a:a + chunk]
-            col = p1 if cls == 1 else (L - 1 - p1)
-            pid = table[u1, col].to(torch.int64)
+            col = p1 if cls != 2 else (L - 1 - p1)
+            pid = (ttable.to(dev) if cls == 4 else table)[u1, col].to(torch.int64)
             idx = torch.arange(C, device=dev, dtype=torch.int64).view(1, -1)
             slot = p1.view(-1, 1) * C + idx
             ok = slot < n64[u1].view(-1, 1)

@@ -149,10 +149,12 @@ class OracleBackend:
 
     def drift(self, step):
         p = self.pool
+        top = self.scn.top_tier
         synth.apply_drift(self.scn.seed, step, self.scn.shape, torch.from_numpy(p.pages),
                           torch.from_numpy(p.table), torch.from_numpy(p.n_h), torch.from_numpy(p.n_l),
-                          {c: (self.geom[c]["C"], self.geom[c]["off_score"], self.geom[c]["off_pos"]) for c in (1, 2)},
-                          self.L)
+                          {c: (self.geom[c]["C"], self.geom[c]["off_score"], self.geom[c]["off_pos"]) for c in self.geom},
+                          self.L, ttable=torch.from_numpy(p.ttable) if top else None,
+                          n_t=torch.from_numpy(p.n_t) if top else None)
 
     def snapshot(self, pages=True):
         p = self.pool

@@ -115,6 +115,7 @@ def test_top_victim_moves_down_requantized_from_fp16():
     p = o.pool
     moved = 0
     for step in range(60):
+        o.drift(step)                                             # the significance drift, then the step itself
         before = {(u, s): p.slot_record(TOP, u, s) for u in range(p.U) for s in range(int(p.n_t[u]))}
         fp16 = {}
         g = p.geom[TOP]
@@ -123,7 +124,7 @@ def test_top_victim_moves_down_requantized_from_fp16():
             pg = p.pages[pid]
             fp16[(u, s)] = (pg[g.off_k + idx * g.k_row: g.off_k + (idx + 1) * g.k_row].view(np.float16).astype(np.float32),
                             pg[g.off_v + idx * g.v_row: g.off_v + (idx + 1) * g.v_row].view(np.float16).astype(np.float32))
-        decs = H.decode_step([o], inp, life, step)
+        decs = H.decode_step([o], inp, life, step, drift=False)
         dec = decs[0]
         for u in np.nonzero((dec["tc_class"] == TOP) & (dec["v_action"] == oracle.V_DOWN))[0]:
             u = int(u)
