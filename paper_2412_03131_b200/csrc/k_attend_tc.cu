@@ -8,8 +8,8 @@
 // exact and only fp32 accumulation rounds:
 //   logit(t, h) = (s_t * sum_f q_hf code_tf + z_t * sum_f q_hf) / sqrt(d)       (X^ = s*Q + z)
 //   out(h, f)   = sum_t (a_ht s_t) code_tf + sum_t a_ht z_t
-// Codes are < 2^8, so they are exact in fp16 and bf16; the queries are fp16 inputs (exact); a_ht s_t is an fp32
-// value split into bf16 hi + lo (16 significant bits, two MMAs).  The FP16 window (<= W tokens) runs on CUDA
+// Codes are < 2^8, so they are exact in fp16; the queries are fp16 inputs (exact); a_ht s_t is an fp32 value,
+// scaled by 2^12, split into fp16 hi + lo (22 significant bits, two MMAs).  The FP16 window (<= W tokens) runs on CUDA
 // cores in fp32.
 //
 // One CTA per unit (the paper's "one thread block per head"), kTcWarps warps; pages go round-robin to
@@ -96,18 +96,28 @@ __device__ __forceinline__ void k4_pairs(uint32_t x, uint32_t& lo, uint32_t& hi)
   lo = hsub2_u((__byte_perm(x, 0u, s0) & 0x00F0000Fu) | 0x54006400u, 0x54006400u);
   hi = hsub2_u((__byte_perm(x, 0u, s1) & 0x00F0000Fu) | 0x54006400u, 0x54006400u);
 }
-// V: byte K of x (token j0) and of y (token j1) -> bf16x2 (field of j0, field of j1) for the field at bits
-// [SH, SH + VB) of that byte; the magic makes bit SH weigh 1 in bf16 (7 mantissa bits)
+// V: byte K of x (token j0) and of y (token j1) -> fp16x2 (field of j0, field of j1) for the field at bits
+// [SH, SH + VB) of that byte; the magic makes bit SH weigh 1 (fp16, 10 mantissa bits: a value in [2^e, 2^(e+1))
+// has ulp 2^(e-10), so e = 10 - SH: 1024 (0x6400) for SH = 0, 256 (0x5C00) for 2, 64 (0x5400) for 4, 16 (0x4C00)
+// for 6)
 template <int K, int SH, int VB>
 __device__ __forceinline__ uint32_t v_pair(uint32_t x, uint32_t y) {
   constexpr uint32_t sel = K | (K << 4) | ((4 + K) << 8) | ((4 + K) << 12);
   constexpr uint32_t mask = (((1u << VB) - 1u) << SH) * 0x00010001u;
-  // bf16 with 7 explicit mantissa bits: a value in [2^e, 2^(e+1)) has ulp 2^(e-7); bit SH weighs 1 when
-  // 2^(e-7) * 2^SH = 1, i.e. e = 7 - SH: 128.0 (0x4300) for SH = 0, 8.0 (0x4100) for 4, 32.0 (0x4200) for 2,
-  // 2.0 (0x4000) for 6
-  constexpr uint32_t magic = (SH == 0 ? 0x4300u : SH == 2 ? 0x4200u : SH == 4 ? 0x4100u : 0x4000u) * 0x00010001u;
-  return bsub2_u((__byte_perm(x, y, sel) & mask) | magic, magic);
+  constexpr uint32_t magic = (SH == 0 ? 0x6400u : SH == 2 ? 0x5C00u : SH == 4 ? 0x5400u : 0x4C00u) * 0x00010001u;
+  return hsub2_u((__byte_perm(x, y, sel) & mask) | magic, magic);
 }
+// fp32 pair -> fp16x2 hi parts and the fp16x2 of the remainders (x = hi + lo to 22 significant bits)
+__device__ __forceinline__ void h2_split(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+// PV's B operand a * s_v is scaled by 2^kPvShift before its fp16 split (a <= 1 and |s_v| < 2^4 keep it below the
+// fp16 maximum; the scale keeps small products out of the subnormal range); the accumulators are scaled back once
+constexpr float kPvScale = 4096.0f, kPvUnscale = 1.0f / 4096.0f;
 
 // Compile-time geometry of one precision class (the paper's K8V4 high / K4V2 low pages): tokens per
 // page, bit widths, code row bytes, 16-B chunks per row and the row swizzle shifts of the staged copies.
@@ -236,14 +246,14 @@ __device__ __forceinline__ void pv_page(const uint8_t* vseg, int t0, int cnt, co
         const float sf = __half2float(__ushort_as_half((unsigned short)(vm & 0xFFFFu)));
         const float zf = __half2float(__ushort_as_half((unsigned short)(vm >> 16)));
         const float a = lg[(size_t)(t0 + j) * GP + grp] * iz;
-        b = a * sf;
+        b = a * sf * kPvScale;
         zsum = fmaf(a, zf, zsum);
       }
       bv[jj] = b;
     }
     uint32_t bh0, bl0, bh1, bl1;
-    bf2_split(bv[0], bv[1], bh0, bl0);
-    bf2_split(bv[2], bv[3], bh1, bl1);
+    h2_split(bv[0], bv[1], bh0, bl0);
+    h2_split(bv[2], bv[3], bh1, bl1);
     uint32_t w[4][NW];
 #pragma unroll
     for (int jj = 0; jj < 4; jj++) lds_row<RB, CL::vc, CL::vsh>(vseg, tile * 16 + 4 * tig + jj, CL::v_row, RB * grp, w[jj]);
@@ -279,8 +289,8 @@ __device__ __forceinline__ void pv_page(const uint8_t* vseg, int t0, int cnt, co
 #undef DKV_V2
         }
       }
-      mma_bf16(acc[g], a, bh0, bh1);
-      mma_bf16(acc[g], a, bl0, bl1);
+      mma_f16(acc[g], a, bh0, bh1);
+      mma_f16(acc[g], a, bl0, bl1);
     }
   }
 }
@@ -467,7 +477,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     __syncthreads();
   }
   // ---- phase 3: PV by MMA (A = value codes^T: m = features f0 = 16g + 2 grp, f0 + 1; k = tokens 4 tig .. +3;
-  // B = (a * s_v) split bf16 hi / lo: k = tokens, n = head grp), significance + minima, page by page
+  // B = 2^12 a * s_v split fp16 hi / lo: k = tokens, n = head grp), significance + minima, page by page
   float acc[NG][4];
 #pragma unroll
   for (int g = 0; g < NG; g++) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.0f;
@@ -569,7 +579,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     for (int c = 0; c < 4; c++) {
       const int h = 2 * tig + (c & 1);
       const int f = (D / 8) * grp + 2 * gg + (c >> 1);          // pv_page's feature mapping
-      if (h < G) part[((size_t)warp * G + h) * D + f] = acc[gg][c];
+      if (h < G) part[((size_t)warp * G + h) * D + f] = acc[gg][c] * kPvUnscale;
     }
   }
   {
