@@ -456,94 +456,6 @@ def run_ours(args, rank, world, local):
     assert st == 0, f"device status {st} after e2e"
     seq[active] += args.steps
 
-    # ---------------- CUDA graph: GRAPH_STEPS decode steps captured once (dkv_decode_graph_create) and replayed;
-    # per-step inputs [GRAPH_STEPS][U][d] (840 MB at this config, >> L2) already in HBM.  No L2 flush between the
-    # steps of a replay: it is the steady state of back-to-back decode steps.
-    from paper_2412_03131_b200 import dkv as D
-    # the replays (two per PDL / plain graph, one event graph) must stay within max_seq_len
-    GS = max(1, min(100, (c["M"] - int(seq.max()) - 4 * (args.warmup + args.steps) - 8) // 6))
-    gsig = torch.empty((GS, wl.U), dtype=torch.float32, device=dev)
-    gk = torch.empty((GS, wl.U, c["d"]), dtype=torch.int16, device=dev)
-    gv = torch.empty_like(gk)
-    for t in range(GS):
-        cand, nk, nv = wl.decode_inputs(seq + t, active)
-        gsig[t].copy_(cand)
-        gk[t].copy_(nk.view(torch.int16))
-        gv[t].copy_(nv.view(torch.int16))
-    gdec = pool.new_decisions()
-    graph_pdl = pool.decode_graph(GS, gsig, gk, gv, gdec, D.DKV_GRAPH_PDL)
-    graph_ev = pool.decode_graph(GS, gsig, gk, gv, gdec, D.DKV_GRAPH_EVENTS)
-    graph_plain = pool.decode_graph(GS, gsig, gk, gv, gdec, 0)
-    graph_us = {}
-    for name, gr in (("pdl", graph_pdl), ("plain", graph_plain)):
-        for rep in range(2):                                 # one untimed replay, one timed
-            flush.zero_()
-            torch.cuda.synchronize()
-            barrier(world)
-            g0, g1 = ev(), ev()
-            torch.cuda._sleep(200_000)
-            g0.record()
-            gr.launch()
-            g1.record()
-            torch.cuda.synchronize()
-            seq[active] += GS
-            launches += 3 * GS if rep else 0
-        graph_us[name] = g0.elapsed_time(g1) * 1e3 / GS
-    flush.zero_()
-    graph_ev.launch()
-    torch.cuda.synchronize()
-    seq[active] += GS
-    kms = graph_ev.kernel_ms() * 1e3                         # [GS][3] us: classify, compact_alloc, quant_write
-    st, _ = pool.query()
-    assert st == 0, f"device status {st} after the graph replays"
-    for gr in (graph_pdl, graph_ev, graph_plain):
-        gr.close()
-    del gsig, gk, gv
-    # a ONE-step graph replayed per step, with the same untimed drift + L2 flush between steps as the eager decode
-    # phase: its device time is directly comparable to decode_step_us.step
-    s_sig = torch.empty(wl.U, dtype=torch.float32, device=dev)
-    s_k = torch.empty((wl.U, c["d"]), dtype=torch.int16, device=dev)
-    s_v = torch.empty_like(s_k)
-    graph1 = pool.decode_graph(1, s_sig, s_k, s_v, gdec, D.DKV_GRAPH_PDL)
-    g1_us = []
-    for s_ in range(args.warmup + args.steps):
-        v = pool.views()
-        synth.apply_drift(c["seed"], 1000 + s_, wl.shape, v["pages"], v["table"], v["n_h"], v["n_l"],
-                          {k_: (geom[k_]["C"], geom[k_]["off_score"], geom[k_]["off_pos"]) for k_ in (1, 2)}, pool.L)
-        cand, nk, nv = wl.decode_inputs(seq, active)
-        s_sig.copy_(cand)
-        s_k.copy_(nk.view(torch.int16))
-        s_v.copy_(nv.view(torch.int16))
-        flush.zero_()
-        torch.cuda.synchronize()
-        barrier(world)
-        g0, g1 = ev(), ev()
-        torch.cuda._sleep(200_000)
-        g0.record()
-        graph1.launch()
-        g1.record()
-        torch.cuda.synchronize()
-        seq[active] += 1
-        if s_ >= args.warmup:
-            g1_us.append(g0.elapsed_time(g1) * 1e3)
-            launches += 3
-    graph1.close()
-    st, _ = pool.query()
-    assert st == 0, f"device status {st} after the one-step graph replays"
-    graph = {"one_step_graph_us": round(max_over_ranks(statistics.mean(g1_us), world), 3),
-             "one_step_graph_us_p50": round(float(np.percentile(g1_us, 50)), 3),
-             "steps_per_graph": GS, "graph_step_us": round(max_over_ranks(graph_us["pdl"], world), 3),
-             "graph_step_us_no_pdl": round(max_over_ranks(graph_us["plain"], world), 3),
-             "in_graph_kernel_us": {nm: {"mean": round(float(kms[:, j].mean()), 3),
-                                         "p50": round(float(np.percentile(kms[:, j], 50)), 3),
-                                         "p99": round(float(np.percentile(kms[:, j], 99)), 3)}
-                                    for j, nm in enumerate(("classify", "compact_alloc", "quant_write"))},
-             "note": "one_step_graph_us: a 1-step graph (PDL) replayed per step with the eager phase's drift and L2 "
-                     "flush in between (compare decode_step_us.step); graph_step_us = device time of one replay of a "
-                     "100-step graph (PDL between kernels) / 100, steady state (no drift, no L2 flush inside a "
-                     "replay: more ties in the scan), inputs 840 MB per replay; in_graph_kernel_us from the same "
-                     "100-step graph with an event node around every kernel (no PDL)"}
-
     # ---------------- NEXT-2: decode steps driven by the attention kernel's significance
     next2 = None
     if args.next2 and c.get("G", 0) > 0:
@@ -648,6 +560,94 @@ def run_ours(args, rank, world, local):
                        "speedup_vs_fp16_roofline": round(fp16_us / statistics.mean(tc_us), 3),
                        "note": "FP16 reference: the same tokens' K and V as fp16 (4 d bytes each) read at the measured "
                                "HBM peak; the paper reports 1.7x for K8V8 over FP16 (P:896-900)"}
+
+    # ---------------- CUDA graph: GRAPH_STEPS decode steps captured once (dkv_decode_graph_create) and replayed;
+    # per-step inputs [GRAPH_STEPS][U][d] (840 MB at this config, >> L2) already in HBM.  No L2 flush between the
+    # steps of a replay: it is the steady state of back-to-back decode steps.
+    from paper_2412_03131_b200 import dkv as D
+    # the replays (two per PDL / plain graph, one event graph) must stay within max_seq_len
+    GS = max(1, min(100, (c["M"] - int(seq.max()) - 4 * (args.warmup + args.steps) - 8) // 6))
+    gsig = torch.empty((GS, wl.U), dtype=torch.float32, device=dev)
+    gk = torch.empty((GS, wl.U, c["d"]), dtype=torch.int16, device=dev)
+    gv = torch.empty_like(gk)
+    for t in range(GS):
+        cand, nk, nv = wl.decode_inputs(seq + t, active)
+        gsig[t].copy_(cand)
+        gk[t].copy_(nk.view(torch.int16))
+        gv[t].copy_(nv.view(torch.int16))
+    gdec = pool.new_decisions()
+    graph_pdl = pool.decode_graph(GS, gsig, gk, gv, gdec, D.DKV_GRAPH_PDL)
+    graph_ev = pool.decode_graph(GS, gsig, gk, gv, gdec, D.DKV_GRAPH_EVENTS)
+    graph_plain = pool.decode_graph(GS, gsig, gk, gv, gdec, 0)
+    graph_us = {}
+    for name, gr in (("pdl", graph_pdl), ("plain", graph_plain)):
+        for rep in range(2):                                 # one untimed replay, one timed
+            flush.zero_()
+            torch.cuda.synchronize()
+            barrier(world)
+            g0, g1 = ev(), ev()
+            torch.cuda._sleep(200_000)
+            g0.record()
+            gr.launch()
+            g1.record()
+            torch.cuda.synchronize()
+            seq[active] += GS
+            launches += 3 * GS if rep else 0
+        graph_us[name] = g0.elapsed_time(g1) * 1e3 / GS
+    flush.zero_()
+    graph_ev.launch()
+    torch.cuda.synchronize()
+    seq[active] += GS
+    kms = graph_ev.kernel_ms() * 1e3                         # [GS][3] us: classify, compact_alloc, quant_write
+    st, _ = pool.query()
+    assert st == 0, f"device status {st} after the graph replays"
+    for gr in (graph_pdl, graph_ev, graph_plain):
+        gr.close()
+    del gsig, gk, gv
+    # a ONE-step graph replayed per step, with the same untimed drift + L2 flush between steps as the eager decode
+    # phase: its device time is directly comparable to decode_step_us.step
+    s_sig = torch.empty(wl.U, dtype=torch.float32, device=dev)
+    s_k = torch.empty((wl.U, c["d"]), dtype=torch.int16, device=dev)
+    s_v = torch.empty_like(s_k)
+    graph1 = pool.decode_graph(1, s_sig, s_k, s_v, gdec, D.DKV_GRAPH_PDL)
+    g1_us = []
+    for s_ in range(args.warmup + args.steps):
+        v = pool.views()
+        synth.apply_drift(c["seed"], 1000 + s_, wl.shape, v["pages"], v["table"], v["n_h"], v["n_l"],
+                          {k_: (geom[k_]["C"], geom[k_]["off_score"], geom[k_]["off_pos"]) for k_ in (1, 2)}, pool.L)
+        cand, nk, nv = wl.decode_inputs(seq, active)
+        s_sig.copy_(cand)
+        s_k.copy_(nk.view(torch.int16))
+        s_v.copy_(nv.view(torch.int16))
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier(world)
+        g0, g1 = ev(), ev()
+        torch.cuda._sleep(200_000)
+        g0.record()
+        graph1.launch()
+        g1.record()
+        torch.cuda.synchronize()
+        seq[active] += 1
+        if s_ >= args.warmup:
+            g1_us.append(g0.elapsed_time(g1) * 1e3)
+            launches += 3
+    graph1.close()
+    st, _ = pool.query()
+    assert st == 0, f"device status {st} after the one-step graph replays"
+    graph = {"one_step_graph_us": round(max_over_ranks(statistics.mean(g1_us), world), 3),
+             "one_step_graph_us_p50": round(float(np.percentile(g1_us, 50)), 3),
+             "steps_per_graph": GS, "graph_step_us": round(max_over_ranks(graph_us["pdl"], world), 3),
+             "graph_step_us_no_pdl": round(max_over_ranks(graph_us["plain"], world), 3),
+             "in_graph_kernel_us": {nm: {"mean": round(float(kms[:, j].mean()), 3),
+                                         "p50": round(float(np.percentile(kms[:, j], 50)), 3),
+                                         "p99": round(float(np.percentile(kms[:, j], 99)), 3)}
+                                    for j, nm in enumerate(("classify", "compact_alloc", "quant_write"))},
+             "note": "one_step_graph_us: a 1-step graph (PDL) replayed per step with the eager phase's drift and L2 "
+                     "flush in between (compare decode_step_us.step); graph_step_us = device time of one replay of a "
+                     "100-step graph (PDL between kernels) / 100, steady state (no drift, no L2 flush inside a "
+                     "replay: more ties in the scan), inputs 840 MB per replay; in_graph_kernel_us from the same "
+                     "100-step graph with an event node around every kernel (no PDL)"}
 
     # ---------------- recycle micro-benchmark: free 1 / 8 / 32 requests, then one decode step whose
     # dkv_compact_alloc recycles all their pages (~37k / 300k / 1.2M page IDs at this config)

@@ -93,7 +93,16 @@ typedef struct {
                                   classes, counts and page bytes; different page IDs and ring order. */
   int32_t q_per_kv;            /* NEXT-2 (dkv_attend): query heads per KV head, the GQA group;
                                   0 = no attention; supported: 1, 2, 4, 5, 7, 8 */
+  /* NEXT-4 three-level tier FP16-K8V4-K4V2 (readings Q38-Q44 of DESIGN.md): top_tier = 1 adds
+     the FP16 class TOP above High — tokens with significance >= alpha_t / den (prompt) or alpha_t / N (decode)
+     are kept unquantized, page_tokens_top (multiple of 4) per page, in a unidirectional table filled left to
+     right next to the bidirectional one.  Requires alpha_t >= alpha_h, prefill_workflow = 0; dkv_attend and
+     dkv_attend_tc return DKV_ERR_INVALID_ARG with the tier. */
+  int32_t top_tier;
+  float   alpha_t;
+  int32_t page_tokens_top;
 } dkv_config_t;
+enum { DKV_CLS_TOP = 4, DKV_GROW_TOP = 3 };          /* NEXT-4: decision codes of the FP16 tier */
 
 /* 16-byte per-unit decision written by dkv_classify(DECODE); padding-free, compared byte for byte.
  * tc_class: class of t_c, the token leaving the window, or NONE when the request is not
@@ -130,6 +139,10 @@ typedef struct {
   int64_t off_head_alpha;      /* fp32[layers * kv_heads][2]: per-head (alpha_h, alpha_l) (NEXT-4) */
   int64_t off_att_scratch;     /* NEXT-2 long contexts: 296 slots of (ceil4(q_per_kv) + 2) * max_seq_len fp32 when
                                   those do not fit in shared memory (0 bytes otherwise) */
+  int64_t off_ttable;          /* NEXT-4: int32[units][table_len_top] TOP page table (left to right) */
+  int64_t off_n_t;             /* NEXT-4: int32[units] stored TOP tokens */
+  int32_t table_len_top;       /* NEXT-4: ceil(max_seq_len / page_tokens_top), 1 without the tier */
+  int32_t C_top, row_top, off_k_top, off_v_top, off_score_top, off_pos_top;   /* TOP page geometry (fp16 rows) */
   int64_t off_qpid;            /* int32[units][2] {page of t_c's slot (= the victim's KV_h page when it is
                                   downgraded), page of a downgraded victim's KV_l slot}: written by
                                   dkv_classify(DECODE) for existing pages and by dkv_compact_alloc for granted

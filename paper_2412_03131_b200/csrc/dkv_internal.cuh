@@ -108,7 +108,26 @@ struct PoolDev {
   int32_t prefill_wf;   // dkv_config_t.prefill_workflow
   int2* qpid;           // [U] {t_c's page, downgraded victim's KV_l page} for dkv_quant_write(DECODE)
   int32_t pdl;          // launch option: 1 = programmatic dependent launch (decode-step CUDA graphs)
+  // NEXT-4 three-level tier FP16-K8V4-K4V2 (readings Q38-Q44)
+  int32_t top;          // 1: the FP16 class TOP above High
+  float alpha_t;
+  int32_t Lt, Ct;       // TOP table slots per unit, tokens per TOP page
+  ClassGeom gt;         // TOP page geometry: fp16 K / V rows (k_row = v_row = 2d), no metadata
+  int32_t* ttable;      // [U][Lt] TOP page table, left to right
+  int32_t* n_t;         // [U] stored TOP tokens
+  int32_t* pf_nt;       // [U] prompt TOP counts
+  int32_t* pf_seg_t;    // [U][nseg] exclusive TOP rank at each segment start
+  FastDiv div_Ct;
 };
+
+// Deferred-recycle record of a freed unit (p.rec, 4 ints): {ring offset from the end pointer, ph, freed pages,
+// pt}.  The unit's freed slots as one flat list: TOP table slots [0, pt), then bidirectional slots [0, ph) and
+// [L - pl, L) (Q13, Q41).
+__device__ __forceinline__ int32_t* freed_slot(const PoolDev& p, int u, int k, int pt, int ph, int nfr) {
+  if (k < pt) return p.ttable + (size_t)u * p.Lt + k;
+  const int kk = k - pt;
+  return p.table + (size_t)u * p.L + (kk < ph ? kk : p.L - (nfr - pt) + kk);
+}
 
 // kernel launch with optional programmatic dependent launch (cudaLaunchKernelEx)
 template <typename... KArgs, typename... Args>

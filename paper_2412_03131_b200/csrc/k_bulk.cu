@@ -21,9 +21,11 @@ constexpr int kBulkWarps = 4;
 constexpr int kBulkG = 4;                                // lanes per token
 constexpr int kBulkTPS = 32 / kBulkG;                    // tokens per warp step
 
-__device__ __forceinline__ int prompt_class_q(float ah, float al, int prompt_den, float s, int t, int T) {
+__device__ __forceinline__ int prompt_class_q(float ah, float al, int prompt_den, float s, int t, int T, int top = 0,
+                                              float at = 0.0f) {
   const float den = (prompt_den == 0) ? (float)(t + 1) : (float)T;
   const float th = __fdiv_rn(ah, den), tl = __fdiv_rn(al, den);
+  if (top && s >= __fdiv_rn(at, den)) return DKV_CLS_TOP;       // NEXT-4 (Q38): written by quant_prefill_top_kernel
   return s >= th ? DKV_CLS_HIGH : (s >= tl ? DKV_CLS_LOW : DKV_CLS_PRUNED);
 }
 
@@ -292,7 +294,7 @@ quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const u
     float s = 0.0f;
     if (t < ke) {
       s = canon_zero(__ldcs(srow + t));
-      cl = prompt_class_q(ah, al, p.prompt_den, s, t, T);
+      cl = prompt_class_q(ah, al, p.prompt_den, s, t, T, p.top, p.alpha_t);
     }
     const unsigned hm = __ballot_sync(kFull, cl == DKV_CLS_HIGH);
     const unsigned lm = __ballot_sync(kFull, cl == DKV_CLS_LOW);
@@ -358,6 +360,75 @@ __global__ void finish_prefill_kernel(PoolDev p, int n) {
 #define DKV_BULK_PF 3
 #endif
 
+// NEXT-4 (Q40): the prompt's TOP tokens, kept as their fp16 K and V rows.  A warp per (admitted unit, 256-token
+// segment) as in quant_prefill_kernel: ranks from classify_prefill's TOP checkpoints plus a ballot per 32 tokens,
+// then one token at a time the whole warp copies its rows (K: lanes 0..15, V: 16..31 at d = 128) into TOP slot
+// `rank` (page ttable[u][rank / Ct]) with its significance and position.  A token with a non-finite element is
+// rejected whole (Q30).
+template <int D>
+__global__ void __launch_bounds__(kBulkWarps * 32)
+quant_prefill_top_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const uint16_t* __restrict__ vin,
+                         int64_t kv_stride, const float* __restrict__ sig, int64_t sig_stride, int nseg_max) {
+  constexpr int LPR = D / 8;                                     // lanes per row (16-B chunks)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long item = (long)blockIdx.x * kBulkWarps + warp;
+  const int seg = (int)(item % nseg_max);
+  const long wi = item / nseg_max;
+  if (wi >= (long)n * p.LyH) return;
+  if (ld_volatile(&p.ctrl->qw_status) != 0) return;             // entry status (Q36)
+  const int i = (int)(wi / p.LyH), j = (int)(wi % p.LyH);
+  const int r = p.admit[i];
+  const int u = r * p.LyH + j;
+  const float ah = unit_alpha_h(p, u), al = unit_alpha_l(p, u);
+  const int T = p.prompt_len[r];
+  const int t0 = seg * kSegTokens;
+  const int kept = max(T - p.W, 0);
+  const int ke = min(t0 + kSegTokens, kept);
+  if (t0 >= ke) return;
+  const float* srow = sig + wi * sig_stride;
+  const uint16_t* kbase = kin + wi * kv_stride * D;
+  const uint16_t* vbase = vin + wi * kv_stride * D;
+  int rank = p.pf_seg_t[(size_t)u * p.nseg + seg];
+  const ClassGeom gt = p.gt;
+  bool bad = false;
+  for (int c = t0; c < ke; c += 32) {
+    const int t = c + lane;
+    float s = 0.0f;
+    int cl = DKV_CLS_NONE;
+    if (t < ke) {
+      s = canon_zero(__ldg(srow + t));
+      cl = prompt_class_q(ah, al, p.prompt_den, s, t, T, 1, p.alpha_t);
+    }
+    unsigned m = __ballot_sync(kFull, cl == DKV_CLS_TOP);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const int tt = c + src;
+      const float st = __shfl_sync(kFull, s, src);
+      const int slot = rank++;
+      const int pg = fdiv(p.div_Ct, slot), idx = slot - pg * p.Ct;
+      uint8_t* page = p.pages + (size_t)p.ttable[(size_t)u * p.Lt + pg] * (size_t)p.page_bytes;
+      uint4 x = make_uint4(0u, 0u, 0u, 0u);
+      const bool isk = lane < LPR;
+      if (lane < 2 * LPR) x = ld_stream_v4((isk ? kbase : vbase) + (size_t)tt * D + 8 * (isk ? lane : lane - LPR));
+      const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+      bool fin = true;
+#pragma unroll
+      for (int e = 0; e < 4; e++)
+        fin &= ((w4[e] & 0x7C00u) != 0x7C00u) && ((w4[e] & 0x7C000000u) != 0x7C000000u);
+      if (__any_sync(kFull, !fin)) { bad = true; continue; }       // Q30: nothing of the token is stored
+      if (lane < 2 * LPR)
+        *reinterpret_cast<uint4*>(page + (isk ? gt.off_k + idx * gt.k_row + 16 * lane
+                                              : gt.off_v + idx * gt.v_row + 16 * (lane - LPR))) = x;
+      if (lane == 0) {
+        *reinterpret_cast<float*>(page + gt.off_score + 4 * idx) = st;
+        *reinterpret_cast<int32_t*>(page + gt.off_pos + 4 * idx) = tt;
+      }
+    }
+  }
+  if (bad && lane == 0) set_status(p.ctrl, DKV_ERR_NONFINITE);
+}
+
 cudaError_t launch_quant_prefill(const PoolDev& p, int n, const uint16_t* k, const uint16_t* v, int64_t kv_stride,
                                  const float* sig, int64_t sig_stride, int max_len, cudaStream_t s) {
   const int nseg_max = (max_len + kSegTokens - 1) / kSegTokens;
@@ -386,6 +457,13 @@ cudaError_t launch_quant_prefill(const PoolDev& p, int n, const uint16_t* k, con
     } else {
       quant_prefill_kernel<64, 0><<<(unsigned)grid, kBulkWarps * 32, 0, s>>>(p, n, k, v, kv_stride, sig, sig_stride, nseg_max);
     }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (p.top && items > 0) {
+    const long grid = (items + kBulkWarps - 1) / kBulkWarps;
+    if (p.d == 128) quant_prefill_top_kernel<128><<<(unsigned)grid, kBulkWarps * 32, 0, s>>>(p, n, k, v, kv_stride, sig, sig_stride, nseg_max);
+    else quant_prefill_top_kernel<64><<<(unsigned)grid, kBulkWarps * 32, 0, s>>>(p, n, k, v, kv_stride, sig, sig_stride, nseg_max);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

@@ -53,7 +53,8 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   if (u >= p.U) return;                                          // whole warps exit together
   pdl_wait();                                                    // (PDL) the previous quant_write's writes
   pdl_trigger();
-  int32_t* s_pid = s_pid_all + warp * p.L;
+  const int LP = p.L > p.Lt ? p.L : p.Lt;                        // page IDs a scanned section can have
+  int32_t* s_pid = s_pid_all + warp * LP;
 #if DKV_CD_SPEC
   // One round trip for everything u alone addresses: the sticky status (read through L1 — 16k warps reading
   // the word at one L2 slice queue there; a status set during this call is seen or not, as before), the
@@ -85,7 +86,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   int v_slot = -1, tc_slot = -1, v_dst_slot = -1;
   bool scan = false;
   int cls = DKV_CLS_NONE, n = 0, nh = 0, nl = 0;
-  float sc = 0.0f, th = 0.0f, tl = 0.0f;
+  float sc = 0.0f, th = 0.0f, tl = 0.0f, tt = 0.0f;
   {
     const int8_t st = p.req_state[r];
     const int N = p.seq_len[r] + 1;                              // Q3: includes this step's token
@@ -93,6 +94,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
     const float s_in = cand_sig ? cand_sig[u]
                                 : (p.W > 0 && N - 1 - p.W >= 0 ? p.win_sig[(size_t)u * p.W + (N - 1 - p.W) % p.W] : 0.0f);
     const int nh_in = p.n_h[u], nl_in = p.n_l[u];
+    const int nt_in = p.top ? p.n_t[u] : 0;
     const int pc = N - 1 - p.W;                                  // t_c = earliest window token
     if (st == DKV_REQ_ACTIVE && pc >= 0) {
       if (!finite_f(s_in) || s_in < 0.0f) {
@@ -102,11 +104,15 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
         th = __fdiv_rn(unit_alpha_h(p, u), (float)N);            // alpha_h / N (per head: Q35)
         tl = __fdiv_rn(unit_alpha_l(p, u), (float)N);            // alpha_l / N
         cls = sc >= th ? DKV_CLS_HIGH : (sc >= tl ? DKV_CLS_LOW : DKV_CLS_PRUNED);
+        if (p.top) {                                             // NEXT-4 (Q38): the FP16 tier above High
+          tt = __fdiv_rn(p.alpha_t, (float)N);
+          if (sc >= tt) cls = DKV_CLS_TOP;
+        }
         tc_class = (uint8_t)cls;
         if (cls != DKV_CLS_PRUNED) {
           nh = nh_in;
           nl = nl_in;
-          n = (cls == DKV_CLS_HIGH) ? nh : nl;
+          n = cls == DKV_CLS_TOP ? nt_in : ((cls == DKV_CLS_HIGH) ? nh : nl);
           scan = true;
         }
       }
@@ -117,14 +123,14 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   // NEXT-2: dkv_attend recorded each section's (significance, position) minimum after its update and no
   // section changed since (quant_write clears the flag): the victim needs no scan
 #if DKV_CD_SPEC
-  const bool fused = scan && n > 0 && __shfl_sync(kFull, sm_w, 6) == 1;
+  const bool fused = scan && n > 0 && cls != DKV_CLS_TOP && __shfl_sync(kFull, sm_w, 6) == 1;
   if (fused) {
     const int b = cls == DKV_CLS_HIGH ? 0 : 3;
     vb = (uint32_t)__shfl_sync(kFull, sm_w, b);
     vs = __shfl_sync(kFull, sm_w, b + 2);
   } else if
 #else
-  const bool fused = scan && n > 0 && p.secmin[8 * (size_t)u + 6] == 1;
+  const bool fused = scan && n > 0 && cls != DKV_CLS_TOP && p.secmin[8 * (size_t)u + 6] == 1;
   if (fused) {
     const int b = cls == DKV_CLS_HIGH ? 0 : 3;
     vb = (uint32_t)p.secmin[8 * (size_t)u + b];
@@ -132,21 +138,23 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   } else if
 #endif
   (scan && n > 0) {                                    // warp-uniform
-    const int C = cls == DKV_CLS_HIGH ? p.g[1].C : p.g[2].C;
-    const int off_score = cls == DKV_CLS_HIGH ? p.g[1].off_score : p.g[2].off_score;
+    const int C = cls == DKV_CLS_TOP ? p.gt.C : (cls == DKV_CLS_HIGH ? p.g[1].C : p.g[2].C);
+    const int off_score = cls == DKV_CLS_TOP ? p.gt.off_score : (cls == DKV_CLS_HIGH ? p.g[1].off_score : p.g[2].off_score);
     const bool pow2 = (C & (C - 1)) == 0;
     const int csh = __popc(C - 1);
     const int npages = (n + C - 1) / C;
 #if DKV_CD_SPEC
     for (int k = lane; k < npages; k += 32) {
       int32_t pid;
-      if (cls == DKV_CLS_HIGH) pid = k < 32 ? sp_h0 : (k < 64 ? sp_h1 : __ldg(row + k));
+      if (cls == DKV_CLS_TOP) pid = __ldg(p.ttable + (size_t)u * p.Lt + k);   // NEXT-4 (Q41)
+      else if (cls == DKV_CLS_HIGH) pid = k < 32 ? sp_h0 : (k < 64 ? sp_h1 : __ldg(row + k));
       else pid = k < 32 ? sp_l0 : __ldg(row + p.L - 1 - k);
       s_pid[k] = pid;
     }
 #else
     const int32_t* row = p.table + (size_t)u * p.L;
-    for (int k = lane; k < npages; k += 32) s_pid[k] = __ldg(row + (cls == DKV_CLS_HIGH ? k : p.L - 1 - k));
+    for (int k = lane; k < npages; k += 32)
+      s_pid[k] = cls == DKV_CLS_TOP ? __ldg(p.ttable + (size_t)u * p.Lt + k) : __ldg(row + (cls == DKV_CLS_HIGH ? k : p.L - 1 - k));
 #endif
     __syncwarp();
     const uint8_t* base_sc = p.pages + off_score;
@@ -198,7 +206,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
       // in flight per lane, then one 16-B position vector (the same 4 slots' positions, contiguous in the
       // page) for every score vector holding m — a section whose minimum is shared by hundreds of slots
       // (exact zeros when nothing is pruned) costs two round trips per batch, not one per tied slot
-      const int off_pos = cls == DKV_CLS_HIGH ? p.g[1].off_pos : p.g[2].off_pos;
+      const int off_pos = cls == DKV_CLS_TOP ? p.gt.off_pos : (cls == DKV_CLS_HIGH ? p.g[1].off_pos : p.g[2].off_pos);
       int32_t bp = 0x7FFFFFFF;
       int bs = -1;
       for (int base = 0; base < n; base += 128 * kXV) {
@@ -235,7 +243,19 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
     // t_c has the largest position, so a stored token wins every score tie with it
     if (vs >= 0 && !(vb <= __float_as_uint(sc))) vs = -1;
     const float sv = __uint_as_float(vb);
-    if (cls == DKV_CLS_HIGH) {
+    if (cls == DKV_CLS_TOP) {                                    // NEXT-4 (Q39): Algorithm 1 one level up
+      if (vs < 0 || sv >= tt) {                                  // t_v stays in KV_t
+        v_action = DKV_V_KEEP; grow = DKV_GROW_TOP; demand = (n % p.Ct == 0); tc_slot = n;
+      } else if (sv >= th) {                                     // t_v moves to KV_h
+        v_action = DKV_V_DOWN; grow = DKV_GROW_HIGH; demand = (nh % p.Ch == 0);
+        v_slot = vs; tc_slot = vs; v_dst_slot = nh;
+      } else if (sv >= tl) {                                     // t_v moves to KV_l
+        v_action = DKV_V_DOWN; grow = DKV_GROW_LOW; demand = (nl % p.Cl == 0);
+        v_slot = vs; tc_slot = vs; v_dst_slot = nl;
+      } else {                                                   // prune t_v
+        v_action = DKV_V_PRUNE; v_slot = vs; tc_slot = vs;
+      }
+    } else if (cls == DKV_CLS_HIGH) {
       if (vs < 0 || sv >= th) {                                  // t_v stays in KV_h
         v_action = DKV_V_KEEP; grow = DKV_GROW_HIGH; demand = (nh % p.Ch == 0); tc_slot = nh;
       } else if (sv >= tl) {                                     // line requant_high
@@ -261,16 +281,17 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   // downgraded victim moves to.  A page the growing section receives this step is not known yet: -1 here,
   // written by dkv_compact_alloc when it grants it.  The scanned section's IDs are in shared memory already.
   if (scan) {
-    const bool hi = cls == DKV_CLS_HIGH;
-    const int C = hi ? p.Ch : p.Cl;
+    const bool hi = cls == DKV_CLS_HIGH, top = cls == DKV_CLS_TOP;
+    const int C = top ? p.Ct : (hi ? p.Ch : p.Cl);
     const int32_t* trow = p.table + (size_t)u * p.L;
     const bool have = n > 0 && !fused;                          // s_pid holds the section's pages
     int pa = -1, pb = -1;
     if (!(v_action == DKV_V_KEEP && demand)) {
       const int k = tc_slot / C;
-      pa = have ? s_pid[k] : __ldg(trow + (hi ? k : p.L - 1 - k));
+      pa = have ? s_pid[k] : (top ? __ldg(p.ttable + (size_t)u * p.Lt + k) : __ldg(trow + (hi ? k : p.L - 1 - k)));
     }
-    if (v_action == DKV_V_DOWN && !demand) pb = __ldg(trow + p.L - 1 - nl / p.Cl);
+    if (v_action == DKV_V_DOWN && !demand)                      // the destination section's tail page
+      pb = grow == DKV_GROW_HIGH ? __ldg(trow + nh / p.Ch) : __ldg(trow + p.L - 1 - nl / p.Cl);
     p.qpid[u] = make_int2(pa, pb);
   }
 }
@@ -281,7 +302,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
 
 template <int MINB>
 static cudaError_t launch_cd(const PoolDev& p, const float* sig, dkv_decision_t* dec, cudaStream_t s) {
-  const size_t smem = 4 * (size_t)p.L * kCDWarps;
+  const size_t smem = 4 * (size_t)(p.L > p.Lt ? p.L : p.Lt) * kCDWarps;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(classify_decode_kernel<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -8,9 +8,11 @@ namespace dkv {
 // ------------------------------------------------------------------------------------------- prefill
 constexpr int kPrefillWarps = 4;
 
-__device__ __forceinline__ int prompt_class(float ah, float al, int prompt_den, float s, int t, int T) {
+__device__ __forceinline__ int prompt_class(float ah, float al, int prompt_den, float s, int t, int T, int top = 0,
+                                            float at = 0.0f) {
   const float den = (prompt_den == 0) ? (float)(t + 1) : (float)T;
   const float th = __fdiv_rn(ah, den), tl = __fdiv_rn(al, den);
+  if (top && s >= __fdiv_rn(at, den)) return DKV_CLS_TOP;       // NEXT-4 (Q38)
   return s >= th ? DKV_CLS_HIGH : (s >= tl ? DKV_CLS_LOW : DKV_CLS_PRUNED);
 }
 
@@ -32,11 +34,12 @@ classify_prefill_kernel(PoolDev p, int n, const float* __restrict__ sig, int64_t
   if (ld_volatile(&p.ctrl->status) != 0) {              // sticky error at entry (Q36): no classes, no counts
     if (crow)
       for (int t = lane; t < T; t += 32) crow[t] = DKV_CLS_NONE;
-    if (lane == 0) { p.pf_nh[u] = 0; p.pf_nl[u] = 0; }
+    if (lane == 0) { p.pf_nh[u] = 0; p.pf_nl[u] = 0; if (p.top) p.pf_nt[u] = 0; }
     return;
   }
   int32_t* seg = p.pf_seg + (size_t)u * p.nseg * 2;
-  int nh = 0, nl = 0;
+  int nh = 0, nl = 0, nt = 0;
+  int32_t* seg_t = p.pf_seg_t + (size_t)u * p.nseg;             // NEXT-4 TOP rank checkpoints
   bool bad = false;
   constexpr int TPL = VEC ? 4 : 1;                               // tokens per lane per step
   constexpr int STEP = 32 * TPL;
@@ -61,8 +64,9 @@ classify_prefill_kernel(PoolDev p, int n, const float* __restrict__ sig, int64_t
       if ((ts % kSegTokens) == 0 && lane == 0) {                 // rank checkpoint at segment start
         seg[2 * (ts / kSegTokens)] = nh;
         seg[2 * (ts / kSegTokens) + 1] = nl;
+        if (p.top) seg_t[ts / kSegTokens] = nt;
       }
-      int ch = 0, cl = 0;
+      int ch = 0, cl = 0, ct = 0;
       uint32_t cbytes = 0;
 #pragma unroll
       for (int e = 0; e < TPL; e++) {
@@ -71,14 +75,16 @@ classify_prefill_kernel(PoolDev p, int n, const float* __restrict__ sig, int64_t
         if (t < kept) {
           float s = sv[k][e];
           if (!finite_f(s) || s < 0.0f) { bad = true; s = 0.0f; }
-          c = prompt_class(ah, al, p.prompt_den, canon_zero(s), t, T);
+          c = prompt_class(ah, al, p.prompt_den, canon_zero(s), t, T, p.top, p.alpha_t);
         }
         ch += c == DKV_CLS_HIGH;
         cl += c == DKV_CLS_LOW;
+        ct += c == DKV_CLS_TOP;
         cbytes |= (uint32_t)c << (8 * e);
       }
       nh += __reduce_add_sync(kFull, (unsigned)ch);
       nl += __reduce_add_sync(kFull, (unsigned)cl);
+      if (p.top) nt += __reduce_add_sync(kFull, (unsigned)ct);
       if (crow) {
         const int t = ts + lane * TPL;
         if constexpr (VEC) {
@@ -91,7 +97,7 @@ classify_prefill_kernel(PoolDev p, int n, const float* __restrict__ sig, int64_t
     }
   }
   if (__any_sync(kFull, bad) && lane == 0) set_pending(p.ctrl, DKV_ERR_NONFINITE);   // Q36
-  if (lane == 0) { p.pf_nh[u] = nh; p.pf_nl[u] = nl; }
+  if (lane == 0) { p.pf_nh[u] = nh; p.pf_nl[u] = nl; if (p.top) p.pf_nt[u] = nt; }
 }
 
 cudaError_t launch_classify_prefill(const PoolDev& p, int n, const float* sig, int64_t sig_stride, uint8_t* cls,

@@ -62,14 +62,15 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   // per-unit loads do not depend on the control block: issue them before the first barrier; the request
   // state and counts are not written by dkv_classify, so they may be read before the PDL wait
   const int u = tile * TU + tid;
-  int st = -1, r = 0, nh = 0, nl = 0;
+  int st = -1, r = 0, nh = 0, nl = 0, nt = 0;
   uint32_t dword = 0;
-  int pfh = 0, pfl = 0;
+  int pfh = 0, pfl = 0, pft = 0;
   if (u < p.U) {
     r = u / p.LyH;
     st = p.req_state[r];
     nh = p.n_h[u];
     nl = p.n_l[u];
+    if (p.top) nt = p.n_t[u];                          // NEXT-4 TOP section
   }
   pdl_wait();                                        // (PDL) the decisions and classify's pending error
   pdl_trigger();
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   }
   if (u < p.U) {
     if (phase == DKV_PHASE_DECODE) dword = __ldg(reinterpret_cast<const uint32_t*>(dec + u));
-    else { pfh = p.pf_nh[u]; pfl = p.pf_nl[u]; }
+    else { pfh = p.pf_nh[u]; pfl = p.pf_nl[u]; if (p.top) pft = p.pf_nt[u]; }
   }
   __syncthreads();
   const unsigned long long epoch = s_epoch;
@@ -95,7 +96,8 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   int grow = 0;
   uint32_t dem = 0, fr = 0;
   if (u < p.U) {
-    if (st == DKV_REQ_PENDING_FREE) fr = ceil_div(nh, p.Ch) + ceil_div(nl, p.Cl);
+    const int pt = p.top ? ceil_div(nt, p.Ct) : 0;
+    if (st == DKV_REQ_PENDING_FREE) fr = pt + ceil_div(nh, p.Ch) + ceil_div(nl, p.Cl);
     if (status0 == 0) {
       if (phase == DKV_PHASE_DECODE) {
         if (st == DKV_REQ_ACTIVE) {
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
           grow = (dword >> 16) & 0xFF;
         }
       } else if (st == DKV_REQ_ADMITTING && alloc) {
-        dem = ceil_div(pfh, p.Ch) + ceil_div(pfl, p.Cl);
+        dem = ceil_div(pfh, p.Ch) + ceil_div(pfl, p.Cl) + (p.top ? ceil_div(pft, p.Ct) : 0);   // Q43
       }
     }
   }
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   {
     constexpr int kRecDepth = 8;
     __shared__ uint32_t s_loc[TU];                               // tile-local exclusive freed offset
-    __shared__ int s_nfr[TU], s_ph[TU];
+    __shared__ int s_nfr[TU], s_ph[TU], s_pt[TU];
     const uint32_t tile_ex = s_exfr;
     const uint32_t Ft = s_incfr - tile_ex;                       // freed slots in this tile
     // deferred: in the decode fast path (grants never read a slot recycled in this call) the copy is left to
@@ -178,9 +180,10 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
     // pointer
     const bool defer = defer_rec && phase == DKV_PHASE_DECODE && status0 == 0 && free0 >= (int64_t)p.U;
     if (defer && fr != 0) {
-      p.rec[3 * (size_t)u] = (int32_t)off_fr;
-      p.rec[3 * (size_t)u + 1] = ceil_div(nh, p.Ch);
-      p.rec[3 * (size_t)u + 2] = (int32_t)fr;
+      p.rec[4 * (size_t)u] = (int32_t)off_fr;
+      p.rec[4 * (size_t)u + 1] = ceil_div(nh, p.Ch);
+      p.rec[4 * (size_t)u + 3] = p.top ? ceil_div(nt, p.Ct) : 0;
+      p.rec[4 * (size_t)u + 2] = (int32_t)fr;                    // the marker (non-zero) last
     }
     if (tid == 0 && tile == 0 && defer_rec) {
       int64_t e0 = start0 + free0;
@@ -192,6 +195,7 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
       ring0 -= ring0 >= P ? P : 0;
       ring0 += tile_ex;
       s_loc[tid] = off_fr - tile_ex; s_nfr[tid] = (int)fr; s_ph[tid] = ceil_div(nh, p.Ch);
+      s_pt[tid] = p.top ? ceil_div(nt, p.Ct) : 0;
       __syncthreads();
       const uint32_t per = ((Ft + NW - 1) / NW + 31) & ~31u;     // per-warp chunk, a multiple of 32
       const uint32_t w0 = (uint32_t)warp * per, w1 = min(w0 + per, Ft);
@@ -205,26 +209,24 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
         }
         t = lo;
       }
-      const uint32_t row0 = (uint32_t)(tile * TU) * (uint32_t)L;
       for (uint32_t base = w0; base < w1; base += 32 * kRecDepth) {
-        uint32_t tix[kRecDepth];                                 // table index (unit * L + slot)
+        int32_t* tix[kRecDepth];                                 // the freed slot (TOP table or bidirectional)
 #pragma unroll
         for (int j = 0; j < kRecDepth; j++) {
           const uint32_t k = base + 32 * j + lane;
-          tix[j] = 0xFFFFFFFFu;
+          tix[j] = nullptr;
           if (k < w1) {
             while (k >= s_loc[t] + (uint32_t)s_nfr[t]) t++;
-            const int jj = (int)(k - s_loc[t]), nfr_t = s_nfr[t];
-            const int slot = jj < s_ph[t] ? jj : L - nfr_t + jj;  // [0, ph) then [L - pl, L)
-            tix[j] = row0 + (uint32_t)t * (uint32_t)L + (uint32_t)slot;
+            // [0, pt) of the TOP table, then [0, ph) and [L - pl, L) of the bidirectional one (Q13, Q41)
+            tix[j] = freed_slot(p, tile * TU + t, (int)(k - s_loc[t]), s_pt[t], s_ph[t], s_nfr[t]);
           }
         }
         int32_t pid[kRecDepth];
 #pragma unroll
-        for (int j = 0; j < kRecDepth; j++) pid[j] = tix[j] != 0xFFFFFFFFu ? __ldcg(p.table + tix[j]) : -1;
+        for (int j = 0; j < kRecDepth; j++) pid[j] = tix[j] != nullptr ? __ldcg(tix[j]) : -1;
 #pragma unroll
         for (int j = 0; j < kRecDepth; j++) {
-          if (tix[j] != 0xFFFFFFFFu) {
+          if (tix[j] != nullptr) {
             int64_t pos = ring0 + base + 32 * j + lane;            // < 3P: two conditional wraps, no division
             pos -= pos >= P ? P : 0;
             pos -= pos >= P ? P : 0;
@@ -233,12 +235,12 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
             // miss is outstanding takes a slow path in L2 (see k_quant_decode.cu)
             int32_t empty = -1;
             asm volatile("" : "+r"(empty) : "r"(pid[j]));
-            p.table[tix[j]] = empty;
+            *tix[j] = empty;
           }
         }
       }
     }
-    if (fr != 0) { p.n_h[u] = 0; p.n_l[u] = 0; }
+    if (fr != 0) { p.n_h[u] = 0; p.n_l[u] = 0; if (p.top) p.n_t[u] = 0; }
   }
   __syncthreads();
 
@@ -274,14 +276,16 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
     if (phase == DKV_PHASE_DECODE) {
       if (dem) {
         const int ph = ceil_div(nh, p.Ch), pl = ceil_div(nl, p.Cl);
-        if (ph + pl + 1 > L) {
+        const bool top = grow == DKV_GROW_TOP;                   // NEXT-4: the TOP table, left to right
+        if (top ? nt / p.Ct >= p.Lt : ph + pl + 1 > L) {
           set_status(ctrl, DKV_ERR_OVERFLOW);
         } else {
-          const int slot = (grow == DKV_GROW_HIGH) ? nh / p.Ch : L - 1 - nl / p.Cl;
+          int32_t* slotp = top ? p.ttable + (size_t)u * p.Lt + nt / p.Ct
+                               : p.table + (size_t)u * L + ((grow == DKV_GROW_HIGH) ? nh / p.Ch : L - 1 - nl / p.Cl);
           int64_t pos = start0 + off_dem;                        // < 2P (off_dem < D <= free)
           pos -= pos >= P ? P : 0;
           const int32_t pid = __ldcg(p.ring + pos);
-          p.table[(size_t)u * L + slot] = pid;
+          *slotp = pid;
           // for dkv_quant_write: the granted page is t_c's (KEEP) or the downgraded victim's KV_l page (DOWN)
           reinterpret_cast<int32_t*>(p.qpid + u)[((dword >> 8) & 0xFF) == DKV_V_DOWN ? 1 : 0] = pid;
         }
@@ -289,6 +293,7 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
       if (st == DKV_REQ_ACTIVE) {
         if (grow == DKV_GROW_HIGH) p.n_h[u] = nh + 1;
         if (grow == DKV_GROW_LOW) p.n_l[u] = nl + 1;             // DOWN: n_h unchanged, n_l + 1
+        if (grow == DKV_GROW_TOP) p.n_t[u] = nt + 1;
       }
     } else {
       unsigned gm = __ballot_sync(kFull, dem != 0);
@@ -299,19 +304,25 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
         const uint32_t off = __shfl_sync(kFull, off_dem, src);
         const int nd = (int)__shfl_sync(kFull, dem, src);
         const int ph = ceil_div(p.pf_nh[uu], p.Ch);
-        if (nd > L) {
+        const int pt = p.top ? ceil_div(p.pf_nt[uu], p.Ct) : 0;   // Q43: a unit's TOP pages first
+        if (nd - pt > L || pt > p.Lt) {
           if (lane == 0) set_status(ctrl, DKV_ERR_OVERFLOW);
           continue;
         }
         int32_t* row = p.table + (size_t)uu * L;
+        int32_t* trow = p.ttable + (size_t)uu * p.Lt;
         for (int k = lane; k < nd; k += 32) {
-          const int slot = k < ph ? k : L - 1 - (k - ph);       // high left-to-right, low right-to-left
+          const int kk = k - pt;                                 // high left-to-right, low right-to-left
+          int32_t* slotp = kk < 0 ? trow + k : row + (kk < ph ? kk : L - 1 - (kk - ph));
           int64_t pos = start0 + off + k;                        // < 2P
           pos -= pos >= P ? P : 0;
-          row[slot] = __ldcg(p.ring + pos);
+          *slotp = __ldcg(p.ring + pos);
         }
       }
-      if (st == DKV_REQ_ADMITTING && alloc) { p.n_h[u] = p.pf_nh[u]; p.n_l[u] = p.pf_nl[u]; }
+      if (st == DKV_REQ_ADMITTING && alloc) {
+        p.n_h[u] = p.pf_nh[u]; p.n_l[u] = p.pf_nl[u];
+        if (p.top) p.n_t[u] = p.pf_nt[u];
+      }
     }
   }
   // ---- request-level transitions, by the tile owning the request's LAST unit: every other tile holding
@@ -409,37 +420,34 @@ __global__ void __launch_bounds__(256) recycle_kernel(PoolDev p, RecList l) {
   const int wu = (blockIdx.x * 256 + threadIdx.x) >> 5;         // index over the freed requests' units
   if (wu >= l.n * p.LyH) return;
   const int u = l.req[wu / p.LyH] * p.LyH + wu % p.LyH;
-  const int32_t nfr = p.rec[3 * (size_t)u + 2];
+  const int32_t nfr = p.rec[4 * (size_t)u + 2];
   if (nfr == 0) return;                                         // warp-uniform
-  const int32_t off = p.rec[3 * (size_t)u], ph = p.rec[3 * (size_t)u + 1];
-  const int P = p.P, L = p.L;
+  const int32_t off = p.rec[4 * (size_t)u], ph = p.rec[4 * (size_t)u + 1], pt = p.rec[4 * (size_t)u + 3];
+  const int P = p.P;
   const int64_t ring0 = p.ctrl->rec_end0 + off;                  // < 2P
-  int32_t* row = p.table + (size_t)u * L;
   for (int k0 = 0; k0 < nfr; k0 += 32 * 8) {
     int32_t pid[8];
 #pragma unroll
     for (int j = 0; j < 8; j++) {
       const int k = k0 + 32 * j + lane;
-      const int slot = k < ph ? k : L - nfr + k;                 // [0, ph) then [L - pl, L)
-      pid[j] = k < nfr ? __ldcg(row + slot) : -1;
+      pid[j] = k < nfr ? __ldcg(freed_slot(p, u, k, pt, ph, nfr)) : -1;
     }
 #pragma unroll
     for (int j = 0; j < 8; j++) {
       const int k = k0 + 32 * j + lane;
       if (k < nfr) {
-        const int slot = k < ph ? k : L - nfr + k;
         int64_t pos = ring0 + k;                                 // < 3P
         pos -= pos >= P ? P : 0;
         pos -= pos >= P ? P : 0;
         p.ring[pos] = pid[j];
         int32_t empty = -1;                                      // clear only after the load returned
         asm volatile("" : "+r"(empty) : "r"(pid[j]));
-        row[slot] = empty;
+        *freed_slot(p, u, k, pt, ph, nfr) = empty;
       }
     }
   }
   __syncwarp();
-  if (lane == 0) p.rec[3 * (size_t)u + 2] = 0;                  // marker consumed
+  if (lane == 0) p.rec[4 * (size_t)u + 2] = 0;                  // marker consumed
 }
 
 cudaError_t launch_recycle(const PoolDev& p, const int32_t* req, int n, cudaStream_t s) {

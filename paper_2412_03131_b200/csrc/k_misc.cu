@@ -10,6 +10,8 @@ __global__ void init_kernel(PoolDev p) {
   for (size_t i = tid; i < (size_t)p.P; i += nth) p.ring[i] = (int32_t)i;
   const size_t UL = (size_t)p.U * p.L;
   for (size_t i = tid; i < UL; i += nth) p.table[i] = -1;
+  const size_t ULt = (size_t)p.U * p.Lt;                    // NEXT-4 TOP table
+  for (size_t i = tid; i < ULt; i += nth) p.ttable[i] = -1;
   for (size_t i = tid; i < (size_t)p.U; i += nth) {
     p.n_h[i] = 0; p.n_l[i] = 0; p.pf_nh[i] = 0; p.pf_nl[i] = 0;
   }

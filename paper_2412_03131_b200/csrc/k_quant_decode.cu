@@ -274,38 +274,35 @@ __device__ __forceinline__ void dequant_lane(const uint4 c, int bits, uint32_t m
 // whose marker (freed != 0) is consumed here.
 template <int G>
 __device__ __forceinline__ void recycle_unit(const PoolDev& p, int u, int q, unsigned gmask, int64_t end0) {
-  const int32_t nfr = p.rec[3 * (size_t)u + 2];
+  const int32_t nfr = p.rec[4 * (size_t)u + 2];
   if (nfr == 0) return;                                  // group-uniform
-  const int32_t off = p.rec[3 * (size_t)u], ph = p.rec[3 * (size_t)u + 1];
-  const int P = p.P, L = p.L;
+  const int32_t off = p.rec[4 * (size_t)u], ph = p.rec[4 * (size_t)u + 1], pt = p.rec[4 * (size_t)u + 3];
+  const int P = p.P;
   const int64_t ring0 = end0 + off;                      // < 2P
-  int32_t* row = p.table + (size_t)u * L;
   constexpr int kDepth = 8;
   for (int k0 = 0; k0 < nfr; k0 += G * kDepth) {
     int32_t pid[kDepth];
 #pragma unroll
     for (int j = 0; j < kDepth; j++) {
       const int k = k0 + G * j + q;
-      const int slot = k < ph ? k : L - nfr + k;
-      pid[j] = k < nfr ? __ldcg(row + slot) : -1;
+      pid[j] = k < nfr ? __ldcg(freed_slot(p, u, k, pt, ph, nfr)) : -1;
     }
 #pragma unroll
     for (int j = 0; j < kDepth; j++) {
       const int k = k0 + G * j + q;
       if (k < nfr) {
-        const int slot = k < ph ? k : L - nfr + k;
         int64_t pos = ring0 + k;                         // < 3P: two conditional wraps, no division
         pos -= pos >= P ? P : 0;
         pos -= pos >= P ? P : 0;
         p.ring[pos] = pid[j];
         int32_t empty = -1;                              // clear only after the load returned (see the header)
         asm volatile("" : "+r"(empty) : "r"(pid[j]));
-        row[slot] = empty;
+        *freed_slot(p, u, k, pt, ph, nfr) = empty;
       }
     }
   }
   __syncwarp(gmask);
-  if (q == 0) p.rec[3 * (size_t)u + 2] = 0;
+  if (q == 0) p.rec[4 * (size_t)u + 2] = 0;
 }
 
 template <int D, int G>
@@ -377,13 +374,37 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
     const int pc = N - 1 - p.W;
     const int tc_class = dw.x & 0xFF, v_action = (dw.x >> 8) & 0xFF;
     const int v_slot = dw.y, tc_slot = dw.z, v_dst = dw.w;
-    const bool has_tc = live && (tc_class == DKV_CLS_HIGH || tc_class == DKV_CLS_LOW);
+    const bool has_tc = live && (tc_class == DKV_CLS_HIGH || tc_class == DKV_CLS_LOW || tc_class == DKV_CLS_TOP);
     const bool down = live && v_action == DKV_V_DOWN;
-    const bool tc_high = tc_class == DKV_CLS_HIGH;
-    const int tc_pg = fdiv(tc_high ? p.div_Ch : p.div_Cl, tc_slot);
+    const bool tc_high = tc_class == DKV_CLS_HIGH, tc_top = tc_class == DKV_CLS_TOP;
+    const int tc_pg = fdiv(tc_top ? p.div_Ct : (tc_high ? p.div_Ch : p.div_Cl), tc_slot);
     const int pid_tc = qp.x, pid_src = qp.x, pid_dst = qp.y;   // the victim's KV_h slot is t_c's slot (Q8)
 
 
+    // ---- C + 1. NEXT-4 (Q42): a TOP victim's fp16 rows quantized at the class it moves to (grow)
+    if (down && tc_top) {                                // group-uniform
+      const ClassGeom gt = p.gt, go = geom_of(p, dw.x >> 16 & 0xFF);
+      const int is = fmod_(p.div_Ct, v_slot);
+      const int id = fmod_((((dw.x >> 16) & 0xFF) == DKV_GROW_HIGH) ? p.div_Ch : p.div_Cl, v_dst);
+      const uint8_t* src = p.pages + (size_t)pid_src * (size_t)p.page_bytes;
+      uint8_t* dst = p.pages + (size_t)pid_dst * (size_t)p.page_bytes;
+      const HVec<EPL> xk = load_hvec<EPL>(reinterpret_cast<const uint16_t*>(src + gt.off_k + is * gt.k_row), q);
+      const HVec<EPL> xv = load_hvec<EPL>(reinterpret_cast<const uint16_t*>(src + gt.off_v + is * gt.v_row), q);
+      uint32_t carry = 0;                                // lane 2: score bits, lane 3: position
+      if (q == 2) carry = *reinterpret_cast<const uint32_t*>(src + gt.off_score + 4 * is);
+      if (q == 3) carry = *reinterpret_cast<const uint32_t*>(src + gt.off_pos + 4 * is);
+      uint32_t mk, mv;
+      bool fk, fv;                                       // stored TOP rows are finite (Q30 at insertion)
+      const uint4 pk = quant_h16_lane<G, EPL>(xk, go.kbits, gmask, mk, fk);
+      const uint4 pv = quant_h16_lane<G, EPL>(xv, go.vbits, gmask, mv, fv);
+      store_codes_lane<EPL>(dst + go.off_k + id * go.k_row, q, go.kbits, pk);
+      store_codes_lane<EPL>(dst + go.off_v + id * go.v_row, q, go.vbits, pv);
+      if (q == 0) *reinterpret_cast<uint32_t*>(dst + go.off_kmeta + 4 * id) = mk;
+      if (q == 1) *reinterpret_cast<uint32_t*>(dst + go.off_vmeta + 4 * id) = mv;
+      if (q == 2) *reinterpret_cast<uint32_t*>(dst + go.off_score + 4 * id) = carry;
+      if (q == 3) *reinterpret_cast<uint32_t*>(dst + go.off_pos + 4 * id) = carry;
+      __syncwarp(gmask);                                 // every lane's read of t_v precedes t_c's stores
+    } else
     // ---- C + 1. downgrade t_v: K8V4 -> K4V2 (Q9)
     if (down) {                                          // group-uniform
       const ClassGeom gh = p.g[1], go = p.g[2];
@@ -417,6 +438,26 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
     bool rejected = false;                               // Q30: a non-finite t_c leaves slot and window as they are
     if (has_tc) {                                        // group-uniform
       if (p.W == 0) { wk = lds_hvec<EPL>(my_nk); wv = lds_hvec<EPL>(my_nv); }   // t_c is the new token
+      if (tc_top) {                                      // NEXT-4 (Q40): t_c kept as its fp16 rows
+        bool fin = true;
+#pragma unroll
+        for (int i = 0; i < EPL / 2; i++) {
+          fin &= ((wk.w[i] & 0x7C00u) != 0x7C00u) && ((wk.w[i] & 0x7C000000u) != 0x7C000000u);
+          fin &= ((wv.w[i] & 0x7C00u) != 0x7C00u) && ((wv.w[i] & 0x7C000000u) != 0x7C000000u);
+        }
+        if ((__ballot_sync(gmask, !fin) & gmask) != 0u) {                       // Q30: rejected whole
+          if (q == 0) set_status(p.ctrl, DKV_ERR_NONFINITE);
+          rejected = true;
+        } else {
+          const ClassGeom gt = p.gt;
+          const int idx = tc_slot - tc_pg * gt.C;
+          uint8_t* pg = p.pages + (size_t)pid_tc * (size_t)p.page_bytes;
+          store_hvec<EPL>(reinterpret_cast<uint16_t*>(pg + gt.off_k + idx * gt.k_row), q, wk);
+          store_hvec<EPL>(reinterpret_cast<uint16_t*>(pg + gt.off_v + idx * gt.v_row), q, wv);
+          if (q == 2) *reinterpret_cast<float*>(pg + gt.off_score + 4 * idx) = canon_zero(s_in);
+          if (q == 3) *reinterpret_cast<int32_t*>(pg + gt.off_pos + 4 * idx) = pc;
+        }
+      } else {
       const ClassGeom g = geom_of(p, tc_class);
       uint32_t mk, mv;
       bool fk, fv;
@@ -434,6 +475,7 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
         if (q == 1) *reinterpret_cast<uint32_t*>(pg + g.off_vmeta + 4 * idx) = mv;
         if (q == 2) *reinterpret_cast<float*>(pg + g.off_score + 4 * idx) = canon_zero(s_in);
         if (q == 3) *reinterpret_cast<int32_t*>(pg + g.off_pos + 4 * idx) = pc;
+      }
       }
     }
     // 3. window push, after t_c's row has been consumed

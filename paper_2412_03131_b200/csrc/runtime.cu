@@ -35,9 +35,25 @@ constexpr int kAttSlots = 296;                               // 2 x 148 SMs
 constexpr int64_t kAttSmemLongThreshold = 160 * 1024;         // logits + (s, z) bytes beyond which HBM slots exist
 
 struct Geometry {
-  int32_t U, L, page_bytes, num_tiles, tile_units, nseg;
+  int32_t U, L, page_bytes, num_tiles, tile_units, nseg, Lt;
   ClassGeom g[3];
+  ClassGeom gt;                                              // NEXT-4 TOP class (fp16 rows)
+  int64_t off_pf_nt, off_pf_seg_t;                           // NEXT-4 prompt scratch (not in dkv_layout_t)
 };
+
+// NEXT-4 (Q40): a TOP page = C fp16 K rows, C fp16 V rows (no metadata), scores, positions; 16-B aligned
+void top_geom(int d, int C, ClassGeom& g) {
+  auto a16 = [](int x) { return (x + 15) / 16 * 16; };
+  g.C = C; g.kbits = 16; g.vbits = 16;
+  g.k_row = 2 * d;
+  g.v_row = 2 * d;
+  g.off_k = 0;
+  g.off_kmeta = g.off_k + C * g.k_row;                       // empty
+  g.off_v = a16(g.off_kmeta);
+  g.off_vmeta = g.off_v + C * g.v_row;                       // empty
+  g.off_score = a16(g.off_vmeta);
+  g.off_pos = a16(g.off_score + 4 * C);
+}
 
 bool validate(const dkv_config_t* c, Geometry& G) {
   if (!c) return false;
@@ -55,6 +71,10 @@ bool validate(const dkv_config_t* c, Geometry& G) {
   if (c->tile_units != 0 && c->tile_units != 256 && c->tile_units != 512 && c->tile_units != 1024) return false;
   if (c->prefill_workflow != 0 && c->prefill_workflow != 1) return false;
   if (c->q_per_kv < 0 || c->q_per_kv > 16) return false;
+  // NEXT-4 (Q38, Q43): alpha_t >= alpha_h, TOP pages of whole 4-token groups, the exact prompt workflow
+  if (c->top_tier != 0 && (c->top_tier != 1 || !(c->alpha_t >= c->alpha_h && c->alpha_t <= 3.0e38f) ||
+                           c->page_tokens_top < 4 || c->page_tokens_top % 4 || c->prefill_workflow != 0))
+    return false;
   const int64_t U = (int64_t)c->max_requests * c->num_layers * c->num_kv_heads;
   if (U >= (1 << 24)) return false;
   G.U = (int32_t)U;
@@ -64,7 +84,15 @@ bool validate(const dkv_config_t* c, Geometry& G) {
   class_geom(c->head_dim, c->page_tokens_high, c->kbits_high, c->vbits_high, G.g[DKV_CLS_HIGH]);
   class_geom(c->head_dim, c->page_tokens_low, c->kbits_low, c->vbits_low, G.g[DKV_CLS_LOW]);
   G.g[0] = G.g[DKV_CLS_HIGH];
-  const int e = class_end(G.g[1]) > class_end(G.g[2]) ? class_end(G.g[1]) : class_end(G.g[2]);
+  int e = class_end(G.g[1]) > class_end(G.g[2]) ? class_end(G.g[1]) : class_end(G.g[2]);
+  G.Lt = 1;
+  memset(&G.gt, 0, sizeof(G.gt));
+  if (c->top_tier) {
+    top_geom(c->head_dim, c->page_tokens_top, G.gt);
+    if (class_end(G.gt) > e) e = class_end(G.gt);
+    G.Lt = (c->max_seq_len + c->page_tokens_top - 1) / c->page_tokens_top;   // Q41
+    if ((int64_t)G.U * G.Lt >= (1 << 28)) return false;
+  }
   G.page_bytes = (e + 127) / 128 * 128;
   G.tile_units = c->tile_units ? c->tile_units : 1024;
   G.num_tiles = (G.U + G.tile_units - 1) / G.tile_units;
@@ -82,7 +110,7 @@ bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
   Lo.off_stats = take(32);
   Lo.off_tile_status = take(8 * (int64_t)G.num_tiles);
   Lo.off_tile_sums = take(24 * (int64_t)G.num_tiles);
-  Lo.off_rec = take(12 * (int64_t)G.U);
+  Lo.off_rec = take(16 * (int64_t)G.U);
   Lo.off_win_sig = take(4 * (int64_t)G.U * c->window);
   Lo.off_secmin = take(32 * (int64_t)G.U);
   Lo.off_head_alpha = take(8 * (int64_t)c->num_layers * c->num_kv_heads);
@@ -96,6 +124,7 @@ bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
   Lo.off_qpid = take(8 * U);
   Lo.off_ring = take(4 * P);
   Lo.off_table = take(4 * U * G.L);
+  Lo.off_ttable = take(4 * U * G.Lt);
   Lo.off_n_h = take(4 * U);
   Lo.off_n_l = take(4 * U);
   Lo.off_req_state = take(R);
@@ -105,6 +134,9 @@ bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
   Lo.off_pf_nh = take(4 * U);
   Lo.off_pf_nl = take(4 * U);
   Lo.off_pf_seg = take(8 * U * G.nseg);
+  Lo.off_n_t = take(4 * U);                                  // NEXT-4 (zeroed with the prefill scratch)
+  G.off_pf_nt = take(4 * U);
+  G.off_pf_seg_t = take(4 * U * G.nseg);
   const int64_t wbytes = 2 * U * (int64_t)c->window * c->head_dim;
   Lo.off_win_k = take(wbytes);
   Lo.off_win_v = take(wbytes);
@@ -113,6 +145,9 @@ bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
   Lo.arena_bytes = o;
   Lo.units = G.U; Lo.table_len = G.L; Lo.page_bytes = G.page_bytes; Lo.num_tiles = G.num_tiles;
   Lo.tile_units = G.tile_units; Lo.seg_tokens = kSegTokens; Lo.num_segs = G.nseg;
+  Lo.table_len_top = G.Lt;
+  Lo.C_top = G.gt.C; Lo.row_top = G.gt.k_row; Lo.off_k_top = G.gt.off_k; Lo.off_v_top = G.gt.off_v;
+  Lo.off_score_top = G.gt.off_score; Lo.off_pos_top = G.gt.off_pos;
   for (int k = 1; k <= 2; k++) {
     const ClassGeom& g = G.g[k];
     Lo.C[k] = g.C; Lo.k_row[k] = g.k_row; Lo.v_row[k] = g.v_row; Lo.off_k[k] = g.off_k;
@@ -239,6 +274,16 @@ dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_
   d.win_sig = (float*)(b + Lo.off_win_sig);
   d.secmin = (int32_t*)(b + Lo.off_secmin);
   d.qpid = (int2*)(b + Lo.off_qpid);
+  d.top = cfg->top_tier;
+  d.alpha_t = cfg->alpha_t;
+  d.Lt = G.Lt;
+  d.Ct = cfg->top_tier ? cfg->page_tokens_top : 4;
+  d.gt = G.gt;
+  d.ttable = (int32_t*)(b + Lo.off_ttable);
+  d.n_t = (int32_t*)(b + Lo.off_n_t);
+  d.pf_nt = (int32_t*)(b + G.off_pf_nt);
+  d.pf_seg_t = (int32_t*)(b + G.off_pf_seg_t);
+  d.div_Ct = make_fastdiv(d.Ct);
   d.head_alpha = (float*)(b + Lo.off_head_alpha);
   {
     const int64_t GP = (cfg->q_per_kv + 3) / 4 * 4, Mp = (cfg->max_seq_len + 31) / 32 * 32;
@@ -405,7 +450,7 @@ dkv_status_t dkv_quant_write(dkv_pool_t p, int32_t phase, const dkv_decision_t* 
 }
 
 dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* d_probs, dkv_stream_t s) {
-  if (!p || !d_q) return DKV_ERR_INVALID_ARG;
+  if (!p || !d_q || p->cfg.top_tier) return DKV_ERR_INVALID_ARG;   // NEXT-4 tier: no attention (Q44)
   if (p->seq != SEQ_IDLE) return DKV_ERR_STATE;                // between sequences only
   const int G = p->cfg.q_per_kv;
   if (!(G == 1 || G == 2 || G == 4 || G == 5 || G == 7 || G == 8)) return DKV_ERR_INVALID_ARG;
@@ -427,7 +472,7 @@ dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* 
 }
 
 dkv_status_t dkv_attend_tc(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* d_probs, dkv_stream_t s) {
-  if (!p || !d_q) return DKV_ERR_INVALID_ARG;
+  if (!p || !d_q || p->cfg.top_tier) return DKV_ERR_INVALID_ARG;
   if (p->seq != SEQ_IDLE) return DKV_ERR_STATE;
   const int G = p->cfg.q_per_kv;
   if (!(G == 1 || G == 2 || G == 4 || G == 5 || G == 7 || G == 8)) return DKV_ERR_INVALID_ARG;
@@ -458,6 +503,7 @@ dkv_status_t dkv_set_head_thresholds(dkv_pool_t p, const float* h_alpha_h, const
   for (int i = 0; i < LyH; i++) {
     const float a = h_alpha_h[i], b = h_alpha_l[i];
     if (!(a >= 0.0f && a <= 3.0e38f) || !(b >= 0.0f && b <= 3.0e38f)) return DKV_ERR_INVALID_ARG;
+    if (p->cfg.top_tier && a > p->cfg.alpha_t) return DKV_ERR_INVALID_ARG;   // Q38: alpha_h <= alpha_t
     v[2 * i] = a;
     v[2 * i + 1] = b;
   }

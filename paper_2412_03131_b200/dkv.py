@@ -42,7 +42,8 @@ class dkv_config_t(C.Structure):
         "max_requests", "num_layers", "num_kv_heads", "head_dim", "max_seq_len", "window", "page_tokens_high",
         "page_tokens_low", "kbits_high", "vbits_high", "kbits_low", "vbits_low", "num_pages")] + \
         [("alpha_h", C.c_float), ("alpha_l", C.c_float), ("prompt_denominator", C.c_int32),
-         ("tile_units", C.c_int32), ("prefill_workflow", C.c_int32), ("q_per_kv", C.c_int32)]
+         ("tile_units", C.c_int32), ("prefill_workflow", C.c_int32), ("q_per_kv", C.c_int32),
+         ("top_tier", C.c_int32), ("alpha_t", C.c_float), ("page_tokens_top", C.c_int32)]
 
 
 class dkv_decision_t(C.Structure):
@@ -66,7 +67,12 @@ class dkv_layout_t(C.Structure):
                                        "off_score", "off_pos")] + [("off_tile_sums", C.c_int64), ("off_rec", C.c_int64),
                                                                   ("off_win_sig", C.c_int64), ("off_secmin", C.c_int64),
                                                                   ("off_head_alpha", C.c_int64),
-                                                                  ("off_att_scratch", C.c_int64), ("off_qpid", C.c_int64)]
+                                                                  ("off_att_scratch", C.c_int64),
+                                                                  ("off_ttable", C.c_int64), ("off_n_t", C.c_int64),
+                                                                  ("table_len_top", C.c_int32), ("C_top", C.c_int32),
+                                                                  ("row_top", C.c_int32), ("off_k_top", C.c_int32),
+                                                                  ("off_v_top", C.c_int32), ("off_score_top", C.c_int32),
+                                                                  ("off_pos_top", C.c_int32), ("off_qpid", C.c_int64)]
 
 
 assert C.sizeof(dkv_decision_t) == 16
@@ -280,10 +286,12 @@ def dkv_status_string(st) -> str:
 
 
 def make_config(R, Ly, H, d, M, W, Ch=16, Cl=32, kbh=8, vbh=4, kbl=4, vbl=2, P=1024, alpha_h=1.0, alpha_l=0.02,
-                prompt_denominator=0, tile_units=0, prefill_workflow=0, q_per_kv=0) -> dkv_config_t:
+                prompt_denominator=0, tile_units=0, prefill_workflow=0, q_per_kv=0, top_tier=0, alpha_t=0.0,
+                page_tokens_top=4) -> dkv_config_t:
     c = dkv_config_t(max_requests=R, num_layers=Ly, num_kv_heads=H, head_dim=d, max_seq_len=M, window=W,
                      page_tokens_high=Ch, page_tokens_low=Cl, kbits_high=kbh, vbits_high=vbh, kbits_low=kbl,
                      vbits_low=vbl, num_pages=P, alpha_h=alpha_h, alpha_l=alpha_l,
                      prompt_denominator=prompt_denominator, tile_units=tile_units,
-                     prefill_workflow=prefill_workflow, q_per_kv=q_per_kv)
+                     prefill_workflow=prefill_workflow, q_per_kv=q_per_kv, top_tier=top_tier, alpha_t=alpha_t,
+                     page_tokens_top=page_tokens_top)
     return c

@@ -118,14 +118,21 @@ class Pool:
             stats=self._view(L.off_stats, 32, torch.int64, (4,)),
             win_sig=self._view(L.off_win_sig, 4 * U * W, torch.float32, (U, W)),
             secmin=self._view(L.off_secmin, 32 * U, torch.int32, (U, 8)),
+            ttable=self._view(L.off_ttable, 4 * U * L.table_len_top, torch.int32, (U, L.table_len_top)),   # NEXT-4
+            n_t=self._view(L.off_n_t, 4 * U, torch.int32, (U,)),
         )
 
     def geom(self):
         L, cf = self.layout, self.cfg
         bits = {1: (cf.kbits_high, cf.vbits_high), 2: (cf.kbits_low, cf.vbits_low)}
-        return {c: dict(C=L.C[c], kbits=bits[c][0], vbits=bits[c][1], k_row=L.k_row[c], v_row=L.v_row[c], off_k=L.off_k[c], off_kmeta=L.off_kmeta[c],
-                        off_v=L.off_v[c], off_vmeta=L.off_vmeta[c], off_score=L.off_score[c], off_pos=L.off_pos[c])
-                for c in (1, 2)}
+        g = {c: dict(C=L.C[c], kbits=bits[c][0], vbits=bits[c][1], k_row=L.k_row[c], v_row=L.v_row[c], off_k=L.off_k[c], off_kmeta=L.off_kmeta[c],
+                     off_v=L.off_v[c], off_vmeta=L.off_vmeta[c], off_score=L.off_score[c], off_pos=L.off_pos[c])
+             for c in (1, 2)}
+        if cf.top_tier:                                  # NEXT-4 TOP pages: fp16 rows, no metadata
+            g[4] = dict(C=L.C_top, kbits=16, vbits=16, k_row=L.row_top, v_row=L.row_top, off_k=L.off_k_top,
+                        off_kmeta=L.off_k_top + L.C_top * L.row_top, off_v=L.off_v_top,
+                        off_vmeta=L.off_v_top + L.C_top * L.row_top, off_score=L.off_score_top, off_pos=L.off_pos_top)
+        return g
 
 
 class DecodeGraph:

@@ -16,7 +16,7 @@ class GpuBackend:
         self.scn = scn
         cfg = D.make_config(scn.R, scn.Ly, scn.H, scn.d, scn.M, scn.W, scn.Ch, scn.Cl, scn.kbh, scn.vbh, scn.kbl,
                             scn.vbl, scn.P, scn.alpha_h, scn.alpha_l, scn.prompt_denominator, scn.tile_units,
-                            scn.prefill_workflow, scn.q_per_kv)
+                            scn.prefill_workflow, scn.q_per_kv, scn.top_tier, scn.alpha_t, scn.Ct)
         self.pool = Pool(cfg, device=device)
         self.U, self.L, self.page_bytes = self.pool.U, self.pool.L, self.pool.page_bytes
         self.v = self.pool.views()
@@ -86,9 +86,10 @@ class GpuBackend:
 
     def drift(self, step):
         v = self.v
+        top = self.scn.top_tier
         synth.apply_drift(self.scn.seed, step, self.scn.shape, v["pages"], v["table"], v["n_h"], v["n_l"],
-                          {c: (self.geom[c]["C"], self.geom[c]["off_score"], self.geom[c]["off_pos"]) for c in (1, 2)},
-                          self.L)
+                          {c: (self.geom[c]["C"], self.geom[c]["off_score"], self.geom[c]["off_pos"]) for c in self.geom},
+                          self.L, ttable=v["ttable"] if top else None, n_t=v["n_t"] if top else None)
 
     def snapshot(self, pages=True):
         torch.cuda.synchronize()
@@ -99,6 +100,8 @@ class GpuBackend:
                  n_l=v["n_l"].cpu().numpy(), req_state=v["req_state"].cpu().numpy(),
                  seq_len=v["seq_len"].cpu().numpy(), win_k=v["win_k"].cpu().numpy().view(np.uint16),
                  win_v=v["win_v"].cpu().numpy().view(np.uint16), win_sig=v["win_sig"].cpu().numpy())
+        if self.scn.top_tier:
+            s.update(ttable=v["ttable"].cpu().numpy(), n_t=v["n_t"].cpu().numpy())
         if pages:
             s["pages"] = v["pages"].cpu().numpy()
         return s
@@ -111,7 +114,7 @@ def dec_np(dec):
 
 
 def compare_state(a, b, keys=("ring", "start", "free", "table", "n_h", "n_l", "req_state", "seq_len", "win_k", "win_v",
-                              "win_sig",
+                              "win_sig", "ttable", "n_t",
                               "pages"), where=""):
     for k in keys:
         if k not in a or k not in b:
