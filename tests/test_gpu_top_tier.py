@@ -33,7 +33,7 @@ def test_top_tier_d128_victims_and_recycling(tile_units, tight):
         probe = H.OracleBackend(base)
         inp, life = H.Inputs(base), H.Lifecycle(base)
         H.admit([probe], inp, life, list(range(6)), lens)
-        scn = base.replace(P=(60000 - int(probe.pool.free)) + base.U // 2)
+        scn = base.replace(P=(60000 - int(probe.pool.free)) + 3 * base.U // 4)   # OOM-free, free < U
     o, g, life = _lifecycle(scn, steps=24, prompt_lens=lens, frees=[(6, [2]), (14, [0, 4])], readmit_len=260,
                             pages_every=3)
     assert (o.pool.n_t > 0).any()

@@ -50,9 +50,14 @@ SHAPES = {
     "qwen32b_thinking": dict(R=32, Ly=64, H=8, world=1, d=128, prompt=16384, M=33792, W=64, Ch=16, Cl=32,
                              P=14 << 20, alpha_h=3.0, alpha_l=0.0, mix=(0.4, 0.6, 0.0), seed=3, G=5, steps=12,
                              churn_every=4, group=1),
+    # SURVEY §8(d) / P:703: alpha (1, 0) for Llama-3-70B, no pruning, mix .25 / .75 / 0
     "llama70b_shard8": dict(R=32, Ly=80, H=8, world=8, d=128, prompt=8192, M=9216, W=64, Ch=16, Cl=32,
-                            P=7 << 20, alpha_h=1.0, alpha_l=0.02, mix=(0.35, 0.45, 0.20), seed=4, G=8, steps=12,
+                            P=7 << 20, alpha_h=1.0, alpha_l=0.0, mix=(0.25, 0.75, 0.0), seed=4, G=8, steps=12,
                             churn_every=4, group=16),
+    # NEXT-4 three-level tier FP16-K8V4-K4V2 (readings Q38-Q44) on configs[1]'s shape; no attention (Q44)
+    "llama3_8b_top_tier": dict(R=64, Ly=32, H=8, world=1, d=128, prompt=4096, M=8192, W=64, Ch=16, Cl=32,
+                               P=1 << 22, alpha_h=1.0, alpha_l=0.02, mix=(0.35, 0.45, 0.20), seed=2, G=4, steps=12,
+                               churn_every=4, group=64, top_tier=1, alpha_t=2.0, Ct=4),
     "frag_shard8": dict(R=128, Ly=32, H=8, world=8, d=128, prompt=(256, 4096), M=4608, W=64, Ch=16, Cl=32,
                         P=2_900_000, alpha_h=1.0, alpha_l=0.02, mix=(0.35, 0.45, 0.20), seed=5, G=4, steps=400,
                         churn_every=1, group=64, occupancy=0.90),
@@ -72,7 +77,8 @@ def run(name):
     Tmax = c["prompt"][1] if ragged else c["prompt"]
     cfg = D.make_config(wl.R, c["Ly"], wl.Hl, c["d"], c["M"], c["W"], c["Ch"], c["Cl"], P=c["P"],
                         alpha_h=c["alpha_h"], alpha_l=c["alpha_l"], q_per_kv=c["G"],
-                        prefill_workflow=c.get("workflow", 0))
+                        prefill_workflow=c.get("workflow", 0), top_tier=c.get("top_tier", 0),
+                        alpha_t=c.get("alpha_t", 0.0), page_tokens_top=c.get("Ct", 4))
     pool = Pool(cfg, device=dev)
     if c.get("head_alpha"):                                      # per-(layer, head) pairs around the pool-wide one
         hr = np.random.default_rng(c["seed"] + 99)
@@ -156,7 +162,7 @@ def run(name):
     gen = torch.Generator(device=dev)
     gen.manual_seed(c["seed"])
     for s in range(c["steps"]):
-        next2 = s >= c["steps"] // 2
+        next2 = s >= c["steps"] // 2 and not c.get("top_tier")     # Q44: no attention with the FP16 tier
         if s % c["churn_every"] == c["churn_every"] - 1:
             live = np.nonzero(active)[0]
             if len(live):
