@@ -777,16 +777,26 @@ def run_oracle_sample(args, sample_requests=1, steps=None):
     import oracle  # test infrastructure: bench's cpu_baseline / --impl reference legs only
 
     host = host_cpu()
-    saved = os.sched_getaffinity(0)
-    core = min(saved)
-    os.sched_setaffinity(0, {core})                       # the serial oracle pinned to one core
-    try:
-        o = _oracle_sample(args, oracle, sample_requests, steps)
-    finally:
-        os.sched_setaffinity(0, saved)
+    core = min(os.sched_getaffinity(0))
+    o = _oracle_sample(args, oracle, sample_requests, steps, core)
     o.update(cores=1, core=core, cpu_model=host["cpu_model"], nproc=host["nproc"],
-             pinning=f"sched_setaffinity to core {core} (1 of {host['nproc']} cores)")
+             pinning=f"sched_setaffinity to core {core} (1 of {host['nproc']} cores) around the timed oracle calls")
     return o
+
+
+class _Pinned:
+    """the serial oracle runs pinned to one core (the input generation, torch on CPU, is not
+    timed and keeps every core)"""
+
+    def __init__(self, core):
+        self.core = core
+
+    def __enter__(self):
+        self.saved = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {self.core})
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.saved)
 
 
 def host_cpu():
@@ -802,7 +812,7 @@ def host_cpu():
     return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
-def _oracle_sample(args, oracle, sample_requests, steps):
+def _oracle_sample(args, oracle, sample_requests, steps, core):
     c = CONFIGS[args.config]
     Rs = sample_requests
     T = c["prompt"]
@@ -814,12 +824,13 @@ def _oracle_sample(args, oracle, sample_requests, steps):
     sig, kk, vv = wl.prefill_inputs(T)
     sig_np = sig.numpy()
     k_np, v_np = kk.view(torch.int16).numpy().view(np.uint16), vv.view(torch.int16).numpy().view(np.uint16)
-    t0 = time.perf_counter()
-    pool.classify_prefill(list(range(Rs)), [T] * Rs, sig_np, want_classes=False)
-    pool.compact_alloc(None)
-    t1 = time.perf_counter()
-    pool.quant_write_prefill(k_np, v_np, sig_np)
-    t2 = time.perf_counter()
+    with _Pinned(core):
+        t0 = time.perf_counter()
+        pool.classify_prefill(list(range(Rs)), [T] * Rs, sig_np, want_classes=False)
+        pool.compact_alloc(None)
+        t1 = time.perf_counter()
+        pool.quant_write_prefill(k_np, v_np, sig_np)
+        t2 = time.perf_counter()
     units = Rs * c["Ly"] * c["H"]
     # algorithmic bytes of the sample's bulk write (same accounting as the GPU)
     g = pool.geom
@@ -834,13 +845,14 @@ def _oracle_sample(args, oracle, sample_requests, steps):
         cand, nk, nv = wl.decode_inputs(seq, act)
         cand_np = cand.numpy()
         nk_np, nv_np = nk.view(torch.int16).numpy().view(np.uint16), nv.view(torch.int16).numpy().view(np.uint16)
-        a = time.perf_counter()
-        st, dec = pool.classify_decode(cand_np)
-        b = time.perf_counter()
-        pool.compact_alloc(dec)
-        cc = time.perf_counter()
-        pool.quant_write_decode(dec, nk_np, nv_np, cand_np)
-        dd = time.perf_counter()
+        with _Pinned(core):
+            a = time.perf_counter()
+            st, dec = pool.classify_decode(cand_np)
+            b = time.perf_counter()
+            pool.compact_alloc(dec)
+            cc = time.perf_counter()
+            pool.quant_write_decode(dec, nk_np, nv_np, cand_np)
+            dd = time.perf_counter()
         cls.append(b - a); comp.append(cc - b); qw.append(dd - cc)
         seq += 1
     scale = (c["R"] * c["Ly"] * c["H"]) / units

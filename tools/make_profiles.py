@@ -54,10 +54,9 @@ def launches(tag, path):
         f.write("id,kernel,us\n")
         for i, k, us in order:
             f.write(f"{i},{k},{us:.3f}\n")
-    # decode-phase launches: the trailing run of decode kernels (after the last bulk/prefill launch)
-    last_bulk = max((i for i, k, _ in order if "prefill" in k), default=-1)
-    # the memory manager's decode step (NEXT-2's attention is model compute, reported on its own)
-    dec = [(k, us) for i, k, us in order if i > last_bulk and "attend" not in k]
+    # the memory manager's decode-step kernels (NEXT-2's attention is model compute, reported on its own)
+    dec = [(k, us) for i, k, us in order
+           if any(x in k for x in ("classify_decode", "compact_alloc", "quant_decode", "recycle_kernel"))]
     dper = {}
     for k, us in dec:
         dper.setdefault(k, []).append(us)
