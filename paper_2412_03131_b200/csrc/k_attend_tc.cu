@@ -184,10 +184,10 @@ __device__ __forceinline__ void qk_page(const uint8_t* kseg, int t0, int cnt, co
 #pragma unroll
   for (int tile = 0; tile < CL::C / 16; tile++) {
     if (tile * 16 >= cnt) break;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    float acc2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};   // even / odd groups: two MMA chains
     uint32_t w[2][NW];
-    lds_row<RB, CL::kc, CL::ksh>(kseg, tile * 16 + grp, CL::k_row, RB * tig, w[0]);
-    lds_row<RB, CL::kc, CL::ksh>(kseg, tile * 16 + grp + 8, CL::k_row, RB * tig, w[1]);
+    lds_row<RB, 1, 0>(kseg, tile * 16 + grp, CL::k_row, RB * tig, w[0]);
+    lds_row<RB, 1, 0>(kseg, tile * 16 + grp + 8, CL::k_row, RB * tig, w[1]);
 #pragma unroll
     for (int g = 0; g < D / 16; g++) {
       uint32_t a[4];                                             // a0 / a1: k = 2 tig, 2 tig + 1 (rows grp, grp + 8)
@@ -201,8 +201,11 @@ __device__ __forceinline__ void qk_page(const uint8_t* kseg, int t0, int cnt, co
           else k4_pairs<0>(w[rr][g >> 1], a[rr], a[2 + rr]);
         }
       }
-      mma_f16(acc, a, qb[g][0], qb[g][1]);
+      mma_f16(acc2[g & 1], a, qb[g][0], qb[g][1]);
     }
+    float acc[4];
+#pragma unroll
+    for (int e = 0; e < 4; e++) acc[e] = acc2[0][e] + acc2[1][e];
 #pragma unroll
     for (int hh = 0; hh < 2; hh++) {                             // rows grp, grp + 8
       const int j = tile * 16 + grp + 8 * hh;
@@ -239,7 +242,7 @@ __device__ __forceinline__ void pv_page(const uint8_t* vseg, int t0, int cnt, co
     float bv[4];
 #pragma unroll
     for (int jj = 0; jj < 4; jj++) {
-      const int j = tile * 16 + 4 * tig + jj;
+      const int j = tile * 16 + tig + 4 * jj;                    // k = 2 tig, 2 tig + 1, +8, +9 <-> tig + 4 jj
       float b = 0.0f;
       if (j < cnt && grp < G) {
         const uint32_t vm = vmeta[j];
@@ -256,7 +259,7 @@ __device__ __forceinline__ void pv_page(const uint8_t* vseg, int t0, int cnt, co
     h2_split(bv[2], bv[3], bh1, bl1);
     uint32_t w[4][NW];
 #pragma unroll
-    for (int jj = 0; jj < 4; jj++) lds_row<RB, CL::vc, CL::vsh>(vseg, tile * 16 + 4 * tig + jj, CL::v_row, RB * grp, w[jj]);
+    for (int jj = 0; jj < 4; jj++) lds_row<RB, 1, 0>(vseg, tile * 16 + tig + 4 * jj, CL::v_row, RB * grp, w[jj]);
 #pragma unroll
     for (int g = 0; g < D / 16; g++) {
       // features 2g, 2g + 1 of the lane's run: V4 -> byte g (low / high nibble); V2 -> byte g/2, crumbs at bits
@@ -308,6 +311,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   __shared__ float s_red[kTcWarps][G];
   __shared__ unsigned long long s_min[2];
   __shared__ int s_slot[2];
+  __shared__ __align__(8) uint64_t s_bar[kTcWarps][kTcStages];   // per-warp stage mbarriers (bulk copies)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = lane >> 2, tig = lane & 3;
   const int u = blockIdx.x;
@@ -331,6 +335,8 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   for (int k = tid; k < G * D; k += kTcThreads)
     s_q[k / D][k % D] = __half2float(__ushort_as_half(q[(size_t)u * G * D + k]));
   if (tid < 2) { s_min[tid] = ~0ull; s_slot[tid] = -1; }
+  if (tid < kTcWarps * kTcStages) mbar_init(&s_bar[tid / kTcStages][tid % kTcStages], 1);
+  fence_mbar_init();
   __syncthreads();
   if (tid < G) {
     float sacc = 0.0f;
@@ -358,29 +364,33 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   // ---- phase 1: logits.  Stored pages: each warp its pages (k = warp + i * kTcWarps), K codes (swizzled) + K
   // meta staged kTcStages - 1 pages ahead
   float mx[2] = {-INFINITY, -INFINITY};                           // heads 2 tig, 2 tig + 1
+  // a page's segments land in the warp's stage by 1-D bulk copies (TMA, cp.async.bulk) issued by lane 0, the
+  // stage's mbarrier counting the bytes; rows keep the global (token-major) layout
+  uint64_t* bars = s_bar[warp];
+  uint32_t phase = 0;                                             // bit s: parity of stage s's next completion
   auto stage_k = [&](int k, int slot) {
+    if (lane != 0) return;
     const uint8_t* pg = page_ptr(k);
     uint8_t* dst = mystage + slot * kTcStage;
-    if (k < ph) {
-      stage_codes<HI::k_row, HI::kc, HI::ksh, HI::C>(dst, pg + gh.off_k, lane);
-      stage_seg<4 * HI::C>(dst + HI::C * HI::k_row, pg + gh.off_kmeta, lane);
-    } else {
-      stage_codes<LO::k_row, LO::kc, LO::ksh, LO::C>(dst, pg + gl.off_k, lane);
-      stage_seg<4 * LO::C>(dst + LO::C * LO::k_row, pg + gl.off_kmeta, lane);
-    }
+    const bool hi = k < ph;
+    const int C = hi ? HI::C : LO::C, krow = hi ? HI::k_row : LO::k_row;
+    const int off_k = hi ? gh.off_k : gl.off_k, off_km = hi ? gh.off_kmeta : gl.off_kmeta;
+    mbar_arrive_expect_tx(&bars[slot], (uint32_t)(C * krow + 4 * C));
+    bulk_g2s(dst, pg + off_k, (uint32_t)(C * krow), &bars[slot]);
+    bulk_g2s(dst + C * krow, pg + off_km, (uint32_t)(4 * C), &bars[slot]);
+  };
+  auto stage_wait = [&](int slot) {
+    mbar_wait(&bars[slot], (phase >> slot) & 1u);
+    phase ^= 1u << slot;
   };
   {
 #pragma unroll
-    for (int i = 0; i < kTcStages - 1; i++) {
+    for (int i = 0; i < kTcStages - 1; i++)
       if (i < my_n) stage_k(warp + i * kTcWarps, i);
-      cp_async_commit();
-    }
     for (int i = 0; i < my_n; i++) {
       const int k = warp + i * kTcWarps, slot = i % kTcStages;
       if (i + kTcStages - 1 < my_n) stage_k(warp + (i + kTcStages - 1) * kTcWarps, (i + kTcStages - 1) % kTcStages);
-      cp_async_commit();
-      cp_async_wait<kTcStages - 1>();
-      __syncwarp();
+      stage_wait(slot);
       const uint8_t* kseg = mystage + slot * kTcStage;
       if (k < ph) {
         const int t0 = k * HI::C;
@@ -389,9 +399,9 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
         const int t0 = nh + (k - ph) * LO::C;
         qk_page<D, G, GP, LO>(kseg, t0, min(LO::C, nh + nl - t0), qb, s_qsum, scale, lg, mx, grp, tig);
       }
+      fence_proxy_async_smem();                                   // this stage's reads before its next bulk fill
       __syncwarp();
     }
-    cp_async_wait<0>();
   }
   // window tokens (FP16 keys): rows staged into shared memory (the page stages are free now), then one
   // (token, head) dot product per thread on CUDA cores
@@ -426,6 +436,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
       if (hh == h) wmx[hh] = fmaxf(wmx[hh], l);
   }
   // ---- phase 2: per-head max, p = exp(l - max), Z
+  fence_proxy_async_smem();                                       // the window rows' reads before phase 3's bulk fills
   {
 #pragma unroll
     for (int c = 0; c < 2; c++) {
@@ -488,35 +499,28 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
 #pragma unroll
   for (int h = 0; h < G; h++) izr[h] = s_iz[h];
   auto stage_v = [&](int k, int slot) {
+    if (lane != 0) return;
     const uint8_t* pg = page_ptr(k);
     uint8_t* dst = mystage + slot * kTcStage;
-    if (k < ph) {
-      stage_codes<HI::v_row, HI::vc, HI::vsh, HI::C>(dst, pg + gh.off_v, lane);
-      uint8_t* d2 = dst + HI::C * HI::v_row;
-      stage_seg<4 * HI::C>(d2, pg + gh.off_vmeta, lane);
-      stage_seg<4 * HI::C>(d2 + 4 * HI::C, pg + gh.off_score, lane);
-      stage_seg<4 * HI::C>(d2 + 8 * HI::C, pg + gh.off_pos, lane);
-    } else {
-      stage_codes<LO::v_row, LO::vc, LO::vsh, LO::C>(dst, pg + gl.off_v, lane);
-      uint8_t* d2 = dst + LO::C * LO::v_row;
-      stage_seg<4 * LO::C>(d2, pg + gl.off_vmeta, lane);
-      stage_seg<4 * LO::C>(d2 + 4 * LO::C, pg + gl.off_score, lane);
-      stage_seg<4 * LO::C>(d2 + 8 * LO::C, pg + gl.off_pos, lane);
-    }
+    const bool hi = k < ph;
+    const ClassGeom& gg = hi ? gh : gl;
+    const int C = hi ? HI::C : LO::C, vrow = hi ? HI::v_row : LO::v_row;
+    mbar_arrive_expect_tx(&bars[slot], (uint32_t)(C * vrow + 12 * C));
+    bulk_g2s(dst, pg + gg.off_v, (uint32_t)(C * vrow), &bars[slot]);
+    uint8_t* d2 = dst + C * vrow;                                  // V meta, scores, positions
+    bulk_g2s(d2, pg + gg.off_vmeta, (uint32_t)(4 * C), &bars[slot]);
+    bulk_g2s(d2 + 4 * C, pg + gg.off_score, (uint32_t)(4 * C), &bars[slot]);
+    bulk_g2s(d2 + 8 * C, pg + gg.off_pos, (uint32_t)(4 * C), &bars[slot]);
   };
   const float iz = grp < G ? s_iz[grp] : 0.0f;
   {
 #pragma unroll
-    for (int i = 0; i < kTcStages - 1; i++) {
+    for (int i = 0; i < kTcStages - 1; i++)
       if (i < my_n) stage_v(warp + i * kTcWarps, i);
-      cp_async_commit();
-    }
     for (int i = 0; i < my_n; i++) {
       const int k = warp + i * kTcWarps, slot = i % kTcStages;
       if (i + kTcStages - 1 < my_n) stage_v(warp + (i + kTcStages - 1) * kTcWarps, (i + kTcStages - 1) % kTcStages);
-      cp_async_commit();
-      cp_async_wait<kTcStages - 1>();
-      __syncwarp();
+      stage_wait(slot);
       const uint8_t* vseg = mystage + slot * kTcStage;
       const bool hi = k < ph;
       const int C = hi ? HI::C : LO::C;
@@ -548,9 +552,9 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
         const unsigned long long key = ((unsigned long long)__float_as_uint(sg) << 32) | (uint32_t)pos;
         if (key < mkey[cls]) { mkey[cls] = key; mslot[cls] = slotj; }
       }
+      fence_proxy_async_smem();                                   // this stage's reads before its next bulk fill
       __syncwarp();
     }
-    cp_async_wait<0>();
   }
   __syncthreads();                                                // staging areas are free: reuse for the reduction
   float* part = reinterpret_cast<float*>(stage0);                 // [kTcWarps][G][D] MMA partials
@@ -591,14 +595,22 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   cp_async_wait<0>();
   __syncthreads();
   if (out != nullptr) {
-    for (int e = tid; e < G * D; e += kTcThreads) {
-      const int h = e / D, f = e % D;
-      float o = 0.0f, z = 0.0f;
-      for (int w = 0; w < kTcWarps; w++) { o += part[((size_t)w * G + h) * D + f]; z += zred[w * G + h]; }
-      float wsum = 0.0f;                                          // the window's values (FP16) on CUDA cores
-      for (int i = 0; i < nw; i++)
-        wsum = fmaf(lg[(size_t)(nh + nl + i) * GP + h] * izr[h], __half2float(__ushort_as_half(wvs[(size_t)i * D + f])), wsum);
-      out[((size_t)u * G + h) * D + f] = o + z + wsum;
+    for (int e = tid; e < G * D / 2; e += kTcThreads) {            // a feature pair per thread
+      const int h = e / (D / 2), f = 2 * (e % (D / 2));
+      float o0 = 0.0f, o1 = 0.0f, z = 0.0f;
+      for (int w = 0; w < kTcWarps; w++) {
+        const float2 pp = *reinterpret_cast<const float2*>(part + ((size_t)w * G + h) * D + f);
+        o0 += pp.x; o1 += pp.y; z += zred[w * G + h];
+      }
+      float w0 = 0.0f, w1 = 0.0f;                                  // the window's values (FP16) on CUDA cores
+      const float izh = izr[h];
+      for (int i = 0; i < nw; i++) {
+        const float a = lg[(size_t)(nh + nl + i) * GP + h] * izh;
+        const float2 vv = __half22float2(*reinterpret_cast<const __half2*>(wvs + (size_t)i * D + f));
+        w0 = fmaf(a, vv.x, w0);
+        w1 = fmaf(a, vv.y, w1);
+      }
+      *reinterpret_cast<float2*>(out + ((size_t)u * G + h) * D + f) = make_float2(o0 + z + w0, o1 + z + w1);
     }
   }
   // section minima (stored sections only; keys are unique: positions differ)
