@@ -25,12 +25,20 @@
 //   phase 3: PV by MMA page by page with a = p / Z, the significance of each stored token (page score
 //            segments) and window token, the section minima; the warps' partial outputs are added in a fixed
 //            order (deterministic for a given launch).
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 
 #include "dkv_internal.cuh"
 
 namespace dkv {
 
+namespace cg = cooperative_groups;
+#ifndef DKV_TC_CLUSTER
+#define DKV_TC_CLUSTER 1        // CTAs (a thread-block cluster) sharing one unit's pages: split-sequence attention
+#endif
+#ifndef DKV_TC_MINB
+#define DKV_TC_MINB 2           // CTAs per SM the register budget is sized for
+#endif
 constexpr int kTcWarps = 8;
 constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTcStages = 2;                   // pages in flight per warp (cp.async groups)
@@ -82,10 +90,23 @@ __device__ __forceinline__ uint32_t bsub2_u(uint32_t x, uint32_t m) {
   const __nv_bfloat162 r = __hsub2(*reinterpret_cast<const __nv_bfloat162*>(&x), *reinterpret_cast<const __nv_bfloat162*>(&m));
   return *reinterpret_cast<const uint32_t*>(&r);
 }
+// (x & MASK) | magic in one LOP3 (the compiler splits it into two when both constants are immediates; the magic
+// lives in a register)
+template <uint32_t MASK>
+__device__ __forceinline__ uint32_t and_or(uint32_t x, uint32_t magic) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(x), "n"(MASK), "r"(magic));
+  return d;
+}
 // K8: bytes (c0, c1, c2, c3) of x -> fp16x2 (c0, c1) and (c2, c3): 0x64XX = 1024 + XX
+// The subtraction stays per pair.  Measured alternative (r2v): operands left at M + code with a second MMA whose A
+// operand is the constant -M removing the bias after each group — 10 % fewer instructions but slower (3.82 vs
+// 3.72 ms: dependent MMA pairs on one accumulator) and outside the Eq. 1 output tolerance (8e-5: the accumulator
+// transiently holds M * sum at the tensor core's accumulation precision).
+__device__ __forceinline__ uint32_t unbias(uint32_t x, uint32_t m) { return hsub2_u(x, m); }
 __device__ __forceinline__ void k8_pairs(uint32_t x, uint32_t& lo, uint32_t& hi) {
-  lo = hsub2_u(__byte_perm(x, 0x64646464u, 0x4140), 0x64006400u);
-  hi = hsub2_u(__byte_perm(x, 0x64646464u, 0x4342), 0x64006400u);
+  lo = unbias(__byte_perm(x, 0x64646464u, 0x4140), 0x64006400u);
+  hi = unbias(__byte_perm(x, 0x64646464u, 0x4342), 0x64006400u);
 }
 // K4: the two bytes at byte index KB0 (codes n0 | n1 << 4) and KB0 + 1 (n2 | n3 << 4) of x -> fp16x2 (n0, n1),
 // (n2, n3): n0 in bits 0-3 with 0x6400 (1024, ulp 1), n1 in bits 20-23 = bits 4-7 of the high half with 0x5400
@@ -93,8 +114,8 @@ __device__ __forceinline__ void k8_pairs(uint32_t x, uint32_t& lo, uint32_t& hi)
 template <int KB0>
 __device__ __forceinline__ void k4_pairs(uint32_t x, uint32_t& lo, uint32_t& hi) {
   constexpr uint32_t s0 = KB0 * 0x1111u, s1 = (KB0 + 1) * 0x1111u;
-  lo = hsub2_u((__byte_perm(x, 0u, s0) & 0x00F0000Fu) | 0x54006400u, 0x54006400u);
-  hi = hsub2_u((__byte_perm(x, 0u, s1) & 0x00F0000Fu) | 0x54006400u, 0x54006400u);
+  lo = unbias(and_or<0x00F0000Fu>(__byte_perm(x, 0u, s0), 0x54006400u), 0x54006400u);
+  hi = unbias(and_or<0x00F0000Fu>(__byte_perm(x, 0u, s1), 0x54006400u), 0x54006400u);
 }
 // V: byte K of x (token j0) and of y (token j1) -> fp16x2 (field of j0, field of j1) for the field at bits
 // [SH, SH + VB) of that byte; the magic makes bit SH weigh 1 (fp16, 10 mantissa bits: a value in [2^e, 2^(e+1))
@@ -105,8 +126,9 @@ __device__ __forceinline__ uint32_t v_pair(uint32_t x, uint32_t y) {
   constexpr uint32_t sel = K | (K << 4) | ((4 + K) << 8) | ((4 + K) << 12);
   constexpr uint32_t mask = (((1u << VB) - 1u) << SH) * 0x00010001u;
   constexpr uint32_t magic = (SH == 0 ? 0x6400u : SH == 2 ? 0x5C00u : SH == 4 ? 0x5400u : 0x4C00u) * 0x00010001u;
-  return hsub2_u((__byte_perm(x, y, sel) & mask) | magic, magic);
+  return unbias(and_or<mask>(__byte_perm(x, y, sel), magic), magic);
 }
+
 // fp32 pair -> fp16x2 hi parts and the fp16x2 of the remainders (x = hi + lo to 22 significant bits)
 __device__ __forceinline__ void h2_split(float x0, float x1, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(x0, x1);
@@ -298,8 +320,13 @@ __device__ __forceinline__ void pv_page(const uint8_t* vseg, int t0, int cnt, co
   }
 }
 
-template <int D, int G>
-__global__ void __launch_bounds__(kTcThreads)
+// One unit per thread-block cluster of NC CTAs (split-sequence attention: "splits the sequence into
+// multiple segments, processes them in parallel ... then merges the results"): CTA `rank` takes the stored pages
+// holding tokens [rank, rank + 1) * (n_h + n_l) / NC (cut at page starts), the last CTA also the window.  The
+// softmax max and sum, the output and the section minima are merged through distributed shared memory.  TS =
+// the logit capacity of one CTA.
+template <int D, int G, int NC>
+__global__ void __launch_bounds__(kTcThreads, DKV_TC_MINB)
 attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs, int TS) {
   constexpr int GP = G <= 4 ? 4 : 8;                             // logit row: GP floats per token
   constexpr int NG = D / 16;                                      // 16-feature groups (QK k-steps, PV m-tiles)
@@ -307,14 +334,16 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   using LO = TcCls<D, 32, 4, 2>;                                  // K4V2, 32-token pages
   extern __shared__ __align__(16) uint8_t tc_smem[];
   __shared__ float s_q[G][D];
-  __shared__ float s_qsum[G], s_m[G], s_iz[G];
+  __shared__ float s_qsum[G], s_m[G], s_iz[G], s_mloc[G], s_zloc[G];
   __shared__ float s_red[kTcWarps][G];
   __shared__ unsigned long long s_min[2];
   __shared__ int s_slot[2];
   __shared__ __align__(8) uint64_t s_bar[kTcWarps][kTcStages];   // per-warp stage mbarriers (bulk copies)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = lane >> 2, tig = lane & 3;
-  const int u = blockIdx.x;
+  const int u = blockIdx.x / NC;
+  const int rank = NC > 1 ? (int)cg::this_cluster().block_rank() : 0;
+  // every CTA of the cluster takes the same early exits (no cluster barrier is left waiting)
   if (ld_volatile(&p.ctrl->status) != 0) return;                  // sticky error: no-op
   const int r = fdiv(p.div_LyH, u);
   if (p.req_state[r] != DKV_REQ_ACTIVE) return;
@@ -325,6 +354,16 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   const int T = nh + nl + nw;
   const int ph = ceil_div(nh, HI::C), pl = ceil_div(nl, LO::C);
   const int npg = ph + pl;
+  // this CTA's pages [kb0, kb1) and tokens [tb0, tb1) (global order: high slots, low slots), window if last
+  const int Ts = nh + nl;
+  auto page_of_tok = [&](int t) { return t < nh ? t / HI::C : (t < Ts ? ph + (t - nh) / LO::C : npg); };
+  auto page_t0 = [&](int k) { return k < ph ? k * HI::C : (k < npg ? nh + (k - ph) * LO::C : Ts); };
+  const int kb0 = rank == 0 ? 0 : page_of_tok((int)((int64_t)Ts * rank / NC));
+  const int kb1 = rank == NC - 1 ? npg : page_of_tok((int)((int64_t)Ts * (rank + 1) / NC));
+  const int tb0 = page_t0(kb0);
+  const int nst = page_t0(kb1) - tb0;                             // this CTA's stored tokens
+  const int nwl = rank == NC - 1 ? nw : 0;                        // its window tokens
+  const int TL = nst + nwl;                                       // its logits (local index = global - tb0)
   const ClassGeom gh = p.g[1], gl = p.g[2];                       // segment offsets inside a page
   float* lg = reinterpret_cast<float*>(tc_smem);                   // [TS][GP]
   int32_t* pid = reinterpret_cast<int32_t*>(tc_smem + (size_t)TS * GP * 4);
@@ -359,7 +398,8 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   __syncthreads();
 
   auto page_ptr = [&](int k) { return p.pages + (size_t)pid[k] * (size_t)p.page_bytes; };
-  const int my_n = npg > warp ? (npg - warp + kTcWarps - 1) / kTcWarps : 0;   // this warp's pages
+  const int npl = kb1 - kb0;
+  const int my_n = npl > warp ? (npl - warp + kTcWarps - 1) / kTcWarps : 0;   // this warp's pages
 
   // ---- phase 1: logits.  Stored pages: each warp its pages (k = warp + i * kTcWarps), K codes (swizzled) + K
   // meta staged kTcStages - 1 pages ahead
@@ -386,18 +426,18 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   {
 #pragma unroll
     for (int i = 0; i < kTcStages - 1; i++)
-      if (i < my_n) stage_k(warp + i * kTcWarps, i);
+      if (i < my_n) stage_k(kb0 + warp + i * kTcWarps, i);
     for (int i = 0; i < my_n; i++) {
-      const int k = warp + i * kTcWarps, slot = i % kTcStages;
-      if (i + kTcStages - 1 < my_n) stage_k(warp + (i + kTcStages - 1) * kTcWarps, (i + kTcStages - 1) % kTcStages);
+      const int k = kb0 + warp + i * kTcWarps, slot = i % kTcStages;
+      if (i + kTcStages - 1 < my_n) stage_k(kb0 + warp + (i + kTcStages - 1) * kTcWarps, (i + kTcStages - 1) % kTcStages);
       stage_wait(slot);
       const uint8_t* kseg = mystage + slot * kTcStage;
       if (k < ph) {
         const int t0 = k * HI::C;
-        qk_page<D, G, GP, HI>(kseg, t0, min(HI::C, nh - t0), qb, s_qsum, scale, lg, mx, grp, tig);
+        qk_page<D, G, GP, HI>(kseg, t0 - tb0, min(HI::C, nh - t0), qb, s_qsum, scale, lg, mx, grp, tig);
       } else {
         const int t0 = nh + (k - ph) * LO::C;
-        qk_page<D, G, GP, LO>(kseg, t0, min(LO::C, nh + nl - t0), qb, s_qsum, scale, lg, mx, grp, tig);
+        qk_page<D, G, GP, LO>(kseg, t0 - tb0, min(LO::C, nh + nl - t0), qb, s_qsum, scale, lg, mx, grp, tig);
       }
       fence_proxy_async_smem();                                   // this stage's reads before its next bulk fill
       __syncwarp();
@@ -409,7 +449,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   const uint16_t* wkg = reinterpret_cast<const uint16_t*>(p.win_k) + (size_t)u * W * D;
   const uint16_t* wvg = reinterpret_cast<const uint16_t*>(p.win_v) + (size_t)u * W * D;
   uint16_t* wks = reinterpret_cast<uint16_t*>(stage0);            // [nw][D] fp16, oldest first
-  for (int c = tid; c < nw * (D / 8); c += kTcThreads) {
+  for (int c = tid; c < nwl * (D / 8); c += kTcThreads) {
     const int i = c / (D / 8), e = c % (D / 8);
     cp_async16(wks + (size_t)i * D + 8 * e, wkg + (size_t)fmod_(p.div_W, N - nw + i) * D + 8 * e, true);
   }
@@ -419,7 +459,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   float wmx[G];
 #pragma unroll
   for (int h = 0; h < G; h++) wmx[h] = -INFINITY;
-  for (int x = tid; x < nw * G; x += kTcThreads) {
+  for (int x = tid; x < nwl * G; x += kTcThreads) {
     const int i = x / G, h = x % G;
     const __half2* kr = reinterpret_cast<const __half2*>(wks + (size_t)i * D);
     float acc0 = 0.0f, acc1 = 0.0f;
@@ -430,7 +470,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
       acc1 = fmaf(s_q[h][2 * e + 1], kv.y, acc1);
     }
     const float l = (acc0 + acc1) * scale;
-    lg[(size_t)(nh + nl + i) * GP + h] = l;
+    lg[(size_t)(nst + i) * GP + h] = l;
 #pragma unroll
     for (int hh = 0; hh < G; hh++)
       if (hh == h) wmx[hh] = fmaxf(wmx[hh], l);
@@ -457,13 +497,20 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     if (tid < G) {
       float v = -INFINITY;
       for (int w = 0; w < kTcWarps; w++) v = fmaxf(v, s_red[w][tid]);
+      s_mloc[tid] = v;
+    }
+    if constexpr (NC > 1) cg::this_cluster().sync(); else __syncthreads();
+    if (tid < G) {                                                // the unit's max over the cluster's CTAs
+      float v = s_mloc[tid];
+      if constexpr (NC > 1)
+        for (int rr = 0; rr < NC; rr++) v = fmaxf(v, *cg::this_cluster().map_shared_rank(&s_mloc[tid], rr));
       s_m[tid] = v;
     }
     __syncthreads();
     float m[G], zs[G];
 #pragma unroll
     for (int h = 0; h < G; h++) { m[h] = s_m[h]; zs[h] = 0.0f; }
-    for (int i = tid; i < T; i += kTcThreads) {
+    for (int i = tid; i < TL; i += kTcThreads) {
       float* row = lg + (size_t)i * GP;
 #pragma unroll
       for (int h = 0; h < G; h++) {
@@ -483,6 +530,16 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     if (tid < G) {
       float v = 0.0f;
       for (int w = 0; w < kTcWarps; w++) v += s_red[w][tid];
+      s_zloc[tid] = v;
+    }
+    if constexpr (NC > 1) cg::this_cluster().sync(); else __syncthreads();
+    if (tid < G) {                                                // Z = the sum over the cluster's CTAs
+      float v = 0.0f;
+      if constexpr (NC > 1) {
+        for (int rr = 0; rr < NC; rr++) v += *cg::this_cluster().map_shared_rank(&s_zloc[tid], rr);
+      } else {
+        v = s_zloc[tid];
+      }
       s_iz[tid] = 1.0f / v;
     }
     __syncthreads();
@@ -516,10 +573,10 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   {
 #pragma unroll
     for (int i = 0; i < kTcStages - 1; i++)
-      if (i < my_n) stage_v(warp + i * kTcWarps, i);
+      if (i < my_n) stage_v(kb0 + warp + i * kTcWarps, i);
     for (int i = 0; i < my_n; i++) {
-      const int k = warp + i * kTcWarps, slot = i % kTcStages;
-      if (i + kTcStages - 1 < my_n) stage_v(warp + (i + kTcStages - 1) * kTcWarps, (i + kTcStages - 1) % kTcStages);
+      const int k = kb0 + warp + i * kTcWarps, slot = i % kTcStages;
+      if (i + kTcStages - 1 < my_n) stage_v(kb0 + warp + (i + kTcStages - 1) * kTcWarps, (i + kTcStages - 1) % kTcStages);
       stage_wait(slot);
       const uint8_t* vseg = mystage + slot * kTcStage;
       const bool hi = k < ph;
@@ -527,15 +584,15 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
       const int t0 = hi ? k * HI::C : nh + (k - ph) * LO::C;
       const int cnt = min(C, (hi ? nh : nh + nl) - t0);
       const int vrow = hi ? HI::v_row : LO::v_row;
-      if (hi) pv_page<D, G, GP, HI>(vseg, t0, cnt, lg, iz, acc, zsum, grp, tig);
-      else pv_page<D, G, GP, LO>(vseg, t0, cnt, lg, iz, acc, zsum, grp, tig);
+      if (hi) pv_page<D, G, GP, HI>(vseg, t0 - tb0, cnt, lg, iz, acc, zsum, grp, tig);
+      else pv_page<D, G, GP, LO>(vseg, t0 - tb0, cnt, lg, iz, acc, zsum, grp, tig);
       // significance (Q33) of the page's tokens: a lane per token
       const float* ssc = reinterpret_cast<const float*>(vseg + C * vrow + 4 * C);
       const int32_t* spos = reinterpret_cast<const int32_t*>(vseg + C * vrow + 8 * C);
       float* gsc = reinterpret_cast<float*>(page_ptr(k) + (hi ? gh.off_score : gl.off_score));
       for (int j = lane; j < cnt; j += 32) {
-        const int i2 = t0 + j;
-        const float* row = lg + (size_t)i2 * GP;
+        const int i2 = t0 + j;                                    // global token index (Q31 order)
+        const float* row = lg + (size_t)(i2 - tb0) * GP;
         float a = 0.0f;
 #pragma unroll
         for (int h = 0; h < G; h++) a = fmaxf(a, row[h] * izr[h]);
@@ -560,15 +617,15 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   float* part = reinterpret_cast<float*>(stage0);                 // [kTcWarps][G][D] MMA partials
   float* zred = part + kTcWarps * G * D;                          // [kTcWarps][G]
   uint16_t* wvs = reinterpret_cast<uint16_t*>(zred + ((kTcWarps * G + 3) & ~3));   // [nw][D] window values
-  for (int c = tid; c < nw * (D / 8); c += kTcThreads) {
+  for (int c = tid; c < nwl * (D / 8); c += kTcThreads) {
     const int i = c / (D / 8), e = c % (D / 8);
     cp_async16(wvs + (size_t)i * D + 8 * e, wvg + (size_t)fmod_(p.div_W, N - nw + i) * D + 8 * e, true);
   }
   cp_async_commit();
   // window: significance on CUDA cores
-  for (int i = tid; i < nw; i += kTcThreads) {
+  for (int i = tid; i < nwl; i += kTcThreads) {
     const int pos = N - nw + i;
-    const float* row = lg + (size_t)(nh + nl + i) * GP;
+    const float* row = lg + (size_t)(nst + i) * GP;
     float a = 0.0f;
 #pragma unroll
     for (int h = 0; h < G; h++) a = fmaxf(a, row[h] * izr[h]);
@@ -594,6 +651,8 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   }
   cp_async_wait<0>();
   __syncthreads();
+  // [G][D] this CTA's output partial, after the window values
+  float* cpart = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(wvs) + (size_t)W * D * 2);
   if (out != nullptr) {
     for (int e = tid; e < G * D / 2; e += kTcThreads) {            // a feature pair per thread
       const int h = e / (D / 2), f = 2 * (e % (D / 2));
@@ -604,13 +663,13 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
       }
       float w0 = 0.0f, w1 = 0.0f;                                  // the window's values (FP16) on CUDA cores
       const float izh = izr[h];
-      for (int i = 0; i < nw; i++) {
-        const float a = lg[(size_t)(nh + nl + i) * GP + h] * izh;
+      for (int i = 0; i < nwl; i++) {
+        const float a = lg[(size_t)(nst + i) * GP + h] * izh;
         const float2 vv = __half22float2(*reinterpret_cast<const __half2*>(wvs + (size_t)i * D + f));
         w0 = fmaf(a, vv.x, w0);
         w1 = fmaf(a, vv.y, w1);
       }
-      *reinterpret_cast<float2*>(out + ((size_t)u * G + h) * D + f) = make_float2(o0 + z + w0, o1 + z + w1);
+      *reinterpret_cast<float2*>(cpart + (size_t)h * D + f) = make_float2(o0 + z + w0, o1 + z + w1);
     }
   }
   // section minima (stored sections only; keys are unique: positions differ)
@@ -621,17 +680,37 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
 #pragma unroll
   for (int c = 0; c < 2; c++)
     if (mkey[c] != ~0ull && mkey[c] == s_min[c]) s_slot[c] = mslot[c];
-  __syncthreads();
-  if (tid == 0) {
-    int32_t* m = p.secmin + 8 * (size_t)u;
-#pragma unroll
-    for (int c = 0; c < 2; c++) {
-      m[3 * c] = (int32_t)(uint32_t)(s_min[c] >> 32);
-      m[3 * c + 1] = (int32_t)(uint32_t)(s_min[c] & 0xFFFFFFFFull);
-      m[3 * c + 2] = s_slot[c];
+  // merge over the cluster: CTA 0 reads every CTA's output partial and minima (distributed shared memory)
+  if constexpr (NC > 1) cg::this_cluster().sync(); else __syncthreads();
+  if (rank == 0) {
+    if (out != nullptr) {
+      for (int e = tid; e < G * D; e += kTcThreads) {
+        float o = cpart[e];
+        if constexpr (NC > 1)
+          for (int rr = 1; rr < NC; rr++) o += *cg::this_cluster().map_shared_rank(cpart + e, rr);
+        out[(size_t)u * G * D + e] = o;
+      }
     }
-    m[6] = 1;
+    if (tid == 0) {
+      unsigned long long key[2] = {s_min[0], s_min[1]};
+      int slot[2] = {s_slot[0], s_slot[1]};
+      if constexpr (NC > 1)
+        for (int rr = 1; rr < NC; rr++)
+          for (int c = 0; c < 2; c++) {
+            const unsigned long long kr = *cg::this_cluster().map_shared_rank(&s_min[c], rr);
+            if (kr < key[c]) { key[c] = kr; slot[c] = *cg::this_cluster().map_shared_rank(&s_slot[c], rr); }
+          }
+      int32_t* m = p.secmin + 8 * (size_t)u;
+#pragma unroll
+      for (int c = 0; c < 2; c++) {
+        m[3 * c] = (int32_t)(uint32_t)(key[c] >> 32);
+        m[3 * c + 1] = (int32_t)(uint32_t)(key[c] & 0xFFFFFFFFull);
+        m[3 * c + 2] = slot[c];
+      }
+      m[6] = 1;
+    }
   }
+  if constexpr (NC > 1) cg::this_cluster().sync();                // CTA 0's remote reads precede the others' exit
 }
 
 // the kernel is specialised for the paper's classes: K8V4 in 16-token pages, K4V2 in 32-token pages;
@@ -642,22 +721,40 @@ bool attend_tc_supported(const PoolDev& p) {
          p.G <= 8 && (p.d == 64 || p.d == 128);
 }
 
+constexpr int kTcNC = DKV_TC_CLUSTER;
+
+// logit capacity of one CTA of the cluster: its stored tokens (at most 1/NC of the unit's, plus a partial page) and
+// the window (the last CTA)
+static int tc_local_tokens(const PoolDev& p, int TS) { return ((TS + kTcNC - 1) / kTcNC + 32 + p.W + 31) & ~31; }
+
 size_t attend_tc_smem_bytes(const PoolDev& p, int TS) {
   const int GP = p.G <= 4 ? 4 : 8;
-  // phase 3's reduction area: warp partials, z sums, the staged window values (phase 1 stages the window keys)
+  const int TL = tc_local_tokens(p, TS);
+  // phase 3's reduction area: warp partials, z sums, the staged window values, the CTA's output partial
   const size_t red = (size_t)kTcWarps * p.G * p.d * 4 + (size_t)((kTcWarps * p.G + 3) & ~3) * 4 +
-                     (size_t)p.W * p.d * 2;
+                     (size_t)p.W * p.d * 2 + (size_t)p.G * p.d * 4;
   const size_t stage = (size_t)kTcWarps * kTcStages * kTcStage;
-  return (size_t)TS * GP * 4 + (size_t)((p.L + 4) & ~3) * 4 + (stage > red ? stage : red);
+  return (size_t)TL * GP * 4 + (size_t)((p.L + 4) & ~3) * 4 + (stage > red ? stage : red);
 }
 
 template <int D, int G>
 static cudaError_t launch_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s) {
   const size_t smem = attend_tc_smem_bytes(p, TS);
-  cudaError_t e = cudaFuncSetAttribute(attend_tc_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(attend_tc_kernel<D, G, kTcNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  attend_tc_kernel<D, G><<<p.U, kTcThreads, smem, s>>>(p, q, out, probs, TS);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)p.U * kTcNC);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;              // one unit per cluster of kTcNC CTAs
+  attr[0].val.clusterDim.x = kTcNC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = kTcNC > 1 ? 1 : 0;                              // NC = 1: a plain launch
+  return cudaLaunchKernelEx(&cfg, attend_tc_kernel<D, G, kTcNC>, p, q, out, probs, tc_local_tokens(p, TS));
 }
 
 template <int D>

@@ -24,6 +24,9 @@ namespace dkv {
 #ifndef DKV_CD_MINB
 #define DKV_CD_MINB 10     // 10 CTAs (40 warps) per SM: 48 registers, a few spilled
 #endif
+#ifndef DKV_CD_PREFETCH
+#define DKV_CD_PREFETCH 0  // L2 prefetch of what dkv_quant_write(DECODE) reads: t_c's window rows, the victim's record
+#endif
 #ifndef DKV_CD_KCV
 #define DKV_CD_KCV 8
 #endif
@@ -44,7 +47,8 @@ constexpr int kXV = 4;                     // the same for the exact (tie-breaki
 #define CD_LD ld_nc_v4
 #endif
 
-template <int MINB>
+// TOP: the pool has the NEXT-4 FP16 tier (compiled out otherwise: its branches cost registers at the 10-CTA budget)
+template <int MINB, bool TOP>
 __global__ void __launch_bounds__(kCDWarps * 32, MINB)
 classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decision_t* __restrict__ dec) {
   extern __shared__ int32_t s_pid_all[];                         // [kCDWarps][L] page IDs of the scanned sections
@@ -53,7 +57,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   if (u >= p.U) return;                                          // whole warps exit together
   pdl_wait();                                                    // (PDL) the previous quant_write's writes
   pdl_trigger();
-  const int LP = p.L > p.Lt ? p.L : p.Lt;                        // page IDs a scanned section can have
+  const int LP = TOP && p.Lt > p.L ? p.Lt : p.L;                 // page IDs a scanned section can have
   int32_t* s_pid = s_pid_all + warp * LP;
 #if DKV_CD_SPEC
   // One round trip for everything u alone addresses: the sticky status (read through L1 — 16k warps reading
@@ -94,9 +98,17 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
     const float s_in = cand_sig ? cand_sig[u]
                                 : (p.W > 0 && N - 1 - p.W >= 0 ? p.win_sig[(size_t)u * p.W + (N - 1 - p.W) % p.W] : 0.0f);
     const int nh_in = p.n_h[u], nl_in = p.n_l[u];
-    const int nt_in = p.top ? p.n_t[u] : 0;
+    const int nt_in = TOP ? p.n_t[u] : 0;
     const int pc = N - 1 - p.W;                                  // t_c = earliest window token
     if (st == DKV_REQ_ACTIVE && pc >= 0) {
+#if DKV_CD_PREFETCH
+      // warm L2 with t_c's window rows (slot p_c mod W), which the following dkv_quant_write reads first
+      const int lines = (p.d * 2 + 127) >> 7;
+      if (p.W > 0 && lane < 2 * lines) {
+        const __half* wrow = (lane < lines ? p.win_k : p.win_v) + ((size_t)u * p.W + (N - 1) % p.W) * p.d;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint8_t*>(wrow) + 128 * (lane % lines)));
+      }
+#endif
       if (!finite_f(s_in) || s_in < 0.0f) {
         if (lane == 0) set_pending(p.ctrl, DKV_ERR_NONFINITE);   // Q36: merged by compact_alloc
       } else {
@@ -104,7 +116,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
         th = __fdiv_rn(unit_alpha_h(p, u), (float)N);            // alpha_h / N (per head: Q35)
         tl = __fdiv_rn(unit_alpha_l(p, u), (float)N);            // alpha_l / N
         cls = sc >= th ? DKV_CLS_HIGH : (sc >= tl ? DKV_CLS_LOW : DKV_CLS_PRUNED);
-        if (p.top) {                                             // NEXT-4 (Q38): the FP16 tier above High
+        if (TOP) {                                               // NEXT-4 (Q38): the FP16 tier above High
           tt = __fdiv_rn(p.alpha_t, (float)N);
           if (sc >= tt) cls = DKV_CLS_TOP;
         }
@@ -112,7 +124,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
         if (cls != DKV_CLS_PRUNED) {
           nh = nh_in;
           nl = nl_in;
-          n = cls == DKV_CLS_TOP ? nt_in : ((cls == DKV_CLS_HIGH) ? nh : nl);
+          n = (TOP && cls == DKV_CLS_TOP) ? nt_in : ((cls == DKV_CLS_HIGH) ? nh : nl);
           scan = true;
         }
       }
@@ -138,15 +150,15 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   } else if
 #endif
   (scan && n > 0) {                                    // warp-uniform
-    const int C = cls == DKV_CLS_TOP ? p.gt.C : (cls == DKV_CLS_HIGH ? p.g[1].C : p.g[2].C);
-    const int off_score = cls == DKV_CLS_TOP ? p.gt.off_score : (cls == DKV_CLS_HIGH ? p.g[1].off_score : p.g[2].off_score);
+    const int C = (TOP && cls == DKV_CLS_TOP) ? p.gt.C : (cls == DKV_CLS_HIGH ? p.g[1].C : p.g[2].C);
+    const int off_score = (TOP && cls == DKV_CLS_TOP) ? p.gt.off_score : (cls == DKV_CLS_HIGH ? p.g[1].off_score : p.g[2].off_score);
     const bool pow2 = (C & (C - 1)) == 0;
     const int csh = __popc(C - 1);
     const int npages = (n + C - 1) / C;
 #if DKV_CD_SPEC
     for (int k = lane; k < npages; k += 32) {
       int32_t pid;
-      if (cls == DKV_CLS_TOP) pid = __ldg(p.ttable + (size_t)u * p.Lt + k);   // NEXT-4 (Q41)
+      if (TOP && cls == DKV_CLS_TOP) pid = __ldg(p.ttable + (size_t)u * p.Lt + k);   // NEXT-4 (Q41)
       else if (cls == DKV_CLS_HIGH) pid = k < 32 ? sp_h0 : (k < 64 ? sp_h1 : __ldg(row + k));
       else pid = k < 32 ? sp_l0 : __ldg(row + p.L - 1 - k);
       s_pid[k] = pid;
@@ -154,7 +166,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
 #else
     const int32_t* row = p.table + (size_t)u * p.L;
     for (int k = lane; k < npages; k += 32)
-      s_pid[k] = cls == DKV_CLS_TOP ? __ldg(p.ttable + (size_t)u * p.Lt + k) : __ldg(row + (cls == DKV_CLS_HIGH ? k : p.L - 1 - k));
+      s_pid[k] = (TOP && cls == DKV_CLS_TOP) ? __ldg(p.ttable + (size_t)u * p.Lt + k) : __ldg(row + (cls == DKV_CLS_HIGH ? k : p.L - 1 - k));
 #endif
     __syncwarp();
     const uint8_t* base_sc = p.pages + off_score;
@@ -206,7 +218,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
       // in flight per lane, then one 16-B position vector (the same 4 slots' positions, contiguous in the
       // page) for every score vector holding m — a section whose minimum is shared by hundreds of slots
       // (exact zeros when nothing is pruned) costs two round trips per batch, not one per tied slot
-      const int off_pos = cls == DKV_CLS_TOP ? p.gt.off_pos : (cls == DKV_CLS_HIGH ? p.g[1].off_pos : p.g[2].off_pos);
+      const int off_pos = (TOP && cls == DKV_CLS_TOP) ? p.gt.off_pos : (cls == DKV_CLS_HIGH ? p.g[1].off_pos : p.g[2].off_pos);
       int32_t bp = 0x7FFFFFFF;
       int bs = -1;
       for (int base = 0; base < n; base += 128 * kXV) {
@@ -243,7 +255,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
     // t_c has the largest position, so a stored token wins every score tie with it
     if (vs >= 0 && !(vb <= __float_as_uint(sc))) vs = -1;
     const float sv = __uint_as_float(vb);
-    if (cls == DKV_CLS_TOP) {                                    // NEXT-4 (Q39): Algorithm 1 one level up
+    if (TOP && cls == DKV_CLS_TOP) {                                      // NEXT-4 (Q39): Algorithm 1 one level up
       if (vs < 0 || sv >= tt) {                                  // t_v stays in KV_t
         v_action = DKV_V_KEEP; grow = DKV_GROW_TOP; demand = (n % p.Ct == 0); tc_slot = n;
       } else if (sv >= th) {                                     // t_v moves to KV_h
@@ -281,7 +293,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   // downgraded victim moves to.  A page the growing section receives this step is not known yet: -1 here,
   // written by dkv_compact_alloc when it grants it.  The scanned section's IDs are in shared memory already.
   if (scan) {
-    const bool hi = cls == DKV_CLS_HIGH, top = cls == DKV_CLS_TOP;
+    const bool hi = cls == DKV_CLS_HIGH, top = TOP && cls == DKV_CLS_TOP;
     const int C = top ? p.Ct : (hi ? p.Ch : p.Cl);
     const int32_t* trow = p.table + (size_t)u * p.L;
     const bool have = n > 0 && !fused;                          // s_pid holds the section's pages
@@ -293,6 +305,21 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
     if (v_action == DKV_V_DOWN && !demand)                      // the destination section's tail page
       pb = grow == DKV_GROW_HIGH ? __ldg(trow + nh / p.Ch) : __ldg(trow + p.L - 1 - nl / p.Cl);
     p.qpid[u] = make_int2(pa, pb);
+#if DKV_CD_PREFETCH
+    if (v_action == DKV_V_DOWN) {                                // warm L2 with the victim's record (read by quant_write)
+      const ClassGeom g = top ? p.gt : p.g[1];
+      const uint8_t* pg = p.pages + (size_t)pa * (size_t)p.page_bytes;
+      const int is = vs - (vs / C) * C;
+      for (int o = 0; o < g.k_row; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(pg + g.off_k + is * g.k_row + o));
+      for (int o = 0; o < g.v_row; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(pg + g.off_v + is * g.v_row + o));
+      if (!top) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(pg + g.off_kmeta + 4 * is));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(pg + g.off_vmeta + 4 * is));
+      }
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pg + g.off_score + 4 * is));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pg + g.off_pos + 4 * is));
+    }
+#endif
   }
 }
 
@@ -300,15 +327,20 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
 #define DKV_CD_LONG_LEN 12288   // longest active request above which the full-register instantiation runs
 #endif
 
-template <int MINB>
-static cudaError_t launch_cd(const PoolDev& p, const float* sig, dkv_decision_t* dec, cudaStream_t s) {
-  const size_t smem = 4 * (size_t)(p.L > p.Lt ? p.L : p.Lt) * kCDWarps;
+template <int MINB, bool TOP>
+static cudaError_t launch_cd_t(const PoolDev& p, const float* sig, dkv_decision_t* dec, cudaStream_t s) {
+  const size_t smem = 4 * (size_t)(TOP && p.Lt > p.L ? p.Lt : p.L) * kCDWarps;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(classify_decode_kernel<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(classify_decode_kernel<MINB, TOP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  return launch_ex(classify_decode_kernel<MINB>, dim3((p.U + kCDWarps - 1) / kCDWarps), dim3(kCDWarps * 32), smem, s,
+  return launch_ex(classify_decode_kernel<MINB, TOP>, dim3((p.U + kCDWarps - 1) / kCDWarps), dim3(kCDWarps * 32), smem, s,
                    p.pdl != 0, p, sig, dec);
+}
+
+template <int MINB>
+static cudaError_t launch_cd(const PoolDev& p, const float* sig, dkv_decision_t* dec, cudaStream_t s) {
+  return p.top ? launch_cd_t<MINB, true>(p, sig, dec, s) : launch_cd_t<MINB, false>(p, sig, dec, s);
 }
 
 // max_len: the longest ACTIVE request (host mirror).  Long sections run the instantiation with the full

@@ -30,7 +30,10 @@ q = torch.randn((wl.U, c["G"], c["d"]), device=dev).to(torch.float16)
 out = torch.empty((wl.U, c["G"], c["d"]), dtype=torch.float32, device=dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 res = {}
-for name, fn in (("exact", pool.attend), ("tc", pool.attend_tc)):
+impls = (("exact", pool.attend), ("tc", pool.attend_tc))
+if os.environ.get("ONLY"):                                     # e.g. ONLY=tc under ncu
+    impls = tuple(x for x in impls if x[0] == os.environ["ONLY"])
+for name, fn in impls:
     ts = []
     for i in range(6):
         flush.zero_()

@@ -55,8 +55,9 @@ SHAPES = {
                             P=7 << 20, alpha_h=1.0, alpha_l=0.0, mix=(0.25, 0.75, 0.0), seed=4, G=8, steps=12,
                             churn_every=4, group=16),
     # NEXT-4 three-level tier FP16-K8V4-K4V2 (readings Q38-Q44) on configs[1]'s shape; no attention (Q44)
+    # (about 42 % of the stored prompt tokens reach alpha_t / n here, at 4 tokens per page: 12 Mi pages)
     "llama3_8b_top_tier": dict(R=64, Ly=32, H=8, world=1, d=128, prompt=4096, M=8192, W=64, Ch=16, Cl=32,
-                               P=1 << 22, alpha_h=1.0, alpha_l=0.02, mix=(0.35, 0.45, 0.20), seed=2, G=4, steps=12,
+                               P=12 << 20, alpha_h=1.0, alpha_l=0.02, mix=(0.35, 0.45, 0.20), seed=2, G=4, steps=12,
                                churn_every=4, group=64, top_tier=1, alpha_t=2.0, Ct=4),
     "frag_shard8": dict(R=128, Ly=32, H=8, world=8, d=128, prompt=(256, 4096), M=4608, W=64, Ch=16, Cl=32,
                         P=2_900_000, alpha_h=1.0, alpha_l=0.02, mix=(0.35, 0.45, 0.20), seed=5, G=4, steps=400,
@@ -155,7 +156,8 @@ def run(name):
     admit_s = time.time() - t0
 
     # ---- decode steps (significance from the synthetic input), then NEXT-2 steps (from the attention)
-    res = {k_: [] for k_ in ("classify", "compact_alloc", "quant_write", "attend", "classify_fused", "occ")}
+    res = {k_: [] for k_ in ("classify", "compact_alloc", "quant_write", "attend", "attend_tc", "classify_fused",
+                             "occ")}
     freed = admitted = 0
     qbuf = torch.empty((wl.U, c["G"], c["d"]), dtype=torch.float16, device=dev)
     obuf = torch.empty((wl.U, c["G"], c["d"]), dtype=torch.float32, device=dev)
@@ -163,6 +165,7 @@ def run(name):
     gen.manual_seed(c["seed"])
     for s in range(c["steps"]):
         next2 = s >= c["steps"] // 2 and not c.get("top_tier")     # Q44: no attention with the FP16 tier
+        tc_ok = c["Ch"] == 16 and c["Cl"] == 32                  # attend_tc's specialisation (K8V4 x16, K4V2 x32)
         if s % c["churn_every"] == c["churn_every"] - 1:
             live = np.nonzero(active)[0]
             if len(live):
@@ -173,6 +176,16 @@ def run(name):
         cand, nk, nv = wl.decode_inputs(seq, active)
         if next2:
             qbuf.normal_(generator=gen)
+        if next2 and tc_ok:                                      # the tensor-core attention on the same state,
+            flush.zero_()                                         # before the exact one (whose minima drive the step)
+            torch.cuda.synchronize()
+            t0e, t1e = ev(), ev()
+            torch.cuda._sleep(200_000)
+            t0e.record()
+            pool.attend_tc(qbuf.view(torch.int16), obuf)
+            t1e.record()
+            torch.cuda.synchronize()
+            res["attend_tc"].append(t0e.elapsed_time(t1e) * 1e3)
         flush.zero_()
         torch.cuda.synchronize()
         e = [ev() for _ in range(5)]
@@ -208,7 +221,8 @@ def run(name):
     v = pool.views()
     ctrl = v["ctrl"].cpu().numpy()
     start, free = int(ctrl[0]), int(ctrl[1])
-    ids = torch.cat([v["ring"][(start + torch.arange(free, device=dev)) % c["P"]], v["table"][v["table"] >= 0]])
+    ids = torch.cat([v["ring"][(start + torch.arange(free, device=dev)) % c["P"]], v["table"][v["table"] >= 0],
+                     v["ttable"][v["ttable"] >= 0]])
     assert ids.numel() == c["P"] and torch.equal(ids.sort().values, torch.arange(c["P"], device=dev, dtype=ids.dtype))
 
     def m(k_):
@@ -226,6 +240,7 @@ def run(name):
                           "quant_write": m("quant_write"), "classify_fused": m("classify_fused"),
                           "compact_alloc_p99": round(float(np.percentile(res["compact_alloc"], 99)), 2)},
             "attend_ms": round(m("attend") / 1e3, 3) if res["attend"] else None,
+            "attend_tc_ms": round(m("attend_tc") / 1e3, 3) if res["attend_tc"] else None,
             "steps": c["steps"], "frees": freed, "admissions_during_decode": admitted,
             "occupancy": {"min": round(min(res["occ"]), 3), "max": round(max(res["occ"]), 3)},
             "mean_context": int(seq[active].mean()) if active.any() else 0, "admit_s": round(admit_s, 1),
