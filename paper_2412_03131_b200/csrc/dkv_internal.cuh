@@ -104,6 +104,8 @@ struct PoolDev {
   float* head_alpha;    // [LyH][2] per-head (alpha_h, alpha_l) (NEXT-4)
   float* att_scratch;   // [att_slots][GP + 2][M] long-context attention scratch (NEXT-2), or null
   int32_t att_slots;
+  float* tc_scratch;    // [tc_slots][tc_slot_rows][GP] logits of the persistent tensor-core attention CTAs, or null
+  int32_t tc_slots, tc_slot_rows;
   int32_t use_head_alpha;   // 1: head_alpha replaces alpha_h / alpha_l
   int32_t prefill_wf;   // dkv_config_t.prefill_workflow
   int2* qpid;           // [U] {t_c's page, downgraded victim's KV_l page} for dkv_quant_write(DECODE)
@@ -1005,8 +1007,8 @@ cudaError_t launch_recycle(const PoolDev& p, const int32_t* req, int n, cudaStre
 cudaError_t launch_attend(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s);
 size_t attend_smem_bytes(const PoolDev& p, int TS);
 size_t attend_long_smem_bytes(const PoolDev& p);
-cudaError_t launch_attend_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s);
-size_t attend_tc_smem_bytes(const PoolDev& p, int TS);
+cudaError_t launch_attend_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s);
+size_t attend_tc_smem_bytes(const PoolDev& p);
 bool attend_tc_supported(const PoolDev& p);
 cudaError_t launch_prefill_conservative(const PoolDev& p, cudaStream_t s);
 // units [u0, u1) (u1 < 0: all U)

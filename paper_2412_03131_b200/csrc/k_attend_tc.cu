@@ -25,24 +25,28 @@
 //   phase 3: PV by MMA page by page with a = p / Z, the significance of each stored token (page score
 //            segments) and window token, the section minima; the warps' partial outputs are added in a fixed
 //            order (deterministic for a given launch).
-#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 
 #include "dkv_internal.cuh"
 
 namespace dkv {
 
-namespace cg = cooperative_groups;
-#ifndef DKV_TC_CLUSTER
-#define DKV_TC_CLUSTER 1        // CTAs (a thread-block cluster) sharing one unit's pages: split-sequence attention
-#endif
 #ifndef DKV_TC_MINB
-#define DKV_TC_MINB 2           // CTAs per SM the register budget is sized for
+#define DKV_TC_MINB 3           // CTAs per SM the register budget is sized for
 #endif
 constexpr int kTcWarps = 8;
 constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTcStages = 2;                   // pages in flight per warp (cp.async groups)
-constexpr int kTcStage = 2304;                 // bytes per warp per stage: >= C*k_row + 4C and C*v_row + 12C
+// bytes per warp per stage: >= C*k_row + 4C (K codes + meta) and C*v_row + 12C + C*GP*4 (V codes, meta, scores,
+// positions, the page's probability rows), for both classes at d <= 128
+constexpr int tc_stage_bytes(int GP) { return GP == 4 ? 2176 : 2432; }
+// the stage area, reused by phase 3's reduction (warp partials, z sums, the staged window values; phase 1 stages the
+// window keys there too), rounded to 16 B
+__host__ __device__ constexpr int tc_area_bytes(int D, int G, int W, int GP) {
+  return ((kTcWarps * kTcStages * tc_stage_bytes(GP) > kTcWarps * G * D * 4 + ((kTcWarps * G + 3) & ~3) * 4 + W * D * 2
+               ? kTcWarps * kTcStages * tc_stage_bytes(GP)
+               : kTcWarps * G * D * 4 + ((kTcWarps * G + 3) & ~3) * 4 + W * D * 2) + 15) & ~15;
+}
 
 __device__ __forceinline__ void mma_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -103,10 +107,17 @@ __device__ __forceinline__ uint32_t and_or(uint32_t x, uint32_t magic) {
 // operand is the constant -M removing the bias after each group — 10 % fewer instructions but slower (3.82 vs
 // 3.72 ms: dependent MMA pairs on one accumulator) and outside the Eq. 1 output tolerance (8e-5: the accumulator
 // transiently holds M * sum at the tensor core's accumulation precision).
+// Centred codes: the subtrahend is M + 2^(bits-1), not M, so the operand is the code minus half its range (exact
+// in fp16) and the offset moves into z (z' = z + 2^(bits-1) s, tc_zc).  The code term and the z term of the output
+// (and of the logit) then no longer nearly cancel — with raw codes both are ~|mean V| and their difference is the
+// output, so the tensor core's fp32 accumulation error over a long context (one rounding per MMA, ~thousands per
+// accumulator at 30k tokens) was amplified into the output.
 __device__ __forceinline__ uint32_t unbias(uint32_t x, uint32_t m) { return hsub2_u(x, m); }
+template <int BITS>
+__device__ __forceinline__ float tc_zc(float zf, float sf) { return fmaf(sf, (float)(1 << (BITS - 1)), zf); }
 __device__ __forceinline__ void k8_pairs(uint32_t x, uint32_t& lo, uint32_t& hi) {
-  lo = unbias(__byte_perm(x, 0x64646464u, 0x4140), 0x64006400u);
-  hi = unbias(__byte_perm(x, 0x64646464u, 0x4342), 0x64006400u);
+  lo = unbias(__byte_perm(x, 0x64646464u, 0x4140), 0x64806480u);   // (1024 + c) - 1152 = c - 128
+  hi = unbias(__byte_perm(x, 0x64646464u, 0x4342), 0x64806480u);
 }
 // K4: the two bytes at byte index KB0 (codes n0 | n1 << 4) and KB0 + 1 (n2 | n3 << 4) of x -> fp16x2 (n0, n1),
 // (n2, n3): n0 in bits 0-3 with 0x6400 (1024, ulp 1), n1 in bits 20-23 = bits 4-7 of the high half with 0x5400
@@ -114,8 +125,8 @@ __device__ __forceinline__ void k8_pairs(uint32_t x, uint32_t& lo, uint32_t& hi)
 template <int KB0>
 __device__ __forceinline__ void k4_pairs(uint32_t x, uint32_t& lo, uint32_t& hi) {
   constexpr uint32_t s0 = KB0 * 0x1111u, s1 = (KB0 + 1) * 0x1111u;
-  lo = unbias(and_or<0x00F0000Fu>(__byte_perm(x, 0u, s0), 0x54006400u), 0x54006400u);
-  hi = unbias(and_or<0x00F0000Fu>(__byte_perm(x, 0u, s1), 0x54006400u), 0x54006400u);
+  lo = unbias(and_or<0x00F0000Fu>(__byte_perm(x, 0u, s0), 0x54006400u), 0x54806408u);   // c - 8 in both halves
+  hi = unbias(and_or<0x00F0000Fu>(__byte_perm(x, 0u, s1), 0x54006400u), 0x54806408u);
 }
 // V: byte K of x (token j0) and of y (token j1) -> fp16x2 (field of j0, field of j1) for the field at bits
 // [SH, SH + VB) of that byte; the magic makes bit SH weigh 1 (fp16, 10 mantissa bits: a value in [2^e, 2^(e+1))
@@ -126,7 +137,8 @@ __device__ __forceinline__ uint32_t v_pair(uint32_t x, uint32_t y) {
   constexpr uint32_t sel = K | (K << 4) | ((4 + K) << 8) | ((4 + K) << 12);
   constexpr uint32_t mask = (((1u << VB) - 1u) << SH) * 0x00010001u;
   constexpr uint32_t magic = (SH == 0 ? 0x6400u : SH == 2 ? 0x5C00u : SH == 4 ? 0x5400u : 0x4C00u) * 0x00010001u;
-  return unbias(and_or<mask>(__byte_perm(x, y, sel), magic), magic);
+  constexpr uint32_t centre = magic + ((1u << (VB - 1)) << SH) * 0x00010001u;   // M + 2^(VB-1): code - half range
+  return unbias(and_or<mask>(__byte_perm(x, y, sel), magic), centre);
 }
 
 // fp32 pair -> fp16x2 hi parts and the fp16x2 of the remainders (x = hi + lo to 22 significant bits)
@@ -137,8 +149,9 @@ __device__ __forceinline__ void h2_split(float x0, float x1, uint32_t& hi, uint3
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
-// PV's B operand a * s_v is scaled by 2^kPvShift before its fp16 split (a <= 1 and |s_v| < 2^4 keep it below the
-// fp16 maximum; the scale keeps small products out of the subnormal range); the accumulators are scaled back once
+// PV's B operand p * s_v (p = exp(l - max) <= 1, unnormalised, so that long contexts' small probabilities do not
+// sink into fp16 subnormals; 1/Z is applied to the partials) is scaled by 2^12 before its fp16 split (|s_v| < 2^4
+// keeps it below the fp16 maximum); the accumulators are scaled back once
 constexpr float kPvScale = 4096.0f, kPvUnscale = 1.0f / 4096.0f;
 
 // Compile-time geometry of one precision class (the paper's K8V4 high / K4V2 low pages): tokens per
@@ -234,7 +247,7 @@ __device__ __forceinline__ void qk_page(const uint8_t* kseg, int t0, int cnt, co
       if (j < cnt) {
         const uint32_t km = kmeta[j];
         const float sf = __half2float(__ushort_as_half((unsigned short)(km & 0xFFFFu)));
-        const float zf = __half2float(__ushort_as_half((unsigned short)(km >> 16)));
+        const float zf = tc_zc<CL::kbits>(__half2float(__ushort_as_half((unsigned short)(km >> 16))), sf);
 #pragma unroll
         for (int c = 0; c < 2; c++) {
           const int h = 2 * tig + c;
@@ -253,7 +266,7 @@ __device__ __forceinline__ void qk_page(const uint8_t* kseg, int t0, int cnt, co
 // is feature FPV*grp + 2g and row grp + 8 is FPV*grp + 2g + 1 (FPV = D/8), so a lane's value codes for all
 // m-tiles are one contiguous run of each value row; k = tokens 4 tig .. 4 tig + 3; n = head.
 template <int D, int G, int GP, class CL>
-__device__ __forceinline__ void pv_page(const uint8_t* vseg, int t0, int cnt, const float* lg, float iz,
+__device__ __forceinline__ void pv_page(const uint8_t* vseg, int t0, int cnt, const float* lg,
                                         float (&acc)[D / 16][4], float& zsum, int grp, int tig) {
   constexpr int FPV = D / 8, RB = FPV * CL::vbits / 8;           // features / bytes per lane per value row
   constexpr int NW = (RB + 3) / 4;
@@ -269,8 +282,8 @@ __device__ __forceinline__ void pv_page(const uint8_t* vseg, int t0, int cnt, co
       if (j < cnt && grp < G) {
         const uint32_t vm = vmeta[j];
         const float sf = __half2float(__ushort_as_half((unsigned short)(vm & 0xFFFFu)));
-        const float zf = __half2float(__ushort_as_half((unsigned short)(vm >> 16)));
-        const float a = lg[(size_t)(t0 + j) * GP + grp] * iz;
+        const float zf = tc_zc<CL::vbits>(__half2float(__ushort_as_half((unsigned short)(vm >> 16))), sf);
+        const float a = lg[(size_t)(t0 + j) * GP + grp];         // unnormalised p = exp(l - max) <= 1
         b = a * sf * kPvScale;
         zsum = fmaf(a, zf, zsum);
       }
@@ -320,397 +333,373 @@ __device__ __forceinline__ void pv_page(const uint8_t* vseg, int t0, int cnt, co
   }
 }
 
-// One unit per thread-block cluster of NC CTAs (split-sequence attention: "splits the sequence into
-// multiple segments, processes them in parallel ... then merges the results"): CTA `rank` takes the stored pages
-// holding tokens [rank, rank + 1) * (n_h + n_l) / NC (cut at page starts), the last CTA also the window.  The
-// softmax max and sum, the output and the section minima are merged through distributed shared memory.  TS =
-// the logit capacity of one CTA.
-template <int D, int G, int NC>
+// Persistent: gridDim.x CTAs (the occupancy limit, at most kTcSlots) take units blockIdx.x, + gridDim.x, ...  A
+// CTA's logits live in its own global scratch slot (p.tc_scratch: [tc_slot_rows][GP] fp32; the slots of the
+// resident CTAs, ~70 MB at configs[1], stay in L2), so shared memory holds only the page stages and the per-unit
+// reduction area and three CTAs fit per SM (logits in shared memory allowed two).  Phase 3 stages each page's
+// probability rows together with its value segments (bulk copies).
+template <int D, int G>
 __global__ void __launch_bounds__(kTcThreads, DKV_TC_MINB)
-attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs, int TS) {
+attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs) {
   constexpr int GP = G <= 4 ? 4 : 8;                             // logit row: GP floats per token
   constexpr int NG = D / 16;                                      // 16-feature groups (QK k-steps, PV m-tiles)
+  constexpr int STG = tc_stage_bytes(GP);                         // bytes per warp per stage
   using HI = TcCls<D, 16, 8, 4>;                                  // K8V4, 16-token pages
   using LO = TcCls<D, 32, 4, 2>;                                  // K4V2, 32-token pages
   extern __shared__ __align__(16) uint8_t tc_smem[];
   __shared__ float s_q[G][D];
-  __shared__ float s_qsum[G], s_m[G], s_iz[G], s_mloc[G], s_zloc[G];
+  __shared__ float s_qsum[G], s_m[G], s_iz[G];
   __shared__ float s_red[kTcWarps][G];
   __shared__ unsigned long long s_min[2];
   __shared__ int s_slot[2];
   __shared__ __align__(8) uint64_t s_bar[kTcWarps][kTcStages];   // per-warp stage mbarriers (bulk copies)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = lane >> 2, tig = lane & 3;
-  const int u = blockIdx.x / NC;
-  const int rank = NC > 1 ? (int)cg::this_cluster().block_rank() : 0;
-  // every CTA of the cluster takes the same early exits (no cluster barrier is left waiting)
   if (ld_volatile(&p.ctrl->status) != 0) return;                  // sticky error: no-op
-  const int r = fdiv(p.div_LyH, u);
-  if (p.req_state[r] != DKV_REQ_ACTIVE) return;
   const int L = p.L, W = p.W;
-  const int N = p.seq_len[r];
-  const int nh = p.n_h[u], nl = p.n_l[u];
-  const int nw = min(W, N);
-  const int T = nh + nl + nw;
-  const int ph = ceil_div(nh, HI::C), pl = ceil_div(nl, LO::C);
-  const int npg = ph + pl;
-  // this CTA's pages [kb0, kb1) and tokens [tb0, tb1) (global order: high slots, low slots), window if last
-  const int Ts = nh + nl;
-  auto page_of_tok = [&](int t) { return t < nh ? t / HI::C : (t < Ts ? ph + (t - nh) / LO::C : npg); };
-  auto page_t0 = [&](int k) { return k < ph ? k * HI::C : (k < npg ? nh + (k - ph) * LO::C : Ts); };
-  const int kb0 = rank == 0 ? 0 : page_of_tok((int)((int64_t)Ts * rank / NC));
-  const int kb1 = rank == NC - 1 ? npg : page_of_tok((int)((int64_t)Ts * (rank + 1) / NC));
-  const int tb0 = page_t0(kb0);
-  const int nst = page_t0(kb1) - tb0;                             // this CTA's stored tokens
-  const int nwl = rank == NC - 1 ? nw : 0;                        // its window tokens
-  const int TL = nst + nwl;                                       // its logits (local index = global - tb0)
   const ClassGeom gh = p.g[1], gl = p.g[2];                       // segment offsets inside a page
-  float* lg = reinterpret_cast<float*>(tc_smem);                   // [TS][GP]
-  int32_t* pid = reinterpret_cast<int32_t*>(tc_smem + (size_t)TS * GP * 4);
-  uint8_t* stage0 = tc_smem + (size_t)TS * GP * 4 + (size_t)((L + 4) & ~3) * 4;
-  uint8_t* mystage = stage0 + (size_t)warp * kTcStages * kTcStage;
-  const int32_t* trow = p.table + (size_t)u * L;
-  for (int k = tid; k < npg; k += kTcThreads) pid[k] = k < ph ? trow[k] : trow[L - 1 - (k - ph)];
-  for (int k = tid; k < G * D; k += kTcThreads)
-    s_q[k / D][k % D] = __half2float(__ushort_as_half(q[(size_t)u * G * D + k]));
-  if (tid < 2) { s_min[tid] = ~0ull; s_slot[tid] = -1; }
+  float* const lg = p.tc_scratch + (size_t)blockIdx.x * p.tc_slot_rows * GP;   // this CTA's logits [rows][GP]
+  // dynamic shared memory: the stage / reduction area first (a compile-time base), then the page IDs and the
+  // window's probability rows
+  uint8_t* stage0 = tc_smem;
+  int32_t* pid = reinterpret_cast<int32_t*>(tc_smem + tc_area_bytes(D, G, W, GP));
+  float* wprob = reinterpret_cast<float*>(pid + ((L + 4) & ~3));     // [W][GP] window probabilities (phase 3)
+  uint8_t* mystage = stage0 + (size_t)warp * kTcStages * STG;
+  uint64_t* bars = s_bar[warp];
   if (tid < kTcWarps * kTcStages) mbar_init(&s_bar[tid / kTcStages][tid % kTcStages], 1);
   fence_mbar_init();
-  __syncthreads();
-  if (tid < G) {
-    float sacc = 0.0f;
-    for (int f = 0; f < D; f++) sacc += s_q[tid][f];
-    s_qsum[tid] = sacc;
-  }
-  const float scale = rsqrtf((float)D);
-  // B fragments of the queries (k = features, permuted as in qk_page; n = head = grp): group g, b0 = features
-  // (D/4) tig + 4g + {0, 1}, b1 = + {2, 3} of head grp
-  uint32_t qb[NG][2];
-#pragma unroll
-  for (int g = 0; g < NG; g++) {
-    uint32_t w0 = 0, w1 = 0;
-    if (grp < G) {
-      const uint2 v = *reinterpret_cast<const uint2*>(q + ((size_t)u * G + grp) * D + (D / 4) * tig + 4 * g);
-      w0 = v.x; w1 = v.y;
-    }
-    qb[g][0] = w0; qb[g][1] = w1;
-  }
-  __syncthreads();
-
-  auto page_ptr = [&](int k) { return p.pages + (size_t)pid[k] * (size_t)p.page_bytes; };
-  const int npl = kb1 - kb0;
-  const int my_n = npl > warp ? (npl - warp + kTcWarps - 1) / kTcWarps : 0;   // this warp's pages
-
-  // ---- phase 1: logits.  Stored pages: each warp its pages (k = warp + i * kTcWarps), K codes (swizzled) + K
-  // meta staged kTcStages - 1 pages ahead
-  float mx[2] = {-INFINITY, -INFINITY};                           // heads 2 tig, 2 tig + 1
-  // a page's segments land in the warp's stage by 1-D bulk copies (TMA, cp.async.bulk) issued by lane 0, the
-  // stage's mbarrier counting the bytes; rows keep the global (token-major) layout
-  uint64_t* bars = s_bar[warp];
   uint32_t phase = 0;                                             // bit s: parity of stage s's next completion
-  auto stage_k = [&](int k, int slot) {
-    if (lane != 0) return;
-    const uint8_t* pg = page_ptr(k);
-    uint8_t* dst = mystage + slot * kTcStage;
-    const bool hi = k < ph;
-    const int C = hi ? HI::C : LO::C, krow = hi ? HI::k_row : LO::k_row;
-    const int off_k = hi ? gh.off_k : gl.off_k, off_km = hi ? gh.off_kmeta : gl.off_kmeta;
-    mbar_arrive_expect_tx(&bars[slot], (uint32_t)(C * krow + 4 * C));
-    bulk_g2s(dst, pg + off_k, (uint32_t)(C * krow), &bars[slot]);
-    bulk_g2s(dst + C * krow, pg + off_km, (uint32_t)(4 * C), &bars[slot]);
-  };
-  auto stage_wait = [&](int slot) {
-    mbar_wait(&bars[slot], (phase >> slot) & 1u);
-    phase ^= 1u << slot;
-  };
-  {
-#pragma unroll
-    for (int i = 0; i < kTcStages - 1; i++)
-      if (i < my_n) stage_k(kb0 + warp + i * kTcWarps, i);
-    for (int i = 0; i < my_n; i++) {
-      const int k = kb0 + warp + i * kTcWarps, slot = i % kTcStages;
-      if (i + kTcStages - 1 < my_n) stage_k(kb0 + warp + (i + kTcStages - 1) * kTcWarps, (i + kTcStages - 1) % kTcStages);
-      stage_wait(slot);
-      const uint8_t* kseg = mystage + slot * kTcStage;
-      if (k < ph) {
-        const int t0 = k * HI::C;
-        qk_page<D, G, GP, HI>(kseg, t0 - tb0, min(HI::C, nh - t0), qb, s_qsum, scale, lg, mx, grp, tig);
-      } else {
-        const int t0 = nh + (k - ph) * LO::C;
-        qk_page<D, G, GP, LO>(kseg, t0 - tb0, min(LO::C, nh + nl - t0), qb, s_qsum, scale, lg, mx, grp, tig);
-      }
-      fence_proxy_async_smem();                                   // this stage's reads before its next bulk fill
-      __syncwarp();
-    }
-  }
-  // window tokens (FP16 keys): rows staged into shared memory (the page stages are free now), then one
-  // (token, head) dot product per thread on CUDA cores
-  __syncthreads();
-  const uint16_t* wkg = reinterpret_cast<const uint16_t*>(p.win_k) + (size_t)u * W * D;
-  const uint16_t* wvg = reinterpret_cast<const uint16_t*>(p.win_v) + (size_t)u * W * D;
-  uint16_t* wks = reinterpret_cast<uint16_t*>(stage0);            // [nw][D] fp16, oldest first
-  for (int c = tid; c < nwl * (D / 8); c += kTcThreads) {
-    const int i = c / (D / 8), e = c % (D / 8);
-    cp_async16(wks + (size_t)i * D + 8 * e, wkg + (size_t)fmod_(p.div_W, N - nw + i) * D + 8 * e, true);
-  }
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  float wmx[G];
-#pragma unroll
-  for (int h = 0; h < G; h++) wmx[h] = -INFINITY;
-  for (int x = tid; x < nwl * G; x += kTcThreads) {
-    const int i = x / G, h = x % G;
-    const __half2* kr = reinterpret_cast<const __half2*>(wks + (size_t)i * D);
-    float acc0 = 0.0f, acc1 = 0.0f;
-#pragma unroll 8
-    for (int e = 0; e < D / 2; e++) {
-      const float2 kv = __half22float2(kr[e]);
-      acc0 = fmaf(s_q[h][2 * e], kv.x, acc0);
-      acc1 = fmaf(s_q[h][2 * e + 1], kv.y, acc1);
-    }
-    const float l = (acc0 + acc1) * scale;
-    lg[(size_t)(nst + i) * GP + h] = l;
-#pragma unroll
-    for (int hh = 0; hh < G; hh++)
-      if (hh == h) wmx[hh] = fmaxf(wmx[hh], l);
-  }
-  // ---- phase 2: per-head max, p = exp(l - max), Z
-  fence_proxy_async_smem();                                       // the window rows' reads before phase 3's bulk fills
-  {
-#pragma unroll
-    for (int c = 0; c < 2; c++) {
-      float v = mx[c];                                            // reduce over the 8 lanes of this tig
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
-      mx[c] = v;
-    }
-#pragma unroll
-    for (int h = 0; h < G; h++) {
-      // head h's MMA maximum is held by the lanes with tig == h / 2
-      float v = fmaxf(wmx[h], __shfl_sync(kFull, mx[h & 1], (h >> 1) & 3));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
-      if (lane == 0) s_red[warp][h] = v;
-    }
+  const uint32_t bar_s = smem_u32(bars), stage_s = smem_u32(mystage);
+  const float scale = rsqrtf((float)D);
+  const uint16_t* const wk_all = reinterpret_cast<const uint16_t*>(p.win_k);
+  const uint16_t* const wv_all = reinterpret_cast<const uint16_t*>(p.win_v);
+
+  for (int u = blockIdx.x; u < p.U; u += gridDim.x) {
+    const int r = fdiv(p.div_LyH, u);
+    if (p.req_state[r] != DKV_REQ_ACTIVE) continue;               // CTA-uniform
+    const int N = p.seq_len[r];
+    const int nh = p.n_h[u], nl = p.n_l[u];
+    const int nw = min(W, N);
+    const int Ts = nh + nl, T = Ts + nw;                          // logit rows: stored tokens, then the window
+    const int ph = ceil_div(nh, HI::C), pl = ceil_div(nl, LO::C);
+    const int npg = ph + pl;
+    const int32_t* trow = p.table + (size_t)u * L;
+    __syncthreads();                                              // the previous unit's readers are done
+    for (int k = tid; k < npg; k += kTcThreads) pid[k] = k < ph ? trow[k] : trow[L - 1 - (k - ph)];
+    for (int k = tid; k < G * D; k += kTcThreads)
+      s_q[k / D][k % D] = __half2float(__ushort_as_half(q[(size_t)u * G * D + k]));
+    if (tid < 2) { s_min[tid] = ~0ull; s_slot[tid] = -1; }
     __syncthreads();
     if (tid < G) {
-      float v = -INFINITY;
-      for (int w = 0; w < kTcWarps; w++) v = fmaxf(v, s_red[w][tid]);
-      s_mloc[tid] = v;
+      float sacc = 0.0f;
+      for (int f = 0; f < D; f++) sacc += s_q[tid][f];
+      s_qsum[tid] = sacc;
     }
-    if constexpr (NC > 1) cg::this_cluster().sync(); else __syncthreads();
-    if (tid < G) {                                                // the unit's max over the cluster's CTAs
-      float v = s_mloc[tid];
-      if constexpr (NC > 1)
-        for (int rr = 0; rr < NC; rr++) v = fmaxf(v, *cg::this_cluster().map_shared_rank(&s_mloc[tid], rr));
-      s_m[tid] = v;
+    // B fragments of the queries (k = features, permuted as in qk_page; n = head = grp): group g, b0 = features
+    // (D/4) tig + 4g + {0, 1}, b1 = + {2, 3} of head grp
+    uint32_t qb[NG][2];
+#pragma unroll
+    for (int g = 0; g < NG; g++) {
+      uint32_t w0 = 0, w1 = 0;
+      if (grp < G) {
+        const uint2 v = *reinterpret_cast<const uint2*>(q + ((size_t)u * G + grp) * D + (D / 4) * tig + 4 * g);
+        w0 = v.x; w1 = v.y;
+      }
+      qb[g][0] = w0; qb[g][1] = w1;
     }
     __syncthreads();
-    float m[G], zs[G];
+
+    auto page_ptr = [&](int k) { return p.pages + (size_t)pid[k] * (size_t)p.page_bytes; };
+    const int my_n = npg > warp ? (npg - warp + kTcWarps - 1) / kTcWarps : 0;   // this warp's pages
+
+    // ---- phase 1: logits.  Stored pages: each warp its pages (k = warp + i * kTcWarps), K codes + K meta staged
+    // kTcStages - 1 pages ahead by bulk copies (lanes 0 and 1: codes, meta, one warp instruction)
+    float mx[2] = {-INFINITY, -INFINITY};                         // heads 2 tig, 2 tig + 1
+    auto stage_k = [&](int k, int slot) {
+      if (lane >= 2) return;
+      const bool hi = k < ph;
+      const int C = hi ? HI::C : LO::C, krow = hi ? HI::k_row : LO::k_row;
+      const uint32_t bar = bar_s + 8 * slot;
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((uint32_t)(C * krow + 4 * C))
+                     : "memory");
+      const int off = lane == 0 ? (hi ? gh.off_k : gl.off_k) : (hi ? gh.off_kmeta : gl.off_kmeta);
+      const uint32_t dst = stage_s + slot * STG + (lane == 0 ? 0 : C * krow);
+      const uint32_t bytes = lane == 0 ? C * krow : 4 * C;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dst), "l"(page_ptr(k) + off), "r"(bytes), "r"(bar) : "memory");
+    };
+    auto stage_wait = [&](int slot) {
+      mbar_wait(&bars[slot], (phase >> slot) & 1u);
+      phase ^= 1u << slot;
+    };
+    {
 #pragma unroll
-    for (int h = 0; h < G; h++) { m[h] = s_m[h]; zs[h] = 0.0f; }
-    for (int i = tid; i < TL; i += kTcThreads) {
-      float* row = lg + (size_t)i * GP;
+      for (int i = 0; i < kTcStages - 1; i++)
+        if (i < my_n) stage_k(warp + i * kTcWarps, i);
+      for (int i = 0; i < my_n; i++) {
+        const int k = warp + i * kTcWarps, slot = i % kTcStages;
+        if (i + kTcStages - 1 < my_n) stage_k(warp + (i + kTcStages - 1) * kTcWarps, (i + kTcStages - 1) % kTcStages);
+        stage_wait(slot);
+        const uint8_t* kseg = mystage + slot * STG;
+        if (k < ph) {
+          const int t0 = k * HI::C;
+          qk_page<D, G, GP, HI>(kseg, t0, min(HI::C, nh - t0), qb, s_qsum, scale, lg, mx, grp, tig);
+        } else {
+          const int t0 = nh + (k - ph) * LO::C;
+          qk_page<D, G, GP, LO>(kseg, t0, min(LO::C, Ts - t0), qb, s_qsum, scale, lg, mx, grp, tig);
+        }
+        fence_proxy_async_smem();                                 // this stage's reads before its next bulk fill
+        __syncwarp();
+      }
+    }
+    // window tokens (FP16 keys): rows staged into shared memory (the page stages are free now), then one
+    // (token, head) dot product per thread on CUDA cores
+    __syncthreads();
+    const uint16_t* wkg = wk_all + (size_t)u * W * D;
+    const uint16_t* wvg = wv_all + (size_t)u * W * D;
+    uint16_t* wks = reinterpret_cast<uint16_t*>(stage0);          // [nw][D] fp16, oldest first
+    for (int c = tid; c < nw * (D / 8); c += kTcThreads) {
+      const int i = c / (D / 8), e = c % (D / 8);
+      cp_async16(wks + (size_t)i * D + 8 * e, wkg + (size_t)fmod_(p.div_W, N - nw + i) * D + 8 * e, true);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    float wmx[G];
+#pragma unroll
+    for (int h = 0; h < G; h++) wmx[h] = -INFINITY;
+    for (int x = tid; x < nw * G; x += kTcThreads) {
+      const int i = x / G, h = x % G;
+      const __half2* kr = reinterpret_cast<const __half2*>(wks + (size_t)i * D);
+      float acc0 = 0.0f, acc1 = 0.0f;
+#pragma unroll 8
+      for (int e = 0; e < D / 2; e++) {
+        const float2 kv = __half22float2(kr[e]);
+        acc0 = fmaf(s_q[h][2 * e], kv.x, acc0);
+        acc1 = fmaf(s_q[h][2 * e + 1], kv.y, acc1);
+      }
+      const float l = (acc0 + acc1) * scale;
+      lg[(size_t)(Ts + i) * GP + h] = l;
+#pragma unroll
+      for (int hh = 0; hh < G; hh++)
+        if (hh == h) wmx[hh] = fmaxf(wmx[hh], l);
+    }
+    // ---- phase 2: per-head max, p = exp(l - max), Z (thread per logit row of the CTA's global slot)
+    fence_proxy_async_smem();                                     // the window rows' reads before phase 3's bulk fills
+    {
+#pragma unroll
+      for (int c = 0; c < 2; c++) {
+        float v = mx[c];                                          // reduce over the 8 lanes of this tig
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+        mx[c] = v;
+      }
 #pragma unroll
       for (int h = 0; h < G; h++) {
-        const float e = __expf(row[h] - m[h]);
-        row[h] = e;
-        zs[h] += e;
+        // head h's MMA maximum is held by the lanes with tig == h / 2
+        float v = fmaxf(wmx[h], __shfl_sync(kFull, mx[h & 1], (h >> 1) & 3));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+        if (lane == 0) s_red[warp][h] = v;
       }
-    }
-#pragma unroll
-    for (int h = 0; h < G; h++) {
-      float v = zs[h];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-      if (lane == 0) s_red[warp][h] = v;
-    }
-    __syncthreads();
-    if (tid < G) {
-      float v = 0.0f;
-      for (int w = 0; w < kTcWarps; w++) v += s_red[w][tid];
-      s_zloc[tid] = v;
-    }
-    if constexpr (NC > 1) cg::this_cluster().sync(); else __syncthreads();
-    if (tid < G) {                                                // Z = the sum over the cluster's CTAs
-      float v = 0.0f;
-      if constexpr (NC > 1) {
-        for (int rr = 0; rr < NC; rr++) v += *cg::this_cluster().map_shared_rank(&s_zloc[tid], rr);
-      } else {
-        v = s_zloc[tid];
+      __syncthreads();                                            // also: every logit row is written
+      if (tid < G) {
+        float v = -INFINITY;
+        for (int w = 0; w < kTcWarps; w++) v = fmaxf(v, s_red[w][tid]);
+        s_m[tid] = v;
       }
-      s_iz[tid] = 1.0f / v;
-    }
-    __syncthreads();
-  }
-  // ---- phase 3: PV by MMA (A = value codes^T: m = features f0 = 16g + 2 grp, f0 + 1; k = tokens 4 tig .. +3;
-  // B = 2^12 a * s_v split fp16 hi / lo: k = tokens, n = head grp), significance + minima, page by page
-  float acc[NG][4];
+      __syncthreads();
+      float m[G], zs[G];
 #pragma unroll
-  for (int g = 0; g < NG; g++) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.0f;
-  float zsum = 0.0f;                                              // sum_t a_t z_t of head grp (this lane's tokens)
-  unsigned long long mkey[2] = {~0ull, ~0ull};
-  int mslot[2] = {-1, -1};
-  float izr[G];
+      for (int h = 0; h < G; h++) { m[h] = s_m[h]; zs[h] = 0.0f; }
+      for (int i = tid; i < T; i += kTcThreads) {
+        float4* row = reinterpret_cast<float4*>(lg + (size_t)i * GP);
 #pragma unroll
-  for (int h = 0; h < G; h++) izr[h] = s_iz[h];
-  auto stage_v = [&](int k, int slot) {
-    if (lane != 0) return;
-    const uint8_t* pg = page_ptr(k);
-    uint8_t* dst = mystage + slot * kTcStage;
-    const bool hi = k < ph;
-    const ClassGeom& gg = hi ? gh : gl;
-    const int C = hi ? HI::C : LO::C, vrow = hi ? HI::v_row : LO::v_row;
-    mbar_arrive_expect_tx(&bars[slot], (uint32_t)(C * vrow + 12 * C));
-    bulk_g2s(dst, pg + gg.off_v, (uint32_t)(C * vrow), &bars[slot]);
-    uint8_t* d2 = dst + C * vrow;                                  // V meta, scores, positions
-    bulk_g2s(d2, pg + gg.off_vmeta, (uint32_t)(4 * C), &bars[slot]);
-    bulk_g2s(d2 + 4 * C, pg + gg.off_score, (uint32_t)(4 * C), &bars[slot]);
-    bulk_g2s(d2 + 8 * C, pg + gg.off_pos, (uint32_t)(4 * C), &bars[slot]);
-  };
-  const float iz = grp < G ? s_iz[grp] : 0.0f;
-  {
+        for (int c4 = 0; c4 < GP / 4; c4++) {
+          float4 v = row[c4];
+          float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int i = 0; i < kTcStages - 1; i++)
-      if (i < my_n) stage_v(kb0 + warp + i * kTcWarps, i);
-    for (int i = 0; i < my_n; i++) {
-      const int k = kb0 + warp + i * kTcWarps, slot = i % kTcStages;
-      if (i + kTcStages - 1 < my_n) stage_v(kb0 + warp + (i + kTcStages - 1) * kTcWarps, (i + kTcStages - 1) % kTcStages);
-      stage_wait(slot);
-      const uint8_t* vseg = mystage + slot * kTcStage;
-      const bool hi = k < ph;
-      const int C = hi ? HI::C : LO::C;
-      const int t0 = hi ? k * HI::C : nh + (k - ph) * LO::C;
-      const int cnt = min(C, (hi ? nh : nh + nl) - t0);
-      const int vrow = hi ? HI::v_row : LO::v_row;
-      if (hi) pv_page<D, G, GP, HI>(vseg, t0 - tb0, cnt, lg, iz, acc, zsum, grp, tig);
-      else pv_page<D, G, GP, LO>(vseg, t0 - tb0, cnt, lg, iz, acc, zsum, grp, tig);
-      // significance (Q33) of the page's tokens: a lane per token
-      const float* ssc = reinterpret_cast<const float*>(vseg + C * vrow + 4 * C);
-      const int32_t* spos = reinterpret_cast<const int32_t*>(vseg + C * vrow + 8 * C);
-      float* gsc = reinterpret_cast<float*>(page_ptr(k) + (hi ? gh.off_score : gl.off_score));
-      for (int j = lane; j < cnt; j += 32) {
-        const int i2 = t0 + j;                                    // global token index (Q31 order)
-        const float* row = lg + (size_t)(i2 - tb0) * GP;
-        float a = 0.0f;
-#pragma unroll
-        for (int h = 0; h < G; h++) a = fmaxf(a, row[h] * izr[h]);
-        if (probs) probs[(size_t)u * p.M + i2] = a;
-        const int pos = spos[j];
-        float sg = ssc[j];
-        const int c = N - 2 - pos;
-        if (c >= 0) {
-          sg = (sg * (float)c + a) * __frcp_rn((float)(c + 1));
-          gsc[j] = sg;
-        }
-        const int cls = hi ? 0 : 1;
-        const int slotj = hi ? t0 + j : t0 - nh + j;
-        const unsigned long long key = ((unsigned long long)__float_as_uint(sg) << 32) | (uint32_t)pos;
-        if (key < mkey[cls]) { mkey[cls] = key; mslot[cls] = slotj; }
-      }
-      fence_proxy_async_smem();                                   // this stage's reads before its next bulk fill
-      __syncwarp();
-    }
-  }
-  __syncthreads();                                                // staging areas are free: reuse for the reduction
-  float* part = reinterpret_cast<float*>(stage0);                 // [kTcWarps][G][D] MMA partials
-  float* zred = part + kTcWarps * G * D;                          // [kTcWarps][G]
-  uint16_t* wvs = reinterpret_cast<uint16_t*>(zred + ((kTcWarps * G + 3) & ~3));   // [nw][D] window values
-  for (int c = tid; c < nwl * (D / 8); c += kTcThreads) {
-    const int i = c / (D / 8), e = c % (D / 8);
-    cp_async16(wvs + (size_t)i * D + 8 * e, wvg + (size_t)fmod_(p.div_W, N - nw + i) * D + 8 * e, true);
-  }
-  cp_async_commit();
-  // window: significance on CUDA cores
-  for (int i = tid; i < nwl; i += kTcThreads) {
-    const int pos = N - nw + i;
-    const float* row = lg + (size_t)(nst + i) * GP;
-    float a = 0.0f;
-#pragma unroll
-    for (int h = 0; h < G; h++) a = fmaxf(a, row[h] * izr[h]);
-    if (probs) probs[(size_t)u * p.M + nh + nl + i] = a;
-    const int c = N - 2 - pos;
-    float* sp = p.win_sig + (size_t)u * W + fmod_(p.div_W, pos);
-    if (c >= 0) *sp = (*sp * (float)c + a) * __frcp_rn((float)(c + 1));
-  }
-#pragma unroll
-  for (int gg = 0; gg < NG; gg++) {
-#pragma unroll
-    for (int c = 0; c < 4; c++) {
-      const int h = 2 * tig + (c & 1);
-      const int f = (D / 8) * grp + 2 * gg + (c >> 1);          // pv_page's feature mapping
-      if (h < G) part[((size_t)warp * G + h) * D + f] = acc[gg][c] * kPvUnscale;
-    }
-  }
-  {
-    float v = zsum;                                               // lanes of head grp: tig = 0..3
-    v += __shfl_xor_sync(kFull, v, 1);
-    v += __shfl_xor_sync(kFull, v, 2);
-    if (tig == 0 && grp < G) zred[warp * G + grp] = v;
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-  // [G][D] this CTA's output partial, after the window values
-  float* cpart = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(wvs) + (size_t)W * D * 2);
-  if (out != nullptr) {
-    for (int e = tid; e < G * D / 2; e += kTcThreads) {            // a feature pair per thread
-      const int h = e / (D / 2), f = 2 * (e % (D / 2));
-      float o0 = 0.0f, o1 = 0.0f, z = 0.0f;
-      for (int w = 0; w < kTcWarps; w++) {
-        const float2 pp = *reinterpret_cast<const float2*>(part + ((size_t)w * G + h) * D + f);
-        o0 += pp.x; o1 += pp.y; z += zred[w * G + h];
-      }
-      float w0 = 0.0f, w1 = 0.0f;                                  // the window's values (FP16) on CUDA cores
-      const float izh = izr[h];
-      for (int i = 0; i < nwl; i++) {
-        const float a = lg[(size_t)(nst + i) * GP + h] * izh;
-        const float2 vv = __half22float2(*reinterpret_cast<const __half2*>(wvs + (size_t)i * D + f));
-        w0 = fmaf(a, vv.x, w0);
-        w1 = fmaf(a, vv.y, w1);
-      }
-      *reinterpret_cast<float2*>(cpart + (size_t)h * D + f) = make_float2(o0 + z + w0, o1 + z + w1);
-    }
-  }
-  // section minima (stored sections only; keys are unique: positions differ)
-#pragma unroll
-  for (int c = 0; c < 2; c++)
-    if (mkey[c] != ~0ull) atomicMin(&s_min[c], mkey[c]);
-  __syncthreads();
-#pragma unroll
-  for (int c = 0; c < 2; c++)
-    if (mkey[c] != ~0ull && mkey[c] == s_min[c]) s_slot[c] = mslot[c];
-  // merge over the cluster: CTA 0 reads every CTA's output partial and minima (distributed shared memory)
-  if constexpr (NC > 1) cg::this_cluster().sync(); else __syncthreads();
-  if (rank == 0) {
-    if (out != nullptr) {
-      for (int e = tid; e < G * D; e += kTcThreads) {
-        float o = cpart[e];
-        if constexpr (NC > 1)
-          for (int rr = 1; rr < NC; rr++) o += *cg::this_cluster().map_shared_rank(cpart + e, rr);
-        out[(size_t)u * G * D + e] = o;
-      }
-    }
-    if (tid == 0) {
-      unsigned long long key[2] = {s_min[0], s_min[1]};
-      int slot[2] = {s_slot[0], s_slot[1]};
-      if constexpr (NC > 1)
-        for (int rr = 1; rr < NC; rr++)
-          for (int c = 0; c < 2; c++) {
-            const unsigned long long kr = *cg::this_cluster().map_shared_rank(&s_min[c], rr);
-            if (kr < key[c]) { key[c] = kr; slot[c] = *cg::this_cluster().map_shared_rank(&s_slot[c], rr); }
+          for (int j = 0; j < 4; j++) {
+            const int h = 4 * c4 + j;
+            if (h < G) { e[j] = __expf(e[j] - m[h]); zs[h] += e[j]; }
           }
+          row[c4] = make_float4(e[0], e[1], e[2], e[3]);
+        }
+      }
+      // the probability rows are read by phase 3's bulk copies (async proxy) after the barrier below
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+#pragma unroll
+      for (int h = 0; h < G; h++) {
+        float v = zs[h];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+        if (lane == 0) s_red[warp][h] = v;
+      }
+      __syncthreads();
+      if (tid < G) {
+        float v = 0.0f;
+        for (int w = 0; w < kTcWarps; w++) v += s_red[w][tid];
+        s_iz[tid] = 1.0f / v;
+      }
+      __syncthreads();
+    }
+    // ---- phase 3: PV by MMA (A = value codes^T: m = features f0 = 16g + 2 grp, f0 + 1; k = tokens 4 tig .. +3;
+    // B = 2^12 p * s_v split fp16 hi / lo, p = exp(l - max) unnormalised (1/Z applied to the partials): k = tokens,
+    // n = head grp), significance + minima, page by page
+    float acc[NG][4];
+#pragma unroll
+    for (int g = 0; g < NG; g++) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.0f;
+    float zsum = 0.0f;                                            // sum_t a_t z_t of head grp (this lane's tokens)
+    unsigned long long mkey[2] = {~0ull, ~0ull};
+    int mslot[2] = {-1, -1};
+    float izr[G];
+#pragma unroll
+    for (int h = 0; h < G; h++) izr[h] = s_iz[h];
+    // lanes 0-4 issue the five segment copies (V codes, V meta, scores, positions, the page's probability rows
+    // from the scratch slot) as one warp instruction
+    auto stage_v = [&](int k, int slot) {
+      if (lane >= 5) return;
+      const bool hi = k < ph;
+      const ClassGeom& gg = hi ? gh : gl;
+      const int C = hi ? HI::C : LO::C, vrow = hi ? HI::v_row : LO::v_row;
+      const int t0 = hi ? k * HI::C : nh + (k - ph) * LO::C;
+      const uint32_t bar = bar_s + 8 * slot;
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"((uint32_t)(C * vrow + 12 * C + C * GP * 4)) : "memory");
+      const uint8_t* src = lane == 4 ? reinterpret_cast<const uint8_t*>(lg + (size_t)t0 * GP)
+                                     : page_ptr(k) + (lane == 0 ? gg.off_v : (lane == 1 ? gg.off_vmeta
+                                                                  : (lane == 2 ? gg.off_score : gg.off_pos)));
+      const uint32_t dst = stage_s + slot * STG + (lane == 0 ? 0 : C * vrow + 4 * C * (lane - 1));
+      const uint32_t bytes = lane == 0 ? C * vrow : (lane == 4 ? C * GP * 4 : 4 * C);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+    };
+    {
+#pragma unroll
+      for (int i = 0; i < kTcStages - 1; i++)
+        if (i < my_n) stage_v(warp + i * kTcWarps, i);
+      for (int i = 0; i < my_n; i++) {
+        const int k = warp + i * kTcWarps, slot = i % kTcStages;
+        if (i + kTcStages - 1 < my_n) stage_v(warp + (i + kTcStages - 1) * kTcWarps, (i + kTcStages - 1) % kTcStages);
+        stage_wait(slot);
+        const uint8_t* vseg = mystage + slot * STG;
+        const bool hi = k < ph;
+        const int C = hi ? HI::C : LO::C;
+        const int t0 = hi ? k * HI::C : nh + (k - ph) * LO::C;
+        const int cnt = min(C, (hi ? nh : Ts) - t0);
+        const int vrow = hi ? HI::v_row : LO::v_row;
+        const float* prow = reinterpret_cast<const float*>(vseg + C * vrow + 12 * C);   // [C][GP] probabilities
+        if (hi) pv_page<D, G, GP, HI>(vseg, 0, cnt, prow, acc, zsum, grp, tig);
+        else pv_page<D, G, GP, LO>(vseg, 0, cnt, prow, acc, zsum, grp, tig);
+        // significance (Q33) of the page's tokens: a lane per token
+        const float* ssc = reinterpret_cast<const float*>(vseg + C * vrow + 4 * C);
+        const int32_t* spos = reinterpret_cast<const int32_t*>(vseg + C * vrow + 8 * C);
+        float* gsc = reinterpret_cast<float*>(page_ptr(k) + (hi ? gh.off_score : gl.off_score));
+        for (int j = lane; j < cnt; j += 32) {
+          const int i2 = t0 + j;                                  // token index (Q31 order)
+          const float* row = prow + (size_t)j * GP;
+          float a = 0.0f;
+#pragma unroll
+          for (int h = 0; h < G; h++) a = fmaxf(a, row[h] * izr[h]);
+          if (probs) probs[(size_t)u * p.M + i2] = a;
+          const int pos = spos[j];
+          float sg = ssc[j];
+          const int c = N - 2 - pos;
+          if (c >= 0) {
+            sg = (sg * (float)c + a) * __frcp_rn((float)(c + 1));
+            gsc[j] = sg;
+          }
+          const int cls = hi ? 0 : 1;
+          const int slotj = hi ? t0 + j : t0 - nh + j;
+          const unsigned long long key = ((unsigned long long)__float_as_uint(sg) << 32) | (uint32_t)pos;
+          if (key < mkey[cls]) { mkey[cls] = key; mslot[cls] = slotj; }
+        }
+        fence_proxy_async_smem();                                 // this stage's reads before its next bulk fill
+        __syncwarp();
+      }
+    }
+    __syncthreads();                                              // staging areas are free: reuse for the reduction
+    float* part = reinterpret_cast<float*>(stage0);               // [kTcWarps][G][D] MMA partials
+    float* zred = part + kTcWarps * G * D;                        // [kTcWarps][G]
+    uint16_t* wvs = reinterpret_cast<uint16_t*>(zred + ((kTcWarps * G + 3) & ~3));   // [nw][D] window values
+    for (int c = tid; c < nw * (D / 8); c += kTcThreads) {
+      const int i = c / (D / 8), e = c % (D / 8);
+      cp_async16(wvs + (size_t)i * D + 8 * e, wvg + (size_t)fmod_(p.div_W, N - nw + i) * D + 8 * e, true);
+    }
+    cp_async_commit();
+    // window: significance on CUDA cores; its normalised probabilities staged for the output below
+    for (int i = tid; i < nw; i += kTcThreads) {
+      const int pos = N - nw + i;
+      const float* row = lg + (size_t)(Ts + i) * GP;
+      float a = 0.0f;
+#pragma unroll
+      for (int h = 0; h < G; h++) {
+        const float ah = row[h] * izr[h];
+        wprob[i * GP + h] = ah;
+        a = fmaxf(a, ah);
+      }
+      if (probs) probs[(size_t)u * p.M + Ts + i] = a;
+      const int c = N - 2 - pos;
+      float* sp = p.win_sig + (size_t)u * W + fmod_(p.div_W, pos);
+      if (c >= 0) *sp = (*sp * (float)c + a) * __frcp_rn((float)(c + 1));
+    }
+#pragma unroll
+    for (int gg = 0; gg < NG; gg++) {
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        const int h = 2 * tig + (c & 1);
+        const int f = (D / 8) * grp + 2 * gg + (c >> 1);        // pv_page's feature mapping
+        if (h < G) part[((size_t)warp * G + h) * D + f] = acc[gg][c] * kPvUnscale * s_iz[h];
+      }
+    }
+    {
+      float v = zsum;                                             // lanes of head grp: tig = 0..3
+      v += __shfl_xor_sync(kFull, v, 1);
+      v += __shfl_xor_sync(kFull, v, 2);
+      if (tig == 0 && grp < G) zred[warp * G + grp] = v * s_iz[grp];
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    if (out != nullptr) {
+      for (int e = tid; e < G * D / 2; e += kTcThreads) {          // a feature pair per thread
+        const int h = e / (D / 2), f = 2 * (e % (D / 2));
+        float o0 = 0.0f, o1 = 0.0f, z = 0.0f;
+        for (int w = 0; w < kTcWarps; w++) {
+          const float2 pp = *reinterpret_cast<const float2*>(part + ((size_t)w * G + h) * D + f);
+          o0 += pp.x; o1 += pp.y; z += zred[w * G + h];
+        }
+        float w0 = 0.0f, w1 = 0.0f;                                // the window's values (FP16) on CUDA cores
+        for (int i = 0; i < nw; i++) {
+          const float a = wprob[i * GP + h];
+          const float2 vv = __half22float2(*reinterpret_cast<const __half2*>(wvs + (size_t)i * D + f));
+          w0 = fmaf(a, vv.x, w0);
+          w1 = fmaf(a, vv.y, w1);
+        }
+        *reinterpret_cast<float2*>(out + ((size_t)u * G + h) * D + f) = make_float2(o0 + z + w0, o1 + z + w1);
+      }
+    }
+    // section minima (stored sections only; keys are unique: positions differ)
+#pragma unroll
+    for (int c = 0; c < 2; c++)
+      if (mkey[c] != ~0ull) atomicMin(&s_min[c], mkey[c]);
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 2; c++)
+      if (mkey[c] != ~0ull && mkey[c] == s_min[c]) s_slot[c] = mslot[c];
+    __syncthreads();
+    if (tid == 0) {
       int32_t* m = p.secmin + 8 * (size_t)u;
 #pragma unroll
       for (int c = 0; c < 2; c++) {
-        m[3 * c] = (int32_t)(uint32_t)(key[c] >> 32);
-        m[3 * c + 1] = (int32_t)(uint32_t)(key[c] & 0xFFFFFFFFull);
-        m[3 * c + 2] = slot[c];
+        m[3 * c] = (int32_t)(uint32_t)(s_min[c] >> 32);
+        m[3 * c + 1] = (int32_t)(uint32_t)(s_min[c] & 0xFFFFFFFFull);
+        m[3 * c + 2] = s_slot[c];
       }
       m[6] = 1;
     }
   }
-  if constexpr (NC > 1) cg::this_cluster().sync();                // CTA 0's remote reads precede the others' exit
 }
 
 // the kernel is specialised for the paper's classes: K8V4 in 16-token pages, K4V2 in 32-token pages;
@@ -718,59 +707,45 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
 bool attend_tc_supported(const PoolDev& p) {
   const ClassGeom &h = p.g[1], &l = p.g[2];
   return h.C == 16 && h.kbits == 8 && h.vbits == 4 && l.C == 32 && l.kbits == 4 && l.vbits == 2 && p.G >= 1 &&
-         p.G <= 8 && (p.d == 64 || p.d == 128);
+         p.G <= 8 && (p.d == 64 || p.d == 128) && p.tc_scratch != nullptr;
 }
 
-constexpr int kTcNC = DKV_TC_CLUSTER;
-
-// logit capacity of one CTA of the cluster: its stored tokens (at most 1/NC of the unit's, plus a partial page) and
-// the window (the last CTA)
-static int tc_local_tokens(const PoolDev& p, int TS) { return ((TS + kTcNC - 1) / kTcNC + 32 + p.W + 31) & ~31; }
-
-size_t attend_tc_smem_bytes(const PoolDev& p, int TS) {
+size_t attend_tc_smem_bytes(const PoolDev& p) {
   const int GP = p.G <= 4 ? 4 : 8;
-  const int TL = tc_local_tokens(p, TS);
-  // phase 3's reduction area: warp partials, z sums, the staged window values, the CTA's output partial
-  const size_t red = (size_t)kTcWarps * p.G * p.d * 4 + (size_t)((kTcWarps * p.G + 3) & ~3) * 4 +
-                     (size_t)p.W * p.d * 2 + (size_t)p.G * p.d * 4;
-  const size_t stage = (size_t)kTcWarps * kTcStages * kTcStage;
-  return (size_t)TL * GP * 4 + (size_t)((p.L + 4) & ~3) * 4 + (stage > red ? stage : red);
+  return (size_t)tc_area_bytes(p.d, p.G, p.W, GP) + (size_t)((p.L + 4) & ~3) * 4 + (size_t)p.W * GP * 4;
 }
 
 template <int D, int G>
-static cudaError_t launch_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s) {
-  const size_t smem = attend_tc_smem_bytes(p, TS);
-  cudaError_t e = cudaFuncSetAttribute(attend_tc_kernel<D, G, kTcNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+static cudaError_t launch_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s) {
+  const size_t smem = attend_tc_smem_bytes(p);
+  cudaError_t e = cudaFuncSetAttribute(attend_tc_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)p.U * kTcNC);
-  cfg.blockDim = dim3(kTcThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;              // one unit per cluster of kTcNC CTAs
-  attr[0].val.clusterDim.x = kTcNC;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = kTcNC > 1 ? 1 : 0;                              // NC = 1: a plain launch
-  return cudaLaunchKernelEx(&cfg, attend_tc_kernel<D, G, kTcNC>, p, q, out, probs, tc_local_tokens(p, TS));
+  int dev = 0, sms = 0, per_sm = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attend_tc_kernel<D, G>, kTcThreads, smem)) != cudaSuccess)
+    return e;
+  int grid = sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > p.tc_slots) grid = p.tc_slots;                       // one scratch slot per CTA
+  if (grid > p.U) grid = p.U;
+  attend_tc_kernel<D, G><<<grid, kTcThreads, smem, s>>>(p, q, out, probs);
+  return cudaGetLastError();
 }
 
 template <int D>
-static cudaError_t launch_tc_d(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s) {
+static cudaError_t launch_tc_d(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s) {
   switch (p.G) {
-    case 1: return launch_tc<D, 1>(p, q, out, probs, TS, s);
-    case 2: return launch_tc<D, 2>(p, q, out, probs, TS, s);
-    case 4: return launch_tc<D, 4>(p, q, out, probs, TS, s);
-    case 5: return launch_tc<D, 5>(p, q, out, probs, TS, s);
-    case 7: return launch_tc<D, 7>(p, q, out, probs, TS, s);
-    default: return launch_tc<D, 8>(p, q, out, probs, TS, s);
+    case 1: return launch_tc<D, 1>(p, q, out, probs, s);
+    case 2: return launch_tc<D, 2>(p, q, out, probs, s);
+    case 4: return launch_tc<D, 4>(p, q, out, probs, s);
+    case 5: return launch_tc<D, 5>(p, q, out, probs, s);
+    case 7: return launch_tc<D, 7>(p, q, out, probs, s);
+    default: return launch_tc<D, 8>(p, q, out, probs, s);
   }
 }
 
-cudaError_t launch_attend_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s) {
-  return p.d == 128 ? launch_tc_d<128>(p, q, out, probs, TS, s) : launch_tc_d<64>(p, q, out, probs, TS, s);
+cudaError_t launch_attend_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s) {
+  return p.d == 128 ? launch_tc_d<128>(p, q, out, probs, s) : launch_tc_d<64>(p, q, out, probs, s);
 }
 
 }  // namespace dkv

@@ -33,6 +33,11 @@ int class_end(const ClassGeom& g) { return g.off_pos + 4 * g.C; }
 
 constexpr int kAttSlots = 296;                               // 2 x 148 SMs
 constexpr int64_t kAttSmemLongThreshold = 160 * 1024;         // logits + (s, z) bytes beyond which HBM slots exist
+constexpr int kTcSlots = 4 * 148;                              // dkv_attend_tc: persistent CTAs (<= 4 per SM)
+// dkv_attend_tc's logit rows per CTA slot (GP floats each): the longest context plus a partial page's overrun
+static int64_t tc_slot_rows(const dkv_config_t* c) { return (c->max_seq_len + 31) / 32 * 32 + 32; }
+static int64_t tc_gp(const dkv_config_t* c) { return c->q_per_kv <= 4 ? 4 : 8; }
+static bool tc_scratch_needed(const dkv_config_t* c) { return c->q_per_kv > 0 && !c->top_tier; }
 
 struct Geometry {
   int32_t U, L, page_bytes, num_tiles, tile_units, nseg, Lt;
@@ -121,6 +126,7 @@ bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
     const bool need = c->q_per_kv > 0 && (GP + 2) * Mp * 4 > kAttSmemLongThreshold;
     Lo.off_att_scratch = take(need ? (int64_t)kAttSlots * (GP + 2) * Mp * 4 : 0);
   }
+  Lo.off_tc_scratch = take(tc_scratch_needed(c) ? (int64_t)kTcSlots * tc_slot_rows(c) * tc_gp(c) * 4 : 0);
   Lo.off_qpid = take(8 * U);
   Lo.off_ring = take(4 * P);
   Lo.off_table = take(4 * U * G.L);
@@ -291,6 +297,9 @@ dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_
     d.att_scratch = need ? (float*)(b + Lo.off_att_scratch) : nullptr;
     d.att_slots = need ? kAttSlots : 0;
   }
+  d.tc_scratch = tc_scratch_needed(cfg) ? (float*)(b + Lo.off_tc_scratch) : nullptr;
+  d.tc_slots = tc_scratch_needed(cfg) ? kTcSlots : 0;
+  d.tc_slot_rows = (int32_t)tc_slot_rows(cfg);
   d.use_head_alpha = 0;
   d.G = cfg->q_per_kv;
   d.prefill_wf = cfg->prefill_workflow;
@@ -480,15 +489,11 @@ dkv_status_t dkv_attend_tc(dkv_pool_t p, const uint16_t* d_q, float* d_out, floa
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
     return DKV_ERR_CUDA;
-  int TS = 1;
-  for (int r = 0; r < p->cfg.max_requests; r++)
-    if (p->req_state[r] == DKV_REQ_ACTIVE && p->seq_len[r] > TS) TS = p->seq_len[r];
-  TS = (TS + 31) & ~31;
-  // contexts whose logits do not fit in shared memory, and page geometries the kernel does not tile, take the
-  // exact path (documented in dkv.h)
-  if (!attend_tc_supported(p->dev) || attend_tc_smem_bytes(p->dev, TS) > (size_t)optin)
+  // page geometries the kernel does not tile take the exact path (documented in dkv.h); logits live in the
+  // arena's per-CTA scratch slots, so any context up to max_seq_len runs here
+  if (!attend_tc_supported(p->dev) || attend_tc_smem_bytes(p->dev) > (size_t)optin)
     return dkv_attend(p, d_q, d_out, d_probs, s);
-  return launch_attend_tc(p->dev, d_q, d_out, d_probs, TS, (cudaStream_t)s) == cudaSuccess ? DKV_OK : DKV_ERR_CUDA;
+  return launch_attend_tc(p->dev, d_q, d_out, d_probs, (cudaStream_t)s) == cudaSuccess ? DKV_OK : DKV_ERR_CUDA;
 }
 
 dkv_status_t dkv_set_head_thresholds(dkv_pool_t p, const float* h_alpha_h, const float* h_alpha_l, dkv_stream_t s) {

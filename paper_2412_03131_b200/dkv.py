@@ -72,7 +72,8 @@ class dkv_layout_t(C.Structure):
                                                                   ("table_len_top", C.c_int32), ("C_top", C.c_int32),
                                                                   ("row_top", C.c_int32), ("off_k_top", C.c_int32),
                                                                   ("off_v_top", C.c_int32), ("off_score_top", C.c_int32),
-                                                                  ("off_pos_top", C.c_int32), ("off_qpid", C.c_int64)]
+                                                                  ("off_pos_top", C.c_int32), ("off_qpid", C.c_int64),
+                                                                  ("off_tc_scratch", C.c_int64)]
 
 
 assert C.sizeof(dkv_decision_t) == 16
