@@ -34,8 +34,9 @@ int class_end(const ClassGeom& g) { return g.off_pos + 4 * g.C; }
 constexpr int kAttSlots = 296;                               // 2 x 148 SMs
 constexpr int64_t kAttSmemLongThreshold = 160 * 1024;         // logits + (s, z) bytes beyond which HBM slots exist
 constexpr int kTcSlots = 4 * 148;                              // dkv_attend_tc: persistent CTAs (<= 4 per SM)
-// dkv_attend_tc's logit rows per CTA slot (GP floats each): the longest context plus a partial page's overrun
-static int64_t tc_slot_rows(const dkv_config_t* c) { return (c->max_seq_len + 31) / 32 * 32 + 32; }
+// dkv_attend_tc's logit rows per CTA slot (GP of them): the longest context plus the padding of the unit's last
+// high and last low page (rows are page-aligned: <= 15 + 31)
+static int64_t tc_slot_rows(const dkv_config_t* c) { return (c->max_seq_len + 31) / 32 * 32 + 64; }
 static int64_t tc_gp(const dkv_config_t* c) { return c->q_per_kv <= 4 ? 4 : 8; }
 static bool tc_scratch_needed(const dkv_config_t* c) { return c->q_per_kv > 0 && !c->top_tier; }
 
