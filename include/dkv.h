@@ -147,8 +147,8 @@ typedef struct {
                                   downgraded), page of a downgraded victim's KV_l slot}: written by
                                   dkv_classify(DECODE) for existing pages and by dkv_compact_alloc for granted
                                   ones, read by dkv_quant_write(DECODE) instead of the tables */
-  int64_t off_tc_scratch;      /* dkv_attend_tc: 592 slots of (max_seq_len rounded to 32, + 32) * (4 if
-                                  q_per_kv <= 4 else 8) fp32 logit rows, one per persistent CTA (0 bytes when
+  int64_t off_tc_scratch;      /* dkv_attend_tc: 2 x 592 buffers of (max_seq_len rounded to 32, + 64) * (4 if
+                                  q_per_kv <= 4 else 8) fp32 logit rows, two per persistent CTA (0 bytes when
                                   q_per_kv = 0 or with the FP16 tier) */
 } dkv_layout_t;
 
@@ -222,11 +222,12 @@ dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* 
 /* NEXT-2 on tensor cores — the same operation as dkv_attend (Eq. 1 with GQA max, the running-mean significance
  * written back, the section minima for the next dkv_classify), computed with mma.sync tensor-core contractions on
  * the integer codes: logit = (s * q.codes + z * sum(q)) / sqrt(d), out = sum_t (a s) codes + sum_t a z, fp32
- * accumulation, the window on CUDA cores.  Not bit-identical to dkv_attend / the oracle: results agree with
+ * accumulation, the FP16 window on the same tensor-core path (online softmax, one pass over the pages).  Not bit-identical to dkv_attend / the oracle: results agree with
  * Eq. 1 evaluated in float64 to the tolerances of tests/test_gpu_attention_tc.py (outputs rtol 2e-4 / atol 2e-5,
  * scores rtol 2e-5 / atol 1e-7); the section minima are exact for the significance values it writes.  Same
  * arguments and errors as dkv_attend.  Falls back to dkv_attend when a class's pages are not the paper's K8V4 x16 /
- * K4V2 x32 tiles.  Persistent CTAs; each keeps its unit's logits in its own slot of the arena's off_tc_scratch. */
+ * K4V2 x32 tiles.  Persistent CTAs; each keeps its units' logits in its own two buffers of the arena's
+ * off_tc_scratch (a unit's significance pass runs during the CTA's next unit). */
 dkv_status_t dkv_attend_tc(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* d_probs, dkv_stream_t s);
 
 /* NEXT-4 — per-head thresholds ("a shared set of thresholds for all attention heads" is the

@@ -384,10 +384,17 @@ __device__ __forceinline__ void tc_window_chunk(const uint16_t* wk, const uint16
   });
 }
 
+// A unit whose significance pass is still pending (its logits, maxima and sums are final): the pass runs during
+// the CTA's next unit, a block of kTcThreads token rows per page iteration of each warp (software pipelining across
+// units), so that its dependent loads (page ID -> score / position) overlap that unit's page computation.
+struct TcSigUnit {
+  int u, N, nh, nl, ph, lo0, wb, nw, Ts, rows, buf;
+};
+
 // Persistent: gridDim.x CTAs (the occupancy limit, at most tc_slots) take units blockIdx.x, + gridDim.x, ...  A
-// CTA's logits (log2 units) live in its own global scratch slot (p.tc_scratch: [tc_slot_rows][GP] fp32, rows
-// page-aligned: high page k at 16 k, low page k' at 16 ph + 32 k', the window after them), written once in the
-// page pass and read once by the significance pass.
+// CTA's logits (log2 units) live in its own global scratch slots (p.tc_scratch: two [tc_slot_rows][GP] fp32
+// buffers per CTA, alternating between units; rows page-aligned: high page k at 16 k, low page k' at 16 ph + 32 k',
+// the window after them), written once in the page pass and read once by the significance pass.
 template <int D, int G>
 __global__ void __launch_bounds__(kTcThreads, DKV_TC_MINB)
 attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs) {
@@ -396,23 +403,26 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   using HI = TcCls<D, 16, 8, 4>;                                  // K8V4, 16-token pages
   using LO = TcCls<D, 32, 4, 2>;                                  // K4V2, 32-token pages
   extern __shared__ __align__(128) uint8_t tc_smem[];
-  __shared__ float s_qsum[8];
   __shared__ float s_mw[kTcWarps][8], s_zw[kTcWarps][8], s_zsw[kTcWarps][8];
-  __shared__ float s_M[8], s_iZ[8], s_fw[kTcWarps][8];
+  __shared__ float s_fw[kTcWarps][8];
+  __shared__ float s_M[2][8], s_iZ[2][8];                         // per logit buffer: the unit's maxima and 1/Z
+  __shared__ TcSigUnit s_prev;
   __shared__ unsigned long long s_min[2];
   __shared__ int s_slot[2];
+  __shared__ __align__(16) float s_sl[2][kTcThreads][GP];         // significance pass: staged logit rows
+  __shared__ __align__(8) float s_ss[2][kTcThreads][2];           //   ... and (score, position bits)
   __shared__ __align__(8) uint64_t s_bar[kTcWarps][kTcStages];   // per-warp stage mbarriers (bulk copies)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = lane >> 2, tig = lane & 3;
   if (ld_volatile(&p.ctrl->status) != 0) return;                  // sticky error: no-op
-  const int L = p.L, W = p.W, R = p.tc_slot_rows;
+  const int L = p.L, W = p.W, R = p.tc_slot_rows, LP = (L + 4) & ~3;
   const ClassGeom gh = p.g[1], gl = p.g[2];
-  float* const lg = p.tc_scratch + (size_t)blockIdx.x * R * GP;  // this CTA's logits [R][GP]
   uint8_t* const stage0 = tc_smem;
-  int32_t* const pid = reinterpret_cast<int32_t*>(tc_smem + tc_area_bytes(D, G, STG));
+  int32_t* const pidb = reinterpret_cast<int32_t*>(tc_smem + tc_area_bytes(D, G, STG));   // [2][LP] page IDs
   uint8_t* const mystage = stage0 + (size_t)warp * kTcStages * STG;
   uint64_t* const bars = s_bar[warp];
   if (tid < kTcWarps * kTcStages) mbar_init(&s_bar[tid / kTcStages][tid % kTcStages], 1);
+  if (tid == 0) s_prev.rows = 0;
   fence_mbar_init();
   uint32_t phase = 0;                                             // bit s: parity of stage s's next completion
   const uint32_t bar_s = smem_u32(bars), stage_s = smem_u32(mystage);
@@ -421,6 +431,94 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   const uint16_t* const wk_all = reinterpret_cast<const uint16_t*>(p.win_k);
   const uint16_t* const wv_all = reinterpret_cast<const uint16_t*>(p.win_v);
+  int buf = 0;                                                    // this unit's logit / page-ID buffer
+
+  // ---- the significance pass of the pending unit `sp` (Q33): row block j = rows j * kTcThreads + tid
+  // issue: stage the row's logits, score and position with cp.async into slot j & 1 (nothing for a padding row)
+  unsigned long long mkey0 = ~0ull, mkey1 = ~0ull;                // this thread's section minima of `sp`
+  int mslot0 = -1, mslot1 = -1;
+  auto sig_issue = [&](const TcSigUnit& sp, int j) {
+    const int row = j * kTcThreads + tid, sl = j & 1;
+    if (row >= sp.rows) return;
+    const float* lgp = p.tc_scratch + ((size_t)(2 * blockIdx.x + sp.buf) * R + row) * GP;
+    if (row < sp.wb) {
+      const bool hi = row < sp.lo0;
+      const int rr = hi ? row : row - sp.lo0;
+      if (rr >= (hi ? sp.nh : sp.nl)) return;                     // a partial page's padding row
+      const int k = hi ? row >> 4 : sp.ph + (rr >> 5), j2 = hi ? row & 15 : rr & 31;
+      const ClassGeom& gg = hi ? gh : gl;
+      const uint8_t* pg = p.pages + (size_t)pidb[sp.buf * LP + k] * (size_t)p.page_bytes;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&s_ss[sl][tid][0])), "l"(pg + gg.off_score + 4 * j2) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&s_ss[sl][tid][1])), "l"(pg + gg.off_pos + 4 * j2) : "memory");
+    } else {
+      const int pos = sp.N - sp.nw + (row - sp.wb);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&s_ss[sl][tid][0])),
+                   "l"(p.win_sig + (size_t)sp.u * W + fmod_(p.div_W, pos)) : "memory");
+    }
+#pragma unroll
+    for (int c4 = 0; c4 < GP / 4; c4++) cp_async16(&s_sl[sl][tid][4 * c4], lgp + 4 * c4, true);
+  };
+  // consume: a = max_h 2^(l2 - M) / Z, the running mean written back, probabilities, section minima
+  auto sig_consume = [&](const TcSigUnit& sp, int j) {
+    const int row = j * kTcThreads + tid, sl = j & 1;
+    if (row >= sp.rows) return;
+    const bool stored = row < sp.wb, hi = row < sp.lo0;
+    const int rr = hi ? row : row - sp.lo0;
+    if (stored && rr >= (hi ? sp.nh : sp.nl)) return;
+    float a = 0.0f;
+#pragma unroll
+    for (int h = 0; h < G; h++) a = fmaxf(a, ex2(s_sl[sl][tid][h] - s_M[sp.buf][h]) * s_iZ[sp.buf][h]);
+    float sg = s_ss[sl][tid][0];
+    const int pos = stored ? __float_as_int(s_ss[sl][tid][1]) : sp.N - sp.nw + (row - sp.wb);
+    const int c = sp.N - 2 - pos;
+    if (c >= 0) sg = (sg * (float)c + a) * __frcp_rn((float)(c + 1));
+    if (stored) {
+      const int k = hi ? row >> 4 : sp.ph + (rr >> 5), j2 = hi ? row & 15 : rr & 31;
+      uint8_t* pg = p.pages + (size_t)pidb[sp.buf * LP + k] * (size_t)p.page_bytes;
+      if (c >= 0) *reinterpret_cast<float*>(pg + (hi ? gh.off_score : gl.off_score) + 4 * j2) = sg;
+      if (probs) probs[(size_t)sp.u * p.M + (hi ? rr : sp.nh + rr)] = a;
+      const unsigned long long key = ((unsigned long long)__float_as_uint(sg) << 32) | (uint32_t)pos;
+      if (hi) {
+        if (key < mkey0) { mkey0 = key; mslot0 = rr; }
+      } else if (key < mkey1) {
+        mkey1 = key; mslot1 = rr;
+      }
+    } else {
+      if (c >= 0) p.win_sig[(size_t)sp.u * W + fmod_(p.div_W, pos)] = sg;
+      if (probs) probs[(size_t)sp.u * p.M + sp.Ts + (row - sp.wb)] = a;
+    }
+  };
+  // one pipeline step: stage block j + 1, then consume block j
+  auto sig_step = [&](const TcSigUnit& sp, int j, int nsig) {
+    if (j + 1 < nsig) sig_issue(sp, j + 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    sig_consume(sp, j);
+  };
+  // the pending unit's section minima (after every thread has consumed its rows)
+  auto sig_finish = [&](const TcSigUnit& sp) {
+    if (mkey0 != ~0ull) atomicMin(&s_min[0], mkey0);
+    if (mkey1 != ~0ull) atomicMin(&s_min[1], mkey1);
+    __syncthreads();
+    if (mkey0 != ~0ull && mkey0 == s_min[0]) s_slot[0] = mslot0;
+    if (mkey1 != ~0ull && mkey1 == s_min[1]) s_slot[1] = mslot1;
+    __syncthreads();
+    if (tid == 0) {
+      int32_t* m = p.secmin + 8 * (size_t)sp.u;
+#pragma unroll
+      for (int c = 0; c < 2; c++) {
+        m[3 * c] = (int32_t)(uint32_t)(s_min[c] >> 32);
+        m[3 * c + 1] = (int32_t)(uint32_t)(s_min[c] & 0xFFFFFFFFull);
+        m[3 * c + 2] = s_slot[c];
+        s_min[c] = ~0ull;
+        s_slot[c] = -1;
+      }
+      m[6] = 1;
+    }
+    mkey0 = mkey1 = ~0ull;
+    mslot0 = mslot1 = -1;
+  };
+  if (tid < 2) { s_min[tid] = ~0ull; s_slot[tid] = -1; }
 
   for (int u = blockIdx.x; u < p.U; u += gridDim.x) {
     const int r = fdiv(p.div_LyH, u);
@@ -428,24 +526,21 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     const int N = p.seq_len[r];
     const int nh = p.n_h[u], nl = p.n_l[u];
     const int nw = min(W, N);
-    const int Ts = nh + nl;
     const int ph = (nh + HI::C - 1) / HI::C, pl = (nl + LO::C - 1) / LO::C;
     const int npg = ph + pl;
     const int lo0 = HI::C * ph, wb = lo0 + LO::C * pl;            // first scratch row of the low pages, window
     const int32_t* trow = p.table + (size_t)u * L;
+    int32_t* const pid = pidb + buf * LP;
+    float* const lg = p.tc_scratch + (size_t)(2 * blockIdx.x + buf) * R * GP;   // this unit's logits [R][GP]
     fence_proxy_async_smem();                                     // the previous unit's generic accesses ...
-    __syncthreads();                                              // ... before this unit's bulk fills
+    __syncthreads();                                              // ... before this unit's bulk fills; s_prev
+    const TcSigUnit sp = s_prev;
+    const int nsig = (sp.rows + kTcThreads - 1) / kTcThreads;     // the pending unit's row blocks
     for (int k = tid; k < npg; k += kTcThreads) pid[k] = k < ph ? trow[k] : trow[L - 1 - (k - ph)];
-    if (tid < 2) { s_min[tid] = ~0ull; s_slot[tid] = -1; }
-    if (tid < 8) {                                                // per-head sum of the query (the z' term)
-      float sacc = 0.0f;
-      if (tid < G)
-        for (int f = 0; f < D; f++) sacc += __half2float(__ushort_as_half(q[((size_t)u * G + tid) * D + f]));
-      s_qsum[tid] = sacc * scale2;
-    }
     // B fragments of the queries (k = features, permuted as the keys' A fragments; n = head grp): k-step g
     // holds features FPK tig + 4g + {0, 1} (b0) and + {2, 3} (b1) of head grp (zero for grp >= G)
     uint32_t qb[NG][2];
+    float qs = 0.0f;                                              // head grp's sum over this lane's features
     {
       const uint16_t* qr = q + ((size_t)u * G + (grp < G ? grp : 0)) * D + FPK * tig;
 #pragma unroll
@@ -453,10 +548,16 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
         uint2 v = make_uint2(0u, 0u);
         if (grp < G) v = *reinterpret_cast<const uint2*>(qr + 4 * g);
         qb[g][0] = v.x; qb[g][1] = v.y;
+        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
+        const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
+        qs += (f0.x + f0.y) + (f1.x + f1.y);
       }
+      qs += __shfl_xor_sync(kFull, qs, 1);
+      qs += __shfl_xor_sync(kFull, qs, 2);
     }
-    __syncthreads();                                              // pid, s_qsum
-    const float qsz[2] = {s_qsum[2 * tig], s_qsum[2 * tig + 1]};  // heads 2 tig, 2 tig + 1 (0 beyond G), x scale2
+    // the z' term's per-head sums for this lane's heads 2 tig, 2 tig + 1 (held by grp = 2 tig, 2 tig + 1), x scale2
+    const float qsz[2] = {__shfl_sync(kFull, qs, 8 * tig) * scale2, __shfl_sync(kFull, qs, 8 * tig + 4) * scale2};
+    __syncthreads();                                              // pid
     float* const lgl = lg + 2 * tig;                              // this lane's logit column
 
     auto page_ptr = [&](int k) { return p.pages + (size_t)pid[k] * (size_t)p.page_bytes; };
@@ -470,7 +571,8 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
                    ::"r"(stage_s + slot * STG), "l"(page_ptr(k)), "r"(bytes), "r"(bar), "l"(pol) : "memory");
     };
 
-    // ---- the page pass: each warp its pages (k = warp + i * kTcWarps), kTcStages - 1 copies ahead
+    // ---- the page pass: each warp its pages (k = warp + i * kTcWarps), kTcStages - 1 copies ahead; page
+    // iteration i also runs block i of the pending unit's significance pass
     TcState<D> st;
 #pragma unroll
     for (int mt = 0; mt < NMT; mt++) st.o[mt][0] = st.o[mt][1] = st.o[mt][2] = st.o[mt][3] = 0.0f;
@@ -483,6 +585,8 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
 #pragma unroll
     for (int i = 0; i < kTcStages - 1; i++)
       if (i < my_n) stage(warp + i * kTcWarps, i);
+    if (nsig > 0) sig_issue(sp, 0);
+    cp_async_commit();
     // page i of this warp sits in stage i mod kTcStages (slot counters, not a modulo; the loop is not unrolled
     // by the stage count — measured: three inlined copies of the chunk code overflowed the instruction cache)
     for (int i = 0, slot = 0, islot = kTcStages - 1; i < my_n; i++) {
@@ -501,9 +605,12 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
       }
       fence_proxy_async_smem();                                   // this stage's reads before its next bulk fill
       __syncwarp();
+      if (i < nsig) sig_step(sp, i, nsig);
       slot = slot + 1 == kTcStages ? 0 : slot + 1;
       islot = islot + 1 == kTcStages ? 0 : islot + 1;
     }
+    // the pending unit's remaining row blocks (a warp with fewer pages than blocks)
+    for (int j = my_n; j < nsig; j++) sig_step(sp, j, nsig);
     // the FP16 window: 16-slot chunks of the ring, round-robin over the warps after their pages
     {
       const int wbase = fmod_(p.div_W, N - nw);                   // ring slot of the oldest window token
@@ -520,6 +627,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
         st.zs[c] += __shfl_xor_sync(kFull, st.zs[c], o);
       }
     __syncthreads();                                              // every warp is out of its stages
+    if (sp.rows > 0) sig_finish(sp);                              // (two barriers inside)
     float* part = reinterpret_cast<float*>(stage0);               // [kTcWarps][G][D] warp partials (hi + lo)
 #pragma unroll
     for (int c = 0; c < 2; c++) {
@@ -544,9 +652,10 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
         s_fw[w][tid] = f;
         Z = fmaf(f, s_zw[w][tid], Z);
       }
-      s_M[tid] = M;
-      s_iZ[tid] = Z > 0.0f ? 1.0f / Z : 0.0f;
+      s_M[buf][tid] = M;
+      s_iZ[buf][tid] = Z > 0.0f ? 1.0f / Z : 0.0f;
     }
+    if (tid == 0) s_prev = TcSigUnit{u, N, nh, nl, ph, lo0, wb, nw, nh + nl, wb + nw, buf};   // pending now
     __syncthreads();
     // ---- the output: the warps' partials (each with its z term), rescaled to the global maximum
     if (out != nullptr) {
@@ -561,94 +670,22 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
           o0 = fmaf(fw, pp.x + zz, o0);
           o1 = fmaf(fw, pp.y + zz, o1);
         }
-        const float iz = s_iZ[h];
+        const float iz = s_iZ[buf][h];
         *reinterpret_cast<float2*>(out + ((size_t)u * G + h) * D + f) = make_float2(o0 * iz, o1 * iz);
       }
     }
-    // ---- significance (Q33) of every stored and window token from its logits: a = max_h 2^(l2 - M) / Z
-    float Mh[G], iZh[G];
-#pragma unroll
-    for (int h = 0; h < G; h++) { Mh[h] = s_M[h]; iZh[h] = s_iZ[h]; }
-    unsigned long long mkey[2] = {~0ull, ~0ull};
-    int mslot[2] = {-1, -1};
-    // a thread per token row, kSigBatch rows at a time with every load of the batch issued first (the loads are
-    // dependent round trips otherwise: page ID -> position / score)
-    constexpr int kSigBatch = 4;
-    for (int base = tid; base < wb + nw; base += kSigBatch * kTcThreads) {
-      float lv[kSigBatch][GP], sgv[kSigBatch];
-      int posv[kSigBatch], rrv[kSigBatch];
-      float* spv[kSigBatch];
-#pragma unroll
-      for (int b = 0; b < kSigBatch; b++) {
-        const int row = base + b * kTcThreads;
-        const bool stored = row < wb, hi = row < lo0;
-        const int rr = hi ? row : row - lo0;                      // slot in its section
-        rrv[b] = -1;
-        spv[b] = nullptr;
-        if (row >= wb + nw || (stored && rr >= (hi ? nh : nl))) continue;   // past the end / a padding row
-        const float4* lr = reinterpret_cast<const float4*>(lg + (size_t)row * GP);
-#pragma unroll
-        for (int c4 = 0; c4 < GP / 4; c4++) {
-          const float4 v = lr[c4];
-          lv[b][4 * c4] = v.x; lv[b][4 * c4 + 1] = v.y; lv[b][4 * c4 + 2] = v.z; lv[b][4 * c4 + 3] = v.w;
-        }
-        rrv[b] = rr;
-        if (stored) {
-          const int k = hi ? row >> 4 : ph + (rr >> 5), j = hi ? row & 15 : rr & 31;
-          const ClassGeom& gg = hi ? gh : gl;
-          uint8_t* pg = page_ptr(k);
-          posv[b] = *reinterpret_cast<const int32_t*>(pg + gg.off_pos + 4 * j);
-          spv[b] = reinterpret_cast<float*>(pg + gg.off_score + 4 * j);
-        } else {
-          posv[b] = N - nw + (row - wb);
-          spv[b] = p.win_sig + (size_t)u * W + fmod_(p.div_W, posv[b]);
-        }
-        sgv[b] = *spv[b];
-      }
-#pragma unroll
-      for (int b = 0; b < kSigBatch; b++) {
-        if (spv[b] == nullptr) continue;
-        const int row = base + b * kTcThreads;
-        float a = 0.0f;
-#pragma unroll
-        for (int h = 0; h < G; h++) a = fmaxf(a, ex2(lv[b][h] - Mh[h]) * iZh[h]);
-        const int pos = posv[b], rr = rrv[b];
-        float sg = sgv[b];
-        const int c = N - 2 - pos;
-        if (c >= 0) {
-          sg = (sg * (float)c + a) * __frcp_rn((float)(c + 1));
-          *spv[b] = sg;
-        }
-        if (row < wb) {
-          const bool hi = row < lo0;
-          if (probs) probs[(size_t)u * p.M + (hi ? rr : nh + rr)] = a;
-          const int cls = hi ? 0 : 1;
-          const unsigned long long key = ((unsigned long long)__float_as_uint(sg) << 32) | (uint32_t)pos;
-          if (key < mkey[cls]) { mkey[cls] = key; mslot[cls] = rr; }
-        } else if (probs) {
-          probs[(size_t)u * p.M + Ts + (row - wb)] = a;
-        }
-      }
-    }
-    // section minima (stored sections only; keys are unique: positions differ)
-#pragma unroll
-    for (int c = 0; c < 2; c++)
-      if (mkey[c] != ~0ull) atomicMin(&s_min[c], mkey[c]);
+    buf ^= 1;
+  }
+  // the last unit's significance pass, on its own
+  __syncthreads();
+  const TcSigUnit sp = s_prev;
+  if (sp.rows > 0) {
+    const int nsig = (sp.rows + kTcThreads - 1) / kTcThreads;
+    sig_issue(sp, 0);
+    cp_async_commit();
+    for (int j = 0; j < nsig; j++) sig_step(sp, j, nsig);
     __syncthreads();
-#pragma unroll
-    for (int c = 0; c < 2; c++)
-      if (mkey[c] != ~0ull && mkey[c] == s_min[c]) s_slot[c] = mslot[c];
-    __syncthreads();
-    if (tid == 0) {
-      int32_t* m = p.secmin + 8 * (size_t)u;
-#pragma unroll
-      for (int c = 0; c < 2; c++) {
-        m[3 * c] = (int32_t)(uint32_t)(s_min[c] >> 32);
-        m[3 * c + 1] = (int32_t)(uint32_t)(s_min[c] & 0xFFFFFFFFull);
-        m[3 * c + 2] = s_slot[c];
-      }
-      m[6] = 1;
-    }
+    sig_finish(sp);
   }
 }
 
@@ -669,7 +706,7 @@ bool attend_tc_supported(const PoolDev& p) {
 
 size_t attend_tc_smem_bytes(const PoolDev& p) {
   const int stg = p.d == 128 ? tc_stage_bytes<128>() : tc_stage_bytes<64>();
-  return (size_t)tc_area_bytes(p.d, p.G, stg) + (size_t)((p.L + 4) & ~3) * 4;
+  return (size_t)tc_area_bytes(p.d, p.G, stg) + (size_t)2 * ((p.L + 4) & ~3) * 4;
 }
 
 template <int D, int G>
@@ -683,7 +720,7 @@ static cudaError_t launch_tc(const PoolDev& p, const uint16_t* q, float* out, fl
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attend_tc_kernel<D, G>, kTcThreads, smem)) != cudaSuccess)
     return e;
   int grid = sms * (per_sm > 0 ? per_sm : 1);
-  if (grid > p.tc_slots) grid = p.tc_slots;                       // one scratch slot per CTA
+  if (grid > p.tc_slots) grid = p.tc_slots;                       // two scratch buffers per CTA slot
   if (grid > p.U) grid = p.U;
   attend_tc_kernel<D, G><<<grid, kTcThreads, smem, s>>>(p, q, out, probs);
   return cudaGetLastError();

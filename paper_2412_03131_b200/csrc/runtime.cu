@@ -127,7 +127,7 @@ bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
     const bool need = c->q_per_kv > 0 && (GP + 2) * Mp * 4 > kAttSmemLongThreshold;
     Lo.off_att_scratch = take(need ? (int64_t)kAttSlots * (GP + 2) * Mp * 4 : 0);
   }
-  Lo.off_tc_scratch = take(tc_scratch_needed(c) ? (int64_t)kTcSlots * tc_slot_rows(c) * tc_gp(c) * 4 : 0);
+  Lo.off_tc_scratch = take(tc_scratch_needed(c) ? (int64_t)kTcSlots * 2 * tc_slot_rows(c) * tc_gp(c) * 4 : 0);
   Lo.off_qpid = take(8 * U);
   Lo.off_ring = take(4 * P);
   Lo.off_table = take(4 * U * G.L);
