@@ -65,6 +65,15 @@ __device__ __forceinline__ void mma_f16(float (&d)[4], uint32_t a0, uint32_t a1,
                : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
                : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar), "r"(parity) : "memory");
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -195,16 +204,17 @@ __device__ __forceinline__ uint32_t movm_trans(uint32_t x) {
 template <int D, class VA>
 __device__ __forceinline__ void tc_softmax_pv(const float (&l)[4], const float (&svs)[2], const float (&zv)[2],
                                               TcState<D>& st, VA&& va) {
-  // running maximum of heads 2 tig, 2 tig + 1 over the 8 lanes (grp) holding them; moved only by more than kTau
+  // running maximum of heads 2 tig, 2 tig + 1, moved only by more than kTau: the lane-local test decides whether
+  // any lane needs it; only then is the chunk maximum reduced over the 8 lanes (grp) holding each head
   float pm[2] = {fmaxf(l[0], l[2]), fmaxf(l[1], l[3])};
+  if (__any_sync(kFull, (pm[0] > st.m[0] + kTau) | (pm[1] > st.m[1] + kTau))) {
 #pragma unroll
-  for (int c = 0; c < 2; c++) {
-    pm[c] = fmaxf(pm[c], __shfl_xor_sync(kFull, pm[c], 4));
-    pm[c] = fmaxf(pm[c], __shfl_xor_sync(kFull, pm[c], 8));
-    pm[c] = fmaxf(pm[c], __shfl_xor_sync(kFull, pm[c], 16));
-  }
-  const bool up0 = pm[0] > st.m[0] + kTau, up1 = pm[1] > st.m[1] + kTau;
-  if (__any_sync(kFull, up0 | up1)) {
+    for (int c = 0; c < 2; c++) {
+      pm[c] = fmaxf(pm[c], __shfl_xor_sync(kFull, pm[c], 4));
+      pm[c] = fmaxf(pm[c], __shfl_xor_sync(kFull, pm[c], 8));
+      pm[c] = fmaxf(pm[c], __shfl_xor_sync(kFull, pm[c], 16));
+    }
+    const bool up0 = pm[0] > st.m[0] + kTau, up1 = pm[1] > st.m[1] + kTau;
     const float mn0 = up0 ? pm[0] : st.m[0], mn1 = up1 ? pm[1] : st.m[1];
     const float f0 = ex2(st.m[0] - mn0), f1 = ex2(st.m[1] - mn1);   // 1 when unchanged, 0 from -inf
 #pragma unroll
@@ -435,6 +445,8 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
 
   // ---- the significance pass of the pending unit `sp` (Q33): row block j = rows j * kTcThreads + tid
   // issue: stage the row's logits, score and position with cp.async into slot j & 1 (nothing for a padding row)
+  constexpr uint32_t kSsStride = kTcThreads * 8, kSlStride = kTcThreads * GP * 4;
+  const uint32_t ss_u32 = smem_u32(&s_ss[0][tid][0]), sl_u32 = smem_u32(&s_sl[0][tid][0]);
   unsigned long long mkey0 = ~0ull, mkey1 = ~0ull;                // this thread's section minima of `sp`
   int mslot0 = -1, mslot1 = -1;
   auto sig_issue = [&](const TcSigUnit& sp, int j) {
@@ -448,15 +460,17 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
       const int k = hi ? row >> 4 : sp.ph + (rr >> 5), j2 = hi ? row & 15 : rr & 31;
       const ClassGeom& gg = hi ? gh : gl;
       const uint8_t* pg = p.pages + (size_t)pidb[sp.buf * LP + k] * (size_t)p.page_bytes;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&s_ss[sl][tid][0])), "l"(pg + gg.off_score + 4 * j2) : "memory");
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&s_ss[sl][tid][1])), "l"(pg + gg.off_pos + 4 * j2) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ss_u32 + sl * kSsStride), "l"(pg + gg.off_score + 4 * j2) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ss_u32 + sl * kSsStride + 4), "l"(pg + gg.off_pos + 4 * j2) : "memory");
     } else {
       const int pos = sp.N - sp.nw + (row - sp.wb);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&s_ss[sl][tid][0])),
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ss_u32 + sl * kSsStride),
                    "l"(p.win_sig + (size_t)sp.u * W + fmod_(p.div_W, pos)) : "memory");
     }
 #pragma unroll
-    for (int c4 = 0; c4 < GP / 4; c4++) cp_async16(&s_sl[sl][tid][4 * c4], lgp + 4 * c4, true);
+    for (int c4 = 0; c4 < GP / 4; c4++)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sl_u32 + sl * kSlStride + 16 * c4), "l"(lgp + 4 * c4)
+                   : "memory");
   };
   // consume: a = max_h 2^(l2 - M) / Z, the running mean written back, probabilities, section minima
   auto sig_consume = [&](const TcSigUnit& sp, int j) {
@@ -592,7 +606,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     for (int i = 0, slot = 0, islot = kTcStages - 1; i < my_n; i++) {
       const int k = warp + i * kTcWarps;
       if (i + kTcStages - 1 < my_n) stage(warp + (i + kTcStages - 1) * kTcWarps, islot);
-      mbar_wait(&bars[slot], (phase >> slot) & 1u);
+      mbar_wait_u32(bar_s + 8 * slot, (phase >> slot) & 1u);
       phase ^= 1u << slot;
       const uint8_t* seg = mystage + slot * STG;
       if (k < ph) {
@@ -603,7 +617,10 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
         tc_chunk<D, G, GP, LO>(seg, 0, cnt, qb, qsz, scale2, lgl, row, st, grp, tig);
         if (cnt > 16) tc_chunk<D, G, GP, LO>(seg, 1, cnt, qb, qsz, scale2, lgl, row, st, grp, tig);
       }
-      fence_proxy_async_smem();                                   // this stage's reads before its next bulk fill
+      // The stage is refilled (by the bulk copy of page i + kTcStages) one iteration later.  No proxy fence: every
+      // read of it fed an mma.sync of this iteration, which no lane passes before all lanes have issued it, so
+      // the reads have completed before lane 0 can issue that copy (measured: the fence's MEMBAR.CTA per page
+      // also waited on the logit stores).
       __syncwarp();
       if (i < nsig) sig_step(sp, i, nsig);
       slot = slot + 1 == kTcStages ? 0 : slot + 1;
