@@ -40,7 +40,7 @@ namespace dkv {
 #define DKV_TC_WARPS 4          // warps per CTA (one unit per CTA)
 #endif
 #ifndef DKV_TC_STAGES
-#define DKV_TC_STAGES 3         // pages in flight per warp
+#define DKV_TC_STAGES 2         // pages in flight per warp (measured: 2 beats 3, tools/tc_ab.sh, profiles/r2o_tc_ab.log)
 #endif
 #ifndef DKV_TC_MINB
 #define DKV_TC_MINB 4           // CTAs per SM the register budget is sized for
