@@ -143,10 +143,11 @@ typedef struct {
   int64_t off_n_t;             /* NEXT-4: int32[units] stored TOP tokens */
   int32_t table_len_top;       /* NEXT-4: ceil(max_seq_len / page_tokens_top), 1 without the tier */
   int32_t C_top, row_top, off_k_top, off_v_top, off_score_top, off_pos_top;   /* TOP page geometry (fp16 rows) */
-  int64_t off_qpid;            /* int32[units][2] {page of t_c's slot (= the victim's KV_h page when it is
-                                  downgraded), page of a downgraded victim's KV_l slot}: written by
-                                  dkv_classify(DECODE) for existing pages and by dkv_compact_alloc for granted
-                                  ones, read by dkv_quant_write(DECODE) instead of the tables */
+  int64_t off_qpid;            /* int32[units][4] {page of t_c's slot (= the victim's KV_h page when it is
+                                  downgraded), page of a downgraded victim's KV_l slot, the request length N
+                                  when it is ACTIVE else 0, 0}: written by dkv_classify(DECODE) (existing pages,
+                                  N) and by dkv_compact_alloc (granted pages), read by dkv_quant_write(DECODE)
+                                  instead of the tables and the request state */
   int64_t off_tc_scratch;      /* dkv_attend_tc: 2 x 592 buffers of (max_seq_len rounded to 32, + 64) * (4 if
                                   q_per_kv <= 4 else 8) fp32 logit rows, two per persistent CTA (0 bytes when
                                   q_per_kv = 0 or with the FP16 tier) */

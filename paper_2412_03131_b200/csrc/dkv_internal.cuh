@@ -108,7 +108,8 @@ struct PoolDev {
   int32_t tc_slots, tc_slot_rows;
   int32_t use_head_alpha;   // 1: head_alpha replaces alpha_h / alpha_l
   int32_t prefill_wf;   // dkv_config_t.prefill_workflow
-  int2* qpid;           // [U] {t_c's page, downgraded victim's KV_l page} for dkv_quant_write(DECODE)
+  int4* qpid;           // [U] {t_c's page, downgraded victim's KV_l page, N if the request is ACTIVE else 0, 0}
+                        // for dkv_quant_write(DECODE), written by dkv_classify(DECODE) (+ granted pages by compact)
   int32_t pdl;          // launch option: 1 = programmatic dependent launch (decode-step CUDA graphs)
   // NEXT-4 three-level tier FP16-K8V4-K4V2 (readings Q38-Q44)
   int32_t top;          // 1: the FP16 class TOP above High

@@ -76,7 +76,10 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   // sticky error at entry (Q36: one snapshot per call; classify kernels never write `status`): the unit's
   // decision is the empty one, nothing else happens
   if (dead) {
-    if (lane == 0) reinterpret_cast<int4*>(dec)[u] = make_int4(0, -1, -1, -1);
+    if (lane == 0) {
+      reinterpret_cast<int4*>(dec)[u] = make_int4(0, -1, -1, -1);
+      p.qpid[u] = make_int4(-1, -1, 0, 0);
+    }
     return;
   }
   if (u < (p.U + 31) / 32 && lane == 0) {
@@ -91,9 +94,11 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   bool scan = false;
   int cls = DKV_CLS_NONE, n = 0, nh = 0, nl = 0;
   float sc = 0.0f, th = 0.0f, tl = 0.0f, tt = 0.0f;
+  int nlive = 0;                                                 // N if the request is ACTIVE (for quant_write)
   {
     const int8_t st = p.req_state[r];
     const int N = p.seq_len[r] + 1;                              // Q3: includes this step's token
+    nlive = st == DKV_REQ_ACTIVE ? N : 0;
     // t_c's significance: given, or (NEXT-2, cand_sig NULL) the running mean kept for its window slot
     const float s_in = cand_sig ? cand_sig[u]
                                 : (p.W > 0 && N - 1 - p.W >= 0 ? p.win_sig[(size_t)u * p.W + (N - 1 - p.W) % p.W] : 0.0f);
@@ -292,6 +297,8 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   // victim's KV_h page when the victim is downgraded, since t_c takes its slot, Q8) and the KV_l page a
   // downgraded victim moves to.  A page the growing section receives this step is not known yet: -1 here,
   // written by dkv_compact_alloc when it grants it.  The scanned section's IDs are in shared memory already.
+  // The record also carries the request length (0: not ACTIVE), so quant_write reads no request state.
+  if (!scan) p.qpid[u] = make_int4(-1, -1, nlive, 0);
   if (scan) {
     const bool hi = cls == DKV_CLS_HIGH, top = TOP && cls == DKV_CLS_TOP;
     const int C = top ? p.Ct : (hi ? p.Ch : p.Cl);
@@ -304,7 +311,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
     }
     if (v_action == DKV_V_DOWN && !demand)                      // the destination section's tail page
       pb = grow == DKV_GROW_HIGH ? __ldg(trow + nh / p.Ch) : __ldg(trow + p.L - 1 - nl / p.Cl);
-    p.qpid[u] = make_int2(pa, pb);
+    p.qpid[u] = make_int4(pa, pb, nlive, 0);
 #if DKV_CD_PREFETCH
     if (v_action == DKV_V_DOWN) {                                // warm L2 with the victim's record (read by quant_write)
       const ClassGeom g = top ? p.gt : p.g[1];

@@ -241,6 +241,9 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
       }
     }
     if (fr != 0) { p.n_h[u] = 0; p.n_l[u] = 0; if (p.top) p.n_t[u] = 0; }
+    // a request freed after this step's dkv_classify (the OOM recovery of dkv.h) is no longer live for the
+    // following dkv_quant_write, which takes liveness from the unit's qpid record
+    if (phase == DKV_PHASE_DECODE && st == DKV_REQ_PENDING_FREE) reinterpret_cast<int32_t*>(p.qpid + u)[2] = 0;
   }
   __syncthreads();
 

@@ -13,12 +13,12 @@
 // What sets the duration (measured, profiles/): the unit count, not the bytes — each unit is a chain of
 // dependent memory round trips, followed by the per-vector scalar work (min/max reduction, two correctly
 // rounded divisions) that a group does once for all its lanes (several units per warp amortise it):
-//   A. everything indexed by u alone: decision word, the page IDs it touches (qpid: dkv_classify recorded
-//      the existing pages, dkv_compact_alloc the granted one — in round 1 this kernel read them from the
-//      tables, a second dependent trip), s_c, t_c's window row (its slot follows from the request length,
-//      which comes from a per-CTA shared-memory copy: thousands of warps reading the same word queue at one
-//      L2 slice) and the new token's K/V;
-//   C. the victim's K8V4 record (downgrades only), addressed by the page ID from A.
+//   A. everything indexed by u alone: decision word, the unit's qpid record (dkv_classify recorded the
+//      existing pages it touches and the request length, dkv_compact_alloc the granted page — in round 1 this
+//      kernel read the pages from the tables and the length from the request state, two more dependent
+//      trips), s_c and the new token's K/V;
+//   B + C. t_c's window row (its slot follows from the length) and the victim's K8V4 record (downgrades
+//      only, addressed by the page ID from A), in flight together.
 // The window push is issued only after t_c's row has been consumed: a store issued while the same line's
 // load miss is outstanding takes a slow path in L2 (measured: 73 -> 26 us at the Llama-3-8B config).
 // Quantizer arithmetic is the oracle's (c.5 / Q16), expressed as in dkv_internal.cuh's quant_h16 /
@@ -311,7 +311,6 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
                     const uint16_t* __restrict__ vnew, const float* __restrict__ cand_sig, int u0, int u1) {
   constexpr int EPL = D / G;                             // elements per lane per vector
   constexpr int UPC = kQDThreads / G;                    // units per CTA per iteration
-  extern __shared__ __align__(16) uint8_t qd_smem[];
   __shared__ __align__(16) uint16_t s_new[2][kQDThreads * EPL];   // the new token's K / V rows, this lane's part
   __shared__ int32_t s_status;
   const int lane = threadIdx.x & 31;
@@ -326,7 +325,13 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
     s_rec = ld_volatile(&p.ctrl->rec_deferred);          // compact_alloc left this step's recycle copies to us
     s_end0 = ld_volatile(&p.ctrl->rec_end0);
   }
-  const ReqCache rc = load_req_cache(p, qd_smem);
+  // the first unit's record and decision are u-indexed: in flight across the barrier
+  int ub = blockIdx.x;
+  int4 dw = make_int4(0, -1, -1, -1), qp = make_int4(-1, -1, 0, 0);
+  {
+    const int uf = u0 + ub * UPC + threadIdx.x / G;
+    if (uf < u1) { dw = __ldg(reinterpret_cast<const int4*>(dec) + uf); qp = __ldg(p.qpid + uf); }
+  }
   __syncthreads();
   const bool dead = s_status != 0;                       // error at entry: no quantization, no window push
   const bool rec_on = s_rec != 0;
@@ -334,12 +339,14 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
   uint16_t* const my_nk = &s_new[0][threadIdx.x * EPL];
   uint16_t* const my_nv = &s_new[1][threadIdx.x * EPL];
 
-  for (int ub = blockIdx.x; u0 + ub * UPC < u1; ub += gridDim.x) {   // units [u0, u1)
+  for (; u0 + ub * UPC < u1; ub += gridDim.x) {         // units [u0, u1)
     const int u = u0 + ub * UPC + threadIdx.x / G;
     if (u >= u1) break;                                  // whole groups leave together (last block only)
-    const int r = fdiv(p.div_LyH, u);
-    const int8_t st = rc.st[r];
-    const bool live = st == DKV_REQ_ACTIVE;
+    if (ub != (int)blockIdx.x) { dw = __ldg(reinterpret_cast<const int4*>(dec) + u); qp = __ldg(p.qpid + u); }
+    // the request length (already including this step's token: dkv_compact_alloc advanced it), 0 when the
+    // request is not ACTIVE — recorded by dkv_classify in the unit's qpid record, so no request state is read
+    const int N = qp.z;
+    const bool live = N > 0;
     if (!live) {
       // a unit of a request this step's dkv_compact_alloc recycled without copying (decode fast path): its
       // page IDs go to the ring here, at the offsets the scan assigned (Q13 order), and its slots are cleared
@@ -348,12 +355,9 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
     }
     if (dead) continue;
 
-    // ---- A: every load indexed by u (or by the request length, from shared memory) — all in flight together:
-    // the decision, the page IDs it needs (classify / compact_alloc left them in qpid, so no table read),
-    // t_c's significance, t_c's window row, and the new token (straight to shared memory)
-    const int N = rc.len[r];                             // already includes this step's token (compact_alloc)
-    const int4 dw = __ldg(reinterpret_cast<const int4*>(dec) + u);
-    const int2 qp = __ldg(p.qpid + u);
+    // ---- A: the loads indexed by u (the decision and the qpid record, above; t_c's significance and the new
+    // token, straight to shared memory) and, one round trip later, by the request length: t_c's window row —
+    // in flight together with the victim's record (C)
     const float s_in_given = cand_sig ? __ldg(cand_sig + u) : 0.0f;
     stage_row<EPL>(my_nk, knew + (size_t)u * D + q * EPL);
     stage_row<EPL>(my_nv, vnew + (size_t)u * D + q * EPL);
@@ -492,9 +496,9 @@ template <int D, int G>
 static cudaError_t launch_qd(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
                              const float* sig, int u0, int u1, cudaStream_t s) {
   constexpr int units_per_cta = kQDThreads / G;
-  const size_t smem = req_cache_bytes(p.R);
+  const size_t smem = 0;
   static int cap = 0;                                    // persistent grid (per template instance)
-  if (cap == 0) cap = persistent_grid(quant_decode_kernel<D, G>, kQDThreads, req_cache_bytes(kReqSmemMax));
+  if (cap == 0) cap = persistent_grid(quant_decode_kernel<D, G>, kQDThreads, 0);
   if (cap == 0) return cudaErrorUnknown;
   if (u1 <= u0) return cudaSuccess;
   const int need = (u1 - u0 + units_per_cta - 1) / units_per_cta;

@@ -128,7 +128,7 @@ bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
     Lo.off_att_scratch = take(need ? (int64_t)kAttSlots * (GP + 2) * Mp * 4 : 0);
   }
   Lo.off_tc_scratch = take(tc_scratch_needed(c) ? (int64_t)kTcSlots * 2 * tc_slot_rows(c) * tc_gp(c) * 4 : 0);
-  Lo.off_qpid = take(8 * U);
+  Lo.off_qpid = take(16 * U);
   Lo.off_ring = take(4 * P);
   Lo.off_table = take(4 * U * G.L);
   Lo.off_ttable = take(4 * U * G.Lt);
@@ -280,7 +280,7 @@ dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_
   d.rec = (int32_t*)(b + Lo.off_rec);
   d.win_sig = (float*)(b + Lo.off_win_sig);
   d.secmin = (int32_t*)(b + Lo.off_secmin);
-  d.qpid = (int2*)(b + Lo.off_qpid);
+  d.qpid = (int4*)(b + Lo.off_qpid);
   d.top = cfg->top_tier;
   d.alpha_t = cfg->alpha_t;
   d.Lt = G.Lt;
