@@ -308,9 +308,11 @@ __device__ __forceinline__ void recycle_unit(const PoolDev& p, int u, int q, uns
 template <int D, int G>
 __global__ void __launch_bounds__(kQDThreads, DKV_QD_MINB)
 quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uint16_t* __restrict__ knew,
-                    const uint16_t* __restrict__ vnew, const float* __restrict__ cand_sig, int u0, int u1) {
+                    const uint16_t* __restrict__ vnew, const float* __restrict__ cand_sig, int u0, int u1, int upc) {
   constexpr int EPL = D / G;                             // elements per lane per vector
-  constexpr int UPC = kQDThreads / G;                    // units per CTA per iteration
+  // upc <= kQDThreads / G units per CTA per iteration (the launch balances them over the resident CTAs); the
+  // groups beyond upc have no unit
+  const int gslot = threadIdx.x / G;
   __shared__ __align__(16) uint16_t s_new[2][kQDThreads * EPL];   // the new token's K / V rows, this lane's part
   __shared__ int32_t s_status;
   const int lane = threadIdx.x & 31;
@@ -329,8 +331,8 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
   int ub = blockIdx.x;
   int4 dw = make_int4(0, -1, -1, -1), qp = make_int4(-1, -1, 0, 0);
   {
-    const int uf = u0 + ub * UPC + threadIdx.x / G;
-    if (uf < u1) { dw = __ldg(reinterpret_cast<const int4*>(dec) + uf); qp = __ldg(p.qpid + uf); }
+    const int uf = u0 + ub * upc + gslot;
+    if (gslot < upc && uf < u1) { dw = __ldg(reinterpret_cast<const int4*>(dec) + uf); qp = __ldg(p.qpid + uf); }
   }
   __syncthreads();
   const bool dead = s_status != 0;                       // error at entry: no quantization, no window push
@@ -339,8 +341,8 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
   uint16_t* const my_nk = &s_new[0][threadIdx.x * EPL];
   uint16_t* const my_nv = &s_new[1][threadIdx.x * EPL];
 
-  for (; u0 + ub * UPC < u1; ub += gridDim.x) {         // units [u0, u1)
-    const int u = u0 + ub * UPC + threadIdx.x / G;
+  for (; gslot < upc && u0 + ub * upc < u1; ub += gridDim.x) {   // units [u0, u1)
+    const int u = u0 + ub * upc + gslot;
     if (u >= u1) break;                                  // whole groups leave together (last block only)
     if (ub != (int)blockIdx.x) { dw = __ldg(reinterpret_cast<const int4*>(dec) + u); qp = __ldg(p.qpid + u); }
     // the request length (already including this step's token: dkv_compact_alloc advanced it), 0 when the
@@ -501,9 +503,13 @@ static cudaError_t launch_qd(const PoolDev& p, const dkv_decision_t* dec, const 
   if (cap == 0) cap = persistent_grid(quant_decode_kernel<D, G>, kQDThreads, 0);
   if (cap == 0) return cudaErrorUnknown;
   if (u1 <= u0) return cudaSuccess;
-  const int need = (u1 - u0 + units_per_cta - 1) / units_per_cta;
+  // every resident CTA takes the same number of units (at most units_per_cta): 16384 units over 592 CTAs is 28
+  // per CTA and 112 per SM, where full 32-unit CTAs put 128 units on some SMs and 96 on others
+  int upc = (u1 - u0 + cap - 1) / cap;
+  if (upc > units_per_cta) upc = units_per_cta;
+  const int need = (u1 - u0 + upc - 1) / upc;
   return launch_ex(quant_decode_kernel<D, G>, dim3(need < cap ? need : cap), dim3(kQDThreads), smem, s, p.pdl != 0, p,
-                   dec, k, v, sig, u0, u1);
+                   dec, k, v, sig, u0, u1, upc);
 }
 
 cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
