@@ -147,3 +147,12 @@ def test_attention_tc_long_context():
     snap = g.snapshot()
     _, og, pg = g.attend_tc(q, want_out=True, want_probs=True)
     eq1.check_units(snap, g.geom, g.L, scn.W, scn.d, scn.LyH, q, og, pg, list(range(scn.U)), where="tc 30k")
+
+
+@pytest.mark.parametrize("W", [0, 24])
+def test_attention_tc_window_not_a_chunk_multiple(W):
+    """A window ring of W = 24 slots (one full and one partial 16-slot MMA chunk; contexts shorter than W leave slots
+    empty) and no window at all (W = 0: t_c is the new token), against Eq. 1 in float64 over a lifecycle"""
+    scn = H.TINY.replace(R=3, Ly=2, H=2, d=128, M=600, W=W, P=6000, seed=41 + W, q_per_kv=4, alpha_h=1.0,
+                         alpha_l=0.02)
+    _run(scn, [300, 11, 90], steps=5, seed=W)
