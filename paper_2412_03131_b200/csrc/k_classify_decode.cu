@@ -180,45 +180,38 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
       const int ix = pow2 ? (s0 & (C - 1)) : s0 % C;
       return base_sc + (size_t)s_pid[pg] * (size_t)p.page_bytes + 4 * ix;
     };
-    // per lane: the smallest score seen, the first vector holding it (its first slot and its four values) and
-    // whether an earlier or later vector holds it too; the slot and the ties inside that vector are resolved
-    // once after the loop (per vector: a 3-way minimum, two compares and selects — no position search)
     uint32_t best = 0xFFFFFFFFu;
-    int bs0 = -1;
-    uint32_t bv0 = 0xFFFFFFFFu, bv1 = 0xFFFFFFFFu, bv2 = 0xFFFFFFFFu, bv3 = 0xFFFFFFFFu;
-    bool multi = false;
+    int bslot = -1;
+    bool tie = false;                                            // best may be held by more than one slot
     for (int base = 0; base < n; base += 128 * kCV) {
-      const bool full = base + 128 * kCV <= n;                   // warp-uniform: no slot of the batch is past n
       uint4 v[kCV];
 #pragma unroll
       for (int j = 0; j < kCV; j++) {
         const int s0 = base + j * 128 + 4 * lane;
         v[j] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        if (full || s0 < n) v[j] = CD_LD(vec_addr(s0));
+        if (s0 < n) v[j] = CD_LD(vec_addr(s0));
       }
 #pragma unroll
       for (int j = 0; j < kCV; j++) {
         const int s0 = base + j * 128 + 4 * lane;
         uint32_t a = v[j].x, b = v[j].y, c = v[j].z, d = v[j].w;
-        if (!full && s0 + 3 >= n) {                              // tail vector: mask slots >= n
+        if (s0 + 3 >= n) {                                       // tail vector: mask slots >= n
           a = s0 < n ? a : 0xFFFFFFFFu;
           b = s0 + 1 < n ? b : 0xFFFFFFFFu;
           c = s0 + 2 < n ? c : 0xFFFFFFFFu;
           d = 0xFFFFFFFFu;
         }
         const uint32_t m4 = min(min(a, b), min(c, d));
-        const bool upd = m4 < best;
-        multi = upd ? false : (multi || (m4 == best && m4 != 0xFFFFFFFFu));
-        best = upd ? m4 : best;
-        bs0 = upd ? s0 : bs0;
-        bv0 = upd ? a : bv0; bv1 = upd ? b : bv1; bv2 = upd ? c : bv2; bv3 = upd ? d : bv3;
+        if (m4 <= best && m4 != 0xFFFFFFFFu) {                   // rare after the first steps
+          if (m4 == best) {
+            tie = true;
+          } else {
+            best = m4;
+            bslot = s0 + (a == m4 ? 0 : (b == m4 ? 1 : (c == m4 ? 2 : 3)));
+            tie = ((a == m4) + (b == m4) + (c == m4) + (d == m4)) > 1;
+          }
+        }
       }
-    }
-    int bslot = -1;
-    bool tie = multi;                                            // best may be held by more than one slot
-    if (best != 0xFFFFFFFFu) {
-      bslot = bs0 + (bv0 == best ? 0 : (bv1 == best ? 1 : (bv2 == best ? 2 : 3)));
-      tie = tie || ((bv0 == best) + (bv1 == best) + (bv2 == best) + (bv3 == best)) > 1;
     }
     const uint32_t m = __reduce_min_sync(kFull, best);
     const unsigned holders = __ballot_sync(kFull, best == m);
