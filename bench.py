@@ -455,6 +455,26 @@ def run_ours(args, rank, world, local):
     st, stats = pool.query()
     assert st == 0, f"device status {st} after e2e"
     seq[active] += args.steps
+    # the host link in the same run: the step's K/V bytes alone (one pinned H2D copy), and a 256 MiB copy
+    link = {}
+    kv_dev = torch.empty_like(pin_kv[0], device=dev)
+    big_h = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+    big_d = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for name, (src, dst) in (("kv", (pin_kv[0], kv_dev)), ("big", (big_h, big_d))):
+        ts = []
+        for i in range(4):
+            torch.cuda.synchronize()
+            e0, e1 = ev(), ev()
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            if i:
+                ts.append(e0.elapsed_time(e1) * 1e3)
+        link[name] = statistics.mean(ts)
+    h2d_link = {"step_kv_copy_us": round(link["kv"], 1), "step_kv_bytes": int(pin_kv[0].numel() * 2),
+                "link_gbs_256mib": round((256 << 20) / (link["big"] * 1e-6) / 1e9, 1)}
+    del big_h, big_d, kv_dev
 
     # ---------------- NEXT-2: decode steps driven by the attention kernel's significance
     next2 = None
@@ -749,7 +769,8 @@ def run_ours(args, rank, world, local):
                             "algorithmic_bytes": int(statistics.mean(cls_bytes)),
                             "traffic": traffic("classify_decode_kernel"), "traffic_unit": "bytes per launch"},
         "e2e": {"value": round(e2e_mean, 3), "unit": E2E_UNIT,
-                "h2d_bytes_per_step": wl.U * (4 + 2 * 2 * c["d"]), "d2h_bytes_per_step": wl.U * 16},
+                "h2d_bytes_per_step": wl.U * (4 + 2 * 2 * c["d"]), "d2h_bytes_per_step": wl.U * 16,
+                "h2d_link": h2d_link},
         "graph": graph if GS >= 10 else None,
         "next2": next2,
         # §8e: the per-step MIN all-reduce of the admission counters (N > 1): its latency on the side stream and
