@@ -426,6 +426,10 @@ def run_ours(args, rank, world, local):
     assert st == 0, f"device status {st} after decode"
     wall = time.time() - t_wall0
     clocks = sampler.stop()
+    # validation, outside every timed region: the device audit of the pool's invariants after the decode phase
+    audit = pool.audit()
+    audit["sound"] = bool(audit["used_pages"] + audit["free_pages"] == c["P"] and
+                          all(v == 0 for k, v in audit.items() if k not in ("used_pages", "free_pages")))
 
     # ---------------- e2e: same decode step through the C ABI with host buffers
     e2e_us = []
@@ -771,6 +775,7 @@ def run_ours(args, rank, world, local):
         "e2e": {"value": round(e2e_mean, 3), "unit": E2E_UNIT,
                 "h2d_bytes_per_step": wl.U * (4 + 2 * 2 * c["d"]), "d2h_bytes_per_step": wl.U * 16,
                 "h2d_link": h2d_link},
+        "audit": audit,
         "graph": graph if GS >= 10 else None,
         "next2": next2,
         # §8e: the per-step MIN all-reduce of the admission counters (N > 1): its latency on the side stream and

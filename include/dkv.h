@@ -231,6 +231,20 @@ dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* 
  * off_tc_scratch (a unit's significance pass runs during the CTA's next unit). */
 dkv_status_t dkv_attend_tc(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* d_probs, dkv_stream_t s);
 
+/* Debug audit of the pool's invariants on the device (SURVEY §8 audit row): the memory layout of P:466-500
+ * — every page of the unified pool is in the circular free list's free region [start, start + free) or in exactly
+ * one occupied page-table slot; a unit's high pages fill its table row left to right and its low pages right to
+ * left, so its occupied slots are exactly [0, ceil(n_h/C_h)) and [L - ceil(n_l/C_l), L) (and
+ * [0, ceil(n_t/C_t)) of the NEXT-4 TOP table) and every other slot is -1 — and, for ACTIVE requests, every
+ * stored position is unique within its unit and below N - W (a stored token has left the recent window).
+ * d_scratch: caller-owned device buffer of at least num_pages uint32 (overwritten, a per-page histogram).
+ * d_result: caller-owned device int64[8], overwritten with {pages owned more than once, pages owned by nobody,
+ *   bad slots (an occupied slot or free-region entry outside [0, P), or an unoccupied slot != -1), used pages
+ *   (occupied slots), free pages, duplicate stored positions, stored positions out of range, units whose page
+ *   counts exceed their table}; a sound pool has zeros except used + free = num_pages.
+ * Asynchronous on `s`; between sequences only (DKV_ERR_STATE otherwise); modifies nothing of the pool. */
+dkv_status_t dkv_audit(dkv_pool_t p, uint32_t* d_scratch, int64_t* d_result, dkv_stream_t s);
+
 /* NEXT-4 — per-head thresholds ("a shared set of thresholds for all attention heads" is the
  * paper's choice; per-head thresholds its stated extension; reading Q35).  h_alpha_h / h_alpha_l: host
  * arrays of num_layers * num_kv_heads finite values >= 0 in (layer, this pool's head) order; unit u uses

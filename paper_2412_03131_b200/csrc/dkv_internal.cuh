@@ -1009,6 +1009,8 @@ cudaError_t launch_attend(const PoolDev& p, const uint16_t* q, float* out, float
 size_t attend_smem_bytes(const PoolDev& p, int TS);
 size_t attend_long_smem_bytes(const PoolDev& p);
 cudaError_t launch_attend_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s);
+constexpr int kAuditResults = 8;
+cudaError_t launch_audit(const PoolDev& p, uint32_t* hist, int64_t* res, cudaStream_t s);
 size_t attend_tc_smem_bytes(const PoolDev& p);
 bool attend_tc_supported(const PoolDev& p);
 cudaError_t launch_prefill_conservative(const PoolDev& p, cudaStream_t s);

@@ -497,6 +497,12 @@ dkv_status_t dkv_attend_tc(dkv_pool_t p, const uint16_t* d_q, float* d_out, floa
   return launch_attend_tc(p->dev, d_q, d_out, d_probs, (cudaStream_t)s) == cudaSuccess ? DKV_OK : DKV_ERR_CUDA;
 }
 
+dkv_status_t dkv_audit(dkv_pool_t p, uint32_t* d_scratch, int64_t* d_result, dkv_stream_t s) {
+  if (!p || !d_scratch || !d_result) return DKV_ERR_INVALID_ARG;
+  if (p->seq != SEQ_IDLE) return DKV_ERR_STATE;                // between sequences only
+  return launch_audit(p->dev, d_scratch, d_result, (cudaStream_t)s) == cudaSuccess ? DKV_OK : DKV_ERR_CUDA;
+}
+
 dkv_status_t dkv_set_head_thresholds(dkv_pool_t p, const float* h_alpha_h, const float* h_alpha_l, dkv_stream_t s) {
   if (!p) return DKV_ERR_INVALID_ARG;
   if (p->seq != SEQ_IDLE) return DKV_ERR_STATE;

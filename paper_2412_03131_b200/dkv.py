@@ -28,7 +28,7 @@ EXPORTED = ("dkv_arena_bytes", "dkv_pool_layout", "dkv_pool_init", "dkv_pool_des
             "dkv_compact_alloc", "dkv_quant_write", "dkv_free", "dkv_pool_query", "dkv_pool_stats_device_ptr",
             "dkv_status_string", "dkv_attend", "dkv_set_head_thresholds", "dkv_decode_stage_bytes",
             "dkv_decode_step_host", "dkv_decode_graph_create", "dkv_decode_graph_launch",
-            "dkv_decode_graph_kernel_ms", "dkv_decode_graph_destroy", "dkv_attend_tc")
+            "dkv_decode_graph_kernel_ms", "dkv_decode_graph_destroy", "dkv_attend_tc", "dkv_audit")
 
 
 class DkvError(RuntimeError):
@@ -98,6 +98,7 @@ _lib.dkv_quant_write.argtypes = [_vp, C.c_int32, _vp, _vp, _vp, C.c_int64, _vp, 
 _lib.dkv_free.argtypes = [_vp, _vp, C.c_int32, _vp]
 _lib.dkv_attend.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _lib.dkv_attend_tc.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_lib.dkv_audit.argtypes = [_vp, _vp, _vp, _vp]
 _lib.dkv_set_head_thresholds.argtypes = [_vp, _vp, _vp, _vp]
 _lib.dkv_pool_query.argtypes = [_vp, _P(dkv_stats_t), _vp]
 _lib.dkv_decode_stage_bytes.argtypes = [_vp]
@@ -114,7 +115,7 @@ _lib.dkv_status_string.restype = C.c_char_p
 for _f in ("dkv_pool_layout", "dkv_pool_init", "dkv_pool_destroy", "dkv_classify", "dkv_compact_alloc",
            "dkv_quant_write", "dkv_free", "dkv_pool_query", "dkv_attend", "dkv_set_head_thresholds",
            "dkv_decode_step_host", "dkv_decode_graph_create", "dkv_decode_graph_launch", "dkv_decode_graph_kernel_ms",
-           "dkv_decode_graph_destroy", "dkv_attend_tc"):
+           "dkv_decode_graph_destroy", "dkv_attend_tc", "dkv_audit"):
     getattr(_lib, _f).restype = C.c_int32
 
 
@@ -207,6 +208,10 @@ def dkv_attend(pool, d_q, d_out, d_probs, stream=None) -> int:
 
 def dkv_attend_tc(pool, d_q, d_out, d_probs, stream=None) -> int:
     return _check("dkv_attend_tc", _lib.dkv_attend_tc(pool, _dev(d_q), _dev(d_out), _dev(d_probs), _stream(stream)))
+
+
+def dkv_audit(pool, d_scratch, d_result, stream=None) -> int:
+    return _check("dkv_audit", _lib.dkv_audit(pool, _dev(d_scratch), _dev(d_result), _stream(stream)))
 
 
 def dkv_set_head_thresholds(pool, alpha_h, alpha_l, stream=None) -> int:

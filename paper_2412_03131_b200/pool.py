@@ -82,6 +82,22 @@ class Pool:
         """NEXT-2 on tensor cores (dkv_attend_tc): same buffers as attend()"""
         return _d.dkv_attend_tc(self.handle, q, out, probs, stream or self.stream)
 
+    AUDIT_KEYS = ("owned_twice", "unowned", "bad_slots", "used_pages", "free_pages", "dup_positions",
+                  "positions_out_of_range", "over_capacity")
+
+    def audit(self, stream=None):
+        """dkv_audit: the pool's invariants checked on the device; returns a dict of AUDIT_KEYS (sound: all zero
+        except used_pages + free_pages == num_pages).  Synchronises the stream."""
+        s = stream or self.stream
+        if getattr(self, "_audit_buf", None) is None:
+            self._audit_buf = (torch.empty(int(self.cfg.num_pages), dtype=torch.int32, device=self.device),
+                               torch.empty(8, dtype=torch.int64, device=self.device))
+        hist, res = self._audit_buf
+        _d.dkv_audit(self.handle, hist, res, s)
+        torch.cuda.synchronize(self.device)
+        vals = res.cpu().tolist()
+        return dict(zip(self.AUDIT_KEYS, vals))
+
     def set_head_thresholds(self, alpha_h, alpha_l, stream=None):
         """NEXT-4: per-(layer, head) thresholds (host sequences of Ly*H floats), or None for the pool-wide pair"""
         return _d.dkv_set_head_thresholds(self.handle, alpha_h, alpha_l, stream or self.stream)

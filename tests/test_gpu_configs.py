@@ -107,6 +107,10 @@ def test_fragmentation_stress(workflow):
         act = life.state == H.REQ_ACTIVE
         gen_left[act] -= 1
         _check(o, g, f"step {step}", decs, pages=step % 20 == 0)
+        if step % 50 == 0:                                      # the device audit agrees (dkv_audit)
+            a = g.pool.audit()
+            assert a["used_pages"] + a["free_pages"] == scn.P and a["used_pages"] == scn.P - o.pool.free, (step, a)
+            assert all(v == 0 for k, v in a.items() if k not in ("used_pages", "free_pages")), (step, a)
         done = [r for r in range(scn.R) if life.state[r] == H.REQ_ACTIVE and gen_left[r] <= 0]
         rng.shuffle(done)
         if done:
