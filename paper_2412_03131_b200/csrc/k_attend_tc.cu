@@ -421,6 +421,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   __shared__ int s_slot[2];
   __shared__ __align__(16) float s_sl[2][kTcThreads][GP];         // significance pass: staged logit rows
   __shared__ __align__(8) float s_ss[2][kTcThreads][2];           //   ... and (score, position bits)
+  __shared__ unsigned long long s_sa[2][kTcThreads];             //   ... and the score's address
   __shared__ __align__(8) uint64_t s_bar[kTcWarps][kTcStages];   // per-warp stage mbarriers (bulk copies)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = lane >> 2, tig = lane & 3;
@@ -460,6 +461,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
       const int k = hi ? row >> 4 : sp.ph + (rr >> 5), j2 = hi ? row & 15 : rr & 31;
       const ClassGeom& gg = hi ? gh : gl;
       const uint8_t* pg = p.pages + (size_t)pidb[sp.buf * LP + k] * (size_t)p.page_bytes;
+      s_sa[sl][tid] = reinterpret_cast<unsigned long long>(pg + gg.off_score + 4 * j2);
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ss_u32 + sl * kSsStride), "l"(pg + gg.off_score + 4 * j2) : "memory");
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ss_u32 + sl * kSsStride + 4), "l"(pg + gg.off_pos + 4 * j2) : "memory");
     } else {
@@ -485,11 +487,11 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     float sg = s_ss[sl][tid][0];
     const int pos = stored ? __float_as_int(s_ss[sl][tid][1]) : sp.N - sp.nw + (row - sp.wb);
     const int c = sp.N - 2 - pos;
-    if (c >= 0) sg = (sg * (float)c + a) * __frcp_rn((float)(c + 1));
+    if (c >= 0) sg = __fdividef(fmaf(sg, (float)c, a), (float)(c + 1));   // (a tolerance path: approximate division)
     if (stored) {
-      const int k = hi ? row >> 4 : sp.ph + (rr >> 5), j2 = hi ? row & 15 : rr & 31;
-      uint8_t* pg = p.pages + (size_t)pidb[sp.buf * LP + k] * (size_t)p.page_bytes;
-      if (c >= 0) *reinterpret_cast<float*>(pg + (hi ? gh.off_score : gl.off_score) + 4 * j2) = sg;
+      // the score's address, left by sig_issue in the staging slot (no second page-ID lookup)
+      float* sp_addr = reinterpret_cast<float*>(s_sa[sl][tid]);
+      if (c >= 0) *sp_addr = sg;
       if (probs) probs[(size_t)sp.u * p.M + (hi ? rr : sp.nh + rr)] = a;
       const unsigned long long key = ((unsigned long long)__float_as_uint(sg) << 32) | (uint32_t)pos;
       if (hi) {
