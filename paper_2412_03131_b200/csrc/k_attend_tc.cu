@@ -415,7 +415,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   extern __shared__ __align__(128) uint8_t tc_smem[];
   __shared__ float s_mw[kTcWarps][8], s_zw[kTcWarps][8], s_zsw[kTcWarps][8];
   __shared__ float s_fw[kTcWarps][8];
-  __shared__ float s_M[2][8], s_iZ[2][8];                         // per logit buffer: the unit's maxima and 1/Z
+  __shared__ float s_C[2][8], s_iZ[2][8];                         // per logit buffer: M + log2 Z per head, and 1/Z
   __shared__ TcSigUnit s_prev;
   __shared__ unsigned long long s_min[2];
   __shared__ int s_slot[2];
@@ -481,9 +481,11 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
     const bool stored = row < sp.wb, hi = row < sp.lo0;
     const int rr = hi ? row : row - sp.lo0;
     if (stored && rr >= (hi ? sp.nh : sp.nl)) return;
-    float a = 0.0f;
+    // a = max_h 2^(l_h - M_h) / Z_h = 2^(max_h (l_h - C_h)), C_h = M_h + log2 Z_h: one exp2 per token
+    float xm = -INFINITY;
 #pragma unroll
-    for (int h = 0; h < G; h++) a = fmaxf(a, ex2(s_sl[sl][tid][h] - s_M[sp.buf][h]) * s_iZ[sp.buf][h]);
+    for (int h = 0; h < G; h++) xm = fmaxf(xm, s_sl[sl][tid][h] - s_C[sp.buf][h]);
+    const float a = ex2(xm);
     float sg = s_ss[sl][tid][0];
     const int pos = stored ? __float_as_int(s_ss[sl][tid][1]) : sp.N - sp.nw + (row - sp.wb);
     const int c = sp.N - 2 - pos;
@@ -671,7 +673,7 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
         s_fw[w][tid] = f;
         Z = fmaf(f, s_zw[w][tid], Z);
       }
-      s_M[buf][tid] = M;
+      s_C[buf][tid] = Z > 0.0f ? M + log2f(Z) : INFINITY;
       s_iZ[buf][tid] = Z > 0.0f ? 1.0f / Z : 0.0f;
     }
     if (tid == 0) s_prev = TcSigUnit{u, N, nh, nl, ph, lo0, wb, nw, nh + nl, wb + nw, buf};   // pending now
