@@ -183,7 +183,14 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
     uint32_t best = 0xFFFFFFFFu;
     int bslot = -1;
     bool tie = false;                                            // best may be held by more than one slot
-    for (int base = 0; base < n; base += 128 * kCV) {
+    // long-section / tie-heavy form (the full-register instantiation): which of this lane's vectors (by
+    // iteration index, 128 per lane at most) hold its running minimum, so that the tie-breaking pass reloads
+    // only those — one round trip instead of a second pass over the whole section
+    constexpr bool kMask = MINB == 1;
+    uint64_t tlo = 0, thi = 0;
+    bool ovf = false;
+    int it0 = 0;
+    for (int base = 0; base < n; base += 128 * kCV, it0 += kCV) {
       uint4 v[kCV];
 #pragma unroll
       for (int j = 0; j < kCV; j++) {
@@ -203,6 +210,13 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
         }
         const uint32_t m4 = min(min(a, b), min(c, d));
         if (m4 <= best && m4 != 0xFFFFFFFFu) {                   // rare after the first steps
+          if constexpr (kMask) {
+            const int it = it0 + j;
+            const uint64_t blo = it < 64 ? 1ull << (it & 63) : 0ull, bhi = it >= 64 && it < 128 ? 1ull << (it & 63) : 0ull;
+            ovf = ovf || it >= 128;
+            if (m4 == best) { tlo |= blo; thi |= bhi; }
+            else { tlo = blo; thi = bhi; }
+          }
           if (m4 == best) {
             tie = true;
           } else {
@@ -218,6 +232,38 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
     const bool any_tie = __any_sync(kFull, best == m && tie);
     if (__popc(holders) == 1 && !any_tie) {
       vs = __shfl_sync(kFull, bslot, __ffs(holders) - 1);
+    } else if (kMask && !__any_sync(kFull, ovf)) {
+      // tie-breaking from the recorded vectors: each holder lane reloads its vectors that hold m (scores and
+      // the same 4 slots' positions, 4 vectors in flight at a time); the oldest position wins (Q6)
+      const int off_pos = (TOP && cls == DKV_CLS_TOP) ? p.gt.off_pos : (cls == DKV_CLS_HIGH ? p.g[1].off_pos : p.g[2].off_pos);
+      uint64_t mlo = best == m ? tlo : 0ull, mhi = best == m ? thi : 0ull;
+      int32_t bp = 0x7FFFFFFF;
+      int bs = -1;
+      while (__any_sync(kFull, (mlo | mhi) != 0ull)) {
+        int s0k[4];
+        uint4 v[4], q[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          int it = -1;
+          if (mlo) { it = __ffsll((long long)mlo) - 1; mlo &= mlo - 1; }
+          else if (mhi) { it = 64 + __ffsll((long long)mhi) - 1; mhi &= mhi - 1; }
+          s0k[k] = it < 0 ? -1 : (it / kCV) * (128 * kCV) + (it % kCV) * 128 + 4 * lane;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          if (s0k[k] >= 0) { v[k] = CD_LD(vec_addr(s0k[k])); q[k] = ld_nc_v4(vec_addr(s0k[k]) - off_score + off_pos); }
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          if (s0k[k] < 0) continue;
+          const uint32_t e4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+          const int32_t p4[4] = {(int32_t)q[k].x, (int32_t)q[k].y, (int32_t)q[k].z, (int32_t)q[k].w};
+#pragma unroll
+          for (int e = 0; e < 4; e++)
+            if (s0k[k] + e < n && e4[e] == m && p4[e] < bp) { bp = p4[e]; bs = s0k[k] + e; }
+        }
+      }
+      const uint32_t mp = __reduce_min_sync(kFull, (uint32_t)bp);
+      vs = __shfl_sync(kFull, bs, __ffs(__ballot_sync(kFull, (uint32_t)bp == mp && bs >= 0)) - 1);
     } else {
       // exact pass: among the slots scoring m, the oldest position wins (Q6).  Batched: kXV score vectors
       // in flight per lane, then one 16-B position vector (the same 4 slots' positions, contiguous in the
@@ -354,7 +400,9 @@ static cudaError_t launch_cd(const PoolDev& p, const float* sig, dkv_decision_t*
 // register budget: their scans take many batches and, when the minimum is shared, the exact pass, which
 // spills at the 10-CTA budget (measured: profiles/r1j_classify_long_ab.log)
 cudaError_t launch_classify_decode(const PoolDev& p, const float* sig, dkv_decision_t* dec, int max_len, cudaStream_t s) {
-  if (max_len > DKV_CD_LONG_LEN) return launch_cd<1>(p, sig, dec, s);
+  // the full-register form also when nothing is pruned (alpha_l = 0): the low sections then hold many exact-zero
+  // significances, a shared minimum, and that form breaks the tie from the vectors it recorded
+  if (max_len > DKV_CD_LONG_LEN || (p.alpha_l == 0.0f && !p.use_head_alpha)) return launch_cd<1>(p, sig, dec, s);
   return launch_cd<DKV_CD_MINB>(p, sig, dec, s);
 }
 
