@@ -30,6 +30,9 @@ namespace dkv {
 #ifndef DKV_CD_KCV
 #define DKV_CD_KCV 8
 #endif
+#ifndef DKV_CD_KCV_LONG
+#define DKV_CD_KCV_LONG 8   // the same for the full-register form (measured: 16 and 24 lose, profiles/r2t_classify_long_ab.log)
+#endif
 constexpr int kCDWarps = DKV_CD_WARPS;     // units (warps) per CTA
 constexpr int kCV = DKV_CD_KCV;            // 16-B score vectors per lane per batch (1024 slots per batch)
 constexpr int kXV = 4;                     // the same for the exact (tie-breaking) pass, which also holds positions
@@ -187,19 +190,20 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
     // iteration index, 128 per lane at most) hold its running minimum, so that the tie-breaking pass reloads
     // only those — one round trip instead of a second pass over the whole section
     constexpr bool kMask = MINB == 1;
+    constexpr int KV = MINB == 1 ? DKV_CD_KCV_LONG : kCV;        // score vectors per lane per batch
     uint64_t tlo = 0, thi = 0;
     bool ovf = false;
     int it0 = 0;
-    for (int base = 0; base < n; base += 128 * kCV, it0 += kCV) {
-      uint4 v[kCV];
+    for (int base = 0; base < n; base += 128 * KV, it0 += KV) {
+      uint4 v[KV];
 #pragma unroll
-      for (int j = 0; j < kCV; j++) {
+      for (int j = 0; j < KV; j++) {
         const int s0 = base + j * 128 + 4 * lane;
         v[j] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
         if (s0 < n) v[j] = CD_LD(vec_addr(s0));
       }
 #pragma unroll
-      for (int j = 0; j < kCV; j++) {
+      for (int j = 0; j < KV; j++) {
         const int s0 = base + j * 128 + 4 * lane;
         uint32_t a = v[j].x, b = v[j].y, c = v[j].z, d = v[j].w;
         if (s0 + 3 >= n) {                                       // tail vector: mask slots >= n
@@ -247,7 +251,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
           int it = -1;
           if (mlo) { it = __ffsll((long long)mlo) - 1; mlo &= mlo - 1; }
           else if (mhi) { it = 64 + __ffsll((long long)mhi) - 1; mhi &= mhi - 1; }
-          s0k[k] = it < 0 ? -1 : (it / kCV) * (128 * kCV) + (it % kCV) * 128 + 4 * lane;
+          s0k[k] = it < 0 ? -1 : (it / KV) * (128 * KV) + (it % KV) * 128 + 4 * lane;
         }
 #pragma unroll
         for (int k = 0; k < 4; k++)
