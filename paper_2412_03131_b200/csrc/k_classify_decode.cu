@@ -164,13 +164,22 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
     const int csh = __popc(C - 1);
     const int npages = (n + C - 1) / C;
 #if DKV_CD_SPEC
+    // the first scan batch's pages (1024 slots: 64 high / 32 low pages) come from the first round trip's
+    // registers; the rest of the row is copied into shared memory asynchronously (cp.async) and waited for only
+    // before the second batch, so that batch 1's score loads do not wait on it
     for (int k = lane; k < npages; k += 32) {
-      int32_t pid;
-      if (TOP && cls == DKV_CLS_TOP) pid = __ldg(p.ttable + (size_t)u * p.Lt + k);   // NEXT-4 (Q41)
-      else if (cls == DKV_CLS_HIGH) pid = k < 32 ? sp_h0 : (k < 64 ? sp_h1 : __ldg(row + k));
-      else pid = k < 32 ? sp_l0 : __ldg(row + p.L - 1 - k);
-      s_pid[k] = pid;
+      if (TOP && cls == DKV_CLS_TOP) {
+        s_pid[k] = __ldg(p.ttable + (size_t)u * p.Lt + k);     // NEXT-4 (Q41)
+      } else if (cls == DKV_CLS_HIGH) {
+        if (k < 64) s_pid[k] = k < 32 ? sp_h0 : sp_h1;
+        else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(s_pid + k)), "l"(row + k) : "memory");
+      } else {
+        if (k < 32) s_pid[k] = sp_l0;
+        else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(s_pid + k)), "l"(row + p.L - 1 - k)
+                          : "memory");
+      }
     }
+    cp_async_commit();
 #else
     const int32_t* row = p.table + (size_t)u * p.L;
     for (int k = lane; k < npages; k += 32)
@@ -195,6 +204,10 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
     bool ovf = false;
     int it0 = 0;
     for (int base = 0; base < n; base += 128 * KV, it0 += KV) {
+      if (base == 128 * KV) {                                    // batch 2 reads the asynchronously copied IDs
+        cp_async_wait<0>();
+        __syncwarp();
+      }
       uint4 v[KV];
 #pragma unroll
       for (int j = 0; j < KV; j++) {
@@ -231,6 +244,8 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
         }
       }
     }
+    cp_async_wait<0>();                                          // every page ID is in shared memory
+    __syncwarp();
     const uint32_t m = __reduce_min_sync(kFull, best);
     const unsigned holders = __ballot_sync(kFull, best == m);
     const bool any_tie = __any_sync(kFull, best == m && tie);
