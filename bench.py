@@ -249,6 +249,20 @@ def load_traffic():
     return get
 
 
+def scatter_note(achieved):
+    """The scan reads one 64-B (high page) or 128-B (low page) score segment per page, scattered over the pool: its
+    ceiling is the measured random-segment gather rate (profiles/scatter_peaks.json, tools/scatter_bench.cu), not the
+    streaming HBM peak."""
+    p = os.path.join(ROOT, "profiles", "scatter_peaks.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        j = json.load(f)
+    return {"random_64B_gbs": j["random_64B_gbs"], "random_128B_gbs": j["random_128B_gbs"],
+            "frac_of_64B": round(achieved / j["random_64B_gbs"], 3), "frac_of_128B": round(achieved / j["random_128B_gbs"], 3),
+            "source": j["source"]}
+
+
 # ----------------------------------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local):
     from paper_2412_03131_b200 import Pool
@@ -771,7 +785,8 @@ def run_ours(args, rank, world, local):
         "roofline_decode": {"kernel": "classify_decode_kernel", "bound": "hbm", "achieved": round(cls_gbs, 1),
                             "peak": peak, "unit": "GB/s", "frac": round(cls_gbs / peak, 4),
                             "algorithmic_bytes": int(statistics.mean(cls_bytes)),
-                            "traffic": traffic("classify_decode_kernel"), "traffic_unit": "bytes per launch"},
+                            "traffic": traffic("classify_decode_kernel"), "traffic_unit": "bytes per launch",
+                            "access_pattern": scatter_note(cls_gbs)},
         "e2e": {"value": round(e2e_mean, 3), "unit": E2E_UNIT,
                 "h2d_bytes_per_step": wl.U * (4 + 2 * 2 * c["d"]), "d2h_bytes_per_step": wl.U * 16,
                 "h2d_link": h2d_link},
