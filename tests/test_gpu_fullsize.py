@@ -257,3 +257,82 @@ def test_llama8b_fullsize_attention_sampled_parity():
         attend_and_compare(f"decode {step}")
     st, _ = pool.query()
     assert st == 0
+
+
+def test_llama8b_fullsize_attention_tc_sampled_and_deterministic():
+    """NEXT-2 on tensor cores at the bench's full size and launch configuration (configs[1], q_per_kv 4, 16384
+    units over the persistent CTAs, each CTA's significance pass deferred into its next unit): outputs and per-token
+    scores of 64 sampled units against Eq. 1 in float64 from the pool's page bytes; the significance written back
+    for those units against the float64 running mean (Q33); and the whole call deterministic — re-run from the same
+    arena bytes it produces bit-identical outputs, scores and arena (a race check in the absence of the sanitizer)."""
+    import bench
+    from paper_2412_03131_b200 import Pool
+    from paper_2412_03131_b200 import dkv as D
+    from tests import eq1
+
+    c = bench.CONFIGS["llama3_8b"]
+    G, d, W = c["G"], c["d"], c["W"]
+    dev = torch.device("cuda", 0)
+    wl = bench.Workload(c, 0, 1, dev)
+    T = c["prompt"]
+    cfg = D.make_config(wl.R, c["Ly"], wl.Hl, d, c["M"], W, c["Ch"], c["Cl"], P=c["P"],
+                        alpha_h=c["alpha_h"], alpha_l=c["alpha_l"], q_per_kv=G)
+    pool = Pool(cfg, device=dev)
+    geom, L, LyH = pool.geom(), pool.L, pool.LyH
+    sig, kk, vv = wl.prefill_inputs(T)
+    pool.classify_prefill(list(range(wl.R)), [T] * wl.R, sig)
+    pool.compact_alloc(None)
+    pool.quant_write_prefill(kk.view(torch.int16), vv.view(torch.int16), sig)
+    del kk, vv, sig
+    q = np.random.default_rng(3).normal(0, 1, size=(wl.U, G, d)).astype(np.float16)
+    qd = torch.from_numpy(q.view(np.int16)).to(dev)
+    sample = list(range(0, wl.U, wl.U // 64))
+    v = pool.views()
+    torch.cuda.synchronize()
+    before = {u: _unit_scores(v, geom, L, u) for u in sample}
+    arena0 = pool.arena.clone()
+    runs = []
+    for rep in range(2):
+        if rep:
+            pool.arena.copy_(arena0)
+        out = torch.empty((wl.U, G, d), dtype=torch.float32, device=dev)
+        probs = torch.zeros((wl.U, c["M"]), dtype=torch.float32, device=dev)
+        assert pool.attend_tc(qd, out, probs) == 0
+        torch.cuda.synchronize()
+        runs.append((out, probs, pool.arena.clone() if rep == 0 else None))
+    assert torch.equal(runs[0][0], runs[1][0]) and torch.equal(runs[0][1], runs[1][1]), "attend_tc not deterministic"
+    assert torch.equal(runs[0][2], pool.arena), "attend_tc arena writes not deterministic"
+    del arena0, runs[0]
+    out, probs = runs[-1][0].cpu().numpy(), runs[-1][1].cpu().numpy()
+    snap = dict(pages=v["pages"], table=v["table"], n_h=v["n_h"], n_l=v["n_l"], seq_len=v["seq_len"],
+                win_k=v["win_k"], win_v=v["win_v"])
+    eq1.check_units(snap, geom, L, W, d, LyH, q, out, probs, sample, where="fullsize tc")
+    # the significance written back (Q33): (s * c + a) / (c + 1), c = N - 2 - pos, a = the float64 score
+    N = T
+    for u in sample:
+        k_, v_, pos = eq1.unit_tokens64(v["pages"], v["table"][u].cpu().numpy(), int(v["n_h"][u]), int(v["n_l"][u]),
+                                        N, v["win_k"][u].cpu().numpy(), v["win_v"][u].cpu().numpy(), geom, L, W, d)
+        _, a = eq1.attend64(q[u], k_, v_)
+        aft = _unit_scores(v, geom, L, u)
+        for i, ps in enumerate(pos[:len(aft)]):
+            s0, s1 = before[u][int(ps)], aft[int(ps)]
+            cc = N - 2 - int(ps)
+            want = (s0 * cc + float(a[i])) / (cc + 1) if cc >= 0 else s0
+            assert abs(s1 - want) <= 1e-4 * max(abs(want), 1e-6), (u, ps, s1, want)
+
+
+def _unit_scores(v, geom, L, u):
+    """{position: significance} of unit u's stored tokens, read from the pool's pages"""
+    out = {}
+    table = v["table"][u].cpu().numpy()
+    for cls, n in ((1, int(v["n_h"][u])), (2, int(v["n_l"][u]))):
+        g = geom[cls]
+        C = g["C"]
+        npg = -(-n // C)
+        cols = np.arange(npg) if cls == 1 else L - 1 - np.arange(npg)
+        pids = torch.from_numpy(table[cols].astype(np.int64)).to(v["pages"].device)
+        pg = v["pages"][pids].cpu().numpy()
+        sc = np.ascontiguousarray(pg[:, g["off_score"]:g["off_score"] + 4 * C]).view(np.float32).reshape(-1)[:n]
+        ps = np.ascontiguousarray(pg[:, g["off_pos"]:g["off_pos"] + 4 * C]).view(np.int32).reshape(-1)[:n]
+        out.update({int(p): float(s) for p, s in zip(ps, sc)})
+    return out
