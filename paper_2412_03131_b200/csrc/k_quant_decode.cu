@@ -305,7 +305,8 @@ __device__ __forceinline__ void recycle_unit(const PoolDev& p, int u, int q, uns
   if (q == 0) p.rec[4 * (size_t)u + 2] = 0;
 }
 
-template <int D, int G>
+// TOP: the pool has the NEXT-4 FP16 tier (its branches compiled out otherwise)
+template <int D, int G, bool TOP>
 __global__ void __launch_bounds__(kQDThreads, DKV_QD_MINB)
 quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uint16_t* __restrict__ knew,
                     const uint16_t* __restrict__ vnew, const float* __restrict__ cand_sig, int u0, int u1, int upc) {
@@ -382,7 +383,7 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
     const int v_slot = dw.y, tc_slot = dw.z, v_dst = dw.w;
     const bool has_tc = live && (tc_class == DKV_CLS_HIGH || tc_class == DKV_CLS_LOW || tc_class == DKV_CLS_TOP);
     const bool down = live && v_action == DKV_V_DOWN;
-    const bool tc_high = tc_class == DKV_CLS_HIGH, tc_top = tc_class == DKV_CLS_TOP;
+    const bool tc_high = tc_class == DKV_CLS_HIGH, tc_top = TOP && tc_class == DKV_CLS_TOP;
     const int tc_pg = fdiv(tc_top ? p.div_Ct : (tc_high ? p.div_Ch : p.div_Cl), tc_slot);
     const int pid_tc = qp.x, pid_src = qp.x, pid_dst = qp.y;   // the victim's KV_h slot is t_c's slot (Q8)
 
@@ -494,13 +495,13 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
   }
 }
 
-template <int D, int G>
-static cudaError_t launch_qd(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
+template <int D, int G, bool TOP>
+static cudaError_t launch_qd_t(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
                              const float* sig, int u0, int u1, cudaStream_t s) {
   constexpr int units_per_cta = kQDThreads / G;
   const size_t smem = 0;
   static int cap = 0;                                    // persistent grid (per template instance)
-  if (cap == 0) cap = persistent_grid(quant_decode_kernel<D, G>, kQDThreads, 0);
+  if (cap == 0) cap = persistent_grid(quant_decode_kernel<D, G, TOP>, kQDThreads, 0);
   if (cap == 0) return cudaErrorUnknown;
   if (u1 <= u0) return cudaSuccess;
   // every resident CTA takes the same number of units (at most units_per_cta): 16384 units over 592 CTAs is 28
@@ -508,8 +509,14 @@ static cudaError_t launch_qd(const PoolDev& p, const dkv_decision_t* dec, const 
   int upc = (u1 - u0 + cap - 1) / cap;
   if (upc > units_per_cta) upc = units_per_cta;
   const int need = (u1 - u0 + upc - 1) / upc;
-  return launch_ex(quant_decode_kernel<D, G>, dim3(need < cap ? need : cap), dim3(kQDThreads), smem, s, p.pdl != 0, p,
+  return launch_ex(quant_decode_kernel<D, G, TOP>, dim3(need < cap ? need : cap), dim3(kQDThreads), smem, s, p.pdl != 0, p,
                    dec, k, v, sig, u0, u1, upc);
+}
+
+template <int D, int G>
+static cudaError_t launch_qd(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
+                             const float* sig, int u0, int u1, cudaStream_t s) {
+  return p.top ? launch_qd_t<D, G, true>(p, dec, k, v, sig, u0, u1, s) : launch_qd_t<D, G, false>(p, dec, k, v, sig, u0, u1, s);
 }
 
 cudaError_t launch_quant_decode(const PoolDev& p, const dkv_decision_t* dec, const uint16_t* k, const uint16_t* v,
