@@ -245,13 +245,16 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
     // following dkv_quant_write, which takes liveness from the unit's qpid record
     if (phase == DKV_PHASE_DECODE && st == DKV_REQ_PENDING_FREE) reinterpret_cast<int32_t*>(p.qpid + u)[2] = 0;
   }
-  __syncthreads();
 
   // ---- Fast path (no grid barrier): with an error pending nothing is granted; in a decode step every unit
   // demands at most one page, so if the free region at entry already holds >= U pages the
   // all-or-nothing check cannot fail and every grant reads a ring slot of that region, never one recycled
   // in this call.  Both conditions are read at entry and identical in every tile.
   const bool fast = (status0 != 0) || (phase == DKV_PHASE_DECODE && free0 >= (int64_t)p.U);
+  // the recycle copies above are complete before a grant (or the grid barrier) — a barrier needed only when
+  // this tile copied in place: a deferred (decode fast path) recycle writes no ring slot here
+  if (!fast || (s_incfr - s_exfr > 0 && !(defer_rec && phase == DKV_PHASE_DECODE && status0 == 0 && free0 >= (int64_t)p.U)))
+    __syncthreads();
   bool ok;
   int64_t D = 0, F = 0;
   if (fast) {
