@@ -1008,7 +1008,8 @@ cudaError_t launch_recycle(const PoolDev& p, const int32_t* req, int n, cudaStre
 cudaError_t launch_attend(const PoolDev& p, const uint16_t* q, float* out, float* probs, int TS, cudaStream_t s);
 size_t attend_smem_bytes(const PoolDev& p, int TS);
 size_t attend_long_smem_bytes(const PoolDev& p);
-cudaError_t launch_attend_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s);
+cudaError_t launch_attend_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, int active_units, int max_len,
+                             cudaStream_t s);
 constexpr int kAuditResults = 8;
 cudaError_t launch_audit(const PoolDev& p, uint32_t* hist, int64_t* res, cudaStream_t s);
 size_t attend_tc_smem_bytes(const PoolDev& p);

@@ -710,6 +710,318 @@ attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ 
   }
 }
 
+// ---- Split-sequence form ("split the sequence into segments processed by separate thread blocks, then
+// merge"): with few active units one CTA per unit leaves most SMs idle, so each unit gets NS CTAs, CTA s over a
+// contiguous range of the unit's pages (the last one also over the window), each writing its partial softmax state
+// (per head: maximum M_s, sum Z_s, sum of p z' and the output accumulator, all relative to M_s); a second kernel
+// merges the NS states (the same rescaling as the warps' merge) and runs the unit's significance pass.  Scratch
+// (U <= kTcSlots): the unit's logit rows in buffer u of tc_scratch, the partial states after buffer kTcSlots.
+constexpr int kTcSplitMax = 32;
+#ifndef DKV_TC_SPLIT
+#define DKV_TC_SPLIT 1      // build-time switch of the split-sequence form (A/B: tools/tc_split_ab.py)
+#endif
+template <int D, int G>
+__host__ __device__ constexpr int tc_partial_floats() { return G * D + 3 * 8 + 8; }   // + minima candidates
+
+template <int D, int G>
+__global__ void __launch_bounds__(kTcThreads, DKV_TC_MINB)
+attend_tc_split_kernel(PoolDev p, const uint16_t* __restrict__ q, int NS, int slots) {
+  constexpr int NG = D / 16, NMT = D / 16, FPK = D / 4, FPV = D / 8, GP = G <= 4 ? 4 : 8;
+  constexpr int STG = tc_stage_bytes<D>();
+  using HI = TcCls<D, 16, 8, 4>;
+  using LO = TcCls<D, 32, 4, 2>;
+  extern __shared__ __align__(128) uint8_t tc_smem[];
+  __shared__ float s_mw[kTcWarps][8], s_zw[kTcWarps][8], s_zsw[kTcWarps][8];
+  __shared__ __align__(8) uint64_t s_bar[kTcWarps][kTcStages];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = lane >> 2, tig = lane & 3;
+  const int u = blockIdx.x, seg = blockIdx.y;
+  if (ld_volatile(&p.ctrl->status) != 0) return;
+  if (p.req_state[fdiv(p.div_LyH, u)] != DKV_REQ_ACTIVE) return;  // CTA-uniform
+  const int L = p.L, W = p.W, R = p.tc_slot_rows;
+  const int N = p.seq_len[fdiv(p.div_LyH, u)];
+  const int nh = p.n_h[u], nl = p.n_l[u];
+  const int nw = min(W, N);
+  const int ph = (nh + HI::C - 1) / HI::C, pl = (nl + LO::C - 1) / LO::C, npg = ph + pl;
+  const int lo0 = HI::C * ph, wb = lo0 + LO::C * pl;
+  const int k0 = (int)((long)seg * npg / NS), k1 = (int)((long)(seg + 1) * npg / NS);   // this CTA's pages
+  uint8_t* const stage0 = tc_smem;
+  int32_t* const pid = reinterpret_cast<int32_t*>(tc_smem + tc_area_bytes(D, G, STG));
+  uint8_t* const mystage = stage0 + (size_t)warp * kTcStages * STG;
+  uint64_t* const bars = s_bar[warp];
+  if (tid < kTcWarps * kTcStages) mbar_init(&s_bar[tid / kTcStages][tid % kTcStages], 1);
+  fence_mbar_init();
+  uint32_t phase = 0;
+  const uint32_t bar_s = smem_u32(bars), stage_s = smem_u32(mystage);
+  const float scale2 = rsqrtf((float)D) * kLog2e;
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  const int32_t* trow = p.table + (size_t)u * L;
+  for (int k = k0 + tid; k < k1; k += kTcThreads) pid[k - k0] = k < ph ? trow[k] : trow[L - 1 - (k - ph)];
+  uint32_t qb[NG][2];
+  float qs = 0.0f;
+  {
+    const uint16_t* qr = q + ((size_t)u * G + (grp < G ? grp : 0)) * D + FPK * tig;
+#pragma unroll
+    for (int g = 0; g < NG; g++) {
+      uint2 v = make_uint2(0u, 0u);
+      if (grp < G) v = *reinterpret_cast<const uint2*>(qr + 4 * g);
+      qb[g][0] = v.x; qb[g][1] = v.y;
+      const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
+      const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
+      qs += (f0.x + f0.y) + (f1.x + f1.y);
+    }
+    qs += __shfl_xor_sync(kFull, qs, 1);
+    qs += __shfl_xor_sync(kFull, qs, 2);
+  }
+  const float qsz[2] = {__shfl_sync(kFull, qs, 8 * tig) * scale2, __shfl_sync(kFull, qs, 8 * tig + 4) * scale2};
+  __syncthreads();                                                // pid, barriers
+  float* const lgl = p.tc_scratch + (size_t)u * R * GP + 2 * tig; // the unit's logit buffer, this lane's column
+  const int npr = k1 - k0;
+  const int my_n = npr > warp ? (npr - warp + kTcWarps - 1) / kTcWarps : 0;
+  auto stage = [&](int kl, int slot) {                            // kl: page index within the range
+    if (lane != 0) return;
+    const int k = k0 + kl;
+    const uint32_t bytes = k < ph ? HI::prefix : LO::prefix;
+    const uint32_t bar = bar_s + 8 * slot;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 ::"r"(stage_s + slot * STG), "l"(p.pages + (size_t)pid[kl] * (size_t)p.page_bytes), "r"(bytes), "r"(bar),
+                 "l"(pol) : "memory");
+  };
+  TcState<D> st;
+#pragma unroll
+  for (int mt = 0; mt < NMT; mt++) st.o[mt][0] = st.o[mt][1] = st.o[mt][2] = st.o[mt][3] = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 2; c++) {
+    st.m[c] = 2 * tig + c < G ? -INFINITY : 0.0f;
+    st.z[c] = 0.0f;
+    st.zs[c] = 0.0f;
+  }
+#pragma unroll
+  for (int i = 0; i < kTcStages - 1; i++)
+    if (i < my_n) stage(warp + i * kTcWarps, i);
+  for (int i = 0, slot = 0, islot = kTcStages - 1; i < my_n; i++) {
+    const int kl = warp + i * kTcWarps, k = k0 + kl;
+    if (i + kTcStages - 1 < my_n) stage(warp + (i + kTcStages - 1) * kTcWarps, islot);
+    mbar_wait_u32(bar_s + 8 * slot, (phase >> slot) & 1u);
+    phase ^= 1u << slot;
+    const uint8_t* sg = mystage + slot * STG;
+    if (k < ph) {
+      const int t0 = HI::C * k;
+      tc_chunk<D, G, GP, HI>(sg, 0, nh - t0, qb, qsz, scale2, lgl, t0, st, grp, tig);
+    } else {
+      const int kk = k - ph, cnt = nl - LO::C * kk, row = lo0 + LO::C * kk;
+      tc_chunk<D, G, GP, LO>(sg, 0, cnt, qb, qsz, scale2, lgl, row, st, grp, tig);
+      if (cnt > 16) tc_chunk<D, G, GP, LO>(sg, 1, cnt, qb, qsz, scale2, lgl, row, st, grp, tig);
+    }
+    __syncwarp();
+    slot = slot + 1 == kTcStages ? 0 : slot + 1;
+    islot = islot + 1 == kTcStages ? 0 : islot + 1;
+  }
+  if (seg == NS - 1) {                                            // the window, by the last segment's CTA
+    const uint16_t* wk_all = reinterpret_cast<const uint16_t*>(p.win_k);
+    const uint16_t* wv_all = reinterpret_cast<const uint16_t*>(p.win_v);
+    const int wbase = fmod_(p.div_W, N - nw);
+    for (int c = warp; 16 * c < nw; c += kTcWarps)
+      tc_window_chunk<D, G, GP>(wk_all + (size_t)u * W * D, wv_all + (size_t)u * W * D, c, nw, W, wbase, qb, scale2,
+                                lgl, wb, st, grp, tig);
+  }
+#pragma unroll
+  for (int c = 0; c < 2; c++)
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      st.z[c] += __shfl_xor_sync(kFull, st.z[c], o);
+      st.zs[c] += __shfl_xor_sync(kFull, st.zs[c], o);
+    }
+  __syncthreads();
+  float* part = reinterpret_cast<float*>(stage0);                 // [kTcWarps][G][D]
+#pragma unroll
+  for (int c = 0; c < 2; c++) {
+    const int h = 2 * tig + c;
+    if (h < G) {
+      if (grp == 0) { s_mw[warp][h] = st.m[c]; s_zw[warp][h] = st.z[c]; s_zsw[warp][h] = st.zs[c]; }
+      float* pr = part + ((size_t)warp * G + h) * D + FPV * grp;
+#pragma unroll
+      for (int mt = 0; mt < NMT; mt++) {
+        pr[2 * mt] = st.o[mt][c] * kPvUnscale;
+        pr[2 * mt + 1] = st.o[mt][2 + c] * kPvUnscale;
+      }
+    }
+  }
+  __syncthreads();
+  // the CTA's partial state, relative to its own maximum
+  float* ps = p.tc_scratch + (size_t)slots * R * GP + ((size_t)u * NS + seg) * tc_partial_floats<D, G>();
+  for (int e = tid; e < G * D; e += kTcThreads) {
+    const int h = e / D;
+    float M = -INFINITY;
+    for (int w = 0; w < kTcWarps; w++) M = fmaxf(M, s_mw[w][h]);
+    float o = 0.0f;
+    for (int w = 0; w < kTcWarps; w++)
+      if (s_mw[w][h] != -INFINITY) o = fmaf(ex2(s_mw[w][h] - M), part[((size_t)w * G + h) * D + (e % D)], o);
+    ps[e] = o;
+  }
+  if (tid < G) {
+    float M = -INFINITY, Z = 0.0f, ZS = 0.0f;
+    for (int w = 0; w < kTcWarps; w++) M = fmaxf(M, s_mw[w][tid]);
+    for (int w = 0; w < kTcWarps; w++)
+      if (s_mw[w][tid] != -INFINITY) {
+        const float f = ex2(s_mw[w][tid] - M);
+        Z = fmaf(f, s_zw[w][tid], Z);
+        ZS = fmaf(f, s_zsw[w][tid], ZS);
+      }
+    ps[G * D + tid] = M;
+    ps[G * D + 8 + tid] = Z;
+    ps[G * D + 16 + tid] = ZS;
+  }
+}
+
+// merge + significance: CTA (u, s) combines the unit's NS partial states (every CTA of the unit, so that none
+// waits for another; CTA s = 0 writes the output), then runs the significance pass (Q33) of its share of the unit's
+// logit rows and leaves its section minima candidates after its partial state; attend_tc_minima_kernel reduces them.
+template <int D, int G>
+__global__ void __launch_bounds__(kTcThreads)
+attend_tc_merge_kernel(PoolDev p, float* __restrict__ out, float* __restrict__ probs, int NS, int slots) {
+  constexpr int GP = G <= 4 ? 4 : 8, PF = tc_partial_floats<D, G>();
+  using HI = TcCls<D, 16, 8, 4>;
+  using LO = TcCls<D, 32, 4, 2>;
+  extern __shared__ __align__(16) int32_t tm_pid[];               // [npg] page IDs
+  __shared__ float s_f[kTcSplitMax][8], s_C[8], s_iZ[8];
+  __shared__ unsigned long long s_min[2];
+  __shared__ int s_slot[2];
+  const int tid = threadIdx.x, u = blockIdx.x, seg = blockIdx.y;
+  if (ld_volatile(&p.ctrl->status) != 0) return;
+  const int r = fdiv(p.div_LyH, u);
+  if (p.req_state[r] != DKV_REQ_ACTIVE) return;
+  const int L = p.L, W = p.W, R = p.tc_slot_rows;
+  const ClassGeom gh = p.g[1], gl = p.g[2];
+  const int N = p.seq_len[r];
+  const int nh = p.n_h[u], nl = p.n_l[u];
+  const int nw = min(W, N), Ts = nh + nl;
+  const int ph = (nh + HI::C - 1) / HI::C, pl = (nl + LO::C - 1) / LO::C, npg = ph + pl;
+  const int lo0 = HI::C * ph, wb = lo0 + LO::C * pl;
+  const int32_t* trow = p.table + (size_t)u * L;
+  for (int k = tid; k < npg; k += kTcThreads) tm_pid[k] = k < ph ? trow[k] : trow[L - 1 - (k - ph)];
+  if (tid < 2) { s_min[tid] = ~0ull; s_slot[tid] = -1; }
+  float* const ps0 = p.tc_scratch + (size_t)slots * R * GP + (size_t)u * NS * PF;
+  if (tid < G) {
+    float M = -INFINITY;
+    for (int s = 0; s < NS; s++) M = fmaxf(M, ps0[(size_t)s * PF + G * D + tid]);
+    float Z = 0.0f;
+    for (int s = 0; s < NS; s++) {
+      const float ms = ps0[(size_t)s * PF + G * D + tid];
+      const float f = ms == -INFINITY ? 0.0f : ex2(ms - M);
+      s_f[s][tid] = f;
+      Z = fmaf(f, ps0[(size_t)s * PF + G * D + 8 + tid], Z);
+    }
+    s_C[tid] = Z > 0.0f ? M + log2f(Z) : INFINITY;
+    s_iZ[tid] = Z > 0.0f ? 1.0f / Z : 0.0f;
+  }
+  __syncthreads();
+  if (out != nullptr && seg == 0)
+    for (int e = tid; e < G * D; e += kTcThreads) {
+      const int h = e / D;
+      float o = 0.0f;
+      for (int s = 0; s < NS; s++) o = fmaf(s_f[s][h], ps0[(size_t)s * PF + e] + ps0[(size_t)s * PF + G * D + 16 + h], o);
+      out[(size_t)u * G * D + e] = o * s_iZ[h];
+    }
+  // significance (Q33) of this CTA's rows: a thread per row, 4 rows in flight
+  const float* lg = p.tc_scratch + (size_t)u * R * GP;
+  const int rows = wb + nw, r0 = (int)((long)seg * rows / NS), r1 = (int)((long)(seg + 1) * rows / NS);
+  unsigned long long mkey[2] = {~0ull, ~0ull};
+  int mslot[2] = {-1, -1};
+  constexpr int kB = 4;
+  for (int base = r0 + tid; base < r1; base += kB * kTcThreads) {
+    float xv[kB], sgv[kB];
+    int posv[kB], rrv[kB];
+    float* spv[kB];
+#pragma unroll
+    for (int b = 0; b < kB; b++) {
+      const int row = base + b * kTcThreads;
+      const bool stored = row < wb, hi = row < lo0;
+      const int rr = hi ? row : row - lo0;
+      spv[b] = nullptr;
+      rrv[b] = rr;
+      if (row >= r1 || (stored && rr >= (hi ? nh : nl))) continue;
+      float xm = -INFINITY;
+#pragma unroll
+      for (int h = 0; h < G; h++) xm = fmaxf(xm, lg[(size_t)row * GP + h] - s_C[h]);
+      xv[b] = xm;
+      if (stored) {
+        const int k = hi ? row >> 4 : ph + (rr >> 5), j = hi ? row & 15 : rr & 31;
+        const ClassGeom& gg = hi ? gh : gl;
+        uint8_t* pg = p.pages + (size_t)tm_pid[k] * (size_t)p.page_bytes;
+        posv[b] = *reinterpret_cast<const int32_t*>(pg + gg.off_pos + 4 * j);
+        spv[b] = reinterpret_cast<float*>(pg + gg.off_score + 4 * j);
+      } else {
+        posv[b] = N - nw + (row - wb);
+        spv[b] = p.win_sig + (size_t)u * W + fmod_(p.div_W, posv[b]);
+      }
+      sgv[b] = *spv[b];
+    }
+#pragma unroll
+    for (int b = 0; b < kB; b++) {
+      if (spv[b] == nullptr) continue;
+      const int row = base + b * kTcThreads, pos = posv[b], rr = rrv[b];
+      const float a = ex2(xv[b]);
+      float sg = sgv[b];
+      const int c = N - 2 - pos;
+      if (c >= 0) {
+        sg = __fdividef(fmaf(sg, (float)c, a), (float)(c + 1));
+        *spv[b] = sg;
+      }
+      if (row < wb) {
+        const bool hi = row < lo0;
+        if (probs) probs[(size_t)u * p.M + (hi ? rr : nh + rr)] = a;
+        const int cls = hi ? 0 : 1;
+        const unsigned long long key = ((unsigned long long)__float_as_uint(sg) << 32) | (uint32_t)pos;
+        if (key < mkey[cls]) { mkey[cls] = key; mslot[cls] = rr; }
+      } else if (probs) {
+        probs[(size_t)u * p.M + Ts + (row - wb)] = a;
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 2; c++)
+    if (mkey[c] != ~0ull) atomicMin(&s_min[c], mkey[c]);
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 2; c++)
+    if (mkey[c] != ~0ull && mkey[c] == s_min[c]) s_slot[c] = mslot[c];
+  __syncthreads();
+  if (tid == 0) {                                                 // this CTA's candidates, after its partial state
+    uint32_t* mc = reinterpret_cast<uint32_t*>(ps0 + (size_t)seg * PF + G * D + 24);
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      mc[3 * c] = (uint32_t)(s_min[c] >> 32);
+      mc[3 * c + 1] = (uint32_t)(s_min[c] & 0xFFFFFFFFull);
+      mc[3 * c + 2] = (uint32_t)s_slot[c];
+    }
+  }
+}
+
+// the section minima of a split unit: the smallest (significance, position) key over its NS CTAs' candidates
+template <int D, int G>
+__global__ void attend_tc_minima_kernel(PoolDev p, int NS, int slots) {
+  constexpr int GP = G <= 4 ? 4 : 8, PF = tc_partial_floats<D, G>();
+  const int u = blockIdx.x, c = threadIdx.x;                      // c: section (0 high, 1 low)
+  if (c >= 2 || ld_volatile(&p.ctrl->status) != 0) return;
+  if (p.req_state[fdiv(p.div_LyH, u)] != DKV_REQ_ACTIVE) return;
+  const float* ps0 = p.tc_scratch + (size_t)slots * p.tc_slot_rows * GP + (size_t)u * NS * PF;
+  unsigned long long best = ~0ull;
+  int slot = -1;
+  for (int s = 0; s < NS; s++) {
+    const uint32_t* mc = reinterpret_cast<const uint32_t*>(ps0 + (size_t)s * PF + G * D + 24) + 3 * c;
+    const unsigned long long key = ((unsigned long long)mc[0] << 32) | mc[1];
+    if (key < best) { best = key; slot = (int)mc[2]; }
+  }
+  int32_t* m = p.secmin + 8 * (size_t)u;
+  m[3 * c] = (int32_t)(uint32_t)(best >> 32);
+  m[3 * c + 1] = (int32_t)(uint32_t)(best & 0xFFFFFFFFull);
+  m[3 * c + 2] = slot;
+  if (c == 0) m[6] = 1;
+}
+
 // the kernel is specialised for the paper's classes: K8V4 in 16-token pages, K4V2 in 32-token pages,
 // with the §4 segment order (K codes, K meta, V codes, V meta, scores, positions); other geometries take the
 // exact path
@@ -731,7 +1043,8 @@ size_t attend_tc_smem_bytes(const PoolDev& p) {
 }
 
 template <int D, int G>
-static cudaError_t launch_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s) {
+static cudaError_t launch_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, int active_units,
+                             int max_len, cudaStream_t s) {
   const size_t smem = attend_tc_smem_bytes(p);
   cudaError_t e = cudaFuncSetAttribute(attend_tc_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -742,25 +1055,54 @@ static cudaError_t launch_tc(const PoolDev& p, const uint16_t* q, float* out, fl
     return e;
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   if (grid > p.tc_slots) grid = p.tc_slots;                       // two scratch buffers per CTA slot
+  // split-sequence form: fewer active units than SMs, long enough to share (>= 2048 tokens, >= 8 pages per
+  // segment), and the partial states fit the scratch's second half
+  const int pages = max_len / 16;
+  int NS = 1;
+  if (DKV_TC_SPLIT && active_units > 0 && active_units < sms && max_len >= 2048 && p.U <= p.tc_slots) {
+    NS = grid / active_units;
+    if (NS > kTcSplitMax) NS = kTcSplitMax;
+    if (NS > pages / 8) NS = pages / 8;
+    const long cap = (long)p.tc_slots * p.tc_slot_rows * (G <= 4 ? 4 : 8) / ((long)p.U * tc_partial_floats<D, G>());
+    if (NS > cap) NS = (int)cap;
+  }
+  if (NS >= 2) {
+    e = cudaFuncSetAttribute(attend_tc_split_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attend_tc_split_kernel<D, G><<<dim3(p.U, NS), kTcThreads, smem, s>>>(p, q, NS, p.tc_slots);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const size_t msm = (size_t)((p.L + 3) & ~3) * 4;
+    if (msm > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(attend_tc_merge_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm)) != cudaSuccess)
+      return e;
+    attend_tc_merge_kernel<D, G><<<dim3(p.U, NS), kTcThreads, msm, s>>>(p, out, probs, NS, p.tc_slots);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    attend_tc_minima_kernel<D, G><<<p.U, 32, 0, s>>>(p, NS, p.tc_slots);
+    return cudaGetLastError();
+  }
   if (grid > p.U) grid = p.U;
   attend_tc_kernel<D, G><<<grid, kTcThreads, smem, s>>>(p, q, out, probs);
   return cudaGetLastError();
 }
 
 template <int D>
-static cudaError_t launch_tc_d(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s) {
+static cudaError_t launch_tc_d(const PoolDev& p, const uint16_t* q, float* out, float* probs, int au, int ml,
+                               cudaStream_t s) {
   switch (p.G) {
-    case 1: return launch_tc<D, 1>(p, q, out, probs, s);
-    case 2: return launch_tc<D, 2>(p, q, out, probs, s);
-    case 4: return launch_tc<D, 4>(p, q, out, probs, s);
-    case 5: return launch_tc<D, 5>(p, q, out, probs, s);
-    case 7: return launch_tc<D, 7>(p, q, out, probs, s);
-    default: return launch_tc<D, 8>(p, q, out, probs, s);
+    case 1: return launch_tc<D, 1>(p, q, out, probs, au, ml, s);
+    case 2: return launch_tc<D, 2>(p, q, out, probs, au, ml, s);
+    case 4: return launch_tc<D, 4>(p, q, out, probs, au, ml, s);
+    case 5: return launch_tc<D, 5>(p, q, out, probs, au, ml, s);
+    case 7: return launch_tc<D, 7>(p, q, out, probs, au, ml, s);
+    default: return launch_tc<D, 8>(p, q, out, probs, au, ml, s);
   }
 }
 
-cudaError_t launch_attend_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, cudaStream_t s) {
-  return p.d == 128 ? launch_tc_d<128>(p, q, out, probs, s) : launch_tc_d<64>(p, q, out, probs, s);
+// active_units / max_len: the ACTIVE requests' units and longest length (host mirror), which choose the form
+cudaError_t launch_attend_tc(const PoolDev& p, const uint16_t* q, float* out, float* probs, int active_units,
+                             int max_len, cudaStream_t s) {
+  return p.d == 128 ? launch_tc_d<128>(p, q, out, probs, active_units, max_len, s)
+                    : launch_tc_d<64>(p, q, out, probs, active_units, max_len, s);
 }
 
 }  // namespace dkv

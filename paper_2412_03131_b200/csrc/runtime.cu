@@ -494,7 +494,12 @@ dkv_status_t dkv_attend_tc(dkv_pool_t p, const uint16_t* d_q, float* d_out, floa
   // arena's per-CTA scratch slots, so any context up to max_seq_len runs here
   if (!attend_tc_supported(p->dev) || attend_tc_smem_bytes(p->dev) > (size_t)optin)
     return dkv_attend(p, d_q, d_out, d_probs, s);
-  return launch_attend_tc(p->dev, d_q, d_out, d_probs, (cudaStream_t)s) == cudaSuccess ? DKV_OK : DKV_ERR_CUDA;
+  int active = 0, max_len = 0;                                   // host mirror: chooses the split-sequence form
+  for (int r = 0; r < p->cfg.max_requests; r++)
+    if (p->req_state[r] == DKV_REQ_ACTIVE) { active++; max_len = p->seq_len[r] > max_len ? p->seq_len[r] : max_len; }
+  const int units = active * p->cfg.num_layers * p->cfg.num_kv_heads;
+  return launch_attend_tc(p->dev, d_q, d_out, d_probs, units, max_len, (cudaStream_t)s) == cudaSuccess ? DKV_OK
+                                                                                                       : DKV_ERR_CUDA;
 }
 
 dkv_status_t dkv_audit(dkv_pool_t p, uint32_t* d_scratch, int64_t* d_result, dkv_stream_t s) {

@@ -156,3 +156,14 @@ def test_attention_tc_window_not_a_chunk_multiple(W):
     scn = H.TINY.replace(R=3, Ly=2, H=2, d=128, M=600, W=W, P=6000, seed=41 + W, q_per_kv=4, alpha_h=1.0,
                          alpha_l=0.02)
     _run(scn, [300, 11, 90], steps=5, seed=W)
+
+
+@pytest.mark.parametrize("G,W", [(4, 64), (8, 24), (5, 0)])
+def test_attention_tc_split_sequence(G, W):
+    """Few active units with long contexts take the split-sequence form: each unit's pages split over
+    several CTAs whose partial softmax states a merge kernel combines (it also runs the significance pass) — outputs,
+    scores, the written significance and the section minima against Eq. 1 in float64 over a lifecycle, as for the
+    single-CTA form"""
+    scn = H.TINY.replace(R=2, Ly=1, H=2, d=128, M=5000, W=W, P=8000, seed=51 + G, q_per_kv=G, alpha_h=1.0,
+                         alpha_l=0.02)
+    _run(scn, [3000, 2300], steps=4, seed=G, frees=[(2, [1])])
