@@ -228,7 +228,9 @@ dkv_status_t dkv_attend(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* 
  * scores rtol 2e-5 / atol 1e-7); the section minima are exact for the significance values it writes.  Same
  * arguments and errors as dkv_attend.  Falls back to dkv_attend when a class's pages are not the paper's K8V4 x16 /
  * K4V2 x32 tiles.  Persistent CTAs; each keeps its units' logits in its own two buffers of the arena's
- * off_tc_scratch (a unit's significance pass runs during the CTA's next unit). */
+ * off_tc_scratch (a unit's significance pass runs during the CTA's next unit).  With fewer ACTIVE units than SMs
+ * and a longest request of >= 2048 tokens, the split-sequence form runs instead: each unit's pages split
+ * over up to 32 CTAs whose partial softmax states are merged; same results to the same tolerances. */
 dkv_status_t dkv_attend_tc(dkv_pool_t p, const uint16_t* d_q, float* d_out, float* d_probs, dkv_stream_t s);
 
 /* Debug audit of the pool's invariants on the device (SURVEY §8 audit row): the memory layout of P:466-500
