@@ -1055,11 +1055,11 @@ static cudaError_t launch_tc(const PoolDev& p, const uint16_t* q, float* out, fl
     return e;
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   if (grid > p.tc_slots) grid = p.tc_slots;                       // two scratch buffers per CTA slot
-  // split-sequence form: fewer active units than SMs, long enough to share (>= 2048 tokens, >= 8 pages per
-  // segment), and the partial states fit the scratch's second half
+  // split-sequence form: at most half as many active units as resident CTAs, long enough to share (>= 2048
+  // tokens, >= 8 pages per segment), and the partial states fit the scratch's second half
   const int pages = max_len / 16;
   int NS = 1;
-  if (DKV_TC_SPLIT && active_units > 0 && active_units < sms && max_len >= 2048 && p.U <= p.tc_slots) {
+  if (DKV_TC_SPLIT && active_units > 0 && 2 * active_units <= grid && max_len >= 2048 && p.U <= p.tc_slots) {
     NS = grid / active_units;
     if (NS > kTcSplitMax) NS = kTcSplitMax;
     if (NS > pages / 8) NS = pages / 8;

@@ -16,7 +16,8 @@ from tests.gpu_backend import GpuBackend  # noqa: E402
 for name, kw, lens in (("1 req x 2 heads, 30k", dict(R=1, Ly=1, H=2, M=33792, P=4000, q_per_kv=8, alpha_l=0.0,
                                                       mix=(0.4, 0.6, 0.0)), [30000]),
                        ("4 req x 8 heads, 16k", dict(R=4, Ly=1, H=8, M=17408, P=40000, q_per_kv=4), [16000] * 4),
-                       ("16 req x 8 heads, 8k", dict(R=16, Ly=1, H=8, M=9216, P=90000, q_per_kv=4), [8000] * 16)):
+                       ("16 req x 8 heads, 8k", dict(R=16, Ly=1, H=8, M=9216, P=90000, q_per_kv=4), [8000] * 16),
+                       ("32 req x 8 heads, 8k", dict(R=32, Ly=1, H=8, M=9216, P=180000, q_per_kv=4), [8000] * 32)):
     scn = H.TINY.replace(d=128, W=64, seed=13, alpha_h=1.0, **kw)
     g = GpuBackend(scn)
     H.admit([g], H.Inputs(scn), H.Lifecycle(scn), list(range(len(lens))), lens)
@@ -34,3 +35,4 @@ for name, kw, lens in (("1 req x 2 heads, 30k", dict(R=1, Ly=1, H=2, M=33792, P=
         if i:
             ts.append(e0.elapsed_time(e1))
     print(f"{name}: {statistics.mean(ts):.3f} ms ({scn.U} units)")
+    del g
