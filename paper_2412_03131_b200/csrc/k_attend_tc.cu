@@ -42,6 +42,9 @@ namespace dkv {
 #ifndef DKV_TC_STAGES
 #define DKV_TC_STAGES 2         // pages in flight per warp (measured: 2 beats 3, tools/tc_ab.sh, profiles/r2o_tc_ab.log)
 #endif
+#ifndef DKV_TC_K8_BIASED
+#define DKV_TC_K8_BIASED 0      // K8 key operands left at 1024 + c (the bias folded into z): A/B of precision and time
+#endif
 #ifndef DKV_TC_MINB
 #define DKV_TC_MINB 4           // CTAs per SM the register budget is sized for
 #endif
@@ -270,8 +273,13 @@ __device__ __forceinline__ void tc_chunk(const uint8_t* seg, int ch, int cnt, co
       constexpr int g = decltype(gi)::value;
       uint32_t a0, a1, a2, a3;
       if constexpr (CL::kbits == 8) {
+#if DKV_TC_K8_BIASED
+        a0 = __byte_perm(w0[g], 0x64646464u, 0x4140); a2 = __byte_perm(w0[g], 0x64646464u, 0x4342);   // 1024 + c
+        a1 = __byte_perm(w1[g], 0x64646464u, 0x4140); a3 = __byte_perm(w1[g], 0x64646464u, 0x4342);
+#else
         k8_pairs(w0[g], a0, a2);                         // features 4g .. 4g+3 = word g of the run
         k8_pairs(w1[g], a1, a3);
+#endif
       } else {
         static_assert(CL::kbits == 4, "tensor-core path: K8 or K4 keys");
         k4_pairs<2 * (g & 1)>(w0[g >> 1], a0, a2);       // bytes 2g, 2g+1 of the run
@@ -291,7 +299,12 @@ __device__ __forceinline__ void tc_chunk(const uint8_t* seg, int ch, int cnt, co
     const uint32_t km = *reinterpret_cast<const uint32_t*>(seg + CL::off_kmeta + 4 * t);
     const uint32_t vm = *reinterpret_cast<const uint32_t*>(seg + CL::off_vmeta + 4 * t);
     const float ks = __half2float(__ushort_as_half((unsigned short)(km & 0xFFFFu)));
+#if DKV_TC_K8_BIASED
+    const float kz = CL::kbits == 8 ? fmaf(ks, -1024.0f, __half2float(__ushort_as_half((unsigned short)(km >> 16))))
+                                    : tc_zc<CL::kbits>(__half2float(__ushort_as_half((unsigned short)(km >> 16))), ks);
+#else
     const float kz = tc_zc<CL::kbits>(__half2float(__ushort_as_half((unsigned short)(km >> 16))), ks);
+#endif
     const float vs = __half2float(__ushort_as_half((unsigned short)(vm & 0xFFFFu)));
     const float vz = tc_zc<CL::vbits>(__half2float(__ushort_as_half((unsigned short)(vm >> 16))), vs);
     svs[rr] = tok ? vs * kPvScale : 0.0f;                // an absent token's stale meta never reaches a product
