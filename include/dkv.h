@@ -148,6 +148,9 @@ typedef struct {
                                   when it is ACTIVE else 0, 0}: written by dkv_classify(DECODE) (existing pages,
                                   N) and by dkv_compact_alloc (granted pages), read by dkv_quant_write(DECODE)
                                   instead of the tables and the request state */
+  int64_t off_tsum;            /* uint32[2][num_tiles][2] decode tile sums {demand, freed pages} that
+                                  dkv_classify(DECODE) accumulates for the following dkv_compact_alloc (by the
+                                  parity of the call counter) */
   int64_t off_tc_scratch;      /* dkv_attend_tc: 2 x 592 buffers of (max_seq_len rounded to 32, + 64) * (4 if
                                   q_per_kv <= 4 else 8) fp32 logit rows, two per persistent CTA (0 bytes when
                                   q_per_kv = 0 or with the FP16 tier) */

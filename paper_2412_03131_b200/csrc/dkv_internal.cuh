@@ -32,7 +32,10 @@ struct Ctrl {
   int32_t pending;
   int32_t qw_status;
   int32_t pad32;
-  int64_t pad[2];
+  // decode tile sums (classify → compact_alloc): the epoch whose sums dkv_classify(DECODE) accumulated in tsum,
+  // and the tiles of each compact_alloc call that have read their entry state (monotonic, num_tiles per call)
+  unsigned long long tsum_ticket;
+  unsigned long long arrive2;
 };
 static_assert(sizeof(Ctrl) <= 256, "ctrl block");
 
@@ -97,6 +100,7 @@ struct PoolDev {
   int64_t* stats;       // int64[4] admission counters
   FastDiv div_LyH, div_W, div_Ch, div_Cl;   // u -> request, position -> window slot, slot -> (page, index)
   int64_t* tile_sums;   // [num_tiles][3] prompt-workflow scan scratch
+  uint32_t* tsum;       // [2][num_tiles][2] decode tile sums {demand, freed pages} by ticket parity (classify)
   int32_t* rec;         // [U][3] deferred recycle: {ring offset from the end pointer, ph, freed pages}
   float* win_sig;       // [U][W] significance of the window tokens (NEXT-2)
   int32_t* secmin;      // [U][8] {sig_h, pos_h, slot_h, sig_l, pos_l, slot_l, valid, 0} from dkv_attend

@@ -98,6 +98,7 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   int cls = DKV_CLS_NONE, n = 0, nh = 0, nl = 0;
   float sc = 0.0f, th = 0.0f, tl = 0.0f, tt = 0.0f;
   int nlive = 0;                                                 // N if the request is ACTIVE (for quant_write)
+  int frp = 0;                                                   // pages a freed request's unit returns (a3)
   {
     const int8_t st = p.req_state[r];
     const int N = p.seq_len[r] + 1;                              // Q3: includes this step's token
@@ -107,6 +108,8 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
                                 : (p.W > 0 && N - 1 - p.W >= 0 ? p.win_sig[(size_t)u * p.W + (N - 1 - p.W) % p.W] : 0.0f);
     const int nh_in = p.n_h[u], nl_in = p.n_l[u];
     const int nt_in = TOP ? p.n_t[u] : 0;
+    if (st == DKV_REQ_PENDING_FREE)
+      frp = (TOP ? (nt_in + p.Ct - 1) / p.Ct : 0) + (nh_in + p.Ch - 1) / p.Ch + (nl_in + p.Cl - 1) / p.Cl;
     const int pc = N - 1 - p.W;                                  // t_c = earliest window token
     if (st == DKV_REQ_ACTIVE && pc >= 0) {
 #if DKV_CD_PREFETCH
@@ -358,6 +361,15 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   w.x = (int)((uint32_t)tc_class | ((uint32_t)v_action << 8) | ((uint32_t)grow << 16) | ((uint32_t)demand << 24));
   w.y = v_slot; w.z = tc_slot; w.w = v_dst_slot;
   reinterpret_cast<int4*>(dec)[u] = w;
+  // the following dkv_compact_alloc's tile sums (demand, freed pages per scan tile), by the parity of its call
+  // counter: with them it needs no look-back across tiles (k_compact.cu)
+  {
+    const unsigned long long tk = __ldg(&p.ctrl->ticket);       // not written before that call
+    uint32_t* ts = p.tsum + 2 * ((size_t)(tk & 1ull) * p.num_tiles + u / p.tile_units);
+    if (demand) atomicAdd(ts, 1u);
+    if (frp) atomicAdd(ts + 1, (uint32_t)frp);
+    if (u == 0) p.ctrl->tsum_ticket = tk;
+  }
   // The page IDs dkv_quant_write(DECODE) will touch, so that it reads no table: t_c's page (which is also the
   // victim's KV_h page when the victim is downgraded, since t_c takes its slot, Q8) and the KV_l page a
   // downgraded victim moves to.  A page the growing section receives this step is not known yet: -1 here,

@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   __shared__ unsigned long long s_epoch;
   __shared__ int64_t s_start0, s_free0, s_D, s_F;
   __shared__ int s_status0;
+  __shared__ unsigned long long s_tst;
   __shared__ uint32_t s_wdem[NW], s_wfr[NW];
   __shared__ uint32_t s_exdem, s_exfr, s_incdem, s_incfr;
 
@@ -81,6 +82,13 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
     const int a = ld_volatile(&ctrl->status);
     s_status0 = a != 0 ? a : ld_volatile(&ctrl->pending);
   }
+  if (tid == 128) s_tst = *(volatile unsigned long long*)&ctrl->tsum_ticket;
+  // decode tile sums left by dkv_classify for both ticket parities (the parity is known after the barrier)
+  uint2 ts0 = make_uint2(0u, 0u), ts1 = ts0;
+  if (phase == DKV_PHASE_DECODE && tid < 32 && tid < p.num_tiles) {
+    ts0 = __ldcg(reinterpret_cast<const uint2*>(p.tsum) + tid);
+    ts1 = __ldcg(reinterpret_cast<const uint2*>(p.tsum) + p.num_tiles + tid);
+  }
   if (u < p.U) {
     if (phase == DKV_PHASE_DECODE) dword = __ldg(reinterpret_cast<const uint32_t*>(dec + u));
     else { pfh = p.pf_nh[u]; pfl = p.pf_nl[u]; if (p.top) pft = p.pf_nt[u]; }
@@ -91,6 +99,15 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   const int64_t start0 = s_start0, free0 = s_free0;
   const int status0 = s_status0;
   const int P = p.P, L = p.L;
+  // every tile has read its entry state (ctrl, request states): counted for the tile that rewrites them
+  if (tid == 0) atomicAdd(&ctrl->arrive2, 1ull);
+  // this call's tile-sum buffer is tsum[epoch & 1]; the other one is the next classify's: cleared here
+  if (tid == 32) reinterpret_cast<uint2*>(p.tsum)[(size_t)((epoch & 1ull) ^ 1ull) * p.num_tiles + tile] = make_uint2(0u, 0u);
+  // Tile sums instead of the look-back (decode, no error, the fast path's free region, and sums this step's
+  // dkv_classify accumulated for this very call): every tile's exclusive demand / freed offsets follow from
+  // the sums directly, with no wait on another tile
+  const bool use_ts = phase == DKV_PHASE_DECODE && alloc && status0 == 0 && free0 >= (int64_t)p.U &&
+                      s_tst == epoch && p.num_tiles <= 32;
 
   // ---- per-unit demand and freed pages (planning results)
   int grow = 0;
@@ -126,10 +143,14 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
     const uint32_t ia = warp_incl_scan(a, lane), ib = warp_incl_scan(b, lane);
     if (lane < NW) { s_wdem[lane] = ia - a; s_wfr[lane] = ib - b; }
     const uint32_t tot_dem = __shfl_sync(kFull, ia, 31), tot_fr = __shfl_sync(kFull, ib, 31);
-    // ---- decoupled look-back across tiles
+    // ---- decoupled look-back across tiles (or the tile sums)
     unsigned long long* stat = p.tile_status;
     uint32_t ex_d = 0, ex_f = 0;
-    if (tile == 0) {
+    if (use_ts) {
+      const uint2 t = (epoch & 1ull) ? ts1 : ts0;                  // lane = tile
+      ex_d = __reduce_add_sync(kFull, lane < tile ? t.x : 0u);
+      ex_f = __reduce_add_sync(kFull, lane < tile ? t.y : 0u);
+    } else if (tile == 0) {
       if (lane == 0) st_release(&stat[0], pack_status(tag, kFlagPre, tot_fr, tot_dem));
     } else {
       if (lane == 0) st_release(&stat[tile], pack_status(tag, kFlagAgg, tot_fr, tot_dem));
@@ -333,8 +354,13 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   }
   // ---- request-level transitions, by the tile owning the request's LAST unit: every other tile holding
   // units of the request is a predecessor, and has read req_state before publishing its look-back status
+  // (with the tile sums there is no look-back: the tile waits for every tile's entry reads instead; only a
+  // freed request's state is read by other tiles — compact_alloc never reads seq_len)
+  const unsigned long long all_read = (epoch + 1ull) * (unsigned long long)p.num_tiles;
   if (u < p.U && u % p.LyH == p.LyH - 1) {
     if (st == DKV_REQ_PENDING_FREE) {
+      if (use_ts)
+        while (ld_acquire(&ctrl->arrive2) < all_read) __nanosleep(32);
       p.req_state[r] = DKV_REQ_IDLE; p.seq_len[r] = 0; p.prompt_len[r] = 0;
     } else if (ok && phase == DKV_PHASE_DECODE && st == DKV_REQ_ACTIVE) {
       p.seq_len[r] += 1;
@@ -345,6 +371,8 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   // ---- pointers: every tile read them before publishing its look-back status, so the last tile (whose
   // inclusive prefix holds the totals) may write them in the fast path; tile 0 after the barrier otherwise
   if (tid == 0 && (fast ? tile == p.num_tiles - 1 : tile == 0)) {
+    if (use_ts)                                                  // every tile has read the pointers and ticket
+      while (ld_acquire(&ctrl->arrive2) < all_read) __nanosleep(32);
     if (fast) { D = s_incdem; F = s_incfr; }
     const int64_t free_avail = free0 + F;
     if (status0 != 0) set_status(ctrl, status0);      // classify's pending error becomes the sticky status

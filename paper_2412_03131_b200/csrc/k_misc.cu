@@ -19,11 +19,13 @@ __global__ void init_kernel(PoolDev p) {
     p.req_state[i] = DKV_REQ_IDLE; p.seq_len[i] = 0; p.prompt_len[i] = 0; p.admit[i] = 0;
   }
   for (size_t i = tid; i < (size_t)p.num_tiles; i += nth) p.tile_status[i] = 0ull;
+  for (size_t i = tid; i < 4 * (size_t)p.num_tiles; i += nth) p.tsum[i] = 0u;
   if (tid == 0) {
     Ctrl* c = p.ctrl;
     c->start = 0; c->free = p.P; c->status = 0; c->oom_count = 0;
     c->ticket = 0ull; c->arrive = 0ull; c->last_demand = 0; c->last_freed = 0;
     c->total_dem = 0; c->total_fr = 0; c->bar_epoch = 0ull;
+    c->tsum_ticket = ~0ull; c->arrive2 = 0ull;
     p.stats[0] = p.P; p.stats[1] = 0; p.stats[2] = 0; p.stats[3] = 0;
   }
 }

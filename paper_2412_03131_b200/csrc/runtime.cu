@@ -116,6 +116,7 @@ bool make_layout(const dkv_config_t* c, Geometry& G, dkv_layout_t& Lo) {
   Lo.off_stats = take(32);
   Lo.off_tile_status = take(8 * (int64_t)G.num_tiles);
   Lo.off_tile_sums = take(24 * (int64_t)G.num_tiles);
+  Lo.off_tsum = take(16 * (int64_t)G.num_tiles);
   Lo.off_rec = take(16 * (int64_t)G.U);
   Lo.off_win_sig = take(4 * (int64_t)G.U * c->window);
   Lo.off_secmin = take(32 * (int64_t)G.U);
@@ -277,6 +278,7 @@ dkv_status_t dkv_pool_init(const dkv_config_t* cfg, void* d_arena, size_t arena_
   d.stats = (int64_t*)(b + Lo.off_stats);
   d.tile_status = (unsigned long long*)(b + Lo.off_tile_status);
   d.tile_sums = (int64_t*)(b + Lo.off_tile_sums);
+  d.tsum = (uint32_t*)(b + Lo.off_tsum);
   d.rec = (int32_t*)(b + Lo.off_rec);
   d.win_sig = (float*)(b + Lo.off_win_sig);
   d.secmin = (int32_t*)(b + Lo.off_secmin);

@@ -73,6 +73,7 @@ class dkv_layout_t(C.Structure):
                                                                   ("row_top", C.c_int32), ("off_k_top", C.c_int32),
                                                                   ("off_v_top", C.c_int32), ("off_score_top", C.c_int32),
                                                                   ("off_pos_top", C.c_int32), ("off_qpid", C.c_int64),
+                                                                  ("off_tsum", C.c_int64),
                                                                   ("off_tc_scratch", C.c_int64)]
 
 
