@@ -44,6 +44,21 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
   return v;
 }
 
+#ifndef DKV_CA_TRACE
+#define DKV_CA_TRACE 0      // debug builds: globaltimer marks of the last tile's phases into rec[0..11] (tools/ca_trace.py)
+#endif
+__device__ __forceinline__ void ca_mark(const PoolDev& p, int idx) {
+#if DKV_CA_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == gridDim.x - 1) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    reinterpret_cast<unsigned long long*>(p.rec)[idx] = t;
+  }
+#else
+  (void)p; (void)idx;
+#endif
+}
+
 template <int TU>
 __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, int phase, int alloc, int defer_rec) {
   constexpr int NW = TU / 32;
@@ -63,6 +78,7 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   // per-unit loads do not depend on the control block: issue them before the first barrier; the request
   // state and counts are not written by dkv_classify, so they may be read before the PDL wait
   const int u = tile * TU + tid;
+  ca_mark(p, 0);
   int st = -1, r = 0, nh = 0, nl = 0, nt = 0;
   uint32_t dword = 0;
   int pfh = 0, pfl = 0, pft = 0;
@@ -85,15 +101,19 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   if (tid == 128) s_tst = *(volatile unsigned long long*)&ctrl->tsum_ticket;
   // decode tile sums left by dkv_classify for both ticket parities (the parity is known after the barrier)
   uint2 ts0 = make_uint2(0u, 0u), ts1 = ts0;
-  if (phase == DKV_PHASE_DECODE && tid < 32 && tid < p.num_tiles) {
-    ts0 = __ldcg(reinterpret_cast<const uint2*>(p.tsum) + tid);
-    ts1 = __ldcg(reinterpret_cast<const uint2*>(p.tsum) + p.num_tiles + tid);
+  if (phase == DKV_PHASE_DECODE && lane < p.num_tiles) {      // every warp (lane = tile)
+    ts0 = __ldcg(reinterpret_cast<const uint2*>(p.tsum) + lane);
+    ts1 = __ldcg(reinterpret_cast<const uint2*>(p.tsum) + p.num_tiles + lane);
   }
   if (u < p.U) {
     if (phase == DKV_PHASE_DECODE) dword = __ldg(reinterpret_cast<const uint32_t*>(dec + u));
     else { pfh = p.pf_nh[u]; pfl = p.pf_nl[u]; if (p.top) pft = p.pf_nt[u]; }
   }
+  // the request state has arrived in every thread before the barrier, so that the arrival count below orders
+  // every read of it before a rewrite by another tile
+  asm volatile("" ::"r"((int)st));
   __syncthreads();
+  ca_mark(p, 1);
   const unsigned long long epoch = s_epoch;
   const uint32_t tag = (uint32_t)(epoch & 63ull);
   const int64_t start0 = s_start0, free0 = s_free0;
@@ -138,50 +158,70 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   const uint32_t inc_fr = warp_incl_scan(fr, lane);
   if (lane == 31) { s_wdem[warp] = inc_dem; s_wfr[warp] = inc_fr; }
   __syncthreads();
-  if (warp == 0) {
-    uint32_t a = lane < NW ? s_wdem[lane] : 0u, b = lane < NW ? s_wfr[lane] : 0u;
-    const uint32_t ia = warp_incl_scan(a, lane), ib = warp_incl_scan(b, lane);
-    if (lane < NW) { s_wdem[lane] = ia - a; s_wfr[lane] = ib - b; }
-    const uint32_t tot_dem = __shfl_sync(kFull, ia, 31), tot_fr = __shfl_sync(kFull, ib, 31);
-    // ---- decoupled look-back across tiles (or the tile sums)
-    unsigned long long* stat = p.tile_status;
-    uint32_t ex_d = 0, ex_f = 0;
-    if (use_ts) {
-      const uint2 t = (epoch & 1ull) ? ts1 : ts0;                  // lane = tile
-      ex_d = __reduce_add_sync(kFull, lane < tile ? t.x : 0u);
-      ex_f = __reduce_add_sync(kFull, lane < tile ? t.y : 0u);
-    } else if (tile == 0) {
-      if (lane == 0) st_release(&stat[0], pack_status(tag, kFlagPre, tot_fr, tot_dem));
-    } else {
-      if (lane == 0) st_release(&stat[tile], pack_status(tag, kFlagAgg, tot_fr, tot_dem));
-      int look = tile - 1;
-      while (true) {
-        const int idx = look - lane;
-        const unsigned long long w = idx >= 0 ? ld_acquire(&stat[idx]) : pack_status(tag, kFlagPre, 0, 0);
-        const bool valid = st_tag(w) == tag && st_flag(w) != 0;
-        const unsigned vm = __ballot_sync(kFull, valid);
-        const unsigned pm = __ballot_sync(kFull, valid && st_flag(w) == kFlagPre);
-        if (pm) {
-          const int jl = __ffs(pm) - 1;
-          const unsigned need = (jl == 31) ? kFull : ((2u << jl) - 1u);
-          if ((vm & need) != need) continue;                     // a nearer predecessor not published yet
-          ex_d += __reduce_add_sync(kFull, lane <= jl ? st_dem(w) : 0u);
-          ex_f += __reduce_add_sync(kFull, lane <= jl ? st_fr(w) : 0u);
-          break;
+  ca_mark(p, 2);
+  uint32_t off_dem, off_fr, tile_ex_fr, tile_inc_fr, tile_inc_dem;
+  unsigned long long a2_early = 0ull;                            // the finalizer's first look at arrive2
+  if (use_ts) {
+    // every warp on its own: the warps before it from the shared warp totals, the tiles before it from the
+    // tile sums — no warp-0 pass and no further barrier
+    const uint2 t = (epoch & 1ull) ? ts1 : ts0;                    // lane = tile
+    const uint32_t wd = __reduce_add_sync(kFull, lane < warp ? s_wdem[lane] : 0u);
+    const uint32_t wf = __reduce_add_sync(kFull, lane < warp ? s_wfr[lane] : 0u);
+    const uint32_t ex_d = __reduce_add_sync(kFull, lane < tile ? t.x : 0u);
+    const uint32_t ex_f = __reduce_add_sync(kFull, lane < tile ? t.y : 0u);
+    const uint2 mine = make_uint2(__shfl_sync(kFull, t.x, tile & 31), __shfl_sync(kFull, t.y, tile & 31));
+    off_dem = ex_d + wd + inc_dem - (dem != 0);
+    off_fr = ex_f + wf + inc_fr - fr;
+    tile_ex_fr = ex_f; tile_inc_fr = ex_f + mine.y; tile_inc_dem = ex_d + mine.x;
+    if (tid == 0 && tile == p.num_tiles - 1) a2_early = *(volatile unsigned long long*)&ctrl->arrive2;   // no stall
+  } else {
+    if (warp == 0) {
+      uint32_t a = lane < NW ? s_wdem[lane] : 0u, b = lane < NW ? s_wfr[lane] : 0u;
+      const uint32_t ia = warp_incl_scan(a, lane), ib = warp_incl_scan(b, lane);
+      if (lane < NW) { s_wdem[lane] = ia - a; s_wfr[lane] = ib - b; }
+      const uint32_t tot_dem = __shfl_sync(kFull, ia, 31), tot_fr = __shfl_sync(kFull, ib, 31);
+      // ---- decoupled look-back across tiles (or the tile sums)
+      unsigned long long* stat = p.tile_status;
+      uint32_t ex_d = 0, ex_f = 0;
+      if (use_ts) {
+        const uint2 t = (epoch & 1ull) ? ts1 : ts0;                  // lane = tile
+        ex_d = __reduce_add_sync(kFull, lane < tile ? t.x : 0u);
+        ex_f = __reduce_add_sync(kFull, lane < tile ? t.y : 0u);
+      } else if (tile == 0) {
+        if (lane == 0) st_release(&stat[0], pack_status(tag, kFlagPre, tot_fr, tot_dem));
+      } else {
+        if (lane == 0) st_release(&stat[tile], pack_status(tag, kFlagAgg, tot_fr, tot_dem));
+        int look = tile - 1;
+        while (true) {
+          const int idx = look - lane;
+          const unsigned long long w = idx >= 0 ? ld_acquire(&stat[idx]) : pack_status(tag, kFlagPre, 0, 0);
+          const bool valid = st_tag(w) == tag && st_flag(w) != 0;
+          const unsigned vm = __ballot_sync(kFull, valid);
+          const unsigned pm = __ballot_sync(kFull, valid && st_flag(w) == kFlagPre);
+          if (pm) {
+            const int jl = __ffs(pm) - 1;
+            const unsigned need = (jl == 31) ? kFull : ((2u << jl) - 1u);
+            if ((vm & need) != need) continue;                     // a nearer predecessor not published yet
+            ex_d += __reduce_add_sync(kFull, lane <= jl ? st_dem(w) : 0u);
+            ex_f += __reduce_add_sync(kFull, lane <= jl ? st_fr(w) : 0u);
+            break;
+          }
+          if (vm == kFull) {
+            ex_d += __reduce_add_sync(kFull, st_dem(w));
+            ex_f += __reduce_add_sync(kFull, st_fr(w));
+            look -= 32;
+          }
         }
-        if (vm == kFull) {
-          ex_d += __reduce_add_sync(kFull, st_dem(w));
-          ex_f += __reduce_add_sync(kFull, st_fr(w));
-          look -= 32;
-        }
+        if (lane == 0) st_release(&stat[tile], pack_status(tag, kFlagPre, ex_f + tot_fr, ex_d + tot_dem));
       }
-      if (lane == 0) st_release(&stat[tile], pack_status(tag, kFlagPre, ex_f + tot_fr, ex_d + tot_dem));
+      if (lane == 0) { s_exdem = ex_d; s_exfr = ex_f; s_incdem = ex_d + tot_dem; s_incfr = ex_f + tot_fr; }
     }
-    if (lane == 0) { s_exdem = ex_d; s_exfr = ex_f; s_incdem = ex_d + tot_dem; s_incfr = ex_f + tot_fr; }
+    __syncthreads();
+    off_dem = s_exdem + s_wdem[warp] + inc_dem - (phase == DKV_PHASE_DECODE ? (dem != 0) : dem);
+    off_fr = s_exfr + s_wfr[warp] + inc_fr - fr;
+    tile_ex_fr = s_exfr; tile_inc_fr = s_incfr; tile_inc_dem = s_incdem;
   }
-  __syncthreads();
-  const uint32_t off_dem = s_exdem + s_wdem[warp] + inc_dem - (phase == DKV_PHASE_DECODE ? (dem != 0) : dem);
-  const uint32_t off_fr = s_exfr + s_wfr[warp] + inc_fr - fr;
+  ca_mark(p, 3);
 
   // ---- recycle: freed IDs -> ring[(end + off + k) mod P], canonical slot order (Q13).  The tile's freed
   // slots form one flat list (k = tile-local exclusive scan of the freed counts + slot rank), cut into one
@@ -193,8 +233,8 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
     constexpr int kRecDepth = 8;
     __shared__ uint32_t s_loc[TU];                               // tile-local exclusive freed offset
     __shared__ int s_nfr[TU], s_ph[TU], s_pt[TU];
-    const uint32_t tile_ex = s_exfr;
-    const uint32_t Ft = s_incfr - tile_ex;                       // freed slots in this tile
+    const uint32_t tile_ex = tile_ex_fr;
+    const uint32_t Ft = tile_inc_fr - tile_ex;                   // freed slots in this tile
     // deferred: in the decode fast path (grants never read a slot recycled in this call) the copy is left to
     // the following dkv_quant_write(DECODE) (quant_decode_kernel, over all SMs — here it would run on the one
     // or two CTAs whose tile holds the request); this kernel records each freed unit's offset from the end
@@ -274,7 +314,7 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   const bool fast = (status0 != 0) || (phase == DKV_PHASE_DECODE && free0 >= (int64_t)p.U);
   // the recycle copies above are complete before a grant (or the grid barrier) — a barrier needed only when
   // this tile copied in place: a deferred (decode fast path) recycle writes no ring slot here
-  if (!fast || (s_incfr - s_exfr > 0 && !(defer_rec && phase == DKV_PHASE_DECODE && status0 == 0 && free0 >= (int64_t)p.U)))
+  if (!fast || (tile_inc_fr - tile_ex_fr > 0 && !(defer_rec && phase == DKV_PHASE_DECODE && status0 == 0 && free0 >= (int64_t)p.U)))
     __syncthreads();
   bool ok;
   int64_t D = 0, F = 0;
@@ -352,6 +392,7 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
       }
     }
   }
+  ca_mark(p, 4);
   // ---- request-level transitions, by the tile owning the request's LAST unit: every other tile holding
   // units of the request is a predecessor, and has read req_state before publishing its look-back status
   // (with the tile sums there is no look-back: the tile waits for every tile's entry reads instead; only a
@@ -371,9 +412,9 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
   // ---- pointers: every tile read them before publishing its look-back status, so the last tile (whose
   // inclusive prefix holds the totals) may write them in the fast path; tile 0 after the barrier otherwise
   if (tid == 0 && (fast ? tile == p.num_tiles - 1 : tile == 0)) {
-    if (use_ts)                                                  // every tile has read the pointers and ticket
+    if (use_ts && a2_early < all_read)                           // every tile has read the pointers and ticket
       while (ld_acquire(&ctrl->arrive2) < all_read) __nanosleep(32);
-    if (fast) { D = s_incdem; F = s_incfr; }
+    if (fast) { D = tile_inc_dem; F = tile_inc_fr; }
     const int64_t free_avail = free0 + F;
     if (status0 != 0) set_status(ctrl, status0);      // classify's pending error becomes the sticky status
     ctrl->pending = 0;
@@ -393,6 +434,7 @@ __global__ void __launch_bounds__(TU) compact_alloc_kernel(PoolDev p, const dkv_
     ctrl->qw_status = fin;                             // entry status of the following dkv_quant_write (Q36)
     p.stats[3] = (int64_t)fin;                         // <= 0: the MIN over GPUs shows any error
   }
+  ca_mark(p, 5);
 }
 
 template <int TU>
