@@ -73,8 +73,10 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   const int32_t sp_h1 = lane + 32 < p.L ? __ldg(row + lane + 32) : 0;
   const int32_t sp_l0 = lane < p.L ? __ldg(row + p.L - 1 - lane) : 0;
   const bool dead = __ldg(&p.ctrl->status) != 0;
+  const unsigned long long tk = __ldg(&p.ctrl->ticket);         // the following compact_alloc's call counter
 #else
   const bool dead = ld_volatile(&p.ctrl->status) != 0;
+  const unsigned long long tk = *(volatile const unsigned long long*)&p.ctrl->ticket;
 #endif
   // sticky error at entry (Q36: one snapshot per call; classify kernels never write `status`): the unit's
   // decision is the empty one, nothing else happens
@@ -364,7 +366,6 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   // the following dkv_compact_alloc's tile sums (demand, freed pages per scan tile), by the parity of its call
   // counter: with them it needs no look-back across tiles (k_compact.cu)
   {
-    const unsigned long long tk = __ldg(&p.ctrl->ticket);       // not written before that call
     uint32_t* ts = p.tsum + 2 * ((size_t)(tk & 1ull) * p.num_tiles + u / p.tile_units);
     if (demand) atomicAdd(ts, 1u);
     if (frp) atomicAdd(ts + 1, (uint32_t)frp);
