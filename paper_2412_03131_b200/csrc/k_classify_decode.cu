@@ -366,9 +366,11 @@ classify_decode_kernel(PoolDev p, const float* __restrict__ cand_sig, dkv_decisi
   // the following dkv_compact_alloc's tile sums (demand, freed pages per scan tile), by the parity of its call
   // counter: with them it needs no look-back across tiles (k_compact.cu)
   {
-    uint32_t* ts = p.tsum + 2 * ((size_t)(tk & 1ull) * p.num_tiles + u / p.tile_units);
-    if (demand) atomicAdd(ts, 1u);
-    if (frp) atomicAdd(ts + 1, (uint32_t)frp);
+    if (demand | frp) {                                          // tile_units is a power of two
+      uint32_t* ts = p.tsum + 2 * ((size_t)(tk & 1ull) * p.num_tiles + (u >> (__ffs(p.tile_units) - 1)));
+      if (demand) atomicAdd(ts, 1u);
+      if (frp) atomicAdd(ts + 1, (uint32_t)frp);
+    }
     if (u == 0) p.ctrl->tsum_ticket = tk;
   }
   // The page IDs dkv_quant_write(DECODE) will touch, so that it reads no table: t_c's page (which is also the
