@@ -60,7 +60,11 @@ def launches(tag, path):
     dper = {}
     for k, us in dec:
         dper.setdefault(k, []).append(us)
-    step = sum(statistics.mean(v) for v in dper.values()) if dper else 0.0
+    # per-step cost: a kernel's total over the decode phase / the number of steps (one classify per step), so the
+    # recycle kernel, which runs only in the steps that free a request, counts at its amortised cost
+    nsteps = max((len(v) for k, v in dper.items() if "classify_decode" in k), default=0) or 1
+    cost = {k: sum(v) / nsteps for k, v in dper.items()}
+    step = sum(cost.values())
     lines = [f"# {tag}: ncu launch list (`--metrics gpu__time_duration.sum --clock-control none`)", "",
              "Per-launch times are cold-cache and serialised (ncu replays each launch alone); the SHARE of each",
              "kernel in the decode step is what bench.py's live CUDA-event timing must agree with.", "",
@@ -69,9 +73,9 @@ def launches(tag, path):
     for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
         share = ""
         if k in dper:
-            share = f"{100 * statistics.mean(dper[k]) / step:.1f}%"
+            share = f"{100 * cost[k] / step:.1f}%"
         lines.append(f"| {k} | {len(v)} | {statistics.mean(v):.2f} | {min(v):.2f} | {max(v):.2f} | {share} |")
-    lines += ["", f"Decode step (sum of per-kernel means over the {len(dec)} decode-phase launches): {step:.2f} us", ""]
+    lines += ["", f"Decode step ({len(dec)} decode-phase launches over {nsteps} steps, per-step total): {step:.2f} us", ""]
     return "\n".join(lines)
 
 
