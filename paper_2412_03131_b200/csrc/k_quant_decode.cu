@@ -30,7 +30,10 @@
 
 namespace dkv {
 
-constexpr int kQDThreads = 256;
+#ifndef DKV_QD_THREADS
+#define DKV_QD_THREADS 256
+#endif
+constexpr int kQDThreads = DKV_QD_THREADS;
 #ifndef DKV_QD_LANES
 #define DKV_QD_LANES 8     // lanes per unit; measured best at d = 128 (profiles/r1g_quant_decode_compact_ab.log)
 #endif
@@ -314,7 +317,9 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
   // upc <= kQDThreads / G units per CTA per iteration (the launch balances them over the resident CTAs); the
   // groups beyond upc have no unit
   const int gslot = threadIdx.x / G;
-  __shared__ __align__(16) uint16_t s_new[2][kQDThreads * EPL];   // the new token's K / V rows, this lane's part
+  // this lane's part of the new token's K / V rows [0] [1] and of t_c's window K / V rows [2] [3], staged by
+  // cp.async so no registers are held across the downgrade while they are in flight
+  __shared__ __align__(16) uint16_t s_new[4][kQDThreads * EPL];
   __shared__ int32_t s_status;
   const int lane = threadIdx.x & 31;
   const int q = lane % G;
@@ -341,6 +346,8 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
   if (dead && !rec_on) return;
   uint16_t* const my_nk = &s_new[0][threadIdx.x * EPL];
   uint16_t* const my_nv = &s_new[1][threadIdx.x * EPL];
+  uint16_t* const my_wk = &s_new[2][threadIdx.x * EPL];
+  uint16_t* const my_wv = &s_new[3][threadIdx.x * EPL];
 
   for (; gslot < upc && u0 + ub * upc < u1; ub += gridDim.x) {   // units [u0, u1)
     const int u = u0 + ub * upc + gslot;
@@ -364,18 +371,17 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
     const float s_in_given = cand_sig ? __ldg(cand_sig + u) : 0.0f;
     stage_row<EPL>(my_nk, knew + (size_t)u * D + q * EPL);
     stage_row<EPL>(my_nv, vnew + (size_t)u * D + q * EPL);
-    cp_async_commit();
     uint16_t* wk_row = nullptr;
     uint16_t* wv_row = nullptr;
-    HVec<EPL> wk, wv;
     int ws = 0;
     if (p.W > 0 && live) {
       ws = fmod_(p.div_W, N - 1);
       wk_row = reinterpret_cast<uint16_t*>(p.win_k) + ((size_t)u * p.W + ws) * D;
       wv_row = reinterpret_cast<uint16_t*>(p.win_v) + ((size_t)u * p.W + ws) * D;
-      wk = load_hvec<EPL>(wk_row, q);
-      wv = load_hvec<EPL>(wv_row, q);
+      stage_row<EPL>(my_wk, wk_row + q * EPL);
+      stage_row<EPL>(my_wv, wv_row + q * EPL);
     }
+    cp_async_commit();
     // t_c's significance: given, or (NEXT-2, cand_sig NULL) the running mean kept for its window slot
     const float s_in = cand_sig ? s_in_given : (p.W > 0 && live ? p.win_sig[(size_t)u * p.W + ws] : 0.0f);
     const int pc = N - 1 - p.W;
@@ -441,10 +447,11 @@ quant_decode_kernel(PoolDev p, const dkv_decision_t* __restrict__ dec, const uin
     }
 
     // ---- 2. t_c -> its section slot at its class bits
-    cp_async_wait<0>();                                  // this lane's part of the new token is in smem
+    cp_async_wait<0>();                                  // this lane's part of the new token and t_c's row are in smem
     bool rejected = false;                               // Q30: a non-finite t_c leaves slot and window as they are
     if (has_tc) {                                        // group-uniform
-      if (p.W == 0) { wk = lds_hvec<EPL>(my_nk); wv = lds_hvec<EPL>(my_nv); }   // t_c is the new token
+      const HVec<EPL> wk = lds_hvec<EPL>(p.W == 0 ? my_nk : my_wk);   // W == 0: t_c is the new token
+      const HVec<EPL> wv = lds_hvec<EPL>(p.W == 0 ? my_nv : my_wv);
       if (tc_top) {                                      // NEXT-4 (Q40): t_c kept as its fp16 rows
         bool fin = true;
 #pragma unroll
