@@ -31,8 +31,8 @@
 namespace dkv {
 
 #ifndef DKV_QD_THREADS
-#define DKV_QD_THREADS 256
-#endif
+#define DKV_QD_THREADS 224  // 28 units of 8 lanes: 4 CTAs x 224 threads x 72 registers fill the SM's register file
+#endif                      // with no spills, and 592 x 28 >= 16384 units take one pass (256: 64 registers, spills)
 constexpr int kQDThreads = DKV_QD_THREADS;
 #ifndef DKV_QD_LANES
 #define DKV_QD_LANES 8     // lanes per unit; measured best at d = 128 (profiles/r1g_quant_decode_compact_ab.log)
