@@ -263,6 +263,21 @@ def scatter_note(achieved):
             "source": j["source"]}
 
 
+def stream_mix_note(achieved):
+    """The bulk writer's DRAM mix is ~3.2 bytes read per byte written (ncu): context for its roofline fraction is
+    the measured rate of contiguous read:write streams at 3:1 and 4:1 on the same kind of box
+    (profiles/scatter_peaks.json); the reported `frac` stays against MEASURED_PEAKS.json."""
+    p = os.path.join(ROOT, "profiles", "scatter_peaks.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        j = json.load(f)
+    if "rw_stream_3to1_gbs" not in j:
+        return None
+    return {"rw_stream_3to1_gbs": j["rw_stream_3to1_gbs"], "rw_stream_4to1_gbs": j["rw_stream_4to1_gbs"],
+            "frac_of_3to1": round(achieved / j["rw_stream_3to1_gbs"], 3), "source": j["source"]}
+
+
 # ----------------------------------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local):
     from paper_2412_03131_b200 import Pool
@@ -781,7 +796,8 @@ def run_ours(args, rank, world, local):
         "roofline": {"kernel": "quant_prefill_kernel (dkv_quant_write PREFILL, bulk writer)", "bound": "hbm",
                      "achieved": round(bulk_gbs_rank, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": round(bulk_gbs_rank / peak, 4),
-                     "traffic": traffic("quant_prefill_kernel"), "traffic_unit": "bytes per launch"},
+                     "traffic": traffic("quant_prefill_kernel"), "traffic_unit": "bytes per launch",
+                     "access_pattern": stream_mix_note(bulk_gbs_rank)},
         "roofline_decode": {"kernel": "classify_decode_kernel", "bound": "hbm", "achieved": round(cls_gbs, 1),
                             "peak": peak, "unit": "GB/s", "frac": round(cls_gbs / peak, 4),
                             "algorithmic_bytes": int(statistics.mean(cls_bytes)),

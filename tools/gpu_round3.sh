@@ -18,3 +18,7 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:quan
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"classify_decode|compact_alloc|quant_decode" -s 27 -c 3 -o gpurun_out/prof_decode_$TAG python tools/decode_only.py --steps 11 > gpurun_out/prof_decode_$TAG.log 2>&1; echo "ncu decode rc=$?"
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:attend_tc -s 1 -c 1 -o gpurun_out/prof_attend_tc_$TAG python tools/decode_only.py --steps 3 --attend tc > gpurun_out/prof_attend_tc_$TAG.log 2>&1; echo "ncu attend_tc rc=$?"
 ls gpurun_out | grep $TAG
+if [ -n "$CONFIGS" ]; then
+  timeout 1500 python tools/bench_configs.py > gpurun_out/configs_$TAG.jsonl 2> gpurun_out/configs_$TAG.err; echo "configs rc=$?"
+fi
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gpurun_out/scatter_bench tools/scatter_bench.cu && timeout 300 gpurun_out/scatter_bench > gpurun_out/scatter_$TAG.log 2>&1; echo "scatter rc=$?"; cat gpurun_out/scatter_$TAG.log

@@ -1,6 +1,8 @@
 // scatter_bench.cu — the access-pattern ceiling of the classify scan (not product code): random 64-B / 128-B
 // segments gathered from a 15 GiB span by 16-B lane loads (4 / 8 lanes per segment, 8 loads in flight per
-// thread), next to a contiguous 16-B-per-lane stream.  Prints achieved GB/s (bytes requested / kernel time).
+// thread), next to a contiguous 16-B-per-lane stream; and, for the bulk writer, contiguous read+write streams
+// at R bytes read per byte written (R = 1: a copy; R = 3, 4 bracket the bulk writer's 3.2 : 1 DRAM mix).
+// Prints achieved GB/s (bytes requested / kernel time).
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scatter_bench tools/scatter_bench.cu
 #include <cstdint>
 #include <cstdio>
@@ -37,6 +39,18 @@ __global__ void stream(const uint4* __restrict__ buf, uint64_t n16, uint64_t* si
   }
   if (acc == 0x12345678u) sink[0] = acc;
 }
+template <int R>
+__global__ void rw_stream(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n_out) {
+  for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n_out; o += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 v[R];
+#pragma unroll
+    for (int j = 0; j < R; j++) v[j] = __ldcs(in + (uint64_t)j * n_out + o);   // R contiguous streams
+    uint4 w = v[0];
+#pragma unroll
+    for (int j = 1; j < R; j++) { w.x ^= v[j].x; w.y ^= v[j].y; w.z ^= v[j].z; w.w ^= v[j].w; }
+    __stcs(out + o, w);
+  }
+}
 int main() {
   const uint64_t span = 15ull << 30;
   uint4* buf;
@@ -64,6 +78,19 @@ int main() {
     stream<<<148 * 8, 256>>>(buf, n16, sink);
     cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
     printf("contiguous read      : %8.1f GB/s (4096 MB)\n", (double)(4ull << 30) / ms / 1e6);
+    // read R x 2 GiB + write 2 GiB (output in the upper part of the span)
+    const uint64_t n_out = (2ull << 30) / 16;
+    uint4* outp = buf + (12ull << 30) / 16;
+    for (int R = 1; R <= 4; R++) {
+      cudaEventRecord(a);
+      if (R == 1) rw_stream<1><<<148 * 8, 256>>>(buf, outp, n_out);
+      if (R == 2) rw_stream<2><<<148 * 8, 256>>>(buf, outp, n_out);
+      if (R == 3) rw_stream<3><<<148 * 8, 256>>>(buf, outp, n_out);
+      if (R == 4) rw_stream<4><<<148 * 8, 256>>>(buf, outp, n_out);
+      cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
+      printf("read:write %d:1 stream: %8.1f GB/s (%d MB)\n", R, (double)(R + 1) * (2ull << 30) / ms / 1e6,
+             (int)((R + 1) * 2048));
+    }
   }
   return 0;
 }
