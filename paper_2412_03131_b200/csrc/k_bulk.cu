@@ -268,6 +268,17 @@ quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const u
   const int seg = (int)(item % nseg_max);
   const long wi = item / nseg_max;                     // admitted unit index (i * LyH + j)
   if (wi >= (long)n * p.LyH) return;
+  // the segment's 256 scores, all in flight at once before anything else (phase A used to wait for them one
+  // 32-token step at a time: eight dependent round trips before the first K/V row was requested); indices up
+  // to sig_stride are inside the caller's array (sig_stride >= the longest prompt), those >= T go unused
+  const float* srow = sig + wi * sig_stride;
+  constexpr int kSigPerLane = kSegTokens / 32;
+  float sv[kSigPerLane];
+#pragma unroll
+  for (int k = 0; k < kSigPerLane; k++) {
+    const long t = (long)seg * kSegTokens + 32 * k + lane;
+    sv[k] = t < sig_stride ? __ldcs(srow + t) : 0.0f;
+  }
   if (ld_volatile(&p.ctrl->qw_status) != 0) return;   // entry status (Q36), left by dkv_compact_alloc
   const int i = (int)(wi / p.LyH), j = (int)(wi % p.LyH);
   const int r = p.admit[i];
@@ -279,7 +290,6 @@ quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const u
   const int t1 = min(t0 + kSegTokens, T);
   const int kept = max(T - p.W, 0);
   const int ke = min(t1, kept);
-  const float* srow = sig + wi * sig_stride;
   const uint16_t* kbase = kin + wi * kv_stride * D;
   const uint16_t* vbase = vin + wi * kv_stride * D;
 
@@ -288,12 +298,15 @@ quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const u
   int lr = p.pf_seg[((size_t)u * p.nseg + seg) * 2 + 1];
   int nh = 0, nl = 0;
   const unsigned lt = (1u << lane) - 1u;
-  for (int c = t0; c < ke; c += 32) {
+#pragma unroll
+  for (int k = 0; k < kSigPerLane; k++) {
+    const int c = t0 + 32 * k;
+    if (c >= ke) break;                                  // warp-uniform
     const int t = c + lane;
     int cl = DKV_CLS_NONE;
     float s = 0.0f;
     if (t < ke) {
-      s = canon_zero(__ldcs(srow + t));
+      s = canon_zero(sv[k]);
       cl = prompt_class_q(ah, al, p.prompt_den, s, t, T, p.top, p.alpha_t);
     }
     const unsigned hm = __ballot_sync(kFull, cl == DKV_CLS_HIGH);
