@@ -279,12 +279,17 @@ quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const u
     const long t = (long)seg * kSegTokens + 32 * k + lane;
     sv[k] = t < sig_stride ? __ldcs(srow + t) : 0.0f;
   }
-  if (ld_volatile(&p.ctrl->qw_status) != 0) return;   // entry status (Q36), left by dkv_compact_alloc
+  // the entry status, the admitted request and everything indexed by it in two round trips: the status is
+  // checked only once they are in flight (a request index from an errored call is clamped, never used)
+  const int entry_status = ld_volatile(&p.ctrl->qw_status);   // Q36, left by dkv_compact_alloc
   const int i = (int)(wi / p.LyH), j = (int)(wi % p.LyH);
-  const int r = p.admit[i];
+  const int r = min(max(p.admit[i], 0), p.R - 1);
   const int u = r * p.LyH + j;
   const float ah = unit_alpha_h(p, u), al = unit_alpha_l(p, u);  // Q35
   const int T = p.prompt_len[r];
+  int hr = p.pf_seg[((size_t)u * p.nseg + seg) * 2];    // seg < nseg_max <= nseg
+  int lr = p.pf_seg[((size_t)u * p.nseg + seg) * 2 + 1];
+  if (entry_status != 0) return;
   const int t0 = seg * kSegTokens;
   if (t0 >= T) return;
   const int t1 = min(t0 + kSegTokens, T);
@@ -294,8 +299,6 @@ quant_prefill_kernel(PoolDev p, int n, const uint16_t* __restrict__ kin, const u
   const uint16_t* vbase = vin + wi * kv_stride * D;
 
   // phase A: classes + per-class ranks (warp ballot/popc + running offsets) -> two kept lists
-  int hr = p.pf_seg[((size_t)u * p.nseg + seg) * 2];
-  int lr = p.pf_seg[((size_t)u * p.nseg + seg) * 2 + 1];
   int nh = 0, nl = 0;
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
