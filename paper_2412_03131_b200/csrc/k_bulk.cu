@@ -62,7 +62,8 @@ struct ListCtx {
 #define DKV_BULK_STAGES 2
 #endif
 #ifndef DKV_BULK_MINB
-#define DKV_BULK_MINB 4
+#define DKV_BULK_MINB 2   // the register cap ptxas schedules against (128 registers used either way): 2 measured
+                          // best, 6.30-6.35 ms vs 6.54-6.57 at 4 (profiles/r2z_bulk_minb_sweep.log)
 #endif
 constexpr int kBulkStages = DKV_BULK_STAGES;               // staging depth (tuning: tools/sweep_bulk.sh)
 
