@@ -791,7 +791,7 @@ def run_ours(args, rank, world, local):
         "dist": {"backend": DIST["backend"], "world": world,
                  "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if DIST["backend"] == "nccl" else None},
         "quant_write": {"gbs": round(agg_bulk_gbs, 1), "gbs_per_gpu": round(bulk_gbs_rank, 1),
-                        "ms": round(bulk_max, 3), "algorithmic_bytes_per_gpu": bbytes, "token_mix": bmix,
+                        "ms": round(bulk_max, 3), "ms_rounds": [round(x, 3) for x in bulk_ms], "algorithmic_bytes_per_gpu": bbytes, "token_mix": bmix,
                         "frac_of_hbm_peak": round(bulk_gbs_rank / peak, 4)},
         "roofline": {"kernel": "quant_prefill_kernel (dkv_quant_write PREFILL, bulk writer)", "bound": "hbm",
                      "achieved": round(bulk_gbs_rank, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
