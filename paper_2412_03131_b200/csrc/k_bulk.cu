@@ -17,7 +17,10 @@
 
 namespace dkv {
 
-constexpr int kBulkWarps = 4;
+#ifndef DKV_BULK_WARPS
+#define DKV_BULK_WARPS 4
+#endif
+constexpr int kBulkWarps = DKV_BULK_WARPS;               // warps (segments) per CTA
 constexpr int kBulkG = 4;                                // lanes per token
 constexpr int kBulkTPS = 32 / kBulkG;                    // tokens per warp step
 
