@@ -212,14 +212,22 @@ __device__ __forceinline__ uint4 quant_h16_lane(const HVec<EPL>& x, int bits, un
   const float sf = __half2float(s16);
   const float inv = __frcp_rn(sf);                      // == fdiv_rn(1, sf)
   const float nz = -mn;                                 // z = min exactly (FP16 input)
-  const float cap = (sf >= 6.103515625e-05f) ? 3.0e38f : Qf;   // clamp only for a subnormal s16
-  const uint32_t zmask = sf != 0.0f ? 0xFFFFFFFFu : 0u;        // s16 == 0: all codes 0
   uint32_t ub[EPL];
+  if (sf >= 6.103515625e-05f) {                         // group-uniform: s16 normal, t <= Q + 1/8, no clamp / mask
 #pragma unroll
-  for (int i = 0; i < EPL; i++) {
-    const float d = mixed_add_h((i & 1) ? (x.w[i >> 1] >> 16) : (x.w[i >> 1] & 0xFFFFu), nz);
-    const float t = fminf(__fmul_rn(d, inv), cap);
-    ub[i] = __float_as_uint(__fadd_rd(__fadd_rd(t, 0.5f), 8388608.0f)) & zmask;
+    for (int i = 0; i < EPL; i++) {
+      const float d = mixed_add_h((i & 1) ? (x.w[i >> 1] >> 16) : (x.w[i >> 1] & 0xFFFFu), nz);
+      ub[i] = __float_as_uint(__fadd_rd(__fadd_rd(__fmul_rn(d, inv), 0.5f), 8388608.0f));
+    }
+  } else {
+    const float cap = Qf;                               // clamp for a subnormal s16
+    const uint32_t zmask = sf != 0.0f ? 0xFFFFFFFFu : 0u;      // s16 == 0: all codes 0
+#pragma unroll
+    for (int i = 0; i < EPL; i++) {
+      const float d = mixed_add_h((i & 1) ? (x.w[i >> 1] >> 16) : (x.w[i >> 1] & 0xFFFFu), nz);
+      const float t = fminf(__fmul_rn(d, inv), cap);
+      ub[i] = __float_as_uint(__fadd_rd(__fadd_rd(t, 0.5f), 8388608.0f)) & zmask;
+    }
   }
   return pack_codes<EPL>(ub, bits);
 }
