@@ -45,6 +45,9 @@ namespace dkv {
 #ifndef DKV_TC_K8_BIASED
 #define DKV_TC_K8_BIASED 0      // K8 key operands left at 1024 + c (the bias folded into z): A/B of precision and time
 #endif
+#ifndef DKV_TC_MAXNREG
+#define DKV_TC_MAXNREG 128   // register cap without a min-blocks hint (4 CTAs/SM all the same): ptxas schedules
+#endif                       // it better than __launch_bounds__(128, 4), 2.374 -> 2.350 ms (tools/tc_ab.sh)
 #ifndef DKV_TC_MINB
 #define DKV_TC_MINB 4           // CTAs per SM the register budget is sized for
 #endif
@@ -419,7 +422,11 @@ struct TcSigUnit {
 // buffers per CTA, alternating between units; rows page-aligned: high page k at 16 k, low page k' at 16 ph + 32 k',
 // the window after them), written once in the page pass and read once by the significance pass.
 template <int D, int G>
+#if DKV_TC_MAXNREG > 0
+__global__ void __maxnreg__(DKV_TC_MAXNREG)
+#else
 __global__ void __launch_bounds__(kTcThreads, DKV_TC_MINB)
+#endif
 attend_tc_kernel(PoolDev p, const uint16_t* __restrict__ q, float* __restrict__ out, float* __restrict__ probs) {
   constexpr int NG = D / 16, NMT = D / 16, FPK = D / 4, FPV = D / 8, GP = G <= 4 ? 4 : 8;
   constexpr int STG = tc_stage_bytes<D>();
@@ -737,7 +744,11 @@ template <int D, int G>
 __host__ __device__ constexpr int tc_partial_floats() { return G * D + 3 * 8 + 8; }   // + minima candidates
 
 template <int D, int G>
+#if DKV_TC_MAXNREG > 0
+__global__ void __maxnreg__(DKV_TC_MAXNREG)
+#else
 __global__ void __launch_bounds__(kTcThreads, DKV_TC_MINB)
+#endif
 attend_tc_split_kernel(PoolDev p, const uint16_t* __restrict__ q, int NS, int slots) {
   constexpr int NG = D / 16, NMT = D / 16, FPK = D / 4, FPV = D / 8, GP = G <= 4 ? 4 : 8;
   constexpr int STG = tc_stage_bytes<D>();
